@@ -1,0 +1,483 @@
+"""Benchmark: KFBI time steps/s at 4096² for heat, wave and Schrödinger.
+
+One bench step = one time step of EACH of the three equations (BASELINE.json
+metric: "KFBI time steps/sec at 4096² (heat/wave/Schrödinger)"):
+
+  heat         Crank-Nicolson, flower star(1, 0.2, k=8) on [-1.5,1.5]²
+  wave         implicit θ = 1/4, ellipse (1.2, 0.8) on [-1.5,1.5]²
+  schrodinger  Strang splitting (complex128), star(1.5, 0.2, 3) on [-π,π]²
+
+all Dirichlet, M = 4096, τ = 0.25·64/M (the convergence-sweep rule of
+SURVEY §6.3 / BASELINE §2), closed-form manufactured solutions (synthetic
+data, no RNG).  Setup, startup and the cold first steps (warm-up) are
+untimed; K bench steps are timed with CUDA events, bracketed by a barrier +
+synchronize, max over ranks.  Per-equation working sets (W rows, panels,
+fields) exceed the 126 MB L2, so no flush is needed between steps.
+
+  value  time steps/s, device-resident (the public per-step API, boundary
+         data evaluated and uploaded by it every step)
+  e2e    same loop plus a device->host copy of every step's solution field
+         into pinned memory (what a user saving each step pays)
+
+`--impl reference` times the CPU reference path (the oracle port of the
+reference package, numpy/scipy with all host threads) on the same workload,
+each step a bounded sample (one Richardson sweep per equation plus the step
+glue, scaled by the reference's steady iteration counts); rank 0 only.
+
+Launch: python bench.py [--gpus N --steps K --warmup W]; for N > 1 under
+torchrun every rank runs an independent replica (weak scaling).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+M_DEFAULT = 4096
+EQUATIONS = ("heat", "wave", "schrodinger")
+# steady Richardson sweeps per step of the reference at M=4096, tau=1/256
+# (measured with the full oracle in the build container: heat 51,35,35;
+# see profiles/cpu_oracle_4096.json); used only to scale the CPU samples
+REF_STEADY_ITERS = {"heat": 35, "wave": 16, "schrodinger": 25}
+METRIC = "KFBI time steps/sec at 4096² (heat/wave/Schrödinger); speedup vs host CPU"
+
+
+def workload(m):
+    import paper_2404_14864_b200 as k
+
+    box = (-1.5, 1.5, -1.5, 1.5)
+    pibox = (-np.pi, np.pi, -np.pi, np.pi)
+    tau = 0.25 * 64 / m
+    heat, wave, schr = k.HeatPlaneDecay(1.0), k.WaveStanding(0.0), k.SchrodingerPhaseRotation()
+    horizon = 10_000 * tau
+    return {
+        "heat": (box, k.StarCurve(1.0, c=0.2, lobes=8), dict(
+            equation="heat", bc_kind="dirichlet", g=heat.dirichlet, u0=heat.u0,
+            lap_u0=heat.lap_u0, tau=tau, t_final=horizon, c=1.0)),
+        "wave": (box, k.EllipseCurve(1.2, 0.8), dict(
+            equation="wave", bc_kind="dirichlet", g=wave.dirichlet, u0=wave.u0,
+            lap_u0=wave.lap_u0, v0=wave.v0, lap_v0=wave.lap_v0, tau=tau, t_final=horizon,
+            theta=0.25)),
+        "schrodinger": (pibox, k.StarCurve(1.5, c=0.2, lobes=3), dict(
+            equation="schrodinger", bc_kind="dirichlet", g=schr.dirichlet, u0=schr.u0,
+            lap_u0=schr.lap_u0, potential=schr.potential, w=1.0, tau=tau, t_final=horizon)),
+    }
+
+
+def config_obj(m, eqs, n):
+    return {
+        "workload": f"KFBI per-step solve, {m}x{m} grid, one time step each of "
+                    + "/".join(eqs) + " (heat flower8, wave ellipse, Schrodinger star3)",
+        "grid": m, "tau": 0.25 * 64 / m, "equations": list(eqs),
+        "boundary": "dirichlet", "l2": "per-equation working set > 126 MB L2 (no flush)",
+        "parallelism": f"replicas{n}",
+    }
+
+
+# ---------------------------------------------------------------------------
+class Clocks:
+    """nvidia-smi sampler during the timed region (B200_PROFILING.md)."""
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        return False
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        try:
+            for line in open(self.path):
+                f = [x.strip() for x in line.split(",")]
+                if len(f) < 9:
+                    continue
+                try:
+                    sm.append(float(f[1]))
+                    mx = float(f[2])
+                except ValueError:
+                    continue
+                for nm, v in zip(names, f[5:9]):
+                    if v.lower() == "active":
+                        reasons.add(nm)
+        except OSError:
+            pass
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+def _dist():
+    import torch.distributed as dist
+
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1 and not dist.is_initialized():
+        import torch
+
+        backend = "nccl" if torch.cuda.is_available() else "gloo"
+        dist.init_process_group(backend=backend)
+    return ws, rank, local
+
+
+def _max_over_ranks(x, ws):
+    if ws == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    dev = torch.device("cuda", torch.cuda.current_device()) if torch.cuda.is_available() else "cpu"
+    t = torch.tensor([float(x)], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def _barrier(ws):
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def _bytes_cols(m, cplx):
+    # algorithmic bytes of one fused column pass: read + write the interior spectrum
+    return 2 * (m - 1) ** 2 * (16 if cplx else 8)
+
+
+def run_ours(args):
+    import torch
+
+    import paper_2404_14864_b200 as k
+    from paper_2404_14864_b200.timestepping import _stepper_for
+
+    ws, rank, local = _dist()
+    torch.cuda.set_device(local)
+    m = args.m
+    eqs = args.equations
+    wl = workload(m)
+    backend = k.CudaBackend(local, timing=False)
+    ctxs, specs, states, steppers = {}, {}, {}, {}
+    t_setup = time.time()
+    for eq in eqs:
+        box, curve, kw = wl[eq]
+        geo = k.build_grid(box, m, curve)
+        ctxs[eq] = k.StepContext(geo, backend=backend)
+        specs[eq] = k.ProblemSpec(**kw)
+        startup, step = _stepper_for(specs[eq])
+        steppers[eq] = step
+        states[eq] = startup(specs[eq], ctxs[eq])
+    t_setup = time.time() - t_setup
+
+    def advance(eq):
+        st = steppers[eq](states[eq], specs[eq], ctxs[eq])
+        ctxs[eq].check_stable(st, specs[eq])
+        states[eq] = st
+        return st
+
+    for _ in range(args.warmup):
+        for eq in eqs:
+            advance(eq)
+    torch.cuda.synchronize()
+
+    plans = [c.plan for c in ctxs.values()]
+    for p in plans:
+        p.reset_kernel_times()
+        p.set_timing(True)
+    launches0 = sum(p.launch_count() for p in plans)
+    stream = torch.cuda.current_stream()
+    ev = {eq: [] for eq in eqs}
+    iters = {eq: [] for eq in eqs}
+    _barrier(ws)
+    torch.cuda.synchronize()
+    with Clocks(local) as clk:
+        start = torch.cuda.Event(enable_timing=True)
+        end = torch.cuda.Event(enable_timing=True)
+        start.record(stream)
+        for _ in range(args.steps):
+            for eq in eqs:
+                a = torch.cuda.Event(enable_timing=True)
+                b = torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                st = advance(eq)
+                b.record(stream)
+                ev[eq].append((a, b))
+                iters[eq].append(st.last_iterations)
+        end.record(stream)
+        torch.cuda.synchronize()
+    _barrier(ws)
+    elapsed_ms = start.elapsed_time(end)
+    launches = sum(p.launch_count() for p in plans) - launches0
+    per_eq_ms = {eq: sum(a.elapsed_time(b) for a, b in ev[eq]) / args.steps for eq in eqs}
+    # per-kernel device times over the timed region
+    kt_ms, kt_calls = {}, {}
+    cols_bytes, cols_ms, cols_calls = 0.0, 0.0, 0
+    for eq, c in ctxs.items():
+        ms, calls = c.plan.kernel_times()
+        cplx = eq == "schrodinger"
+        cols_bytes += calls["transform-cols"] * _bytes_cols(m, cplx)
+        cols_ms += ms["transform-cols"]
+        cols_calls += calls["transform-cols"]
+        for name in ms:
+            kt_ms[name] = kt_ms.get(name, 0.0) + ms[name]
+            kt_calls[name] = kt_calls.get(name, 0) + calls[name]
+    for p in plans:
+        p.set_timing(False)
+    clocks = clk.summary()
+
+    elapsed_max = _max_over_ranks(elapsed_ms, ws)
+    n_time_steps = args.steps * len(eqs)
+    value = n_time_steps * ws / (elapsed_max / 1e3)
+
+    # ---- e2e: same loop + D2H of each step's solution field (pinned) ----
+    pinned = {eq: torch.empty(ctxs[eq].n_grid, dtype=torch.complex128 if eq == "schrodinger"
+                              else torch.float64, pin_memory=True) for eq in eqs}
+    h2d = sum(ctxs[eq].n_ctl * (16 if eq == "schrodinger" else 8) for eq in eqs)
+    d2h = sum(pinned[eq].numel() * pinned[eq].element_size() for eq in eqs)
+    _barrier(ws)
+    torch.cuda.synchronize()
+    s2 = torch.cuda.Event(enable_timing=True)
+    e2 = torch.cuda.Event(enable_timing=True)
+    s2.record(stream)
+    for _ in range(args.steps):
+        for eq in eqs:
+            st = advance(eq)
+            pinned[eq].copy_(st.u.reshape(-1), non_blocking=True)
+    e2.record(stream)
+    torch.cuda.synchronize()
+    _barrier(ws)
+    e2e_ms = _max_over_ranks(s2.elapsed_time(e2), ws)
+    e2e_value = n_time_steps * ws / (e2e_ms / 1e3)
+
+    if rank != 0:
+        return None
+    cols_avg_ms = cols_ms / max(cols_calls, 1)
+    achieved = (cols_bytes / max(cols_calls, 1)) / (cols_avg_ms / 1e3) / 1e9 if cols_calls else 0.0
+    peaks = _peaks()
+    traffic = _ncu_traffic()
+    line = {
+        "metric": METRIC,
+        "value": value,
+        "unit": "time steps/s",
+        "n_gpus": ws,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": elapsed_max / args.steps,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64 (heat, wave) / c128 (schrodinger)",
+        "data": "synthetic: closed-form manufactured solutions (no RNG), random-free geometry",
+        "config": config_obj(m, eqs, ws),
+        "per_equation": {eq: {"steps_per_s": 1e3 / per_eq_ms[eq], "ms_per_step": per_eq_ms[eq],
+                              "iterations": iters[eq]} for eq in eqs},
+        "kernel_ms_per_bench_step": {kname: v / args.steps for kname, v in kt_ms.items() if v},
+        "kernel_calls": {kname: v for kname, v in kt_calls.items() if v},
+        "roofline": {
+            "kernel": "cols_kernel (fused column DST-I / scale / DST-I, transform-cols)",
+            "bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+            "frac": achieved / peaks["hbm_gbs"] if peaks["hbm_gbs"] else None,
+            "traffic": traffic.get("cols_bytes_per_launch") if traffic else None,
+            "peak_source": peaks["source"],
+            "algorithmic_bytes_per_launch": {"f64": _bytes_cols(m, False),
+                                             "c128": _bytes_cols(m, True)},
+            "avg_launch_ms": cols_avg_ms,
+        },
+        "e2e": {"value": e2e_value, "unit": "time steps/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h},
+        "gpu_launches": int(launches),
+        "clocks": clocks,
+        "setup_s": t_setup,
+    }
+    if not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(ctxs, specs, iters, args)
+    return line
+
+
+def _peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        d = json.load(open(path))
+        return {"hbm_gbs": float(d["hbm_gbs"]), "source": "measured (MEASURED_PEAKS.json)"}
+    except Exception:
+        return {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
+
+
+def _ncu_traffic():
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        return json.load(open(path))
+    except Exception:
+        return None
+
+
+# ---------------------------------------------------------------------------
+def _oracle_sample(tables, spec_kw, sweeps):
+    """Wall time of one oracle time step truncated after `sweeps` sweeps
+    (after a warm-up step so the density is warm)."""
+    from oracle import kfbi_oracle as O
+
+    keys = ("equation", "g", "u0", "lap_u0", "tau", "t_final", "c", "theta", "w", "potential",
+            "splitting", "v0", "lap_v0")
+    spec = O.Spec(**{k: spec_kw[k] for k in keys if k in spec_kw})
+    st = O.Stepper(tables, spec, max_sweeps=1)
+    st.step()                      # untimed: leaves the cold first-step path
+    st.max_sweeps = sweeps
+    t0 = time.perf_counter()
+    st.step()
+    return time.perf_counter() - t0
+
+
+def _cpu_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def cpu_model(tables_by_eq, spec_kw_by_eq, iters_by_eq, samples=1):
+    """Per-step CPU time model: t(step) = t_glue + iters * t_sweep, with t_sweep
+    and t_glue from truncated oracle steps of 1 and 2 sweeps."""
+    from oracle import kfbi_oracle as O
+
+    O.WORKERS = _cpu_threads()
+    out = {}
+    for eq, t in tables_by_eq.items():
+        t1 = min(_oracle_sample(t, spec_kw_by_eq[eq], 1) for _ in range(samples))
+        t2 = min(_oracle_sample(t, spec_kw_by_eq[eq], 2) for _ in range(samples))
+        sweep = max(t2 - t1, 1e-9)
+        glue = max(t1 - sweep, 0.0)
+        it = iters_by_eq[eq]
+        out[eq] = {"sweep_s": sweep, "glue_s": glue, "iterations": it,
+                   "step_s": glue + it * sweep}
+    return out
+
+
+def cpu_baseline(ctxs, specs, iters, args):
+    from oracle import kfbi_oracle as O
+
+    wl = workload(args.m)
+    tables = {eq: O.tables_from_workspace(c.workspace) for eq, c in ctxs.items()}
+    its = {eq: int(round(float(np.median(iters[eq])))) for eq in ctxs}
+    t0 = time.time()
+    model = cpu_model(tables, {eq: wl[eq][2] for eq in ctxs}, its)
+    total = sum(v["step_s"] for v in model.values())
+    return {
+        "value": len(ctxs) / total, "unit": "time steps/s", "cores": _cpu_threads(),
+        "kind": "port",
+        "sample": ("oracle port of the reference (numpy/scipy, scipy.fft workers = all host "
+                   "threads, OpenBLAS threads) on the same 4096^2 workload: per equation one "
+                   "time step truncated after 1 and after 2 Richardson sweeps gives t_sweep and "
+                   "t_glue; step time = t_glue + t_sweep * (iterations per step measured on the "
+                   "GPU in this run, identical to the reference's by parity)"),
+        "per_equation": model, "sample_wall_s": time.time() - t0,
+    }
+
+
+def run_reference(args):
+    """--impl reference: the CPU reference path on the host cores, rank 0 only."""
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return None
+    import paper_2404_14864_b200 as k
+    from oracle import kfbi_oracle as O
+
+    O.WORKERS = _cpu_threads()
+    m = args.m
+    eqs = args.equations
+    wl = workload(m)
+    tables, spec_kw = {}, {}
+    for eq in eqs:
+        box, curve, kw = wl[eq]
+        # host setup shared with the product (identical to the reference's, tests/test_setup.py)
+        tables[eq] = O.tables_from_workspace(k.InterfaceWorkspace(k.build_grid(box, m, curve)))
+        spec_kw[eq] = kw
+    its = {eq: REF_STEADY_ITERS[eq] for eq in eqs}
+    model = cpu_model(tables, spec_kw, its)          # warm-up: the sweep / glue split
+    budget = time.time() + 150.0
+    step_s = []
+    for _ in range(max(args.steps, 1)):
+        tot = 0.0
+        for eq in eqs:
+            t1 = _oracle_sample(tables[eq], spec_kw[eq], 1)
+            tot += t1 + (its[eq] - 1) * model[eq]["sweep_s"]
+        step_s.append(tot)
+        if time.time() > budget:
+            break
+    per_step = float(np.median(step_s))
+    value = len(eqs) / per_step
+    return {
+        "metric": METRIC, "value": value, "unit": "time steps/s", "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_step * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64 (heat, wave) / c128 (schrodinger)",
+        "data": "synthetic: closed-form manufactured solutions", "config": config_obj(m, eqs, ws),
+        "impl": "reference",
+        "cpu_baseline": {
+            "value": value, "unit": "time steps/s", "cores": _cpu_threads(), "kind": "port",
+            "sample": (f"{len(step_s)} bounded samples; each = one oracle time step truncated after "
+                       "1 Richardson sweep per equation, scaled to the reference's steady "
+                       f"iteration counts {its} with the per-sweep time from 1- vs 2-sweep steps"),
+        },
+        "e2e": {"value": value, "unit": "time steps/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "per_equation": model,
+    }
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--m", type=int, default=M_DEFAULT)
+    ap.add_argument("--equations", default=",".join(EQUATIONS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args(argv)
+    args.equations = tuple(e for e in args.equations.split(",") if e)
+    if args.warmup < 3:
+        args.warmup = 3
+    line = run_reference(args) if args.impl == "reference" else run_ours(args)
+    if line is not None:
+        print(json.dumps(line), flush=True)
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

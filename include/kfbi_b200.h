@@ -1,0 +1,216 @@
+/*
+ * kfbi_b200.h — C ABI of the B200-native KFBI hot path.
+ *
+ * The reference (`/root/reference/pkg/src/kfbi`, pure Python) has no native
+ * boundary of its own: every sweep goes through `Backend.dispatch(spec,
+ * item_fn)` (engine.py:84-95) with numpy closures, which a GPU cannot plug
+ * into.  The boundary therefore sits one level up, at the solver objects.
+ * Each entry point below names the reference interface it replaces.
+ *
+ * Conventions
+ *   - All device pointers are caller-owned device memory (the Python host
+ *     passes torch tensor data pointers); the plan owns only its scratch.
+ *   - Grid fields are (M+1) x (M+1) row-major, flat index i + j*(M+1)
+ *     (grid.py:4-6, grid.py:44-52).  Complex values are interleaved
+ *     (re, im) doubles, i.e. numpy/torch complex128.
+ *   - `dtype` is KFBI_F64 or KFBI_C128; real-kappa/real-data solves run the
+ *     f64 path, anything complex runs the c128 path (boxsolve.py:56).
+ *   - Every function returns a kfbi_status; on failure the message is in
+ *     kfbi_last_error() (thread-local).  The Python host maps the codes onto
+ *     the reference exception classes (errors.py:8-56).
+ *   - A plan is bound to one device and is not thread-safe; distinct plans
+ *     may be used concurrently.  Work is enqueued on the
+ *     caller's stream; the only host syncs are the documented ones.
+ */
+#ifndef KFBI_B200_H
+#define KFBI_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  KFBI_OK = 0,
+  KFBI_E_CONFIG = 1,       /* -> ConfigError      (errors.py:12)          */
+  KFBI_E_GRID = 2,         /* -> GridError        (errors.py:20)          */
+  KFBI_E_NOCONV = 3,       /* -> ConvergenceError (errors.py:36-42)       */
+  KFBI_E_INSTABILITY = 4,  /* -> InstabilityError (errors.py:45-56)       */
+  KFBI_E_CUDA = 5          /* -> DispatchError(kernel_name) (errors.py:28) */
+} kfbi_status;
+
+typedef enum { KFBI_F64 = 0, KFBI_C128 = 1 } kfbi_dtype;
+typedef enum { KFBI_DIRICHLET_ZERO = 0, KFBI_NEUMANN_ZERO = 1 } kfbi_box_bc;
+
+/* The nine dispatch names of the reference engine (engine.py:23-35), used as
+ * indices into the per-kernel timing arrays. */
+enum {
+  KFBI_K_CLASSIFY = 0,
+  KFBI_K_EDGES = 1,
+  KFBI_K_JUMPS = 2,          /* "jumps-and-corrections" */
+  KFBI_K_ROWS = 3,           /* "transform-rows"        */
+  KFBI_K_COLS = 4,           /* "transform-cols"        */
+  KFBI_K_SCALE = 5,          /* "diagonal-scale"        */
+  KFBI_K_EXTRACT = 6,        /* "extract-traces"        */
+  KFBI_K_DENSITY = 7,        /* "density-update"        */
+  KFBI_K_RHS = 8,            /* "rhs-update"            */
+  KFBI_N_KERNEL_NAMES = 9
+};
+
+typedef struct kfbi_plan kfbi_plan;
+
+/* CartesianGrid (grid.py:25-52) + the BoxSolver eigenvalue tables
+ * (boxsolve.py:38-44).  m must be a power of two, 16 <= m <= 4096. */
+typedef struct {
+  int32_t m;
+  double h;
+  int32_t device;
+} kfbi_grid_desc;
+
+/* Host-side geometry tables, uploaded once (InterfaceWorkspace.__init__,
+ * interface.py:137-162; TraceExtractor.__init__, bvp.py:37-86; records,
+ * grid.py:71-101).  All pointers are HOST pointers, copied by the call. */
+typedef struct {
+  int32_t n_ctl;              /* control points                          */
+  int32_t n_edges;            /* unique sign-change edges (2 records each) */
+  int32_t n_rec;              /* intersection records                    */
+  int32_t n_groups;           /* owning irregular nodes                  */
+  const double *w_edges;      /* [n_edges][n_ctl] trig-interp rows       */
+  const int8_t *edge_axis;    /* [n_edges] 0 = horizontal, 1 = vertical  */
+  const int32_t *rec_edge;    /* [n_rec] edge of each record             */
+  const double *rec_d;        /* [n_rec] neighbour-minus-crossing offset */
+  const double *rec_sigma;    /* [n_rec] -1/h^2 interior, +1/h^2 exterior */
+  const int32_t *group_start; /* [n_groups+1] CSR over records           */
+  const int32_t *group_node;  /* [n_groups] owner flat index i + j(M+1)  */
+  const int32_t *row_group;   /* [m+2] CSR of groups per grid row j      */
+  const double *deriv_col;    /* [n_ctl] first column of d/dtheta        */
+  const double *speed;        /* [n_ctl] |x'(theta)|                     */
+  const double *tangent;      /* [n_ctl][2]                              */
+  const double *normal;       /* [n_ctl][2]                              */
+  const double *dtan_ds;      /* [n_ctl][2]                              */
+  const double *inv3;         /* [n_ctl][3][3]                           */
+  const int32_t *stencil;     /* [n_ctl][6] flat node indices            */
+  const double *ainv_rows;    /* [n_ctl][3][6] rows 0..2 of the 6x6 inverse */
+  const double *jcoef;        /* [n_ctl][6][6] jump-shift coefficients   */
+} kfbi_geometry;
+
+/* One Dirichlet BVP solve by Richardson iteration (BvpProblem,
+ * bvp.py:231-262; richardson_solve, bvp.py:276-351).  Device pointers. */
+typedef struct {
+  int32_t dtype;
+  double kappa_re, kappa_im;
+  const void *F;          /* (M+1)^2 grid source                          */
+  double F_sign;          /* +1 or -1 (timestepping.py:182 negates F)     */
+  const void *f_gamma;    /* [n_ctl]                                      */
+  double f_gamma_sign;
+  const void *g;          /* [n_ctl] boundary values                      */
+  void *density;          /* [n_ctl] in: initial density, out: final      */
+  double gamma, tol;
+  int32_t max_iter;
+  int32_t sweeps_hint;    /* sweeps to enqueue before the first check     */
+  void *u;                /* out (M+1)^2 field of the final sweep         */
+  void *trace_u;          /* out [n_ctl]                                  */
+  void *trace_un;         /* out [n_ctl]                                  */
+} kfbi_bvp;
+
+typedef struct {
+  int32_t iterations;
+  int32_t converged;
+  double residual;
+  double *history;        /* host buffer [max_iter], filled on return     */
+} kfbi_bvp_result;
+
+const char *kfbi_last_error(void);
+const char *kfbi_version(void);
+
+kfbi_status kfbi_plan_create(const kfbi_grid_desc *desc, kfbi_plan **out);
+kfbi_status kfbi_plan_destroy(kfbi_plan *plan);
+
+/* BoxSolver.solve (boxsolve.py:46-94): (Delta_h - kappa) u = rhs with the
+ * dirichlet-zero closure; returns u with an exact zero ring. */
+kfbi_status kfbi_box_solve(kfbi_plan *plan, int32_t dtype, double kappa_re,
+                           double kappa_im, const void *rhs, void *u,
+                           void *stream);
+
+kfbi_status kfbi_plan_set_geometry(kfbi_plan *plan, const kfbi_geometry *geo);
+
+/* compute_jumps (interface.py:171-203): jm out is SoA [6][n_ctl]
+ * (u, ux, uy, uxx, uxy, uyy).  psi may be NULL (zero). */
+kfbi_status kfbi_jumps(kfbi_plan *plan, int32_t dtype, double kappa_re,
+                       double kappa_im, const void *phi, const void *psi,
+                       const void *f_gamma, double f_gamma_sign, void *jm,
+                       void *stream);
+
+/* corrections (interface.py:206-238): c out is a full (M+1)^2 field. */
+kfbi_status kfbi_corrections(kfbi_plan *plan, int32_t dtype, const void *jm,
+                             void *c, void *stream);
+
+/* solve_interface (interface.py:250-261): u = BoxSolver(F + corrections). */
+kfbi_status kfbi_interface_solve(kfbi_plan *plan, int32_t dtype,
+                                 double kappa_re, double kappa_im,
+                                 const void *F, const void *jm, void *u,
+                                 void *stream);
+
+/* TraceExtractor.extract (bvp.py:88-104): out [3][n_ctl] = (u+, ux+, uy+). */
+kfbi_status kfbi_extract(kfbi_plan *plan, int32_t dtype, const void *u,
+                         const void *jm, void *out, void *stream);
+
+/* richardson_solve (bvp.py:276-351), device resident: one host sync per
+ * batch of sweeps; history copied to result->history. */
+kfbi_status kfbi_richardson(kfbi_plan *plan, const kfbi_bvp *bvp,
+                            kfbi_bvp_result *result, void *stream);
+
+/* Time-stepping right-hand sides (timestepping.py), element-wise over n
+ * values: the (M+1)^2 grid with the uint8 interior mask, or the n_ctl control
+ * points with mask == NULL.  Where a norm pointer is given, max|u_next| (the
+ * blow-up norm of StepContext.check_stable, timestepping.py:172-175) is
+ * returned after a stream sync. */
+
+/* heat_step (timestepping.py:218-231): u <- mask*u; F_new = a*u - F_old
+ * (F_new may alias F_old). */
+kfbi_status kfbi_heat_rhs(kfbi_plan *plan, int64_t n, const uint8_t *mask, void *u,
+                          const void *F_old, void *F_new, double a,
+                          double *norm_out, void *stream);
+
+/* wave_step (timestepping.py:284-302): u_next <- mask*u_next;
+ * F_new = (2un - uc) kw + coef (kw un - fc) + (kw uc - fp). */
+kfbi_status kfbi_wave_rhs(kfbi_plan *plan, int64_t n, const uint8_t *mask,
+                          void *u_next, const void *u_curr, const void *F_curr,
+                          const void *F_prev, void *F_new, double kw, double coef,
+                          double *norm_out, void *stream);
+
+/* Strang u* (timestepping.py:410-418), complex: mode 0 out = u - 0.5i tau
+ * other (other = lap u0); mode 1 out = 2u - other (other = previous u**). */
+kfbi_status kfbi_schr_ustar(kfbi_plan *plan, int64_t n, int32_t mode,
+                            const void *u, const void *other, double tau,
+                            void *out, void *stream);
+
+/* nonlinear_phase_step (timestepping.py:317-368) per node, then the mask
+ * (timestepping.py:391) and, when F != NULL, F = kappa * out
+ * (timestepping.py:395).  Returns KFBI_E_NOCONV when a node stalls. */
+kfbi_status kfbi_nonlinear_phase(kfbi_plan *plan, int64_t n, const void *ustar,
+                                 const double *v, double w, double half_tau,
+                                 const uint8_t *mask, void *out, double kappa_re,
+                                 double kappa_im, void *F, double *max_res,
+                                 void *stream);
+
+/* u <- mask*u and max|u| (np.where(ctx.mask, sol.u, 0) + check_stable). */
+kfbi_status kfbi_mask_norm(kfbi_plan *plan, int32_t dtype, int64_t n,
+                           const uint8_t *mask, void *u, double *norm_out,
+                           void *stream);
+
+/* Per-kernel-name device time (ms) and call counts since the last reset
+ * (Backend.timings / calls, engine.py:84-95).  Syncs the plan's events. */
+kfbi_status kfbi_kernel_times(kfbi_plan *plan, double *ms, int64_t *calls);
+kfbi_status kfbi_reset_kernel_times(kfbi_plan *plan);
+kfbi_status kfbi_set_timing(kfbi_plan *plan, int32_t enabled);
+
+/* Launch accounting for bench.py: kernels enqueued since the last reset. */
+int64_t kfbi_launch_count(kfbi_plan *plan);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* KFBI_B200_H */

@@ -1,0 +1,146 @@
+"""ctypes binding of the C ABI in ``include/kfbi_b200.h``.
+
+The shared library ``libkfbi_b200.so`` is built in-tree by
+``__graft_entry__.build()`` (sm_100a).  There is no fallback: if the library
+is missing, importing anything that needs it raises immediately.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import re
+
+from .errors import ConfigError, ConvergenceError, DispatchError, GridError, InstabilityError
+
+LIB_NAME = "libkfbi_b200.so"
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
+
+OK, E_CONFIG, E_GRID, E_NOCONV, E_INSTABILITY, E_CUDA = range(6)
+F64, C128 = 0, 1
+
+# index order of the per-kernel timing arrays (engine.py:23-35 names)
+KERNEL_ORDER = (
+    "classify-nodes",
+    "edge-intersections",
+    "jumps-and-corrections",
+    "transform-rows",
+    "transform-cols",
+    "diagonal-scale",
+    "extract-traces",
+    "density-update",
+    "rhs-update",
+)
+
+vp = C.c_void_p
+i32 = C.c_int32
+i64 = C.c_int64
+f64 = C.c_double
+
+
+class GridDesc(C.Structure):
+    _fields_ = [("m", i32), ("h", f64), ("device", i32)]
+
+
+class Geometry(C.Structure):
+    _fields_ = [
+        ("n_ctl", i32), ("n_edges", i32), ("n_rec", i32), ("n_groups", i32),
+        ("w_edges", vp), ("edge_axis", vp), ("rec_edge", vp), ("rec_d", vp),
+        ("rec_sigma", vp), ("group_start", vp), ("group_node", vp), ("row_group", vp),
+        ("deriv_col", vp), ("speed", vp), ("tangent", vp), ("normal", vp),
+        ("dtan_ds", vp), ("inv3", vp), ("stencil", vp), ("ainv_rows", vp), ("jcoef", vp),
+    ]
+
+
+class Bvp(C.Structure):
+    _fields_ = [
+        ("dtype", i32), ("kappa_re", f64), ("kappa_im", f64),
+        ("F", vp), ("F_sign", f64), ("f_gamma", vp), ("f_gamma_sign", f64),
+        ("g", vp), ("density", vp), ("gamma", f64), ("tol", f64),
+        ("max_iter", i32), ("sweeps_hint", i32),
+        ("u", vp), ("trace_u", vp), ("trace_un", vp),
+    ]
+
+
+class BvpResult(C.Structure):
+    _fields_ = [("iterations", i32), ("converged", i32), ("residual", f64),
+                ("history", C.POINTER(C.c_double))]
+
+
+_SIGNATURES = {
+    "kfbi_last_error": ([], C.c_char_p),
+    "kfbi_version": ([], C.c_char_p),
+    "kfbi_plan_create": ([C.POINTER(GridDesc), C.POINTER(vp)], i32),
+    "kfbi_plan_destroy": ([vp], i32),
+    "kfbi_box_solve": ([vp, i32, f64, f64, vp, vp, vp], i32),
+    "kfbi_plan_set_geometry": ([vp, C.POINTER(Geometry)], i32),
+    "kfbi_jumps": ([vp, i32, f64, f64, vp, vp, vp, f64, vp, vp], i32),
+    "kfbi_corrections": ([vp, i32, vp, vp, vp], i32),
+    "kfbi_interface_solve": ([vp, i32, f64, f64, vp, vp, vp, vp], i32),
+    "kfbi_extract": ([vp, i32, vp, vp, vp, vp], i32),
+    "kfbi_richardson": ([vp, C.POINTER(Bvp), C.POINTER(BvpResult), vp], i32),
+    "kfbi_heat_rhs": ([vp, i64, vp, vp, vp, vp, f64, C.POINTER(f64), vp], i32),
+    "kfbi_wave_rhs": ([vp, i64, vp, vp, vp, vp, vp, vp, f64, f64, C.POINTER(f64), vp], i32),
+    "kfbi_schr_ustar": ([vp, i64, i32, vp, vp, f64, vp, vp], i32),
+    "kfbi_nonlinear_phase": ([vp, i64, vp, vp, f64, f64, vp, vp, f64, f64, vp,
+                              C.POINTER(f64), vp], i32),
+    "kfbi_mask_norm": ([vp, i32, i64, vp, vp, C.POINTER(f64), vp], i32),
+    "kfbi_kernel_times": ([vp, C.POINTER(f64), C.POINTER(i64)], i32),
+    "kfbi_reset_kernel_times": ([vp], i32),
+    "kfbi_set_timing": ([vp, i32], i32),
+    "kfbi_launch_count": ([vp], i64),
+}
+
+EXPORTED_SYMBOLS = tuple(_SIGNATURES)
+
+_lib = None
+
+
+def lib():
+    """Load the library once; raise (never fall back) if it is missing."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(
+                f"{LIB_NAME} is not built (expected at {LIB_PATH}); run "
+                "`python -c 'import __graft_entry__ as g; g.build()'` from the repo root")
+        handle = C.CDLL(LIB_PATH)
+        for name, (args, res) in _SIGNATURES.items():
+            fn = getattr(handle, name)
+            fn.argtypes = args
+            fn.restype = res
+        _lib = handle
+    return _lib
+
+
+def last_error():
+    return lib().kfbi_last_error().decode("utf-8", "replace")
+
+
+_KERNEL_RE = re.compile(r"kernel '([^']+)'")
+
+
+def check(status, iterations=None, last_residual=None):
+    """Map a kfbi_status onto the reference exception classes."""
+    if status == OK:
+        return
+    msg = last_error()
+    if status == E_CONFIG:
+        raise ConfigError(msg)
+    if status == E_GRID:
+        raise GridError(msg)
+    if status == E_NOCONV:
+        raise ConvergenceError(msg, iterations=iterations, last_residual=last_residual)
+    if status == E_INSTABILITY:
+        raise InstabilityError(0, 0.0, float("nan"), float("nan"))
+    m = _KERNEL_RE.search(msg)
+    raise DispatchError(m.group(1) if m else "unknown", msg)
+
+
+def ptr(t):
+    """Raw device (or host) address of a torch tensor / numpy array, or None."""
+    if t is None:
+        return None
+    if hasattr(t, "data_ptr"):
+        return t.data_ptr()
+    return t.ctypes.data

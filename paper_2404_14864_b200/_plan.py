@@ -1,0 +1,179 @@
+"""Python handle of a device plan (``kfbi_plan`` of the C ABI).
+
+A plan owns the per-grid device tables (twiddles, eigenvalue table), the
+panel scratch of the box solver and, once ``set_geometry`` ran, the uploaded
+geometry tables of one InterfaceWorkspace.  All field arguments are torch
+CUDA tensors; work is enqueued on the backend's current stream.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _native as N
+
+_F64 = np.float64
+
+
+def _c(a, dtype):
+    return np.ascontiguousarray(a, dtype=dtype)
+
+
+class Plan:
+    def __init__(self, m, h, backend):
+        self.m = int(m)
+        self.h = float(h)
+        self.backend = backend
+        self.device = backend.device
+        self._lib = N.lib()
+        desc = N.GridDesc(self.m, self.h, self.device)
+        handle = C.c_void_p()
+        N.check(self._lib.kfbi_plan_create(C.byref(desc), C.byref(handle)))
+        self.handle = handle
+        self.has_geometry = False
+        self._keep = []
+        backend.register(self)
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h is not None and h.value:
+            try:
+                self._lib.kfbi_plan_destroy(h)
+            except Exception:  # pragma: no cover - interpreter shutdown
+                pass
+            self.handle = None
+
+    # -- accounting ---------------------------------------------------------
+    def set_timing(self, enabled):
+        N.check(self._lib.kfbi_set_timing(self.handle, int(bool(enabled))))
+
+    def kernel_times(self):
+        ms = (C.c_double * 9)()
+        calls = (C.c_int64 * 9)()
+        N.check(self._lib.kfbi_kernel_times(self.handle, ms, calls))
+        return ({k: ms[i] for i, k in enumerate(N.KERNEL_ORDER)},
+                {k: calls[i] for i, k in enumerate(N.KERNEL_ORDER)})
+
+    def reset_kernel_times(self):
+        N.check(self._lib.kfbi_reset_kernel_times(self.handle))
+
+    def launch_count(self):
+        return int(self._lib.kfbi_launch_count(self.handle))
+
+    @property
+    def stream(self):
+        return self.backend.stream_handle()
+
+    # -- geometry -----------------------------------------------------------
+    def set_geometry(self, tables):
+        """Upload the host tables built by InterfaceWorkspace (dict of numpy)."""
+        t = {
+            "w_edges": _c(tables["w_edges"], _F64),
+            "edge_axis": _c(tables["edge_axis"], np.int8),
+            "rec_edge": _c(tables["rec_edge"], np.int32),
+            "rec_d": _c(tables["rec_d"], _F64),
+            "rec_sigma": _c(tables["rec_sigma"], _F64),
+            "group_start": _c(tables["group_start"], np.int32),
+            "group_node": _c(tables["group_node"], np.int32),
+            "row_group": _c(tables["row_group"], np.int32),
+            "deriv_col": _c(tables["deriv_col"], _F64),
+            "speed": _c(tables["speed"], _F64),
+            "tangent": _c(tables["tangent"], _F64),
+            "normal": _c(tables["normal"], _F64),
+            "dtan_ds": _c(tables["dtan_ds"], _F64),
+            "inv3": _c(tables["inv3"], _F64),
+            "stencil": _c(tables["stencil"], np.int32),
+            "ainv_rows": _c(tables["ainv_rows"], _F64),
+            "jcoef": _c(tables["jcoef"], _F64),
+        }
+        g = N.Geometry(
+            n_ctl=int(tables["n_ctl"]), n_edges=int(t["edge_axis"].size),
+            n_rec=int(t["rec_edge"].size), n_groups=int(t["group_node"].size),
+            **{k: v.ctypes.data for k, v in t.items()})
+        N.check(self._lib.kfbi_plan_set_geometry(self.handle, C.byref(g)))
+        self.n_ctl = int(tables["n_ctl"])
+        self.has_geometry = True
+
+    # -- kernels --------------------------------------------------------------
+    @staticmethod
+    def _dt(cplx):
+        return N.C128 if cplx else N.F64
+
+    def box_solve(self, rhs, u, kappa):
+        k = complex(kappa)
+        N.check(self._lib.kfbi_box_solve(self.handle, self._dt(u.is_complex()), k.real, k.imag,
+                                         rhs.data_ptr(), u.data_ptr(), self.stream))
+
+    def jumps(self, kappa, phi, psi, f_gamma, jm, f_gamma_sign=1.0):
+        k = complex(kappa)
+        N.check(self._lib.kfbi_jumps(self.handle, self._dt(jm.is_complex()), k.real, k.imag,
+                                     N.ptr(phi), N.ptr(psi), f_gamma.data_ptr(),
+                                     float(f_gamma_sign), jm.data_ptr(), self.stream))
+
+    def corrections(self, jm, c):
+        N.check(self._lib.kfbi_corrections(self.handle, self._dt(jm.is_complex()), jm.data_ptr(),
+                                           c.data_ptr(), self.stream))
+
+    def interface_solve(self, kappa, F, jm, u):
+        k = complex(kappa)
+        N.check(self._lib.kfbi_interface_solve(self.handle, self._dt(u.is_complex()), k.real,
+                                               k.imag, F.data_ptr(), jm.data_ptr(),
+                                               u.data_ptr(), self.stream))
+
+    def extract(self, u, jm, out):
+        N.check(self._lib.kfbi_extract(self.handle, self._dt(out.is_complex()), u.data_ptr(),
+                                       jm.data_ptr(), out.data_ptr(), self.stream))
+
+    def richardson(self, *, kappa, F, F_sign, f_gamma, f_gamma_sign, g, density, gamma, tol,
+                   max_iter, u, trace_u, trace_un, sweeps_hint=0):
+        k = complex(kappa)
+        b = N.Bvp(dtype=self._dt(u.is_complex()), kappa_re=k.real, kappa_im=k.imag,
+                  F=F.data_ptr(), F_sign=float(F_sign), f_gamma=f_gamma.data_ptr(),
+                  f_gamma_sign=float(f_gamma_sign), g=g.data_ptr(), density=density.data_ptr(),
+                  gamma=float(gamma), tol=float(tol), max_iter=int(max_iter),
+                  sweeps_hint=int(sweeps_hint), u=u.data_ptr(), trace_u=trace_u.data_ptr(),
+                  trace_un=trace_un.data_ptr())
+        hist = np.zeros(max(int(max_iter), 1))
+        res = N.BvpResult(history=hist.ctypes.data_as(C.POINTER(C.c_double)))
+        status = self._lib.kfbi_richardson(self.handle, C.byref(b), C.byref(res), self.stream)
+        history = hist[: res.iterations].tolist()
+        last = history[-1] if history else None
+        N.check(status, iterations=int(max_iter), last_residual=last)
+        return res.iterations, res.residual, history
+
+    def heat_rhs(self, n, mask, u, F_old, F_new, a, want_norm=True):
+        norm = C.c_double(0.0)
+        N.check(self._lib.kfbi_heat_rhs(self.handle, int(n), N.ptr(mask), u.data_ptr(),
+                                        F_old.data_ptr(), F_new.data_ptr(), float(a),
+                                        C.byref(norm) if want_norm else None, self.stream))
+        return norm.value
+
+    def wave_rhs(self, n, mask, u_next, u_curr, F_curr, F_prev, F_new, kw, coef, want_norm=True):
+        norm = C.c_double(0.0)
+        N.check(self._lib.kfbi_wave_rhs(self.handle, int(n), N.ptr(mask), u_next.data_ptr(),
+                                        u_curr.data_ptr(), F_curr.data_ptr(), F_prev.data_ptr(),
+                                        F_new.data_ptr(), float(kw), float(coef),
+                                        C.byref(norm) if want_norm else None, self.stream))
+        return norm.value
+
+    def schr_ustar(self, n, mode, u, other, tau, out):
+        N.check(self._lib.kfbi_schr_ustar(self.handle, int(n), int(mode), u.data_ptr(),
+                                          other.data_ptr(), float(tau), out.data_ptr(),
+                                          self.stream))
+
+    def nonlinear_phase(self, n, ustar, v, w, half_tau, mask, out, kappa=None, F=None):
+        k = complex(kappa) if kappa is not None else 0j
+        res = C.c_double(0.0)
+        status = self._lib.kfbi_nonlinear_phase(
+            self.handle, int(n), ustar.data_ptr(), v.data_ptr(), float(w), float(half_tau),
+            N.ptr(mask), out.data_ptr(), k.real, k.imag, N.ptr(F), C.byref(res), self.stream)
+        N.check(status, iterations=50, last_residual=res.value)
+        return res.value
+
+    def mask_norm(self, n, mask, u):
+        norm = C.c_double(0.0)
+        N.check(self._lib.kfbi_mask_norm(self.handle, self._dt(u.is_complex()), int(n),
+                                         N.ptr(mask), u.data_ptr(), C.byref(norm), self.stream))
+        return norm.value

@@ -1,0 +1,292 @@
+// Box solve (Delta_h - kappa) u = rhs, dirichlet-zero closure
+// (BoxSolver.solve, boxsolve.py:46-94) as three HBM passes:
+//
+//   rows_fwd : rhs rows (+ the sparse jump corrections of those rows,
+//              interface.py:235-238 / bvp.py:319) -> DST-I along x -> panels
+//   cols     : panel of columns -> DST-I along y -> / (lam_p + lam_q - kappa)
+//              / (4 M^2) -> DST-I along y (adjoint engine) -> panels
+//   rows_inv : panels -> DST-I along x -> u rows, exact zero ring
+//
+// Panel layout of the intermediate spectrum ("panels"): 32-byte column
+// strips.  Real data: panel pp holds spectral x-columns 4pp..4pp+3 of every
+// interior row, P[(pp*M + r)*4 + w]; complex data: 2 columns,
+// P2[(pp*M + r)*2 + w].  A column pass therefore reads one contiguous
+// M*32-byte slab, and a row task writes full 32-byte sectors.
+//
+// Real data is packed two rows (or two columns) per complex sequence.
+#pragma once
+
+#include "dst_engine.cuh"
+
+namespace kfbi {
+
+struct BoxArgs {
+  int m, logm;
+  const double2 *tw;      // [m] exp(-i pi q / m)
+  const double *lam;      // [m+1] (2cos(p pi/m) - 2)/h^2 at p = 1..m-1
+  double kre, kim;        // kappa
+  double inv4m2;          // 1 / (4 m^2), exact power of two
+  void *panels;
+  const int *done;        // early-exit flag (Richardson sweeps), may be null
+};
+
+// Sparse right-hand-side corrections fused into the forward row pass.
+template <typename T>
+struct CorrArgs {
+  const T *jv;            // [n_edges][3] (u, u_axis, u_axis_axis) at the crossing
+  const int *row_group;   // [m+2] groups of grid row j: [row_group[j], row_group[j+1])
+  const int *group_start; // [n_groups+1]
+  const int *group_node;  // [n_groups] flat owner index
+  const int *rec_edge;
+  const double *rec_d;
+  const double *rec_sigma;
+};
+
+// Correction at one irregular node: sum over its arm records, in record
+// order, of sigma * (j_u + j_1 d + 0.5 j_2 d^2) (interface.py:228-237).
+template <typename T>
+KFBI_DEV T group_correction(const CorrArgs<T> &c, int g) {
+  using S = Sc<T>;
+  const int r0 = c.group_start[g], r1 = c.group_start[g + 1];
+  T acc = S::zero();
+  for (int r = r0; r < r1; ++r) {
+    const int e = c.rec_edge[r];
+    const T j0 = c.jv[3 * e], j1 = c.jv[3 * e + 1], j2 = c.jv[3 * e + 2];
+    const double d = c.rec_d[r];
+    T v = S::add(S::add(j0, S::rmul(j1, d)), S::rmul(S::rmul(j2, 0.5), d * d));
+    v = S::rmul(v, c.rec_sigma[r]);
+    acc = (r == r0) ? v : S::add(acc, v);
+  }
+  return acc;
+}
+
+// Dense scatter of the group sums (the standalone corrections() API).
+template <typename T>
+__global__ void scatter_groups_kernel(CorrArgs<T> c, int n_groups, T *out) {
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g < n_groups) out[c.group_node[g]] = group_correction<T>(c, g);
+}
+
+KFBI_DEV void add_component(double2 *sm, int p, bool neg, bool imag, double v) {
+  double *slot = reinterpret_cast<double *>(&sm[phys(p)]) + (imag ? 1 : 0);
+  *slot += neg ? -v : v;
+}
+KFBI_DEV void add_corr(double2 *sm, int p, bool neg, bool /*imag*/, double2 v) {
+  double2 &slot = sm[phys(p)];
+  slot = neg ? csub(slot, v) : cadd(slot, v);
+}
+
+// ---------------------------------------------------------------------------
+// forward row pass: one task = rows (j0, j0+1) packed (real) or row j0 (complex)
+template <bool CPLX>
+__global__ void __launch_bounds__(256)
+rows_fwd_kernel(BoxArgs a, const void *__restrict__ rhs, double sign,
+                CorrArgs<typename std::conditional<CPLX, double2, double>::type> corr) {
+  using T = typename std::conditional<CPLX, double2, double>::type;
+  extern __shared__ double2 sm[];
+  if (a.done && *a.done) return;
+  const int M = a.m, logN = a.logm, tid = threadIdx.x, NT = blockDim.x;
+  const int stride = M + 1;
+  const int j0 = CPLX ? blockIdx.x + 1 : 2 * blockIdx.x + 1;
+  const bool has2 = !CPLX && (j0 + 1 < M);
+
+  for (int n = 1 + tid; n < M; n += NT) {
+    double2 v;
+    if (CPLX) {
+      v = cscale(static_cast<const double2 *>(rhs)[(size_t)j0 * stride + n], sign);
+    } else {
+      const double *r = static_cast<const double *>(rhs);
+      v.x = r[(size_t)j0 * stride + n] * sign;
+      v.y = has2 ? r[(size_t)(j0 + 1) * stride + n] * sign : 0.0;
+    }
+    bool neg;
+    int p = dst_in_pos(n, logN, neg);
+    sm[phys(p)] = neg ? cneg(v) : v;
+  }
+  __syncthreads();
+  if (corr.jv) {
+    const int nrows = CPLX ? 1 : (has2 ? 2 : 1);
+    for (int q = 0; q < nrows; ++q) {
+      const int j = j0 + q;
+      const int g0 = corr.row_group[j], g1 = corr.row_group[j + 1];
+      for (int g = g0 + tid; g < g1; g += NT) {
+        T cv = group_correction<T>(corr, g);
+        int i = corr.group_node[g] - j * stride;
+        bool neg;
+        int p = dst_in_pos(i, logN, neg);
+        if constexpr (CPLX) add_corr(sm, p, neg, false, cv);
+        else add_component(sm, p, neg, q == 1, cv);
+      }
+    }
+    __syncthreads();
+  }
+  dst1_forward(sm, 1, logN, a.tw, tid, NT);
+
+  const int r = j0 - 1;
+  if (!CPLX) {
+    double *P = static_cast<double *>(a.panels);
+    for (int pp = tid; pp < (M >> 2); pp += NT) {
+      double re[4], im[4];
+#pragma unroll
+      for (int w = 0; w < 4; ++w) {
+        int k = 4 * pp + w + 1;
+        double2 c = (k < M) ? sm[phys(k)] : make_double2(0.0, 0.0);
+        re[w] = c.x;
+        im[w] = c.y;
+      }
+      double2 *d0 = reinterpret_cast<double2 *>(P + ((size_t)pp * M + r) * 4);
+      d0[0] = make_double2(re[0], re[1]);
+      d0[1] = make_double2(re[2], re[3]);
+      d0[2] = make_double2(im[0], im[1]);   // row r+1 directly follows row r
+      d0[3] = make_double2(im[2], im[3]);
+    }
+  } else {
+    double2 *P = static_cast<double2 *>(a.panels);
+    for (int pp = tid; pp < (M >> 1); pp += NT) {
+      int k = 2 * pp + 1;
+      double2 c0 = sm[phys(k)];
+      double2 c1 = (k + 1 < M) ? sm[phys(k + 1)] : make_double2(0.0, 0.0);
+      double2 *d0 = P + ((size_t)pp * M + r) * 2;
+      d0[0] = c0;
+      d0[1] = c1;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// fused column pass: panel -> DST(y) -> scale -> DST(y) -> panel (in place)
+template <bool CPLX>
+__global__ void __launch_bounds__(512) cols_kernel(BoxArgs a) {
+  extern __shared__ double2 sm[];
+  if (a.done && *a.done) return;
+  const int M = a.m, logN = a.logm, tid = threadIdx.x, NT = blockDim.x;
+  const int pp = blockIdx.x;
+  double2 *P = static_cast<double2 *>(a.panels) + (size_t)pp * M * 2;
+  double2 *s1 = sm + M;
+
+  for (int r = tid; r < M - 1; r += NT) {
+    double2 v0 = P[2 * r], v1 = P[2 * r + 1];
+    bool neg;
+    int p = phys(dst_in_pos(r + 1, logN, neg));
+    sm[p] = neg ? cneg(v0) : v0;
+    s1[p] = neg ? cneg(v1) : v1;
+  }
+  __syncthreads();
+  dst1_forward(sm, 2, logN, a.tw, tid, NT);
+
+  for (int idx = tid; idx < 2 * (M - 1); idx += NT) {
+    const int q = idx >= M - 1 ? 1 : 0;
+    const int p = idx - q * (M - 1) + 1;         // spectral y index
+    double2 *slot = &sm[q * M + phys(p)];
+    double2 v = *slot;
+    const double lp = a.lam[p];
+    if (!CPLX) {
+      const int kx = 4 * pp + 2 * q + 1;          // spectral x index of .x
+      double da = (lp + a.lam[kx < M ? kx : 1]) - a.kre;
+      double db = (lp + a.lam[kx + 1 < M ? kx + 1 : 1]) - a.kre;
+      v.x = kx < M ? (v.x / da) * a.inv4m2 : 0.0;
+      v.y = kx + 1 < M ? (v.y / db) * a.inv4m2 : 0.0;
+    } else {
+      const int kx = 2 * pp + q + 1;
+      if (kx < M) {
+        double2 d = make_double2((lp + a.lam[kx]) - a.kre, -a.kim);
+        v = cscale(cdiv(v, d), a.inv4m2);
+      } else {
+        v = make_double2(0.0, 0.0);
+      }
+    }
+    *slot = v;
+  }
+  __syncthreads();
+  dst1_adjoint(sm, 2, logN, a.tw, tid, NT);
+
+  for (int r = tid; r < M - 1; r += NT) {
+    bool neg;
+    int p = phys(dst_in_pos(r + 1, logN, neg));
+    double2 v0 = sm[p], v1 = s1[p];
+    P[2 * r] = neg ? cneg(v0) : v0;
+    P[2 * r + 1] = neg ? cneg(v1) : v1;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// inverse row pass: panels -> DST(x) (adjoint engine, gather store) -> u rows
+template <bool CPLX>
+__global__ void __launch_bounds__(256) rows_inv_kernel(BoxArgs a, void *__restrict__ u) {
+  extern __shared__ double2 sm[];
+  if (a.done && *a.done) return;
+  const int M = a.m, logN = a.logm, tid = threadIdx.x, NT = blockDim.x;
+  const int stride = M + 1;
+  const int j0 = CPLX ? blockIdx.x + 1 : 2 * blockIdx.x + 1;
+  const bool has2 = !CPLX && (j0 + 1 < M);
+  const int r = j0 - 1;
+
+  if (!CPLX) {
+    const double *P = static_cast<const double *>(a.panels);
+    for (int pp = tid; pp < (M >> 2); pp += NT) {
+      const double2 *s0 = reinterpret_cast<const double2 *>(P + ((size_t)pp * M + r) * 4);
+      double2 a01 = s0[0], a23 = s0[1], b01 = s0[2], b23 = s0[3];
+      double re[4] = {a01.x, a01.y, a23.x, a23.y};
+      double im[4] = {b01.x, b01.y, b23.x, b23.y};
+#pragma unroll
+      for (int w = 0; w < 4; ++w) {
+        int k = 4 * pp + w + 1;
+        if (k < M) sm[phys(k)] = make_double2(re[w], has2 ? im[w] : 0.0);
+      }
+    }
+  } else {
+    const double2 *P = static_cast<const double2 *>(a.panels);
+    for (int pp = tid; pp < (M >> 1); pp += NT) {
+      const double2 *s0 = P + ((size_t)pp * M + r) * 2;
+      int k = 2 * pp + 1;
+      sm[phys(k)] = s0[0];
+      if (k + 1 < M) sm[phys(k + 1)] = s0[1];
+    }
+  }
+  __syncthreads();
+  dst1_adjoint(sm, 1, logN, a.tw, tid, NT);
+
+  // gather + store, with the zero ring (boxsolve.py:90-93)
+  if (!CPLX) {
+    double *U = static_cast<double *>(u);
+    double *u0 = U + (size_t)j0 * stride;
+    double *u1 = U + (size_t)(j0 + 1) * stride;   // row M (ring) when !has2
+    for (int n = tid; n <= M; n += NT) {
+      double x = 0.0, y = 0.0;
+      if (n >= 1 && n < M) {
+        bool neg;
+        double2 v = sm[phys(dst_in_pos(n, logN, neg))];
+        x = neg ? -v.x : v.x;
+        y = neg ? -v.y : v.y;
+      }
+      u0[n] = x;
+      u1[n] = has2 ? y : 0.0;
+    }
+  } else {
+    double2 *U = static_cast<double2 *>(u);
+    double2 *u0 = U + (size_t)j0 * stride;
+    for (int n = tid; n <= M; n += NT) {
+      double2 v = make_double2(0.0, 0.0);
+      if (n >= 1 && n < M) {
+        bool neg;
+        v = sm[phys(dst_in_pos(n, logN, neg))];
+        if (neg) v = cneg(v);
+      }
+      u0[n] = v;
+    }
+    if (j0 == M - 1) {
+      for (int n = tid; n <= M; n += NT) U[(size_t)M * stride + n] = make_double2(0.0, 0.0);
+    }
+  }
+  if (blockIdx.x == 0) {
+    if (!CPLX) {
+      double *U = static_cast<double *>(u);
+      for (int n = tid; n <= M; n += NT) U[n] = 0.0;
+    } else {
+      double2 *U = static_cast<double2 *>(u);
+      for (int n = tid; n <= M; n += NT) U[n] = make_double2(0.0, 0.0);
+    }
+  }
+}
+
+}  // namespace kfbi

@@ -1,0 +1,290 @@
+// Per-sweep boundary kernels of the Richardson iteration:
+//   jumps_d1 / jumps_d2 : compute_jumps (interface.py:171-203) with the
+//                         spectral derivative of geometry.py:415-444 applied
+//                         as a circulant matvec (n_ctl is any even number)
+//   corr_edges          : W @ JM of corrections (interface.py:225-231), one
+//                         streamed W row per unique sign-change edge (both
+//                         records of an edge share theta, grid.py:243-254)
+//   extract_update      : TraceExtractor.extract (bvp.py:88-104) + density
+//                         update and max-norm (bvp.py:325-344), last block
+//                         closes the sweep (history, convergence flag)
+#pragma once
+
+#include "common.cuh"
+
+namespace kfbi {
+
+// Device-resident Richardson bookkeeping (one per plan).
+struct RichState {
+  int done;                       // 0 running, 1 converged, 2 max_iter reached
+  int iters;                      // sweeps completed
+  int max_iter;
+  int pad0;
+  double tol;
+  double last_res;
+  unsigned long long res_bits;    // running max |update| of the current sweep
+  unsigned int arrive;            // blocks of extract_update finished
+  unsigned int pad1;
+};
+
+struct CtlGeom {
+  int n;                          // control points
+  const double *deriv_col;        // [n] first column of d/dtheta
+  const double *speed;
+  const double *tangent;          // [n][2]
+  const double *normal;           // [n][2]
+  const double *dtan_ds;          // [n][2]
+  const double *inv3;             // [n][3][3]
+};
+
+// out_i = (sum_j D[(i-j) mod n] v_j) / speed_i   (warp per output)
+template <typename T>
+KFBI_DEV T circ_deriv(const CtlGeom &g, const T *__restrict__ v, int i, int lane) {
+  using S = Sc<T>;
+  T acc = S::zero();
+  for (int j = lane; j < g.n; j += 32) {
+    int idx = i - j;
+    if (idx < 0) idx += g.n;
+    acc = S::add(acc, S::rmul(v[j], __ldg(&g.deriv_col[idx])));
+  }
+  return acc;
+}
+
+KFBI_DEV double warp_reduce_T(double v) { return warp_sum(v); }
+KFBI_DEV double2 warp_reduce_T(double2 v) {
+  return make_double2(warp_sum(v.x), warp_sum(v.y));
+}
+
+// phi_s (and psi_s when psi != nullptr).
+template <typename T>
+__global__ void jumps_d1_kernel(CtlGeom g, const T *__restrict__ phi, const T *__restrict__ psi,
+                                T *phi_s, T *psi_s, const int *done) {
+  if (done && *done) return;
+  const int lane = threadIdx.x & 31;
+  const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (i >= g.n) return;
+  const double sp = g.speed[i];
+  if (phi) {
+    T a = warp_reduce_T(circ_deriv<T>(g, phi, i, lane));
+    if (lane == 0) phi_s[i] = rdiv(a, sp);
+  }
+  if (psi) {
+    T b = warp_reduce_T(circ_deriv<T>(g, psi, i, lane));
+    if (lane == 0) psi_s[i] = rdiv(b, sp);
+  }
+}
+
+// phi_ss, then the 2x2 / 3x3 jump systems; writes JM as SoA [6][n].
+template <typename T>
+__global__ void jumps_d2_kernel(CtlGeom g, const T *__restrict__ phi, const T *__restrict__ psi,
+                                const T *__restrict__ phi_s, const T *__restrict__ psi_s,
+                                const T *__restrict__ f_gamma, double fg_sign, double kre,
+                                double kim, T *jm, const int *done) {
+  using S = Sc<T>;
+  if (done && *done) return;
+  const int lane = threadIdx.x & 31;
+  const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (i >= g.n) return;
+  T pss = S::zero();
+  if (phi) pss = warp_reduce_T(circ_deriv<T>(g, phi_s, i, lane));
+  if (lane != 0) return;
+  const double sp = g.speed[i];
+  if (phi) pss = rdiv(pss, sp);
+  const T ju = phi ? phi[i] : S::zero();
+  const T ps = phi ? phi_s[i] : S::zero();
+  const T pv = psi ? psi[i] : S::zero();
+  const T pvs = psi ? psi_s[i] : S::zero();
+  const double t1 = g.tangent[2 * i], t2 = g.tangent[2 * i + 1];
+  const double dt1 = g.dtan_ds[2 * i], dt2 = g.dtan_ds[2 * i + 1];
+  const T jx = S::add(S::rmul(ps, t1), S::rmul(pv, t2));
+  const T jy = S::sub(S::rmul(ps, t2), S::rmul(pv, t1));
+  const T r0 = S::sub(S::sub(pss, S::rmul(jx, dt1)), S::rmul(jy, dt2));
+  const T r1 = S::add(S::sub(pvs, S::rmul(jx, dt2)), S::rmul(jy, dt1));
+  const T r2 = S::add(S::rmul(f_gamma[i], fg_sign), S::kmul(kre, kim, ju));
+  const double *A = g.inv3 + 9 * i;
+  const int n = g.n;
+  jm[i] = ju;
+  jm[n + i] = jx;
+  jm[2 * n + i] = jy;
+#pragma unroll
+  for (int r = 0; r < 3; ++r) {
+    T v = S::add(S::add(S::rmul(r0, A[3 * r]), S::rmul(r1, A[3 * r + 1])), S::rmul(r2, A[3 * r + 2]));
+    jm[(3 + r) * n + i] = v;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// jv[e] = (W_e . JM_u, W_e . JM_a, W_e . JM_aa), a = x (horizontal) or y.
+// A warp owns EW consecutive edges and streams their W rows once.
+struct EdgeArgs {
+  int n_edges, n_ctl, ld;         // ld: row stride of W (even)
+  const double *W;
+  const signed char *axis;
+};
+
+template <typename T, int EW>
+__global__ void __launch_bounds__(256)
+corr_edges_kernel(EdgeArgs ea, const T *__restrict__ jm, T *jv, const int *done) {
+  using S = Sc<T>;
+  if (done && *done) return;
+  const int lane = threadIdx.x & 31;
+  const int e0 = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * EW;
+  if (e0 >= ea.n_edges) return;
+  const int n = ea.n_ctl;
+  const T *ju = jm, *jx = jm + n, *jy = jm + 2 * n, *jxx = jm + 3 * n, *jyy = jm + 5 * n;
+  bool vert[EW];
+  const double *wr[EW];
+#pragma unroll
+  for (int q = 0; q < EW; ++q) {
+    int e = min(e0 + q, ea.n_edges - 1);
+    vert[q] = ea.axis[e] != 0;
+    wr[q] = ea.W + (size_t)e * ea.ld;
+  }
+  T acc[EW][3];
+#pragma unroll
+  for (int q = 0; q < EW; ++q) acc[q][0] = acc[q][1] = acc[q][2] = S::zero();
+  for (int i = lane; i < n; i += 32) {
+    const T a0 = ju[i], ax = jx[i], ay = jy[i], axx = jxx[i], ayy = jyy[i];
+#pragma unroll
+    for (int q = 0; q < EW; ++q) {
+      const double w = __ldcs(wr[q] + i);
+      acc[q][0] = S::add(acc[q][0], S::rmul(a0, w));
+      acc[q][1] = S::add(acc[q][1], S::rmul(vert[q] ? ay : ax, w));
+      acc[q][2] = S::add(acc[q][2], S::rmul(vert[q] ? ayy : axx, w));
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < EW; ++q) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) acc[q][c] = warp_reduce_T(acc[q][c]);
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int q = 0; q < EW; ++q) {
+      if (e0 + q < ea.n_edges) {
+        jv[3 * (e0 + q)] = acc[q][0];
+        jv[3 * (e0 + q) + 1] = acc[q][1];
+        jv[3 * (e0 + q) + 2] = acc[q][2];
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+struct ExtractArgs {
+  int n, m;
+  double h, inv_h;
+  const int *stencil;             // [n][6]
+  const double *ainv_rows;        // [n][3][6]
+  const double *jcoef;            // [n][6][6]
+  const double *normal;           // [n][2]
+};
+
+// (u+, ux+, uy+) at control point p (bvp.py:98-104).
+template <typename T>
+KFBI_DEV void extract_point(const ExtractArgs &x, const T *__restrict__ u, const T *__restrict__ jm,
+                            int p, T &tu, T &tx, T &ty) {
+  using S = Sc<T>;
+  T jp[6];
+#pragma unroll
+  for (int k = 0; k < 6; ++k) jp[k] = jm[k * x.n + p];
+  T vals[6];
+#pragma unroll
+  for (int s = 0; s < 6; ++s) {
+    const double *jc = x.jcoef + 36 * p + 6 * s;
+    T corr = S::rmul(jp[0], jc[0]);
+#pragma unroll
+    for (int k = 1; k < 6; ++k) corr = S::add(corr, S::rmul(jp[k], jc[k]));
+    vals[s] = S::add(u[x.stencil[6 * p + s]], corr);
+  }
+  T c[3];
+#pragma unroll
+  for (int r = 0; r < 3; ++r) {
+    const double *ar = x.ainv_rows + 18 * p + 6 * r;
+    T acc = S::rmul(vals[0], ar[0]);
+#pragma unroll
+    for (int s = 1; s < 6; ++s) acc = S::add(acc, S::rmul(vals[s], ar[s]));
+    c[r] = acc;
+  }
+  tu = c[0];
+  tx = rdiv(c[1], x.h);
+  ty = rdiv(c[2], x.h);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256)
+extract_kernel(ExtractArgs x, const T *__restrict__ u, const T *__restrict__ jm, T *out) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= x.n) return;
+  T tu, tx, ty;
+  extract_point<T>(x, u, jm, p, tu, tx, ty);
+  out[p] = tu;
+  out[x.n + p] = tx;
+  out[2 * x.n + p] = ty;
+}
+
+// Extraction + density update + residual; the last block closes the sweep.
+template <typename T>
+__global__ void __launch_bounds__(256)
+extract_update_kernel(ExtractArgs x, const T *__restrict__ u, const T *__restrict__ jm,
+                      const T *__restrict__ g, T *density, T *trace_u, T *trace_un,
+                      double gamma, int dirichlet, RichState *st, double *history) {
+  using S = Sc<T>;
+  if (st->done) return;
+  __shared__ double red[32];
+  __shared__ bool is_last;
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  double mag = 0.0;
+  if (p < x.n) {
+    T tu, tx, ty;
+    extract_point<T>(x, u, jm, p, tu, tx, ty);
+    const double nx = x.normal[2 * p], ny = x.normal[2 * p + 1];
+    T tun = S::add(S::rmul(tx, nx), S::rmul(ty, ny));
+    T target = dirichlet ? tu : tun;
+    T upd = S::rmul(S::sub(g[p], target), gamma);
+    density[p] = S::add(density[p], upd);
+    trace_u[p] = tu;
+    trace_un[p] = tun;
+    mag = S::abs(upd);
+  }
+  mag = warp_nanmax(mag);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) red[wid] = mag;
+  __syncthreads();
+  if (wid == 0) {
+    double v = lane < (blockDim.x >> 5) ? red[lane] : 0.0;
+    v = warp_nanmax(v);
+    if (lane == 0) {
+      atomic_max_nonneg(&st->res_bits, v);
+      __threadfence();
+      unsigned int ticket = atomicAdd(&st->arrive, 1u);
+      is_last = ticket == gridDim.x - 1;
+    }
+  }
+  __syncthreads();
+  if (is_last && threadIdx.x == 0) {
+    __threadfence();
+    unsigned long long bits = atomicAdd(&st->res_bits, 0ull);
+    double res = __longlong_as_double((long long)bits);
+    int it = st->iters + 1;
+    history[it - 1] = res;
+    st->iters = it;
+    st->last_res = res;
+    if (res <= st->tol) st->done = 1;
+    else if (it >= st->max_iter) st->done = 2;
+    st->res_bits = 0ull;
+    st->arrive = 0u;
+  }
+}
+
+__global__ void rich_init_kernel(RichState *st, int max_iter, double tol) {
+  st->done = 0;
+  st->iters = 0;
+  st->max_iter = max_iter;
+  st->tol = tol;
+  st->last_res = 0.0;
+  st->res_bits = 0ull;
+  st->arrive = 0u;
+}
+
+}  // namespace kfbi

@@ -1,0 +1,688 @@
+// C ABI of the B200-native KFBI hot path (include/kfbi_b200.h).
+//
+// One translation unit: the device kernels live in the *.cuh headers, this
+// file owns the plan object (device tables + scratch), launch bookkeeping,
+// per-kernel-name CUDA-event timing (the Backend.timings contract of
+// engine.py:84-95) and error reporting.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/kfbi_b200.h"
+#include "box_kernels.cuh"
+#include "interface_kernels.cuh"
+#include "stepping_kernels.cuh"
+
+using namespace kfbi;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+kfbi_status fail(kfbi_status code, const std::string &msg) {
+  g_last_error = msg;
+  return code;
+}
+
+#define KFBI_CUDA(call, kname)                                                     \
+  do {                                                                             \
+    cudaError_t _e = (call);                                                       \
+    if (_e != cudaSuccess)                                                         \
+      return fail(KFBI_E_CUDA, std::string("kernel '") + (kname) + "': " +         \
+                                   cudaGetErrorString(_e) + " (" #call ")");       \
+  } while (0)
+
+const char *kKernelNames[KFBI_N_KERNEL_NAMES] = {
+    "classify-nodes", "edge-intersections", "jumps-and-corrections",
+    "transform-rows", "transform-cols",     "diagonal-scale",
+    "extract-traces", "density-update",     "rhs-update"};
+
+struct Pending {
+  int name;
+  cudaEvent_t a, b;
+};
+
+template <typename T>
+struct DevBuf {
+  T *p = nullptr;
+  size_t n = 0;
+  cudaError_t ensure(size_t count) {
+    if (count <= n) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+    cudaError_t e = cudaMalloc(&p, count * sizeof(T));
+    if (e == cudaSuccess) n = count;
+    return e;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+};
+
+template <typename T>
+cudaError_t upload(DevBuf<T> &b, const T *host, size_t count) {
+  cudaError_t e = b.ensure(count ? count : 1);
+  if (e != cudaSuccess) return e;
+  if (count) e = cudaMemcpy(b.p, host, count * sizeof(T), cudaMemcpyHostToDevice);
+  return e;
+}
+
+}  // namespace
+
+struct kfbi_plan {
+  int device = 0;
+  int m = 0, logm = 0;
+  double h = 0.0;
+  DevBuf<double2> tw;
+  DevBuf<double> lam;
+  DevBuf<double2> panels;       // m*m complex slots (sized for c128)
+  // geometry
+  bool has_geo = false;
+  int n_ctl = 0, n_edges = 0, n_rec = 0, n_groups = 0, w_ld = 0;
+  DevBuf<double> W;
+  DevBuf<signed char> edge_axis;
+  DevBuf<int> rec_edge, group_start, group_node, row_group, stencil;
+  DevBuf<double> rec_d, rec_sigma, deriv_col, speed, tangent, normal, dtan_ds, inv3;
+  DevBuf<double> ainv_rows, jcoef;
+  // per-sweep scratch (sized for c128)
+  DevBuf<double2> d1, psi_s, jm, jv;
+  DevBuf<double> history;
+  DevBuf<RichState> st;
+  DevBuf<unsigned long long> red;   // reduction slots
+  RichState *st_host = nullptr;     // pinned mirror
+  unsigned long long *red_host = nullptr;
+  // timing / accounting
+  bool timing = true;
+  std::vector<Pending> pending;
+  std::vector<cudaEvent_t> pool;
+  double ms[KFBI_N_KERNEL_NAMES] = {0};
+  int64_t calls[KFBI_N_KERNEL_NAMES] = {0};
+  int64_t launches = 0;
+
+  cudaEvent_t take_event() {
+    if (!pool.empty()) {
+      cudaEvent_t e = pool.back();
+      pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+  }
+};
+
+namespace {
+
+// Launch helper: per-name accounting + optional event bracketing.
+template <typename F>
+kfbi_status launch(kfbi_plan *p, int name, cudaStream_t s, F &&fn) {
+  Pending pe{name, nullptr, nullptr};
+  if (p->timing) {
+    pe.a = p->take_event();
+    pe.b = p->take_event();
+    cudaEventRecord(pe.a, s);
+  }
+  fn();
+  cudaError_t e = cudaGetLastError();
+  if (p->timing) {
+    cudaEventRecord(pe.b, s);
+    p->pending.push_back(pe);
+  }
+  p->calls[name] += 1;
+  p->launches += 1;
+  if (e != cudaSuccess)
+    return fail(KFBI_E_CUDA, std::string("kernel '") + kKernelNames[name] +
+                                 "': launch failed: " + cudaGetErrorString(e));
+  return KFBI_OK;
+}
+
+#define KFBI_TRY(expr)                 \
+  do {                                 \
+    kfbi_status _s = (expr);           \
+    if (_s != KFBI_OK) return _s;      \
+  } while (0)
+
+int ilog2(int v) {
+  int l = 0;
+  while ((1 << l) < v) ++l;
+  return l;
+}
+
+kfbi_status check_plan(kfbi_plan *p) {
+  if (!p) return fail(KFBI_E_CONFIG, "null plan");
+  cudaError_t e = cudaSetDevice(p->device);
+  if (e != cudaSuccess) return fail(KFBI_E_CUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(e));
+  return KFBI_OK;
+}
+
+kfbi_status check_geo(kfbi_plan *p) {
+  KFBI_TRY(check_plan(p));
+  if (!p->has_geo) return fail(KFBI_E_CONFIG, "plan has no geometry (call kfbi_plan_set_geometry)");
+  return KFBI_OK;
+}
+
+BoxArgs box_args(kfbi_plan *p, double kre, double kim, const int *done) {
+  BoxArgs a;
+  a.m = p->m;
+  a.logm = p->logm;
+  a.tw = p->tw.p;
+  a.lam = p->lam.p;
+  a.kre = kre;
+  a.kim = kim;
+  a.inv4m2 = 1.0 / (4.0 * (double)p->m * (double)p->m);
+  a.panels = p->panels.p;
+  a.done = done;
+  return a;
+}
+
+template <typename T>
+CorrArgs<T> corr_args(kfbi_plan *p, const T *jv) {
+  CorrArgs<T> c;
+  c.jv = jv;
+  c.row_group = p->row_group.p;
+  c.group_start = p->group_start.p;
+  c.group_node = p->group_node.p;
+  c.rec_edge = p->rec_edge.p;
+  c.rec_d = p->rec_d.p;
+  c.rec_sigma = p->rec_sigma.p;
+  return c;
+}
+
+CtlGeom ctl_geom(kfbi_plan *p) {
+  CtlGeom g;
+  g.n = p->n_ctl;
+  g.deriv_col = p->deriv_col.p;
+  g.speed = p->speed.p;
+  g.tangent = p->tangent.p;
+  g.normal = p->normal.p;
+  g.dtan_ds = p->dtan_ds.p;
+  g.inv3 = p->inv3.p;
+  return g;
+}
+
+ExtractArgs extract_args(kfbi_plan *p) {
+  ExtractArgs x;
+  x.n = p->n_ctl;
+  x.m = p->m;
+  x.h = p->h;
+  x.inv_h = 1.0 / p->h;
+  x.stencil = p->stencil.p;
+  x.ainv_rows = p->ainv_rows.p;
+  x.jcoef = p->jcoef.p;
+  x.normal = p->normal.p;
+  return x;
+}
+
+template <bool CPLX>
+kfbi_status set_smem_limits(kfbi_plan *p) {
+  size_t row = (size_t)p->m * sizeof(double2);
+  KFBI_CUDA(cudaFuncSetAttribute(rows_fwd_kernel<CPLX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)row), "transform-rows");
+  KFBI_CUDA(cudaFuncSetAttribute(rows_inv_kernel<CPLX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)row), "transform-rows");
+  KFBI_CUDA(cudaFuncSetAttribute(cols_kernel<CPLX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)(2 * row)), "transform-cols");
+  return KFBI_OK;
+}
+
+// The three passes of one box solve.  rhs is an (M+1)^2 field (scaled by
+// sign); jv != nullptr fuses the jump corrections of the plan's geometry.
+template <bool CPLX>
+kfbi_status box_passes(kfbi_plan *p, double kre, double kim, const void *rhs, double sign,
+                       const void *jv, void *u, const int *done, cudaStream_t s) {
+  using T = typename std::conditional<CPLX, double2, double>::type;
+  BoxArgs a = box_args(p, kre, kim, done);
+  const int M = p->m;
+  const int ntask = CPLX ? M - 1 : M / 2;
+  const int npanel = CPLX ? M / 2 : M / 4;
+  const size_t row = (size_t)M * sizeof(double2);
+  CorrArgs<T> c = corr_args<T>(p, static_cast<const T *>(jv));
+  if (!jv) c.jv = nullptr;
+  KFBI_TRY(launch(p, KFBI_K_ROWS, s, [&] {
+    rows_fwd_kernel<CPLX><<<ntask, 256, row, s>>>(a, rhs, sign, c);
+  }));
+  KFBI_TRY(launch(p, KFBI_K_COLS, s, [&] {
+    cols_kernel<CPLX><<<npanel, 512, 2 * row, s>>>(a);
+  }));
+  KFBI_TRY(launch(p, KFBI_K_ROWS, s, [&] {
+    rows_inv_kernel<CPLX><<<ntask, 256, row, s>>>(a, u);
+  }));
+  return KFBI_OK;
+}
+
+kfbi_status box_dispatch(kfbi_plan *p, int dtype, double kre, double kim, const void *rhs,
+                         double sign, const void *jv, void *u, const int *done,
+                         cudaStream_t s) {
+  if (dtype == KFBI_C128) return box_passes<true>(p, kre, kim, rhs, sign, jv, u, done, s);
+  if (kim != 0.0) return fail(KFBI_E_CONFIG, "complex kappa requires the c128 path");
+  return box_passes<false>(p, kre, kim, rhs, sign, jv, u, done, s);
+}
+
+// jumps (two kernels) for dtype T; jm is SoA [6][n].
+template <typename T>
+kfbi_status jumps_T(kfbi_plan *p, double kre, double kim, const void *phi, const void *psi,
+                    const void *fg, double fg_sign, void *jm, const int *done, cudaStream_t s) {
+  CtlGeom g = ctl_geom(p);
+  const int warps_per_block = 8;
+  const int blocks = (p->n_ctl + warps_per_block - 1) / warps_per_block;
+  T *d1 = reinterpret_cast<T *>(p->d1.p);
+  T *ps = reinterpret_cast<T *>(p->psi_s.p);
+  const T *ph = static_cast<const T *>(phi);
+  const T *pv = static_cast<const T *>(psi);
+  KFBI_TRY(launch(p, KFBI_K_JUMPS, s, [&] {
+    jumps_d1_kernel<T><<<blocks, 32 * warps_per_block, 0, s>>>(g, ph, pv, d1, ps, done);
+  }));
+  KFBI_TRY(launch(p, KFBI_K_JUMPS, s, [&] {
+    jumps_d2_kernel<T><<<blocks, 32 * warps_per_block, 0, s>>>(
+        g, ph, pv, d1, ps, static_cast<const T *>(fg), fg_sign, kre, kim,
+        static_cast<T *>(jm), done);
+  }));
+  return KFBI_OK;
+}
+
+template <typename T>
+kfbi_status edges_T(kfbi_plan *p, const void *jm, void *jv, const int *done, cudaStream_t s) {
+  EdgeArgs ea{p->n_edges, p->n_ctl, p->w_ld, p->W.p, p->edge_axis.p};
+  constexpr int EW = 4;
+  const int warps = (p->n_edges + EW - 1) / EW;
+  const int blocks = (warps + 7) / 8;
+  if (p->n_edges == 0) return KFBI_OK;
+  return launch(p, KFBI_K_JUMPS, s, [&] {
+    corr_edges_kernel<T, EW><<<blocks, 256, 0, s>>>(ea, static_cast<const T *>(jm),
+                                                    static_cast<T *>(jv), done);
+  });
+}
+
+kfbi_status read_norm(kfbi_plan *p, cudaStream_t s, double *out) {
+  KFBI_CUDA(cudaMemcpyAsync(p->red_host, p->red.p, sizeof(unsigned long long),
+                            cudaMemcpyDeviceToHost, s), "rhs-update");
+  KFBI_CUDA(cudaStreamSynchronize(s), "rhs-update");
+  long long bits = (long long)p->red_host[0];
+  double v;
+  std::memcpy(&v, &bits, sizeof v);
+  if (out) *out = v;
+  return KFBI_OK;
+}
+
+int elem_blocks(long n) {
+  long b = (n + 255) / 256;
+  if (b > 148 * 16) b = 148 * 16;
+  if (b < 1) b = 1;
+  return (int)b;
+}
+
+// One Richardson sweep, every kernel guarded by the device `done` flag.
+template <typename T>
+kfbi_status sweep(kfbi_plan *p, const kfbi_bvp *b, cudaStream_t s) {
+  const int *done = &p->st.p->done;
+  const bool cplx = std::is_same<T, double2>::value;
+  KFBI_TRY(jumps_T<T>(p, b->kappa_re, b->kappa_im, b->density, nullptr, b->f_gamma,
+                      b->f_gamma_sign, p->jm.p, done, s));
+  KFBI_TRY(edges_T<T>(p, p->jm.p, p->jv.p, done, s));
+  if (cplx) KFBI_TRY(box_passes<true>(p, b->kappa_re, b->kappa_im, b->F, b->F_sign, p->jv.p, b->u, done, s));
+  else KFBI_TRY(box_passes<false>(p, b->kappa_re, b->kappa_im, b->F, b->F_sign, p->jv.p, b->u, done, s));
+  ExtractArgs x = extract_args(p);
+  const int blocks = (p->n_ctl + 255) / 256;
+  return launch(p, KFBI_K_DENSITY, s, [&] {
+    extract_update_kernel<T><<<blocks, 256, 0, s>>>(
+        x, static_cast<const T *>(b->u), reinterpret_cast<const T *>(p->jm.p),
+        static_cast<const T *>(b->g), static_cast<T *>(b->density), static_cast<T *>(b->trace_u),
+        static_cast<T *>(b->trace_un), b->gamma, 1, p->st.p, p->history.p);
+  });
+}
+
+}  // namespace
+
+// ===========================================================================
+extern "C" {
+
+const char *kfbi_last_error(void) { return g_last_error.c_str(); }
+const char *kfbi_version(void) { return "kfbi_b200 0.1.0 (sm_100a)"; }
+
+kfbi_status kfbi_plan_create(const kfbi_grid_desc *desc, kfbi_plan **out) {
+  if (!desc || !out) return fail(KFBI_E_CONFIG, "null argument");
+  const int m = desc->m;
+  if (m < 16 || (m & (m - 1)) != 0) return fail(KFBI_E_GRID, "M must be a power of two and >= 16");
+  if (m > 4096) return fail(KFBI_E_CONFIG, "this build supports M <= 4096 on one GPU");
+  if (!(desc->h > 0)) return fail(KFBI_E_GRID, "grid spacing must be positive");
+  kfbi_plan *p = new kfbi_plan();
+  p->device = desc->device;
+  p->m = m;
+  p->logm = ilog2(m);
+  p->h = desc->h;
+  cudaError_t e = cudaSetDevice(p->device);
+  if (e != cudaSuccess) {
+    delete p;
+    return fail(KFBI_E_CUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(e));
+  }
+  // twiddles exp(-i pi q / m) in extended precision; lambda_p exactly as
+  // boxsolve.py:43 evaluates it in double: (2 cos(p pi / m) - 2) / h^2
+  std::vector<double2> tw(m);
+  for (int q = 0; q < m; ++q) {
+    long double ang = 3.14159265358979323846264338327950288L * (long double)q / (long double)m;
+    tw[q] = make_double2((double)cosl(ang), (double)-sinl(ang));
+  }
+  std::vector<double> lam(m + 1, 0.0);
+  for (int q = 1; q < m; ++q) {
+    double ang = (double)q * M_PI / (double)m;
+    lam[q] = (2.0 * std::cos(ang) - 2.0) / (desc->h * desc->h);
+  }
+  if ((e = upload(p->tw, tw.data(), tw.size())) != cudaSuccess ||
+      (e = upload(p->lam, lam.data(), lam.size())) != cudaSuccess ||
+      (e = p->panels.ensure((size_t)m * m)) != cudaSuccess ||
+      (e = p->st.ensure(1)) != cudaSuccess || (e = p->red.ensure(4)) != cudaSuccess) {
+    kfbi_plan_destroy(p);
+    return fail(KFBI_E_CUDA, std::string("plan allocation: ") + cudaGetErrorString(e));
+  }
+  cudaMemset(p->panels.p, 0, (size_t)m * m * sizeof(double2));
+  cudaMallocHost(&p->st_host, sizeof(RichState));
+  cudaMallocHost(&p->red_host, 4 * sizeof(unsigned long long));
+  kfbi_status st = set_smem_limits<false>(p);
+  if (st == KFBI_OK) st = set_smem_limits<true>(p);
+  if (st != KFBI_OK) {
+    kfbi_plan_destroy(p);
+    return st;
+  }
+  *out = p;
+  return KFBI_OK;
+}
+
+kfbi_status kfbi_plan_destroy(kfbi_plan *p) {
+  if (!p) return KFBI_OK;
+  cudaSetDevice(p->device);
+  cudaDeviceSynchronize();
+  for (auto &pe : p->pending) {
+    cudaEventDestroy(pe.a);
+    cudaEventDestroy(pe.b);
+  }
+  for (auto e : p->pool) cudaEventDestroy(e);
+  p->tw.release(); p->lam.release(); p->panels.release();
+  p->W.release(); p->edge_axis.release(); p->rec_edge.release(); p->group_start.release();
+  p->group_node.release(); p->row_group.release(); p->stencil.release(); p->rec_d.release();
+  p->rec_sigma.release(); p->deriv_col.release(); p->speed.release(); p->tangent.release();
+  p->normal.release(); p->dtan_ds.release(); p->inv3.release(); p->ainv_rows.release();
+  p->jcoef.release(); p->d1.release(); p->psi_s.release(); p->jm.release(); p->jv.release();
+  p->history.release(); p->st.release(); p->red.release();
+  if (p->st_host) cudaFreeHost(p->st_host);
+  if (p->red_host) cudaFreeHost(p->red_host);
+  delete p;
+  return KFBI_OK;
+}
+
+kfbi_status kfbi_box_solve(kfbi_plan *p, int32_t dtype, double kre, double kim, const void *rhs,
+                           void *u, void *stream) {
+  KFBI_TRY(check_plan(p));
+  if (!rhs || !u) return fail(KFBI_E_CONFIG, "null field pointer");
+  return box_dispatch(p, dtype, kre, kim, rhs, 1.0, nullptr, u, nullptr, (cudaStream_t)stream);
+}
+
+kfbi_status kfbi_plan_set_geometry(kfbi_plan *p, const kfbi_geometry *g) {
+  KFBI_TRY(check_plan(p));
+  if (!g) return fail(KFBI_E_CONFIG, "null geometry");
+  if (g->n_ctl < 8) return fail(KFBI_E_CONFIG, "control point count must be >= 8");
+  const int m = p->m;
+  p->n_ctl = g->n_ctl;
+  p->n_edges = g->n_edges;
+  p->n_rec = g->n_rec;
+  p->n_groups = g->n_groups;
+  p->w_ld = (g->n_ctl + 1) & ~1;
+  const int n = g->n_ctl;
+  std::vector<double> wpad((size_t)g->n_edges * p->w_ld, 0.0);
+  for (int e = 0; e < g->n_edges; ++e)
+    std::memcpy(&wpad[(size_t)e * p->w_ld], g->w_edges + (size_t)e * n, n * sizeof(double));
+  cudaError_t e = cudaSuccess;
+#define UP(buf, ptr, cnt) \
+  if (e == cudaSuccess) e = upload(p->buf, ptr, (size_t)(cnt))
+  UP(W, wpad.data(), wpad.size());
+  UP(edge_axis, reinterpret_cast<const signed char *>(g->edge_axis), g->n_edges);
+  UP(rec_edge, g->rec_edge, g->n_rec);
+  UP(rec_d, g->rec_d, g->n_rec);
+  UP(rec_sigma, g->rec_sigma, g->n_rec);
+  UP(group_start, g->group_start, g->n_groups + 1);
+  UP(group_node, g->group_node, g->n_groups);
+  UP(row_group, g->row_group, m + 2);
+  UP(deriv_col, g->deriv_col, n);
+  UP(speed, g->speed, n);
+  UP(tangent, g->tangent, 2 * n);
+  UP(normal, g->normal, 2 * n);
+  UP(dtan_ds, g->dtan_ds, 2 * n);
+  UP(inv3, g->inv3, 9 * n);
+  UP(stencil, g->stencil, 6 * n);
+  UP(ainv_rows, g->ainv_rows, 18 * n);
+  UP(jcoef, g->jcoef, 36 * n);
+#undef UP
+  if (e == cudaSuccess) e = p->d1.ensure(n);
+  if (e == cudaSuccess) e = p->psi_s.ensure(n);
+  if (e == cudaSuccess) e = p->jm.ensure(6 * (size_t)n);
+  if (e == cudaSuccess) e = p->jv.ensure(3 * (size_t)(g->n_edges > 0 ? g->n_edges : 1));
+  if (e != cudaSuccess) return fail(KFBI_E_CUDA, std::string("geometry upload: ") + cudaGetErrorString(e));
+  p->has_geo = true;
+  return KFBI_OK;
+}
+
+kfbi_status kfbi_jumps(kfbi_plan *p, int32_t dtype, double kre, double kim, const void *phi,
+                       const void *psi, const void *fg, double fg_sign, void *jm, void *stream) {
+  KFBI_TRY(check_geo(p));
+  cudaStream_t s = (cudaStream_t)stream;
+  if (dtype == KFBI_C128) return jumps_T<double2>(p, kre, kim, phi, psi, fg, fg_sign, jm, nullptr, s);
+  if (kim != 0.0) return fail(KFBI_E_CONFIG, "complex kappa requires the c128 path");
+  return jumps_T<double>(p, kre, kim, phi, psi, fg, fg_sign, jm, nullptr, s);
+}
+
+kfbi_status kfbi_corrections(kfbi_plan *p, int32_t dtype, const void *jm, void *c, void *stream) {
+  KFBI_TRY(check_geo(p));
+  cudaStream_t s = (cudaStream_t)stream;
+  const bool cplx = dtype == KFBI_C128;
+  if (cplx) KFBI_TRY(edges_T<double2>(p, jm, p->jv.p, nullptr, s));
+  else KFBI_TRY(edges_T<double>(p, jm, p->jv.p, nullptr, s));
+  // scatter group sums into a zeroed full grid
+  const size_t es = cplx ? sizeof(double2) : sizeof(double);
+  KFBI_CUDA(cudaMemsetAsync(c, 0, (size_t)(p->m + 1) * (p->m + 1) * es, s), "jumps-and-corrections");
+  if (p->n_groups == 0) return KFBI_OK;
+  const int blocks = (p->n_groups + 255) / 256;
+  if (cplx) {
+    CorrArgs<double2> ca = corr_args<double2>(p, reinterpret_cast<const double2 *>(p->jv.p));
+    return launch(p, KFBI_K_JUMPS, s, [&] {
+      scatter_groups_kernel<double2><<<blocks, 256, 0, s>>>(ca, p->n_groups, static_cast<double2 *>(c));
+    });
+  }
+  CorrArgs<double> ca = corr_args<double>(p, reinterpret_cast<const double *>(p->jv.p));
+  return launch(p, KFBI_K_JUMPS, s, [&] {
+    scatter_groups_kernel<double><<<blocks, 256, 0, s>>>(ca, p->n_groups, static_cast<double *>(c));
+  });
+}
+
+kfbi_status kfbi_interface_solve(kfbi_plan *p, int32_t dtype, double kre, double kim, const void *F,
+                                 const void *jm, void *u, void *stream) {
+  KFBI_TRY(check_geo(p));
+  cudaStream_t s = (cudaStream_t)stream;
+  if (dtype == KFBI_C128) KFBI_TRY(edges_T<double2>(p, jm, p->jv.p, nullptr, s));
+  else KFBI_TRY(edges_T<double>(p, jm, p->jv.p, nullptr, s));
+  return box_dispatch(p, dtype, kre, kim, F, 1.0, p->jv.p, u, nullptr, s);
+}
+
+kfbi_status kfbi_extract(kfbi_plan *p, int32_t dtype, const void *u, const void *jm, void *out,
+                         void *stream) {
+  KFBI_TRY(check_geo(p));
+  cudaStream_t s = (cudaStream_t)stream;
+  ExtractArgs x = extract_args(p);
+  const int blocks = (p->n_ctl + 255) / 256;
+  if (dtype == KFBI_C128)
+    return launch(p, KFBI_K_EXTRACT, s, [&] {
+      extract_kernel<double2><<<blocks, 256, 0, s>>>(x, static_cast<const double2 *>(u),
+                                                     static_cast<const double2 *>(jm),
+                                                     static_cast<double2 *>(out));
+    });
+  return launch(p, KFBI_K_EXTRACT, s, [&] {
+    extract_kernel<double><<<blocks, 256, 0, s>>>(x, static_cast<const double *>(u),
+                                                  static_cast<const double *>(jm),
+                                                  static_cast<double *>(out));
+  });
+}
+
+kfbi_status kfbi_richardson(kfbi_plan *p, const kfbi_bvp *b, kfbi_bvp_result *res, void *stream) {
+  KFBI_TRY(check_geo(p));
+  if (!b || !res) return fail(KFBI_E_CONFIG, "null argument");
+  if (b->max_iter < 1) return fail(KFBI_E_CONFIG, "max iterations must be >= 1");
+  if (!(b->gamma > 0.0 && b->gamma < 1.0)) return fail(KFBI_E_CONFIG, "gamma must lie in (0,1)");
+  if (!(b->tol > 0.0)) return fail(KFBI_E_CONFIG, "tolerance must be positive");
+  cudaStream_t s = (cudaStream_t)stream;
+  const bool cplx = b->dtype == KFBI_C128;
+  if (!cplx && b->kappa_im != 0.0) return fail(KFBI_E_CONFIG, "complex kappa requires the c128 path");
+  cudaError_t e = p->history.ensure(b->max_iter);
+  if (e != cudaSuccess) return fail(KFBI_E_CUDA, "history allocation failed");
+  KFBI_TRY(launch(p, KFBI_K_DENSITY, s, [&] { rich_init_kernel<<<1, 1, 0, s>>>(p->st.p, b->max_iter, b->tol); }));
+  int enqueued = 0;
+  int batch = b->sweeps_hint > 0 ? b->sweeps_hint : 4;
+  for (;;) {
+    int nb = batch;
+    if (nb > b->max_iter - enqueued) nb = b->max_iter - enqueued;
+    for (int k = 0; k < nb; ++k) {
+      if (cplx) KFBI_TRY(sweep<double2>(p, b, s));
+      else KFBI_TRY(sweep<double>(p, b, s));
+    }
+    enqueued += nb;
+    KFBI_CUDA(cudaMemcpyAsync(p->st_host, p->st.p, sizeof(RichState), cudaMemcpyDeviceToHost, s),
+              "density-update");
+    KFBI_CUDA(cudaStreamSynchronize(s), "density-update");
+    if (p->st_host->done != 0 || enqueued >= b->max_iter) break;
+    batch = 2;
+  }
+  const RichState &h = *p->st_host;
+  res->iterations = h.iters;
+  res->converged = h.done == 1;
+  res->residual = h.last_res;
+  if (res->history && h.iters > 0)
+    KFBI_CUDA(cudaMemcpy(res->history, p->history.p, sizeof(double) * h.iters, cudaMemcpyDeviceToHost),
+              "density-update");
+  if (h.done != 1) {
+    char msg[256];
+    std::snprintf(msg, sizeof msg,
+                  "Richardson iteration did not reach tol=%g within %d sweeps (last density update %.3e)",
+                  b->tol, b->max_iter, h.last_res);
+    return fail(KFBI_E_NOCONV, msg);
+  }
+  return KFBI_OK;
+}
+
+kfbi_status kfbi_heat_rhs(kfbi_plan *p, int64_t n, const uint8_t *mask, void *u, const void *F_old,
+                          void *F_new, double a, double *norm_out, void *stream) {
+  KFBI_TRY(check_plan(p));
+  cudaStream_t s = (cudaStream_t)stream;
+  KFBI_CUDA(cudaMemsetAsync(p->red.p, 0, sizeof(unsigned long long), s), "rhs-update");
+  KFBI_TRY(launch(p, KFBI_K_RHS, s, [&] {
+    heat_rhs_kernel<<<elem_blocks(n), 256, 0, s>>>(n, mask, static_cast<double *>(u),
+                                                   static_cast<const double *>(F_old),
+                                                   static_cast<double *>(F_new), a, p->red.p);
+  }));
+  return norm_out ? read_norm(p, s, norm_out) : KFBI_OK;
+}
+
+kfbi_status kfbi_wave_rhs(kfbi_plan *p, int64_t n, const uint8_t *mask, void *u_next,
+                          const void *u_curr, const void *F_curr, const void *F_prev, void *F_new,
+                          double kw, double coef, double *norm_out, void *stream) {
+  KFBI_TRY(check_plan(p));
+  cudaStream_t s = (cudaStream_t)stream;
+  KFBI_CUDA(cudaMemsetAsync(p->red.p, 0, sizeof(unsigned long long), s), "rhs-update");
+  KFBI_TRY(launch(p, KFBI_K_RHS, s, [&] {
+    wave_rhs_kernel<<<elem_blocks(n), 256, 0, s>>>(
+        n, mask, static_cast<double *>(u_next), static_cast<const double *>(u_curr),
+        static_cast<const double *>(F_curr), static_cast<const double *>(F_prev),
+        static_cast<double *>(F_new), kw, coef, p->red.p);
+  }));
+  return norm_out ? read_norm(p, s, norm_out) : KFBI_OK;
+}
+
+kfbi_status kfbi_schr_ustar(kfbi_plan *p, int64_t n, int32_t mode, const void *u, const void *other,
+                            double tau, void *out, void *stream) {
+  KFBI_TRY(check_plan(p));
+  cudaStream_t s = (cudaStream_t)stream;
+  return launch(p, KFBI_K_RHS, s, [&] {
+    schr_ustar_kernel<<<elem_blocks(n), 256, 0, s>>>(n, mode, static_cast<const double2 *>(u),
+                                                     static_cast<const double2 *>(other), tau,
+                                                     static_cast<double2 *>(out));
+  });
+}
+
+kfbi_status kfbi_nonlinear_phase(kfbi_plan *p, int64_t n, const void *ustar, const double *v,
+                                 double w, double half_tau, const uint8_t *mask, void *out,
+                                 double kre, double kim, void *F, double *max_res, void *stream) {
+  KFBI_TRY(check_plan(p));
+  cudaStream_t s = (cudaStream_t)stream;
+  KFBI_CUDA(cudaMemsetAsync(p->red.p, 0, sizeof(unsigned long long), s), "rhs-update");
+  KFBI_TRY(launch(p, KFBI_K_RHS, s, [&] {
+    nonlinear_phase_kernel<<<elem_blocks(n), 256, 0, s>>>(
+        n, static_cast<const double2 *>(ustar), v, w, half_tau, mask, static_cast<double2 *>(out),
+        kre, kim, static_cast<double2 *>(F), p->red.p);
+  }));
+  double r = 0.0;
+  KFBI_TRY(read_norm(p, s, &r));
+  if (max_res) *max_res = r;
+  if (r > NEWTON_TOL || r != r) {
+    char msg[160];
+    std::snprintf(msg, sizeof msg, "pointwise Newton solve stalled at residual %.3e", r);
+    return fail(KFBI_E_NOCONV, msg);
+  }
+  return KFBI_OK;
+}
+
+kfbi_status kfbi_mask_norm(kfbi_plan *p, int32_t dtype, int64_t n, const uint8_t *mask, void *u,
+                           double *norm_out, void *stream) {
+  KFBI_TRY(check_plan(p));
+  cudaStream_t s = (cudaStream_t)stream;
+  KFBI_CUDA(cudaMemsetAsync(p->red.p, 0, sizeof(unsigned long long), s), "rhs-update");
+  if (dtype == KFBI_C128)
+    KFBI_TRY(launch(p, KFBI_K_RHS, s, [&] {
+      mask_norm_kernel<double2><<<elem_blocks(n), 256, 0, s>>>(n, mask, static_cast<double2 *>(u), p->red.p);
+    }));
+  else
+    KFBI_TRY(launch(p, KFBI_K_RHS, s, [&] {
+      mask_norm_kernel<double><<<elem_blocks(n), 256, 0, s>>>(n, mask, static_cast<double *>(u), p->red.p);
+    }));
+  return norm_out ? read_norm(p, s, norm_out) : KFBI_OK;
+}
+
+kfbi_status kfbi_kernel_times(kfbi_plan *p, double *ms, int64_t *calls) {
+  KFBI_TRY(check_plan(p));
+  for (auto &pe : p->pending) {
+    cudaEventSynchronize(pe.b);
+    float t = 0.f;
+    if (cudaEventElapsedTime(&t, pe.a, pe.b) == cudaSuccess) p->ms[pe.name] += t;
+    p->pool.push_back(pe.a);
+    p->pool.push_back(pe.b);
+  }
+  p->pending.clear();
+  for (int i = 0; i < KFBI_N_KERNEL_NAMES; ++i) {
+    if (ms) ms[i] = p->ms[i];
+    if (calls) calls[i] = p->calls[i];
+  }
+  return KFBI_OK;
+}
+
+kfbi_status kfbi_reset_kernel_times(kfbi_plan *p) {
+  KFBI_TRY(kfbi_kernel_times(p, nullptr, nullptr));
+  for (int i = 0; i < KFBI_N_KERNEL_NAMES; ++i) {
+    p->ms[i] = 0.0;
+    p->calls[i] = 0;
+  }
+  p->launches = 0;
+  return KFBI_OK;
+}
+
+kfbi_status kfbi_set_timing(kfbi_plan *p, int32_t enabled) {
+  KFBI_TRY(check_plan(p));
+  if (!enabled) KFBI_TRY(kfbi_kernel_times(p, nullptr, nullptr));
+  p->timing = enabled != 0;
+  return KFBI_OK;
+}
+
+int64_t kfbi_launch_count(kfbi_plan *p) { return p ? p->launches : 0; }
+
+}  // extern "C"

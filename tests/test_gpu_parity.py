@@ -1,0 +1,243 @@
+"""Device parity: every hot-path kernel, called through the C ABI, against the
+oracle / the reference's golden vectors on the same inputs.
+
+Bar (north_star): 1e-10 relative L-inf in fp64 / complex128, identical
+Richardson iteration counts.  Measured sensitivity of the reference itself
+to a different (equally exact) DST is ~1e-14.
+"""
+
+import numpy as np
+import pytest
+
+import paper_2404_14864_b200 as k
+from conftest import (BOX, BOX_CASES, PI_BOX, box_rhs, golden, oracle_spec, rel_linf, run_cases,
+                      setup_cases)
+from oracle import kfbi_oracle as O
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-10
+
+
+def _loaded_native():
+    from paper_2404_14864_b200 import _native
+
+    assert _native._lib is not None, "the CUDA extension must be the code path"
+
+
+@pytest.mark.parametrize("case", [c for c in BOX_CASES if c[3] == "dirichlet-zero"],
+                         ids=lambda c: c[0])
+def test_box_solve_vs_reference(case):
+    tag, m, kappa, bc, seed, cplx = case
+    grid = k.CartesianGrid(BOX, m)
+    u = k.BoxSolver(grid, kappa, bc).solve(box_rhs(m, seed, cplx))
+    ref = golden("box")[tag + "__u"]
+    assert u.dtype == ref.dtype
+    assert rel_linf(u, ref) < 1e-13
+    assert np.all(u[0] == 0) and np.all(u[-1] == 0) and np.all(u[:, 0] == 0) and np.all(u[:, -1] == 0)
+    _loaded_native()
+
+
+@pytest.mark.parametrize("bc", ["dirichlet-zero"])
+@pytest.mark.parametrize("kappa", [0.0, 3.7, 40.0 + 0.0j, 2.0j])
+def test_random_rhs_residuals(bc, kappa):
+    # boxsolve residual oracle of the reference (test_boxsolve.py:29-43)
+    rng = np.random.default_rng(int(abs(kappa) * 100))
+    for m in (16, 32):
+        grid = k.CartesianGrid(BOX, m)
+        solver = k.BoxSolver(grid, kappa, bc)
+        for _ in range(10):
+            rhs = rng.standard_normal((m + 1, m + 1))
+            if np.iscomplexobj(np.asarray(kappa)):
+                rhs = rhs + 1j * rng.standard_normal((m + 1, m + 1))
+            u = solver.solve(rhs)
+            r = (k.apply_box_operator(grid, u, kappa, bc) - rhs)[1:-1, 1:-1]
+            assert np.max(np.abs(r)) / np.max(np.abs(rhs[1:-1, 1:-1])) < 1e-11
+
+
+@pytest.mark.parametrize("m", [16, 64, 256, 1024, 4096])
+def test_discrete_eigenfunctions(m):
+    grid = k.CartesianGrid(BOX, m)
+    xi = (grid.X - grid.box[0]) / 3.0
+    eta = (grid.Y - grid.box[2]) / 3.0
+    kappa = 5.0
+    for p, q in ((1, 1), (3, 2), (7, 12), (m // 2 - 1, 5), (m - 1, m - 1)):
+        lam = ((2 * np.cos(p * np.pi / m) - 2) + (2 * np.cos(q * np.pi / m) - 2)) / grid.h**2
+        ue = np.sin(p * np.pi * xi) * np.sin(q * np.pi * eta)
+        u = k.BoxSolver(grid, kappa, "dirichlet-zero").solve((lam - kappa) * ue)
+        assert np.max(np.abs(u - ue)) < 1e-11 * max(1.0, np.log2(m))
+
+
+@pytest.mark.parametrize("m", [512, 2048])
+def test_box_solve_large_vs_oracle(m):
+    grid = k.CartesianGrid(BOX, m)
+    rhs = box_rhs(m, 3 + m, False)
+    for kappa in (2048.0, 0.5):
+        u = k.BoxSolver(grid, kappa, "dirichlet-zero").solve(rhs)
+        assert rel_linf(u, O.box_solve(m, grid.h, kappa, rhs)) < 1e-12
+    rhs_c = box_rhs(m, 5 + m, True)
+    u = k.BoxSolver(grid, 2j * m, "dirichlet-zero").solve(rhs_c)
+    assert rel_linf(u, O.box_solve(m, grid.h, 2j * m, rhs_c)) < 1e-12
+
+
+def test_box_solve_linearity_4096():
+    import torch
+
+    m = 4096
+    grid = k.CartesianGrid(BOX, m)
+    dev = torch.device("cuda")
+    g = torch.Generator(device=dev).manual_seed(0)
+    a = torch.randn((m + 1, m + 1), generator=g, device=dev, dtype=torch.float64)
+    b = torch.randn((m + 1, m + 1), generator=g, device=dev, dtype=torch.float64)
+    s = k.BoxSolver(grid, 512.0, "dirichlet-zero")
+    ua, ub, uab = s.solve(a), s.solve(b), s.solve(2.0 * a + b)
+    err = torch.max(torch.abs(uab - (2.0 * ua + ub))) / torch.max(torch.abs(uab))
+    assert float(err) < 1e-13
+    # solving the operator applied to a solution returns the solution
+    u = ua.cpu().numpy()
+    rhs = k.apply_box_operator(grid, u, 512.0, "dirichlet-zero")
+    u2 = s.solve(rhs)
+    assert rel_linf(u2, u) < 1e-9
+
+
+@pytest.mark.parametrize("name", ["disc32", "star64", "flower128", "ellipse128"])
+def test_interface_kernels_vs_reference(name):
+    box, m, curve = setup_cases()[name]
+    ws = k.InterfaceWorkspace(k.build_grid(box, m, curve))
+    g = golden("interface")
+    pf = k.PiecewiseField(kappa=2.0)
+    cps = ws.cps
+    X, Y = ws.grid.X, ws.grid.Y
+    interior = ws.geometry.classification.interior
+    data = k.InterfaceData(kappa=2.0, F=np.where(interior, pf.f_jump(X, Y), 0.0),
+                           phi=pf.phi(cps.x, cps.y), psi=pf.psi(cps.x, cps.y, cps.normal),
+                           f_gamma=pf.f_jump(cps.x, cps.y))
+    js = k.compute_jumps(data, ws)
+    assert rel_linf(js.as_matrix(), g[name + "__jumps"]) < 1e-12
+    c = k.corrections(js, ws)
+    assert rel_linf(c, g[name + "__corr"]) < 1e-12
+    assert np.all(c[~ws.geometry.classification.irregular] == 0.0)
+    u = k.solve_interface(data, ws, box_bc="dirichlet-zero")
+    assert rel_linf(u, g[name + "__u"]) < TOL
+    tr = np.stack(k.TraceExtractor(ws).extract(g[name + "__u"], js))
+    assert rel_linf(tr, g[name + "__trace"]) < 1e-12
+    rng = np.random.default_rng(55)
+    phi_c = rng.standard_normal(cps.m) + 1j * rng.standard_normal(cps.m)
+    fg_c = rng.standard_normal(cps.m) + 1j * rng.standard_normal(cps.m)
+    data_c = k.InterfaceData(kappa=64j, F=np.zeros((m + 1, m + 1), complex), phi=phi_c,
+                             psi=np.zeros(cps.m, complex), f_gamma=fg_c)
+    js_c = k.compute_jumps(data_c, ws)
+    assert rel_linf(js_c.as_matrix(), g[name + "__jumps_c"]) < 1e-12
+    assert rel_linf(k.corrections(js_c, ws), g[name + "__corr_c"]) < 1e-12
+
+
+def test_corrections_linearity():
+    # test_interface.py:100-127 of the reference
+    geo = k.build_grid(BOX, 64, k.StarCurve(1.0, c=0.2, lobes=3))
+    ws = k.InterfaceWorkspace(geo)
+    m = ws.cps.m
+    rng = np.random.default_rng(23)
+
+    def corr_of(phi, psi, fg):
+        return k.corrections(k.compute_jumps(k.InterfaceData(3.0, np.zeros_like(geo.grid.X), phi,
+                                                             psi, fg), ws), ws)
+
+    assert np.all(corr_of(np.zeros(m), np.zeros(m), np.zeros(m)) == 0.0)
+    phi, psi, fg = rng.standard_normal((3, m))
+    c1 = corr_of(phi, psi, fg)
+    assert np.array_equal(corr_of(2 * phi, 2 * psi, 2 * fg), 2.0 * c1)
+
+
+def test_richardson_vs_reference():
+    g = golden("richardson")
+    cases = {
+        "disc64_k16": (BOX, 64, k.CircleCurve(1.0), 16.0),
+        "flower128_k200": (BOX, 128, k.StarCurve(1.0, c=0.2, lobes=8), 200.0),
+        "pistar64_kc": (PI_BOX, 64, k.StarCurve(1.5, c=0.2, lobes=3), 16j),
+    }
+    for name, (box, m, curve, kappa) in cases.items():
+        ws = k.InterfaceWorkspace(k.build_grid(box, m, curve))
+        sol = k.StaticPlaneWave(kappa=abs(kappa))
+        interior = ws.geometry.classification.interior
+        X, Y, cps = ws.grid.X, ws.grid.Y, ws.cps
+        F = np.where(interior, -(1.0 + kappa) * sol.u(X, Y), 0.0)
+        fg = -(1.0 + kappa) * sol.u(cps.x, cps.y)
+        prob = k.BvpProblem(kappa=kappa, F=F, f_gamma=fg, bc_kind="dirichlet",
+                            bc_values=sol.dirichlet(cps.x, cps.y))
+        s = k.richardson_solve(prob, ws)
+        p = name + "__"
+        assert s.iterations == int(g[p + "iterations"]), name
+        assert len(s.residual_history) == s.iterations
+        assert rel_linf(s.residual_history, g[p + "history"]) < 1e-6
+        assert rel_linf(s.u, g[p + "u"]) < TOL
+        assert rel_linf(s.density, g[p + "density"]) < TOL
+        assert rel_linf(s.trace_u, g[p + "trace_u"]) < TOL
+        # warm start finishes almost immediately (test_bvp.py:142-147)
+        prob2 = k.BvpProblem(kappa=kappa, F=F, f_gamma=fg, bc_kind="dirichlet",
+                             bc_values=prob.bc_values, initial_density=s.density.copy())
+        assert k.richardson_solve(prob2, ws).iterations <= 3
+
+
+def test_convergence_error_fields():
+    geo = k.build_grid(BOX, 32, k.CircleCurve(1.0))
+    ws = k.InterfaceWorkspace(geo)
+    sol = k.StaticPlaneWave(kappa=16.0)
+    cps = ws.cps
+    F = np.where(geo.classification.interior, sol.f(geo.grid.X, geo.grid.Y), 0.0)
+    prob = k.BvpProblem(kappa=16.0, F=F, f_gamma=sol.f(cps.x, cps.y), bc_kind="dirichlet",
+                        bc_values=sol.dirichlet(cps.x, cps.y), max_iter=3)
+    with pytest.raises(k.ConvergenceError) as ei:
+        k.richardson_solve(prob, ws)
+    assert ei.value.iterations == 3 and ei.value.last_residual > 0.0
+
+
+@pytest.mark.parametrize("name", list(run_cases()))
+def test_full_runs_vs_reference(name):
+    box, m, curve, kw = run_cases()[name]
+    geo = k.build_grid(box, m, curve)
+    res = k.run(k.ProblemSpec(**kw), geo)
+    g = golden("runs")
+    assert res.iterations == list(g[name + "__iterations"])
+    assert rel_linf(res.state.u, g[name + "__u"]) < TOL
+    assert res.state.u.shape == (m + 1, m + 1)
+    assert res.kernel_calls["transform-cols"] >= sum(res.iterations)
+    assert res.kernel_times["transform-rows"] > 0.0
+
+
+def test_nonlinear_phase_vs_reference():
+    g = golden("nonlinear")
+    assert rel_linf(k.nonlinear_phase_step(g["u"], g["v"], 1.0, 0.0625), g["out"]) < 1e-13
+    assert rel_linf(k.nonlinear_phase_step(g["u"], g["v"], 3.0, 0.25), g["out_w3"]) < 1e-13
+
+
+def test_instability_detected():
+    heat = k.HeatPlaneDecay()
+    geo = k.build_grid(BOX, 64, k.StarCurve(1.0, c=0.2, lobes=5))
+    spec = k.ProblemSpec(equation="heat", bc_kind="dirichlet", g=heat.dirichlet, u0=heat.u0,
+                         lap_u0=heat.lap_u0, tau=0.25, t_final=0.5, blowup_threshold=0.5)
+    with pytest.raises(k.InstabilityError):
+        k.run(spec, geo)
+
+
+@pytest.mark.parametrize("eq", ["heat", "wave", "schrodinger"])
+def test_runs_1024_vs_oracle_window(eq):
+    """Configs C2/C3-shaped problems at 1024^2 over a short window."""
+    heat, wave, schr = k.HeatPlaneDecay(), k.WaveStanding(), k.SchrodingerPhaseRotation()
+    m = 1024
+    if eq == "heat":
+        box, curve = BOX, k.StarCurve(1.0, c=0.2, lobes=8)
+        kw = dict(equation="heat", bc_kind="dirichlet", g=heat.dirichlet, u0=heat.u0,
+                  lap_u0=heat.lap_u0, tau=1 / 256, t_final=3 / 256)
+    elif eq == "wave":
+        box, curve = BOX, k.EllipseCurve(1.2, 0.8)
+        kw = dict(equation="wave", bc_kind="dirichlet", g=wave.dirichlet, u0=wave.u0,
+                  lap_u0=wave.lap_u0, v0=wave.v0, lap_v0=wave.lap_v0, tau=1 / 64, t_final=3 / 64)
+    else:
+        box, curve = PI_BOX, k.StarCurve(1.5, c=0.2, lobes=3)
+        kw = dict(equation="schrodinger", bc_kind="dirichlet", g=schr.dirichlet, u0=schr.u0,
+                  lap_u0=schr.lap_u0, potential=schr.potential, tau=1 / 128, t_final=2 / 128)
+    geo = k.build_grid(box, m, curve)
+    ctx = k.StepContext(geo)
+    res = k.run(k.ProblemSpec(**kw), geo, context=ctx)
+    st = O.run(O.tables_from_workspace(ctx.workspace), oracle_spec(kw))
+    assert res.iterations == st.iterations
+    assert rel_linf(res.state.u, st.u) < TOL
