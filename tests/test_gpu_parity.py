@@ -63,8 +63,17 @@ def test_discrete_eigenfunctions(m):
     for p, q in ((1, 1), (3, 2), (7, 12), (m // 2 - 1, 5), (m - 1, m - 1)):
         lam = ((2 * np.cos(p * np.pi / m) - 2) + (2 * np.cos(q * np.pi / m) - 2)) / grid.h**2
         ue = np.sin(p * np.pi * xi) * np.sin(q * np.pi * eta)
-        u = k.BoxSolver(grid, kappa, "dirichlet-zero").solve((lam - kappa) * ue)
-        assert np.max(np.abs(u - ue)) < 1e-11 * max(1.0, np.log2(m))
+        rhs = (lam - kappa) * ue
+        u = k.BoxSolver(grid, kappa, "dirichlet-zero").solve(rhs)
+        if max(p, q) <= 12:
+            assert np.max(np.abs(u - ue)) < 1e-13
+        else:
+            # high modes: sin(p pi xi) with rounded grid coordinates limits the
+            # analytic comparison (scipy itself is off by 1.8e-10 at M=1024,
+            # p=511); compare with the reference transform instead
+            ref = O.box_solve(m, grid.h, kappa, rhs)
+            assert np.max(np.abs(u - ref)) < 1e-12
+            assert np.max(np.abs(u - ue)) < 2.0 * np.max(np.abs(ref - ue)) + 1e-13
 
 
 @pytest.mark.parametrize("m", [512, 2048])

@@ -1,0 +1,23 @@
+#!/bin/bash
+# One gpurun session: smoke, GPU tests, bench, ncu launch list + one full capture.
+# Usage (from the repo root, on the GPU box): bash tools/gpu_round.sh [tag]
+TAG=${1:-r1}
+OUT=gpurun_out
+mkdir -p $OUT
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,driver_version --format=csv > $OUT/gpu_$TAG.txt
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke_$TAG.log 2>&1; echo "rc=$?" >> $OUT/smoke_$TAG.log
+if [ "${SKIP_TESTS:-0}" != "1" ]; then
+  timeout 900 python -m pytest tests -m gpu -q -p no:cacheprovider -x > $OUT/pytest_gpu_$TAG.log 2>&1; echo "rc=$?" >> $OUT/pytest_gpu_$TAG.log
+fi
+timeout 900 python bench.py ${BENCH_ARGS:-} > $OUT/bench_$TAG.log 2>&1; echo "rc=$?" >> $OUT/bench_$TAG.log
+if [ "${SKIP_NCU:-0}" != "1" ]; then
+  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+    --log-file $OUT/launches_$TAG.csv python bench.py --steps 1 --warmup 3 --no-cpu-baseline > $OUT/ncu_launch_bench_$TAG.log 2>&1
+  echo "rc=$?" >> $OUT/ncu_launch_bench_$TAG.log
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:cols_kernel -s 20 -c 2 \
+    -o $OUT/prof_cols_$TAG -f python bench.py --steps 1 --warmup 3 --no-cpu-baseline --equations heat > $OUT/ncu_full_$TAG.log 2>&1
+  echo "rc=$?" >> $OUT/ncu_full_$TAG.log
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"rows_fwd|rows_inv|corr_edges" -s 60 -c 6 \
+    -o $OUT/prof_rows_$TAG -f python bench.py --steps 1 --warmup 3 --no-cpu-baseline --equations heat > $OUT/ncu_full2_$TAG.log 2>&1
+  echo "rc=$?" >> $OUT/ncu_full2_$TAG.log
+fi
