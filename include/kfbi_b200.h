@@ -112,6 +112,7 @@ typedef struct {
   void *u;                /* out (M+1)^2 field of the final sweep         */
   void *trace_u;          /* out [n_ctl]                                  */
   void *trace_un;         /* out [n_ctl]                                  */
+  int32_t use_operator;   /* 1: sweeps >= 2 use the plan's trace operator */
 } kfbi_bvp;
 
 typedef struct {
@@ -160,6 +161,18 @@ kfbi_status kfbi_extract(kfbi_plan *plan, int32_t dtype, const void *u,
  * batch of sweeps; history copied to result->history. */
 kfbi_status kfbi_richardson(kfbi_plan *plan, const kfbi_bvp *bvp,
                             kfbi_bvp_result *result, void *stream);
+
+/* Build the trace operator T (n_ctl x n_ctl, row-major) of the plan's
+ * geometry for one kappa: column p is the sweep pipeline (jumps ->
+ * corrections -> box solve -> extraction) applied to the unit density e_p
+ * with F = 0, f_gamma = 0.  With kfbi_bvp.use_operator = 1, Richardson
+ * sweeps k >= 2 evaluate trace_k = trace_1 + T (phi_k - phi_0): the same
+ * affine map as the pipeline (bvp.py:313-323), identical iterates up to
+ * rounding; sweep 1 and the returned field still run the full pipeline.
+ * Costs n_ctl pipeline evaluations once per (geometry, kappa). */
+kfbi_status kfbi_build_trace_operator(kfbi_plan *plan, int32_t dtype,
+                                      double kappa_re, double kappa_im,
+                                      void *stream);
 
 /* Time-stepping right-hand sides (timestepping.py), element-wise over n
  * values: the (M+1)^2 grid with the uint8 interior mask, or the n_ctl control

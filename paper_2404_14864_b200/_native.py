@@ -58,7 +58,7 @@ class Bvp(C.Structure):
         ("F", vp), ("F_sign", f64), ("f_gamma", vp), ("f_gamma_sign", f64),
         ("g", vp), ("density", vp), ("gamma", f64), ("tol", f64),
         ("max_iter", i32), ("sweeps_hint", i32),
-        ("u", vp), ("trace_u", vp), ("trace_un", vp),
+        ("u", vp), ("trace_u", vp), ("trace_un", vp), ("use_operator", i32),
     ]
 
 
@@ -79,6 +79,7 @@ _SIGNATURES = {
     "kfbi_interface_solve": ([vp, i32, f64, f64, vp, vp, vp, vp], i32),
     "kfbi_extract": ([vp, i32, vp, vp, vp, vp], i32),
     "kfbi_richardson": ([vp, C.POINTER(Bvp), C.POINTER(BvpResult), vp], i32),
+    "kfbi_build_trace_operator": ([vp, i32, f64, f64, vp], i32),
     "kfbi_heat_rhs": ([vp, i64, vp, vp, vp, vp, f64, C.POINTER(f64), vp], i32),
     "kfbi_wave_rhs": ([vp, i64, vp, vp, vp, vp, vp, vp, f64, f64, C.POINTER(f64), vp], i32),
     "kfbi_schr_ustar": ([vp, i64, i32, vp, vp, f64, vp, vp], i32),

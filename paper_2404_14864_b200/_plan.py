@@ -126,15 +126,23 @@ class Plan:
         N.check(self._lib.kfbi_extract(self.handle, self._dt(out.is_complex()), u.data_ptr(),
                                        jm.data_ptr(), out.data_ptr(), self.stream))
 
+    def build_operator(self, kappa, cplx):
+        """Trace operator T of this geometry for one kappa (n_ctl pipeline
+        evaluations, once per (geometry, kappa))."""
+        k = complex(kappa)
+        N.check(self._lib.kfbi_build_trace_operator(self.handle, self._dt(cplx), k.real, k.imag,
+                                                    self.stream))
+        self.operator_key = (k, bool(cplx))
+
     def richardson(self, *, kappa, F, F_sign, f_gamma, f_gamma_sign, g, density, gamma, tol,
-                   max_iter, u, trace_u, trace_un, sweeps_hint=0):
+                   max_iter, u, trace_u, trace_un, sweeps_hint=0, use_operator=False):
         k = complex(kappa)
         b = N.Bvp(dtype=self._dt(u.is_complex()), kappa_re=k.real, kappa_im=k.imag,
                   F=F.data_ptr(), F_sign=float(F_sign), f_gamma=f_gamma.data_ptr(),
                   f_gamma_sign=float(f_gamma_sign), g=g.data_ptr(), density=density.data_ptr(),
                   gamma=float(gamma), tol=float(tol), max_iter=int(max_iter),
                   sweeps_hint=int(sweeps_hint), u=u.data_ptr(), trace_u=trace_u.data_ptr(),
-                  trace_un=trace_un.data_ptr())
+                  trace_un=trace_un.data_ptr(), use_operator=int(bool(use_operator)))
         hist = np.zeros(max(int(max_iter), 1))
         res = N.BvpResult(history=hist.ctypes.data_as(C.POINTER(C.c_double)))
         status = self._lib.kfbi_richardson(self.handle, C.byref(b), C.byref(res), self.stream)

@@ -92,7 +92,9 @@ rows_fwd_kernel(BoxArgs a, const void *__restrict__ rhs, double sign,
 
   for (int n = 1 + tid; n < M; n += NT) {
     double2 v;
-    if (CPLX) {
+    if (rhs == nullptr) {
+      v = make_double2(0.0, 0.0);
+    } else if (CPLX) {
       v = cscale(static_cast<const double2 *>(rhs)[(size_t)j0 * stride + n], sign);
     } else {
       const double *r = static_cast<const double *>(rhs);

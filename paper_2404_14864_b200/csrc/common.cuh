@@ -30,6 +30,7 @@ KFBI_DEV double2 rdiv(double2 a, double s) { return make_double2(a.x / s, a.y / 
 template <typename T> struct Sc;
 template <> struct Sc<double> {
   static KFBI_DEV double zero() { return 0.0; }
+  static KFBI_DEV double one() { return 1.0; }
   static KFBI_DEV double abs(double v) { return fabs(v); }
   static KFBI_DEV double add(double a, double b) { return a + b; }
   static KFBI_DEV double sub(double a, double b) { return a - b; }
@@ -40,6 +41,7 @@ template <> struct Sc<double> {
 };
 template <> struct Sc<double2> {
   static KFBI_DEV double2 zero() { return make_double2(0.0, 0.0); }
+  static KFBI_DEV double2 one() { return make_double2(1.0, 0.0); }
   static KFBI_DEV double abs(double2 v) { return hypot(v.x, v.y); }
   static KFBI_DEV double2 add(double2 a, double2 b) { return cadd(a, b); }
   static KFBI_DEV double2 sub(double2 a, double2 b) { return csub(a, b); }

@@ -95,6 +95,11 @@ struct kfbi_plan {
   DevBuf<double2> d1, psi_s, jm, jv;
   DevBuf<double> history;
   DevBuf<RichState> st;
+  // operator form (trace operator T of one kappa / dtype)
+  DevBuf<double2> Top, phi0, phi_prev, trace1, trace_tmp, zvec, evec, out3, ufield;
+  bool op_valid = false;
+  int op_dtype = -1;
+  double op_kre = 0.0, op_kim = 0.0;
   DevBuf<unsigned long long> red;   // reduction slots
   RichState *st_host = nullptr;     // pinned mirror
   unsigned long long *red_host = nullptr;
@@ -338,6 +343,99 @@ kfbi_status sweep(kfbi_plan *p, const kfbi_bvp *b, cudaStream_t s) {
   });
 }
 
+
+kfbi_status ensure_op_scratch(kfbi_plan *p) {
+  const size_t n = (size_t)p->n_ctl;
+  cudaError_t e = cudaSuccess;
+  DevBuf<double2> *bufs[] = {&p->phi0, &p->phi_prev, &p->trace1, &p->trace_tmp, &p->zvec, &p->evec};
+  for (auto *b : bufs)
+    if (e == cudaSuccess) e = b->ensure(n);
+  if (e == cudaSuccess) e = p->out3.ensure(3 * n);
+  if (e != cudaSuccess) return fail(KFBI_E_CUDA, std::string("operator scratch: ") + cudaGetErrorString(e));
+  return KFBI_OK;
+}
+
+// Column p of T = trace of the pipeline applied to e_p with F = 0, f_gamma = 0.
+template <typename T>
+kfbi_status build_operator_T(kfbi_plan *p, double kre, double kim, cudaStream_t s) {
+  constexpr bool CPLX = std::is_same<T, double2>::value;
+  const int n = p->n_ctl;
+  const size_t nf = (size_t)(p->m + 1) * (p->m + 1);
+  KFBI_TRY(ensure_op_scratch(p));
+  cudaError_t e = p->Top.ensure((size_t)n * n);
+  if (e == cudaSuccess) e = p->ufield.ensure(nf);
+  if (e != cudaSuccess) return fail(KFBI_E_CUDA, std::string("operator allocation: ") + cudaGetErrorString(e));
+  p->op_valid = false;
+  T *z = reinterpret_cast<T *>(p->zvec.p), *ev = reinterpret_cast<T *>(p->evec.p);
+  T *out = reinterpret_cast<T *>(p->out3.p), *Top = reinterpret_cast<T *>(p->Top.p);
+  KFBI_CUDA(cudaMemsetAsync(z, 0, n * sizeof(T), s), "jumps-and-corrections");
+  ExtractArgs x = extract_args(p);
+  const int eb = (n + 255) / 256;
+  const bool timing = p->timing;
+  p->timing = false;
+  kfbi_status st = KFBI_OK;
+  for (int col = 0; col < n && st == KFBI_OK; ++col) {
+    st = launch(p, KFBI_K_JUMPS, s, [&] { unit_vector_kernel<T><<<eb, 256, 0, s>>>(ev, n, col); });
+    if (st == KFBI_OK) st = jumps_T<T>(p, kre, kim, ev, nullptr, z, 1.0, p->jm.p, nullptr, s);
+    if (st == KFBI_OK) st = edges_T<T>(p, p->jm.p, p->jv.p, nullptr, s);
+    if (st == KFBI_OK) st = box_passes<CPLX>(p, kre, kim, nullptr, 1.0, p->jv.p, p->ufield.p, nullptr, s);
+    if (st == KFBI_OK)
+      st = launch(p, KFBI_K_EXTRACT, s, [&] {
+        extract_kernel<T><<<eb, 256, 0, s>>>(x, reinterpret_cast<const T *>(p->ufield.p),
+                                             reinterpret_cast<const T *>(p->jm.p), out);
+      });
+    if (st == KFBI_OK)
+      st = launch(p, KFBI_K_EXTRACT, s, [&] { op_column_kernel<T><<<eb, 256, 0, s>>>(n, col, out, Top); });
+  }
+  p->timing = timing;
+  KFBI_TRY(st);
+  KFBI_CUDA(cudaStreamSynchronize(s), "extract-traces");
+  p->op_valid = true;
+  p->op_dtype = CPLX ? KFBI_C128 : KFBI_F64;
+  p->op_kre = kre;
+  p->op_kim = kim;
+  return KFBI_OK;
+}
+
+// Operator sweeps k >= 2 (trace = trace_1 + T (phi - phi_0), then the update).
+template <typename T>
+kfbi_status op_sweep(kfbi_plan *p, const kfbi_bvp *b, cudaStream_t s) {
+  const int n = p->n_ctl;
+  const int *done = &p->st.p->done;
+  const int wb = (n * 32 + 255) / 256, eb = (n + 255) / 256;
+  T *trace = reinterpret_cast<T *>(p->trace_tmp.p);
+  KFBI_TRY(launch(p, KFBI_K_EXTRACT, s, [&] {
+    op_trace_kernel<T><<<wb, 256, 0, s>>>(n, reinterpret_cast<const T *>(p->Top.p),
+                                          static_cast<const T *>(b->density),
+                                          reinterpret_cast<const T *>(p->phi0.p),
+                                          reinterpret_cast<const T *>(p->trace1.p), trace, done);
+  }));
+  return launch(p, KFBI_K_DENSITY, s, [&] {
+    op_update_kernel<T><<<eb, 256, 0, s>>>(n, static_cast<const T *>(b->g), trace,
+                                           static_cast<T *>(b->density),
+                                           reinterpret_cast<T *>(p->phi_prev.p), b->gamma,
+                                           p->st.p, p->history.p);
+  });
+}
+
+// Full pipeline from the density before the converging update: the field and
+// traces the reference returns (bvp.py:319-323, 336-344).
+template <typename T>
+kfbi_status final_pipeline(kfbi_plan *p, const kfbi_bvp *b, cudaStream_t s) {
+  constexpr bool CPLX = std::is_same<T, double2>::value;
+  const int n = p->n_ctl;
+  KFBI_TRY(jumps_T<T>(p, b->kappa_re, b->kappa_im, p->phi_prev.p, nullptr, b->f_gamma,
+                      b->f_gamma_sign, p->jm.p, nullptr, s));
+  KFBI_TRY(edges_T<T>(p, p->jm.p, p->jv.p, nullptr, s));
+  KFBI_TRY(box_passes<CPLX>(p, b->kappa_re, b->kappa_im, b->F, b->F_sign, p->jv.p, b->u, nullptr, s));
+  ExtractArgs x = extract_args(p);
+  return launch(p, KFBI_K_EXTRACT, s, [&] {
+    extract_traces_kernel<T><<<(n + 255) / 256, 256, 0, s>>>(
+        x, static_cast<const T *>(b->u), reinterpret_cast<const T *>(p->jm.p),
+        static_cast<T *>(b->trace_u), static_cast<T *>(b->trace_un));
+  });
+}
+
 }  // namespace
 
 // ===========================================================================
@@ -410,6 +508,9 @@ kfbi_status kfbi_plan_destroy(kfbi_plan *p) {
   p->normal.release(); p->dtan_ds.release(); p->inv3.release(); p->ainv_rows.release();
   p->jcoef.release(); p->d1.release(); p->psi_s.release(); p->jm.release(); p->jv.release();
   p->history.release(); p->st.release(); p->red.release();
+  p->Top.release(); p->phi0.release(); p->phi_prev.release(); p->trace1.release();
+  p->trace_tmp.release(); p->zvec.release(); p->evec.release(); p->out3.release();
+  p->ufield.release();
   if (p->st_host) cudaFreeHost(p->st_host);
   if (p->red_host) cudaFreeHost(p->red_host);
   delete p;
@@ -464,6 +565,7 @@ kfbi_status kfbi_plan_set_geometry(kfbi_plan *p, const kfbi_geometry *g) {
   if (e == cudaSuccess) e = p->jv.ensure(3 * (size_t)(g->n_edges > 0 ? g->n_edges : 1));
   if (e != cudaSuccess) return fail(KFBI_E_CUDA, std::string("geometry upload: ") + cudaGetErrorString(e));
   p->has_geo = true;
+  p->op_valid = false;
   return KFBI_OK;
 }
 
@@ -538,22 +640,45 @@ kfbi_status kfbi_richardson(kfbi_plan *p, const kfbi_bvp *b, kfbi_bvp_result *re
   if (!cplx && b->kappa_im != 0.0) return fail(KFBI_E_CONFIG, "complex kappa requires the c128 path");
   cudaError_t e = p->history.ensure(b->max_iter);
   if (e != cudaSuccess) return fail(KFBI_E_CUDA, "history allocation failed");
+  const bool use_op = b->use_operator != 0;
+  const size_t es = cplx ? sizeof(double2) : sizeof(double);
+  if (use_op) {
+    if (!p->op_valid || p->op_dtype != b->dtype || p->op_kre != b->kappa_re || p->op_kim != b->kappa_im)
+      return fail(KFBI_E_CONFIG, "trace operator not built for this kappa / dtype (kfbi_build_trace_operator)");
+    KFBI_TRY(ensure_op_scratch(p));
+  }
   KFBI_TRY(launch(p, KFBI_K_DENSITY, s, [&] { rich_init_kernel<<<1, 1, 0, s>>>(p->st.p, b->max_iter, b->tol); }));
+  if (use_op)
+    KFBI_CUDA(cudaMemcpyAsync(p->phi0.p, b->density, p->n_ctl * es, cudaMemcpyDeviceToDevice, s),
+              "density-update");
   int enqueued = 0;
   int batch = b->sweeps_hint > 0 ? b->sweeps_hint : 4;
   for (;;) {
     int nb = batch;
     if (nb > b->max_iter - enqueued) nb = b->max_iter - enqueued;
     for (int k = 0; k < nb; ++k) {
-      if (cplx) KFBI_TRY(sweep<double2>(p, b, s));
-      else KFBI_TRY(sweep<double>(p, b, s));
+      const int idx = enqueued + k;      // 0-based sweep index
+      if (idx == 0 || !use_op) {
+        if (cplx) KFBI_TRY(sweep<double2>(p, b, s));
+        else KFBI_TRY(sweep<double>(p, b, s));
+        if (idx == 0 && use_op)
+          KFBI_CUDA(cudaMemcpyAsync(p->trace1.p, b->trace_u, p->n_ctl * es, cudaMemcpyDeviceToDevice, s),
+                    "density-update");
+      } else {
+        if (cplx) KFBI_TRY(op_sweep<double2>(p, b, s));
+        else KFBI_TRY(op_sweep<double>(p, b, s));
+      }
     }
     enqueued += nb;
     KFBI_CUDA(cudaMemcpyAsync(p->st_host, p->st.p, sizeof(RichState), cudaMemcpyDeviceToHost, s),
               "density-update");
     KFBI_CUDA(cudaStreamSynchronize(s), "density-update");
     if (p->st_host->done != 0 || enqueued >= b->max_iter) break;
-    batch = 2;
+    batch = use_op ? 8 : 2;
+  }
+  if (use_op && p->st_host->done == 1 && p->st_host->iters >= 2) {
+    if (cplx) KFBI_TRY(final_pipeline<double2>(p, b, s));
+    else KFBI_TRY(final_pipeline<double>(p, b, s));
   }
   const RichState &h = *p->st_host;
   res->iterations = h.iters;
@@ -570,6 +695,14 @@ kfbi_status kfbi_richardson(kfbi_plan *p, const kfbi_bvp *b, kfbi_bvp_result *re
     return fail(KFBI_E_NOCONV, msg);
   }
   return KFBI_OK;
+}
+
+kfbi_status kfbi_build_trace_operator(kfbi_plan *p, int32_t dtype, double kre, double kim, void *stream) {
+  KFBI_TRY(check_geo(p));
+  cudaStream_t s = (cudaStream_t)stream;
+  if (dtype == KFBI_C128) return build_operator_T<double2>(p, kre, kim, s);
+  if (kim != 0.0) return fail(KFBI_E_CONFIG, "complex kappa requires the c128 path");
+  return build_operator_T<double>(p, kre, kim, s);
 }
 
 kfbi_status kfbi_heat_rhs(kfbi_plan *p, int64_t n, const uint8_t *mask, void *u, const void *F_old,

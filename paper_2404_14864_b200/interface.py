@@ -248,6 +248,13 @@ class InterfaceWorkspace:
             self._plan = plan
         return self._plan
 
+    def ensure_operator(self, kappa, cplx):
+        """Build (once per kappa) the explicit trace operator used by the
+        operator form of the Richardson sweeps."""
+        key = (complex(kappa), bool(cplx))
+        if getattr(self.plan, "operator_key", None) != key:
+            self.plan.build_operator(kappa, cplx)
+
     def box_solver(self, kappa, bc):
         key = (complex(kappa), bc)
         if key not in self._box_solvers:

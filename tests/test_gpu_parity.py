@@ -199,16 +199,18 @@ def test_convergence_error_fields():
     assert ei.value.iterations == 3 and ei.value.last_residual > 0.0
 
 
+@pytest.mark.parametrize("operator", [False, True], ids=["pipeline", "operator"])
 @pytest.mark.parametrize("name", list(run_cases()))
-def test_full_runs_vs_reference(name):
+def test_full_runs_vs_reference(name, operator):
     box, m, curve, kw = run_cases()[name]
     geo = k.build_grid(box, m, curve)
-    res = k.run(k.ProblemSpec(**kw), geo)
+    res = k.run(k.ProblemSpec(**kw), geo, operator=operator)
     g = golden("runs")
     assert res.iterations == list(g[name + "__iterations"])
     assert rel_linf(res.state.u, g[name + "__u"]) < TOL
     assert res.state.u.shape == (m + 1, m + 1)
-    assert res.kernel_calls["transform-cols"] >= sum(res.iterations)
+    assert res.kernel_calls["transform-cols"] >= (sum(res.iterations) if not operator
+                                                  else len(res.iterations))
     assert res.kernel_times["transform-rows"] > 0.0
 
 
@@ -246,7 +248,12 @@ def test_runs_1024_vs_oracle_window(eq):
                   lap_u0=schr.lap_u0, potential=schr.potential, tau=1 / 128, t_final=2 / 128)
     geo = k.build_grid(box, m, curve)
     ctx = k.StepContext(geo)
-    res = k.run(k.ProblemSpec(**kw), geo, context=ctx)
+    res = k.run(k.ProblemSpec(**kw), geo, context=ctx, operator=False)
     st = O.run(O.tables_from_workspace(ctx.workspace), oracle_spec(kw))
     assert res.iterations == st.iterations
     assert rel_linf(res.state.u, st.u) < TOL
+    if eq != "wave":
+        # operator form of the sweeps on the same problem
+        res2 = k.run(k.ProblemSpec(**kw), geo, context=ctx, operator=True)
+        assert res2.iterations == st.iterations
+        assert rel_linf(res2.state.u, st.u) < TOL
