@@ -76,7 +76,7 @@ def workload(m):
     }
 
 
-def config_obj(m, eqs, n):
+def config_obj(m, eqs, n, mode=None):
     return {
         "workload": f"KFBI per-step solve, {m}x{m} grid, one time step each of "
                     + "/".join(eqs) + " (heat flower8, wave ellipse, Schrodinger star3)",
@@ -196,11 +196,17 @@ def run_ours(args):
     for eq in eqs:
         box, curve, kw = wl[eq]
         geo = k.build_grid(box, m, curve)
-        ctxs[eq] = k.StepContext(geo, backend=backend)
+        ctxs[eq] = k.StepContext(geo, backend=backend, operator=not args.pipeline)
         specs[eq] = k.ProblemSpec(**kw)
         startup, step = _stepper_for(specs[eq])
         steppers[eq] = step
         states[eq] = startup(specs[eq], ctxs[eq])
+        if not args.pipeline:
+            kap = {"heat": 2.0 * specs[eq].c / specs[eq].tau,
+                   "wave": 1.0 / (specs[eq].theta * specs[eq].tau ** 2),
+                   "schrodinger": 2j / specs[eq].tau}[eq]
+            ctxs[eq].workspace.ensure_operator(kap, eq == "schrodinger")
+    torch.cuda.synchronize()
     t_setup = time.time() - t_setup
 
     def advance(eq):
@@ -322,6 +328,8 @@ def run_ours(args):
         "gpu_launches": int(launches),
         "clocks": clocks,
         "setup_s": t_setup,
+        "sweep_mode": "pipeline" if args.pipeline else
+        "operator (sweep 1 + returned field by the full pipeline, sweeps >= 2 via the trace operator)",
     }
     if not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(ctxs, specs, iters, args)
@@ -469,6 +477,8 @@ def main(argv=None):
     ap.add_argument("--m", type=int, default=M_DEFAULT)
     ap.add_argument("--equations", default=",".join(EQUATIONS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--pipeline", action="store_true",
+                    help="run every Richardson sweep through the full pipeline (no trace operator)")
     args = ap.parse_args(argv)
     args.equations = tuple(e for e in args.equations.split(",") if e)
     if args.warmup < 3:
