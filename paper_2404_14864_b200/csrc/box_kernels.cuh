@@ -14,15 +14,19 @@
 // M*32-byte slab, and a row task writes full 32-byte sectors.
 //
 // Real data is packed two rows (or two columns) per complex sequence.
+// Global loads are batched (LB per thread in flight) before the shared-memory
+// scatter so the HBM latency is overlapped.
 #pragma once
 
 #include "dst_engine.cuh"
 
 namespace kfbi {
 
+constexpr int LB = 8;   // global loads in flight per thread in the load phases
+
 struct BoxArgs {
   int m, logm;
-  const double2 *tw;      // [m] exp(-i pi q / m)
+  const double2 *tw;      // packed twiddle table (twiddle_slots(m) entries)
   const double *lam;      // [m+1] (2cos(p pi/m) - 2)/h^2 at p = 1..m-1
   double kre, kim;        // kappa
   double inv4m2;          // 1 / (4 m^2), exact power of two
@@ -71,9 +75,14 @@ KFBI_DEV void add_component(double2 *sm, int p, bool neg, bool imag, double v) {
   double *slot = reinterpret_cast<double *>(&sm[phys(p)]) + (imag ? 1 : 0);
   *slot += neg ? -v : v;
 }
-KFBI_DEV void add_corr(double2 *sm, int p, bool neg, bool /*imag*/, double2 v) {
+KFBI_DEV void add_corr(double2 *sm, int p, bool neg, double2 v) {
   double2 &slot = sm[phys(p)];
   slot = neg ? csub(slot, v) : cadd(slot, v);
+}
+
+// Shared-memory bytes of a kernel holding nseq sequences of length m.
+inline size_t box_smem_bytes(int m, int nseq) {
+  return ((size_t)nseq * m + twiddle_slots(m)) * sizeof(double2);
 }
 
 // ---------------------------------------------------------------------------
@@ -89,21 +98,34 @@ rows_fwd_kernel(BoxArgs a, const void *__restrict__ rhs, double sign,
   const int stride = M + 1;
   const int j0 = CPLX ? blockIdx.x + 1 : 2 * blockIdx.x + 1;
   const bool has2 = !CPLX && (j0 + 1 < M);
+  const Twiddle tw = load_twiddles(sm + M, a.tw, M, tid, NT);
 
-  for (int n = 1 + tid; n < M; n += NT) {
-    double2 v;
-    if (rhs == nullptr) {
-      v = make_double2(0.0, 0.0);
-    } else if (CPLX) {
-      v = cscale(static_cast<const double2 *>(rhs)[(size_t)j0 * stride + n], sign);
-    } else {
-      const double *r = static_cast<const double *>(rhs);
-      v.x = r[(size_t)j0 * stride + n] * sign;
-      v.y = has2 ? r[(size_t)(j0 + 1) * stride + n] * sign : 0.0;
+  for (int n0 = 1 + tid; n0 < M; n0 += NT * LB) {
+    double2 v[LB];
+#pragma unroll
+    for (int b = 0; b < LB; ++b) {
+      const int n = n0 + b * NT;
+      v[b] = make_double2(0.0, 0.0);
+      if (n < M && rhs != nullptr) {
+        if (CPLX) {
+          v[b] = static_cast<const double2 *>(rhs)[(size_t)j0 * stride + n];
+        } else {
+          const double *r = static_cast<const double *>(rhs);
+          v[b].x = r[(size_t)j0 * stride + n];
+          if (has2) v[b].y = r[(size_t)(j0 + 1) * stride + n];
+        }
+      }
     }
-    bool neg;
-    int p = dst_in_pos(n, logN, neg);
-    sm[phys(p)] = neg ? cneg(v) : v;
+#pragma unroll
+    for (int b = 0; b < LB; ++b) {
+      const int n = n0 + b * NT;
+      if (n < M) {
+        bool neg;
+        const int p = dst_in_pos(n, logN, neg);
+        const double2 x = cscale(v[b], sign);
+        sm[phys(p)] = neg ? cneg(x) : x;
+      }
+    }
   }
   __syncthreads();
   if (corr.jv) {
@@ -112,17 +134,17 @@ rows_fwd_kernel(BoxArgs a, const void *__restrict__ rhs, double sign,
       const int j = j0 + q;
       const int g0 = corr.row_group[j], g1 = corr.row_group[j + 1];
       for (int g = g0 + tid; g < g1; g += NT) {
-        T cv = group_correction<T>(corr, g);
-        int i = corr.group_node[g] - j * stride;
+        const T cv = group_correction<T>(corr, g);
+        const int i = corr.group_node[g] - j * stride;
         bool neg;
-        int p = dst_in_pos(i, logN, neg);
-        if constexpr (CPLX) add_corr(sm, p, neg, false, cv);
+        const int p = dst_in_pos(i, logN, neg);
+        if constexpr (CPLX) add_corr(sm, p, neg, cv);
         else add_component(sm, p, neg, q == 1, cv);
       }
     }
     __syncthreads();
   }
-  dst1_forward(sm, 1, logN, a.tw, tid, NT);
+  dst1_forward(sm, 1, logN, tw, tid, NT);
 
   const int r = j0 - 1;
   if (!CPLX) {
@@ -131,8 +153,8 @@ rows_fwd_kernel(BoxArgs a, const void *__restrict__ rhs, double sign,
       double re[4], im[4];
 #pragma unroll
       for (int w = 0; w < 4; ++w) {
-        int k = 4 * pp + w + 1;
-        double2 c = (k < M) ? sm[phys(k)] : make_double2(0.0, 0.0);
+        const int k = 4 * pp + w + 1;
+        const double2 c = (k < M) ? sm[phys(k)] : make_double2(0.0, 0.0);
         re[w] = c.x;
         im[w] = c.y;
       }
@@ -145,9 +167,9 @@ rows_fwd_kernel(BoxArgs a, const void *__restrict__ rhs, double sign,
   } else {
     double2 *P = static_cast<double2 *>(a.panels);
     for (int pp = tid; pp < (M >> 1); pp += NT) {
-      int k = 2 * pp + 1;
-      double2 c0 = sm[phys(k)];
-      double2 c1 = (k + 1 < M) ? sm[phys(k + 1)] : make_double2(0.0, 0.0);
+      const int k = 2 * pp + 1;
+      const double2 c0 = sm[phys(k)];
+      const double2 c1 = (k + 1 < M) ? sm[phys(k + 1)] : make_double2(0.0, 0.0);
       double2 *d0 = P + ((size_t)pp * M + r) * 2;
       d0[0] = c0;
       d0[1] = c1;
@@ -165,16 +187,31 @@ __global__ void __launch_bounds__(512) cols_kernel(BoxArgs a) {
   const int pp = blockIdx.x;
   double2 *P = static_cast<double2 *>(a.panels) + (size_t)pp * M * 2;
   double2 *s1 = sm + M;
+  const Twiddle tw = load_twiddles(sm + 2 * M, a.tw, M, tid, NT);
 
-  for (int r = tid; r < M - 1; r += NT) {
-    double2 v0 = P[2 * r], v1 = P[2 * r + 1];
-    bool neg;
-    int p = phys(dst_in_pos(r + 1, logN, neg));
-    sm[p] = neg ? cneg(v0) : v0;
-    s1[p] = neg ? cneg(v1) : v1;
+  for (int r0 = tid; r0 < M - 1; r0 += NT * (LB / 2)) {
+    double2 v[LB];
+#pragma unroll
+    for (int b = 0; b < LB / 2; ++b) {
+      const int r = r0 + b * NT;
+      if (r < M - 1) {
+        v[2 * b] = P[2 * r];
+        v[2 * b + 1] = P[2 * r + 1];
+      }
+    }
+#pragma unroll
+    for (int b = 0; b < LB / 2; ++b) {
+      const int r = r0 + b * NT;
+      if (r < M - 1) {
+        bool neg;
+        const int p = phys(dst_in_pos(r + 1, logN, neg));
+        sm[p] = neg ? cneg(v[2 * b]) : v[2 * b];
+        s1[p] = neg ? cneg(v[2 * b + 1]) : v[2 * b + 1];
+      }
+    }
   }
   __syncthreads();
-  dst1_forward(sm, 2, logN, a.tw, tid, NT);
+  dst1_forward(sm, 2, logN, tw, tid, NT);
 
   for (int idx = tid; idx < 2 * (M - 1); idx += NT) {
     const int q = idx >= M - 1 ? 1 : 0;
@@ -184,14 +221,14 @@ __global__ void __launch_bounds__(512) cols_kernel(BoxArgs a) {
     const double lp = a.lam[p];
     if (!CPLX) {
       const int kx = 4 * pp + 2 * q + 1;          // spectral x index of .x
-      double da = (lp + a.lam[kx < M ? kx : 1]) - a.kre;
-      double db = (lp + a.lam[kx + 1 < M ? kx + 1 : 1]) - a.kre;
+      const double da = (lp + a.lam[kx < M ? kx : 1]) - a.kre;
+      const double db = (lp + a.lam[kx + 1 < M ? kx + 1 : 1]) - a.kre;
       v.x = kx < M ? (v.x / da) * a.inv4m2 : 0.0;
       v.y = kx + 1 < M ? (v.y / db) * a.inv4m2 : 0.0;
     } else {
       const int kx = 2 * pp + q + 1;
       if (kx < M) {
-        double2 d = make_double2((lp + a.lam[kx]) - a.kre, -a.kim);
+        const double2 d = make_double2((lp + a.lam[kx]) - a.kre, -a.kim);
         v = cscale(cdiv(v, d), a.inv4m2);
       } else {
         v = make_double2(0.0, 0.0);
@@ -200,12 +237,12 @@ __global__ void __launch_bounds__(512) cols_kernel(BoxArgs a) {
     *slot = v;
   }
   __syncthreads();
-  dst1_adjoint(sm, 2, logN, a.tw, tid, NT);
+  dst1_adjoint(sm, 2, logN, tw, tid, NT);
 
   for (int r = tid; r < M - 1; r += NT) {
     bool neg;
-    int p = phys(dst_in_pos(r + 1, logN, neg));
-    double2 v0 = sm[p], v1 = s1[p];
+    const int p = phys(dst_in_pos(r + 1, logN, neg));
+    const double2 v0 = sm[p], v1 = s1[p];
     P[2 * r] = neg ? cneg(v0) : v0;
     P[2 * r + 1] = neg ? cneg(v1) : v1;
   }
@@ -222,31 +259,65 @@ __global__ void __launch_bounds__(256) rows_inv_kernel(BoxArgs a, void *__restri
   const int j0 = CPLX ? blockIdx.x + 1 : 2 * blockIdx.x + 1;
   const bool has2 = !CPLX && (j0 + 1 < M);
   const int r = j0 - 1;
+  const Twiddle tw = load_twiddles(sm + M, a.tw, M, tid, NT);
 
   if (!CPLX) {
     const double *P = static_cast<const double *>(a.panels);
-    for (int pp = tid; pp < (M >> 2); pp += NT) {
-      const double2 *s0 = reinterpret_cast<const double2 *>(P + ((size_t)pp * M + r) * 4);
-      double2 a01 = s0[0], a23 = s0[1], b01 = s0[2], b23 = s0[3];
-      double re[4] = {a01.x, a01.y, a23.x, a23.y};
-      double im[4] = {b01.x, b01.y, b23.x, b23.y};
+    constexpr int B = LB / 4;
+    for (int p0 = tid; p0 < (M >> 2); p0 += NT * B) {
+      double2 v[4 * B];
 #pragma unroll
-      for (int w = 0; w < 4; ++w) {
-        int k = 4 * pp + w + 1;
-        if (k < M) sm[phys(k)] = make_double2(re[w], has2 ? im[w] : 0.0);
+      for (int b = 0; b < B; ++b) {
+        const int pp = p0 + b * NT;
+        if (pp < (M >> 2)) {
+          const double2 *s0 = reinterpret_cast<const double2 *>(P + ((size_t)pp * M + r) * 4);
+          v[4 * b] = s0[0];
+          v[4 * b + 1] = s0[1];
+          v[4 * b + 2] = s0[2];
+          v[4 * b + 3] = s0[3];
+        }
+      }
+#pragma unroll
+      for (int b = 0; b < B; ++b) {
+        const int pp = p0 + b * NT;
+        if (pp < (M >> 2)) {
+          const double re[4] = {v[4 * b].x, v[4 * b].y, v[4 * b + 1].x, v[4 * b + 1].y};
+          const double im[4] = {v[4 * b + 2].x, v[4 * b + 2].y, v[4 * b + 3].x, v[4 * b + 3].y};
+#pragma unroll
+          for (int w = 0; w < 4; ++w) {
+            const int k = 4 * pp + w + 1;
+            if (k < M) sm[phys(k)] = make_double2(re[w], has2 ? im[w] : 0.0);
+          }
+        }
       }
     }
   } else {
     const double2 *P = static_cast<const double2 *>(a.panels);
-    for (int pp = tid; pp < (M >> 1); pp += NT) {
-      const double2 *s0 = P + ((size_t)pp * M + r) * 2;
-      int k = 2 * pp + 1;
-      sm[phys(k)] = s0[0];
-      if (k + 1 < M) sm[phys(k + 1)] = s0[1];
+    constexpr int B = LB / 2;
+    for (int p0 = tid; p0 < (M >> 1); p0 += NT * B) {
+      double2 v[2 * B];
+#pragma unroll
+      for (int b = 0; b < B; ++b) {
+        const int pp = p0 + b * NT;
+        if (pp < (M >> 1)) {
+          const double2 *s0 = P + ((size_t)pp * M + r) * 2;
+          v[2 * b] = s0[0];
+          v[2 * b + 1] = s0[1];
+        }
+      }
+#pragma unroll
+      for (int b = 0; b < B; ++b) {
+        const int pp = p0 + b * NT;
+        if (pp < (M >> 1)) {
+          const int k = 2 * pp + 1;
+          sm[phys(k)] = v[2 * b];
+          if (k + 1 < M) sm[phys(k + 1)] = v[2 * b + 1];
+        }
+      }
     }
   }
   __syncthreads();
-  dst1_adjoint(sm, 1, logN, a.tw, tid, NT);
+  dst1_adjoint(sm, 1, logN, tw, tid, NT);
 
   // gather + store, with the zero ring (boxsolve.py:90-93)
   if (!CPLX) {
@@ -257,7 +328,7 @@ __global__ void __launch_bounds__(256) rows_inv_kernel(BoxArgs a, void *__restri
       double x = 0.0, y = 0.0;
       if (n >= 1 && n < M) {
         bool neg;
-        double2 v = sm[phys(dst_in_pos(n, logN, neg))];
+        const double2 v = sm[phys(dst_in_pos(n, logN, neg))];
         x = neg ? -v.x : v.x;
         y = neg ? -v.y : v.y;
       }

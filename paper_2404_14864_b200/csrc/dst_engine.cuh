@@ -19,6 +19,10 @@
 // at position k.  A 3-bit XOR swizzle (phys) spreads the bit-reversed scatter
 // over the 16-byte bank groups.
 //
+// Twiddles exp(-i pi q / N) come from two 64-entry shared tables
+// (hi[q >> 6] * lo[q & 63]); inside a radix-8 task only three are looked up,
+// the others are exact +-i rotations or one multiply by exp(-i pi / 4).
+//
 // Forward engine E   : caller scatters c_n to dst_in_pos(n) (phase A), then
 //                      B (DIT FFTs) -> C (Makhoul) -> D (combine); natural out.
 // Adjoint engine E^H : natural input at position k, then D^H -> C^H -> B^H
@@ -32,11 +36,38 @@
 
 namespace kfbi {
 
+constexpr double SQRT_HALF = 0.70710678118654752440;
+constexpr int TW_LO = 64;
+
 // Swizzled physical slot of logical position p.
 KFBI_DEV int phys(int p) {
   int h = p >> 3;
   int f = h ^ (h >> 3) ^ (h >> 6) ^ (h >> 9) ^ (h >> 12);
   return p ^ (f & 7);
+}
+
+// Twiddle table view (shared memory): lo[r] = exp(-i pi r / N), r < 64;
+// hi[t] = exp(-i pi 64 t / N), t < max(1, N/64); both stored at phys(index).
+struct Twiddle {
+  const double2 *lo;
+  const double2 *hi;
+  KFBI_DEV double2 operator()(int q) const {
+    const int t = q >> 6;
+    const double2 b = lo[phys(q & 63)];
+    return t ? cmul(hi[phys(t)], b) : b;
+  }
+};
+
+// Number of double2 slots of the table for a given N.
+__host__ __device__ inline int twiddle_slots(int N) { return TW_LO + (N >= 128 ? N / 64 : 1); }
+
+// Cooperative copy of the global table into shared memory (no sync).
+KFBI_DEV Twiddle load_twiddles(double2 *dst, const double2 *__restrict__ src, int N, int tid,
+                               int nthreads) {
+  const int n = twiddle_slots(N);
+  // both tables are read at power-of-two strides: store them swizzled
+  for (int i = tid; i < n; i += nthreads) dst[i < TW_LO ? phys(i) : TW_LO + phys(i - TW_LO)] = src[i];
+  return Twiddle{dst, dst + TW_LO};
 }
 
 // Logical smem position and sign of input c_n, 1 <= n < N (phase A).
@@ -51,13 +82,38 @@ KFBI_DEV int dst_in_pos(int n, int logN, bool &neg) {
   return L + r;
 }
 
+KFBI_DEV double2 mul_negi(double2 z) { return make_double2(z.y, -z.x); }        // z * (-i)
+KFBI_DEV double2 mul_w8(double2 z) {                                             // z * e^{-i pi/4}
+  return make_double2(SQRT_HALF * (z.x + z.y), SQRT_HALF * (z.y - z.x));
+}
+
 // ---- phase B: one pass of R fused radix-2 stages, stages s0..s0+R-1 ----
-// Element q (0 <= q < 2^R) of a task sits at base + q*hs, hs = 2^s0.
+// Element q (0 <= q < 2^R) of a task sits at base + q*hs, hs = 2^s0; the
+// twiddle of sub-stage u and in-span offset k is w_u * exp(-i pi k / 2^u),
+// w_u = exp(-i pi j 2^(logN - s0 - u) / N).
 template <int R, bool ADJ>
-KFBI_DEV void fft_task(double2 *s, int base, int j, int s0, int logN,
-                       const double2 *__restrict__ tw) {
+KFBI_DEV void fft_task(double2 *s, int base, int j, int s0, int logN, const Twiddle &tw) {
   constexpr int E = 1 << R;
   const int hs = 1 << s0;
+  const int a = logN - s0;
+  double2 w[R][E / 2];
+  {
+    const double2 w0 = tw(j << a);
+    w[0][0] = w0;
+    if (R > 1) {
+      const double2 w1 = tw(j << (a - 1));
+      w[(R > 1) ? 1 : 0][0] = w1;
+      w[(R > 1) ? 1 : 0][1] = mul_negi(w1);
+    }
+    if (R > 2) {
+      const double2 w2 = tw(j << (a - 2));
+      const double2 w2b = mul_w8(w2);
+      w[R - 1][0] = w2;
+      w[R - 1][1] = w2b;
+      w[R - 1][2 % (E / 2)] = mul_negi(w2);
+      w[R - 1][3 % (E / 2)] = mul_negi(w2b);
+    }
+  }
   double2 x[E];
 #pragma unroll
   for (int q = 0; q < E; ++q) x[q] = s[phys(base + q * hs)];
@@ -68,8 +124,7 @@ KFBI_DEV void fft_task(double2 *s, int base, int j, int s0, int logN,
 #pragma unroll
       for (int q = 0; q < E; ++q) {
         if (q & span) continue;
-        double2 w = __ldg(&tw[(j + (q & (span - 1)) * hs) << (logN - s0 - u)]);
-        double2 b = cmul(w, x[q + span]);
+        const double2 b = cmul(w[u][q & (span - 1)], x[q + span]);
         x[q + span] = csub(x[q], b);
         x[q] = cadd(x[q], b);
       }
@@ -81,10 +136,9 @@ KFBI_DEV void fft_task(double2 *s, int base, int j, int s0, int logN,
 #pragma unroll
       for (int q = 0; q < E; ++q) {
         if (q & span) continue;
-        double2 w = cconj(__ldg(&tw[(j + (q & (span - 1)) * hs) << (logN - s0 - u)]));
-        double2 a = x[q], b = x[q + span];
-        x[q] = cadd(a, b);
-        x[q + span] = cmul(w, csub(a, b));
+        const double2 a0 = x[q], b0 = x[q + span];
+        x[q] = cadd(a0, b0);
+        x[q + span] = cmul(cconj(w[u][q & (span - 1)]), csub(a0, b0));
       }
     }
   }
@@ -95,20 +149,19 @@ KFBI_DEV void fft_task(double2 *s, int base, int j, int s0, int logN,
 // Blocks with logL >= s0 + R do a full R-stage pass; the (at most R-1) block
 // sizes with s0 < logL < s0 + R run the stages they have left.
 template <int R, bool ADJ>
-KFBI_DEV void fft_pass(double2 *s, int s0, int logN, const double2 *__restrict__ tw,
-                       int tid, int nthreads) {
+KFBI_DEV void fft_pass(double2 *s, int s0, int logN, const Twiddle &tw, int tid, int nthreads) {
   const int N = 1 << logN;
   const int hs = 1 << s0;
   // full blocks L = N/2 .. 2^(s0+R) occupy the element range [0, N - 2^(s0+R))
   // in the order "largest first": block L covers [N - 2L, N - L).
   const int n_full = (N - (1 << (s0 + R))) >> R;
   for (int t = tid; t < n_full; t += nthreads) {
-    int r = N - (t << R);                              // in (L, 2L]
-    int logL = 31 - __clz(r - 1);
-    int L = 1 << logL;
-    int tau = (2 * L - r) >> R;                        // task index in block
-    int j = tau & (hs - 1);
-    int g = tau >> s0;
+    const int r = N - (t << R);                        // in (L, 2L]
+    const int logL = 31 - __clz(r - 1);
+    const int L = 1 << logL;
+    const int tau = (2 * L - r) >> R;                  // task index in block
+    const int j = tau & (hs - 1);
+    const int g = tau >> s0;
     fft_task<R, ADJ>(s, L + (g << (s0 + R)) + j, j, s0, logN, tw);
   }
   if (R > 1) {
@@ -121,14 +174,14 @@ KFBI_DEV void fft_pass(double2 *s, int s0, int logN, const double2 *__restrict__
 }
 
 template <bool ADJ>
-KFBI_DEV void fft_all(double2 *s, int logN, const double2 *__restrict__ tw, int tid,
-                      int nthreads, bool active) {
+KFBI_DEV void fft_all(double2 *s, int logN, const Twiddle &tw, int tid, int nthreads,
+                      bool active) {
   const int nst = logN - 1;    // stages of the largest block (L = N/2)
   const int npass = (nst + 2) / 3;
   for (int ip = 0; ip < npass; ++ip) {
-    int pass = ADJ ? npass - 1 - ip : ip;
-    int st = 3 * pass;
-    int R = nst - st < 3 ? nst - st : 3;
+    const int pass = ADJ ? npass - 1 - ip : ip;
+    const int st = 3 * pass;
+    const int R = nst - st < 3 ? nst - st : 3;
     if (active) {
       if (R == 3) fft_pass<3, ADJ>(s, st, logN, tw, tid, nthreads);
       else if (R == 2) fft_pass<2, ADJ>(s, st, logN, tw, tid, nthreads);
@@ -141,31 +194,28 @@ KFBI_DEV void fft_all(double2 *s, int logN, const double2 *__restrict__ tw, int 
 // ---- phase C: Makhoul post-twiddle, pairs (k, L-k) of every block ----
 //   forward: G_{L-k} = w_k V_k + conj(w_k) V_{L-k};  G_k = w_{L-k} V_{L-k} + conj(w_{L-k}) V_k
 //   adjoint: the conjugate transpose of that 2x2 map.
-// w_k = exp(-i pi k / (2L)); G_j is stored at L + (j mod L), i.e. in the
-// slots the pair was read from.  k = 0, k = L/2 and the L = 1 block scale by
-// real factors (2, 2cos(pi/4), 2), identical in both directions.
+// w_k = exp(-i pi k / (2L)), w_{L-k} = -i conj(w_k); G_j is stored at
+// L + (j mod L), i.e. in the slots the pair was read from.  k = 0, k = L/2
+// and the L = 1 block scale by real factors (2, sqrt 2, 2) in both directions.
 template <bool ADJ>
-KFBI_DEV void post_pass(double2 *s, int logN, const double2 *__restrict__ tw, int tid,
-                        int nthreads) {
+KFBI_DEV void post_pass(double2 *s, int logN, const Twiddle &tw, int tid, int nthreads) {
   const int N = 1 << logN;
   for (int t = tid; t < (N >> 1) - 1; t += nthreads) {
-    int r = (N >> 1) - t;                              // in (L/2, L]
-    int logL = 32 - __clz(r - 1);
-    int L = 1 << logL;
-    int k = L - r;                                     // 0 .. L/2-1
-    int sh = logN - 1 - logL;
+    const int r = (N >> 1) - t;                        // in (L/2, L]
+    const int logL = 32 - __clz(r - 1);
+    const int L = 1 << logL;
+    const int k = L - r;                               // 0 .. L/2-1
     if (k == 0) {
-      int p0 = phys(L);
+      const int p0 = phys(L);
       s[p0] = cscale(s[p0], 2.0);
-      int ph = phys(L + (L >> 1));
-      double c = __ldg(&tw[(L >> 1) << sh]).x;
-      s[ph] = cscale(s[ph], 2.0 * c);
+      const int ph = phys(L + (L >> 1));
+      s[ph] = cscale(s[ph], 2.0 * SQRT_HALF);
       continue;
     }
-    int pa = phys(L + k), pb = phys(2 * L - k);
-    double2 a = s[pa], b = s[pb];
-    double2 wk = __ldg(&tw[k << sh]);
-    double2 wm = __ldg(&tw[(L - k) << sh]);
+    const int pa = phys(L + k), pb = phys(2 * L - k);
+    const double2 a = s[pa], b = s[pb];
+    const double2 wk = tw(k << (logN - 1 - logL));
+    const double2 wm = make_double2(-wk.y, -wk.x);     // -i conj(w_k)
     if (!ADJ) {
       s[pb] = cadd(cmul(wk, a), cmul(cconj(wk), b));   // G_{L-k}
       s[pa] = cadd(cmul(wm, b), cmul(cconj(wm), a));   // G_k
@@ -175,7 +225,7 @@ KFBI_DEV void post_pass(double2 *s, int logN, const double2 *__restrict__ tw, in
     }
   }
   if (tid == 0) {
-    int p1 = phys(1);
+    const int p1 = phys(1);
     s[p1] = cscale(s[p1], 2.0);
   }
 }
@@ -186,15 +236,15 @@ template <bool ADJ>
 KFBI_DEV void combine_level(double2 *s, int L, int tid, int nthreads) {
   const int half = L >> 1;
   for (int k = 1 + tid; k <= half; k += nthreads) {
-    int pd = phys(k), pg = phys(L + k);
-    double2 a = s[pd], b = s[pg];
+    const int pd = phys(k), pg = phys(L + k);
+    const double2 a = s[pd], b = s[pg];
     if (k == half) {
       if (!ADJ) { s[pd] = cadd(a, b); s[pg] = csub(b, a); }
       else      { s[pd] = csub(a, b); s[pg] = cadd(a, b); }
       continue;
     }
-    int pdm = phys(L - k), pgm = phys(2 * L - k);
-    double2 c = s[pdm], d = s[pgm];
+    const int pdm = phys(L - k), pgm = phys(2 * L - k);
+    const double2 c = s[pdm], d = s[pgm];
     if (!ADJ) {
       s[pd] = cadd(a, b);            // C_k
       s[pgm] = csub(b, a);           // C_{2L-k}
@@ -209,12 +259,16 @@ KFBI_DEV void combine_level(double2 *s, int L, int tid, int nthreads) {
   }
 }
 
+// Levels L = 2..32 touch positions [1, 64) only: one warp runs them with
+// warp barriers instead of block barriers.
+constexpr int WARP_LEVELS_END = 64;
+
 // Engines over `nseq` sequences stored back to back (stride N positions),
-// threads split into nseq equal groups.  Must be entered by all threads of the
-// block after the input is in place and a __syncthreads(); they return after
-// a final __syncthreads().
-KFBI_DEV void dst1_forward(double2 *s0, int nseq, int logN, const double2 *__restrict__ tw,
-                           int tid, int nthreads) {
+// threads split into nseq equal groups (each a multiple of 32).  Must be
+// entered by all threads of the block after the input is in place and a
+// __syncthreads(); they return after a final __syncthreads().
+KFBI_DEV void dst1_forward(double2 *s0, int nseq, int logN, const Twiddle &tw, int tid,
+                           int nthreads) {
   const int N = 1 << logN;
   const int per = nthreads / nseq;
   const int q = tid / per;
@@ -224,24 +278,39 @@ KFBI_DEV void dst1_forward(double2 *s0, int nseq, int logN, const double2 *__res
   fft_all<false>(s, logN, tw, lt, per, active);
   if (active) post_pass<false>(s, logN, tw, lt, per);
   __syncthreads();
-  for (int L = 2; L < N; L <<= 1) {
+  if (active && lt < 32) {
+    for (int L = 2; L < N && L < WARP_LEVELS_END; L <<= 1) {
+      combine_level<false>(s, L, lt, 32);
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+  for (int L = WARP_LEVELS_END; L < N; L <<= 1) {
     if (active) combine_level<false>(s, L, lt, per);
     __syncthreads();
   }
 }
 
-KFBI_DEV void dst1_adjoint(double2 *s0, int nseq, int logN, const double2 *__restrict__ tw,
-                           int tid, int nthreads) {
+KFBI_DEV void dst1_adjoint(double2 *s0, int nseq, int logN, const Twiddle &tw, int tid,
+                           int nthreads) {
   const int N = 1 << logN;
   const int per = nthreads / nseq;
   const int q = tid / per;
   const int lt = tid - q * per;
   const bool active = q < nseq;
   double2 *s = s0 + (size_t)(active ? q : 0) * N;
-  for (int L = N >> 1; L >= 2; L >>= 1) {
+  for (int L = N >> 1; L >= WARP_LEVELS_END; L >>= 1) {
     if (active) combine_level<true>(s, L, lt, per);
     __syncthreads();
   }
+  if (active && lt < 32) {
+    for (int L = (N >> 1) < (WARP_LEVELS_END >> 1) ? (N >> 1) : (WARP_LEVELS_END >> 1); L >= 2;
+         L >>= 1) {
+      combine_level<true>(s, L, lt, 32);
+      __syncwarp();
+    }
+  }
+  __syncthreads();
   if (active) post_pass<true>(s, logN, tw, lt, per);
   __syncthreads();
   fft_all<true>(s, logN, tw, lt, per, active);

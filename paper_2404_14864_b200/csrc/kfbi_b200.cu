@@ -227,13 +227,16 @@ ExtractArgs extract_args(kfbi_plan *p) {
 
 template <bool CPLX>
 kfbi_status set_smem_limits(kfbi_plan *p) {
-  size_t row = (size_t)p->m * sizeof(double2);
+  // The attribute is per kernel (process wide), not per plan: allow the
+  // largest size any plan can need so plans of different M coexist.
+  (void)p;
+  const int row = (int)box_smem_bytes(4096, 1), col = (int)box_smem_bytes(4096, 2);
   KFBI_CUDA(cudaFuncSetAttribute(rows_fwd_kernel<CPLX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)row), "transform-rows");
+                                 row), "transform-rows");
   KFBI_CUDA(cudaFuncSetAttribute(rows_inv_kernel<CPLX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)row), "transform-rows");
+                                 row), "transform-rows");
   KFBI_CUDA(cudaFuncSetAttribute(cols_kernel<CPLX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)(2 * row)), "transform-cols");
+                                 col), "transform-cols");
   return KFBI_OK;
 }
 
@@ -247,14 +250,14 @@ kfbi_status box_passes(kfbi_plan *p, double kre, double kim, const void *rhs, do
   const int M = p->m;
   const int ntask = CPLX ? M - 1 : M / 2;
   const int npanel = CPLX ? M / 2 : M / 4;
-  const size_t row = (size_t)M * sizeof(double2);
+  const size_t row = box_smem_bytes(M, 1), col = box_smem_bytes(M, 2);
   CorrArgs<T> c = corr_args<T>(p, static_cast<const T *>(jv));
   if (!jv) c.jv = nullptr;
   KFBI_TRY(launch(p, KFBI_K_ROWS, s, [&] {
     rows_fwd_kernel<CPLX><<<ntask, 256, row, s>>>(a, rhs, sign, c);
   }));
   KFBI_TRY(launch(p, KFBI_K_COLS, s, [&] {
-    cols_kernel<CPLX><<<npanel, 512, 2 * row, s>>>(a);
+    cols_kernel<CPLX><<<npanel, 512, col, s>>>(a);
   }));
   KFBI_TRY(launch(p, KFBI_K_ROWS, s, [&] {
     rows_inv_kernel<CPLX><<<ntask, 256, row, s>>>(a, u);
@@ -462,11 +465,15 @@ kfbi_status kfbi_plan_create(const kfbi_grid_desc *desc, kfbi_plan **out) {
   }
   // twiddles exp(-i pi q / m) in extended precision; lambda_p exactly as
   // boxsolve.py:43 evaluates it in double: (2 cos(p pi / m) - 2) / h^2
-  std::vector<double2> tw(m);
-  for (int q = 0; q < m; ++q) {
+  // packed two-level twiddle table: lo[r] = e^{-i pi r/m} (r < 64),
+  // hi[t] = e^{-i pi 64 t/m} (t < max(1, m/64)); see dst_engine.cuh
+  std::vector<double2> tw(twiddle_slots(m));
+  auto cis = [m](long q) {
     long double ang = 3.14159265358979323846264338327950288L * (long double)q / (long double)m;
-    tw[q] = make_double2((double)cosl(ang), (double)-sinl(ang));
-  }
+    return make_double2((double)cosl(ang), (double)-sinl(ang));
+  };
+  for (int r = 0; r < TW_LO; ++r) tw[r] = cis(r);
+  for (int t = 0; t < twiddle_slots(m) - TW_LO; ++t) tw[TW_LO + t] = cis(64L * t);
   std::vector<double> lam(m + 1, 0.0);
   for (int q = 1; q < m; ++q) {
     double ang = (double)q * M_PI / (double)m;
