@@ -146,87 +146,77 @@ rows_fwd_kernel(BoxArgs a, const void *__restrict__ rhs, double sign,
   }
   dst1_forward(sm, 1, logN, tw, tid, NT);
 
+  // lane-contiguous spectral index k: conflict-free shared reads; 4 (real)
+  // or 2 (complex) consecutive lanes fill one 32-byte panel sector.  The
+  // padding column k = M is never written (zero since plan creation).
   const int r = j0 - 1;
   if (!CPLX) {
     double *P = static_cast<double *>(a.panels);
-    for (int pp = tid; pp < (M >> 2); pp += NT) {
-      double re[4], im[4];
-#pragma unroll
-      for (int w = 0; w < 4; ++w) {
-        const int k = 4 * pp + w + 1;
-        const double2 c = (k < M) ? sm[phys(k)] : make_double2(0.0, 0.0);
-        re[w] = c.x;
-        im[w] = c.y;
-      }
-      double2 *d0 = reinterpret_cast<double2 *>(P + ((size_t)pp * M + r) * 4);
-      d0[0] = make_double2(re[0], re[1]);
-      d0[1] = make_double2(re[2], re[3]);
-      d0[2] = make_double2(im[0], im[1]);   // row r+1 directly follows row r
-      d0[3] = make_double2(im[2], im[3]);
+    for (int k = tid; k < M; k += NT) {   // k = 0 skipped: windows stay aligned
+      if (k == 0) continue;
+      const double2 c = sm[phys(k)];
+      const int kk = k - 1;
+      double *d0 = P + ((size_t)(kk >> 2) * M + r) * 4 + (kk & 3);
+      d0[0] = c.x;
+      d0[4] = c.y;                              // row r+1 follows row r
     }
   } else {
     double2 *P = static_cast<double2 *>(a.panels);
-    for (int pp = tid; pp < (M >> 1); pp += NT) {
-      const int k = 2 * pp + 1;
-      const double2 c0 = sm[phys(k)];
-      const double2 c1 = (k + 1 < M) ? sm[phys(k + 1)] : make_double2(0.0, 0.0);
-      double2 *d0 = P + ((size_t)pp * M + r) * 2;
-      d0[0] = c0;
-      d0[1] = c1;
+    for (int k = tid; k < M; k += NT) {
+      if (k == 0) continue;
+      const int kk = k - 1;
+      P[((size_t)(kk >> 1) * M + r) * 2 + (kk & 1)] = sm[phys(k)];
     }
   }
 }
 
 // ---------------------------------------------------------------------------
 // fused column pass: panel -> DST(y) -> scale -> DST(y) -> panel (in place)
+// One CTA per complex sequence = half a 32-byte panel (two real columns or one
+// complex column); the two halves of a panel are adjacent CTAs, so each
+// 32-byte sector is read from DRAM once and served to the second CTA by L2.
 template <bool CPLX>
-__global__ void __launch_bounds__(512) cols_kernel(BoxArgs a) {
+__global__ void __launch_bounds__(256) cols_kernel(BoxArgs a) {
   extern __shared__ double2 sm[];
   if (a.done && *a.done) return;
   const int M = a.m, logN = a.logm, tid = threadIdx.x, NT = blockDim.x;
-  const int pp = blockIdx.x;
-  double2 *P = static_cast<double2 *>(a.panels) + (size_t)pp * M * 2;
-  double2 *s1 = sm + M;
-  const Twiddle tw = load_twiddles(sm + 2 * M, a.tw, M, tid, NT);
+  const int pp = blockIdx.x >> 1, half = blockIdx.x & 1;
+  double2 *P = static_cast<double2 *>(a.panels) + (size_t)pp * M * 2 + half;
+  const Twiddle tw = load_twiddles(sm + M, a.tw, M, tid, NT);
 
-  for (int r0 = tid; r0 < M - 1; r0 += NT * (LB / 2)) {
+  for (int r0 = tid; r0 < M - 1; r0 += NT * LB) {
     double2 v[LB];
 #pragma unroll
-    for (int b = 0; b < LB / 2; ++b) {
+    for (int b = 0; b < LB; ++b) {
       const int r = r0 + b * NT;
-      if (r < M - 1) {
-        v[2 * b] = P[2 * r];
-        v[2 * b + 1] = P[2 * r + 1];
-      }
+      if (r < M - 1) v[b] = P[2 * r];
     }
 #pragma unroll
-    for (int b = 0; b < LB / 2; ++b) {
+    for (int b = 0; b < LB; ++b) {
       const int r = r0 + b * NT;
       if (r < M - 1) {
         bool neg;
         const int p = phys(dst_in_pos(r + 1, logN, neg));
-        sm[p] = neg ? cneg(v[2 * b]) : v[2 * b];
-        s1[p] = neg ? cneg(v[2 * b + 1]) : v[2 * b + 1];
+        sm[p] = neg ? cneg(v[b]) : v[b];
       }
     }
   }
   __syncthreads();
-  dst1_forward(sm, 2, logN, tw, tid, NT);
+  dst1_forward(sm, 1, logN, tw, tid, NT);
 
-  for (int idx = tid; idx < 2 * (M - 1); idx += NT) {
-    const int q = idx >= M - 1 ? 1 : 0;
-    const int p = idx - q * (M - 1) + 1;         // spectral y index
-    double2 *slot = &sm[q * M + phys(p)];
+  for (int p = tid; p < M; p += NT) {            // spectral y index (p = 0 unused)
+    if (p == 0) continue;
+    double2 *slot = &sm[phys(p)];
     double2 v = *slot;
     const double lp = a.lam[p];
     if (!CPLX) {
-      const int kx = 4 * pp + 2 * q + 1;          // spectral x index of .x
+      const int kx = 4 * pp + 2 * half + 1;      // spectral x index of .x
       const double da = (lp + a.lam[kx < M ? kx : 1]) - a.kre;
       const double db = (lp + a.lam[kx + 1 < M ? kx + 1 : 1]) - a.kre;
       v.x = kx < M ? (v.x / da) * a.inv4m2 : 0.0;
       v.y = kx + 1 < M ? (v.y / db) * a.inv4m2 : 0.0;
     } else {
-      const int kx = 2 * pp + q + 1;
+      const int kx = 2 * pp + half + 1;
       if (kx < M) {
         const double2 d = make_double2((lp + a.lam[kx]) - a.kre, -a.kim);
         v = cscale(cdiv(v, d), a.inv4m2);
@@ -237,14 +227,12 @@ __global__ void __launch_bounds__(512) cols_kernel(BoxArgs a) {
     *slot = v;
   }
   __syncthreads();
-  dst1_adjoint(sm, 2, logN, tw, tid, NT);
+  dst1_adjoint(sm, 1, logN, tw, tid, NT);
 
   for (int r = tid; r < M - 1; r += NT) {
     bool neg;
-    const int p = phys(dst_in_pos(r + 1, logN, neg));
-    const double2 v0 = sm[p], v1 = s1[p];
-    P[2 * r] = neg ? cneg(v0) : v0;
-    P[2 * r + 1] = neg ? cneg(v1) : v1;
+    const double2 v = sm[phys(dst_in_pos(r + 1, logN, neg))];
+    P[2 * r] = neg ? cneg(v) : v;
   }
 }
 
@@ -261,59 +249,28 @@ __global__ void __launch_bounds__(256) rows_inv_kernel(BoxArgs a, void *__restri
   const int r = j0 - 1;
   const Twiddle tw = load_twiddles(sm + M, a.tw, M, tid, NT);
 
-  if (!CPLX) {
-    const double *P = static_cast<const double *>(a.panels);
-    constexpr int B = LB / 4;
-    for (int p0 = tid; p0 < (M >> 2); p0 += NT * B) {
-      double2 v[4 * B];
+  for (int k0 = tid; k0 < M; k0 += NT * LB) {
+    double2 v[LB];
 #pragma unroll
-      for (int b = 0; b < B; ++b) {
-        const int pp = p0 + b * NT;
-        if (pp < (M >> 2)) {
-          const double2 *s0 = reinterpret_cast<const double2 *>(P + ((size_t)pp * M + r) * 4);
-          v[4 * b] = s0[0];
-          v[4 * b + 1] = s0[1];
-          v[4 * b + 2] = s0[2];
-          v[4 * b + 3] = s0[3];
-        }
-      }
-#pragma unroll
-      for (int b = 0; b < B; ++b) {
-        const int pp = p0 + b * NT;
-        if (pp < (M >> 2)) {
-          const double re[4] = {v[4 * b].x, v[4 * b].y, v[4 * b + 1].x, v[4 * b + 1].y};
-          const double im[4] = {v[4 * b + 2].x, v[4 * b + 2].y, v[4 * b + 3].x, v[4 * b + 3].y};
-#pragma unroll
-          for (int w = 0; w < 4; ++w) {
-            const int k = 4 * pp + w + 1;
-            if (k < M) sm[phys(k)] = make_double2(re[w], has2 ? im[w] : 0.0);
-          }
+    for (int b = 0; b < LB; ++b) {
+      const int k = k0 + b * NT;
+      v[b] = make_double2(0.0, 0.0);
+      if (k >= 1 && k < M) {
+        const int kk = k - 1;
+        if (!CPLX) {
+          const double *s0 = static_cast<const double *>(a.panels) +
+                             ((size_t)(kk >> 2) * M + r) * 4 + (kk & 3);
+          v[b].x = s0[0];
+          if (has2) v[b].y = s0[4];
+        } else {
+          v[b] = static_cast<const double2 *>(a.panels)[((size_t)(kk >> 1) * M + r) * 2 + (kk & 1)];
         }
       }
     }
-  } else {
-    const double2 *P = static_cast<const double2 *>(a.panels);
-    constexpr int B = LB / 2;
-    for (int p0 = tid; p0 < (M >> 1); p0 += NT * B) {
-      double2 v[2 * B];
 #pragma unroll
-      for (int b = 0; b < B; ++b) {
-        const int pp = p0 + b * NT;
-        if (pp < (M >> 1)) {
-          const double2 *s0 = P + ((size_t)pp * M + r) * 2;
-          v[2 * b] = s0[0];
-          v[2 * b + 1] = s0[1];
-        }
-      }
-#pragma unroll
-      for (int b = 0; b < B; ++b) {
-        const int pp = p0 + b * NT;
-        if (pp < (M >> 1)) {
-          const int k = 2 * pp + 1;
-          sm[phys(k)] = v[2 * b];
-          if (k + 1 < M) sm[phys(k + 1)] = v[2 * b + 1];
-        }
-      }
+    for (int b = 0; b < LB; ++b) {
+      const int k = k0 + b * NT;
+      if (k >= 1 && k < M) sm[phys(k)] = v[b];
     }
   }
   __syncthreads();

@@ -96,17 +96,19 @@ KFBI_DEV void fft_task(double2 *s, int base, int j, int s0, int logN, const Twid
   constexpr int E = 1 << R;
   const int hs = 1 << s0;
   const int a = logN - s0;
+  // one table lookup per task: w_{u-1} = w_u^2 (two extra roundings at most)
   double2 w[R][E / 2];
   {
-    const double2 w0 = tw(j << a);
+    const double2 wtop = tw(j << (a - (R - 1)));
+    const double2 w1 = (R > 2) ? cmul(wtop, wtop) : wtop;
+    const double2 w0 = (R > 1) ? cmul(w1, w1) : wtop;
     w[0][0] = w0;
     if (R > 1) {
-      const double2 w1 = tw(j << (a - 1));
       w[(R > 1) ? 1 : 0][0] = w1;
       w[(R > 1) ? 1 : 0][1] = mul_negi(w1);
     }
     if (R > 2) {
-      const double2 w2 = tw(j << (a - 2));
+      const double2 w2 = wtop;
       const double2 w2b = mul_w8(w2);
       w[R - 1][0] = w2;
       w[R - 1][1] = w2b;
@@ -191,70 +193,60 @@ KFBI_DEV void fft_all(double2 *s, int logN, const Twiddle &tw, int tid, int nthr
   }
 }
 
-// ---- phase C: Makhoul post-twiddle, pairs (k, L-k) of every block ----
-//   forward: G_{L-k} = w_k V_k + conj(w_k) V_{L-k};  G_k = w_{L-k} V_{L-k} + conj(w_{L-k}) V_k
-//   adjoint: the conjugate transpose of that 2x2 map.
-// w_k = exp(-i pi k / (2L)), w_{L-k} = -i conj(w_k); G_j is stored at
-// L + (j mod L), i.e. in the slots the pair was read from.  k = 0, k = L/2
-// and the L = 1 block scale by real factors (2, sqrt 2, 2) in both directions.
+// ---- phases C + D fused: per level L (small to large), Makhoul post-twiddle
+// of block L, then the combine with the lower levels ----
+// Region [1, 2L): D_k = C^(l+1)_k at position k (k < L); block L holds V_j at
+// L + j.  For the pair (k, L-k), 0 < k < L/2, with w_k = exp(-i pi k / (2L))
+// and w_{L-k} = -i conj(w_k):
+//   G_{L-k} = w_k V_k + conj(w_k) V_{L-k},  G_k = w_{L-k} V_{L-k} + conj(w_{L-k}) V_k
+//   C_k = D_k + G_k,  C_{2L-k} = G_k - D_k,  C_{L-k} = D_{L-k} + G_{L-k},
+//   C_{L+k} = G_{L-k} - D_{L-k}
+// (the Makhoul pair is exactly the G half of the combine quad, so both phases
+// run in place on the same four slots).  k = L/2 is self-paired
+// (G = sqrt2 V_{L/2}); C_L = G_L = 2 V_0; the L = 1 block enters level 2 as
+// D_1 = 2 V_0.  The adjoint runs the conjugate-transposed steps in reverse.
 template <bool ADJ>
-KFBI_DEV void post_pass(double2 *s, int logN, const Twiddle &tw, int tid, int nthreads) {
-  const int N = 1 << logN;
-  for (int t = tid; t < (N >> 1) - 1; t += nthreads) {
-    const int r = (N >> 1) - t;                        // in (L/2, L]
-    const int logL = 32 - __clz(r - 1);
-    const int L = 1 << logL;
-    const int k = L - r;                               // 0 .. L/2-1
-    if (k == 0) {
-      const int p0 = phys(L);
-      s[p0] = cscale(s[p0], 2.0);
-      const int ph = phys(L + (L >> 1));
-      s[ph] = cscale(s[ph], 2.0 * SQRT_HALF);
-      continue;
-    }
-    const int pa = phys(L + k), pb = phys(2 * L - k);
-    const double2 a = s[pa], b = s[pb];
-    const double2 wk = tw(k << (logN - 1 - logL));
-    const double2 wm = make_double2(-wk.y, -wk.x);     // -i conj(w_k)
-    if (!ADJ) {
-      s[pb] = cadd(cmul(wk, a), cmul(cconj(wk), b));   // G_{L-k}
-      s[pa] = cadd(cmul(wm, b), cmul(cconj(wm), a));   // G_k
-    } else {
-      s[pa] = cadd(cmul(wm, a), cmul(cconj(wk), b));
-      s[pb] = cadd(cmul(cconj(wm), a), cmul(wk, b));
-    }
-  }
-  if (tid == 0) {
-    const int p1 = phys(1);
-    s[p1] = cscale(s[p1], 2.0);
-  }
-}
-
-// ---- phase D: level combine, region [1, 2L): D_k at k, G_k at L + (k mod L) ----
-//   forward: C_k = D_k + G_k, C_{2L-k} = G_k - D_k (pairs (k, L-k), in place)
-template <bool ADJ>
-KFBI_DEV void combine_level(double2 *s, int L, int tid, int nthreads) {
+KFBI_DEV void level_pass(double2 *s, int L, int logN, const Twiddle &tw, int tid, int nthreads) {
   const int half = L >> 1;
+  const int sh = logN - 1 - (31 - __clz(L));
   for (int k = 1 + tid; k <= half; k += nthreads) {
     const int pd = phys(k), pg = phys(L + k);
-    const double2 a = s[pd], b = s[pg];
     if (k == half) {
-      if (!ADJ) { s[pd] = cadd(a, b); s[pg] = csub(b, a); }
-      else      { s[pd] = csub(a, b); s[pg] = cadd(a, b); }
+      const int p0 = phys(L);
+      s[p0] = cscale(s[p0], 2.0);
+      const double dscale = (L == 2) ? 2.0 : 1.0;
+      if (!ADJ) {
+        const double2 d = cscale(s[pd], dscale);
+        const double2 g = cscale(s[pg], 2.0 * SQRT_HALF);
+        s[pd] = cadd(d, g);
+        s[pg] = csub(g, d);
+      } else {
+        const double2 x = s[pd], y = s[pg];
+        s[pd] = cscale(csub(x, y), dscale);
+        s[pg] = cscale(cadd(x, y), 2.0 * SQRT_HALF);
+      }
       continue;
     }
     const int pdm = phys(L - k), pgm = phys(2 * L - k);
-    const double2 c = s[pdm], d = s[pgm];
+    const double2 wk = tw(k << sh);
+    const double2 wm = make_double2(-wk.y, -wk.x);     // -i conj(w_k)
     if (!ADJ) {
-      s[pd] = cadd(a, b);            // C_k
-      s[pgm] = csub(b, a);           // C_{2L-k}
-      s[pdm] = cadd(c, d);           // C_{L-k}
-      s[pg] = csub(d, c);            // C_{L+k}
+      const double2 a = s[pg], b = s[pgm];               // V_k, V_{L-k}
+      const double2 gk = cadd(cmul(wm, b), cmul(cconj(wm), a));
+      const double2 glk = cadd(cmul(wk, a), cmul(cconj(wk), b));
+      const double2 dk = s[pd], dlk = s[pdm];
+      s[pd] = cadd(dk, gk);                              // C_k
+      s[pgm] = csub(gk, dk);                             // C_{2L-k}
+      s[pdm] = cadd(dlk, glk);                           // C_{L-k}
+      s[pg] = csub(glk, dlk);                            // C_{L+k}
     } else {
-      s[pd] = csub(a, d);
-      s[pg] = cadd(a, d);
-      s[pdm] = csub(c, b);
-      s[pgm] = cadd(b, c);
+      const double2 xk = s[pd], xlk = s[pg], xmk = s[pdm], x2k = s[pgm];
+      const double2 a = cadd(xk, x2k);                   // G^H_k
+      const double2 b = cadd(xlk, xmk);                  // G^H_{L-k}
+      s[pd] = csub(xk, x2k);
+      s[pdm] = csub(xmk, xlk);
+      s[pg] = cadd(cmul(wm, a), cmul(cconj(wk), b));
+      s[pgm] = cadd(cmul(cconj(wm), a), cmul(wk, b));
     }
   }
 }
@@ -276,17 +268,15 @@ KFBI_DEV void dst1_forward(double2 *s0, int nseq, int logN, const Twiddle &tw, i
   const bool active = q < nseq;
   double2 *s = s0 + (size_t)(active ? q : 0) * N;
   fft_all<false>(s, logN, tw, lt, per, active);
-  if (active) post_pass<false>(s, logN, tw, lt, per);
-  __syncthreads();
   if (active && lt < 32) {
     for (int L = 2; L < N && L < WARP_LEVELS_END; L <<= 1) {
-      combine_level<false>(s, L, lt, 32);
+      level_pass<false>(s, L, logN, tw, lt, 32);
       __syncwarp();
     }
   }
   __syncthreads();
   for (int L = WARP_LEVELS_END; L < N; L <<= 1) {
-    if (active) combine_level<false>(s, L, lt, per);
+    if (active) level_pass<false>(s, L, logN, tw, lt, per);
     __syncthreads();
   }
 }
@@ -300,18 +290,16 @@ KFBI_DEV void dst1_adjoint(double2 *s0, int nseq, int logN, const Twiddle &tw, i
   const bool active = q < nseq;
   double2 *s = s0 + (size_t)(active ? q : 0) * N;
   for (int L = N >> 1; L >= WARP_LEVELS_END; L >>= 1) {
-    if (active) combine_level<true>(s, L, lt, per);
+    if (active) level_pass<true>(s, L, logN, tw, lt, per);
     __syncthreads();
   }
   if (active && lt < 32) {
     for (int L = (N >> 1) < (WARP_LEVELS_END >> 1) ? (N >> 1) : (WARP_LEVELS_END >> 1); L >= 2;
          L >>= 1) {
-      combine_level<true>(s, L, lt, 32);
+      level_pass<true>(s, L, logN, tw, lt, 32);
       __syncwarp();
     }
   }
-  __syncthreads();
-  if (active) post_pass<true>(s, logN, tw, lt, per);
   __syncthreads();
   fft_all<true>(s, logN, tw, lt, per, active);
 }

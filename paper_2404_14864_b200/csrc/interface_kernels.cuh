@@ -143,14 +143,25 @@ corr_edges_kernel(EdgeArgs ea, const T *__restrict__ jm, T *jv, const int *done)
   T acc[EW][3];
 #pragma unroll
   for (int q = 0; q < EW; ++q) acc[q][0] = acc[q][1] = acc[q][2] = S::zero();
-  for (int i = lane; i < n; i += 32) {
-    const T a0 = ju[i], ax = jx[i], ay = jy[i], axx = jxx[i], ayy = jyy[i];
+  // 16-byte W loads (rows padded to an even length with zeros), two pairs of
+  // control points per lane per iteration: 2*EW streaming loads in flight
+  const int n2 = ea.ld >> 1;
+#pragma unroll 2
+  for (int i2 = lane; i2 < n2; i2 += 32) {
+    double2 w2[EW];
 #pragma unroll
-    for (int q = 0; q < EW; ++q) {
-      const double w = __ldcs(wr[q] + i);
-      acc[q][0] = S::add(acc[q][0], S::rmul(a0, w));
-      acc[q][1] = S::add(acc[q][1], S::rmul(vert[q] ? ay : ax, w));
-      acc[q][2] = S::add(acc[q][2], S::rmul(vert[q] ? ayy : axx, w));
+    for (int q = 0; q < EW; ++q) w2[q] = __ldcs(reinterpret_cast<const double2 *>(wr[q]) + i2);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int i = min(2 * i2 + h, n - 1);
+      const T a0 = ju[i], ax = jx[i], ay = jy[i], axx = jxx[i], ayy = jyy[i];
+#pragma unroll
+      for (int q = 0; q < EW; ++q) {
+        const double w = h ? w2[q].y : w2[q].x;
+        acc[q][0] = S::add(acc[q][0], S::rmul(a0, w));
+        acc[q][1] = S::add(acc[q][1], S::rmul(vert[q] ? ay : ax, w));
+        acc[q][2] = S::add(acc[q][2], S::rmul(vert[q] ? ayy : axx, w));
+      }
     }
   }
 #pragma unroll
@@ -340,6 +351,52 @@ op_update_kernel(int n, const T *__restrict__ g, const T *__restrict__ trace, T 
     T upd = S::rmul(S::sub(g[p], trace[p]), gamma);
     phi_prev[p] = ph;
     phi[p] = S::add(ph, upd);
+    mag = S::abs(upd);
+  }
+  sweep_close(mag, st, history);
+}
+
+// One whole operator sweep in one launch.  A warp owns RW rows q:
+//   trace_q = trace1_q + sum_p T[q][p] (phi_in[p] - phi0[p])
+//   upd_q   = gamma (g_q - trace_q);  phi_out[q] = phi_in[q] + upd_q
+// A row's update needs only its own trace, so the densities ping-pong
+// between two buffers (phi_in is read-only during the sweep).
+template <typename T, int RW>
+__global__ void __launch_bounds__(256)
+op_sweep_kernel(int n, const T *__restrict__ Top, const T *__restrict__ phi_in,
+                const T *__restrict__ phi0, const T *__restrict__ trace1,
+                const T *__restrict__ g, T *__restrict__ phi_out, double gamma, RichState *st,
+                double *history) {
+  using S = Sc<T>;
+  if (st->done) return;
+  const int lane = threadIdx.x & 31;
+  const int q0 = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * RW;
+  T acc[RW];
+#pragma unroll
+  for (int r = 0; r < RW; ++r) acc[r] = S::zero();
+  if (q0 < n) {
+    const T *rows[RW];
+#pragma unroll
+    for (int r = 0; r < RW; ++r) rows[r] = Top + (size_t)min(q0 + r, n - 1) * n;
+#pragma unroll 8
+    for (int p = lane; p < n; p += 32) {
+      const T d = S::sub(phi_in[p], phi0[p]);
+#pragma unroll
+      for (int r = 0; r < RW; ++r) acc[r] = S::add(acc[r], S::mul(__ldcg(rows[r] + p), d));
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < RW; ++r) acc[r] = warp_reduce_T(acc[r]);
+  double mag = 0.0;
+  if (lane < RW && q0 + lane < n) {
+    const int q = q0 + lane;
+    T a = acc[0];
+#pragma unroll
+    for (int r = 1; r < RW; ++r)
+      if (lane == r) a = acc[r];
+    const T trace = S::add(trace1[q], a);
+    const T upd = S::rmul(S::sub(g[q], trace), gamma);
+    phi_out[q] = S::add(phi_in[q], upd);
     mag = S::abs(upd);
   }
   sweep_close(mag, st, history);

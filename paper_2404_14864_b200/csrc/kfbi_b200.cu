@@ -230,7 +230,7 @@ kfbi_status set_smem_limits(kfbi_plan *p) {
   // The attribute is per kernel (process wide), not per plan: allow the
   // largest size any plan can need so plans of different M coexist.
   (void)p;
-  const int row = (int)box_smem_bytes(4096, 1), col = (int)box_smem_bytes(4096, 2);
+  const int row = (int)box_smem_bytes(4096, 1), col = (int)box_smem_bytes(4096, 1);
   KFBI_CUDA(cudaFuncSetAttribute(rows_fwd_kernel<CPLX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  row), "transform-rows");
   KFBI_CUDA(cudaFuncSetAttribute(rows_inv_kernel<CPLX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -250,14 +250,14 @@ kfbi_status box_passes(kfbi_plan *p, double kre, double kim, const void *rhs, do
   const int M = p->m;
   const int ntask = CPLX ? M - 1 : M / 2;
   const int npanel = CPLX ? M / 2 : M / 4;
-  const size_t row = box_smem_bytes(M, 1), col = box_smem_bytes(M, 2);
+  const size_t row = box_smem_bytes(M, 1), col = box_smem_bytes(M, 1);
   CorrArgs<T> c = corr_args<T>(p, static_cast<const T *>(jv));
   if (!jv) c.jv = nullptr;
   KFBI_TRY(launch(p, KFBI_K_ROWS, s, [&] {
     rows_fwd_kernel<CPLX><<<ntask, 256, row, s>>>(a, rhs, sign, c);
   }));
   KFBI_TRY(launch(p, KFBI_K_COLS, s, [&] {
-    cols_kernel<CPLX><<<npanel, 512, col, s>>>(a);
+    cols_kernel<CPLX><<<2 * npanel, 256, col, s>>>(a);
   }));
   KFBI_TRY(launch(p, KFBI_K_ROWS, s, [&] {
     rows_inv_kernel<CPLX><<<ntask, 256, row, s>>>(a, u);
@@ -402,32 +402,29 @@ kfbi_status build_operator_T(kfbi_plan *p, double kre, double kim, cudaStream_t 
 
 // Operator sweeps k >= 2 (trace = trace_1 + T (phi - phi_0), then the update).
 template <typename T>
-kfbi_status op_sweep(kfbi_plan *p, const kfbi_bvp *b, cudaStream_t s) {
+kfbi_status op_sweep(kfbi_plan *p, const kfbi_bvp *b, int idx, cudaStream_t s) {
+  // sweep idx >= 1 (0-based) reads phi_(idx) and writes phi_(idx+1); the
+  // densities alternate between b->density (even idx reads it) and phi_prev
+  constexpr int RW = 1;
   const int n = p->n_ctl;
-  const int *done = &p->st.p->done;
-  const int wb = (n * 32 + 255) / 256, eb = (n + 255) / 256;
-  T *trace = reinterpret_cast<T *>(p->trace_tmp.p);
-  KFBI_TRY(launch(p, KFBI_K_EXTRACT, s, [&] {
-    op_trace_kernel<T><<<wb, 256, 0, s>>>(n, reinterpret_cast<const T *>(p->Top.p),
-                                          static_cast<const T *>(b->density),
-                                          reinterpret_cast<const T *>(p->phi0.p),
-                                          reinterpret_cast<const T *>(p->trace1.p), trace, done);
-  }));
+  T *A = static_cast<T *>(b->density), *B = reinterpret_cast<T *>(p->phi_prev.p);
+  T *in = (idx & 1) ? A : B, *out = (idx & 1) ? B : A;
+  const int warps = (n + RW - 1) / RW;
   return launch(p, KFBI_K_DENSITY, s, [&] {
-    op_update_kernel<T><<<eb, 256, 0, s>>>(n, static_cast<const T *>(b->g), trace,
-                                           static_cast<T *>(b->density),
-                                           reinterpret_cast<T *>(p->phi_prev.p), b->gamma,
-                                           p->st.p, p->history.p);
+    op_sweep_kernel<T, RW><<<(warps * 32 + 255) / 256, 256, 0, s>>>(
+        n, reinterpret_cast<const T *>(p->Top.p), in, reinterpret_cast<const T *>(p->phi0.p),
+        reinterpret_cast<const T *>(p->trace1.p), static_cast<const T *>(b->g), out, b->gamma,
+        p->st.p, p->history.p);
   });
 }
 
 // Full pipeline from the density before the converging update: the field and
 // traces the reference returns (bvp.py:319-323, 336-344).
 template <typename T>
-kfbi_status final_pipeline(kfbi_plan *p, const kfbi_bvp *b, cudaStream_t s) {
+kfbi_status final_pipeline(kfbi_plan *p, const kfbi_bvp *b, const void *phi_before, cudaStream_t s) {
   constexpr bool CPLX = std::is_same<T, double2>::value;
   const int n = p->n_ctl;
-  KFBI_TRY(jumps_T<T>(p, b->kappa_re, b->kappa_im, p->phi_prev.p, nullptr, b->f_gamma,
+  KFBI_TRY(jumps_T<T>(p, b->kappa_re, b->kappa_im, phi_before, nullptr, b->f_gamma,
                       b->f_gamma_sign, p->jm.p, nullptr, s));
   KFBI_TRY(edges_T<T>(p, p->jm.p, p->jv.p, nullptr, s));
   KFBI_TRY(box_passes<CPLX>(p, b->kappa_re, b->kappa_im, b->F, b->F_sign, p->jv.p, b->u, nullptr, s));
@@ -672,8 +669,8 @@ kfbi_status kfbi_richardson(kfbi_plan *p, const kfbi_bvp *b, kfbi_bvp_result *re
           KFBI_CUDA(cudaMemcpyAsync(p->trace1.p, b->trace_u, p->n_ctl * es, cudaMemcpyDeviceToDevice, s),
                     "density-update");
       } else {
-        if (cplx) KFBI_TRY(op_sweep<double2>(p, b, s));
-        else KFBI_TRY(op_sweep<double>(p, b, s));
+        if (cplx) KFBI_TRY(op_sweep<double2>(p, b, idx, s));
+        else KFBI_TRY(op_sweep<double>(p, b, idx, s));
       }
     }
     enqueued += nb;
@@ -683,9 +680,19 @@ kfbi_status kfbi_richardson(kfbi_plan *p, const kfbi_bvp *b, kfbi_bvp_result *re
     if (p->st_host->done != 0 || enqueued >= b->max_iter) break;
     batch = use_op ? 8 : 2;
   }
-  if (use_op && p->st_host->done == 1 && p->st_host->iters >= 2) {
-    if (cplx) KFBI_TRY(final_pipeline<double2>(p, b, s));
-    else KFBI_TRY(final_pipeline<double>(p, b, s));
+  if (use_op && p->st_host->iters >= 2) {
+    // after K sweeps: phi_K sits in density when K is odd, in phi_prev when
+    // K is even (op_sweep ping-pong); phi_(K-1) in the other buffer
+    const int K = p->st_host->iters;
+    void *phiK = (K & 1) ? b->density : (void *)p->phi_prev.p;
+    void *phiK1 = (K & 1) ? (void *)p->phi_prev.p : b->density;
+    if (p->st_host->done == 1) {
+      if (cplx) KFBI_TRY(final_pipeline<double2>(p, b, phiK1, s));
+      else KFBI_TRY(final_pipeline<double>(p, b, phiK1, s));
+    }
+    if (phiK != b->density)
+      KFBI_CUDA(cudaMemcpyAsync(b->density, phiK, p->n_ctl * es, cudaMemcpyDeviceToDevice, s),
+                "density-update");
   }
   const RichState &h = *p->st_host;
   res->iterations = h.iters;
