@@ -10,6 +10,8 @@
 //                         closes the sweep (history, convergence flag)
 #pragma once
 
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 
 namespace kfbi {
@@ -400,6 +402,76 @@ op_sweep_kernel(int n, const T *__restrict__ Top, const T *__restrict__ phi_in,
     mag = S::abs(upd);
   }
   sweep_close(mag, st, history);
+}
+
+// All operator sweeps of one solve in ONE cooperative launch.  Sweep idx
+// (0-based, idx >= 1) reads phi_idx from A (idx odd) or B (idx even) and
+// writes phi_(idx+1) to the other buffer; warps stride over the rows.  The
+// sweep's max |update| goes to slot idx % 3 (block 0 clears slot
+// (idx+1) % 3, last read two sweeps ago), one grid barrier, then every CTA
+// reads the same max and takes the same decision (bvp.py:333-344).
+struct OpSolveArgs {
+  int n, first_idx, max_iter;
+  double gamma, tol;
+  RichState *st;
+  double *history;
+  unsigned long long *slots;      // [3]
+};
+
+template <typename T>
+__global__ void __launch_bounds__(256)
+op_solve_kernel(OpSolveArgs a, const T *__restrict__ Top, T *A, T *B,
+                const T *__restrict__ phi0, const T *__restrict__ trace1,
+                const T *__restrict__ g) {
+  using S = Sc<T>;
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double red[8];
+  if (a.st->done) return;                       // uniform: set before launch
+  const int n = a.n;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int idx = a.first_idx; idx < a.max_iter; ++idx) {
+    const T *in = (idx & 1) ? A : B;
+    T *out = (idx & 1) ? B : A;
+    double mag = 0.0;
+    for (int q = gwarp; q < n; q += nwarps) {
+      const T *row = Top + (size_t)q * n;
+      T acc = S::zero();
+#pragma unroll 8
+      for (int p = lane; p < n; p += 32)
+        acc = S::add(acc, S::mul(__ldcg(row + p), S::sub(in[p], phi0[p])));
+      acc = warp_reduce_T(acc);
+      if (lane == 0) {
+        const T trace = S::add(trace1[q], acc);
+        const T upd = S::rmul(S::sub(g[q], trace), a.gamma);
+        out[q] = S::add(in[q], upd);
+        mag = nanmax(mag, S::abs(upd));
+      }
+    }
+    mag = warp_nanmax(mag);
+    if (lane == 0) red[wid] = mag;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double m = red[0];
+      for (int w = 1; w < (int)(blockDim.x >> 5); ++w) m = nanmax(m, red[w]);
+      atomic_max_nonneg(&a.slots[idx % 3], m);
+      if (blockIdx.x == 0) a.slots[(idx + 1) % 3] = 0ull;
+    }
+    grid.sync();
+    const double res = __longlong_as_double((long long)atomicAdd(&a.slots[idx % 3], 0ull));
+    const bool conv = res <= a.tol;
+    const bool last = conv || idx + 1 >= a.max_iter;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      a.history[idx] = res;
+      a.st->iters = idx + 1;
+      a.st->last_res = res;
+      if (conv) a.st->done = 1;
+      else if (idx + 1 >= a.max_iter) a.st->done = 2;
+    }
+    if (last) break;
+  }
 }
 
 // Extraction writing the BvpSolution traces (u+, d_n u+) of a final field.

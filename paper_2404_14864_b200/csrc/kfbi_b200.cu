@@ -418,6 +418,41 @@ kfbi_status op_sweep(kfbi_plan *p, const kfbi_bvp *b, int idx, cudaStream_t s) {
   });
 }
 
+// All operator sweeps of one solve: one cooperative launch (op_solve_kernel).
+template <typename T>
+kfbi_status op_solve(kfbi_plan *p, const kfbi_bvp *b, cudaStream_t s) {
+  static int blocks_per_sm[2] = {0, 0};
+  constexpr int CP = std::is_same<T, double2>::value ? 1 : 0;
+  if (!blocks_per_sm[CP]) {
+    int nb = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, op_solve_kernel<T>, 256, 0);
+    blocks_per_sm[CP] = nb < 1 ? 1 : (nb > 4 ? 4 : nb);
+  }
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->device);
+  unsigned long long *slots = p->red.p + 4;
+  KFBI_CUDA(cudaMemsetAsync(slots, 0, 3 * sizeof(unsigned long long), s), "density-update");
+  OpSolveArgs a;
+  a.n = p->n_ctl;
+  a.first_idx = 1;
+  a.max_iter = b->max_iter;
+  a.gamma = b->gamma;
+  a.tol = b->tol;
+  a.st = p->st.p;
+  a.history = p->history.p;
+  a.slots = slots;
+  const T *Top = reinterpret_cast<const T *>(p->Top.p);
+  T *A = static_cast<T *>(b->density), *B = reinterpret_cast<T *>(p->phi_prev.p);
+  const T *phi0 = reinterpret_cast<const T *>(p->phi0.p);
+  const T *tr1 = reinterpret_cast<const T *>(p->trace1.p);
+  const T *g = static_cast<const T *>(b->g);
+  void *args[] = {&a, (void *)&Top, &A, &B, (void *)&phi0, (void *)&tr1, (void *)&g};
+  return launch(p, KFBI_K_DENSITY, s, [&] {
+    cudaLaunchCooperativeKernel((const void *)op_solve_kernel<T>, dim3(sms * blocks_per_sm[CP]),
+                                dim3(256), args, 0, s);
+  });
+}
+
 // Full pipeline from the density before the converging update: the field and
 // traces the reference returns (bvp.py:319-323, 336-344).
 template <typename T>
@@ -479,7 +514,7 @@ kfbi_status kfbi_plan_create(const kfbi_grid_desc *desc, kfbi_plan **out) {
   if ((e = upload(p->tw, tw.data(), tw.size())) != cudaSuccess ||
       (e = upload(p->lam, lam.data(), lam.size())) != cudaSuccess ||
       (e = p->panels.ensure((size_t)m * m)) != cudaSuccess ||
-      (e = p->st.ensure(1)) != cudaSuccess || (e = p->red.ensure(4)) != cudaSuccess) {
+      (e = p->st.ensure(1)) != cudaSuccess || (e = p->red.ensure(8)) != cudaSuccess) {
     kfbi_plan_destroy(p);
     return fail(KFBI_E_CUDA, std::string("plan allocation: ") + cudaGetErrorString(e));
   }
@@ -655,30 +690,46 @@ kfbi_status kfbi_richardson(kfbi_plan *p, const kfbi_bvp *b, kfbi_bvp_result *re
   if (use_op)
     KFBI_CUDA(cudaMemcpyAsync(p->phi0.p, b->density, p->n_ctl * es, cudaMemcpyDeviceToDevice, s),
               "density-update");
-  int enqueued = 0;
-  int batch = b->sweeps_hint > 0 ? b->sweeps_hint : 4;
-  for (;;) {
-    int nb = batch;
-    if (nb > b->max_iter - enqueued) nb = b->max_iter - enqueued;
-    for (int k = 0; k < nb; ++k) {
-      const int idx = enqueued + k;      // 0-based sweep index
-      if (idx == 0 || !use_op) {
-        if (cplx) KFBI_TRY(sweep<double2>(p, b, s));
-        else KFBI_TRY(sweep<double>(p, b, s));
-        if (idx == 0 && use_op)
-          KFBI_CUDA(cudaMemcpyAsync(p->trace1.p, b->trace_u, p->n_ctl * es, cudaMemcpyDeviceToDevice, s),
-                    "density-update");
-      } else {
-        if (cplx) KFBI_TRY(op_sweep<double2>(p, b, idx, s));
-        else KFBI_TRY(op_sweep<double>(p, b, idx, s));
-      }
+  if (use_op) {
+    // sweep 1 through the pipeline, then every further sweep inside one
+    // cooperative launch; a single host sync per solve
+    if (cplx) KFBI_TRY(sweep<double2>(p, b, s));
+    else KFBI_TRY(sweep<double>(p, b, s));
+    KFBI_CUDA(cudaMemcpyAsync(p->trace1.p, b->trace_u, p->n_ctl * es, cudaMemcpyDeviceToDevice, s),
+              "density-update");
+    if (b->max_iter > 1) {
+      if (cplx) KFBI_TRY(op_solve<double2>(p, b, s));
+      else KFBI_TRY(op_solve<double>(p, b, s));
     }
-    enqueued += nb;
     KFBI_CUDA(cudaMemcpyAsync(p->st_host, p->st.p, sizeof(RichState), cudaMemcpyDeviceToHost, s),
               "density-update");
     KFBI_CUDA(cudaStreamSynchronize(s), "density-update");
-    if (p->st_host->done != 0 || enqueued >= b->max_iter) break;
-    batch = use_op ? 8 : 2;
+  } else {
+    int enqueued = 0;
+    int batch = b->sweeps_hint > 0 ? b->sweeps_hint : 4;
+    for (;;) {
+      int nb = batch;
+      if (nb > b->max_iter - enqueued) nb = b->max_iter - enqueued;
+      for (int k = 0; k < nb; ++k) {
+        const int idx = enqueued + k;      // 0-based sweep index
+        if (idx == 0 || !use_op) {
+          if (cplx) KFBI_TRY(sweep<double2>(p, b, s));
+          else KFBI_TRY(sweep<double>(p, b, s));
+          if (idx == 0 && use_op)
+            KFBI_CUDA(cudaMemcpyAsync(p->trace1.p, b->trace_u, p->n_ctl * es, cudaMemcpyDeviceToDevice, s),
+                      "density-update");
+        } else {
+          if (cplx) KFBI_TRY(op_sweep<double2>(p, b, idx, s));
+          else KFBI_TRY(op_sweep<double>(p, b, idx, s));
+        }
+      }
+      enqueued += nb;
+      KFBI_CUDA(cudaMemcpyAsync(p->st_host, p->st.p, sizeof(RichState), cudaMemcpyDeviceToHost, s),
+                "density-update");
+      KFBI_CUDA(cudaStreamSynchronize(s), "density-update");
+      if (p->st_host->done != 0 || enqueued >= b->max_iter) break;
+      batch = use_op ? 8 : 2;
+    }
   }
   if (use_op && p->st_host->iters >= 2) {
     // after K sweeps: phi_K sits in density when K is odd, in phi_prev when
