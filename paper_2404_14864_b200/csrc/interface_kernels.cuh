@@ -460,7 +460,12 @@ op_solve_kernel(OpSolveArgs a, const T *__restrict__ Top, T *A, T *B,
       if (blockIdx.x == 0) a.slots[(idx + 1) % 3] = 0ull;
     }
     grid.sync();
-    const double res = __longlong_as_double((long long)atomicAdd(&a.slots[idx % 3], 0ull));
+    // one L2 read per block (an atomic per thread would serialise ~1e5
+    // operations on one address)
+    __shared__ double res_s;
+    if (threadIdx.x == 0) res_s = __longlong_as_double((long long)__ldcg(&a.slots[idx % 3]));
+    __syncthreads();
+    const double res = res_s;
     const bool conv = res <= a.tol;
     const bool last = conv || idx + 1 >= a.max_iter;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
