@@ -43,18 +43,66 @@ struct CtlGeom {
 template <typename T>
 KFBI_DEV T circ_deriv(const CtlGeom &g, const T *__restrict__ v, int i, int lane) {
   using S = Sc<T>;
-  T acc = S::zero();
-  for (int j = lane; j < g.n; j += 32) {
+  constexpr int U = 8;                // independent partial sums: U loads in flight
+  T acc[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) acc[u] = S::zero();
+  int j = lane;
+  for (; j + 32 * (U - 1) < g.n; j += 32 * U) {
+    T x[U];
+    double d[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      int idx = i - (j + 32 * u);
+      if (idx < 0) idx += g.n;
+      x[u] = v[j + 32 * u];
+      d[u] = __ldg(&g.deriv_col[idx]);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) acc[u] = S::add(acc[u], S::rmul(x[u], d[u]));
+  }
+  for (; j < g.n; j += 32) {
     int idx = i - j;
     if (idx < 0) idx += g.n;
-    acc = S::add(acc, S::rmul(v[j], __ldg(&g.deriv_col[idx])));
+    acc[0] = S::add(acc[0], S::rmul(v[j], __ldg(&g.deriv_col[idx])));
   }
-  return acc;
+#pragma unroll
+  for (int u = 1; u < U; ++u) acc[0] = S::add(acc[0], acc[u]);
+  return acc[0];
 }
+
+// Warp dot product  sum_p row[p] (x[p] - x0[p])  with U independent partial
+// sums (U streaming row loads in flight per lane); result in every lane.
+template <typename T, int U>
+KFBI_DEV T warp_row_dot(const T *__restrict__ row, const T *__restrict__ x,
+                        const T *__restrict__ x0, int n, int lane);
 
 KFBI_DEV double warp_reduce_T(double v) { return warp_sum(v); }
 KFBI_DEV double2 warp_reduce_T(double2 v) {
   return make_double2(warp_sum(v.x), warp_sum(v.y));
+}
+
+template <typename T, int U>
+KFBI_DEV T warp_row_dot(const T *__restrict__ row, const T *__restrict__ x,
+                        const T *__restrict__ x0, int n, int lane) {
+  using S = Sc<T>;
+  T acc[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) acc[u] = S::zero();
+  int p = lane;
+  for (; p + 32 * (U - 1) < n; p += 32 * U) {
+    T r[U], d[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) r[u] = __ldcg(row + p + 32 * u);
+#pragma unroll
+    for (int u = 0; u < U; ++u) d[u] = S::sub(x[p + 32 * u], x0[p + 32 * u]);
+#pragma unroll
+    for (int u = 0; u < U; ++u) acc[u] = S::add(acc[u], S::mul(r[u], d[u]));
+  }
+  for (; p < n; p += 32) acc[0] = S::add(acc[0], S::mul(__ldcg(row + p), S::sub(x[p], x0[p])));
+#pragma unroll
+  for (int u = 1; u < U; ++u) acc[0] = S::add(acc[0], acc[u]);
+  return warp_reduce_T(acc[0]);
 }
 
 // phi_s (and psi_s when psi != nullptr).
@@ -147,22 +195,34 @@ corr_edges_kernel(EdgeArgs ea, const T *__restrict__ jm, T *jv, const int *done)
   for (int q = 0; q < EW; ++q) acc[q][0] = acc[q][1] = acc[q][2] = S::zero();
   // 16-byte W loads (rows padded to an even length with zeros), two pairs of
   // control points per lane per iteration: 2*EW streaming loads in flight
+  // U iterations of EW rows are loaded before any is used: U*EW 16-byte
+  // streaming loads in flight per lane (the compiler does not hoist them
+  // across the FMA chains on its own).
+  constexpr int U = 4;
   const int n2 = ea.ld >> 1;
-#pragma unroll 2
-  for (int i2 = lane; i2 < n2; i2 += 32) {
-    double2 w2[EW];
+  for (int i0 = lane; i0 < n2; i0 += 32 * U) {
+    double2 w2[U][EW];
 #pragma unroll
-    for (int q = 0; q < EW; ++q) w2[q] = __ldcs(reinterpret_cast<const double2 *>(wr[q]) + i2);
+    for (int u = 0; u < U; ++u) {
+      const int i2 = i0 + 32 * u;
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int i = min(2 * i2 + h, n - 1);
-      const T a0 = ju[i], ax = jx[i], ay = jy[i], axx = jxx[i], ayy = jyy[i];
+      for (int q = 0; q < EW; ++q)
+        w2[u][q] = i2 < n2 ? __ldcs(reinterpret_cast<const double2 *>(wr[q]) + i2)
+                           : make_double2(0.0, 0.0);
+    }
 #pragma unroll
-      for (int q = 0; q < EW; ++q) {
-        const double w = h ? w2[q].y : w2[q].x;
-        acc[q][0] = S::add(acc[q][0], S::rmul(a0, w));
-        acc[q][1] = S::add(acc[q][1], S::rmul(vert[q] ? ay : ax, w));
-        acc[q][2] = S::add(acc[q][2], S::rmul(vert[q] ? ayy : axx, w));
+    for (int u = 0; u < U; ++u) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int i = min(2 * (i0 + 32 * u) + h, n - 1);
+        const T a0 = ju[i], ax = jx[i], ay = jy[i], axx = jxx[i], ayy = jyy[i];
+#pragma unroll
+        for (int q = 0; q < EW; ++q) {
+          const double w = h ? w2[u][q].y : w2[u][q].x;
+          acc[q][0] = S::add(acc[q][0], S::rmul(a0, w));
+          acc[q][1] = S::add(acc[q][1], S::rmul(vert[q] ? ay : ax, w));
+          acc[q][2] = S::add(acc[q][2], S::rmul(vert[q] ? ayy : axx, w));
+        }
       }
     }
   }
@@ -437,12 +497,7 @@ op_solve_kernel(OpSolveArgs a, const T *__restrict__ Top, T *A, T *B,
     T *out = (idx & 1) ? B : A;
     double mag = 0.0;
     for (int q = gwarp; q < n; q += nwarps) {
-      const T *row = Top + (size_t)q * n;
-      T acc = S::zero();
-#pragma unroll 8
-      for (int p = lane; p < n; p += 32)
-        acc = S::add(acc, S::mul(__ldcg(row + p), S::sub(in[p], phi0[p])));
-      acc = warp_reduce_T(acc);
+      const T acc = warp_row_dot<T, 8>(Top + (size_t)q * n, in, phi0, n, lane);
       if (lane == 0) {
         const T trace = S::add(trace1[q], acc);
         const T upd = S::rmul(S::sub(g[q], trace), a.gamma);
