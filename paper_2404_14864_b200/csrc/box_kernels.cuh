@@ -23,6 +23,7 @@
 namespace kfbi {
 
 constexpr int LB = 8;   // global loads in flight per thread in the load phases
+constexpr int DST_THREADS = 256;   // threads per DST CTA (one sequence; 3 CTAs / SM: 512 measured slower)
 
 struct BoxArgs {
   int m, logm;
@@ -88,7 +89,7 @@ inline size_t box_smem_bytes(int m, int nseq) {
 // ---------------------------------------------------------------------------
 // forward row pass: one task = rows (j0, j0+1) packed (real) or row j0 (complex)
 template <bool CPLX>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(DST_THREADS)
 rows_fwd_kernel(BoxArgs a, const void *__restrict__ rhs, double sign,
                 CorrArgs<typename std::conditional<CPLX, double2, double>::type> corr) {
   using T = typename std::conditional<CPLX, double2, double>::type;
@@ -176,7 +177,7 @@ rows_fwd_kernel(BoxArgs a, const void *__restrict__ rhs, double sign,
 // complex column); the two halves of a panel are adjacent CTAs, so each
 // 32-byte sector is read from DRAM once and served to the second CTA by L2.
 template <bool CPLX>
-__global__ void __launch_bounds__(256) cols_kernel(BoxArgs a) {
+__global__ void __launch_bounds__(DST_THREADS) cols_kernel(BoxArgs a) {
   extern __shared__ double2 sm[];
   if (a.done && *a.done) return;
   const int M = a.m, logN = a.logm, tid = threadIdx.x, NT = blockDim.x;
@@ -239,7 +240,7 @@ __global__ void __launch_bounds__(256) cols_kernel(BoxArgs a) {
 // ---------------------------------------------------------------------------
 // inverse row pass: panels -> DST(x) (adjoint engine, gather store) -> u rows
 template <bool CPLX>
-__global__ void __launch_bounds__(256) rows_inv_kernel(BoxArgs a, void *__restrict__ u) {
+__global__ void __launch_bounds__(DST_THREADS) rows_inv_kernel(BoxArgs a, void *__restrict__ u) {
   extern __shared__ double2 sm[];
   if (a.done && *a.done) return;
   const int M = a.m, logN = a.logm, tid = threadIdx.x, NT = blockDim.x;

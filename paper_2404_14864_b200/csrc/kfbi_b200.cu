@@ -254,13 +254,13 @@ kfbi_status box_passes(kfbi_plan *p, double kre, double kim, const void *rhs, do
   CorrArgs<T> c = corr_args<T>(p, static_cast<const T *>(jv));
   if (!jv) c.jv = nullptr;
   KFBI_TRY(launch(p, KFBI_K_ROWS, s, [&] {
-    rows_fwd_kernel<CPLX><<<ntask, 256, row, s>>>(a, rhs, sign, c);
+    rows_fwd_kernel<CPLX><<<ntask, DST_THREADS, row, s>>>(a, rhs, sign, c);
   }));
   KFBI_TRY(launch(p, KFBI_K_COLS, s, [&] {
-    cols_kernel<CPLX><<<2 * npanel, 256, col, s>>>(a);
+    cols_kernel<CPLX><<<2 * npanel, DST_THREADS, col, s>>>(a);
   }));
   KFBI_TRY(launch(p, KFBI_K_ROWS, s, [&] {
-    rows_inv_kernel<CPLX><<<ntask, 256, row, s>>>(a, u);
+    rows_inv_kernel<CPLX><<<ntask, DST_THREADS, row, s>>>(a, u);
   }));
   return KFBI_OK;
 }
