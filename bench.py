@@ -219,6 +219,8 @@ def run_ours(args):
         for eq in eqs:
             advance(eq)
     torch.cuda.synchronize()
+    for c in ctxs.values():
+        c.flush()
 
     plans = [c.plan for c in ctxs.values()]
     for p in plans:
@@ -241,11 +243,15 @@ def run_ours(args):
                 st = advance(eq)
                 b.record(stream)
                 ev[eq].append((a, b))
-                iters[eq].append(st.last_iterations)
+                if st.log_slot is None:
+                    iters[eq].append(st.last_iterations)
         end.record(stream)
         torch.cuda.synchronize()
     _barrier(ws)
     elapsed_ms = start.elapsed_time(end)
+    for eq in eqs:                 # asynchronous stepping: per-step log (+ error checks)
+        if ctxs[eq].asynchronous:
+            iters[eq] = ctxs[eq].flush()
     launches = sum(p.launch_count() for p in plans) - launches0
     per_eq_ms = {eq: sum(a.elapsed_time(b) for a, b in ev[eq]) / args.steps for eq in eqs}
 
@@ -259,6 +265,8 @@ def run_ours(args):
         for eq in eqs:
             advance(eq)
     torch.cuda.synchronize()
+    for c in ctxs.values():
+        c.flush()
     # per-kernel device times over the timed region
     kt_ms, kt_calls = {}, {}
     cols_bytes, cols_ms, cols_calls = 0.0, 0.0, 0
@@ -295,6 +303,8 @@ def run_ours(args):
             pinned[eq].copy_(st.u.reshape(-1), non_blocking=True)
     e2.record(stream)
     torch.cuda.synchronize()
+    for c in ctxs.values():
+        c.flush()
     _barrier(ws)
     e2e_ms = _max_over_ranks(s2.elapsed_time(e2), ws)
     e2e_value = n_time_steps * ws / (e2e_ms / 1e3)

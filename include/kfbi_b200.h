@@ -113,7 +113,19 @@ typedef struct {
   void *trace_u;          /* out [n_ctl]                                  */
   void *trace_un;         /* out [n_ctl]                                  */
   int32_t use_operator;   /* 1: sweeps >= 2 use the plan's trace operator */
+  int32_t log_slot;       /* >= 0 (operator form only): fully asynchronous;
+                             iterations / status land in the plan's step log
+                             (kfbi_log_fetch), result fields are -1 (pending) */
 } kfbi_bvp;
+
+/* One entry of the plan's device-side step log (asynchronous stepping). */
+typedef struct {
+  int32_t iterations;
+  int32_t status;         /* 1 converged, 2 max_iter reached */
+  double residual;        /* last density update max-norm */
+  double norm;            /* blow-up norm of the step (kfbi_log_norm, which=0) */
+  double newton;          /* worst pointwise Newton residual (which=1)      */
+} kfbi_step_log;
 
 typedef struct {
   int32_t iterations;
@@ -201,7 +213,9 @@ kfbi_status kfbi_schr_ustar(kfbi_plan *plan, int64_t n, int32_t mode,
 
 /* nonlinear_phase_step (timestepping.py:317-368) per node, then the mask
  * (timestepping.py:391) and, when F != NULL, F = kappa * out
- * (timestepping.py:395).  Returns KFBI_E_NOCONV when a node stalls. */
+ * (timestepping.py:395).  Returns KFBI_E_NOCONV when a node stalls; with
+ * max_res == NULL it does not wait and the caller logs the residual
+ * (kfbi_log_norm(..., which = 1)). */
 kfbi_status kfbi_nonlinear_phase(kfbi_plan *plan, int64_t n, const void *ustar,
                                  const double *v, double w, double half_tau,
                                  const uint8_t *mask, void *out, double kappa_re,
@@ -212,6 +226,13 @@ kfbi_status kfbi_nonlinear_phase(kfbi_plan *plan, int64_t n, const void *ustar,
 kfbi_status kfbi_mask_norm(kfbi_plan *plan, int32_t dtype, int64_t n,
                            const uint8_t *mask, void *u, double *norm_out,
                            void *stream);
+
+/* Step log of asynchronous stepping: capacity, the norm of the last
+ * *_rhs / mask_norm reduction into a slot, and a synchronous read-back. */
+kfbi_status kfbi_log_reserve(kfbi_plan *plan, int32_t count);
+kfbi_status kfbi_log_norm(kfbi_plan *plan, int32_t slot, int32_t which, void *stream);
+kfbi_status kfbi_log_fetch(kfbi_plan *plan, int32_t first, int32_t count,
+                           kfbi_step_log *out, void *stream);
 
 /* Per-kernel-name device time (ms) and call counts since the last reset
  * (Backend.timings / calls, engine.py:84-95).  Syncs the plan's events. */

@@ -59,7 +59,13 @@ class Bvp(C.Structure):
         ("g", vp), ("density", vp), ("gamma", f64), ("tol", f64),
         ("max_iter", i32), ("sweeps_hint", i32),
         ("u", vp), ("trace_u", vp), ("trace_un", vp), ("use_operator", i32),
+        ("log_slot", i32),
     ]
+
+
+class StepLog(C.Structure):
+    _fields_ = [("iterations", i32), ("status", i32), ("residual", f64), ("norm", f64),
+                ("newton", f64)]
 
 
 class BvpResult(C.Structure):
@@ -80,6 +86,9 @@ _SIGNATURES = {
     "kfbi_extract": ([vp, i32, vp, vp, vp, vp], i32),
     "kfbi_richardson": ([vp, C.POINTER(Bvp), C.POINTER(BvpResult), vp], i32),
     "kfbi_build_trace_operator": ([vp, i32, f64, f64, vp], i32),
+    "kfbi_log_reserve": ([vp, i32], i32),
+    "kfbi_log_norm": ([vp, i32, i32, vp], i32),
+    "kfbi_log_fetch": ([vp, i32, i32, vp, vp], i32),
     "kfbi_heat_rhs": ([vp, i64, vp, vp, vp, vp, f64, C.POINTER(f64), vp], i32),
     "kfbi_wave_rhs": ([vp, i64, vp, vp, vp, vp, vp, vp, f64, f64, C.POINTER(f64), vp], i32),
     "kfbi_schr_ustar": ([vp, i64, i32, vp, vp, f64, vp, vp], i32),

@@ -135,21 +135,39 @@ class Plan:
         self.operator_key = (k, bool(cplx))
 
     def richardson(self, *, kappa, F, F_sign, f_gamma, f_gamma_sign, g, density, gamma, tol,
-                   max_iter, u, trace_u, trace_un, sweeps_hint=0, use_operator=False):
+                   max_iter, u, trace_u, trace_un, sweeps_hint=0, use_operator=False,
+                   log_slot=-1):
         k = complex(kappa)
         b = N.Bvp(dtype=self._dt(u.is_complex()), kappa_re=k.real, kappa_im=k.imag,
                   F=F.data_ptr(), F_sign=float(F_sign), f_gamma=f_gamma.data_ptr(),
                   f_gamma_sign=float(f_gamma_sign), g=g.data_ptr(), density=density.data_ptr(),
                   gamma=float(gamma), tol=float(tol), max_iter=int(max_iter),
                   sweeps_hint=int(sweeps_hint), u=u.data_ptr(), trace_u=trace_u.data_ptr(),
-                  trace_un=trace_un.data_ptr(), use_operator=int(bool(use_operator)))
+                  trace_un=trace_un.data_ptr(), use_operator=int(bool(use_operator)),
+                  log_slot=int(log_slot))
         hist = np.zeros(max(int(max_iter), 1))
         res = N.BvpResult(history=hist.ctypes.data_as(C.POINTER(C.c_double)))
         status = self._lib.kfbi_richardson(self.handle, C.byref(b), C.byref(res), self.stream)
+        if log_slot >= 0:                       # asynchronous: results pending in the log
+            N.check(status)
+            return None, None, None
         history = hist[: res.iterations].tolist()
         last = history[-1] if history else None
         N.check(status, iterations=int(max_iter), last_residual=last)
         return res.iterations, res.residual, history
+
+    # -- asynchronous step log ----------------------------------------------
+    def log_reserve(self, count):
+        N.check(self._lib.kfbi_log_reserve(self.handle, int(count)))
+
+    def log_norm(self, slot, which=0):
+        N.check(self._lib.kfbi_log_norm(self.handle, int(slot), int(which), self.stream))
+
+    def log_fetch(self, first, count):
+        out = (N.StepLog * max(int(count), 1))()
+        N.check(self._lib.kfbi_log_fetch(self.handle, int(first), int(count), out, self.stream))
+        return [(out[i].iterations, out[i].status, out[i].residual, out[i].norm, out[i].newton)
+                for i in range(int(count))]
 
     def heat_rhs(self, n, mask, u, F_old, F_new, a, want_norm=True):
         norm = C.c_double(0.0)
@@ -171,17 +189,24 @@ class Plan:
                                           other.data_ptr(), float(tau), out.data_ptr(),
                                           self.stream))
 
-    def nonlinear_phase(self, n, ustar, v, w, half_tau, mask, out, kappa=None, F=None):
+    def nonlinear_phase(self, n, ustar, v, w, half_tau, mask, out, kappa=None, F=None,
+                        log_slot=None):
         k = complex(kappa) if kappa is not None else 0j
         res = C.c_double(0.0)
         status = self._lib.kfbi_nonlinear_phase(
             self.handle, int(n), ustar.data_ptr(), v.data_ptr(), float(w), float(half_tau),
-            N.ptr(mask), out.data_ptr(), k.real, k.imag, N.ptr(F), C.byref(res), self.stream)
+            N.ptr(mask), out.data_ptr(), k.real, k.imag, N.ptr(F),
+            None if log_slot is not None else C.byref(res), self.stream)
+        if log_slot is not None:
+            N.check(status)
+            self.log_norm(log_slot, which=1)
+            return None
         N.check(status, iterations=50, last_residual=res.value)
         return res.value
 
-    def mask_norm(self, n, mask, u):
+    def mask_norm(self, n, mask, u, want_norm=True):
         norm = C.c_double(0.0)
         N.check(self._lib.kfbi_mask_norm(self.handle, self._dt(u.is_complex()), int(n),
-                                         N.ptr(mask), u.data_ptr(), C.byref(norm), self.stream))
+                                         N.ptr(mask), u.data_ptr(),
+                                         C.byref(norm) if want_norm else None, self.stream))
         return norm.value

@@ -538,14 +538,57 @@ op_solve_kernel(OpSolveArgs a, const T *__restrict__ Top, T *A, T *B,
 template <typename T>
 __global__ void __launch_bounds__(256)
 extract_traces_kernel(ExtractArgs x, const T *__restrict__ u, const T *__restrict__ jm,
-                      T *trace_u, T *trace_un) {
+                      T *trace_u, T *trace_un, const int *skip) {
   using S = Sc<T>;
+  if (skip && *skip) return;
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= x.n) return;
   T tu, tx, ty;
   extract_point<T>(x, u, jm, p, tu, tx, ty);
   trace_u[p] = tu;
   trace_un[p] = S::add(S::rmul(tx, x.normal[2 * p]), S::rmul(ty, x.normal[2 * p + 1]));
+}
+
+// Per-step record of an asynchronous solve (read back in batches by the host).
+struct StepLog {
+  int iterations;
+  int status;                     // 1 converged, 2 max_iter reached
+  double residual;
+  double norm;                    // blow-up norm of the step, when logged
+  double newton;                  // worst pointwise Newton residual (Schrodinger)
+};
+
+// Closes an operator-form solve on the device, without the host:
+//   K = sweeps done; skip[0] = 0 only if the converging sweep was an
+//   operator sweep (then the full pipeline must recompute the field from
+//   phi_(K-1)); phi_(K-1) -> phik1, phi_K -> A (ping-pong parity of
+//   op_solve_kernel); the step log entry.
+template <typename T>
+__global__ void op_finalize_kernel(const RichState *st, int n, T *A, const T *B, T *phik1,
+                                   int *skip, StepLog *log) {
+  const int K = st->iters, done = st->done;
+  const bool odd = (K & 1) != 0;
+  for (int p = threadIdx.x; p < n; p += blockDim.x) {
+    if (K >= 2) {
+      const T a = A[p], b = B[p];
+      phik1[p] = odd ? b : a;       // phi_(K-1)
+      if (!odd) A[p] = b;           // phi_K into the density buffer
+    }
+  }
+  if (threadIdx.x == 0) {
+    skip[0] = (K >= 2 && done == 1) ? 0 : 1;
+    if (log) {
+      log->iterations = K;
+      log->status = done;
+      log->residual = st->last_res;
+    }
+  }
+}
+
+__global__ void log_norm_kernel(const unsigned long long *norm_bits, StepLog *log, int which) {
+  const double v = __longlong_as_double((long long)*norm_bits);
+  if (which == 0) log->norm = v;
+  else log->newton = nanmax(log->newton, v);
 }
 
 __global__ void rich_init_kernel(RichState *st, int max_iter, double tol) {

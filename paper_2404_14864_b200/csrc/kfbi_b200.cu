@@ -97,6 +97,10 @@ struct kfbi_plan {
   DevBuf<RichState> st;
   // operator form (trace operator T of one kappa / dtype)
   DevBuf<double2> Top, phi0, phi_prev, trace1, trace_tmp, zvec, evec, out3, ufield;
+  DevBuf<double2> phik1;
+  DevBuf<int> skip;
+  DevBuf<StepLog> log;
+  int log_cap = 0;
   bool op_valid = false;
   int op_dtype = -1;
   double op_kre = 0.0, op_kim = 0.0;
@@ -358,6 +362,13 @@ kfbi_status ensure_op_scratch(kfbi_plan *p) {
   return KFBI_OK;
 }
 
+kfbi_status ensure_async_scratch(kfbi_plan *p) {
+  cudaError_t e = p->phik1.ensure((size_t)p->n_ctl);
+  if (e == cudaSuccess) e = p->skip.ensure(1);
+  if (e != cudaSuccess) return fail(KFBI_E_CUDA, std::string("async scratch: ") + cudaGetErrorString(e));
+  return KFBI_OK;
+}
+
 // Column p of T = trace of the pipeline applied to e_p with F = 0, f_gamma = 0.
 template <typename T>
 kfbi_status build_operator_T(kfbi_plan *p, double kre, double kim, cudaStream_t s) {
@@ -456,18 +467,19 @@ kfbi_status op_solve(kfbi_plan *p, const kfbi_bvp *b, cudaStream_t s) {
 // Full pipeline from the density before the converging update: the field and
 // traces the reference returns (bvp.py:319-323, 336-344).
 template <typename T>
-kfbi_status final_pipeline(kfbi_plan *p, const kfbi_bvp *b, const void *phi_before, cudaStream_t s) {
+kfbi_status final_pipeline(kfbi_plan *p, const kfbi_bvp *b, const void *phi_before, cudaStream_t s,
+                           const int *skip = nullptr) {
   constexpr bool CPLX = std::is_same<T, double2>::value;
   const int n = p->n_ctl;
   KFBI_TRY(jumps_T<T>(p, b->kappa_re, b->kappa_im, phi_before, nullptr, b->f_gamma,
-                      b->f_gamma_sign, p->jm.p, nullptr, s));
-  KFBI_TRY(edges_T<T>(p, p->jm.p, p->jv.p, nullptr, s));
-  KFBI_TRY(box_passes<CPLX>(p, b->kappa_re, b->kappa_im, b->F, b->F_sign, p->jv.p, b->u, nullptr, s));
+                      b->f_gamma_sign, p->jm.p, skip, s));
+  KFBI_TRY(edges_T<T>(p, p->jm.p, p->jv.p, skip, s));
+  KFBI_TRY(box_passes<CPLX>(p, b->kappa_re, b->kappa_im, b->F, b->F_sign, p->jv.p, b->u, skip, s));
   ExtractArgs x = extract_args(p);
   return launch(p, KFBI_K_EXTRACT, s, [&] {
     extract_traces_kernel<T><<<(n + 255) / 256, 256, 0, s>>>(
         x, static_cast<const T *>(b->u), reinterpret_cast<const T *>(p->jm.p),
-        static_cast<T *>(b->trace_u), static_cast<T *>(b->trace_un));
+        static_cast<T *>(b->trace_u), static_cast<T *>(b->trace_un), skip);
   });
 }
 
@@ -549,7 +561,7 @@ kfbi_status kfbi_plan_destroy(kfbi_plan *p) {
   p->history.release(); p->st.release(); p->red.release();
   p->Top.release(); p->phi0.release(); p->phi_prev.release(); p->trace1.release();
   p->trace_tmp.release(); p->zvec.release(); p->evec.release(); p->out3.release();
-  p->ufield.release();
+  p->ufield.release(); p->phik1.release(); p->skip.release(); p->log.release();
   if (p->st_host) cudaFreeHost(p->st_host);
   if (p->red_host) cudaFreeHost(p->red_host);
   delete p;
@@ -690,6 +702,41 @@ kfbi_status kfbi_richardson(kfbi_plan *p, const kfbi_bvp *b, kfbi_bvp_result *re
   if (use_op)
     KFBI_CUDA(cudaMemcpyAsync(p->phi0.p, b->density, p->n_ctl * es, cudaMemcpyDeviceToDevice, s),
               "density-update");
+  if (use_op && b->log_slot >= 0) {
+    // asynchronous operator form: no host sync at all; the device decides
+    // whether the full pipeline must recompute the field and logs the step
+    if (b->log_slot >= p->log_cap) return fail(KFBI_E_CONFIG, "log slot out of range (kfbi_log_reserve)");
+    KFBI_TRY(ensure_async_scratch(p));
+    if (cplx) KFBI_TRY(sweep<double2>(p, b, s));
+    else KFBI_TRY(sweep<double>(p, b, s));
+    KFBI_CUDA(cudaMemcpyAsync(p->trace1.p, b->trace_u, p->n_ctl * es, cudaMemcpyDeviceToDevice, s),
+              "density-update");
+    if (b->max_iter > 1) {
+      if (cplx) KFBI_TRY(op_solve<double2>(p, b, s));
+      else KFBI_TRY(op_solve<double>(p, b, s));
+    }
+    StepLog *entry = p->log.p + b->log_slot;
+    int *skip = p->skip.p;
+    if (cplx) {
+      KFBI_TRY(launch(p, KFBI_K_DENSITY, s, [&] {
+        op_finalize_kernel<double2><<<1, 256, 0, s>>>(p->st.p, p->n_ctl, static_cast<double2 *>(b->density),
+                                                      p->phi_prev.p, p->phik1.p, skip, entry);
+      }));
+      KFBI_TRY(final_pipeline<double2>(p, b, p->phik1.p, s, skip));
+    } else {
+      KFBI_TRY(launch(p, KFBI_K_DENSITY, s, [&] {
+        op_finalize_kernel<double><<<1, 256, 0, s>>>(
+            p->st.p, p->n_ctl, static_cast<double *>(b->density),
+            reinterpret_cast<const double *>(p->phi_prev.p), reinterpret_cast<double *>(p->phik1.p),
+            skip, entry);
+      }));
+      KFBI_TRY(final_pipeline<double>(p, b, p->phik1.p, s, skip));
+    }
+    res->iterations = -1;     // pending: read with kfbi_log_fetch
+    res->converged = -1;
+    res->residual = 0.0;
+    return KFBI_OK;
+  }
   if (use_op) {
     // sweep 1 through the pipeline, then every further sweep inside one
     // cooperative launch; a single host sync per solve
@@ -770,6 +817,45 @@ kfbi_status kfbi_build_trace_operator(kfbi_plan *p, int32_t dtype, double kre, d
   return build_operator_T<double>(p, kre, kim, s);
 }
 
+kfbi_status kfbi_log_reserve(kfbi_plan *p, int32_t count) {
+  KFBI_TRY(check_plan(p));
+  if (count <= p->log_cap) return KFBI_OK;
+  DevBuf<StepLog> nb;
+  cudaError_t e = nb.ensure((size_t)count);
+  if (e == cudaSuccess && p->log_cap > 0)
+    e = cudaMemcpy(nb.p, p->log.p, sizeof(StepLog) * p->log_cap, cudaMemcpyDeviceToDevice);
+  if (e == cudaSuccess) e = cudaMemset(nb.p + p->log_cap, 0, sizeof(StepLog) * (count - p->log_cap));
+  if (e != cudaSuccess) {
+    nb.release();
+    return fail(KFBI_E_CUDA, std::string("log allocation: ") + cudaGetErrorString(e));
+  }
+  p->log.release();
+  p->log = nb;
+  nb.p = nullptr;
+  p->log_cap = count;
+  return KFBI_OK;
+}
+
+kfbi_status kfbi_log_norm(kfbi_plan *p, int32_t slot, int32_t which, void *stream) {
+  KFBI_TRY(check_plan(p));
+  if (slot < 0 || slot >= p->log_cap) return fail(KFBI_E_CONFIG, "log slot out of range");
+  cudaStream_t s = (cudaStream_t)stream;
+  return launch(p, KFBI_K_RHS, s, [&] { log_norm_kernel<<<1, 1, 0, s>>>(p->red.p, p->log.p + slot, which); });
+}
+
+kfbi_status kfbi_log_fetch(kfbi_plan *p, int32_t first, int32_t count, kfbi_step_log *out,
+                           void *stream) {
+  KFBI_TRY(check_plan(p));
+  if (first < 0 || count < 0 || first + count > p->log_cap)
+    return fail(KFBI_E_CONFIG, "log range out of bounds");
+  static_assert(sizeof(kfbi_step_log) == sizeof(StepLog), "log layout");
+  cudaStream_t s = (cudaStream_t)stream;
+  KFBI_CUDA(cudaMemcpyAsync(out, p->log.p + first, sizeof(StepLog) * count, cudaMemcpyDeviceToHost, s),
+            "density-update");
+  KFBI_CUDA(cudaStreamSynchronize(s), "density-update");
+  return KFBI_OK;
+}
+
 kfbi_status kfbi_heat_rhs(kfbi_plan *p, int64_t n, const uint8_t *mask, void *u, const void *F_old,
                           void *F_new, double a, double *norm_out, void *stream) {
   KFBI_TRY(check_plan(p));
@@ -820,6 +906,7 @@ kfbi_status kfbi_nonlinear_phase(kfbi_plan *p, int64_t n, const void *ustar, con
         n, static_cast<const double2 *>(ustar), v, w, half_tau, mask, static_cast<double2 *>(out),
         kre, kim, static_cast<double2 *>(F), p->red.p);
   }));
+  if (!max_res) return KFBI_OK;    // asynchronous: the caller logs red[0] (kfbi_log_norm)
   double r = 0.0;
   KFBI_TRY(read_norm(p, s, &r));
   if (max_res) *max_res = r;
