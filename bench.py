@@ -234,6 +234,8 @@ def run_ours(args):
     with Clocks(local) as clk:
         start = torch.cuda.Event(enable_timing=True)
         end = torch.cuda.Event(enable_timing=True)
+        if args.profile:
+            torch.cuda.profiler.start()
         start.record(stream)
         for _ in range(args.steps):
             for eq in eqs:
@@ -247,6 +249,8 @@ def run_ours(args):
                     iters[eq].append(st.last_iterations)
         end.record(stream)
         torch.cuda.synchronize()
+        if args.profile:
+            torch.cuda.profiler.stop()
     _barrier(ws)
     elapsed_ms = start.elapsed_time(end)
     for eq in eqs:                 # asynchronous stepping: per-step log (+ error checks)
@@ -497,6 +501,9 @@ def main(argv=None):
     ap.add_argument("--m", type=int, default=M_DEFAULT)
     ap.add_argument("--equations", default=",".join(EQUATIONS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile", action="store_true",
+                    help="bracket the headline loop with cudaProfilerStart/Stop (for ncu "
+                         "--profile-from-start off launch lists of the timed region only)")
     ap.add_argument("--pipeline", action="store_true",
                     help="run every Richardson sweep through the full pipeline (no trace operator)")
     args = ap.parse_args(argv)

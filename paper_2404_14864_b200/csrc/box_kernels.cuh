@@ -33,6 +33,8 @@ struct BoxArgs {
   double inv4m2;          // 1 / (4 m^2), exact power of two
   void *panels;
   const int *done;        // early-exit flag (Richardson sweeps), may be null
+  const double2 *twg;     // [m] exp(-2 pi i q / m)        (register engine)
+  const double *sinv;     // [m] sin(pi j / m)              (register engine)
 };
 
 // Sparse right-hand-side corrections fused into the forward row pass.

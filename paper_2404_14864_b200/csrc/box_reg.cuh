@@ -1,0 +1,263 @@
+// Box solve (Delta_h - kappa) u = rhs, dirichlet-zero closure
+// (BoxSolver.solve, boxsolve.py:46-94) on the register DST-I engine
+// (dst_reg.cuh), three HBM passes:
+//
+//   rows_fwd_reg : rhs rows (+ the sparse jump corrections of those rows,
+//                  interface.py:235-238 / bvp.py:319) -> DST-I along x -> panels
+//   cols_reg     : panel column -> DST-I along y -> / (lam_p + lam_q - kappa)
+//                  / (4 M^2) -> DST-I along y -> panel column (in place)
+//   rows_inv_reg : panels -> DST-I along x -> u rows with the exact zero ring
+//
+// Panels (the intermediate spectrum): 32-byte column strips indexed by the
+// spectral x index kx (column 0 is padding) and the row / spectral y index j
+// (row 0 is padding).  Real: panel pp holds kx = 4pp..4pp+3,
+// P[(pp*M + j)*4 + w]; complex: kx = 2pp..2pp+1, P2[(pp*M + j)*2 + w].  A
+// column pass reads one M*32-byte slab (two CTAs per slab, one per 16-byte
+// half), a row task writes whole 32-byte sectors straight from registers.
+//
+// One CTA = 256 threads = 256*16 complex elements in registers: one length-
+// 4096 sequence, or 4096/N shorter ones.  Real rows/columns are packed two
+// per complex sequence.
+#pragma once
+
+#include "box_kernels.cuh"
+#include "dst_reg.cuh"
+
+namespace kfbi {
+
+constexpr size_t REG_SMEM_BYTES =
+    (size_t)reg::CTA * reg::E * sizeof(double2) + (reg::CTA / 32) * sizeof(double2);
+
+// stage x (natural order) into the sequence's smem, x_0 = 0
+template <int LOGN>
+KFBI_DEV void stage(double2 *sm, const double2 (&v)[reg::E], int t) {
+#pragma unroll
+  for (int m = 0; m < reg::E; ++m) sm[reg::sw(t + m * reg::Cfg<LOGN>::T)] = v[m];
+}
+
+// x staged in sm -> C = DST-I(x) in out[c] (index 16 t + c).  Entry: staged
+// data visible (after a barrier).  Exit: sm may still be read by other
+// threads (barrier needed before the next write).
+template <int LOGN>
+KFBI_DEV void dst_staged(double2 *sm, double2 *scratch, int t, const BoxArgs &a,
+                         double2 (&out)[reg::E]) {
+  double2 v[reg::E];
+  reg::pre_from_smem<LOGN>(v, sm, t, a.sinv);
+  __syncthreads();
+  reg::fft<LOGN>(v, sm, t, a.twg);
+  reg::post<LOGN>(sm, t, out, scratch);
+}
+
+// ---------------------------------------------------------------------------
+template <bool CPLX, int LOGN>
+__global__ void __launch_bounds__(reg::CTA, 2)
+rows_fwd_reg(BoxArgs a, const void *__restrict__ rhs, double sign,
+             CorrArgs<typename std::conditional<CPLX, double2, double>::type> corr) {
+  using T = typename std::conditional<CPLX, double2, double>::type;
+  using C = reg::Cfg<LOGN>;
+  constexpr int M = C::N, TT = C::T;
+  extern __shared__ double2 smem[];
+  if (a.done && *a.done) return;
+  const int seq = threadIdx.x / TT, t = threadIdx.x % TT;
+  double2 *sm = smem + seq * M;
+  double2 *scratch = smem + reg::CTA * reg::E;
+  const int stride = M + 1;
+  const int q = blockIdx.x * C::S + seq;
+  const int nseq = CPLX ? M - 1 : M / 2;
+  const bool valid = q < nseq;
+  const int j0 = CPLX ? q + 1 : 2 * q + 1;
+  const bool has2 = !CPLX && valid && j0 + 1 < M;
+
+  double2 v[reg::E];
+#pragma unroll
+  for (int m = 0; m < reg::E; ++m) {
+    const int n = t + m * TT;
+    v[m] = make_double2(0.0, 0.0);
+    if (valid && n >= 1 && rhs != nullptr) {
+      if (CPLX) {
+        v[m] = static_cast<const double2 *>(rhs)[(size_t)j0 * stride + n];
+      } else {
+        const double *r = static_cast<const double *>(rhs);
+        v[m].x = r[(size_t)j0 * stride + n];
+        if (has2) v[m].y = r[(size_t)(j0 + 1) * stride + n];
+      }
+    }
+  }
+#pragma unroll
+  for (int m = 0; m < reg::E; ++m) v[m] = cscale(v[m], sign);
+  stage<LOGN>(sm, v, t);
+  if (corr.jv) {
+    __syncthreads();
+    if (valid) {
+      const int nrows = has2 ? 2 : 1;
+      for (int qq = 0; qq < nrows; ++qq) {
+        const int j = j0 + qq;
+        const int g0 = corr.row_group[j], g1 = corr.row_group[j + 1];
+        for (int g = g0 + t; g < g1; g += TT) {
+          const T cv = group_correction<T>(corr, g);
+          const int i = corr.group_node[g] - j * stride;
+          if constexpr (CPLX) {
+            double2 &slot = sm[reg::sw(i)];
+            slot = cadd(slot, cv);
+          } else {
+            double *slot = reinterpret_cast<double *>(&sm[reg::sw(i)]) + qq;
+            *slot += cv;
+          }
+        }
+      }
+    }
+  }
+  __syncthreads();
+  double2 out[reg::E];
+  dst_staged<LOGN>(sm, scratch, t, a, out);
+  if (!valid) return;
+  // panel stores straight from registers: whole 32-byte sectors
+  double2 *P2 = static_cast<double2 *>(a.panels);
+  if (!CPLX) {
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {
+      const size_t pp = 4 * t + g;
+      double2 *d = P2 + (pp * M + j0) * 2;
+      d[0] = make_double2(out[4 * g].x, out[4 * g + 1].x);
+      d[1] = make_double2(out[4 * g + 2].x, out[4 * g + 3].x);
+      if (has2) {
+        d[2] = make_double2(out[4 * g].y, out[4 * g + 1].y);
+        d[3] = make_double2(out[4 * g + 2].y, out[4 * g + 3].y);
+      }
+    }
+  } else {
+#pragma unroll
+    for (int g = 0; g < 8; ++g) {
+      const size_t pp = 8 * t + g;
+      double2 *d = P2 + (pp * M + j0) * 2;
+      d[0] = out[2 * g];
+      d[1] = out[2 * g + 1];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+template <bool CPLX, int LOGN>
+__global__ void __launch_bounds__(reg::CTA, 2) cols_reg(BoxArgs a) {
+  using C = reg::Cfg<LOGN>;
+  constexpr int M = C::N, TT = C::T;
+  extern __shared__ double2 smem[];
+  if (a.done && *a.done) return;
+  const int seq = threadIdx.x / TT, t = threadIdx.x % TT;
+  double2 *sm = smem + seq * M;
+  double2 *scratch = smem + reg::CTA * reg::E;
+  const int q = blockIdx.x * C::S + seq;
+  const int nseq = CPLX ? M : M / 2;
+  const bool valid = q < nseq;
+  const int pp = q >> 1, half = q & 1;
+  double2 *col = static_cast<double2 *>(a.panels) + (size_t)pp * M * 2 + half;
+
+  double2 v[reg::E];
+#pragma unroll
+  for (int m = 0; m < reg::E; ++m) {
+    const int n = t + m * TT;
+    v[m] = (valid && n >= 1) ? col[2 * n] : make_double2(0.0, 0.0);
+  }
+  stage<LOGN>(sm, v, t);
+  __syncthreads();
+  double2 out[reg::E];
+  dst_staged<LOGN>(sm, scratch, t, a, out);
+
+  // spectral division (boxsolve.py:74-76): (v / (lam_p + lam_q - kappa)) / (4 M^2)
+#pragma unroll
+  for (int c = 0; c < reg::E; ++c) {
+    const int p = reg::E * t + c;
+    const double lp = a.lam[p];
+    if (!CPLX) {
+      const int kx = 4 * pp + 2 * half;
+      const double da = (lp + a.lam[kx]) - a.kre;
+      const double db = (lp + a.lam[kx + 1]) - a.kre;
+      out[c] = make_double2((out[c].x / da) * a.inv4m2, (out[c].y / db) * a.inv4m2);
+    } else {
+      const int kx = 2 * pp + half;
+      const double2 d = make_double2((lp + a.lam[kx]) - a.kre, -a.kim);
+      out[c] = cscale(cdiv(out[c], d), a.inv4m2);
+    }
+  }
+  if (t == 0) out[0] = make_double2(0.0, 0.0);   // x_0 = 0 for the second transform
+  __syncthreads();
+#pragma unroll
+  for (int c = 0; c < reg::E; ++c) sm[reg::sw(reg::E * t + c)] = out[c];
+  __syncthreads();
+  dst_staged<LOGN>(sm, scratch, t, a, out);
+  if (!valid) return;
+#pragma unroll
+  for (int c = 0; c < reg::E; ++c) col[2 * (reg::E * t + c)] = out[c];
+}
+
+// ---------------------------------------------------------------------------
+template <bool CPLX, int LOGN>
+__global__ void __launch_bounds__(reg::CTA, 2) rows_inv_reg(BoxArgs a, void *__restrict__ u) {
+  using C = reg::Cfg<LOGN>;
+  constexpr int M = C::N, TT = C::T;
+  extern __shared__ double2 smem[];
+  if (a.done && *a.done) return;
+  const int seq = threadIdx.x / TT, t = threadIdx.x % TT;
+  double2 *sm = smem + seq * M;
+  double2 *scratch = smem + reg::CTA * reg::E;
+  const int stride = M + 1;
+  const int q = blockIdx.x * C::S + seq;
+  const int nseq = CPLX ? M - 1 : M / 2;
+  const bool valid = q < nseq;
+  const int j0 = CPLX ? q + 1 : 2 * q + 1;
+  const bool has2 = !CPLX && valid && j0 + 1 < M;
+
+  double2 v[reg::E];
+#pragma unroll
+  for (int m = 0; m < reg::E; ++m) {
+    const int n = t + m * TT;
+    v[m] = make_double2(0.0, 0.0);
+    if (valid && n >= 1) {
+      if (!CPLX) {
+        const double *s0 = static_cast<const double *>(a.panels) + ((size_t)(n >> 2) * M + j0) * 4 + (n & 3);
+        v[m].x = s0[0];
+        if (has2) v[m].y = s0[4];
+      } else {
+        v[m] = static_cast<const double2 *>(a.panels)[((size_t)(n >> 1) * M + j0) * 2 + (n & 1)];
+      }
+    }
+  }
+  stage<LOGN>(sm, v, t);
+  __syncthreads();
+  double2 out[reg::E];
+  dst_staged<LOGN>(sm, scratch, t, a, out);
+  __syncthreads();
+#pragma unroll
+  for (int c = 0; c < reg::E; ++c) sm[reg::sw(reg::E * t + c)] = out[c];
+  __syncthreads();
+  if (!valid) return;
+  // coalesced row stores with the zero ring (boxsolve.py:90-93)
+  if (!CPLX) {
+    double *U = static_cast<double *>(u);
+    double *u0 = U + (size_t)j0 * stride;
+    double *u1 = U + (size_t)(j0 + 1) * stride;   // ring row M when !has2
+    for (int n = t; n <= M; n += TT) {
+      double x = 0.0, y = 0.0;
+      if (n >= 1 && n < M) {
+        const double2 w = sm[reg::sw(n)];
+        x = w.x;
+        y = has2 ? w.y : 0.0;
+      }
+      u0[n] = x;
+      u1[n] = y;
+    }
+    if (q == 0)
+      for (int n = t; n <= M; n += TT) U[n] = 0.0;
+  } else {
+    double2 *U = static_cast<double2 *>(u);
+    double2 *u0 = U + (size_t)j0 * stride;
+    for (int n = t; n <= M; n += TT)
+      u0[n] = (n >= 1 && n < M) ? sm[reg::sw(n)] : make_double2(0.0, 0.0);
+    if (q == 0)
+      for (int n = t; n <= M; n += TT) U[n] = make_double2(0.0, 0.0);
+    if (j0 == M - 1)
+      for (int n = t; n <= M; n += TT) U[(size_t)M * stride + n] = make_double2(0.0, 0.0);
+  }
+}
+
+}  // namespace kfbi

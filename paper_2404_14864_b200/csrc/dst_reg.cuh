@@ -1,0 +1,287 @@
+// Register-resident DST-I engine: the transform of boxsolve.py:70-82
+// (scipy.fft.dst(type=1), unnormalised) on complex sequences.
+//
+// For a complex sequence x_1..x_{N-1} (x_0 = x_N = 0), N = 2^LOGN, scipy's
+// DST-I is C_k = 2 sum_n x_n sin(pi k n / N).  One complex FFT of length N:
+//
+//   y_j  = sin(pi j / N) (x_j + x_{N-j}) + (x_j - x_{N-j}) / 2       (pre)
+//   Z    = FFT_N(y)
+//   C_2k   = i (Z_k - Z_{N-k})                                        (post)
+//   C_2k+1 = C_2k-1 + (Z_k + Z_{N-k}),   C_1 = Z_0
+//
+// (the symmetric half of y carries the odd outputs through the cosine sums,
+// the antisymmetric half the even ones).  Real rows/columns are packed two
+// per complex sequence; DST-I is real-linear, so one engine serves f64 and
+// c128.  The odd outputs are a prefix sum, done as an 8-term serial scan per
+// thread + a shuffle / shared-memory scan across threads (error O(log N)).
+//
+// Layout: T = N/16 threads per sequence, each holding 16 elements in
+// registers; element m of thread t is index t + m*T in every pass.  The FFT
+// is Stockham autosort, radix 16 (last pass radix 2^(LOGN mod 4) if any), so
+// 4096 = 16*16*16 is three register passes and two shared-memory exchanges.
+// The first pass needs no twiddles; pass p multiplies by w^s, w = e^{-2 pi i
+// k / (Ns R)}, w from a global table and its powers by complex products.
+//
+// Shared memory: N double2 per sequence, swizzled (sw) so that every access
+// pattern below is free of bank conflicts for 16-byte slots.
+#pragma once
+
+#include "common.cuh"
+
+namespace kfbi {
+namespace reg {
+
+constexpr int E = 16;          // elements per thread
+constexpr int CTA = 256;       // threads per CTA
+constexpr double RSQ2 = 0.70710678118654752440;
+
+// conflict-free 16-byte slot swizzle: XOR bits 0-2 with bits 3-5 ^ 6-8
+KFBI_DEV int sw(int i) { return i ^ (((i >> 3) ^ (i >> 6)) & 7); }
+
+template <int LOGN>
+struct Cfg {
+  static constexpr int N = 1 << LOGN;
+  static constexpr int T = N / E;                 // threads per sequence
+  static constexpr int S = CTA / T;               // sequences per CTA
+  static constexpr int P = (LOGN + 3) / 4;        // Stockham passes
+  static constexpr int RLAST = 1 << (LOGN - 4 * (P - 1));
+  static_assert(LOGN >= 4 && LOGN <= 12, "DST length 16..4096");
+};
+
+// ---- constant twiddles w16^e = exp(-2 pi i e / 16) ----
+template <int e>
+KFBI_DEV double2 w16(double2 z) {
+  constexpr int k = e & 15;
+  constexpr double C1 = 0.92387953251128675613, S1 = 0.38268343236508977173;
+  if constexpr (k == 0) return z;
+  else if constexpr (k == 4) return make_double2(z.y, -z.x);
+  else if constexpr (k == 8) return make_double2(-z.x, -z.y);
+  else if constexpr (k == 12) return make_double2(-z.y, z.x);
+  else if constexpr (k == 2) return make_double2(RSQ2 * (z.x + z.y), RSQ2 * (z.y - z.x));
+  else if constexpr (k == 6) return make_double2(RSQ2 * (z.y - z.x), -RSQ2 * (z.x + z.y));
+  else if constexpr (k == 10) return make_double2(-RSQ2 * (z.x + z.y), RSQ2 * (z.x - z.y));
+  else if constexpr (k == 14) return make_double2(RSQ2 * (z.x - z.y), RSQ2 * (z.x + z.y));
+  else {
+    // cos / -sin of 2 pi k / 16 for odd k
+    constexpr double c = (k == 1 || k == 15) ? C1 : (k == 3 || k == 13) ? S1 : (k == 5 || k == 11) ? -S1 : -C1;
+    constexpr double s = (k == 1 || k == 7) ? -S1 : (k == 3 || k == 5) ? -C1 : (k == 9 || k == 15) ? S1 : C1;
+    return make_double2(z.x * c - z.y * s, z.x * s + z.y * c);
+  }
+}
+
+// ---- in-register DFTs (natural order in and out), a[i*ST] for i < R ----
+template <int ST, int OFF>
+KFBI_DEV void dft4(double2 *a) {
+  double2 &a0 = a[OFF], &a1 = a[OFF + ST], &a2 = a[OFF + 2 * ST], &a3 = a[OFF + 3 * ST];
+  const double2 t0 = cadd(a0, a2), t1 = csub(a0, a2), t2 = cadd(a1, a3);
+  const double2 d = csub(a1, a3);
+  const double2 t3 = make_double2(d.y, -d.x);   // -i (a1 - a3)
+  a0 = cadd(t0, t2);
+  a2 = csub(t0, t2);
+  a1 = cadd(t1, t3);
+  a3 = csub(t1, t3);
+}
+
+template <int R>
+KFBI_DEV void dft(double2 (&a)[R]) {
+  if constexpr (R == 2) {
+    const double2 t = a[0];
+    a[0] = cadd(t, a[1]);
+    a[1] = csub(t, a[1]);
+  } else if constexpr (R == 4) {
+    dft4<1, 0>(a);
+  } else if constexpr (R == 8) {
+    // n = n1 + 2 n2, k = k2 + 4 k1
+    dft4<2, 0>(a);
+    dft4<2, 1>(a);                      // b[n1][k2] at a[n1 + 2 k2]
+    double2 o[8];
+#pragma unroll
+    for (int k2 = 0; k2 < 4; ++k2) {
+      const double2 b0 = a[2 * k2];
+      double2 b1 = a[2 * k2 + 1];
+      if (k2 == 1) b1 = w16<2>(b1);
+      if (k2 == 2) b1 = w16<4>(b1);
+      if (k2 == 3) b1 = w16<6>(b1);
+      o[k2] = cadd(b0, b1);
+      o[k2 + 4] = csub(b0, b1);
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) a[i] = o[i];
+  } else {
+    static_assert(R == 16, "radix");
+    // n = n1 + 4 n2, k = k2 + 4 k1
+    dft4<4, 0>(a);
+    dft4<4, 1>(a);
+    dft4<4, 2>(a);
+    dft4<4, 3>(a);                      // b[n1][k2] at a[n1 + 4 k2]
+    a[1 + 4] = w16<1>(a[1 + 4]);
+    a[1 + 8] = w16<2>(a[1 + 8]);
+    a[1 + 12] = w16<3>(a[1 + 12]);
+    a[2 + 4] = w16<2>(a[2 + 4]);
+    a[2 + 8] = w16<4>(a[2 + 8]);
+    a[2 + 12] = w16<6>(a[2 + 12]);
+    a[3 + 4] = w16<3>(a[3 + 4]);
+    a[3 + 8] = w16<6>(a[3 + 8]);
+    a[3 + 12] = w16<9>(a[3 + 12]);
+    dft4<1, 0>(a);
+    dft4<1, 4>(a);
+    dft4<1, 8>(a);
+    dft4<1, 12>(a);                     // X[k2 + 4 k1] at a[4 k2 + k1]
+    double2 o[16];
+#pragma unroll
+    for (int k2 = 0; k2 < 4; ++k2)
+#pragma unroll
+      for (int k1 = 0; k1 < 4; ++k1) o[k2 + 4 * k1] = a[4 * k2 + k1];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) a[i] = o[i];
+  }
+}
+
+// w^s for s < R from w = w^1 (products of at most 4 factors)
+template <int R>
+KFBI_DEV void powers(double2 w1, double2 (&w)[R]) {
+  w[0] = make_double2(1.0, 0.0);
+  if constexpr (R >= 2) w[1] = w1;
+  if constexpr (R >= 4) {
+    w[2] = cmul(w1, w1);
+    w[3] = cmul(w[2], w1);
+  }
+  if constexpr (R >= 8) {
+    w[4] = cmul(w[2], w[2]);
+    w[5] = cmul(w[4], w1);
+    w[6] = cmul(w[3], w[3]);
+    w[7] = cmul(w[4], w[3]);
+  }
+  if constexpr (R >= 16) {
+    w[8] = cmul(w[4], w[4]);
+    w[9] = cmul(w[8], w1);
+    w[10] = cmul(w[5], w[5]);
+    w[11] = cmul(w[8], w[3]);
+    w[12] = cmul(w[6], w[6]);
+    w[13] = cmul(w[8], w[5]);
+    w[14] = cmul(w[7], w[7]);
+    w[15] = cmul(w[8], w[7]);
+  }
+}
+
+// One Stockham pass: radix R, current span NS; thread t holds inputs
+// v[m] = x[t + m T]; writes the pass output to sm (swizzled).
+template <int LOGN, int R, int NS>
+KFBI_DEV void stockham_pass(double2 (&v)[E], double2 *sm, int t, const double2 *__restrict__ twg) {
+  constexpr int N = 1 << LOGN;
+  constexpr int T = Cfg<LOGN>::T;
+  constexpr int B = E / R;              // butterflies per thread
+#pragma unroll
+  for (int i = 0; i < B; ++i) {
+    const int b = t + i * T;
+    const int k = b & (NS - 1);
+    double2 a[R];
+#pragma unroll
+    for (int s = 0; s < R; ++s) a[s] = v[i + s * B];
+    if constexpr (NS > 1) {
+      double2 w[R];
+      powers<R>(__ldg(&twg[k * (N / (NS * R))]), w);
+#pragma unroll
+      for (int s = 1; s < R; ++s) a[s] = cmul(a[s], w[s]);
+    }
+    dft<R>(a);
+    const int base = (b - k) * R + k;
+#pragma unroll
+    for (int r = 0; r < R; ++r) sm[sw(base + r * NS)] = a[r];
+  }
+}
+
+template <int LOGN, int PASS>
+KFBI_DEV void fft_passes(double2 (&v)[E], double2 *sm, int t, const double2 *__restrict__ twg) {
+  using C = Cfg<LOGN>;
+  constexpr int R = (PASS < C::P - 1) ? 16 : C::RLAST;
+  constexpr int NS = 1 << (4 * PASS);
+  stockham_pass<LOGN, R, NS>(v, sm, t, twg);
+  if constexpr (PASS + 1 < C::P) {
+    __syncthreads();
+#pragma unroll
+    for (int m = 0; m < E; ++m) v[m] = sm[sw(t + m * C::T)];
+    __syncthreads();
+    fft_passes<LOGN, PASS + 1>(v, sm, t, twg);
+  }
+}
+
+// Z = FFT_N(y): y in registers (v[m] = y_{t + m T}), Z left in sm in natural
+// order.  All threads of the CTA must call it; sm must be free on entry.
+// Returns after a __syncthreads() (Z visible to all threads).
+template <int LOGN>
+KFBI_DEV void fft(double2 (&v)[E], double2 *sm, int t, const double2 *__restrict__ twg) {
+  fft_passes<LOGN, 0>(v, sm, t, twg);
+  __syncthreads();
+}
+
+// y from a staged natural-order x (sm[sw(n)] = x_n, x_0 = 0 stored).
+template <int LOGN>
+KFBI_DEV void pre_from_smem(double2 (&v)[E], const double2 *sm, int t, const double *__restrict__ sinv) {
+  constexpr int N = 1 << LOGN;
+  constexpr int T = Cfg<LOGN>::T;
+#pragma unroll
+  for (int m = 0; m < E; ++m) {
+    const int j = t + m * T;
+    const double2 xj = sm[sw(j)];
+    const double2 xr = sm[sw((N - j) & (N - 1))];   // j = 0 -> x_0 = 0
+    const double s = __ldg(&sinv[j]);
+    const double2 a = cadd(xj, xr), d = csub(xj, xr);
+    v[m] = make_double2(fma(s, a.x, 0.5 * d.x), fma(s, a.y, 0.5 * d.y));
+  }
+}
+
+// Post-processing + scan: out[c] = C_{16 t + c} (out[0] of t = 0 is C_0 = 0).
+// scratch: >= (CTA / 32) double2 (used when T > 32).  Ends with no barrier
+// pending on sm (the caller must __syncthreads() before overwriting sm).
+template <int LOGN>
+KFBI_DEV void post(const double2 *sm, int t, double2 (&out)[E], double2 *scratch) {
+  constexpr int N = 1 << LOGN;
+  constexpr int T = Cfg<LOGN>::T;
+  double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const int k = 8 * t + c;
+    const double2 zk = sm[sw(k)];
+    const double2 zm = sm[sw((N - k) & (N - 1))];
+    const double2 d = csub(zk, zm);
+    out[2 * c] = make_double2(-d.y, d.x);              // i (Z_k - Z_{N-k})
+    const double2 r = (k == 0) ? zk : cadd(zk, zm);
+    acc = (c == 0) ? r : cadd(acc, r);
+    out[2 * c + 1] = acc;
+  }
+  // exclusive scan of the per-thread totals across the sequence
+  double2 off = make_double2(0.0, 0.0);
+  if constexpr (T > 1) {
+    constexpr int W = T < 32 ? T : 32;
+    const int lane = threadIdx.x & 31;
+    const int sl = lane & (W - 1);
+    double2 inc = acc;
+#pragma unroll
+    for (int o = 1; o < W; o <<= 1) {
+      const double ux = __shfl_up_sync(0xffffffffu, inc.x, o, W);
+      const double uy = __shfl_up_sync(0xffffffffu, inc.y, o, W);
+      if (sl >= o) {
+        inc.x += ux;
+        inc.y += uy;
+      }
+    }
+    const double ex = __shfl_up_sync(0xffffffffu, inc.x, 1, W);
+    const double ey = __shfl_up_sync(0xffffffffu, inc.y, 1, W);
+    if (sl >= 1) off = make_double2(ex, ey);
+    if constexpr (T > 32) {
+      const int warp = threadIdx.x >> 5;
+      if (lane == 31) scratch[warp] = inc;
+      __syncthreads();
+      const int w0 = warp & ~(T / 32 - 1);              // first warp of this sequence
+      double2 pw = make_double2(0.0, 0.0);
+      for (int w = w0; w < warp; ++w) pw = cadd(pw, scratch[w]);
+      off = cadd(pw, off);
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < 8; ++c) out[2 * c + 1] = cadd(off, out[2 * c + 1]);
+}
+
+}  // namespace reg
+}  // namespace kfbi

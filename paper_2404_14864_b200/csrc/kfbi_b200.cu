@@ -8,12 +8,14 @@
 
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
 
 #include "../../include/kfbi_b200.h"
 #include "box_kernels.cuh"
+#include "box_reg.cuh"
 #include "interface_kernels.cuh"
 #include "stepping_kernels.cuh"
 
@@ -83,6 +85,9 @@ struct kfbi_plan {
   DevBuf<double2> tw;
   DevBuf<double> lam;
   DevBuf<double2> panels;       // m*m complex slots (sized for c128)
+  DevBuf<double2> twg;          // register engine: exp(-2 pi i q / m), q < m
+  DevBuf<double> sinv;          // register engine: sin(pi j / m), j < m
+  bool legacy_dst = false;      // KFBI_DST=legacy selects the v2 shared-memory engine
   // geometry
   bool has_geo = false;
   int n_ctl = 0, n_edges = 0, n_rec = 0, n_groups = 0, w_ld = 0;
@@ -188,6 +193,8 @@ BoxArgs box_args(kfbi_plan *p, double kre, double kim, const int *done) {
   a.inv4m2 = 1.0 / (4.0 * (double)p->m * (double)p->m);
   a.panels = p->panels.p;
   a.done = done;
+  a.twg = p->twg.p;
+  a.sinv = p->sinv.p;
   return a;
 }
 
@@ -244,6 +251,56 @@ kfbi_status set_smem_limits(kfbi_plan *p) {
   return KFBI_OK;
 }
 
+// Register-engine passes for one (dtype, log2 M).
+template <bool CPLX, int LOGN>
+kfbi_status box_reg_launch(kfbi_plan *p, const BoxArgs &a, const void *rhs, double sign,
+                           const CorrArgs<typename std::conditional<CPLX, double2, double>::type> &c,
+                           void *u, cudaStream_t s) {
+  static bool attr = false;   // per instantiation, process wide
+  if (!attr) {
+    const int bytes = (int)REG_SMEM_BYTES;
+    KFBI_CUDA(cudaFuncSetAttribute(rows_fwd_reg<CPLX, LOGN>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, bytes), "transform-rows");
+    KFBI_CUDA(cudaFuncSetAttribute(rows_inv_reg<CPLX, LOGN>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, bytes), "transform-rows");
+    KFBI_CUDA(cudaFuncSetAttribute(cols_reg<CPLX, LOGN>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, bytes), "transform-cols");
+    attr = true;
+  }
+  using Cf = reg::Cfg<LOGN>;
+  const int M = Cf::N;
+  const int nrow = CPLX ? M - 1 : M / 2;     // row sequences
+  const int ncol = CPLX ? M : M / 2;         // half-panel sequences
+  const int grow = (nrow + Cf::S - 1) / Cf::S, gcol = (ncol + Cf::S - 1) / Cf::S;
+  KFBI_TRY(launch(p, KFBI_K_ROWS, s, [&] {
+    rows_fwd_reg<CPLX, LOGN><<<grow, reg::CTA, REG_SMEM_BYTES, s>>>(a, rhs, sign, c);
+  }));
+  KFBI_TRY(launch(p, KFBI_K_COLS, s, [&] {
+    cols_reg<CPLX, LOGN><<<gcol, reg::CTA, REG_SMEM_BYTES, s>>>(a);
+  }));
+  return launch(p, KFBI_K_ROWS, s, [&] {
+    rows_inv_reg<CPLX, LOGN><<<grow, reg::CTA, REG_SMEM_BYTES, s>>>(a, u);
+  });
+}
+
+template <bool CPLX>
+kfbi_status box_passes_reg(kfbi_plan *p, const BoxArgs &a, const void *rhs, double sign,
+                           const CorrArgs<typename std::conditional<CPLX, double2, double>::type> &c,
+                           void *u, cudaStream_t s) {
+  switch (p->logm) {
+    case 4: return box_reg_launch<CPLX, 4>(p, a, rhs, sign, c, u, s);
+    case 5: return box_reg_launch<CPLX, 5>(p, a, rhs, sign, c, u, s);
+    case 6: return box_reg_launch<CPLX, 6>(p, a, rhs, sign, c, u, s);
+    case 7: return box_reg_launch<CPLX, 7>(p, a, rhs, sign, c, u, s);
+    case 8: return box_reg_launch<CPLX, 8>(p, a, rhs, sign, c, u, s);
+    case 9: return box_reg_launch<CPLX, 9>(p, a, rhs, sign, c, u, s);
+    case 10: return box_reg_launch<CPLX, 10>(p, a, rhs, sign, c, u, s);
+    case 11: return box_reg_launch<CPLX, 11>(p, a, rhs, sign, c, u, s);
+    case 12: return box_reg_launch<CPLX, 12>(p, a, rhs, sign, c, u, s);
+    default: return fail(KFBI_E_CONFIG, "register DST engine: unsupported M");
+  }
+}
+
 // The three passes of one box solve.  rhs is an (M+1)^2 field (scaled by
 // sign); jv != nullptr fuses the jump corrections of the plan's geometry.
 template <bool CPLX>
@@ -257,6 +314,7 @@ kfbi_status box_passes(kfbi_plan *p, double kre, double kim, const void *rhs, do
   const size_t row = box_smem_bytes(M, 1), col = box_smem_bytes(M, 1);
   CorrArgs<T> c = corr_args<T>(p, static_cast<const T *>(jv));
   if (!jv) c.jv = nullptr;
+  if (!p->legacy_dst) return box_passes_reg<CPLX>(p, a, rhs, sign, c, u, s);
   KFBI_TRY(launch(p, KFBI_K_ROWS, s, [&] {
     rows_fwd_kernel<CPLX><<<ntask, DST_THREADS, row, s>>>(a, rhs, sign, c);
   }));
@@ -523,7 +581,19 @@ kfbi_status kfbi_plan_create(const kfbi_grid_desc *desc, kfbi_plan **out) {
     double ang = (double)q * M_PI / (double)m;
     lam[q] = (2.0 * std::cos(ang) - 2.0) / (desc->h * desc->h);
   }
-  if ((e = upload(p->tw, tw.data(), tw.size())) != cudaSuccess ||
+  // register engine tables: exp(-2 pi i q / m) and sin(pi j / m), q, j < m
+  std::vector<double2> twg(m);
+  std::vector<double> sinv(m);
+  for (int q = 0; q < m; ++q) {
+    long double ang = 3.14159265358979323846264338327950288L * (long double)q / (long double)m;
+    twg[q] = make_double2((double)cosl(2.0L * ang), (double)-sinl(2.0L * ang));
+    sinv[q] = (double)sinl(ang);
+  }
+  const char *eng = getenv("KFBI_DST");
+  p->legacy_dst = eng && std::strcmp(eng, "legacy") == 0;
+  if ((e = upload(p->twg, twg.data(), twg.size())) != cudaSuccess ||
+      (e = upload(p->sinv, sinv.data(), sinv.size())) != cudaSuccess ||
+      (e = upload(p->tw, tw.data(), tw.size())) != cudaSuccess ||
       (e = upload(p->lam, lam.data(), lam.size())) != cudaSuccess ||
       (e = p->panels.ensure((size_t)m * m)) != cudaSuccess ||
       (e = p->st.ensure(1)) != cudaSuccess || (e = p->red.ensure(8)) != cudaSuccess) {
@@ -552,7 +622,7 @@ kfbi_status kfbi_plan_destroy(kfbi_plan *p) {
     cudaEventDestroy(pe.b);
   }
   for (auto e : p->pool) cudaEventDestroy(e);
-  p->tw.release(); p->lam.release(); p->panels.release();
+  p->tw.release(); p->lam.release(); p->panels.release(); p->twg.release(); p->sinv.release();
   p->W.release(); p->edge_axis.release(); p->rec_edge.release(); p->group_start.release();
   p->group_node.release(); p->row_group.release(); p->stencil.release(); p->rec_d.release();
   p->rec_sigma.release(); p->deriv_col.release(); p->speed.release(); p->tangent.release();

@@ -1,0 +1,48 @@
+"""GPU check of the box solve at every supported size: error against the
+oracle's scipy box solve and device time per solve.  Select the engine with
+KFBI_DST=legacy (shared-memory v2) or leave unset (register engine).
+
+    python tools/check_box.py [sizes...]
+"""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_2404_14864_b200 as k  # noqa: E402
+from oracle import kfbi_oracle as O  # noqa: E402
+
+sizes = [int(a) for a in sys.argv[1:]] or [16, 32, 64, 128, 256, 512, 1024, 2048, 4096]
+eng = os.environ.get("KFBI_DST", "register")
+rng = np.random.default_rng(0)
+for m in sizes:
+    grid = k.CartesianGrid((-1.5, 1.5, -1.5, 1.5), m)
+    for cplx in (False, True):
+        kappa = 2j * m if cplx else 2.0 * m
+        rhs = rng.standard_normal((m + 1, m + 1))
+        if cplx:
+            rhs = rhs + 1j * rng.standard_normal((m + 1, m + 1))
+        solver = k.BoxSolver(grid, kappa, "dirichlet-zero")
+        u = solver.solve(rhs)
+        ref = O.box_solve(m, grid.h, kappa, rhs)
+        err = np.max(np.abs(u - ref)) / np.max(np.abs(ref))
+        ring = max(np.max(np.abs(u[0])), np.max(np.abs(u[-1])), np.max(np.abs(u[:, 0])),
+                   np.max(np.abs(u[:, -1])))
+        rd = torch.from_numpy(rhs).cuda()
+        for _ in range(3):
+            solver.solve(rd)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = 20
+        a.record()
+        for _ in range(reps):
+            solver.solve(rd)
+        b.record()
+        torch.cuda.synchronize()
+        ms = a.elapsed_time(b) / reps
+        print(f"[{eng}] M={m:5d} {'c128' if cplx else 'f64 '} rel_err={err:.2e} ring={ring:.1e} "
+              f"{ms:.4f} ms/solve", flush=True)
