@@ -174,7 +174,7 @@ kfbi_status kfbi_extract(kfbi_plan *plan, int32_t dtype, const void *u,
 kfbi_status kfbi_richardson(kfbi_plan *plan, const kfbi_bvp *bvp,
                             kfbi_bvp_result *result, void *stream);
 
-/* Build the trace operator T (n_ctl x n_ctl, row-major) of the plan's
+/* Build the trace operator T (n_ctl x n_ctl, column-major) of the plan's
  * geometry for one kappa: column p is the sweep pipeline (jumps ->
  * corrections -> box solve -> extraction) applied to the unit density e_p
  * with F = 0, f_gamma = 0.  With kfbi_bvp.use_operator = 1, Richardson

@@ -13,7 +13,9 @@
 // (row 0 is padding).  Real: panel pp holds kx = 4pp..4pp+3,
 // P[(pp*M + j)*4 + w]; complex: kx = 2pp..2pp+1, P2[(pp*M + j)*2 + w].  A
 // column pass reads one M*32-byte slab (two CTAs per slab, one per 16-byte
-// half), a row task writes whole 32-byte sectors straight from registers.
+// half); a row pair of a real panel is one contiguous 64-byte chunk.  All
+// global traffic goes through the shared-memory staging buffer so that
+// consecutive lanes touch consecutive 16-byte pieces.
 //
 // One CTA = 256 threads = 256*16 complex elements in registers: one length-
 // 4096 sequence, or 4096/N shorter ones.  Real rows/columns are packed two
@@ -110,29 +112,26 @@ rows_fwd_reg(BoxArgs a, const void *__restrict__ rhs, double sign,
   __syncthreads();
   double2 out[reg::E];
   dst_staged<LOGN>(sm, scratch, t, a, out);
+  __syncthreads();
+#pragma unroll
+  for (int c = 0; c < reg::E; ++c) sm[reg::sw(reg::E * t + c)] = out[c];
+  __syncthreads();
   if (!valid) return;
-  // panel stores straight from registers: whole 32-byte sectors
+  // panel stores: consecutive lanes write consecutive 16-byte pieces of a
+  // panel's (row j0, row j0+1) 64-byte chunk (real) / 32-byte row (complex)
   double2 *P2 = static_cast<double2 *>(a.panels);
   if (!CPLX) {
-#pragma unroll
-    for (int g = 0; g < 4; ++g) {
-      const size_t pp = 4 * t + g;
-      double2 *d = P2 + (pp * M + j0) * 2;
-      d[0] = make_double2(out[4 * g].x, out[4 * g + 1].x);
-      d[1] = make_double2(out[4 * g + 2].x, out[4 * g + 3].x);
-      if (has2) {
-        d[2] = make_double2(out[4 * g].y, out[4 * g + 1].y);
-        d[3] = make_double2(out[4 * g + 2].y, out[4 * g + 3].y);
-      }
+    for (int i = t; i < M; i += TT) {          // M/4 panels x 4 pieces
+      const int pp = i >> 2, part = i & 3, row = part >> 1;
+      if (row && !has2) continue;
+      const int n0 = 4 * pp + 2 * (part & 1);
+      const double2 v0 = sm[reg::sw(n0)], v1 = sm[reg::sw(n0 + 1)];
+      P2[((size_t)pp * M + j0 + row) * 2 + (part & 1)] =
+          row ? make_double2(v0.y, v1.y) : make_double2(v0.x, v1.x);
     }
   } else {
-#pragma unroll
-    for (int g = 0; g < 8; ++g) {
-      const size_t pp = 8 * t + g;
-      double2 *d = P2 + (pp * M + j0) * 2;
-      d[0] = out[2 * g];
-      d[1] = out[2 * g + 1];
-    }
+    for (int i = t; i < M; i += TT)            // M/2 panels x 2 pieces
+      P2[((size_t)(i >> 1) * M + j0) * 2 + (i & 1)] = sm[reg::sw(i)];
   }
 }
 
@@ -185,9 +184,12 @@ __global__ void __launch_bounds__(reg::CTA, 2) cols_reg(BoxArgs a) {
   for (int c = 0; c < reg::E; ++c) sm[reg::sw(reg::E * t + c)] = out[c];
   __syncthreads();
   dst_staged<LOGN>(sm, scratch, t, a, out);
-  if (!valid) return;
+  __syncthreads();
 #pragma unroll
-  for (int c = 0; c < reg::E; ++c) col[2 * (reg::E * t + c)] = out[c];
+  for (int c = 0; c < reg::E; ++c) sm[reg::sw(reg::E * t + c)] = out[c];
+  __syncthreads();
+  if (!valid) return;
+  for (int n = t; n < M; n += TT) col[2 * n] = sm[reg::sw(n)];
 }
 
 // ---------------------------------------------------------------------------
@@ -207,22 +209,35 @@ __global__ void __launch_bounds__(reg::CTA, 2) rows_inv_reg(BoxArgs a, void *__r
   const int j0 = CPLX ? q + 1 : 2 * q + 1;
   const bool has2 = !CPLX && valid && j0 + 1 < M;
 
-  double2 v[reg::E];
+  const double2 *P2 = static_cast<const double2 *>(a.panels);
+  if (!CPLX) {
+    // lanes read consecutive 16-byte pieces of each panel's (j0, j0+1)
+    // 64-byte chunk and scatter them into the .x / .y halves of the slots
+    double2 v[reg::E];
 #pragma unroll
-  for (int m = 0; m < reg::E; ++m) {
-    const int n = t + m * TT;
-    v[m] = make_double2(0.0, 0.0);
-    if (valid && n >= 1) {
-      if (!CPLX) {
-        const double *s0 = static_cast<const double *>(a.panels) + ((size_t)(n >> 2) * M + j0) * 4 + (n & 3);
-        v[m].x = s0[0];
-        if (has2) v[m].y = s0[4];
-      } else {
-        v[m] = static_cast<const double2 *>(a.panels)[((size_t)(n >> 1) * M + j0) * 2 + (n & 1)];
-      }
+    for (int m = 0; m < reg::E; ++m) {
+      const int i = t + m * TT, pp = i >> 2, part = i & 3, row = part >> 1;
+      v[m] = (valid && (has2 || !row)) ? P2[((size_t)pp * M + j0 + row) * 2 + (part & 1)]
+                                       : make_double2(0.0, 0.0);
     }
+#pragma unroll
+    for (int m = 0; m < reg::E; ++m) {
+      const int i = t + m * TT, pp = i >> 2, part = i & 3, row = part >> 1;
+      const int n0 = 4 * pp + 2 * (part & 1);
+      double *s0 = reinterpret_cast<double *>(&sm[reg::sw(n0)]) + row;
+      double *s1 = reinterpret_cast<double *>(&sm[reg::sw(n0 + 1)]) + row;
+      *s0 = n0 == 0 ? 0.0 : v[m].x;            // x_0 = 0
+      *s1 = v[m].y;
+    }
+  } else {
+    double2 v[reg::E];
+#pragma unroll
+    for (int m = 0; m < reg::E; ++m) {
+      const int n = t + m * TT;
+      v[m] = (valid && n >= 1) ? P2[((size_t)(n >> 1) * M + j0) * 2 + (n & 1)] : make_double2(0.0, 0.0);
+    }
+    stage<LOGN>(sm, v, t);
   }
-  stage<LOGN>(sm, v, t);
   __syncthreads();
   double2 out[reg::E];
   dst_staged<LOGN>(sm, scratch, t, a, out);

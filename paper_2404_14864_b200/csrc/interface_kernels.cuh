@@ -374,156 +374,139 @@ __global__ void unit_vector_kernel(T *v, int n, int p) {
     v[i] = (i == p) ? Sc<T>::one() : Sc<T>::zero();
 }
 
-// Top[q * n + p] = out[q]  (u+ row of an extraction)
+// Column p of the trace operator, stored column-major: Tcm[p * n + q] = out[q].
 template <typename T>
-__global__ void op_column_kernel(int n, int p, const T *out, T *Top) {
+__global__ void op_column_kernel(int n, int p, const T *out, T *Tcm) {
   const int q = blockIdx.x * blockDim.x + threadIdx.x;
-  if (q < n) Top[(size_t)q * n + p] = out[q];
+  if (q < n) Tcm[(size_t)p * n + q] = out[q];
 }
 
-// trace[q] = trace1[q] + sum_p Top[q][p] (phi[p] - phi0[p])   (warp per row)
-template <typename T>
-__global__ void __launch_bounds__(256)
-op_trace_kernel(int n, const T *__restrict__ Top, const T *__restrict__ phi,
-                const T *__restrict__ phi0, const T *__restrict__ trace1, T *trace,
-                const int *done) {
-  using S = Sc<T>;
-  if (*done) return;
-  const int lane = threadIdx.x & 31;
-  const int q = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (q >= n) return;
-  const T *row = Top + (size_t)q * n;
-  T acc = S::zero();
-  for (int p = lane; p < n; p += 32) acc = S::add(acc, S::mul(row[p], S::sub(phi[p], phi0[p])));
-  acc = warp_reduce_T(acc);
-  if (lane == 0) trace[q] = S::add(trace1[q], acc);
-}
-
-// phi_prev = phi; upd = gamma (g - trace); phi += upd; residual max |upd|.
-template <typename T>
-__global__ void __launch_bounds__(256)
-op_update_kernel(int n, const T *__restrict__ g, const T *__restrict__ trace, T *phi,
-                 T *phi_prev, double gamma, RichState *st, double *history) {
-  using S = Sc<T>;
-  if (st->done) return;
-  const int p = blockIdx.x * blockDim.x + threadIdx.x;
-  double mag = 0.0;
-  if (p < n) {
-    const T ph = phi[p];
-    T upd = S::rmul(S::sub(g[p], trace[p]), gamma);
-    phi_prev[p] = ph;
-    phi[p] = S::add(ph, upd);
-    mag = S::abs(upd);
-  }
-  sweep_close(mag, st, history);
-}
-
-// One whole operator sweep in one launch.  A warp owns RW rows q:
+// All operator sweeps of one solve in ONE cooperative launch, with the trace
+// operator held on chip across the sweeps (bvp.py:312-344 semantics).
+//
+// CTA c owns rows [c R, c R + R) of T (one CTA per SM); lane = row within a
+// 32-row tile, warp w = columns w, w + NW, ...  Per sweep
 //   trace_q = trace1_q + sum_p T[q][p] (phi_in[p] - phi0[p])
 //   upd_q   = gamma (g_q - trace_q);  phi_out[q] = phi_in[q] + upd_q
-// A row's update needs only its own trace, so the densities ping-pong
-// between two buffers (phi_in is read-only during the sweep).
-template <typename T, int RW>
-__global__ void __launch_bounds__(256)
-op_sweep_kernel(int n, const T *__restrict__ Top, const T *__restrict__ phi_in,
-                const T *__restrict__ phi0, const T *__restrict__ trace1,
-                const T *__restrict__ g, T *__restrict__ phi_out, double gamma, RichState *st,
-                double *history) {
-  using S = Sc<T>;
-  if (st->done) return;
-  const int lane = threadIdx.x & 31;
-  const int q0 = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * RW;
-  T acc[RW];
-#pragma unroll
-  for (int r = 0; r < RW; ++r) acc[r] = S::zero();
-  if (q0 < n) {
-    const T *rows[RW];
-#pragma unroll
-    for (int r = 0; r < RW; ++r) rows[r] = Top + (size_t)min(q0 + r, n - 1) * n;
-#pragma unroll 8
-    for (int p = lane; p < n; p += 32) {
-      const T d = S::sub(phi_in[p], phi0[p]);
-#pragma unroll
-      for (int r = 0; r < RW; ++r) acc[r] = S::add(acc[r], S::mul(__ldcg(rows[r] + p), d));
-    }
-  }
-#pragma unroll
-  for (int r = 0; r < RW; ++r) acc[r] = warp_reduce_T(acc[r]);
-  double mag = 0.0;
-  if (lane < RW && q0 + lane < n) {
-    const int q = q0 + lane;
-    T a = acc[0];
-#pragma unroll
-    for (int r = 1; r < RW; ++r)
-      if (lane == r) a = acc[r];
-    const T trace = S::add(trace1[q], a);
-    const T upd = S::rmul(S::sub(g[q], trace), gamma);
-    phi_out[q] = S::add(phi_in[q], upd);
-    mag = S::abs(upd);
-  }
-  sweep_close(mag, st, history);
-}
-
-// All operator sweeps of one solve in ONE cooperative launch.  Sweep idx
-// (0-based, idx >= 1) reads phi_idx from A (idx odd) or B (idx even) and
-// writes phi_(idx+1) to the other buffer; warps stride over the rows.  The
-// sweep's max |update| goes to slot idx % 3 (block 0 clears slot
-// (idx+1) % 3, last read two sweeps ago), one grid barrier, then every CTA
-// reads the same max and takes the same decision (bvp.py:333-344).
+// T's columns are split three ways: [0, Creg) live in registers (K per
+// thread, first row tile), [Creg, Creg + Cs) in shared memory, the rest is
+// streamed from L2 (column segments of R rows are contiguous in the
+// column-major layout).  The densities ping-pong between A and B: sweep idx
+// reads A (idx odd) or B (idx even).  The sweep's max |update| goes to slot
+// idx % 3 (block 0 clears slot (idx+1) % 3), one grid barrier, then every
+// CTA reads the same max and takes the same decision.
 struct OpSolveArgs {
   int n, first_idx, max_iter;
   double gamma, tol;
   RichState *st;
   double *history;
   unsigned long long *slots;      // [3]
+  int rows;                       // R, rows per CTA
+  int smem_cols;                  // Cs
 };
 
+constexpr int OP_THREADS = 512;
+constexpr int OP_WARPS = OP_THREADS / 32;
+constexpr int OP_UNROLL = 8;
+
 template <typename T>
-__global__ void __launch_bounds__(256)
-op_solve_kernel(OpSolveArgs a, const T *__restrict__ Top, T *A, T *B,
+inline size_t op_smem_fixed(int n) {
+  return ((size_t)((n + 1) & ~1) + OP_WARPS * 32) * sizeof(T);
+}
+
+template <typename T, int K>
+__global__ void __launch_bounds__(OP_THREADS, 1)
+op_solve_kernel(OpSolveArgs a, const T *__restrict__ Tcm, T *A, T *B,
                 const T *__restrict__ phi0, const T *__restrict__ trace1,
                 const T *__restrict__ g) {
   using S = Sc<T>;
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
-  __shared__ double red[8];
+  extern __shared__ __align__(16) unsigned char op_smem[];
+  __shared__ double res_s;
+  const int n = a.n, R = a.rows, Cs = a.smem_cols;
+  T *d = reinterpret_cast<T *>(op_smem);                 // phi_in - phi0, [n]
+  T *part = d + ((n + 1) & ~1);                          // [OP_WARPS][32]
+  T *cache = part + OP_WARPS * 32;                       // [Cs][R], column-major
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int r0 = blockIdx.x * R;
+  const int nr = max(0, min(R, n - r0));
+  const int creg = min(n, OP_WARPS * K);
+  const int cs0 = creg, cg0 = min(n, creg + Cs);
+
+  T treg[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const int c = warp + OP_WARPS * k;
+    treg[k] = (lane < nr && c < creg) ? Tcm[(size_t)c * n + r0 + lane] : S::zero();
+  }
+  for (int i = tid; i < (cg0 - cs0) * R; i += OP_THREADS) {
+    const int c = cs0 + i / R, r = i - (i / R) * R;
+    cache[i] = r < nr ? Tcm[(size_t)c * n + r0 + r] : S::zero();
+  }
   if (a.st->done) return;                       // uniform: set before launch
-  const int n = a.n;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+
   for (int idx = a.first_idx; idx < a.max_iter; ++idx) {
     const T *in = (idx & 1) ? A : B;
     T *out = (idx & 1) ? B : A;
+    for (int p = tid; p < n; p += OP_THREADS) d[p] = S::sub(__ldcg(in + p), phi0[p]);
+    __syncthreads();
     double mag = 0.0;
-    for (int q = gwarp; q < n; q += nwarps) {
-      const T acc = warp_row_dot<T, 8>(Top + (size_t)q * n, in, phi0, n, lane);
-      if (lane == 0) {
-        const T trace = S::add(trace1[q], acc);
+    for (int rt = 0; rt < nr; rt += 32) {       // row tiles (one unless R > 32)
+      const int row = rt + lane;
+      const bool rok = row < nr;
+      T acc = S::zero();
+      if (rt == 0) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          const int c = warp + OP_WARPS * k;
+          if (c < creg) acc = S::add(acc, S::mul(treg[k], d[c]));
+        }
+      }
+      if (rok)
+        for (int c = cs0 + warp; c < cg0; c += OP_WARPS)
+          acc = S::add(acc, S::mul(cache[(size_t)(c - cs0) * R + row], d[c]));
+      for (int c = cg0 + warp; c < n; c += OP_WARPS * OP_UNROLL) {
+        T v[OP_UNROLL];
+#pragma unroll
+        for (int u = 0; u < OP_UNROLL; ++u) {
+          const int cc = c + OP_WARPS * u;
+          v[u] = (rok && cc < n) ? __ldcg(Tcm + (size_t)cc * n + r0 + row) : S::zero();
+        }
+#pragma unroll
+        for (int u = 0; u < OP_UNROLL; ++u) {
+          const int cc = c + OP_WARPS * u;
+          if (cc < n) acc = S::add(acc, S::mul(v[u], d[cc]));
+        }
+      }
+      part[warp * 32 + lane] = acc;
+      __syncthreads();
+      if (tid < 32 && rt + tid < nr) {
+        const int q = r0 + rt + tid;
+        T s = part[tid];
+        for (int w = 1; w < OP_WARPS; ++w) s = S::add(s, part[w * 32 + tid]);
+        const T trace = S::add(trace1[q], s);
         const T upd = S::rmul(S::sub(g[q], trace), a.gamma);
-        out[q] = S::add(in[q], upd);
+        out[q] = S::add(__ldcg(in + q), upd);
         mag = nanmax(mag, S::abs(upd));
       }
+      __syncthreads();
     }
-    mag = warp_nanmax(mag);
-    if (lane == 0) red[wid] = mag;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      double m = red[0];
-      for (int w = 1; w < (int)(blockDim.x >> 5); ++w) m = nanmax(m, red[w]);
-      atomic_max_nonneg(&a.slots[idx % 3], m);
-      if (blockIdx.x == 0) a.slots[(idx + 1) % 3] = 0ull;
+    if (warp == 0) {
+      mag = warp_nanmax(mag);
+      if (lane == 0) {
+        atomic_max_nonneg(&a.slots[idx % 3], mag);
+        if (blockIdx.x == 0) a.slots[(idx + 1) % 3] = 0ull;
+      }
     }
     grid.sync();
-    // one L2 read per block (an atomic per thread would serialise ~1e5
-    // operations on one address)
-    __shared__ double res_s;
-    if (threadIdx.x == 0) res_s = __longlong_as_double((long long)__ldcg(&a.slots[idx % 3]));
+    // one L2 read per block (an atomic per thread would serialise)
+    if (tid == 0) res_s = __longlong_as_double((long long)__ldcg(&a.slots[idx % 3]));
     __syncthreads();
     const double res = res_s;
     const bool conv = res <= a.tol;
     const bool last = conv || idx + 1 >= a.max_iter;
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (blockIdx.x == 0 && tid == 0) {
       a.history[idx] = res;
       a.st->iters = idx + 1;
       a.st->last_res = res;

@@ -469,40 +469,33 @@ kfbi_status build_operator_T(kfbi_plan *p, double kre, double kim, cudaStream_t 
   return KFBI_OK;
 }
 
-// Operator sweeps k >= 2 (trace = trace_1 + T (phi - phi_0), then the update).
-template <typename T>
-kfbi_status op_sweep(kfbi_plan *p, const kfbi_bvp *b, int idx, cudaStream_t s) {
-  // sweep idx >= 1 (0-based) reads phi_(idx) and writes phi_(idx+1); the
-  // densities alternate between b->density (even idx reads it) and phi_prev
-  constexpr int RW = 1;
-  const int n = p->n_ctl;
-  T *A = static_cast<T *>(b->density), *B = reinterpret_cast<T *>(p->phi_prev.p);
-  T *in = (idx & 1) ? A : B, *out = (idx & 1) ? B : A;
-  const int warps = (n + RW - 1) / RW;
-  return launch(p, KFBI_K_DENSITY, s, [&] {
-    op_sweep_kernel<T, RW><<<(warps * 32 + 255) / 256, 256, 0, s>>>(
-        n, reinterpret_cast<const T *>(p->Top.p), in, reinterpret_cast<const T *>(p->phi0.p),
-        reinterpret_cast<const T *>(p->trace1.p), static_cast<const T *>(b->g), out, b->gamma,
-        p->st.p, p->history.p);
-  });
-}
-
-// All operator sweeps of one solve: one cooperative launch (op_solve_kernel).
+// All operator sweeps of one solve: one cooperative launch (op_solve_kernel),
+// T resident on chip (registers + shared memory) across the sweeps.
 template <typename T>
 kfbi_status op_solve(kfbi_plan *p, const kfbi_bvp *b, cudaStream_t s) {
-  static int blocks_per_sm[2] = {0, 0};
-  constexpr int CP = std::is_same<T, double2>::value ? 1 : 0;
-  if (!blocks_per_sm[CP]) {
-    int nb = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, op_solve_kernel<T>, 256, 0);
-    blocks_per_sm[CP] = nb < 1 ? 1 : (nb > 4 ? 4 : nb);
+  constexpr int K = std::is_same<T, double2>::value ? 16 : 32;
+  static int smem_optin = 0, sms = 0;
+  if (!smem_optin) {
+    cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, p->device);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->device);
+    KFBI_CUDA(cudaFuncSetAttribute(op_solve_kernel<T, K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   smem_optin - 1024), "density-update");
   }
-  int sms = 0;
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->device);
+  const int n = p->n_ctl;
+  int rows = (n + sms - 1) / sms;
+  const int grid = (n + rows - 1) / rows;
+  const size_t fixed = op_smem_fixed<T>(n);
+  const size_t avail = (size_t)(smem_optin - 1024) > fixed ? (size_t)(smem_optin - 1024) - fixed : 0;
+  const int creg = n < OP_WARPS * K ? n : OP_WARPS * K;
+  size_t cs = avail / ((size_t)rows * sizeof(T));
+  if (cs > (size_t)(n - creg)) cs = (size_t)(n - creg);
+  const size_t smem = fixed + cs * rows * sizeof(T);
+  if (fixed > (size_t)(smem_optin - 1024))
+    return fail(KFBI_E_CONFIG, "operator form: n_ctl too large for the on-chip sweep kernel");
   unsigned long long *slots = p->red.p + 4;
   KFBI_CUDA(cudaMemsetAsync(slots, 0, 3 * sizeof(unsigned long long), s), "density-update");
   OpSolveArgs a;
-  a.n = p->n_ctl;
+  a.n = n;
   a.first_idx = 1;
   a.max_iter = b->max_iter;
   a.gamma = b->gamma;
@@ -510,15 +503,17 @@ kfbi_status op_solve(kfbi_plan *p, const kfbi_bvp *b, cudaStream_t s) {
   a.st = p->st.p;
   a.history = p->history.p;
   a.slots = slots;
-  const T *Top = reinterpret_cast<const T *>(p->Top.p);
+  a.rows = rows;
+  a.smem_cols = (int)cs;
+  const T *Tcm = reinterpret_cast<const T *>(p->Top.p);
   T *A = static_cast<T *>(b->density), *B = reinterpret_cast<T *>(p->phi_prev.p);
   const T *phi0 = reinterpret_cast<const T *>(p->phi0.p);
   const T *tr1 = reinterpret_cast<const T *>(p->trace1.p);
   const T *g = static_cast<const T *>(b->g);
-  void *args[] = {&a, (void *)&Top, &A, &B, (void *)&phi0, (void *)&tr1, (void *)&g};
+  void *args[] = {&a, (void *)&Tcm, &A, &B, (void *)&phi0, (void *)&tr1, (void *)&g};
   return launch(p, KFBI_K_DENSITY, s, [&] {
-    cudaLaunchCooperativeKernel((const void *)op_solve_kernel<T>, dim3(sms * blocks_per_sm[CP]),
-                                dim3(256), args, 0, s);
+    cudaLaunchCooperativeKernel((const void *)op_solve_kernel<T, K>, dim3(grid), dim3(OP_THREADS), args,
+                                smem, s);
   });
 }
 
@@ -828,24 +823,15 @@ kfbi_status kfbi_richardson(kfbi_plan *p, const kfbi_bvp *b, kfbi_bvp_result *re
       int nb = batch;
       if (nb > b->max_iter - enqueued) nb = b->max_iter - enqueued;
       for (int k = 0; k < nb; ++k) {
-        const int idx = enqueued + k;      // 0-based sweep index
-        if (idx == 0 || !use_op) {
-          if (cplx) KFBI_TRY(sweep<double2>(p, b, s));
-          else KFBI_TRY(sweep<double>(p, b, s));
-          if (idx == 0 && use_op)
-            KFBI_CUDA(cudaMemcpyAsync(p->trace1.p, b->trace_u, p->n_ctl * es, cudaMemcpyDeviceToDevice, s),
-                      "density-update");
-        } else {
-          if (cplx) KFBI_TRY(op_sweep<double2>(p, b, idx, s));
-          else KFBI_TRY(op_sweep<double>(p, b, idx, s));
-        }
+        if (cplx) KFBI_TRY(sweep<double2>(p, b, s));
+        else KFBI_TRY(sweep<double>(p, b, s));
       }
       enqueued += nb;
       KFBI_CUDA(cudaMemcpyAsync(p->st_host, p->st.p, sizeof(RichState), cudaMemcpyDeviceToHost, s),
                 "density-update");
       KFBI_CUDA(cudaStreamSynchronize(s), "density-update");
       if (p->st_host->done != 0 || enqueued >= b->max_iter) break;
-      batch = use_op ? 8 : 2;
+      batch = 2;
     }
   }
   if (use_op && p->st_host->iters >= 2) {

@@ -1,12 +1,14 @@
 """Per-instruction hot spots from an ncu report's SASS source page.
 
-    python tools/ncu_src.py report.ncu-rep kernel_regex [top]
+    python tools/ncu_src.py report.ncu-rep kernel_regex [top] [launch_skip]
 Prints the instructions with the most stall samples and the shared-memory
 instructions with excessive wavefronts (bank conflicts)."""
 import csv, io, subprocess, sys
 rep, kern = sys.argv[1], sys.argv[2]
 top = int(sys.argv[3]) if len(sys.argv) > 3 else 25
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--kernel-name", "regex:" + kern],
+skip = sys.argv[4] if len(sys.argv) > 4 else "0"
+out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--kernel-name", "regex:" + kern,
+                      "--launch-skip", skip, "--launch-count", "1"],
                      capture_output=True, text=True).stdout
 lines = out.splitlines()
 rows = list(csv.reader(io.StringIO("\n".join(lines[1:]))))
