@@ -222,6 +222,17 @@ kfbi_status kfbi_nonlinear_phase(kfbi_plan *plan, int64_t n, const void *ustar,
                                  double kappa_im, void *F, double *max_res,
                                  void *stream);
 
+/* Strang B-phase of one step with u* formed inline: u* = u - (i tau/2) other
+ * (mode 0, first step, other = lap u0) or 2u - other (mode 1, other = u** of
+ * the previous step) (timestepping.py:410-418), then the pointwise Newton of
+ * kfbi_nonlinear_phase on u*.  Same results as kfbi_schr_ustar followed by
+ * kfbi_nonlinear_phase, without the full-grid u* round trip. */
+kfbi_status kfbi_strang_phase(kfbi_plan *plan, int64_t n, int32_t mode, const void *u,
+                              const void *other, double tau, const double *v, double w,
+                              double half_tau, const uint8_t *mask, void *out,
+                              double kappa_re, double kappa_im, void *F,
+                              double *max_res, void *stream);
+
 /* u <- mask*u and max|u| (np.where(ctx.mask, sol.u, 0) + check_stable). */
 kfbi_status kfbi_mask_norm(kfbi_plan *plan, int32_t dtype, int64_t n,
                            const uint8_t *mask, void *u, double *norm_out,

@@ -94,6 +94,8 @@ _SIGNATURES = {
     "kfbi_schr_ustar": ([vp, i64, i32, vp, vp, f64, vp, vp], i32),
     "kfbi_nonlinear_phase": ([vp, i64, vp, vp, f64, f64, vp, vp, f64, f64, vp,
                               C.POINTER(f64), vp], i32),
+    "kfbi_strang_phase": ([vp, i64, i32, vp, vp, f64, vp, f64, f64, vp, vp, f64, f64, vp,
+                           C.POINTER(f64), vp], i32),
     "kfbi_mask_norm": ([vp, i32, i64, vp, vp, C.POINTER(f64), vp], i32),
     "kfbi_kernel_times": ([vp, C.POINTER(f64), C.POINTER(i64)], i32),
     "kfbi_reset_kernel_times": ([vp], i32),

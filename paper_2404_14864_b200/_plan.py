@@ -204,6 +204,22 @@ class Plan:
         N.check(status, iterations=50, last_residual=res.value)
         return res.value
 
+    def strang_phase(self, n, mode, u, other, tau, v, w, half_tau, mask, out, kappa=None,
+                     F=None, log_slot=None):
+        """schr_ustar + nonlinear_phase in one pass (kfbi_strang_phase)."""
+        k = complex(kappa) if kappa is not None else 0j
+        res = C.c_double(0.0)
+        status = self._lib.kfbi_strang_phase(
+            self.handle, int(n), int(mode), u.data_ptr(), other.data_ptr(), float(tau),
+            v.data_ptr(), float(w), float(half_tau), N.ptr(mask), out.data_ptr(), k.real, k.imag,
+            N.ptr(F), None if log_slot is not None else C.byref(res), self.stream)
+        if log_slot is not None:
+            N.check(status)
+            self.log_norm(log_slot, which=1)
+            return None
+        N.check(status, iterations=50, last_residual=res.value)
+        return res.value
+
     def mask_norm(self, n, mask, u, want_norm=True):
         norm = C.c_double(0.0)
         N.check(self._lib.kfbi_mask_norm(self.handle, self._dt(u.is_complex()), int(n),

@@ -168,17 +168,21 @@ __global__ void jumps_d2_kernel(CtlGeom g, const T *__restrict__ phi, const T *_
 // A warp owns EW consecutive edges and streams their W rows once.
 struct EdgeArgs {
   int n_edges, n_ctl, ld;         // ld: row stride of W (even)
+  int per_warp;                   // edges per warp (<= EW of the launch)
   const double *W;
   const signed char *axis;
 };
 
-template <typename T, int EW>
+template <typename T, int EW, int U>
 __global__ void __launch_bounds__(256)
 corr_edges_kernel(EdgeArgs ea, const T *__restrict__ jm, T *jv, const int *done) {
   using S = Sc<T>;
   if (done && *done) return;
   const int lane = threadIdx.x & 31;
-  const int e0 = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * EW;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  // balanced contiguous ranges of <= EW edges per warp (ea.per_warp)
+  const int e0 = gw * ea.per_warp;
+  const int e_end = min(e0 + ea.per_warp, ea.n_edges);
   if (e0 >= ea.n_edges) return;
   const int n = ea.n_ctl;
   const T *ju = jm, *jx = jm + n, *jy = jm + 2 * n, *jxx = jm + 3 * n, *jyy = jm + 5 * n;
@@ -186,7 +190,7 @@ corr_edges_kernel(EdgeArgs ea, const T *__restrict__ jm, T *jv, const int *done)
   const double *wr[EW];
 #pragma unroll
   for (int q = 0; q < EW; ++q) {
-    int e = min(e0 + q, ea.n_edges - 1);
+    int e = min(e0 + q, e_end - 1);
     vert[q] = ea.axis[e] != 0;
     wr[q] = ea.W + (size_t)e * ea.ld;
   }
@@ -198,7 +202,6 @@ corr_edges_kernel(EdgeArgs ea, const T *__restrict__ jm, T *jv, const int *done)
   // U iterations of EW rows are loaded before any is used: U*EW 16-byte
   // streaming loads in flight per lane (the compiler does not hoist them
   // across the FMA chains on its own).
-  constexpr int U = 4;
   const int n2 = ea.ld >> 1;
   for (int i0 = lane; i0 < n2; i0 += 32 * U) {
     double2 w2[U][EW];
@@ -234,7 +237,7 @@ corr_edges_kernel(EdgeArgs ea, const T *__restrict__ jm, T *jv, const int *done)
   if (lane == 0) {
 #pragma unroll
     for (int q = 0; q < EW; ++q) {
-      if (e0 + q < ea.n_edges) {
+      if (e0 + q < e_end) {
         jv[3 * (e0 + q)] = acc[q][0];
         jv[3 * (e0 + q) + 1] = acc[q][1];
         jv[3 * (e0 + q) + 2] = acc[q][2];

@@ -359,14 +359,23 @@ kfbi_status jumps_T(kfbi_plan *p, double kre, double kim, const void *phi, const
 
 template <typename T>
 kfbi_status edges_T(kfbi_plan *p, const void *jm, void *jv, const int *done, cudaStream_t s) {
-  EdgeArgs ea{p->n_edges, p->n_ctl, p->w_ld, p->W.p, p->edge_axis.p};
-  constexpr int EW = 4;
-  const int warps = (p->n_edges + EW - 1) / EW;
+  // one wave of 2 CTAs per SM, the edges spread evenly over its warps in
+  // contiguous ranges of at most EW (a partial second wave ran on half the
+  // SMs); larger problems use more waves of full ranges
+  constexpr int EW = std::is_same<T, double2>::value ? 4 : 8, U = 2;
+  static int sms = 0;
+  if (!sms) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->device);
+  const int wave_warps = sms * 2 * 8;
+  int per_warp = (p->n_edges + wave_warps - 1) / wave_warps;
+  if (per_warp > EW) per_warp = EW;
+  if (per_warp < 1) per_warp = 1;
+  EdgeArgs ea{p->n_edges, p->n_ctl, p->w_ld, per_warp, p->W.p, p->edge_axis.p};
+  const int warps = (p->n_edges + per_warp - 1) / per_warp;
   const int blocks = (warps + 7) / 8;
   if (p->n_edges == 0) return KFBI_OK;
   return launch(p, KFBI_K_JUMPS, s, [&] {
-    corr_edges_kernel<T, EW><<<blocks, 256, 0, s>>>(ea, static_cast<const T *>(jm),
-                                                    static_cast<T *>(jv), done);
+    corr_edges_kernel<T, EW, U><<<blocks, 256, 0, s>>>(ea, static_cast<const T *>(jm),
+                                                       static_cast<T *>(jv), done);
   });
 }
 
@@ -386,6 +395,20 @@ int elem_blocks(long n) {
   if (b > 148 * 16) b = 148 * 16;
   if (b < 1) b = 1;
   return (int)b;
+}
+
+// grid of the two-elements-per-step passes (elementwise_pairs)
+int pair_blocks(long n) {
+  long b = (n + 1023) / 1024;
+  if (b > 148 * 8) b = 148 * 8;
+  if (b < 1) b = 1;
+  return (int)b;
+}
+
+bool aligned16(std::initializer_list<const void *> ptrs) {
+  for (const void *q : ptrs)
+    if (q && (reinterpret_cast<uintptr_t>(q) & 15)) return false;
+  return true;
 }
 
 // One Richardson sweep, every kernel guarded by the device `done` flag.
@@ -918,9 +941,13 @@ kfbi_status kfbi_heat_rhs(kfbi_plan *p, int64_t n, const uint8_t *mask, void *u,
   cudaStream_t s = (cudaStream_t)stream;
   KFBI_CUDA(cudaMemsetAsync(p->red.p, 0, sizeof(unsigned long long), s), "rhs-update");
   KFBI_TRY(launch(p, KFBI_K_RHS, s, [&] {
-    heat_rhs_kernel<<<elem_blocks(n), 256, 0, s>>>(n, mask, static_cast<double *>(u),
-                                                   static_cast<const double *>(F_old),
-                                                   static_cast<double *>(F_new), a, p->red.p);
+    auto *uu = static_cast<double *>(u);
+    auto *fo = static_cast<const double *>(F_old);
+    auto *fn = static_cast<double *>(F_new);
+    if (aligned16({uu, fo, fn}) && !((uintptr_t)mask & 1))
+      heat_rhs_kernel<true><<<pair_blocks(n), 256, 0, s>>>(n, mask, uu, fo, fn, a, p->red.p);
+    else
+      heat_rhs_kernel<false><<<elem_blocks(n), 256, 0, s>>>(n, mask, uu, fo, fn, a, p->red.p);
   }));
   return norm_out ? read_norm(p, s, norm_out) : KFBI_OK;
 }
@@ -932,10 +959,15 @@ kfbi_status kfbi_wave_rhs(kfbi_plan *p, int64_t n, const uint8_t *mask, void *u_
   cudaStream_t s = (cudaStream_t)stream;
   KFBI_CUDA(cudaMemsetAsync(p->red.p, 0, sizeof(unsigned long long), s), "rhs-update");
   KFBI_TRY(launch(p, KFBI_K_RHS, s, [&] {
-    wave_rhs_kernel<<<elem_blocks(n), 256, 0, s>>>(
-        n, mask, static_cast<double *>(u_next), static_cast<const double *>(u_curr),
-        static_cast<const double *>(F_curr), static_cast<const double *>(F_prev),
-        static_cast<double *>(F_new), kw, coef, p->red.p);
+    auto *un = static_cast<double *>(u_next);
+    auto *uc = static_cast<const double *>(u_curr);
+    auto *fc = static_cast<const double *>(F_curr);
+    auto *fp = static_cast<const double *>(F_prev);
+    auto *fn = static_cast<double *>(F_new);
+    if (aligned16({un, uc, fc, fp, fn}) && !((uintptr_t)mask & 1))
+      wave_rhs_kernel<true><<<pair_blocks(n), 256, 0, s>>>(n, mask, un, uc, fc, fp, fn, kw, coef, p->red.p);
+    else
+      wave_rhs_kernel<false><<<elem_blocks(n), 256, 0, s>>>(n, mask, un, uc, fc, fp, fn, kw, coef, p->red.p);
   }));
   return norm_out ? read_norm(p, s, norm_out) : KFBI_OK;
 }
@@ -959,13 +991,38 @@ kfbi_status kfbi_nonlinear_phase(kfbi_plan *p, int64_t n, const void *ustar, con
   KFBI_CUDA(cudaMemsetAsync(p->red.p, 0, sizeof(unsigned long long), s), "rhs-update");
   KFBI_TRY(launch(p, KFBI_K_RHS, s, [&] {
     nonlinear_phase_kernel<<<elem_blocks(n), 256, 0, s>>>(
-        n, static_cast<const double2 *>(ustar), v, w, half_tau, mask, static_cast<double2 *>(out),
-        kre, kim, static_cast<double2 *>(F), p->red.p);
+        n, static_cast<const double2 *>(ustar), nullptr, 0, 0.0, v, w, half_tau, mask,
+        static_cast<double2 *>(out), kre, kim, static_cast<double2 *>(F), p->red.p);
   }));
   if (!max_res) return KFBI_OK;    // asynchronous: the caller logs red[0] (kfbi_log_norm)
   double r = 0.0;
   KFBI_TRY(read_norm(p, s, &r));
   if (max_res) *max_res = r;
+  if (r > NEWTON_TOL || r != r) {
+    char msg[160];
+    std::snprintf(msg, sizeof msg, "pointwise Newton solve stalled at residual %.3e", r);
+    return fail(KFBI_E_NOCONV, msg);
+  }
+  return KFBI_OK;
+}
+
+kfbi_status kfbi_strang_phase(kfbi_plan *p, int64_t n, int32_t mode, const void *u, const void *other,
+                              double tau, const double *v, double w, double half_tau,
+                              const uint8_t *mask, void *out, double kre, double kim, void *F,
+                              double *max_res, void *stream) {
+  KFBI_TRY(check_plan(p));
+  if (!other) return fail(KFBI_E_CONFIG, "kfbi_strang_phase: `other` is required");
+  cudaStream_t s = (cudaStream_t)stream;
+  KFBI_CUDA(cudaMemsetAsync(p->red.p, 0, sizeof(unsigned long long), s), "rhs-update");
+  KFBI_TRY(launch(p, KFBI_K_RHS, s, [&] {
+    nonlinear_phase_kernel<<<elem_blocks(n), 256, 0, s>>>(
+        n, static_cast<const double2 *>(u), static_cast<const double2 *>(other), mode, tau, v, w,
+        half_tau, mask, static_cast<double2 *>(out), kre, kim, static_cast<double2 *>(F), p->red.p);
+  }));
+  if (!max_res) return KFBI_OK;
+  double r = 0.0;
+  KFBI_TRY(read_norm(p, s, &r));
+  *max_res = r;
   if (r > NEWTON_TOL || r != r) {
     char msg[160];
     std::snprintf(msg, sizeof msg, "pointwise Newton solve stalled at residual %.3e", r);
@@ -981,11 +1038,19 @@ kfbi_status kfbi_mask_norm(kfbi_plan *p, int32_t dtype, int64_t n, const uint8_t
   KFBI_CUDA(cudaMemsetAsync(p->red.p, 0, sizeof(unsigned long long), s), "rhs-update");
   if (dtype == KFBI_C128)
     KFBI_TRY(launch(p, KFBI_K_RHS, s, [&] {
-      mask_norm_kernel<double2><<<elem_blocks(n), 256, 0, s>>>(n, mask, static_cast<double2 *>(u), p->red.p);
+      auto *uu = static_cast<double2 *>(u);
+      if (!((uintptr_t)mask & 1))
+        mask_norm_kernel<double2, true><<<pair_blocks(n), 256, 0, s>>>(n, mask, uu, p->red.p);
+      else
+        mask_norm_kernel<double2, false><<<elem_blocks(n), 256, 0, s>>>(n, mask, uu, p->red.p);
     }));
   else
     KFBI_TRY(launch(p, KFBI_K_RHS, s, [&] {
-      mask_norm_kernel<double><<<elem_blocks(n), 256, 0, s>>>(n, mask, static_cast<double *>(u), p->red.p);
+      auto *uu = static_cast<double *>(u);
+      if (aligned16({uu}) && !((uintptr_t)mask & 1))
+        mask_norm_kernel<double, true><<<pair_blocks(n), 256, 0, s>>>(n, mask, uu, p->red.p);
+      else
+        mask_norm_kernel<double, false><<<elem_blocks(n), 256, 0, s>>>(n, mask, uu, p->red.p);
     }));
   return norm_out ? read_norm(p, s, norm_out) : KFBI_OK;
 }

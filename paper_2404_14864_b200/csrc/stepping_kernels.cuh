@@ -21,63 +21,184 @@ KFBI_DEV void block_nanmax_to(unsigned long long *dst, double v) {
   }
 }
 
+// Element-wise passes over n values, two adjacent elements per step (16-byte
+// loads, aligned buffers: every field here is a whole torch allocation) and
+// two steps in flight per thread; the odd tail element is done by thread 0.
+// VEC = false is the scalar fallback for unaligned views.
+template <bool VEC, typename F>
+KFBI_DEV void elementwise_pairs(long n, F &&f) {
+  const long tid = blockIdx.x * (long)blockDim.x + threadIdx.x;
+  const long stride = (long)gridDim.x * blockDim.x;
+  if (VEC) {
+    const long np = n >> 1;
+    long i = tid;
+    for (; i + stride < np; i += 2 * stride) f.template pair<2>(i, i + stride);
+    if (i < np) f.template pair<1>(i, i);
+    if (tid == 0 && (n & 1)) f.one(n - 1);
+  } else {
+    for (long i = tid; i < n; i += stride) f.one(i);
+  }
+}
+
 // u <- mask ? u : 0 ; norm = max|u|   (np.where(ctx.mask, sol.u, 0.0))
 template <typename T>
-__global__ void mask_norm_kernel(long n, const unsigned char *mask, T *u,
-                                 unsigned long long *norm) {
-  double mag = 0.0;
-  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n;
-       i += (long)gridDim.x * blockDim.x) {
+struct MaskNormOp {
+  const unsigned char *__restrict__ mask;
+  T *__restrict__ u;
+  double mag;
+  template <int K>
+  KFBI_DEV void pair(long i0, long i1) {
+    const long ii[2] = {i0, i1};
+    T v[K][2];
+    uchar2 mk[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      if constexpr (std::is_same<T, double>::value) {
+        const double2 w = reinterpret_cast<const double2 *>(u)[ii[k]];
+        v[k][0] = w.x;
+        v[k][1] = w.y;
+      } else {
+        v[k][0] = u[2 * ii[k]];
+        v[k][1] = u[2 * ii[k] + 1];
+      }
+      mk[k] = mask ? reinterpret_cast<const uchar2 *>(mask)[ii[k]] : make_uchar2(1, 1);
+    }
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      if (!mk[k].x) { v[k][0] = Sc<T>::zero(); u[2 * ii[k]] = v[k][0]; }
+      if (!mk[k].y) { v[k][1] = Sc<T>::zero(); u[2 * ii[k] + 1] = v[k][1]; }
+      mag = nanmax(mag, nanmax(Sc<T>::abs(v[k][0]), Sc<T>::abs(v[k][1])));
+    }
+  }
+  KFBI_DEV void one(long i) {
     T v = u[i];
     if (mask && !mask[i]) { v = Sc<T>::zero(); u[i] = v; }
     mag = nanmax(mag, Sc<T>::abs(v));
   }
-  block_nanmax_to(norm, mag);
+};
+
+template <typename T, bool VEC>
+__global__ void __launch_bounds__(256) mask_norm_kernel(long n, const unsigned char *mask, T *u,
+                                                        unsigned long long *norm) {
+  MaskNormOp<T> op{mask, u, 0.0};
+  elementwise_pairs<VEC>(n, op);
+  block_nanmax_to(norm, op.mag);
 }
 
 // heat (timestepping.py:218-228): u <- mask u;  F_new = a u - F_old
-__global__ void heat_rhs_kernel(long n, const unsigned char *mask, double *u, const double *F_old,
-                                double *F_new, double a, unsigned long long *norm) {
-  double mag = 0.0;
-  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n;
-       i += (long)gridDim.x * blockDim.x) {
+struct HeatOp {
+  const unsigned char *__restrict__ mask;
+  double *__restrict__ u;
+  const double *__restrict__ F_old;
+  double *__restrict__ F_new;
+  double a, mag;
+  template <int K>
+  KFBI_DEV void pair(long i0, long i1) {
+    const long ii[2] = {i0, i1};
+    double2 v[K], fo[K];
+    uchar2 mk[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      v[k] = reinterpret_cast<const double2 *>(u)[ii[k]];
+      fo[k] = reinterpret_cast<const double2 *>(F_old)[ii[k]];
+      mk[k] = mask ? reinterpret_cast<const uchar2 *>(mask)[ii[k]] : make_uchar2(1, 1);
+    }
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      if (!mk[k].x || !mk[k].y) {
+        if (!mk[k].x) v[k].x = 0.0;
+        if (!mk[k].y) v[k].y = 0.0;
+        reinterpret_cast<double2 *>(u)[ii[k]] = v[k];
+      }
+      reinterpret_cast<double2 *>(F_new)[ii[k]] = make_double2(a * v[k].x - fo[k].x, a * v[k].y - fo[k].y);
+      mag = nanmax(mag, nanmax(fabs(v[k].x), fabs(v[k].y)));
+    }
+  }
+  KFBI_DEV void one(long i) {
     double v = u[i];
     if (mask && !mask[i]) { v = 0.0; u[i] = v; }
     F_new[i] = a * v - F_old[i];
     mag = nanmax(mag, fabs(v));
   }
-  block_nanmax_to(norm, mag);
+};
+
+template <bool VEC>
+__global__ void __launch_bounds__(256) heat_rhs_kernel(long n, const unsigned char *mask, double *u,
+                                                       const double *F_old, double *F_new, double a,
+                                                       unsigned long long *norm) {
+  HeatOp op{mask, u, F_old, F_new, a, 0.0};
+  elementwise_pairs<VEC>(n, op);
+  block_nanmax_to(norm, op.mag);
 }
 
 // wave (timestepping.py:284-297)
 //   un <- mask un;  F_new = (2 un - uc) kw + coef (kw un - fc) + (kw uc - fp)
-__global__ void wave_rhs_kernel(long n, const unsigned char *mask, double *un,
-                                const double *uc, const double *fc, const double *fp,
-                                double *F_new, double kw, double coef,
-                                unsigned long long *norm) {
-  double mag = 0.0;
-  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n;
-       i += (long)gridDim.x * blockDim.x) {
+struct WaveOp {
+  const unsigned char *__restrict__ mask;
+  double *__restrict__ un;
+  const double *__restrict__ uc, *__restrict__ fc, *__restrict__ fp;
+  double *__restrict__ F_new;
+  double kw, coef, mag;
+  KFBI_DEV double f(double v, double c, double fcv, double fpv) const {
+    return (2.0 * v - c) * kw + coef * (kw * v - fcv) + (kw * c - fpv);
+  }
+  template <int K>
+  KFBI_DEV void pair(long i0, long i1) {
+    const long ii[2] = {i0, i1};
+    double2 v[K], c[K], a[K], b[K];
+    uchar2 mk[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      v[k] = reinterpret_cast<const double2 *>(un)[ii[k]];
+      c[k] = reinterpret_cast<const double2 *>(uc)[ii[k]];
+      a[k] = reinterpret_cast<const double2 *>(fc)[ii[k]];
+      b[k] = reinterpret_cast<const double2 *>(fp)[ii[k]];
+      mk[k] = mask ? reinterpret_cast<const uchar2 *>(mask)[ii[k]] : make_uchar2(1, 1);
+    }
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      if (!mk[k].x || !mk[k].y) {
+        if (!mk[k].x) v[k].x = 0.0;
+        if (!mk[k].y) v[k].y = 0.0;
+        reinterpret_cast<double2 *>(un)[ii[k]] = v[k];
+      }
+      reinterpret_cast<double2 *>(F_new)[ii[k]] =
+          make_double2(f(v[k].x, c[k].x, a[k].x, b[k].x), f(v[k].y, c[k].y, a[k].y, b[k].y));
+      mag = nanmax(mag, nanmax(fabs(v[k].x), fabs(v[k].y)));
+    }
+  }
+  KFBI_DEV void one(long i) {
     double v = un[i];
     if (mask && !mask[i]) { v = 0.0; un[i] = v; }
-    const double c = uc[i];
-    F_new[i] = (2.0 * v - c) * kw + coef * (kw * v - fc[i]) + (kw * c - fp[i]);
+    F_new[i] = f(v, uc[i], fc[i], fp[i]);
     mag = nanmax(mag, fabs(v));
   }
-  block_nanmax_to(norm, mag);
+};
+
+template <bool VEC>
+__global__ void __launch_bounds__(256) wave_rhs_kernel(long n, const unsigned char *mask, double *un,
+                                                       const double *uc, const double *fc,
+                                                       const double *fp, double *F_new, double kw,
+                                                       double coef, unsigned long long *norm) {
+  WaveOp op{mask, un, uc, fc, fp, F_new, kw, coef, 0.0};
+  elementwise_pairs<VEC>(n, op);
+  block_nanmax_to(norm, op.mag);
 }
 
 // u* of the Strang step (timestepping.py:410-418):
 //   mode 0: u - (0.5 i tau) other   (first step, other = lap u0)
 //   mode 1: 2 u - other             (other = u** of the previous step)
-__global__ void schr_ustar_kernel(long n, int mode, const double2 *u, const double2 *other,
-                                  double tau, double2 *out) {
+KFBI_DEV double2 ustar_of(int mode, double2 a, double2 b, double tau) {
+  if (mode == 0) return csub(a, cmul(make_double2(0.0, 0.5 * tau), b));
+  return csub(make_double2(2.0 * a.x, 2.0 * a.y), b);
+}
+
+__global__ void schr_ustar_kernel(long n, int mode, const double2 *__restrict__ u,
+                                  const double2 *__restrict__ other, double tau,
+                                  double2 *__restrict__ out) {
   for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n;
-       i += (long)gridDim.x * blockDim.x) {
-    double2 a = u[i], b = other[i];
-    if (mode == 0) out[i] = csub(a, cmul(make_double2(0.0, 0.5 * tau), b));
-    else out[i] = csub(make_double2(2.0 * a.x, 2.0 * a.y), b);
-  }
+       i += (long)gridDim.x * blockDim.x)
+    out[i] = ustar_of(mode, u[i], other[i], tau);
 }
 
 // Pointwise damped Newton of nonlinear_phase_step (timestepping.py:317-368)
@@ -131,15 +252,20 @@ KFBI_DEV double2 newton_node(double2 us, double v, double w, double c, double &r
 }
 
 // out = masked Newton(u*); optionally F = kappa * out; reports max residual.
-__global__ void nonlinear_phase_kernel(long n, const double2 *ustar, const double *v, double w,
-                                       double c, const unsigned char *mask, double2 *out,
-                                       double kre, double kim, double2 *F,
-                                       unsigned long long *max_res) {
+// With `other` != nullptr, u* is formed inline from (ustar = u, other, mode)
+// (the schr_ustar_kernel expression), saving a full-grid write and read.
+__global__ void __launch_bounds__(256)
+nonlinear_phase_kernel(long n, const double2 *__restrict__ ustar, const double2 *__restrict__ other,
+                       int mode, double tau, const double *__restrict__ v, double w, double c,
+                       const unsigned char *__restrict__ mask, double2 *__restrict__ out,
+                       double kre, double kim, double2 *__restrict__ F,
+                       unsigned long long *max_res) {
   double worst = 0.0;
   for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n;
        i += (long)gridDim.x * blockDim.x) {
     double r;
-    double2 z = newton_node(ustar[i], v[i], w, c, r);
+    const double2 us = other ? ustar_of(mode, ustar[i], other[i], tau) : ustar[i];
+    double2 z = newton_node(us, v[i], w, c, r);
     worst = nanmax(worst, r);
     if (mask && !mask[i]) z = make_double2(0.0, 0.0);
     out[i] = z;
