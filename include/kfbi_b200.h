@@ -61,7 +61,7 @@ enum {
 typedef struct kfbi_plan kfbi_plan;
 
 /* CartesianGrid (grid.py:25-52) + the BoxSolver eigenvalue tables
- * (boxsolve.py:38-44).  m must be a power of two, 16 <= m <= 4096. */
+ * (boxsolve.py:38-44).  m must be a power of two, 16 <= m <= 16384. */
 typedef struct {
   int32_t m;
   double h;

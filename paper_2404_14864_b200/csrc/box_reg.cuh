@@ -27,32 +27,43 @@
 
 namespace kfbi {
 
-constexpr size_t REG_SMEM_BYTES =
-    (size_t)reg::CTA * reg::E * sizeof(double2) + (reg::CTA / 32) * sizeof(double2);
-
-// stage x (natural order) into the sequence's smem, x_0 = 0
+// stage x (natural order) into the sequence's smem
 template <int LOGN>
-KFBI_DEV void stage(double2 *sm, const double2 (&v)[reg::E], int t) {
+KFBI_DEV void stage(const reg::View<LOGN> &sm, const double2 (&v)[reg::E], int t) {
 #pragma unroll
-  for (int m = 0; m < reg::E; ++m) sm[reg::sw(t + m * reg::Cfg<LOGN>::T)] = v[m];
+  for (int m = 0; m < reg::E; ++m) sm[t + m * reg::Cfg<LOGN>::T] = v[m];
+}
+
+// write out[c] (index 16 t + c) to the sequence's smem in natural order
+template <int LOGN>
+KFBI_DEV void unstage(const reg::View<LOGN> &sm, const double2 (&out)[reg::E], int t) {
+#pragma unroll
+  for (int c = 0; c < reg::E; ++c) sm[reg::E * t + c] = out[c];
 }
 
 // x staged in sm -> C = DST-I(x) in out[c] (index 16 t + c).  Entry: staged
 // data visible (after a barrier).  Exit: sm may still be read by other
 // threads (barrier needed before the next write).
 template <int LOGN>
-KFBI_DEV void dst_staged(double2 *sm, double2 *scratch, int t, const BoxArgs &a,
-                         double2 (&out)[reg::E]) {
+KFBI_DEV void dst_staged(const reg::View<LOGN> &sm, int t, const BoxArgs &a, double2 (&out)[reg::E]) {
   double2 v[reg::E];
   reg::pre_from_smem<LOGN>(v, sm, t, a.sinv);
-  __syncthreads();
+  reg::seq_sync<LOGN>();
   reg::fft<LOGN>(v, sm, t, a.twg);
-  reg::post<LOGN>(sm, t, out, scratch);
+  reg::post<LOGN>(sm, t, out);
+}
+
+// sequence index of the calling thread's sequence
+template <int LOGN>
+KFBI_DEV int seq_index(int seq) {
+  using C = reg::Cfg<LOGN>;
+  if constexpr (C::CL == 1) return blockIdx.x * C::S + seq;
+  else return blockIdx.x / C::CL;
 }
 
 // ---------------------------------------------------------------------------
 template <bool CPLX, int LOGN>
-__global__ void __launch_bounds__(reg::CTA, 2)
+__global__ void __launch_bounds__(reg::Cfg<LOGN>::CTA_T, reg::Cfg<LOGN>::MINB)
 rows_fwd_reg(BoxArgs a, const void *__restrict__ rhs, double sign,
              CorrArgs<typename std::conditional<CPLX, double2, double>::type> corr) {
   using T = typename std::conditional<CPLX, double2, double>::type;
@@ -60,11 +71,10 @@ rows_fwd_reg(BoxArgs a, const void *__restrict__ rhs, double sign,
   constexpr int M = C::N, TT = C::T;
   extern __shared__ double2 smem[];
   if (a.done && *a.done) return;
-  const int seq = threadIdx.x / TT, t = threadIdx.x % TT;
-  double2 *sm = smem + seq * M;
-  double2 *scratch = smem + reg::CTA * reg::E;
+  int seq, t;
+  const reg::View<LOGN> sm = reg::make_view<LOGN>(smem, seq, t);
   const int stride = M + 1;
-  const int q = blockIdx.x * C::S + seq;
+  const int q = seq_index<LOGN>(seq);
   const int nseq = CPLX ? M - 1 : M / 2;
   const bool valid = q < nseq;
   const int j0 = CPLX ? q + 1 : 2 * q + 1;
@@ -89,7 +99,7 @@ rows_fwd_reg(BoxArgs a, const void *__restrict__ rhs, double sign,
   for (int m = 0; m < reg::E; ++m) v[m] = cscale(v[m], sign);
   stage<LOGN>(sm, v, t);
   if (corr.jv) {
-    __syncthreads();
+    reg::seq_sync<LOGN>();
     if (valid) {
       const int nrows = has2 ? 2 : 1;
       for (int qq = 0; qq < nrows; ++qq) {
@@ -99,53 +109,53 @@ rows_fwd_reg(BoxArgs a, const void *__restrict__ rhs, double sign,
           const T cv = group_correction<T>(corr, g);
           const int i = corr.group_node[g] - j * stride;
           if constexpr (CPLX) {
-            double2 &slot = sm[reg::sw(i)];
+            double2 &slot = sm[i];
             slot = cadd(slot, cv);
           } else {
-            double *slot = reinterpret_cast<double *>(&sm[reg::sw(i)]) + qq;
+            double *slot = reinterpret_cast<double *>(&sm[i]) + qq;
             *slot += cv;
           }
         }
       }
     }
   }
-  __syncthreads();
+  reg::seq_sync<LOGN>();
   double2 out[reg::E];
-  dst_staged<LOGN>(sm, scratch, t, a, out);
-  __syncthreads();
-#pragma unroll
-  for (int c = 0; c < reg::E; ++c) sm[reg::sw(reg::E * t + c)] = out[c];
-  __syncthreads();
-  if (!valid) return;
-  // panel stores: consecutive lanes write consecutive 16-byte pieces of a
-  // panel's (row j0, row j0+1) 64-byte chunk (real) / 32-byte row (complex)
-  double2 *P2 = static_cast<double2 *>(a.panels);
-  if (!CPLX) {
-    for (int i = t; i < M; i += TT) {          // M/4 panels x 4 pieces
-      const int pp = i >> 2, part = i & 3, row = part >> 1;
-      if (row && !has2) continue;
-      const int n0 = 4 * pp + 2 * (part & 1);
-      const double2 v0 = sm[reg::sw(n0)], v1 = sm[reg::sw(n0 + 1)];
-      P2[((size_t)pp * M + j0 + row) * 2 + (part & 1)] =
-          row ? make_double2(v0.y, v1.y) : make_double2(v0.x, v1.x);
+  dst_staged<LOGN>(sm, t, a, out);
+  reg::seq_sync<LOGN>();
+  unstage<LOGN>(sm, out, t);
+  reg::seq_sync<LOGN>();
+  if (valid) {
+    // panel stores: consecutive lanes write consecutive 16-byte pieces of a
+    // panel's (row j0, row j0+1) 64-byte chunk (real) / 32-byte row (complex)
+    double2 *P2 = static_cast<double2 *>(a.panels);
+    if (!CPLX) {
+      for (int i = t; i < M; i += TT) {          // M/4 panels x 4 pieces
+        const int pp = i >> 2, part = i & 3, row = part >> 1;
+        if (row && !has2) continue;
+        const int n0 = 4 * pp + 2 * (part & 1);
+        const double2 v0 = sm[n0], v1 = sm[n0 + 1];
+        P2[((size_t)pp * M + j0 + row) * 2 + (part & 1)] =
+            row ? make_double2(v0.y, v1.y) : make_double2(v0.x, v1.x);
+      }
+    } else {
+      for (int i = t; i < M; i += TT)            // M/2 panels x 2 pieces
+        P2[((size_t)(i >> 1) * M + j0) * 2 + (i & 1)] = sm[i];
     }
-  } else {
-    for (int i = t; i < M; i += TT)            // M/2 panels x 2 pieces
-      P2[((size_t)(i >> 1) * M + j0) * 2 + (i & 1)] = sm[reg::sw(i)];
   }
+  if constexpr (C::CL > 1) reg::seq_sync<LOGN>();   // keep the cluster's smem alive
 }
 
 // ---------------------------------------------------------------------------
 template <bool CPLX, int LOGN>
-__global__ void __launch_bounds__(reg::CTA, 2) cols_reg(BoxArgs a) {
+__global__ void __launch_bounds__(reg::Cfg<LOGN>::CTA_T, reg::Cfg<LOGN>::MINB) cols_reg(BoxArgs a) {
   using C = reg::Cfg<LOGN>;
   constexpr int M = C::N, TT = C::T;
   extern __shared__ double2 smem[];
   if (a.done && *a.done) return;
-  const int seq = threadIdx.x / TT, t = threadIdx.x % TT;
-  double2 *sm = smem + seq * M;
-  double2 *scratch = smem + reg::CTA * reg::E;
-  const int q = blockIdx.x * C::S + seq;
+  int seq, t;
+  const reg::View<LOGN> sm = reg::make_view<LOGN>(smem, seq, t);
+  const int q = seq_index<LOGN>(seq);
   const int nseq = CPLX ? M : M / 2;
   const bool valid = q < nseq;
   const int pp = q >> 1, half = q & 1;
@@ -158,9 +168,9 @@ __global__ void __launch_bounds__(reg::CTA, 2) cols_reg(BoxArgs a) {
     v[m] = (valid && n >= 1) ? col[2 * n] : make_double2(0.0, 0.0);
   }
   stage<LOGN>(sm, v, t);
-  __syncthreads();
+  reg::seq_sync<LOGN>();
   double2 out[reg::E];
-  dst_staged<LOGN>(sm, scratch, t, a, out);
+  dst_staged<LOGN>(sm, t, a, out);
 
   // spectral division (boxsolve.py:74-76): (v / (lam_p + lam_q - kappa)) / (4 M^2)
 #pragma unroll
@@ -179,31 +189,30 @@ __global__ void __launch_bounds__(reg::CTA, 2) cols_reg(BoxArgs a) {
     }
   }
   if (t == 0) out[0] = make_double2(0.0, 0.0);   // x_0 = 0 for the second transform
-  __syncthreads();
-#pragma unroll
-  for (int c = 0; c < reg::E; ++c) sm[reg::sw(reg::E * t + c)] = out[c];
-  __syncthreads();
-  dst_staged<LOGN>(sm, scratch, t, a, out);
-  __syncthreads();
-#pragma unroll
-  for (int c = 0; c < reg::E; ++c) sm[reg::sw(reg::E * t + c)] = out[c];
-  __syncthreads();
-  if (!valid) return;
-  for (int n = t; n < M; n += TT) col[2 * n] = sm[reg::sw(n)];
+  reg::seq_sync<LOGN>();
+  unstage<LOGN>(sm, out, t);
+  reg::seq_sync<LOGN>();
+  dst_staged<LOGN>(sm, t, a, out);
+  reg::seq_sync<LOGN>();
+  unstage<LOGN>(sm, out, t);
+  reg::seq_sync<LOGN>();
+  if (valid)
+    for (int n = t; n < M; n += TT) col[2 * n] = sm[n];
+  if constexpr (C::CL > 1) reg::seq_sync<LOGN>();
 }
 
 // ---------------------------------------------------------------------------
 template <bool CPLX, int LOGN>
-__global__ void __launch_bounds__(reg::CTA, 2) rows_inv_reg(BoxArgs a, void *__restrict__ u) {
+__global__ void __launch_bounds__(reg::Cfg<LOGN>::CTA_T, reg::Cfg<LOGN>::MINB)
+rows_inv_reg(BoxArgs a, void *__restrict__ u) {
   using C = reg::Cfg<LOGN>;
   constexpr int M = C::N, TT = C::T;
   extern __shared__ double2 smem[];
   if (a.done && *a.done) return;
-  const int seq = threadIdx.x / TT, t = threadIdx.x % TT;
-  double2 *sm = smem + seq * M;
-  double2 *scratch = smem + reg::CTA * reg::E;
+  int seq, t;
+  const reg::View<LOGN> sm = reg::make_view<LOGN>(smem, seq, t);
   const int stride = M + 1;
-  const int q = blockIdx.x * C::S + seq;
+  const int q = seq_index<LOGN>(seq);
   const int nseq = CPLX ? M - 1 : M / 2;
   const bool valid = q < nseq;
   const int j0 = CPLX ? q + 1 : 2 * q + 1;
@@ -224,8 +233,8 @@ __global__ void __launch_bounds__(reg::CTA, 2) rows_inv_reg(BoxArgs a, void *__r
     for (int m = 0; m < reg::E; ++m) {
       const int i = t + m * TT, pp = i >> 2, part = i & 3, row = part >> 1;
       const int n0 = 4 * pp + 2 * (part & 1);
-      double *s0 = reinterpret_cast<double *>(&sm[reg::sw(n0)]) + row;
-      double *s1 = reinterpret_cast<double *>(&sm[reg::sw(n0 + 1)]) + row;
+      double *s0 = reinterpret_cast<double *>(&sm[n0]) + row;
+      double *s1 = reinterpret_cast<double *>(&sm[n0 + 1]) + row;
       *s0 = n0 == 0 ? 0.0 : v[m].x;            // x_0 = 0
       *s1 = v[m].y;
     }
@@ -238,41 +247,42 @@ __global__ void __launch_bounds__(reg::CTA, 2) rows_inv_reg(BoxArgs a, void *__r
     }
     stage<LOGN>(sm, v, t);
   }
-  __syncthreads();
+  reg::seq_sync<LOGN>();
   double2 out[reg::E];
-  dst_staged<LOGN>(sm, scratch, t, a, out);
-  __syncthreads();
-#pragma unroll
-  for (int c = 0; c < reg::E; ++c) sm[reg::sw(reg::E * t + c)] = out[c];
-  __syncthreads();
-  if (!valid) return;
-  // coalesced row stores with the zero ring (boxsolve.py:90-93)
-  if (!CPLX) {
-    double *U = static_cast<double *>(u);
-    double *u0 = U + (size_t)j0 * stride;
-    double *u1 = U + (size_t)(j0 + 1) * stride;   // ring row M when !has2
-    for (int n = t; n <= M; n += TT) {
-      double x = 0.0, y = 0.0;
-      if (n >= 1 && n < M) {
-        const double2 w = sm[reg::sw(n)];
-        x = w.x;
-        y = has2 ? w.y : 0.0;
+  dst_staged<LOGN>(sm, t, a, out);
+  reg::seq_sync<LOGN>();
+  unstage<LOGN>(sm, out, t);
+  reg::seq_sync<LOGN>();
+  if (valid) {
+    // coalesced row stores with the zero ring (boxsolve.py:90-93)
+    if (!CPLX) {
+      double *U = static_cast<double *>(u);
+      double *u0 = U + (size_t)j0 * stride;
+      double *u1 = U + (size_t)(j0 + 1) * stride;   // ring row M when !has2
+      for (int n = t; n <= M; n += TT) {
+        double x = 0.0, y = 0.0;
+        if (n >= 1 && n < M) {
+          const double2 w = sm[n];
+          x = w.x;
+          y = has2 ? w.y : 0.0;
+        }
+        u0[n] = x;
+        u1[n] = y;
       }
-      u0[n] = x;
-      u1[n] = y;
+      if (q == 0)
+        for (int n = t; n <= M; n += TT) U[n] = 0.0;
+    } else {
+      double2 *U = static_cast<double2 *>(u);
+      double2 *u0 = U + (size_t)j0 * stride;
+      for (int n = t; n <= M; n += TT)
+        u0[n] = (n >= 1 && n < M) ? sm[n] : make_double2(0.0, 0.0);
+      if (q == 0)
+        for (int n = t; n <= M; n += TT) U[n] = make_double2(0.0, 0.0);
+      if (j0 == M - 1)
+        for (int n = t; n <= M; n += TT) U[(size_t)M * stride + n] = make_double2(0.0, 0.0);
     }
-    if (q == 0)
-      for (int n = t; n <= M; n += TT) U[n] = 0.0;
-  } else {
-    double2 *U = static_cast<double2 *>(u);
-    double2 *u0 = U + (size_t)j0 * stride;
-    for (int n = t; n <= M; n += TT)
-      u0[n] = (n >= 1 && n < M) ? sm[reg::sw(n)] : make_double2(0.0, 0.0);
-    if (q == 0)
-      for (int n = t; n <= M; n += TT) U[n] = make_double2(0.0, 0.0);
-    if (j0 == M - 1)
-      for (int n = t; n <= M; n += TT) U[(size_t)M * stride + n] = make_double2(0.0, 0.0);
   }
+  if constexpr (C::CL > 1) reg::seq_sync<LOGN>();
 }
 
 }  // namespace kfbi

@@ -23,8 +23,14 @@
 // k / (Ns R)}, w from a global table and its powers by complex products.
 //
 // Shared memory: N double2 per sequence, swizzled (sw) so that every access
-// pattern below is free of bank conflicts for 16-byte slots.
+// pattern below is free of bank conflicts for 16-byte slots.  Up to N = 4096
+// a 256-thread CTA holds 4096/N sequences; N = 8192 is one 512-thread CTA
+// (128 KB); N = 16384 is a cluster of two 512-thread CTAs, the sequence split
+// in halves across their shared memories (distributed shared memory, cluster
+// barriers instead of CTA barriers).
 #pragma once
+
+#include <cooperative_groups.h>
 
 #include "common.cuh"
 
@@ -42,11 +48,66 @@ template <int LOGN>
 struct Cfg {
   static constexpr int N = 1 << LOGN;
   static constexpr int T = N / E;                 // threads per sequence
-  static constexpr int S = CTA / T;               // sequences per CTA
+  static constexpr int CL = T > 512 ? T / 512 : 1;          // CTAs per sequence
+  static constexpr int CTA_T = T >= 256 ? (T > 512 ? 512 : T) : CTA;  // threads per CTA
+  static constexpr int S = T >= 256 ? 1 : CTA / T;          // sequences per CTA
+  static constexpr int LOCAL = CTA_T * E;                   // elements per CTA buffer
+  static constexpr int MINB = CTA_T == 256 ? 2 : 1;         // CTAs per SM
   static constexpr int P = (LOGN + 3) / 4;        // Stockham passes
   static constexpr int RLAST = 1 << (LOGN - 4 * (P - 1));
-  static_assert(LOGN >= 4 && LOGN <= 12, "DST length 16..4096");
+  static_assert(LOGN >= 4 && LOGN <= 14, "DST length 16..16384");
 };
+
+// Shared memory bytes of one CTA (sequence buffer + scan scratch).
+template <int LOGN>
+constexpr size_t smem_bytes() {
+  return (size_t)Cfg<LOGN>::LOCAL * sizeof(double2) + (Cfg<LOGN>::CTA_T / 32) * sizeof(double2);
+}
+
+// Barrier over the threads of one sequence (CTA, or the cluster).
+template <int LOGN>
+KFBI_DEV void seq_sync() {
+  if constexpr (Cfg<LOGN>::CL == 1) __syncthreads();
+  else cooperative_groups::this_cluster().sync();
+}
+
+// One sequence's shared memory: element i lives in CTA rank i / LOCAL of the
+// cluster (always rank 0 without a cluster), swizzled within the CTA buffer.
+template <int LOGN>
+struct View {
+  using C = Cfg<LOGN>;
+  double2 *p[C::CL];              // per-rank sequence buffer
+  double2 *scr[C::CL];            // per-rank scan scratch (CTA_T / 32 slots)
+  KFBI_DEV double2 &operator[](int i) const {
+    if constexpr (C::CL == 1) return p[0][sw(i)];
+    else return p[i / C::LOCAL][sw(i & (C::LOCAL - 1))];
+  }
+};
+
+// View of the calling thread's sequence and its logical thread index t.
+template <int LOGN>
+KFBI_DEV View<LOGN> make_view(double2 *smem, int &seq, int &t) {
+  using C = Cfg<LOGN>;
+  View<LOGN> v;
+  double2 *scr = smem + C::LOCAL;
+  if constexpr (C::CL == 1) {
+    seq = threadIdx.x / C::T;
+    t = threadIdx.x % C::T;
+    v.p[0] = smem + seq * C::N;
+    v.scr[0] = scr;
+  } else {
+    auto cl = cooperative_groups::this_cluster();
+    const int rank = (int)cl.block_rank();
+    seq = 0;
+    t = rank * C::CTA_T + threadIdx.x;
+#pragma unroll
+    for (int r = 0; r < C::CL; ++r) {
+      v.p[r] = cl.map_shared_rank(smem, r);
+      v.scr[r] = cl.map_shared_rank(scr, r);
+    }
+  }
+  return v;
+}
 
 // ---- constant twiddles w16^e = exp(-2 pi i e / 16) ----
 template <int e>
@@ -167,7 +228,8 @@ KFBI_DEV void powers(double2 w1, double2 (&w)[R]) {
 // One Stockham pass: radix R, current span NS; thread t holds inputs
 // v[m] = x[t + m T]; writes the pass output to sm (swizzled).
 template <int LOGN, int R, int NS>
-KFBI_DEV void stockham_pass(double2 (&v)[E], double2 *sm, int t, const double2 *__restrict__ twg) {
+KFBI_DEV void stockham_pass(double2 (&v)[E], const View<LOGN> &sm, int t,
+                            const double2 *__restrict__ twg) {
   constexpr int N = 1 << LOGN;
   constexpr int T = Cfg<LOGN>::T;
   constexpr int B = E / R;              // butterflies per thread
@@ -187,44 +249,46 @@ KFBI_DEV void stockham_pass(double2 (&v)[E], double2 *sm, int t, const double2 *
     dft<R>(a);
     const int base = (b - k) * R + k;
 #pragma unroll
-    for (int r = 0; r < R; ++r) sm[sw(base + r * NS)] = a[r];
+    for (int r = 0; r < R; ++r) sm[base + r * NS] = a[r];
   }
 }
 
 template <int LOGN, int PASS>
-KFBI_DEV void fft_passes(double2 (&v)[E], double2 *sm, int t, const double2 *__restrict__ twg) {
+KFBI_DEV void fft_passes(double2 (&v)[E], const View<LOGN> &sm, int t,
+                         const double2 *__restrict__ twg) {
   using C = Cfg<LOGN>;
   constexpr int R = (PASS < C::P - 1) ? 16 : C::RLAST;
   constexpr int NS = 1 << (4 * PASS);
   stockham_pass<LOGN, R, NS>(v, sm, t, twg);
   if constexpr (PASS + 1 < C::P) {
-    __syncthreads();
+    seq_sync<LOGN>();
 #pragma unroll
-    for (int m = 0; m < E; ++m) v[m] = sm[sw(t + m * C::T)];
-    __syncthreads();
+    for (int m = 0; m < E; ++m) v[m] = sm[t + m * C::T];
+    seq_sync<LOGN>();
     fft_passes<LOGN, PASS + 1>(v, sm, t, twg);
   }
 }
 
 // Z = FFT_N(y): y in registers (v[m] = y_{t + m T}), Z left in sm in natural
 // order.  All threads of the CTA must call it; sm must be free on entry.
-// Returns after a __syncthreads() (Z visible to all threads).
+// Returns after a sequence barrier (Z visible to all threads).
 template <int LOGN>
-KFBI_DEV void fft(double2 (&v)[E], double2 *sm, int t, const double2 *__restrict__ twg) {
+KFBI_DEV void fft(double2 (&v)[E], const View<LOGN> &sm, int t, const double2 *__restrict__ twg) {
   fft_passes<LOGN, 0>(v, sm, t, twg);
-  __syncthreads();
+  seq_sync<LOGN>();
 }
 
 // y from a staged natural-order x (sm[sw(n)] = x_n, x_0 = 0 stored).
 template <int LOGN>
-KFBI_DEV void pre_from_smem(double2 (&v)[E], const double2 *sm, int t, const double *__restrict__ sinv) {
+KFBI_DEV void pre_from_smem(double2 (&v)[E], const View<LOGN> &sm, int t,
+                            const double *__restrict__ sinv) {
   constexpr int N = 1 << LOGN;
   constexpr int T = Cfg<LOGN>::T;
 #pragma unroll
   for (int m = 0; m < E; ++m) {
     const int j = t + m * T;
-    const double2 xj = sm[sw(j)];
-    const double2 xr = sm[sw((N - j) & (N - 1))];   // j = 0 -> x_0 = 0
+    const double2 xj = sm[j];
+    const double2 xr = sm[(N - j) & (N - 1)];       // j = 0 -> x_0 = 0
     const double s = __ldg(&sinv[j]);
     const double2 a = cadd(xj, xr), d = csub(xj, xr);
     v[m] = make_double2(fma(s, a.x, 0.5 * d.x), fma(s, a.y, 0.5 * d.y));
@@ -232,18 +296,18 @@ KFBI_DEV void pre_from_smem(double2 (&v)[E], const double2 *sm, int t, const dou
 }
 
 // Post-processing + scan: out[c] = C_{16 t + c} (out[0] of t = 0 is C_0 = 0).
-// scratch: >= (CTA / 32) double2 (used when T > 32).  Ends with no barrier
-// pending on sm (the caller must __syncthreads() before overwriting sm).
+// The view's scratch (CTA_T / 32 slots per rank) is used when T > 32.  Ends
+// with no barrier pending on sm (the caller syncs before overwriting sm).
 template <int LOGN>
-KFBI_DEV void post(const double2 *sm, int t, double2 (&out)[E], double2 *scratch) {
+KFBI_DEV void post(const View<LOGN> &sm, int t, double2 (&out)[E]) {
   constexpr int N = 1 << LOGN;
   constexpr int T = Cfg<LOGN>::T;
   double2 acc = make_double2(0.0, 0.0);
 #pragma unroll
   for (int c = 0; c < 8; ++c) {
     const int k = 8 * t + c;
-    const double2 zk = sm[sw(k)];
-    const double2 zm = sm[sw((N - k) & (N - 1))];
+    const double2 zk = sm[k];
+    const double2 zm = sm[(N - k) & (N - 1)];
     const double2 d = csub(zk, zm);
     out[2 * c] = make_double2(-d.y, d.x);              // i (Z_k - Z_{N-k})
     const double2 r = (k == 0) ? zk : cadd(zk, zm);
@@ -270,12 +334,16 @@ KFBI_DEV void post(const double2 *sm, int t, double2 (&out)[E], double2 *scratch
     const double ey = __shfl_up_sync(0xffffffffu, inc.y, 1, W);
     if (sl >= 1) off = make_double2(ex, ey);
     if constexpr (T > 32) {
-      const int warp = threadIdx.x >> 5;
-      if (lane == 31) scratch[warp] = inc;
-      __syncthreads();
-      const int w0 = warp & ~(T / 32 - 1);              // first warp of this sequence
+      // warp totals: warp w of the sequence (logical) is local warp w % WPC
+      // of rank w / WPC; the sequence's warps of a multi-sequence CTA start
+      // at its first local warp
+      constexpr int WPC = Cfg<LOGN>::CTA_T / 32;
+      const int warp = t >> 5;                           // warp within the sequence
+      const int lw0 = (threadIdx.x >> 5) - (warp % WPC); // first local warp of the sequence
+      if (lane == 31) sm.scr[warp / WPC][lw0 + warp % WPC] = inc;
+      seq_sync<LOGN>();
       double2 pw = make_double2(0.0, 0.0);
-      for (int w = w0; w < warp; ++w) pw = cadd(pw, scratch[w]);
+      for (int w = 0; w < warp; ++w) pw = cadd(pw, sm.scr[w / WPC][lw0 + w % WPC]);
       off = cadd(pw, off);
     }
   }

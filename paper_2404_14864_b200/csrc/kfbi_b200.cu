@@ -82,12 +82,10 @@ struct kfbi_plan {
   int device = 0;
   int m = 0, logm = 0;
   double h = 0.0;
-  DevBuf<double2> tw;
   DevBuf<double> lam;
   DevBuf<double2> panels;       // m*m complex slots (sized for c128)
   DevBuf<double2> twg;          // register engine: exp(-2 pi i q / m), q < m
   DevBuf<double> sinv;          // register engine: sin(pi j / m), j < m
-  bool legacy_dst = false;      // KFBI_DST=legacy selects the v2 shared-memory engine
   // geometry
   bool has_geo = false;
   int n_ctl = 0, n_edges = 0, n_rec = 0, n_groups = 0, w_ld = 0;
@@ -186,7 +184,6 @@ BoxArgs box_args(kfbi_plan *p, double kre, double kim, const int *done) {
   BoxArgs a;
   a.m = p->m;
   a.logm = p->logm;
-  a.tw = p->tw.p;
   a.lam = p->lam.p;
   a.kre = kre;
   a.kim = kim;
@@ -236,19 +233,29 @@ ExtractArgs extract_args(kfbi_plan *p) {
   return x;
 }
 
-template <bool CPLX>
-kfbi_status set_smem_limits(kfbi_plan *p) {
-  // The attribute is per kernel (process wide), not per plan: allow the
-  // largest size any plan can need so plans of different M coexist.
-  (void)p;
-  const int row = (int)box_smem_bytes(4096, 1), col = (int)box_smem_bytes(4096, 1);
-  KFBI_CUDA(cudaFuncSetAttribute(rows_fwd_kernel<CPLX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 row), "transform-rows");
-  KFBI_CUDA(cudaFuncSetAttribute(rows_inv_kernel<CPLX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 row), "transform-rows");
-  KFBI_CUDA(cudaFuncSetAttribute(cols_kernel<CPLX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 col), "transform-cols");
-  return KFBI_OK;
+// Launch one register-engine kernel: plain, or as clusters of Cfg::CL CTAs.
+template <int LOGN, typename K, typename... Args>
+cudaError_t reg_launch(K kernel, int grid, cudaStream_t s, Args... args) {
+  using Cf = reg::Cfg<LOGN>;
+  const size_t smem = reg::smem_bytes<LOGN>();
+  if constexpr (Cf::CL == 1) {
+    kernel<<<grid, Cf::CTA_T, smem, s>>>(args...);
+    return cudaGetLastError();
+  } else {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(Cf::CTA_T);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = Cf::CL;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, args...);
+  }
 }
 
 // Register-engine passes for one (dtype, log2 M).
@@ -256,9 +263,10 @@ template <bool CPLX, int LOGN>
 kfbi_status box_reg_launch(kfbi_plan *p, const BoxArgs &a, const void *rhs, double sign,
                            const CorrArgs<typename std::conditional<CPLX, double2, double>::type> &c,
                            void *u, cudaStream_t s) {
+  using Cf = reg::Cfg<LOGN>;
   static bool attr = false;   // per instantiation, process wide
   if (!attr) {
-    const int bytes = (int)REG_SMEM_BYTES;
+    const int bytes = (int)reg::smem_bytes<LOGN>();
     KFBI_CUDA(cudaFuncSetAttribute(rows_fwd_reg<CPLX, LOGN>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, bytes), "transform-rows");
     KFBI_CUDA(cudaFuncSetAttribute(rows_inv_reg<CPLX, LOGN>,
@@ -267,20 +275,17 @@ kfbi_status box_reg_launch(kfbi_plan *p, const BoxArgs &a, const void *rhs, doub
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, bytes), "transform-cols");
     attr = true;
   }
-  using Cf = reg::Cfg<LOGN>;
   const int M = Cf::N;
   const int nrow = CPLX ? M - 1 : M / 2;     // row sequences
   const int ncol = CPLX ? M : M / 2;         // half-panel sequences
-  const int grow = (nrow + Cf::S - 1) / Cf::S, gcol = (ncol + Cf::S - 1) / Cf::S;
+  const int grow = Cf::CL > 1 ? nrow * Cf::CL : (nrow + Cf::S - 1) / Cf::S;
+  const int gcol = Cf::CL > 1 ? ncol * Cf::CL : (ncol + Cf::S - 1) / Cf::S;
+  using CT = typename std::conditional<CPLX, double2, double>::type;
   KFBI_TRY(launch(p, KFBI_K_ROWS, s, [&] {
-    rows_fwd_reg<CPLX, LOGN><<<grow, reg::CTA, REG_SMEM_BYTES, s>>>(a, rhs, sign, c);
+    reg_launch<LOGN>(rows_fwd_reg<CPLX, LOGN>, grow, s, a, rhs, sign, CorrArgs<CT>(c));
   }));
-  KFBI_TRY(launch(p, KFBI_K_COLS, s, [&] {
-    cols_reg<CPLX, LOGN><<<gcol, reg::CTA, REG_SMEM_BYTES, s>>>(a);
-  }));
-  return launch(p, KFBI_K_ROWS, s, [&] {
-    rows_inv_reg<CPLX, LOGN><<<grow, reg::CTA, REG_SMEM_BYTES, s>>>(a, u);
-  });
+  KFBI_TRY(launch(p, KFBI_K_COLS, s, [&] { reg_launch<LOGN>(cols_reg<CPLX, LOGN>, gcol, s, a); }));
+  return launch(p, KFBI_K_ROWS, s, [&] { reg_launch<LOGN>(rows_inv_reg<CPLX, LOGN>, grow, s, a, u); });
 }
 
 template <bool CPLX>
@@ -297,6 +302,8 @@ kfbi_status box_passes_reg(kfbi_plan *p, const BoxArgs &a, const void *rhs, doub
     case 10: return box_reg_launch<CPLX, 10>(p, a, rhs, sign, c, u, s);
     case 11: return box_reg_launch<CPLX, 11>(p, a, rhs, sign, c, u, s);
     case 12: return box_reg_launch<CPLX, 12>(p, a, rhs, sign, c, u, s);
+    case 13: return box_reg_launch<CPLX, 13>(p, a, rhs, sign, c, u, s);
+    case 14: return box_reg_launch<CPLX, 14>(p, a, rhs, sign, c, u, s);
     default: return fail(KFBI_E_CONFIG, "register DST engine: unsupported M");
   }
 }
@@ -308,23 +315,9 @@ kfbi_status box_passes(kfbi_plan *p, double kre, double kim, const void *rhs, do
                        const void *jv, void *u, const int *done, cudaStream_t s) {
   using T = typename std::conditional<CPLX, double2, double>::type;
   BoxArgs a = box_args(p, kre, kim, done);
-  const int M = p->m;
-  const int ntask = CPLX ? M - 1 : M / 2;
-  const int npanel = CPLX ? M / 2 : M / 4;
-  const size_t row = box_smem_bytes(M, 1), col = box_smem_bytes(M, 1);
   CorrArgs<T> c = corr_args<T>(p, static_cast<const T *>(jv));
   if (!jv) c.jv = nullptr;
-  if (!p->legacy_dst) return box_passes_reg<CPLX>(p, a, rhs, sign, c, u, s);
-  KFBI_TRY(launch(p, KFBI_K_ROWS, s, [&] {
-    rows_fwd_kernel<CPLX><<<ntask, DST_THREADS, row, s>>>(a, rhs, sign, c);
-  }));
-  KFBI_TRY(launch(p, KFBI_K_COLS, s, [&] {
-    cols_kernel<CPLX><<<2 * npanel, DST_THREADS, col, s>>>(a);
-  }));
-  KFBI_TRY(launch(p, KFBI_K_ROWS, s, [&] {
-    rows_inv_kernel<CPLX><<<ntask, DST_THREADS, row, s>>>(a, u);
-  }));
-  return KFBI_OK;
+  return box_passes_reg<CPLX>(p, a, rhs, sign, c, u, s);
 }
 
 kfbi_status box_dispatch(kfbi_plan *p, int dtype, double kre, double kim, const void *rhs,
@@ -571,7 +564,7 @@ kfbi_status kfbi_plan_create(const kfbi_grid_desc *desc, kfbi_plan **out) {
   if (!desc || !out) return fail(KFBI_E_CONFIG, "null argument");
   const int m = desc->m;
   if (m < 16 || (m & (m - 1)) != 0) return fail(KFBI_E_GRID, "M must be a power of two and >= 16");
-  if (m > 4096) return fail(KFBI_E_CONFIG, "this build supports M <= 4096 on one GPU");
+  if (m > 16384) return fail(KFBI_E_CONFIG, "this build supports M <= 16384");
   if (!(desc->h > 0)) return fail(KFBI_E_GRID, "grid spacing must be positive");
   kfbi_plan *p = new kfbi_plan();
   p->device = desc->device;
@@ -583,17 +576,8 @@ kfbi_status kfbi_plan_create(const kfbi_grid_desc *desc, kfbi_plan **out) {
     delete p;
     return fail(KFBI_E_CUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(e));
   }
-  // twiddles exp(-i pi q / m) in extended precision; lambda_p exactly as
-  // boxsolve.py:43 evaluates it in double: (2 cos(p pi / m) - 2) / h^2
-  // packed two-level twiddle table: lo[r] = e^{-i pi r/m} (r < 64),
-  // hi[t] = e^{-i pi 64 t/m} (t < max(1, m/64)); see dst_engine.cuh
-  std::vector<double2> tw(twiddle_slots(m));
-  auto cis = [m](long q) {
-    long double ang = 3.14159265358979323846264338327950288L * (long double)q / (long double)m;
-    return make_double2((double)cosl(ang), (double)-sinl(ang));
-  };
-  for (int r = 0; r < TW_LO; ++r) tw[r] = cis(r);
-  for (int t = 0; t < twiddle_slots(m) - TW_LO; ++t) tw[TW_LO + t] = cis(64L * t);
+  // lambda_p exactly as boxsolve.py:43 evaluates it in double:
+  // (2 cos(p pi / m) - 2) / h^2
   std::vector<double> lam(m + 1, 0.0);
   for (int q = 1; q < m; ++q) {
     double ang = (double)q * M_PI / (double)m;
@@ -607,11 +591,8 @@ kfbi_status kfbi_plan_create(const kfbi_grid_desc *desc, kfbi_plan **out) {
     twg[q] = make_double2((double)cosl(2.0L * ang), (double)-sinl(2.0L * ang));
     sinv[q] = (double)sinl(ang);
   }
-  const char *eng = getenv("KFBI_DST");
-  p->legacy_dst = eng && std::strcmp(eng, "legacy") == 0;
   if ((e = upload(p->twg, twg.data(), twg.size())) != cudaSuccess ||
       (e = upload(p->sinv, sinv.data(), sinv.size())) != cudaSuccess ||
-      (e = upload(p->tw, tw.data(), tw.size())) != cudaSuccess ||
       (e = upload(p->lam, lam.data(), lam.size())) != cudaSuccess ||
       (e = p->panels.ensure((size_t)m * m)) != cudaSuccess ||
       (e = p->st.ensure(1)) != cudaSuccess || (e = p->red.ensure(8)) != cudaSuccess) {
@@ -621,12 +602,6 @@ kfbi_status kfbi_plan_create(const kfbi_grid_desc *desc, kfbi_plan **out) {
   cudaMemset(p->panels.p, 0, (size_t)m * m * sizeof(double2));
   cudaMallocHost(&p->st_host, sizeof(RichState));
   cudaMallocHost(&p->red_host, 4 * sizeof(unsigned long long));
-  kfbi_status st = set_smem_limits<false>(p);
-  if (st == KFBI_OK) st = set_smem_limits<true>(p);
-  if (st != KFBI_OK) {
-    kfbi_plan_destroy(p);
-    return st;
-  }
   *out = p;
   return KFBI_OK;
 }
@@ -640,7 +615,7 @@ kfbi_status kfbi_plan_destroy(kfbi_plan *p) {
     cudaEventDestroy(pe.b);
   }
   for (auto e : p->pool) cudaEventDestroy(e);
-  p->tw.release(); p->lam.release(); p->panels.release(); p->twg.release(); p->sinv.release();
+  p->lam.release(); p->panels.release(); p->twg.release(); p->sinv.release();
   p->W.release(); p->edge_axis.release(); p->rec_edge.release(); p->group_start.release();
   p->group_node.release(); p->row_group.release(); p->stencil.release(); p->rec_d.release();
   p->rec_sigma.release(); p->deriv_col.release(); p->speed.release(); p->tangent.release();
