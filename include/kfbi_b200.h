@@ -169,6 +169,34 @@ kfbi_status kfbi_interface_solve(kfbi_plan *plan, int32_t dtype,
 kfbi_status kfbi_extract(kfbi_plan *plan, int32_t dtype, const void *u,
                          const void *jm, void *out, void *stream);
 
+/* ---- slab-decomposed box solve (multi-GPU) ----
+ * Rank `rank` of `nranks` (a power of two) owns grid rows
+ * [rank*m/nranks, (rank+1)*m/nranks); its rhs / u arrays hold exactly those
+ * rows, (m+1) values each (row 0 is the zero ring, row m is not stored).
+ * One solve is
+ *   kfbi_slab_rows_fwd -> all-to-all -> kfbi_slab_cols -> all-to-all ->
+ *   kfbi_slab_rows_inv
+ * where both all-to-alls exchange equal contiguous chunks of the panel
+ * buffer (kfbi_slab_panel_bytes bytes per rank; nranks chunks, chunk g goes
+ * to rank g), e.g. torch.distributed.all_to_all_single over NCCL.  With
+ * nranks = 1 the two exchanges are identities and the result equals
+ * kfbi_box_solve.  jv != NULL fuses the jump corrections of the plan's
+ * geometry (rows of this slab) like the Richardson sweep does. */
+typedef struct {
+  int32_t nranks;
+  int32_t rank;
+} kfbi_slab;
+
+kfbi_status kfbi_slab_panel_bytes(kfbi_plan *plan, int32_t dtype, int32_t nranks,
+                                  int64_t *bytes);
+kfbi_status kfbi_slab_rows_fwd(kfbi_plan *plan, int32_t dtype, const kfbi_slab *slab,
+                               const void *rhs, double sign, const void *jv,
+                               void *panels, void *stream);
+kfbi_status kfbi_slab_cols(kfbi_plan *plan, int32_t dtype, const kfbi_slab *slab,
+                           double kappa_re, double kappa_im, void *panels, void *stream);
+kfbi_status kfbi_slab_rows_inv(kfbi_plan *plan, int32_t dtype, const kfbi_slab *slab,
+                               const void *panels, void *u, void *stream);
+
 /* richardson_solve (bvp.py:276-351), device resident: one host sync per
  * batch of sweeps; history copied to result->history. */
 kfbi_status kfbi_richardson(kfbi_plan *plan, const kfbi_bvp *bvp,

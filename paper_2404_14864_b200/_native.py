@@ -42,6 +42,10 @@ class GridDesc(C.Structure):
     _fields_ = [("m", i32), ("h", f64), ("device", i32)]
 
 
+class Slab(C.Structure):
+    _fields_ = [("nranks", i32), ("rank", i32)]
+
+
 class Geometry(C.Structure):
     _fields_ = [
         ("n_ctl", i32), ("n_edges", i32), ("n_rec", i32), ("n_groups", i32),
@@ -97,6 +101,10 @@ _SIGNATURES = {
     "kfbi_strang_phase": ([vp, i64, i32, vp, vp, f64, vp, f64, f64, vp, vp, f64, f64, vp,
                            C.POINTER(f64), vp], i32),
     "kfbi_mask_norm": ([vp, i32, i64, vp, vp, C.POINTER(f64), vp], i32),
+    "kfbi_slab_panel_bytes": ([vp, i32, i32, C.POINTER(i64)], i32),
+    "kfbi_slab_rows_fwd": ([vp, i32, vp, vp, f64, vp, vp, vp], i32),
+    "kfbi_slab_cols": ([vp, i32, vp, f64, f64, vp, vp], i32),
+    "kfbi_slab_rows_inv": ([vp, i32, vp, vp, vp, vp], i32),
     "kfbi_kernel_times": ([vp, C.POINTER(f64), C.POINTER(i64)], i32),
     "kfbi_reset_kernel_times": ([vp], i32),
     "kfbi_set_timing": ([vp, i32], i32),

@@ -106,6 +106,28 @@ class Plan:
         N.check(self._lib.kfbi_box_solve(self.handle, self._dt(u.is_complex()), k.real, k.imag,
                                          rhs.data_ptr(), u.data_ptr(), self.stream))
 
+    # -- slab-decomposed box solve (dist.py) ----------------------------------
+    def slab_panel_bytes(self, cplx, nranks):
+        b = C.c_int64(0)
+        N.check(self._lib.kfbi_slab_panel_bytes(self.handle, self._dt(cplx), int(nranks), C.byref(b)))
+        return b.value
+
+    def slab_rows_fwd(self, cplx, nranks, rank, rhs, panels, sign=1.0, jv=None):
+        sl = N.Slab(int(nranks), int(rank))
+        N.check(self._lib.kfbi_slab_rows_fwd(self.handle, self._dt(cplx), C.byref(sl), N.ptr(rhs),
+                                             float(sign), N.ptr(jv), panels.data_ptr(), self.stream))
+
+    def slab_cols(self, cplx, nranks, rank, kappa, panels):
+        k = complex(kappa)
+        sl = N.Slab(int(nranks), int(rank))
+        N.check(self._lib.kfbi_slab_cols(self.handle, self._dt(cplx), C.byref(sl), k.real, k.imag,
+                                         panels.data_ptr(), self.stream))
+
+    def slab_rows_inv(self, cplx, nranks, rank, panels, u):
+        sl = N.Slab(int(nranks), int(rank))
+        N.check(self._lib.kfbi_slab_rows_inv(self.handle, self._dt(cplx), C.byref(sl),
+                                             panels.data_ptr(), u.data_ptr(), self.stream))
+
     def jumps(self, kappa, phi, psi, f_gamma, jm, f_gamma_sign=1.0):
         k = complex(kappa)
         N.check(self._lib.kfbi_jumps(self.handle, self._dt(jm.is_complex()), k.real, k.imag,

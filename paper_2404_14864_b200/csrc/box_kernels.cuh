@@ -15,6 +15,13 @@ struct BoxArgs {
   const int *done;        // early-exit flag (Richardson sweeps), may be null
   const double2 *twg;     // [m] exp(-2 pi i q / m)        (register engine)
   const double *sinv;     // [m] sin(pi j / m)              (register engine)
+  // Row slabs (one GPU: a single slab, rows = m, row0 = 0, npl = all panels).
+  // This rank's row pass covers grid rows [row0, row0 + rows); its field
+  // arrays hold exactly those rows (row j at (j - row0) * (m + 1)), and its
+  // panel buffer is [panel][rows][w].  Its column pass covers panels
+  // [pp0, pp0 + npl) of every row, received as nranks blocks [rank][npl][rows][w].
+  int rows, row0, pp0, npl;
+  int ring_end;           // the field array also holds row m (zero ring)
 };
 
 // Sparse right-hand-side corrections fused into the forward row pass.

@@ -10,12 +10,18 @@
 //
 // Panels (the intermediate spectrum): 32-byte column strips indexed by the
 // spectral x index kx (column 0 is padding) and the row / spectral y index j
-// (row 0 is padding).  Real: panel pp holds kx = 4pp..4pp+3,
-// P[(pp*M + j)*4 + w]; complex: kx = 2pp..2pp+1, P2[(pp*M + j)*2 + w].  A
-// column pass reads one M*32-byte slab (two CTAs per slab, one per 16-byte
-// half); a row pair of a real panel is one contiguous 64-byte chunk.  All
-// global traffic goes through the shared-memory staging buffer so that
-// consecutive lanes touch consecutive 16-byte pieces.
+// (row 0 is the zero ring).  Real: panel pp holds kx = 4pp..4pp+3,
+// P[(pp*R + r)*4 + w]; complex: kx = 2pp..2pp+1, P2[(pp*R + r)*2 + w], with
+// r the row within the slab of R rows (R = M on one GPU).  A column pass
+// reads one 32-byte-wide strip per panel (two CTAs per strip, one per
+// 16-byte half); a row pair (2q, 2q+1) of a real panel is one contiguous
+// 64-byte chunk.  All global traffic goes through the shared-memory staging
+// buffer so that consecutive lanes touch consecutive 16-byte pieces.
+//
+// Slab decomposition (BoxArgs rows/row0/pp0/npl): the row passes of rank g
+// touch only its rows, the column pass only its panels, and the two
+// all-to-all transposes between them (NCCL, dist.py) move whole contiguous
+// [panel range][rows] blocks, so no pack / unpack pass exists.
 //
 // One CTA = 256 threads = 256*16 complex elements in registers: one length-
 // 4096 sequence, or 4096/N shorter ones.  Real rows/columns are packed two
@@ -75,10 +81,10 @@ rows_fwd_reg(BoxArgs a, const void *__restrict__ rhs, double sign,
   const reg::View<LOGN> sm = reg::make_view<LOGN>(smem, seq, t);
   const int stride = M + 1;
   const int q = seq_index<LOGN>(seq);
-  const int nseq = CPLX ? M - 1 : M / 2;
+  const int nseq = CPLX ? a.rows : a.rows / 2;
   const bool valid = q < nseq;
-  const int j0 = CPLX ? q + 1 : 2 * q + 1;
-  const bool has2 = !CPLX && valid && j0 + 1 < M;
+  const int r0 = CPLX ? q : 2 * q;               // slab row of the sequence
+  const int j0 = a.row0 + r0;                    // grid row (row 0: zero ring)
 
   double2 v[reg::E];
 #pragma unroll
@@ -87,11 +93,11 @@ rows_fwd_reg(BoxArgs a, const void *__restrict__ rhs, double sign,
     v[m] = make_double2(0.0, 0.0);
     if (valid && n >= 1 && rhs != nullptr) {
       if (CPLX) {
-        v[m] = static_cast<const double2 *>(rhs)[(size_t)j0 * stride + n];
+        if (j0 >= 1) v[m] = static_cast<const double2 *>(rhs)[(size_t)r0 * stride + n];
       } else {
         const double *r = static_cast<const double *>(rhs);
-        v[m].x = r[(size_t)j0 * stride + n];
-        if (has2) v[m].y = r[(size_t)(j0 + 1) * stride + n];
+        if (j0 >= 1) v[m].x = r[(size_t)r0 * stride + n];
+        v[m].y = r[(size_t)(r0 + 1) * stride + n];
       }
     }
   }
@@ -101,8 +107,8 @@ rows_fwd_reg(BoxArgs a, const void *__restrict__ rhs, double sign,
   if (corr.jv) {
     reg::seq_sync<LOGN>();
     if (valid) {
-      const int nrows = has2 ? 2 : 1;
-      for (int qq = 0; qq < nrows; ++qq) {
+      const int nrows = CPLX ? 1 : 2;
+      for (int qq = (j0 == 0); qq < nrows; ++qq) {
         const int j = j0 + qq;
         const int g0 = corr.row_group[j], g1 = corr.row_group[j + 1];
         for (int g = g0 + t; g < g1; g += TT) {
@@ -129,18 +135,18 @@ rows_fwd_reg(BoxArgs a, const void *__restrict__ rhs, double sign,
     // panel stores: consecutive lanes write consecutive 16-byte pieces of a
     // panel's (row j0, row j0+1) 64-byte chunk (real) / 32-byte row (complex)
     double2 *P2 = static_cast<double2 *>(a.panels);
+    const size_t R = a.rows;
     if (!CPLX) {
       for (int i = t; i < M; i += TT) {          // M/4 panels x 4 pieces
         const int pp = i >> 2, part = i & 3, row = part >> 1;
-        if (row && !has2) continue;
         const int n0 = 4 * pp + 2 * (part & 1);
         const double2 v0 = sm[n0], v1 = sm[n0 + 1];
-        P2[((size_t)pp * M + j0 + row) * 2 + (part & 1)] =
+        P2[(pp * R + r0 + row) * 2 + (part & 1)] =
             row ? make_double2(v0.y, v1.y) : make_double2(v0.x, v1.x);
       }
     } else {
       for (int i = t; i < M; i += TT)            // M/2 panels x 2 pieces
-        P2[((size_t)(i >> 1) * M + j0) * 2 + (i & 1)] = sm[i];
+        P2[((i >> 1) * R + r0) * 2 + (i & 1)] = sm[i];
     }
   }
   if constexpr (C::CL > 1) reg::seq_sync<LOGN>();   // keep the cluster's smem alive
@@ -156,16 +162,23 @@ __global__ void __launch_bounds__(reg::Cfg<LOGN>::CTA_T, reg::Cfg<LOGN>::MINB) c
   int seq, t;
   const reg::View<LOGN> sm = reg::make_view<LOGN>(smem, seq, t);
   const int q = seq_index<LOGN>(seq);
-  const int nseq = CPLX ? M : M / 2;
+  const int nseq = 2 * a.npl;                    // half panels of this rank
   const bool valid = q < nseq;
-  const int pp = q >> 1, half = q & 1;
-  double2 *col = static_cast<double2 *>(a.panels) + (size_t)pp * M * 2 + half;
+  const int pl = q >> 1, half = q & 1;
+  const int pp = a.pp0 + pl;                     // global panel
+  // row j of the strip lives in rank block j / R (R = a.rows, a power of two)
+  const int lr = 31 - __clz(a.rows);
+  double2 *P2 = static_cast<double2 *>(a.panels);
+  auto at = [&](int j) -> double2 & {
+    const size_t blk = (size_t)(j >> lr) * a.npl + pl;
+    return P2[(blk * a.rows + (j & (a.rows - 1))) * 2 + half];
+  };
 
   double2 v[reg::E];
 #pragma unroll
   for (int m = 0; m < reg::E; ++m) {
     const int n = t + m * TT;
-    v[m] = (valid && n >= 1) ? col[2 * n] : make_double2(0.0, 0.0);
+    v[m] = (valid && n >= 1) ? at(n) : make_double2(0.0, 0.0);
   }
   stage<LOGN>(sm, v, t);
   reg::seq_sync<LOGN>();
@@ -197,7 +210,7 @@ __global__ void __launch_bounds__(reg::Cfg<LOGN>::CTA_T, reg::Cfg<LOGN>::MINB) c
   unstage<LOGN>(sm, out, t);
   reg::seq_sync<LOGN>();
   if (valid)
-    for (int n = t; n < M; n += TT) col[2 * n] = sm[n];
+    for (int n = t; n < M; n += TT) at(n) = sm[n];
   if constexpr (C::CL > 1) reg::seq_sync<LOGN>();
 }
 
@@ -213,21 +226,21 @@ rows_inv_reg(BoxArgs a, void *__restrict__ u) {
   const reg::View<LOGN> sm = reg::make_view<LOGN>(smem, seq, t);
   const int stride = M + 1;
   const int q = seq_index<LOGN>(seq);
-  const int nseq = CPLX ? M - 1 : M / 2;
+  const int nseq = CPLX ? a.rows : a.rows / 2;
   const bool valid = q < nseq;
-  const int j0 = CPLX ? q + 1 : 2 * q + 1;
-  const bool has2 = !CPLX && valid && j0 + 1 < M;
+  const int r0 = CPLX ? q : 2 * q;               // slab row of the sequence
+  const int j0 = a.row0 + r0;                    // grid row (row 0: zero ring)
+  const size_t R = a.rows;
 
   const double2 *P2 = static_cast<const double2 *>(a.panels);
   if (!CPLX) {
-    // lanes read consecutive 16-byte pieces of each panel's (j0, j0+1)
+    // lanes read consecutive 16-byte pieces of each panel's (r0, r0+1)
     // 64-byte chunk and scatter them into the .x / .y halves of the slots
     double2 v[reg::E];
 #pragma unroll
     for (int m = 0; m < reg::E; ++m) {
       const int i = t + m * TT, pp = i >> 2, part = i & 3, row = part >> 1;
-      v[m] = (valid && (has2 || !row)) ? P2[((size_t)pp * M + j0 + row) * 2 + (part & 1)]
-                                       : make_double2(0.0, 0.0);
+      v[m] = valid ? P2[(pp * R + r0 + row) * 2 + (part & 1)] : make_double2(0.0, 0.0);
     }
 #pragma unroll
     for (int m = 0; m < reg::E; ++m) {
@@ -243,7 +256,7 @@ rows_inv_reg(BoxArgs a, void *__restrict__ u) {
 #pragma unroll
     for (int m = 0; m < reg::E; ++m) {
       const int n = t + m * TT;
-      v[m] = (valid && n >= 1) ? P2[((size_t)(n >> 1) * M + j0) * 2 + (n & 1)] : make_double2(0.0, 0.0);
+      v[m] = (valid && n >= 1) ? P2[((n >> 1) * R + r0) * 2 + (n & 1)] : make_double2(0.0, 0.0);
     }
     stage<LOGN>(sm, v, t);
   }
@@ -254,32 +267,31 @@ rows_inv_reg(BoxArgs a, void *__restrict__ u) {
   unstage<LOGN>(sm, out, t);
   reg::seq_sync<LOGN>();
   if (valid) {
-    // coalesced row stores with the zero ring (boxsolve.py:90-93)
+    // coalesced row stores with the zero ring (boxsolve.py:90-93); grid row
+    // 0 comes out of the transforms as exact zeros (its input is zero)
+    const bool last = a.ring_end && q == nseq - 1;   // also write ring row M
     if (!CPLX) {
       double *U = static_cast<double *>(u);
-      double *u0 = U + (size_t)j0 * stride;
-      double *u1 = U + (size_t)(j0 + 1) * stride;   // ring row M when !has2
+      double *u0 = U + (size_t)r0 * stride;
+      double *u1 = u0 + stride;
       for (int n = t; n <= M; n += TT) {
         double x = 0.0, y = 0.0;
         if (n >= 1 && n < M) {
           const double2 w = sm[n];
-          x = w.x;
-          y = has2 ? w.y : 0.0;
+          x = j0 ? w.x : 0.0;
+          y = w.y;
         }
         u0[n] = x;
         u1[n] = y;
+        if (last) u1[stride + n] = 0.0;
       }
-      if (q == 0)
-        for (int n = t; n <= M; n += TT) U[n] = 0.0;
     } else {
       double2 *U = static_cast<double2 *>(u);
-      double2 *u0 = U + (size_t)j0 * stride;
-      for (int n = t; n <= M; n += TT)
-        u0[n] = (n >= 1 && n < M) ? sm[n] : make_double2(0.0, 0.0);
-      if (q == 0)
-        for (int n = t; n <= M; n += TT) U[n] = make_double2(0.0, 0.0);
-      if (j0 == M - 1)
-        for (int n = t; n <= M; n += TT) U[(size_t)M * stride + n] = make_double2(0.0, 0.0);
+      double2 *u0 = U + (size_t)r0 * stride;
+      for (int n = t; n <= M; n += TT) {
+        u0[n] = (n >= 1 && n < M && j0) ? sm[n] : make_double2(0.0, 0.0);
+        if (last) u0[stride + n] = make_double2(0.0, 0.0);
+      }
     }
   }
   if constexpr (C::CL > 1) reg::seq_sync<LOGN>();

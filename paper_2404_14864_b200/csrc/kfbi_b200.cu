@@ -141,8 +141,11 @@ kfbi_status launch(kfbi_plan *p, int name, cudaStream_t s, F &&fn) {
     pe.b = p->take_event();
     cudaEventRecord(pe.a, s);
   }
-  fn();
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e = cudaSuccess;
+  if constexpr (std::is_same<decltype(fn()), cudaError_t>::value) e = fn();
+  else fn();
+  cudaError_t e2 = cudaGetLastError();
+  if (e == cudaSuccess) e = e2;
   if (p->timing) {
     cudaEventRecord(pe.b, s);
     p->pending.push_back(pe);
@@ -192,7 +195,28 @@ BoxArgs box_args(kfbi_plan *p, double kre, double kim, const int *done) {
   a.done = done;
   a.twg = p->twg.p;
   a.sinv = p->sinv.p;
+  a.rows = p->m;             // one slab: the whole grid
+  a.row0 = 0;
+  a.pp0 = 0;
+  a.npl = 0;                 // set per dtype by the launcher
+  a.ring_end = 1;
   return a;
+}
+
+// Slab geometry of rank `rank` of `nranks` (rows and panels split evenly).
+kfbi_status slab_args(kfbi_plan *p, bool cplx, int nranks, int rank, BoxArgs &a) {
+  const int m = p->m;
+  if (nranks < 1 || rank < 0 || rank >= nranks || (nranks & (nranks - 1)) != 0)
+    return fail(KFBI_E_CONFIG, "slab: nranks must be a power of two and 0 <= rank < nranks");
+  const int npanels = cplx ? m / 2 : m / 4;
+  if (m / nranks < 2 || npanels % nranks != 0)
+    return fail(KFBI_E_CONFIG, "slab: too many ranks for this grid");
+  a.rows = m / nranks;
+  a.row0 = rank * a.rows;
+  a.npl = npanels / nranks;
+  a.pp0 = rank * a.npl;
+  a.ring_end = 0;
+  return KFBI_OK;
 }
 
 template <typename T>
@@ -258,11 +282,12 @@ cudaError_t reg_launch(K kernel, int grid, cudaStream_t s, Args... args) {
   }
 }
 
-// Register-engine passes for one (dtype, log2 M).
+// Register-engine passes for one (dtype, log2 M); `passes` selects any of
+// rows_fwd (1), cols (2), rows_inv (4).
 template <bool CPLX, int LOGN>
 kfbi_status box_reg_launch(kfbi_plan *p, const BoxArgs &a, const void *rhs, double sign,
                            const CorrArgs<typename std::conditional<CPLX, double2, double>::type> &c,
-                           void *u, cudaStream_t s) {
+                           void *u, int passes, cudaStream_t s) {
   using Cf = reg::Cfg<LOGN>;
   static bool attr = false;   // per instantiation, process wide
   if (!attr) {
@@ -275,35 +300,32 @@ kfbi_status box_reg_launch(kfbi_plan *p, const BoxArgs &a, const void *rhs, doub
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, bytes), "transform-cols");
     attr = true;
   }
-  const int M = Cf::N;
-  const int nrow = CPLX ? M - 1 : M / 2;     // row sequences
-  const int ncol = CPLX ? M : M / 2;         // half-panel sequences
+  const int nrow = CPLX ? a.rows : a.rows / 2;     // row sequences of the slab
+  const int ncol = 2 * a.npl;                      // half-panel sequences
   const int grow = Cf::CL > 1 ? nrow * Cf::CL : (nrow + Cf::S - 1) / Cf::S;
   const int gcol = Cf::CL > 1 ? ncol * Cf::CL : (ncol + Cf::S - 1) / Cf::S;
   using CT = typename std::conditional<CPLX, double2, double>::type;
-  KFBI_TRY(launch(p, KFBI_K_ROWS, s, [&] {
-    reg_launch<LOGN>(rows_fwd_reg<CPLX, LOGN>, grow, s, a, rhs, sign, CorrArgs<CT>(c));
-  }));
-  KFBI_TRY(launch(p, KFBI_K_COLS, s, [&] { reg_launch<LOGN>(cols_reg<CPLX, LOGN>, gcol, s, a); }));
-  return launch(p, KFBI_K_ROWS, s, [&] { reg_launch<LOGN>(rows_inv_reg<CPLX, LOGN>, grow, s, a, u); });
+  if (passes & 1)
+    KFBI_TRY(launch(p, KFBI_K_ROWS, s, [&] {
+      return reg_launch<LOGN>(rows_fwd_reg<CPLX, LOGN>, grow, s, a, rhs, sign, CorrArgs<CT>(c));
+    }));
+  if (passes & 2)
+    KFBI_TRY(launch(p, KFBI_K_COLS, s, [&] { return reg_launch<LOGN>(cols_reg<CPLX, LOGN>, gcol, s, a); }));
+  if (passes & 4)
+    KFBI_TRY(launch(p, KFBI_K_ROWS, s, [&] { return reg_launch<LOGN>(rows_inv_reg<CPLX, LOGN>, grow, s, a, u); }));
+  return KFBI_OK;
 }
 
 template <bool CPLX>
 kfbi_status box_passes_reg(kfbi_plan *p, const BoxArgs &a, const void *rhs, double sign,
                            const CorrArgs<typename std::conditional<CPLX, double2, double>::type> &c,
-                           void *u, cudaStream_t s) {
+                           void *u, cudaStream_t s, int passes = 7) {
   switch (p->logm) {
-    case 4: return box_reg_launch<CPLX, 4>(p, a, rhs, sign, c, u, s);
-    case 5: return box_reg_launch<CPLX, 5>(p, a, rhs, sign, c, u, s);
-    case 6: return box_reg_launch<CPLX, 6>(p, a, rhs, sign, c, u, s);
-    case 7: return box_reg_launch<CPLX, 7>(p, a, rhs, sign, c, u, s);
-    case 8: return box_reg_launch<CPLX, 8>(p, a, rhs, sign, c, u, s);
-    case 9: return box_reg_launch<CPLX, 9>(p, a, rhs, sign, c, u, s);
-    case 10: return box_reg_launch<CPLX, 10>(p, a, rhs, sign, c, u, s);
-    case 11: return box_reg_launch<CPLX, 11>(p, a, rhs, sign, c, u, s);
-    case 12: return box_reg_launch<CPLX, 12>(p, a, rhs, sign, c, u, s);
-    case 13: return box_reg_launch<CPLX, 13>(p, a, rhs, sign, c, u, s);
-    case 14: return box_reg_launch<CPLX, 14>(p, a, rhs, sign, c, u, s);
+#define KFBI_CASE(L) \
+    case L: return box_reg_launch<CPLX, L>(p, a, rhs, sign, c, u, passes, s);
+    KFBI_CASE(4) KFBI_CASE(5) KFBI_CASE(6) KFBI_CASE(7) KFBI_CASE(8) KFBI_CASE(9)
+    KFBI_CASE(10) KFBI_CASE(11) KFBI_CASE(12) KFBI_CASE(13) KFBI_CASE(14)
+#undef KFBI_CASE
     default: return fail(KFBI_E_CONFIG, "register DST engine: unsupported M");
   }
 }
@@ -315,9 +337,33 @@ kfbi_status box_passes(kfbi_plan *p, double kre, double kim, const void *rhs, do
                        const void *jv, void *u, const int *done, cudaStream_t s) {
   using T = typename std::conditional<CPLX, double2, double>::type;
   BoxArgs a = box_args(p, kre, kim, done);
+  a.npl = CPLX ? p->m / 2 : p->m / 4;
   CorrArgs<T> c = corr_args<T>(p, static_cast<const T *>(jv));
   if (!jv) c.jv = nullptr;
   return box_passes_reg<CPLX>(p, a, rhs, sign, c, u, s);
+}
+
+// One pass of the slab-decomposed box solve (kfbi_slab_*).
+kfbi_status slab_pass(kfbi_plan *p, int32_t dtype, const kfbi_slab *sl, int passes, double kre,
+                      double kim, const void *rhs, double sign, const void *jv, void *panels,
+                      void *u, void *stream) {
+  KFBI_TRY(check_plan(p));
+  if (!sl || !panels) return fail(KFBI_E_CONFIG, "slab: null argument");
+  const bool cplx = dtype == KFBI_C128;
+  if (!cplx && kim != 0.0) return fail(KFBI_E_CONFIG, "complex kappa requires the c128 path");
+  if (jv && !p->has_geo) return fail(KFBI_E_CONFIG, "slab: corrections need the plan's geometry");
+  BoxArgs a = box_args(p, kre, kim, nullptr);
+  KFBI_TRY(slab_args(p, cplx, sl->nranks, sl->rank, a));
+  a.panels = panels;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (cplx) {
+    CorrArgs<double2> c = corr_args<double2>(p, static_cast<const double2 *>(jv));
+    if (!jv) c.jv = nullptr;
+    return box_passes_reg<true>(p, a, rhs, sign, c, u, s, passes);
+  }
+  CorrArgs<double> c = corr_args<double>(p, static_cast<const double *>(jv));
+  if (!jv) c.jv = nullptr;
+  return box_passes_reg<false>(p, a, rhs, sign, c, u, s, passes);
 }
 
 kfbi_status box_dispatch(kfbi_plan *p, int dtype, double kre, double kim, const void *rhs,
@@ -604,6 +650,29 @@ kfbi_status kfbi_plan_create(const kfbi_grid_desc *desc, kfbi_plan **out) {
   cudaMallocHost(&p->red_host, 4 * sizeof(unsigned long long));
   *out = p;
   return KFBI_OK;
+}
+
+kfbi_status kfbi_slab_panel_bytes(kfbi_plan *p, int32_t dtype, int32_t nranks, int64_t *bytes) {
+  KFBI_TRY(check_plan(p));
+  if (!bytes || nranks < 1) return fail(KFBI_E_CONFIG, "slab: bad argument");
+  *bytes = (int64_t)(p->m / nranks) * p->m * (dtype == KFBI_C128 ? 16 : 8);
+  return KFBI_OK;
+}
+
+kfbi_status kfbi_slab_rows_fwd(kfbi_plan *p, int32_t dtype, const kfbi_slab *sl, const void *rhs,
+                               double sign, const void *jv, void *panels, void *stream) {
+  return slab_pass(p, dtype, sl, 1, 0.0, 0.0, rhs, sign, jv, panels, nullptr, stream);
+}
+
+kfbi_status kfbi_slab_cols(kfbi_plan *p, int32_t dtype, const kfbi_slab *sl, double kappa_re,
+                           double kappa_im, void *panels, void *stream) {
+  return slab_pass(p, dtype, sl, 2, kappa_re, kappa_im, nullptr, 1.0, nullptr, panels, nullptr, stream);
+}
+
+kfbi_status kfbi_slab_rows_inv(kfbi_plan *p, int32_t dtype, const kfbi_slab *sl, const void *panels,
+                               void *u, void *stream) {
+  return slab_pass(p, dtype, sl, 4, 0.0, 0.0, nullptr, 1.0, nullptr, const_cast<void *>(panels), u,
+                   stream);
 }
 
 kfbi_status kfbi_plan_destroy(kfbi_plan *p) {
