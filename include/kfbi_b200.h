@@ -95,7 +95,7 @@ typedef struct {
   const double *jcoef;        /* [n_ctl][6][6] jump-shift coefficients   */
 } kfbi_geometry;
 
-/* One Dirichlet BVP solve by Richardson iteration (BvpProblem,
+/* One Dirichlet or Neumann BVP solve by Richardson iteration (BvpProblem,
  * bvp.py:231-262; richardson_solve, bvp.py:276-351).  Device pointers. */
 typedef struct {
   int32_t dtype;
@@ -116,6 +116,10 @@ typedef struct {
   int32_t log_slot;       /* >= 0 (operator form only): fully asynchronous;
                              iterations / status land in the plan's step log
                              (kfbi_log_fetch), result fields are -1 (pending) */
+  int32_t bc_kind;        /* 0 Dirichlet (density = phi, trace u+), 1 Neumann
+                             (density = psi, trace d_n u+, one-sided
+                             extraction; bvp.py:313-323) */
+  int32_t box_bc;         /* kfbi_box_bc closure of the box solves          */
 } kfbi_bvp;
 
 /* One entry of the plan's device-side step log (asynchronous stepping). */
@@ -146,7 +150,24 @@ kfbi_status kfbi_box_solve(kfbi_plan *plan, int32_t dtype, double kappa_re,
                            double kappa_im, const void *rhs, void *u,
                            void *stream);
 
+/* BoxSolver.solve with either closure (boxsolve.py:46-94): dirichlet-zero
+ * (DST-I, zero ring) or neumann-zero (DCT-I, mirror ghost, rhs read on the
+ * whole grid; kappa = 0 rejected as singular, boxsolve.py:32-33). */
+kfbi_status kfbi_box_solve_bc(kfbi_plan *plan, int32_t dtype, int32_t box_bc,
+                              double kappa_re, double kappa_im, const void *rhs,
+                              void *u, void *stream);
+
 kfbi_status kfbi_plan_set_geometry(kfbi_plan *plan, const kfbi_geometry *geo);
+
+/* OneSidedExtractor tables (bvp.py:115-212), host pointers: stencil7
+ * [n_ctl][7] flat node indices, rows [n_ctl][3][7] (rows 0..2 of inv(A)),
+ * fallback [n_ctl] (1: the point uses the six-point straddling stencil). */
+kfbi_status kfbi_plan_set_onesided(kfbi_plan *plan, int32_t n_ctl, const int32_t *stencil7,
+                                   const double *rows, const uint8_t *fallback);
+
+/* OneSidedExtractor.extract (bvp.py:214-228): out [3][n_ctl]. */
+kfbi_status kfbi_extract_onesided(kfbi_plan *plan, int32_t dtype, const void *u,
+                                  const void *jm, void *out, void *stream);
 
 /* compute_jumps (interface.py:171-203): jm out is SoA [6][n_ctl]
  * (u, ux, uy, uxx, uxy, uyy).  psi may be NULL (zero). */
@@ -164,6 +185,10 @@ kfbi_status kfbi_interface_solve(kfbi_plan *plan, int32_t dtype,
                                  double kappa_re, double kappa_im,
                                  const void *F, const void *jm, void *u,
                                  void *stream);
+kfbi_status kfbi_interface_solve_bc(kfbi_plan *plan, int32_t dtype, int32_t box_bc,
+                                    double kappa_re, double kappa_im,
+                                    const void *F, const void *jm, void *u,
+                                    void *stream);
 
 /* TraceExtractor.extract (bvp.py:88-104): out [3][n_ctl] = (u+, ux+, uy+). */
 kfbi_status kfbi_extract(kfbi_plan *plan, int32_t dtype, const void *u,
@@ -213,6 +238,11 @@ kfbi_status kfbi_richardson(kfbi_plan *plan, const kfbi_bvp *bvp,
 kfbi_status kfbi_build_trace_operator(kfbi_plan *plan, int32_t dtype,
                                       double kappa_re, double kappa_im,
                                       void *stream);
+/* ... for a Dirichlet (bc_kind 0, T: phi -> u+) or Neumann (bc_kind 1,
+ * T: psi -> d_n u+) BVP with the given box closure. */
+kfbi_status kfbi_build_trace_operator_bc(kfbi_plan *plan, int32_t dtype, int32_t bc_kind,
+                                         int32_t box_bc, double kappa_re,
+                                         double kappa_im, void *stream);
 
 /* Time-stepping right-hand sides (timestepping.py), element-wise over n
  * values: the (M+1)^2 grid with the uint8 interior mask, or the n_ctl control

@@ -25,7 +25,7 @@ import os
 from dataclasses import dataclass, field
 
 import numpy as np
-from scipy.fft import dst, idst
+from scipy.fft import dct, dst, idct, idst
 
 WORKERS = int(os.environ.get("KFBI_ORACLE_WORKERS", "1"))
 
@@ -61,34 +61,51 @@ class Tables:
     stencil: np.ndarray
     ainv: np.ndarray
     jcoef: np.ndarray
+    # one-sided extractor (Neumann; bvp.py:115-212), optional
+    os_stencil: np.ndarray = None
+    os_rows: np.ndarray = None
+    os_fallback: np.ndarray = None
 
 
-def tables_from_workspace(ws):
+def tables_from_workspace(ws, onesided=False):
     grid, cps, rec = ws.grid, ws.cps, ws.records
     stencil, ainv, jcoef = ws.trace_tables()
+    os_tabs = {}
+    if onesided:
+        ox = ws.onesided()
+        os_tabs = dict(os_stencil=ox.stencil_flat, os_rows=ox._rows, os_fallback=ox._fallback)
     return Tables(
         m=grid.m, h=grid.h, mask=ws.geometry.classification.interior, X=grid.X, Y=grid.Y,
         ctl_x=cps.x, ctl_y=cps.y, theta=cps.theta, dtheta=cps.dtheta, tangent=cps.tangent,
         normal=cps.normal, dtan_ds=cps.dtan_ds, speed=cps.speed, inv3=ws._inv3,
         w_records=ws.w_records, rec_d=rec.d, rec_axis=rec.axis,
         rec_owner_interior=rec.owner_interior, group_starts=rec.group_starts,
-        group_owners=rec.group_owners, stencil=stencil, ainv=ainv, jcoef=jcoef)
+        group_owners=rec.group_owners, stencil=stencil, ainv=ainv, jcoef=jcoef, **os_tabs)
 
 
 # ---------------------------------------------------------------------------
 # box solve — boxsolve.py:38-44 (eigenvalues), :46-94 (dirichlet-zero solve)
 
-def eigen_denominators(m, h, kappa):
-    lam = (2.0 * np.cos(np.arange(1, m) * np.pi / m) - 2.0) / h**2
+def eigen_denominators(m, h, kappa, bc="dirichlet-zero"):
+    p = np.arange(1, m) if bc == "dirichlet-zero" else np.arange(0, m + 1)
+    lam = (2.0 * np.cos(p * np.pi / m) - 2.0) / h**2
     return lam[:, None] + lam[None, :] - kappa
 
 
-def box_solve(m, h, kappa, rhs, denom=None):
-    """(Δ_h - κ) u = rhs, u = 0 on the box ring: DST-I rows, DST-I columns,
-    divide, inverse columns, inverse rows (boxsolve.py:58-93)."""
+def box_solve(m, h, kappa, rhs, denom=None, bc="dirichlet-zero"):
+    """(Δ_h - κ) u = rhs.  dirichlet-zero: u = 0 on the box ring, DST-I rows,
+    DST-I columns, divide, inverse columns, inverse rows (boxsolve.py:58-93);
+    neumann-zero: the same with DCT-I over the whole grid (mirror ghost)."""
     if denom is None:
-        denom = eigen_denominators(m, h, kappa)
+        denom = eigen_denominators(m, h, kappa, bc)
     dtype = np.result_type(rhs.dtype, np.asarray(kappa).dtype)
+    if bc == "neumann-zero":
+        w = np.array(rhs, dtype=dtype)
+        w = dct(w, type=1, axis=1, workers=WORKERS)
+        w = dct(w, type=1, axis=0, workers=WORKERS)
+        w /= denom
+        w = idct(w, type=1, axis=0, workers=WORKERS)
+        return idct(w, type=1, axis=1, workers=WORKERS)
     w = np.array(rhs[1:m, 1:m], dtype=dtype)
     w = dst(w, type=1, axis=1, workers=WORKERS)
     w = dst(w, type=1, axis=0, workers=WORKERS)
@@ -164,6 +181,20 @@ def extract(t, field, jm):
     return coeffs[:, 0], coeffs[:, 1] / t.h, coeffs[:, 2] / t.h
 
 
+# one-sided extraction — bvp.py:214-228 (Neumann)
+def extract_onesided(t, field, jm):
+    flat = field.ravel()
+    dtype = np.result_type(flat.dtype, float)
+    coeffs = np.einsum("pin,pn->pi", t.os_rows, flat[t.os_stencil]).astype(dtype)
+    fb = t.os_fallback
+    if len(fb):
+        su, sx, sy = extract(t, field, jm)
+        coeffs[fb, 0] = su[fb]
+        coeffs[fb, 1] = sx[fb] * t.h
+        coeffs[fb, 2] = sy[fb] * t.h
+    return coeffs[:, 0], coeffs[:, 1] / t.h, coeffs[:, 2] / t.h
+
+
 # ---------------------------------------------------------------------------
 # Richardson — bvp.py:276-351 (Dirichlet)
 
@@ -186,25 +217,32 @@ class NotConverged(Exception):
 
 
 def richardson(t, kappa, F, f_gamma, g, density0=None, gamma=0.8, tol=1e-8, max_iter=200,
-               max_sweeps=None):
-    """Damped fixed point φ <- φ + γ(g - u+[φ]).  Returns the field of the
-    converging sweep and the density after its update.  `max_sweeps` stops
-    early (timing samples) without raising."""
+               max_sweeps=None, bc_kind="dirichlet"):
+    """Damped fixed point φ <- φ + γ(g - u+[φ]) (Dirichlet) or
+    ψ <- ψ + γ(g - ∂ₙu+[ψ]) (Neumann: neumann-zero box, one-sided
+    extraction).  Returns the field of the converging sweep and the density
+    after its update.  `max_sweeps` stops early (timing samples) without
+    raising."""
+    dirichlet = bc_kind == "dirichlet"
+    box_bc = "dirichlet-zero" if dirichlet else "neumann-zero"
     dtype = np.result_type(F.dtype, np.asarray(kappa).dtype, np.asarray(g).dtype)
     n = t.theta.size
     density = (np.array(density0, dtype=dtype) if density0 is not None
                else np.zeros(n, dtype=dtype))
     zero = np.zeros(n, dtype=dtype)
     g = np.asarray(g, dtype=dtype)
-    denom = eigen_denominators(t.m, t.h, kappa)
+    denom = eigen_denominators(t.m, t.h, kappa, box_bc)
     history = []
     for it in range(1, max_iter + 1):
-        jm = jumps(t, kappa, density, zero, f_gamma)
+        if dirichlet:
+            jm = jumps(t, kappa, density, zero, f_gamma)
+        else:
+            jm = jumps(t, kappa, zero, density, f_gamma)
         c = corrections(t, jm)
-        u = box_solve(t.m, t.h, kappa, F + c, denom)
-        tu, tx, ty = extract(t, u, jm)
+        u = box_solve(t.m, t.h, kappa, F + c, denom, box_bc)
+        tu, tx, ty = (extract if dirichlet else extract_onesided)(t, u, jm)
         tun = tx * t.normal[:, 0] + ty * t.normal[:, 1]
-        update = gamma * (g - tu)
+        update = gamma * (g - (tu if dirichlet else tun))
         density += update
         res = float(np.max(np.abs(update)))
         history.append(res)
@@ -282,6 +320,7 @@ class Spec:
     gamma: float = 0.8
     tol: float = 1e-8
     max_iter: int = 200
+    bc_kind: str = "dirichlet"
 
     def n_steps(self):
         return int(round(self.t_final / self.tau))
@@ -329,30 +368,40 @@ class Stepper:
 
     def _solve(self, kappa, F, fg, g):
         sol = richardson(self.t, kappa, -F, -fg, g, self.density, self.spec.gamma, self.spec.tol,
-                         self.spec.max_iter, max_sweeps=self.max_sweeps)
+                         self.spec.max_iter, max_sweeps=self.max_sweeps,
+                         bc_kind=self.spec.bc_kind)
         self.density = sol.density
         self.iterations.append(sol.iterations)
         return sol
+
+    def _g(self, time):
+        """Boundary data at the controls (timestepping.py:166-170)."""
+        t, s = self.t, self.spec
+        if s.bc_kind == "neumann":
+            return np.asarray(s.g(t.ctl_x, t.ctl_y, time, t.normal))
+        return np.asarray(s.g(t.ctl_x, t.ctl_y, time))
 
     def step(self):
         t, s = self.t, self.spec
         zx, zy = t.ctl_x, t.ctl_y
         t_next = self.time + s.tau
+        neumann = s.bc_kind == "neumann"
         if s.equation == "heat":
             kappa = 2.0 * s.c / s.tau
-            g = s.g(zx, zy, t_next)
+            g = self._g(t_next)
             sol = self._solve(kappa, self.F, self.fg, g)
             u_next = np.where(t.mask, sol.u, 0.0)
             a = 4.0 * s.c / s.tau
             self.F = a * u_next - self.F
-            self.fg = a * g - self.fg
+            trace = sol.trace_u if neumann else g          # timestepping.py:230
+            self.fg = a * trace - self.fg
             self.u = u_next
         elif s.equation == "wave":
             tau, th = s.tau, s.theta
             kw = 1.0 / (th * tau**2)
             coef = (1.0 - 2.0 * th) / th
-            g_next = s.g(zx, zy, t_next)
-            sol = self._solve(kw, self.F, self.fg, g_next)
+            sol = self._solve(kw, self.F, self.fg, self._g(t_next))
+            g_next = sol.trace_u if neumann else self._g(t_next)   # timestepping.py:299
             un = np.where(t.mask, sol.u, 0.0)
             uc = self.u
             F_new = (2.0 * un - uc) * kw + coef * (kw * un - self.F) + (kw * uc - self.F_prev)

@@ -63,7 +63,7 @@ class Bvp(C.Structure):
         ("g", vp), ("density", vp), ("gamma", f64), ("tol", f64),
         ("max_iter", i32), ("sweeps_hint", i32),
         ("u", vp), ("trace_u", vp), ("trace_un", vp), ("use_operator", i32),
-        ("log_slot", i32),
+        ("log_slot", i32), ("bc_kind", i32), ("box_bc", i32),
     ]
 
 
@@ -90,6 +90,11 @@ _SIGNATURES = {
     "kfbi_extract": ([vp, i32, vp, vp, vp, vp], i32),
     "kfbi_richardson": ([vp, C.POINTER(Bvp), C.POINTER(BvpResult), vp], i32),
     "kfbi_build_trace_operator": ([vp, i32, f64, f64, vp], i32),
+    "kfbi_build_trace_operator_bc": ([vp, i32, i32, i32, f64, f64, vp], i32),
+    "kfbi_box_solve_bc": ([vp, i32, i32, f64, f64, vp, vp, vp], i32),
+    "kfbi_interface_solve_bc": ([vp, i32, i32, f64, f64, vp, vp, vp, vp], i32),
+    "kfbi_plan_set_onesided": ([vp, i32, vp, vp, vp], i32),
+    "kfbi_extract_onesided": ([vp, i32, vp, vp, vp, vp], i32),
     "kfbi_log_reserve": ([vp, i32], i32),
     "kfbi_log_norm": ([vp, i32, i32, vp], i32),
     "kfbi_log_fetch": ([vp, i32, i32, vp, vp], i32),

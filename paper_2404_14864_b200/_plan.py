@@ -15,6 +15,8 @@ import numpy as np
 from . import _native as N
 
 _F64 = np.float64
+_BOX = {"dirichlet-zero": 0, "neumann-zero": 1}
+_KIND = {"dirichlet": 0, "neumann": 1}
 
 
 def _c(a, dtype):
@@ -33,6 +35,7 @@ class Plan:
         N.check(self._lib.kfbi_plan_create(C.byref(desc), C.byref(handle)))
         self.handle = handle
         self.has_geometry = False
+        self.has_onesided = False
         self._keep = []
         backend.register(self)
 
@@ -101,10 +104,11 @@ class Plan:
     def _dt(cplx):
         return N.C128 if cplx else N.F64
 
-    def box_solve(self, rhs, u, kappa):
+    def box_solve(self, rhs, u, kappa, bc="dirichlet-zero"):
         k = complex(kappa)
-        N.check(self._lib.kfbi_box_solve(self.handle, self._dt(u.is_complex()), k.real, k.imag,
-                                         rhs.data_ptr(), u.data_ptr(), self.stream))
+        N.check(self._lib.kfbi_box_solve_bc(self.handle, self._dt(u.is_complex()), _BOX[bc],
+                                            k.real, k.imag, rhs.data_ptr(), u.data_ptr(),
+                                            self.stream))
 
     # -- slab-decomposed box solve (dist.py) ----------------------------------
     def slab_panel_bytes(self, cplx, nranks):
@@ -138,35 +142,52 @@ class Plan:
         N.check(self._lib.kfbi_corrections(self.handle, self._dt(jm.is_complex()), jm.data_ptr(),
                                            c.data_ptr(), self.stream))
 
-    def interface_solve(self, kappa, F, jm, u):
+    def interface_solve(self, kappa, F, jm, u, bc="dirichlet-zero"):
         k = complex(kappa)
-        N.check(self._lib.kfbi_interface_solve(self.handle, self._dt(u.is_complex()), k.real,
-                                               k.imag, F.data_ptr(), jm.data_ptr(),
-                                               u.data_ptr(), self.stream))
+        N.check(self._lib.kfbi_interface_solve_bc(self.handle, self._dt(u.is_complex()), _BOX[bc],
+                                                  k.real, k.imag, F.data_ptr(), jm.data_ptr(),
+                                                  u.data_ptr(), self.stream))
 
     def extract(self, u, jm, out):
         N.check(self._lib.kfbi_extract(self.handle, self._dt(out.is_complex()), u.data_ptr(),
                                        jm.data_ptr(), out.data_ptr(), self.stream))
 
-    def build_operator(self, kappa, cplx):
-        """Trace operator T of this geometry for one kappa (n_ctl pipeline
-        evaluations, once per (geometry, kappa))."""
+    def set_onesided(self, stencil7, rows, fallback_mask):
+        """Upload the OneSidedExtractor tables (Neumann BVPs)."""
+        st = _c(stencil7, np.int32)
+        rw = _c(rows, _F64)
+        fb = _c(fallback_mask, np.uint8)
+        N.check(self._lib.kfbi_plan_set_onesided(self.handle, int(st.shape[0]),
+                                                 st.ctypes.data, rw.ctypes.data, fb.ctypes.data))
+        self.has_onesided = True
+
+    def extract_onesided(self, u, jm, out):
+        N.check(self._lib.kfbi_extract_onesided(self.handle, self._dt(out.is_complex()),
+                                                u.data_ptr(), jm.data_ptr(), out.data_ptr(),
+                                                self.stream))
+
+    def build_operator(self, kappa, cplx, bc_kind="dirichlet", box_bc=None):
+        """Trace operator T of this geometry for one kappa and BVP kind (n_ctl
+        pipeline evaluations, once per (geometry, kappa, kind))."""
         k = complex(kappa)
-        N.check(self._lib.kfbi_build_trace_operator(self.handle, self._dt(cplx), k.real, k.imag,
-                                                    self.stream))
-        self.operator_key = (k, bool(cplx))
+        box_bc = box_bc or ("dirichlet-zero" if bc_kind == "dirichlet" else "neumann-zero")
+        N.check(self._lib.kfbi_build_trace_operator_bc(
+            self.handle, self._dt(cplx), _KIND[bc_kind], _BOX[box_bc], k.real, k.imag,
+            self.stream))
+        self.operator_key = (k, bool(cplx), bc_kind, box_bc)
 
     def richardson(self, *, kappa, F, F_sign, f_gamma, f_gamma_sign, g, density, gamma, tol,
                    max_iter, u, trace_u, trace_un, sweeps_hint=0, use_operator=False,
-                   log_slot=-1):
+                   log_slot=-1, bc_kind="dirichlet", box_bc=None):
         k = complex(kappa)
+        box_bc = box_bc or ("dirichlet-zero" if bc_kind == "dirichlet" else "neumann-zero")
         b = N.Bvp(dtype=self._dt(u.is_complex()), kappa_re=k.real, kappa_im=k.imag,
                   F=F.data_ptr(), F_sign=float(F_sign), f_gamma=f_gamma.data_ptr(),
                   f_gamma_sign=float(f_gamma_sign), g=g.data_ptr(), density=density.data_ptr(),
                   gamma=float(gamma), tol=float(tol), max_iter=int(max_iter),
                   sweeps_hint=int(sweeps_hint), u=u.data_ptr(), trace_u=trace_u.data_ptr(),
                   trace_un=trace_un.data_ptr(), use_operator=int(bool(use_operator)),
-                  log_slot=int(log_slot))
+                  log_slot=int(log_slot), bc_kind=_KIND[bc_kind], box_bc=_BOX[box_bc])
         hist = np.zeros(max(int(max_iter), 1))
         res = N.BvpResult(history=hist.ctypes.data_as(C.POINTER(C.c_double)))
         status = self._lib.kfbi_richardson(self.handle, C.byref(b), C.byref(res), self.stream)

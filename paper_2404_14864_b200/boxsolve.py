@@ -4,7 +4,8 @@
 The dirichlet-zero closure diagonalises in the tensor-product sine basis with
 eigenvalues (2cos(p pi/M) - 2)/h^2, p = 1..M-1 (boxsolve.py:1-9, 38-44).  The
 solve is three sm_100a passes (rows DST-I, fused columns DST-I / scale /
-DST-I, rows DST-I) in ``libkfbi_b200.so``; see csrc/box_kernels.cuh.
+DST-I, rows DST-I) in ``libkfbi_b200.so``; see csrc/box_reg.cuh.  The
+neumann-zero closure is the same three passes with DCT-I (csrc/box_neu.cuh).
 """
 
 from __future__ import annotations
@@ -68,16 +69,15 @@ class BoxSolver:
         return lam[:, None] + lam[None, :] - self.kappa
 
     def solve(self, rhs):
-        """Full (M+1, M+1) solution; reads rhs at interior nodes only and
-        returns an exact zero ring (dirichlet-zero).  numpy in -> numpy out;
-        a CUDA tensor in -> CUDA tensor out (no host round trip)."""
+        """Full (M+1, M+1) solution.  dirichlet-zero reads rhs at interior
+        nodes only and returns an exact zero ring; neumann-zero reads rhs
+        everywhere (mirror ghost, DCT-I).  numpy in -> numpy out; a CUDA
+        tensor in -> CUDA tensor out (no host round trip)."""
         import torch
 
         m = self.grid.m
         if tuple(rhs.shape) != (m + 1, m + 1):
             raise GridError(f"rhs shape {tuple(rhs.shape)} does not match grid ({m + 1}, {m + 1})")
-        if self.bc != "dirichlet-zero":
-            raise ConfigError("the neumann-zero box closure is not available in this build")
         is_tensor = isinstance(rhs, torch.Tensor)
         rdt = np.complex128 if (rhs.is_complex() if is_tensor else np.iscomplexobj(rhs)) else np.float64
         out_dtype = np.result_type(rdt, np.asarray(self.kappa).dtype)
@@ -85,7 +85,7 @@ class BoxSolver:
 
         r = to_device(rhs, out_dtype, self.backend)
         u = torch.empty_like(r)
-        self.plan.box_solve(r, u, self.kappa)
+        self.plan.box_solve(r, u, self.kappa, self.bc)
         if is_tensor:
             return u.reshape(m + 1, m + 1)
         return u.cpu().numpy().reshape(m + 1, m + 1)

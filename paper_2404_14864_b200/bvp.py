@@ -60,9 +60,9 @@ def extract_trace(field, jumps, extractor, backend=None):
 class OneSidedExtractor:
     """Interior-only 7-node stencils for Neumann traces (bvp.py:115-228).
 
-    The tables are built on the host exactly as the reference does; the
-    Neumann device path (DCT-I box solve + this extractor) is the next item
-    of the build plan, so `extract` raises in this build."""
+    The tables are built on the host exactly as the reference does and
+    uploaded to the plan once (InterfaceWorkspace.ensure_onesided); the
+    extraction runs on the device (kfbi_extract_onesided)."""
 
     def __init__(self, workspace):
         self.workspace = workspace
@@ -134,8 +134,26 @@ class OneSidedExtractor:
         return None
 
     def extract(self, field, jumps, backend=None):
-        raise ConfigError("Neumann (one-sided) trace extraction is not available on the "
-                          "device in this build")
+        """(u+, u_x+, u_y+) from the interior-only stencils, the straddling
+        six-point stencil at the fallback points (bvp.py:214-228)."""
+        import torch
+
+        from .device import to_device
+        from .interface import _jm_device
+
+        ws = self.workspace
+        ws.ensure_onesided()
+        jm, cplx_j = _jm_device(jumps, ws)
+        cplx = cplx_j or (field.is_complex() if isinstance(field, torch.Tensor)
+                          else np.iscomplexobj(field))
+        dt = np.complex128 if cplx else np.float64
+        if cplx and not jm.is_complex():
+            jm = jm.to(torch.complex128)
+        u = to_device(field, dt, ws.backend)
+        out = torch.empty(3 * ws.cps.m, dtype=u.dtype, device=u.device)
+        ws.plan.extract_onesided(u, jm, out)
+        c = out.cpu().numpy().reshape(3, ws.cps.m)
+        return c[0], c[1], c[2]
 
 
 @dataclass
@@ -197,7 +215,7 @@ class DeviceBvp:
 
 def solve_device(ws, *, kappa, F, f_gamma, g, density, F_sign=1.0, f_gamma_sign=1.0,
                  gamma=0.8, tol=1e-8, max_iter=200, sweeps_hint=0, u_out=None,
-                 use_operator=False, log_slot=-1):
+                 use_operator=False, log_slot=-1, bc_kind="dirichlet", box_bc=None):
     """Richardson solve on device tensors (the inner loop of every time step).
 
     `density` is updated in place (it carries the warm start); F and f_gamma
@@ -209,13 +227,16 @@ def solve_device(ws, *, kappa, F, f_gamma, g, density, F_sign=1.0, f_gamma_sign=
 
     cplx = F.is_complex()
     n = ws.cps.m
+    if bc_kind == "neumann":
+        ws.ensure_onesided()
     u = u_out if u_out is not None else torch.empty_like(F)
     tu = torch.empty(n, dtype=F.dtype, device=F.device)
     tn = torch.empty_like(tu)
     it, res, hist = ws.plan.richardson(
         kappa=kappa, F=F, F_sign=F_sign, f_gamma=f_gamma, f_gamma_sign=f_gamma_sign, g=g,
         density=density, gamma=gamma, tol=tol, max_iter=max_iter, u=u, trace_u=tu,
-        trace_un=tn, sweeps_hint=sweeps_hint, use_operator=use_operator, log_slot=log_slot)
+        trace_un=tn, sweeps_hint=sweeps_hint, use_operator=use_operator, log_slot=log_slot,
+        bc_kind=bc_kind, box_bc=box_bc)
     del cplx
     return DeviceBvp(u=u, density=density, trace_u=tu, trace_un=tn, iterations=it,
                      residual=res, residual_history=hist)
@@ -231,12 +252,13 @@ def richardson_solve(problem, workspace, backend=None, extractor=None):
     if np.shape(problem.bc_values) != (m_ctl,):
         raise ConfigError(f"boundary data must have shape ({m_ctl},), got "
                           f"{np.shape(problem.bc_values)}")
-    if problem.bc_kind != "dirichlet" or problem.box_bc != "dirichlet-zero":
-        raise ConfigError("Neumann BVPs (one-sided extraction, DCT-I box) are not available "
-                          "on the device in this build")
-    if extractor is not None and not isinstance(extractor, TraceExtractor):
-        raise ConfigError("the device Richardson solve uses the six-point TraceExtractor")
-    ws.trace_tables()
+    dirichlet = problem.bc_kind == "dirichlet"
+    want = TraceExtractor if dirichlet else OneSidedExtractor
+    if extractor is not None and not isinstance(extractor, want):
+        raise ConfigError(f"the device Richardson solve of a {problem.bc_kind} BVP uses the "
+                          f"{want.__name__}")
+    if dirichlet:
+        ws.trace_tables()
     dtype = np.result_type(np.asarray(problem.F).dtype, np.asarray(problem.kappa).dtype,
                            np.asarray(problem.bc_values).dtype)
     cplx = np.issubdtype(dtype, np.complexfloating)
@@ -248,7 +270,8 @@ def richardson_solve(problem, workspace, backend=None, extractor=None):
     dens0 = problem.initial_density if problem.initial_density is not None else np.zeros(m_ctl, dt)
     density = to_device(dens0, dt, ws.backend).clone()
     sol = solve_device(ws, kappa=problem.kappa, F=F, f_gamma=fg, g=g, density=density,
-                       gamma=problem.gamma, tol=problem.tol, max_iter=problem.max_iter)
+                       gamma=problem.gamma, tol=problem.tol, max_iter=problem.max_iter,
+                       bc_kind=problem.bc_kind, box_bc=problem.box_bc)
     return BvpSolution(
         u=sol.u.cpu().numpy().reshape(mg + 1, mg + 1),
         density=sol.density.cpu().numpy(),

@@ -61,7 +61,7 @@ struct Cfg {
 // Shared memory bytes of one CTA (sequence buffer + scan scratch).
 template <int LOGN>
 constexpr size_t smem_bytes() {
-  return (size_t)Cfg<LOGN>::LOCAL * sizeof(double2) + (Cfg<LOGN>::CTA_T / 32) * sizeof(double2);
+  return ((size_t)Cfg<LOGN>::LOCAL + Cfg<LOGN>::CTA_T / 32 + Cfg<LOGN>::S) * sizeof(double2);
 }
 
 // Barrier over the threads of one sequence (CTA, or the cluster).
@@ -78,6 +78,7 @@ struct View {
   using C = Cfg<LOGN>;
   double2 *p[C::CL];              // per-rank sequence buffer
   double2 *scr[C::CL];            // per-rank scan scratch (CTA_T / 32 slots)
+  double2 *ext;                   // one extra slot (x_N of a DCT-I), rank 0
   KFBI_DEV double2 &operator[](int i) const {
     if constexpr (C::CL == 1) return p[0][sw(i)];
     else return p[i / C::LOCAL][sw(i & (C::LOCAL - 1))];
@@ -90,11 +91,13 @@ KFBI_DEV View<LOGN> make_view(double2 *smem, int &seq, int &t) {
   using C = Cfg<LOGN>;
   View<LOGN> v;
   double2 *scr = smem + C::LOCAL;
+  double2 *ext = scr + C::CTA_T / 32;
   if constexpr (C::CL == 1) {
     seq = threadIdx.x / C::T;
     t = threadIdx.x % C::T;
     v.p[0] = smem + seq * C::N;
     v.scr[0] = scr;
+    v.ext = ext + seq;
   } else {
     auto cl = cooperative_groups::this_cluster();
     const int rank = (int)cl.block_rank();
@@ -105,6 +108,7 @@ KFBI_DEV View<LOGN> make_view(double2 *smem, int &seq, int &t) {
       v.p[r] = cl.map_shared_rank(smem, r);
       v.scr[r] = cl.map_shared_rank(scr, r);
     }
+    v.ext = cl.map_shared_rank(ext, 0);
   }
   return v;
 }
@@ -295,11 +299,16 @@ KFBI_DEV void pre_from_smem(double2 (&v)[E], const View<LOGN> &sm, int t,
   }
 }
 
-// Post-processing + scan: out[c] = C_{16 t + c} (out[0] of t = 0 is C_0 = 0).
-// The view's scratch (CTA_T / 32 slots per rank) is used when T > 32.  Ends
-// with no barrier pending on sm (the caller syncs before overwriting sm).
-template <int LOGN>
-KFBI_DEV void post(const View<LOGN> &sm, int t, double2 (&out)[E]) {
+// Post-processing + scan: out[c] = C_{16 t + c}.  DST-I (DCT = false):
+// C_2k = i (Z_k - Z_{N-k}), odd terms R_k = Z_k + Z_{N-k}, R_0 = Z_0 (so
+// out[0] of t = 0 is C_0 = 0).  DCT-I (DCT = true): C_2k = Z_k + Z_{N-k},
+// R_k = i (Z_k - Z_{N-k}), R_0 = c1 (the separately reduced C_1).  Odd
+// outputs C_2k+1 = sum_{k' <= k} R_k'.  The view's scratch (CTA_T / 32
+// slots per rank) is used when T > 32.  Ends with no barrier pending on sm
+// (the caller syncs before overwriting sm).
+template <int LOGN, bool DCT = false>
+KFBI_DEV void post(const View<LOGN> &sm, int t, double2 (&out)[E],
+                   double2 c1 = make_double2(0.0, 0.0)) {
   constexpr int N = 1 << LOGN;
   constexpr int T = Cfg<LOGN>::T;
   double2 acc = make_double2(0.0, 0.0);
@@ -309,8 +318,15 @@ KFBI_DEV void post(const View<LOGN> &sm, int t, double2 (&out)[E]) {
     const double2 zk = sm[k];
     const double2 zm = sm[(N - k) & (N - 1)];
     const double2 d = csub(zk, zm);
-    out[2 * c] = make_double2(-d.y, d.x);              // i (Z_k - Z_{N-k})
-    const double2 r = (k == 0) ? zk : cadd(zk, zm);
+    const double2 id = make_double2(-d.y, d.x);        // i (Z_k - Z_{N-k})
+    double2 r;
+    if constexpr (!DCT) {
+      out[2 * c] = id;
+      r = (k == 0) ? zk : cadd(zk, zm);
+    } else {
+      out[2 * c] = cadd(zk, zm);
+      r = (k == 0) ? c1 : id;
+    }
     acc = (c == 0) ? r : cadd(acc, r);
     out[2 * c + 1] = acc;
   }
@@ -349,6 +365,59 @@ KFBI_DEV void post(const View<LOGN> &sm, int t, double2 (&out)[E]) {
   }
 #pragma unroll
   for (int c = 0; c < 8; ++c) out[2 * c + 1] = cadd(off, out[2 * c + 1]);
+}
+
+// Sum of v over the threads of the sequence, returned to every thread
+// (warp butterfly + the scan scratch; ends after a sequence barrier, with
+// the scratch free again after the next barrier).
+template <int LOGN>
+KFBI_DEV double2 seq_allreduce(const View<LOGN> &sm, int t, double2 v) {
+  constexpr int T = Cfg<LOGN>::T;
+  constexpr int W = T < 32 ? T : 32;
+#pragma unroll
+  for (int o = 1; o < W; o <<= 1) {
+    v.x += __shfl_xor_sync(0xffffffffu, v.x, o, W);
+    v.y += __shfl_xor_sync(0xffffffffu, v.y, o, W);
+  }
+  if constexpr (T > 32) {
+    constexpr int WPC = Cfg<LOGN>::CTA_T / 32;
+    const int warp = t >> 5;
+    const int lw0 = (threadIdx.x >> 5) - (warp % WPC);
+    if ((threadIdx.x & 31) == 0) sm.scr[warp / WPC][lw0 + warp % WPC] = v;
+    seq_sync<LOGN>();
+    v = make_double2(0.0, 0.0);
+    for (int w = 0; w < T / 32; ++w) v = cadd(v, sm.scr[w / WPC][lw0 + w % WPC]);
+    seq_sync<LOGN>();
+  }
+  return v;
+}
+
+// DCT-I pre-processing (NR cosft1 form) from a staged natural-order x_0..x_N
+// (x_N in sm.ext): y_j = (x_j + x_{N-j}) / 2 - sin(pi j / N) (x_j - x_{N-j}),
+// and C_1 = 2 [(x_0 - x_N) / 2 + sum_{n=1}^{N-1} x_n cos(pi n / N)] reduced
+// over the sequence (returned to every thread).  cos(pi n / N) comes from
+// the sine table: sin(pi (n + N/2) / N) for n < N/2, -sin(pi (n - N/2) / N).
+template <int LOGN>
+KFBI_DEV double2 pre_dct(double2 (&v)[E], const View<LOGN> &sm, int t,
+                         const double *__restrict__ sinv) {
+  constexpr int N = 1 << LOGN;
+  constexpr int T = Cfg<LOGN>::T;
+  const double2 xN = *sm.ext;
+  double2 seed = make_double2(0.0, 0.0);
+#pragma unroll
+  for (int m = 0; m < E; ++m) {
+    const int j = t + m * T;
+    const double2 xj = sm[j];
+    const double2 xr = j == 0 ? xN : sm[N - j];
+    const double s = __ldg(&sinv[j]);
+    const double2 a = cadd(xj, xr), d = csub(xj, xr);
+    v[m] = make_double2(fma(-s, d.x, 0.5 * a.x), fma(-s, d.y, 0.5 * a.y));
+    const double c = j == 0 ? 0.5 : (j < N / 2 ? __ldg(&sinv[j + N / 2]) : -__ldg(&sinv[j - N / 2]));
+    seed = make_double2(fma(c, xj.x, seed.x), fma(c, xj.y, seed.y));
+  }
+  if (t == 0) seed = make_double2(seed.x - 0.5 * xN.x, seed.y - 0.5 * xN.y);
+  seed = seq_allreduce<LOGN>(sm, t, seed);
+  return make_double2(2.0 * seed.x, 2.0 * seed.y);
 }
 
 }  // namespace reg

@@ -254,6 +254,10 @@ struct ExtractArgs {
   const double *ainv_rows;        // [n][3][6]
   const double *jcoef;            // [n][6][6]
   const double *normal;           // [n][2]
+  // OneSidedExtractor (bvp.py:115-228), Neumann BVPs; null -> six-point
+  const int *os_stencil;          // [n][7] interior nodes
+  const double *os_rows;          // [n][3][7] rows 0..2 of inv(A)
+  const unsigned char *os_fb;     // [n] 1: fall back to the six-point stencil
 };
 
 // (u+, ux+, uy+) at control point p (bvp.py:98-104).
@@ -287,13 +291,46 @@ KFBI_DEV void extract_point(const ExtractArgs &x, const T *__restrict__ u, const
   ty = rdiv(c[2], x.h);
 }
 
+// The extractor of the BVP kind: one-sided rows . u[7 nodes] (bvp.py:215-221)
+// with the straddling fallback (bvp.py:222-227: the fallback's gradient goes
+// through * h / h like the reference's coefficient array), or the six-point
+// straddling stencil.
+template <typename T>
+KFBI_DEV void extract_any(const ExtractArgs &x, const T *__restrict__ u, const T *__restrict__ jm,
+                          int p, T &tu, T &tx, T &ty) {
+  using S = Sc<T>;
+  if (x.os_stencil && !x.os_fb[p]) {
+    T v[7];
+#pragma unroll
+    for (int k = 0; k < 7; ++k) v[k] = u[x.os_stencil[7 * p + k]];
+    T c[3];
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+      const double *rr = x.os_rows + 21 * p + 7 * r;
+      T acc = S::rmul(v[0], rr[0]);
+#pragma unroll
+      for (int k = 1; k < 7; ++k) acc = S::add(acc, S::rmul(v[k], rr[k]));
+      c[r] = acc;
+    }
+    tu = c[0];
+    tx = rdiv(c[1], x.h);
+    ty = rdiv(c[2], x.h);
+    return;
+  }
+  extract_point<T>(x, u, jm, p, tu, tx, ty);
+  if (x.os_stencil) {
+    tx = rdiv(S::rmul(tx, x.h), x.h);
+    ty = rdiv(S::rmul(ty, x.h), x.h);
+  }
+}
+
 template <typename T>
 __global__ void __launch_bounds__(256)
 extract_kernel(ExtractArgs x, const T *__restrict__ u, const T *__restrict__ jm, T *out) {
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= x.n) return;
   T tu, tx, ty;
-  extract_point<T>(x, u, jm, p, tu, tx, ty);
+  extract_any<T>(x, u, jm, p, tu, tx, ty);
   out[p] = tu;
   out[x.n + p] = tx;
   out[2 * x.n + p] = ty;
@@ -345,7 +382,7 @@ extract_update_kernel(ExtractArgs x, const T *__restrict__ u, const T *__restric
   double mag = 0.0;
   if (p < x.n) {
     T tu, tx, ty;
-    extract_point<T>(x, u, jm, p, tu, tx, ty);
+    extract_any<T>(x, u, jm, p, tu, tx, ty);
     const double nx = x.normal[2 * p], ny = x.normal[2 * p + 1];
     T tun = S::add(S::rmul(tx, nx), S::rmul(ty, ny));
     T target = dirichlet ? tu : tun;
@@ -377,11 +414,18 @@ __global__ void unit_vector_kernel(T *v, int n, int p) {
     v[i] = (i == p) ? Sc<T>::one() : Sc<T>::zero();
 }
 
-// Column p of the trace operator, stored column-major: Tcm[p * n + q] = out[q].
+// Column p of the trace operator, stored column-major: Tcm[p * n + q] = the
+// target trace of an extraction out[3][n] = (u+, ux+, uy+): u+ (Dirichlet) or
+// d_n u+ = ux+ nx + uy+ ny (Neumann).
 template <typename T>
-__global__ void op_column_kernel(int n, int p, const T *out, T *Tcm) {
+__global__ void op_column_kernel(int n, int p, const T *out, const double *normal, int neumann,
+                                 T *Tcm) {
+  using S = Sc<T>;
   const int q = blockIdx.x * blockDim.x + threadIdx.x;
-  if (q < n) Tcm[(size_t)p * n + q] = out[q];
+  if (q >= n) return;
+  Tcm[(size_t)p * n + q] =
+      neumann ? S::add(S::rmul(out[n + q], normal[2 * q]), S::rmul(out[2 * n + q], normal[2 * q + 1]))
+              : out[q];
 }
 
 // All operator sweeps of one solve in ONE cooperative launch, with the trace
@@ -530,7 +574,7 @@ extract_traces_kernel(ExtractArgs x, const T *__restrict__ u, const T *__restric
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= x.n) return;
   T tu, tx, ty;
-  extract_point<T>(x, u, jm, p, tu, tx, ty);
+  extract_any<T>(x, u, jm, p, tu, tx, ty);
   trace_u[p] = tu;
   trace_un[p] = S::add(S::rmul(tx, x.normal[2 * p]), S::rmul(ty, x.normal[2 * p + 1]));
 }

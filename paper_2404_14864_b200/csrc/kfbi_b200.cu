@@ -16,6 +16,7 @@
 #include "../../include/kfbi_b200.h"
 #include "box_kernels.cuh"
 #include "box_reg.cuh"
+#include "box_neu.cuh"
 #include "interface_kernels.cuh"
 #include "stepping_kernels.cuh"
 
@@ -94,6 +95,11 @@ struct kfbi_plan {
   DevBuf<int> rec_edge, group_start, group_node, row_group, stencil;
   DevBuf<double> rec_d, rec_sigma, deriv_col, speed, tangent, normal, dtan_ds, inv3;
   DevBuf<double> ainv_rows, jcoef;
+  // OneSidedExtractor tables (Neumann BVPs)
+  bool has_os = false;
+  DevBuf<int> os_stencil;
+  DevBuf<double> os_rows;
+  DevBuf<unsigned char> os_fb;
   // per-sweep scratch (sized for c128)
   DevBuf<double2> d1, psi_s, jm, jv;
   DevBuf<double> history;
@@ -106,6 +112,7 @@ struct kfbi_plan {
   int log_cap = 0;
   bool op_valid = false;
   int op_dtype = -1;
+  int op_bc = -1;                   // bc_kind the operator was built for
   double op_kre = 0.0, op_kim = 0.0;
   DevBuf<unsigned long long> red;   // reduction slots
   RichState *st_host = nullptr;     // pinned mirror
@@ -244,7 +251,7 @@ CtlGeom ctl_geom(kfbi_plan *p) {
   return g;
 }
 
-ExtractArgs extract_args(kfbi_plan *p) {
+ExtractArgs extract_args(kfbi_plan *p, bool onesided = false) {
   ExtractArgs x;
   x.n = p->n_ctl;
   x.m = p->m;
@@ -254,6 +261,9 @@ ExtractArgs extract_args(kfbi_plan *p) {
   x.ainv_rows = p->ainv_rows.p;
   x.jcoef = p->jcoef.p;
   x.normal = p->normal.p;
+  x.os_stencil = onesided ? p->os_stencil.p : nullptr;
+  x.os_rows = onesided ? p->os_rows.p : nullptr;
+  x.os_fb = onesided ? p->os_fb.p : nullptr;
   return x;
 }
 
@@ -366,11 +376,65 @@ kfbi_status slab_pass(kfbi_plan *p, int32_t dtype, const kfbi_slab *sl, int pass
   return box_passes_reg<false>(p, a, rhs, sign, c, u, s, passes);
 }
 
+// neumann-zero closure: DCT-I passes (box_neu.cuh), one GPU
+template <bool CPLX, int LOGN>
+kfbi_status box_neu_launch(kfbi_plan *p, const BoxArgs &a, const void *rhs, double sign,
+                           const CorrArgs<typename std::conditional<CPLX, double2, double>::type> &c,
+                           void *u, cudaStream_t s) {
+  using Cf = reg::Cfg<LOGN>;
+  static bool attr = false;
+  if (!attr) {
+    const int bytes = (int)reg::smem_bytes<LOGN>();
+    KFBI_CUDA(cudaFuncSetAttribute(rows_fwd_neu<CPLX, LOGN>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, bytes), "transform-rows");
+    KFBI_CUDA(cudaFuncSetAttribute(rows_inv_neu<CPLX, LOGN>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, bytes), "transform-rows");
+    KFBI_CUDA(cudaFuncSetAttribute(cols_neu<CPLX, LOGN>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, bytes), "transform-cols");
+    attr = true;
+  }
+  const int M = Cf::N;
+  const int nrow = CPLX ? M + 1 : M / 2 + 1;
+  const int ncol = 2 * (CPLX ? M / 2 + 1 : M / 4 + 1);
+  const int grow = Cf::CL > 1 ? nrow * Cf::CL : (nrow + Cf::S - 1) / Cf::S;
+  const int gcol = Cf::CL > 1 ? ncol * Cf::CL : (ncol + Cf::S - 1) / Cf::S;
+  using CT = typename std::conditional<CPLX, double2, double>::type;
+  KFBI_TRY(launch(p, KFBI_K_ROWS, s, [&] {
+    return reg_launch<LOGN>(rows_fwd_neu<CPLX, LOGN>, grow, s, a, rhs, sign, CorrArgs<CT>(c));
+  }));
+  KFBI_TRY(launch(p, KFBI_K_COLS, s, [&] { return reg_launch<LOGN>(cols_neu<CPLX, LOGN>, gcol, s, a); }));
+  return launch(p, KFBI_K_ROWS, s, [&] { return reg_launch<LOGN>(rows_inv_neu<CPLX, LOGN>, grow, s, a, u); });
+}
+
+template <bool CPLX>
+kfbi_status box_neu_passes(kfbi_plan *p, double kre, double kim, const void *rhs, double sign,
+                           const void *jv, void *u, const int *done, cudaStream_t s) {
+  using T = typename std::conditional<CPLX, double2, double>::type;
+  if (kre == 0.0 && kim == 0.0)
+    return fail(KFBI_E_CONFIG, "neumann-zero box with kappa = 0 is singular (constant null mode)");
+  BoxArgs a = box_args(p, kre, kim, done);
+  CorrArgs<T> c = corr_args<T>(p, static_cast<const T *>(jv));
+  if (!jv) c.jv = nullptr;
+  switch (p->logm) {
+#define KFBI_CASE(L) \
+    case L: return box_neu_launch<CPLX, L>(p, a, rhs, sign, c, u, s);
+    KFBI_CASE(4) KFBI_CASE(5) KFBI_CASE(6) KFBI_CASE(7) KFBI_CASE(8) KFBI_CASE(9)
+    KFBI_CASE(10) KFBI_CASE(11) KFBI_CASE(12) KFBI_CASE(13) KFBI_CASE(14)
+#undef KFBI_CASE
+    default: return fail(KFBI_E_CONFIG, "DCT-I engine: unsupported M");
+  }
+}
+
 kfbi_status box_dispatch(kfbi_plan *p, int dtype, double kre, double kim, const void *rhs,
                          double sign, const void *jv, void *u, const int *done,
-                         cudaStream_t s) {
+                         cudaStream_t s, int box_bc = KFBI_DIRICHLET_ZERO) {
+  if (dtype != KFBI_C128 && kim != 0.0) return fail(KFBI_E_CONFIG, "complex kappa requires the c128 path");
+  if (box_bc == KFBI_NEUMANN_ZERO) {
+    if (dtype == KFBI_C128) return box_neu_passes<true>(p, kre, kim, rhs, sign, jv, u, done, s);
+    return box_neu_passes<false>(p, kre, kim, rhs, sign, jv, u, done, s);
+  }
+  if (box_bc != KFBI_DIRICHLET_ZERO) return fail(KFBI_E_CONFIG, "unknown box boundary condition");
   if (dtype == KFBI_C128) return box_passes<true>(p, kre, kim, rhs, sign, jv, u, done, s);
-  if (kim != 0.0) return fail(KFBI_E_CONFIG, "complex kappa requires the c128 path");
   return box_passes<false>(p, kre, kim, rhs, sign, jv, u, done, s);
 }
 
@@ -454,19 +518,20 @@ bool aligned16(std::initializer_list<const void *> ptrs) {
 template <typename T>
 kfbi_status sweep(kfbi_plan *p, const kfbi_bvp *b, cudaStream_t s) {
   const int *done = &p->st.p->done;
-  const bool cplx = std::is_same<T, double2>::value;
-  KFBI_TRY(jumps_T<T>(p, b->kappa_re, b->kappa_im, b->density, nullptr, b->f_gamma,
-                      b->f_gamma_sign, p->jm.p, done, s));
+  const bool dir = b->bc_kind == 0;
+  // Dirichlet: density = phi = [u]; Neumann: density = psi = [u_n] (bvp.py:313-317)
+  KFBI_TRY(jumps_T<T>(p, b->kappa_re, b->kappa_im, dir ? b->density : nullptr,
+                      dir ? nullptr : b->density, b->f_gamma, b->f_gamma_sign, p->jm.p, done, s));
   KFBI_TRY(edges_T<T>(p, p->jm.p, p->jv.p, done, s));
-  if (cplx) KFBI_TRY(box_passes<true>(p, b->kappa_re, b->kappa_im, b->F, b->F_sign, p->jv.p, b->u, done, s));
-  else KFBI_TRY(box_passes<false>(p, b->kappa_re, b->kappa_im, b->F, b->F_sign, p->jv.p, b->u, done, s));
-  ExtractArgs x = extract_args(p);
+  KFBI_TRY(box_dispatch(p, std::is_same<T, double2>::value ? KFBI_C128 : KFBI_F64, b->kappa_re,
+                        b->kappa_im, b->F, b->F_sign, p->jv.p, b->u, done, s, b->box_bc));
+  ExtractArgs x = extract_args(p, !dir);
   const int blocks = (p->n_ctl + 255) / 256;
   return launch(p, KFBI_K_DENSITY, s, [&] {
     extract_update_kernel<T><<<blocks, 256, 0, s>>>(
         x, static_cast<const T *>(b->u), reinterpret_cast<const T *>(p->jm.p),
         static_cast<const T *>(b->g), static_cast<T *>(b->density), static_cast<T *>(b->trace_u),
-        static_cast<T *>(b->trace_un), b->gamma, 1, p->st.p, p->history.p);
+        static_cast<T *>(b->trace_un), b->gamma, dir ? 1 : 0, p->st.p, p->history.p);
   });
 }
 
@@ -491,7 +556,8 @@ kfbi_status ensure_async_scratch(kfbi_plan *p) {
 
 // Column p of T = trace of the pipeline applied to e_p with F = 0, f_gamma = 0.
 template <typename T>
-kfbi_status build_operator_T(kfbi_plan *p, double kre, double kim, cudaStream_t s) {
+kfbi_status build_operator_T(kfbi_plan *p, double kre, double kim, int bc_kind, int box_bc,
+                             cudaStream_t s) {
   constexpr bool CPLX = std::is_same<T, double2>::value;
   const int n = p->n_ctl;
   const size_t nf = (size_t)(p->m + 1) * (p->m + 1);
@@ -503,23 +569,29 @@ kfbi_status build_operator_T(kfbi_plan *p, double kre, double kim, cudaStream_t 
   T *z = reinterpret_cast<T *>(p->zvec.p), *ev = reinterpret_cast<T *>(p->evec.p);
   T *out = reinterpret_cast<T *>(p->out3.p), *Top = reinterpret_cast<T *>(p->Top.p);
   KFBI_CUDA(cudaMemsetAsync(z, 0, n * sizeof(T), s), "jumps-and-corrections");
-  ExtractArgs x = extract_args(p);
+  const bool dir = bc_kind == 0;
+  ExtractArgs x = extract_args(p, !dir);
   const int eb = (n + 255) / 256;
   const bool timing = p->timing;
   p->timing = false;
   kfbi_status st = KFBI_OK;
   for (int col = 0; col < n && st == KFBI_OK; ++col) {
     st = launch(p, KFBI_K_JUMPS, s, [&] { unit_vector_kernel<T><<<eb, 256, 0, s>>>(ev, n, col); });
-    if (st == KFBI_OK) st = jumps_T<T>(p, kre, kim, ev, nullptr, z, 1.0, p->jm.p, nullptr, s);
+    if (st == KFBI_OK)
+      st = jumps_T<T>(p, kre, kim, dir ? ev : nullptr, dir ? nullptr : ev, z, 1.0, p->jm.p, nullptr, s);
     if (st == KFBI_OK) st = edges_T<T>(p, p->jm.p, p->jv.p, nullptr, s);
-    if (st == KFBI_OK) st = box_passes<CPLX>(p, kre, kim, nullptr, 1.0, p->jv.p, p->ufield.p, nullptr, s);
+    if (st == KFBI_OK)
+      st = box_dispatch(p, CPLX ? KFBI_C128 : KFBI_F64, kre, kim, nullptr, 1.0, p->jv.p, p->ufield.p,
+                        nullptr, s, box_bc);
     if (st == KFBI_OK)
       st = launch(p, KFBI_K_EXTRACT, s, [&] {
         extract_kernel<T><<<eb, 256, 0, s>>>(x, reinterpret_cast<const T *>(p->ufield.p),
                                              reinterpret_cast<const T *>(p->jm.p), out);
       });
     if (st == KFBI_OK)
-      st = launch(p, KFBI_K_EXTRACT, s, [&] { op_column_kernel<T><<<eb, 256, 0, s>>>(n, col, out, Top); });
+      st = launch(p, KFBI_K_EXTRACT, s, [&] {
+        op_column_kernel<T><<<eb, 256, 0, s>>>(n, col, out, p->normal.p, dir ? 0 : 1, Top);
+      });
   }
   p->timing = timing;
   KFBI_TRY(st);
@@ -528,6 +600,7 @@ kfbi_status build_operator_T(kfbi_plan *p, double kre, double kim, cudaStream_t 
   p->op_dtype = CPLX ? KFBI_C128 : KFBI_F64;
   p->op_kre = kre;
   p->op_kim = kim;
+  p->op_bc = bc_kind * 2 + box_bc;
   return KFBI_OK;
 }
 
@@ -586,11 +659,13 @@ kfbi_status final_pipeline(kfbi_plan *p, const kfbi_bvp *b, const void *phi_befo
                            const int *skip = nullptr) {
   constexpr bool CPLX = std::is_same<T, double2>::value;
   const int n = p->n_ctl;
-  KFBI_TRY(jumps_T<T>(p, b->kappa_re, b->kappa_im, phi_before, nullptr, b->f_gamma,
-                      b->f_gamma_sign, p->jm.p, skip, s));
+  const bool dir = b->bc_kind == 0;
+  KFBI_TRY(jumps_T<T>(p, b->kappa_re, b->kappa_im, dir ? phi_before : nullptr,
+                      dir ? nullptr : phi_before, b->f_gamma, b->f_gamma_sign, p->jm.p, skip, s));
   KFBI_TRY(edges_T<T>(p, p->jm.p, p->jv.p, skip, s));
-  KFBI_TRY(box_passes<CPLX>(p, b->kappa_re, b->kappa_im, b->F, b->F_sign, p->jv.p, b->u, skip, s));
-  ExtractArgs x = extract_args(p);
+  KFBI_TRY(box_dispatch(p, CPLX ? KFBI_C128 : KFBI_F64, b->kappa_re, b->kappa_im, b->F, b->F_sign,
+                        p->jv.p, b->u, skip, s, b->box_bc));
+  ExtractArgs x = extract_args(p, !dir);
   return launch(p, KFBI_K_EXTRACT, s, [&] {
     extract_traces_kernel<T><<<(n + 255) / 256, 256, 0, s>>>(
         x, static_cast<const T *>(b->u), reinterpret_cast<const T *>(p->jm.p),
@@ -625,7 +700,7 @@ kfbi_status kfbi_plan_create(const kfbi_grid_desc *desc, kfbi_plan **out) {
   // lambda_p exactly as boxsolve.py:43 evaluates it in double:
   // (2 cos(p pi / m) - 2) / h^2
   std::vector<double> lam(m + 1, 0.0);
-  for (int q = 1; q < m; ++q) {
+  for (int q = 1; q <= m; ++q) {      // p = m only for the neumann-zero closure
     double ang = (double)q * M_PI / (double)m;
     lam[q] = (2.0 * std::cos(ang) - 2.0) / (desc->h * desc->h);
   }
@@ -640,12 +715,12 @@ kfbi_status kfbi_plan_create(const kfbi_grid_desc *desc, kfbi_plan **out) {
   if ((e = upload(p->twg, twg.data(), twg.size())) != cudaSuccess ||
       (e = upload(p->sinv, sinv.data(), sinv.size())) != cudaSuccess ||
       (e = upload(p->lam, lam.data(), lam.size())) != cudaSuccess ||
-      (e = p->panels.ensure((size_t)m * m)) != cudaSuccess ||
+      (e = p->panels.ensure((size_t)(m + 2) * (m + 2))) != cudaSuccess ||
       (e = p->st.ensure(1)) != cudaSuccess || (e = p->red.ensure(8)) != cudaSuccess) {
     kfbi_plan_destroy(p);
     return fail(KFBI_E_CUDA, std::string("plan allocation: ") + cudaGetErrorString(e));
   }
-  cudaMemset(p->panels.p, 0, (size_t)m * m * sizeof(double2));
+  cudaMemset(p->panels.p, 0, (size_t)(m + 2) * (m + 2) * sizeof(double2));
   cudaMallocHost(&p->st_host, sizeof(RichState));
   cudaMallocHost(&p->red_host, 4 * sizeof(unsigned long long));
   *out = p;
@@ -689,7 +764,7 @@ kfbi_status kfbi_plan_destroy(kfbi_plan *p) {
   p->group_node.release(); p->row_group.release(); p->stencil.release(); p->rec_d.release();
   p->rec_sigma.release(); p->deriv_col.release(); p->speed.release(); p->tangent.release();
   p->normal.release(); p->dtan_ds.release(); p->inv3.release(); p->ainv_rows.release();
-  p->jcoef.release(); p->d1.release(); p->psi_s.release(); p->jm.release(); p->jv.release();
+  p->jcoef.release(); p->os_stencil.release(); p->os_rows.release(); p->os_fb.release(); p->d1.release(); p->psi_s.release(); p->jm.release(); p->jv.release();
   p->history.release(); p->st.release(); p->red.release();
   p->Top.release(); p->phi0.release(); p->phi_prev.release(); p->trace1.release();
   p->trace_tmp.release(); p->zvec.release(); p->evec.release(); p->out3.release();
@@ -823,10 +898,16 @@ kfbi_status kfbi_richardson(kfbi_plan *p, const kfbi_bvp *b, kfbi_bvp_result *re
   if (!cplx && b->kappa_im != 0.0) return fail(KFBI_E_CONFIG, "complex kappa requires the c128 path");
   cudaError_t e = p->history.ensure(b->max_iter);
   if (e != cudaSuccess) return fail(KFBI_E_CUDA, "history allocation failed");
+  if (b->bc_kind != 0 && b->bc_kind != 1) return fail(KFBI_E_CONFIG, "unknown boundary condition kind");
+  if (b->box_bc != KFBI_DIRICHLET_ZERO && b->box_bc != KFBI_NEUMANN_ZERO)
+    return fail(KFBI_E_CONFIG, "unknown box boundary condition");
+  if (b->bc_kind == 1 && !p->has_os)
+    return fail(KFBI_E_CONFIG, "Neumann BVP: one-sided extraction tables missing (kfbi_plan_set_onesided)");
   const bool use_op = b->use_operator != 0;
   const size_t es = cplx ? sizeof(double2) : sizeof(double);
   if (use_op) {
-    if (!p->op_valid || p->op_dtype != b->dtype || p->op_kre != b->kappa_re || p->op_kim != b->kappa_im)
+    if (!p->op_valid || p->op_dtype != b->dtype || p->op_kre != b->kappa_re || p->op_kim != b->kappa_im ||
+        p->op_bc != b->bc_kind * 2 + b->box_bc)
       return fail(KFBI_E_CONFIG, "trace operator not built for this kappa / dtype (kfbi_build_trace_operator)");
     KFBI_TRY(ensure_op_scratch(p));
   }
@@ -841,7 +922,7 @@ kfbi_status kfbi_richardson(kfbi_plan *p, const kfbi_bvp *b, kfbi_bvp_result *re
     KFBI_TRY(ensure_async_scratch(p));
     if (cplx) KFBI_TRY(sweep<double2>(p, b, s));
     else KFBI_TRY(sweep<double>(p, b, s));
-    KFBI_CUDA(cudaMemcpyAsync(p->trace1.p, b->trace_u, p->n_ctl * es, cudaMemcpyDeviceToDevice, s),
+    KFBI_CUDA(cudaMemcpyAsync(p->trace1.p, b->bc_kind ? b->trace_un : b->trace_u, p->n_ctl * es, cudaMemcpyDeviceToDevice, s),
               "density-update");
     if (b->max_iter > 1) {
       if (cplx) KFBI_TRY(op_solve<double2>(p, b, s));
@@ -874,7 +955,7 @@ kfbi_status kfbi_richardson(kfbi_plan *p, const kfbi_bvp *b, kfbi_bvp_result *re
     // cooperative launch; a single host sync per solve
     if (cplx) KFBI_TRY(sweep<double2>(p, b, s));
     else KFBI_TRY(sweep<double>(p, b, s));
-    KFBI_CUDA(cudaMemcpyAsync(p->trace1.p, b->trace_u, p->n_ctl * es, cudaMemcpyDeviceToDevice, s),
+    KFBI_CUDA(cudaMemcpyAsync(p->trace1.p, b->bc_kind ? b->trace_un : b->trace_u, p->n_ctl * es, cudaMemcpyDeviceToDevice, s),
               "density-update");
     if (b->max_iter > 1) {
       if (cplx) KFBI_TRY(op_solve<double2>(p, b, s));
@@ -932,12 +1013,69 @@ kfbi_status kfbi_richardson(kfbi_plan *p, const kfbi_bvp *b, kfbi_bvp_result *re
   return KFBI_OK;
 }
 
+kfbi_status kfbi_build_trace_operator_bc(kfbi_plan *p, int32_t dtype, int32_t bc_kind, int32_t box_bc,
+                                         double kre, double kim, void *stream) {
+  KFBI_TRY(check_geo(p));
+  if (bc_kind == 1 && !p->has_os)
+    return fail(KFBI_E_CONFIG, "Neumann operator: one-sided extraction tables missing");
+  cudaStream_t s = (cudaStream_t)stream;
+  if (dtype == KFBI_C128) return build_operator_T<double2>(p, kre, kim, bc_kind, box_bc, s);
+  if (kim != 0.0) return fail(KFBI_E_CONFIG, "complex kappa requires the c128 path");
+  return build_operator_T<double>(p, kre, kim, bc_kind, box_bc, s);
+}
+
 kfbi_status kfbi_build_trace_operator(kfbi_plan *p, int32_t dtype, double kre, double kim, void *stream) {
+  return kfbi_build_trace_operator_bc(p, dtype, 0, KFBI_DIRICHLET_ZERO, kre, kim, stream);
+}
+
+kfbi_status kfbi_box_solve_bc(kfbi_plan *p, int32_t dtype, int32_t box_bc, double kre, double kim,
+                              const void *rhs, void *u, void *stream) {
+  KFBI_TRY(check_plan(p));
+  if (!rhs || !u) return fail(KFBI_E_CONFIG, "null field pointer");
+  return box_dispatch(p, dtype, kre, kim, rhs, 1.0, nullptr, u, nullptr, (cudaStream_t)stream, box_bc);
+}
+
+kfbi_status kfbi_interface_solve_bc(kfbi_plan *p, int32_t dtype, int32_t box_bc, double kre, double kim,
+                                    const void *F, const void *jm, void *u, void *stream) {
   KFBI_TRY(check_geo(p));
   cudaStream_t s = (cudaStream_t)stream;
-  if (dtype == KFBI_C128) return build_operator_T<double2>(p, kre, kim, s);
-  if (kim != 0.0) return fail(KFBI_E_CONFIG, "complex kappa requires the c128 path");
-  return build_operator_T<double>(p, kre, kim, s);
+  if (dtype == KFBI_C128) KFBI_TRY(edges_T<double2>(p, jm, p->jv.p, nullptr, s));
+  else KFBI_TRY(edges_T<double>(p, jm, p->jv.p, nullptr, s));
+  return box_dispatch(p, dtype, kre, kim, F, 1.0, p->jv.p, u, nullptr, s, box_bc);
+}
+
+kfbi_status kfbi_plan_set_onesided(kfbi_plan *p, int32_t n_ctl, const int32_t *stencil7,
+                                   const double *rows, const uint8_t *fallback) {
+  KFBI_TRY(check_geo(p));
+  if (n_ctl != p->n_ctl || !stencil7 || !rows || !fallback)
+    return fail(KFBI_E_CONFIG, "one-sided tables: bad argument");
+  cudaError_t e;
+  if ((e = upload(p->os_stencil, stencil7, (size_t)7 * n_ctl)) != cudaSuccess ||
+      (e = upload(p->os_rows, rows, (size_t)21 * n_ctl)) != cudaSuccess ||
+      (e = upload(p->os_fb, fallback, (size_t)n_ctl)) != cudaSuccess)
+    return fail(KFBI_E_CUDA, std::string("one-sided tables: ") + cudaGetErrorString(e));
+  p->has_os = true;
+  return KFBI_OK;
+}
+
+kfbi_status kfbi_extract_onesided(kfbi_plan *p, int32_t dtype, const void *u, const void *jm, void *out,
+                                  void *stream) {
+  KFBI_TRY(check_geo(p));
+  if (!p->has_os) return fail(KFBI_E_CONFIG, "one-sided extraction tables missing");
+  cudaStream_t s = (cudaStream_t)stream;
+  ExtractArgs x = extract_args(p, true);
+  const int blocks = (p->n_ctl + 255) / 256;
+  if (dtype == KFBI_C128)
+    return launch(p, KFBI_K_EXTRACT, s, [&] {
+      extract_kernel<double2><<<blocks, 256, 0, s>>>(x, static_cast<const double2 *>(u),
+                                                     static_cast<const double2 *>(jm),
+                                                     static_cast<double2 *>(out));
+    });
+  return launch(p, KFBI_K_EXTRACT, s, [&] {
+    extract_kernel<double><<<blocks, 256, 0, s>>>(x, static_cast<const double *>(u),
+                                                  static_cast<const double *>(jm),
+                                                  static_cast<double *>(out));
+  });
 }
 
 kfbi_status kfbi_log_reserve(kfbi_plan *p, int32_t count) {

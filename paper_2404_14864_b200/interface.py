@@ -171,6 +171,7 @@ class InterfaceWorkspace:
         self._box_solvers = {}
         self._plan = None
         self._trace = None
+        self._onesided = None
         self._trace_error = None
 
     # -- host views kept for API compatibility --------------------------------
@@ -248,12 +249,33 @@ class InterfaceWorkspace:
             self._plan = plan
         return self._plan
 
-    def ensure_operator(self, kappa, cplx):
-        """Build (once per kappa) the explicit trace operator used by the
-        operator form of the Richardson sweeps."""
-        key = (complex(kappa), bool(cplx))
+    def ensure_operator(self, kappa, cplx, bc_kind="dirichlet", box_bc=None):
+        """Build (once per kappa and BVP kind) the explicit trace operator used
+        by the operator form of the Richardson sweeps."""
+        box_bc = box_bc or ("dirichlet-zero" if bc_kind == "dirichlet" else "neumann-zero")
+        if bc_kind == "neumann":
+            self.ensure_onesided()
+        key = (complex(kappa), bool(cplx), bc_kind, box_bc)
         if getattr(self.plan, "operator_key", None) != key:
-            self.plan.build_operator(kappa, cplx)
+            self.plan.build_operator(kappa, cplx, bc_kind, box_bc)
+
+    def onesided(self):
+        """The OneSidedExtractor of this workspace (host tables, built once)."""
+        if self._onesided is None:
+            from .bvp import OneSidedExtractor
+
+            self._onesided = OneSidedExtractor(self)
+        return self._onesided
+
+    def ensure_onesided(self):
+        """Upload the one-sided extraction tables to the plan (Neumann BVPs)."""
+        if not getattr(self.plan, "has_onesided", False):
+            ex = self.onesided()
+            fb = np.zeros(self.cps.m, np.uint8)
+            fb[ex._fallback] = 1
+            if len(ex._fallback):
+                self.trace_tables()         # the fallback points use the 6-point tables
+            self.plan.set_onesided(ex.stencil_flat, ex._rows, fb)
 
     def box_solver(self, kappa, bc):
         key = (complex(kappa), bc)
@@ -349,8 +371,8 @@ def solve_interface(data, workspace, box_bc, backend=None):
 
     if box_bc not in BOX_BCS:
         raise ConfigError(f"unknown box boundary condition {box_bc!r}; expected one of {BOX_BCS}")
-    if box_bc != "dirichlet-zero":
-        raise ConfigError("the neumann-zero box closure is not available in this build")
+    if box_bc == "neumann-zero" and complex(data.kappa) == 0:
+        raise ConfigError("neumann-zero box with κ = 0 is singular (constant null mode)")
     ws = workspace
     jm, cplx = _jumps_device(data, ws)
     cplx = cplx or np.iscomplexobj(np.asarray(data.F))
@@ -360,5 +382,5 @@ def solve_interface(data, workspace, box_bc, backend=None):
     m = ws.grid.m
     F = _dev(ws, data.F, dt)
     u = torch.empty_like(F)
-    ws.plan.interface_solve(data.kappa, F, jm, u)
+    ws.plan.interface_solve(data.kappa, F, jm, u, box_bc)
     return u.cpu().numpy().reshape(m + 1, m + 1)

@@ -114,7 +114,7 @@ def oracle_spec(kw):
     from oracle import kfbi_oracle as O
 
     keys = ("equation", "g", "u0", "lap_u0", "tau", "t_final", "c", "theta", "w", "potential",
-            "splitting", "v0", "lap_v0")
+            "splitting", "v0", "lap_v0", "bc_kind")
     return O.Spec(**{k: kw[k] for k in keys if k in kw})
 
 
@@ -123,3 +123,32 @@ def rel_linf(a, b):
     b = np.asarray(b)
     scale = np.max(np.abs(b))
     return float(np.max(np.abs(a - b)) / (scale if scale > 0 else 1.0))
+
+
+def neumann_run_cases():
+    """Neumann full-run golden cases (make_golden.gen_neumann)."""
+    import paper_2404_14864_b200 as k
+
+    heat = k.HeatPlaneDecay(c=1.0)
+    wave = k.WaveStanding(phase=0.0)
+    return {
+        "heat_flower64": (BOX, 64, k.StarCurve(1.0, c=0.2, lobes=5), dict(
+            equation="heat", bc_kind="neumann", g=heat.neumann, u0=heat.u0,
+            lap_u0=heat.lap_u0, tau=0.25, t_final=1.0, c=1.0)),
+        "wave_ellipse64": (BOX, 64, k.EllipseCurve(1.2, 0.8), dict(
+            equation="wave", bc_kind="neumann", g=wave.neumann, u0=wave.u0,
+            lap_u0=wave.lap_u0, v0=wave.v0, lap_v0=wave.lap_v0, tau=0.25,
+            t_final=1.0, theta=0.25)),
+    }
+
+
+NEUMANN_RICH_CASES = {
+    "disc64_k16": (BOX, 64, "disc", 16.0),
+    "flower128_k200": (BOX, 128, "flower8", 200.0),
+}
+
+
+def curve_of(tag):
+    import paper_2404_14864_b200 as k
+
+    return {"disc": k.CircleCurve(1.0), "flower8": k.StarCurve(1.0, c=0.2, lobes=8)}[tag]

@@ -9,7 +9,7 @@ which is not installed here, so a two-function stub is placed in
 The GPU box has no ``/root/reference``: tests only ever read the committed
 ``.npz`` files, never the reference itself.  Re-run with
 
-    python tests/golden/make_golden.py
+    python tests/golden/make_golden.py [name ...]   (default: all files)
 
 Inputs that are large (random right-hand sides) are regenerated in the tests
 from the same ``np.random.default_rng(seed)`` streams instead of being stored.
@@ -267,14 +267,83 @@ def gen_nonlinear(k):
             "out_w3": nonlinear_phase_step(u, v, 3.0, 0.25)}
 
 
+def gen_neumann(k):
+    """Neumann path: neumann-zero interface solves + one-sided extraction,
+    Neumann Richardson solves, Neumann heat / wave runs."""
+    out = {}
+    pf = k.PiecewiseField(kappa=2.0)
+    for name in ("flower128", "ellipse128"):
+        box, m, curve = setup_cases(k)[name]
+        geo = k.build_grid(box, m, curve)
+        ws = k.InterfaceWorkspace(geo)
+        cps = ws.cps
+        X, Y = geo.grid.X, geo.grid.Y
+        interior = geo.classification.interior
+        data = k.InterfaceData(kappa=2.0, F=np.where(interior, pf.f_jump(X, Y), 0.0),
+                               phi=np.zeros(cps.m), psi=pf.psi(cps.x, cps.y, cps.normal),
+                               f_gamma=pf.f_jump(cps.x, cps.y))
+        js = k.compute_jumps(data, ws)
+        u = k.solve_interface(data, ws, box_bc="neumann-zero")
+        tu, tx, ty = k.OneSidedExtractor(ws).extract(u, js)
+        p = f"{name}__"
+        out[p + "u"] = u
+        out[p + "trace"] = np.stack([tu, tx, ty])
+    cases = {
+        "disc64_k16": (BOX, 64, k.CircleCurve(1.0), 16.0),
+        "flower128_k200": (BOX, 128, k.StarCurve(1.0, c=0.2, lobes=8), 200.0),
+    }
+    for name, (box, m, curve, kappa) in cases.items():
+        geo = k.build_grid(box, m, curve)
+        ws = k.InterfaceWorkspace(geo)
+        cps = ws.cps
+        X, Y = geo.grid.X, geo.grid.Y
+        interior = geo.classification.interior
+        sol = k.StaticPlaneWave(kappa=kappa)
+        F = np.where(interior, sol.f(X, Y), 0.0)
+        prob = k.BvpProblem(kappa=kappa, F=F, f_gamma=sol.f(cps.x, cps.y), bc_kind="neumann",
+                            bc_values=sol.neumann(cps.x, cps.y, cps.normal))
+        s = k.richardson_solve(prob, ws)
+        p = f"rich_{name}__"
+        out[p + "u"] = s.u
+        out[p + "density"] = s.density
+        out[p + "trace_u"] = s.trace_u
+        out[p + "trace_un"] = s.trace_un
+        out[p + "iterations"] = np.array(s.iterations)
+        out[p + "history"] = np.array(s.residual_history)
+    heat = k.HeatPlaneDecay(c=1.0)
+    wave = k.WaveStanding(phase=0.0)
+    runs = {
+        "heat_flower64": (BOX, 64, k.StarCurve(1.0, c=0.2, lobes=5), dict(
+            equation="heat", bc_kind="neumann", g=heat.neumann, u0=heat.u0,
+            lap_u0=heat.lap_u0, tau=0.25, t_final=1.0, c=1.0)),
+        "wave_ellipse64": (BOX, 64, k.EllipseCurve(1.2, 0.8), dict(
+            equation="wave", bc_kind="neumann", g=wave.neumann, u0=wave.u0,
+            lap_u0=wave.lap_u0, v0=wave.v0, lap_v0=wave.lap_v0, tau=0.25,
+            t_final=1.0, theta=0.25)),
+    }
+    for name, (box, m, curve, kw) in runs.items():
+        geo = k.build_grid(box, m, curve)
+        res = k.run(k.ProblemSpec(**kw), geo)
+        p = f"run_{name}__"
+        out[p + "u"] = res.state.u
+        out[p + "density"] = res.state.density
+        out[p + "iterations"] = np.array(res.iterations)
+        print(name, "iterations", res.iterations)
+    return out
+
+
 def main():
     k = load_reference()
     import scipy
 
     stamp = np.array(f"kfbi {k.__version__}; numpy {np.__version__}; scipy {scipy.__version__}")
-    for fname, gen in (("setup", gen_setup), ("box", gen_box), ("interface", gen_interface),
-                       ("richardson", gen_richardson), ("runs", gen_runs),
-                       ("nonlinear", gen_nonlinear)):
+    gens = (("setup", gen_setup), ("box", gen_box), ("interface", gen_interface),
+            ("richardson", gen_richardson), ("runs", gen_runs),
+            ("nonlinear", gen_nonlinear), ("neumann", gen_neumann))
+    only = set(sys.argv[1:])
+    for fname, gen in gens:
+        if only and fname not in only:
+            continue
         data = gen(k)
         data["stamp"] = stamp
         path = os.path.join(HERE, f"{fname}.npz")

@@ -9,7 +9,8 @@ import numpy as np
 import pytest
 
 import paper_2404_14864_b200 as k
-from conftest import BOX, BOX_CASES, box_rhs, golden, oracle_spec, rel_linf, run_cases, setup_cases
+from conftest import (BOX, BOX_CASES, NEUMANN_RICH_CASES, box_rhs, curve_of, golden,
+                      neumann_run_cases, oracle_spec, rel_linf, run_cases, setup_cases)
 from oracle import kfbi_oracle as O
 
 
@@ -19,12 +20,11 @@ def _tables(name):
     return ws, O.tables_from_workspace(ws)
 
 
-@pytest.mark.parametrize("case", [c for c in BOX_CASES if c[3] == "dirichlet-zero"],
-                         ids=lambda c: c[0])
+@pytest.mark.parametrize("case", BOX_CASES, ids=lambda c: c[0])
 def test_box_solve_matches_reference(case):
     tag, m, kappa, bc, seed, cplx = case
     grid = k.CartesianGrid(BOX, m)
-    u = O.box_solve(m, grid.h, kappa, box_rhs(m, seed, cplx))
+    u = O.box_solve(m, grid.h, kappa, box_rhs(m, seed, cplx), bc=bc)
     assert np.array_equal(u, golden("box")[tag + "__u"])
 
 
@@ -102,3 +102,54 @@ def test_oracle_residual_oracle():
     u = O.box_solve(32, grid.h, 3.7, rhs)
     r = k.apply_box_operator(grid, u, 3.7, "dirichlet-zero") - rhs
     assert np.max(np.abs(r[1:-1, 1:-1])) / np.max(np.abs(rhs)) < 1e-11
+
+
+# ---------------------------------------------------------------------------
+# Neumann path (neumann-zero box, one-sided extraction, psi iteration)
+
+@pytest.mark.parametrize("name", ["flower128", "ellipse128"])
+def test_neumann_interface_and_onesided_match_reference(name):
+    box, m, curve = setup_cases()[name]
+    ws = k.InterfaceWorkspace(k.build_grid(box, m, curve))
+    t = O.tables_from_workspace(ws, onesided=True)
+    g = golden("neumann")
+    pf = k.PiecewiseField(kappa=2.0)
+    cps = ws.cps
+    interior = ws.geometry.classification.interior
+    jm = O.jumps(t, 2.0, np.zeros(cps.m), pf.psi(cps.x, cps.y, cps.normal),
+                 pf.f_jump(cps.x, cps.y))
+    c = O.corrections(t, jm)
+    F = np.where(interior, pf.f_jump(ws.grid.X, ws.grid.Y), 0.0)
+    u = O.box_solve(t.m, t.h, 2.0, F + c, bc="neumann-zero")
+    assert np.array_equal(u, g[name + "__u"])
+    assert np.array_equal(np.stack(O.extract_onesided(t, u, jm)), g[name + "__trace"])
+
+
+@pytest.mark.parametrize("name", list(NEUMANN_RICH_CASES))
+def test_neumann_richardson_matches_reference(name):
+    box, m, ctag, kappa = NEUMANN_RICH_CASES[name]
+    ws = k.InterfaceWorkspace(k.build_grid(box, m, curve_of(ctag)))
+    t = O.tables_from_workspace(ws, onesided=True)
+    sol = k.StaticPlaneWave(kappa=kappa)
+    cps = ws.cps
+    interior = ws.geometry.classification.interior
+    F = np.where(interior, sol.f(ws.grid.X, ws.grid.Y), 0.0)
+    s = O.richardson(t, kappa, F, sol.f(cps.x, cps.y), sol.neumann(cps.x, cps.y, cps.normal),
+                     bc_kind="neumann")
+    g = golden("neumann")
+    p = "rich_" + name + "__"
+    assert s.iterations == int(g[p + "iterations"])
+    assert np.array_equal(np.array(s.history), g[p + "history"])
+    assert np.array_equal(s.u, g[p + "u"])
+    assert np.array_equal(s.density, g[p + "density"])
+    assert np.array_equal(s.trace_un, g[p + "trace_un"])
+
+
+@pytest.mark.parametrize("name", list(neumann_run_cases()))
+def test_neumann_runs_match_reference(name):
+    box, m, curve, kw = neumann_run_cases()[name]
+    ws = k.InterfaceWorkspace(k.build_grid(box, m, curve))
+    st = O.run(O.tables_from_workspace(ws, onesided=True), oracle_spec(kw))
+    g = golden("neumann")
+    assert st.iterations == list(g["run_" + name + "__iterations"])
+    assert rel_linf(st.u, g["run_" + name + "__u"]) == 0.0
