@@ -291,6 +291,12 @@ kfbi_status kfbi_strang_phase(kfbi_plan *plan, int64_t n, int32_t mode, const vo
                               double kappa_re, double kappa_im, void *F,
                               double *max_res, void *stream);
 
+/* dst[i] = src[idx[i]], i < n (device pointers): packs the interior nodes
+ * of a masked field (whose exterior is zero by construction) for a compact
+ * device -> host copy of a step's result. */
+kfbi_status kfbi_gather(kfbi_plan *plan, int32_t dtype, int64_t n, const int32_t *idx,
+                        const void *src, void *dst, void *stream);
+
 /* u <- mask*u and max|u| (np.where(ctx.mask, sol.u, 0) + check_stable). */
 kfbi_status kfbi_mask_norm(kfbi_plan *plan, int32_t dtype, int64_t n,
                            const uint8_t *mask, void *u, double *norm_out,

@@ -106,6 +106,7 @@ _SIGNATURES = {
     "kfbi_strang_phase": ([vp, i64, i32, vp, vp, f64, vp, f64, f64, vp, vp, f64, f64, vp,
                            C.POINTER(f64), vp], i32),
     "kfbi_mask_norm": ([vp, i32, i64, vp, vp, C.POINTER(f64), vp], i32),
+    "kfbi_gather": ([vp, i32, i64, vp, vp, vp, vp], i32),
     "kfbi_slab_panel_bytes": ([vp, i32, i32, C.POINTER(i64)], i32),
     "kfbi_slab_rows_fwd": ([vp, i32, vp, vp, f64, vp, vp, vp], i32),
     "kfbi_slab_cols": ([vp, i32, vp, f64, f64, vp, vp], i32),

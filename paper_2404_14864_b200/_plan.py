@@ -263,6 +263,11 @@ class Plan:
         N.check(status, iterations=50, last_residual=res.value)
         return res.value
 
+    def gather(self, idx, src, dst):
+        """dst[i] = src[idx[i]] on the device (kfbi_gather)."""
+        N.check(self._lib.kfbi_gather(self.handle, self._dt(src.is_complex()), int(idx.numel()),
+                                      idx.data_ptr(), src.data_ptr(), dst.data_ptr(), self.stream))
+
     def mask_norm(self, n, mask, u, want_norm=True):
         norm = C.c_double(0.0)
         N.check(self._lib.kfbi_mask_norm(self.handle, self._dt(u.is_complex()), int(n),

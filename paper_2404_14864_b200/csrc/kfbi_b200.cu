@@ -1213,6 +1213,21 @@ kfbi_status kfbi_strang_phase(kfbi_plan *p, int64_t n, int32_t mode, const void 
   return KFBI_OK;
 }
 
+kfbi_status kfbi_gather(kfbi_plan *p, int32_t dtype, int64_t n, const int32_t *idx, const void *src,
+                        void *dst, void *stream) {
+  KFBI_TRY(check_plan(p));
+  cudaStream_t s = (cudaStream_t)stream;
+  if (n <= 0) return KFBI_OK;
+  return launch(p, KFBI_K_RHS, s, [&] {
+    if (dtype == KFBI_C128)
+      gather_kernel<double2><<<elem_blocks(n), 256, 0, s>>>(n, idx, static_cast<const double2 *>(src),
+                                                            static_cast<double2 *>(dst));
+    else
+      gather_kernel<double><<<elem_blocks(n), 256, 0, s>>>(n, idx, static_cast<const double *>(src),
+                                                           static_cast<double *>(dst));
+  });
+}
+
 kfbi_status kfbi_mask_norm(kfbi_plan *p, int32_t dtype, int64_t n, const uint8_t *mask, void *u,
                            double *norm_out, void *stream) {
   KFBI_TRY(check_plan(p));

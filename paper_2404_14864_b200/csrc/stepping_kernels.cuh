@@ -201,6 +201,15 @@ __global__ void schr_ustar_kernel(long n, int mode, const double2 *__restrict__ 
     out[i] = ustar_of(mode, u[i], other[i], tau);
 }
 
+// dst[i] = src[idx[i]] (packing the interior nodes of a masked field for a
+// compact device -> host copy of a step's result)
+template <typename T>
+__global__ void __launch_bounds__(256) gather_kernel(long n, const int *__restrict__ idx,
+                                                     const T *__restrict__ src, T *__restrict__ dst) {
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x)
+    dst[i] = src[idx[i]];
+}
+
 // Pointwise damped Newton of nonlinear_phase_step (timestepping.py:317-368)
 // for u** + ic(v + w|u**|^2)u** = u* - ic(v + w|u*|^2)u*, c = tau/2.
 // Per node this is exactly the reference's vectorised iteration: a node stops

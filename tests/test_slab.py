@@ -204,3 +204,18 @@ def test_two_rank_gloo_slab_choreography():
     for g in range(world):
         assert out[("x", g)] == [100.0 * h + g for h in range(world) for _ in range(3)]
         assert out[("u", g)] < 1e-12
+
+
+@pytest.mark.gpu
+def test_packed_field_to_host_roundtrip():
+    import torch
+
+    geo = k.build_grid(BOX, 128, k.StarCurve(1.0, c=0.2, lobes=8))
+    ctx = k.StepContext(geo)
+    u = torch.randn(ctx.n_grid, dtype=torch.float64, device="cuda")
+    u[~torch.from_numpy(ctx.mask.ravel()).cuda()] = 0.0
+    out = torch.empty(ctx.interior_index.numel(), dtype=torch.float64, pin_memory=True)
+    ev = ctx.field_to_host(u, out, packed=True)
+    ev.synchronize()
+    full = ctx.unpack_interior(out.numpy())
+    assert np.array_equal(full.ravel(), u.cpu().numpy())
