@@ -454,7 +454,10 @@ struct OpSolveArgs {
 
 constexpr int OP_THREADS = 512;
 constexpr int OP_WARPS = OP_THREADS / 32;
-constexpr int OP_UNROLL = 8;
+template <typename T>
+struct OpTune;                    // register cache K and streamed loads in flight U
+template <> struct OpTune<double> { static constexpr int K = 24, U = 16; };
+template <> struct OpTune<double2> { static constexpr int K = 12, U = 8; };
 
 template <typename T>
 inline size_t op_smem_fixed(int n) {
@@ -496,7 +499,22 @@ op_solve_kernel(OpSolveArgs a, const T *__restrict__ Tcm, T *A, T *B,
   for (int idx = a.first_idx; idx < a.max_iter; ++idx) {
     const T *in = (idx & 1) ? A : B;
     T *out = (idx & 1) ? B : A;
-    for (int p = tid; p < n; p += OP_THREADS) d[p] = S::sub(__ldcg(in + p), phi0[p]);
+    // d = phi_in - phi0: all of a thread's loads in flight at once (a
+    // dependent loop of L2 round trips dominated the sweep before)
+    for (int p0 = tid; p0 < n; p0 += OP_THREADS * 5) {
+      T vi[5], v0[5];
+#pragma unroll
+      for (int u = 0; u < 5; ++u) {
+        const int p = p0 + u * OP_THREADS;
+        vi[u] = p < n ? __ldcg(in + p) : S::zero();
+        v0[u] = p < n ? __ldg(phi0 + p) : S::zero();
+      }
+#pragma unroll
+      for (int u = 0; u < 5; ++u) {
+        const int p = p0 + u * OP_THREADS;
+        if (p < n) d[p] = S::sub(vi[u], v0[u]);
+      }
+    }
     __syncthreads();
     double mag = 0.0;
     for (int rt = 0; rt < nr; rt += 32) {       // row tiles (one unless R > 32)
@@ -513,15 +531,16 @@ op_solve_kernel(OpSolveArgs a, const T *__restrict__ Tcm, T *A, T *B,
       if (rok)
         for (int c = cs0 + warp; c < cg0; c += OP_WARPS)
           acc = S::add(acc, S::mul(cache[(size_t)(c - cs0) * R + row], d[c]));
-      for (int c = cg0 + warp; c < n; c += OP_WARPS * OP_UNROLL) {
-        T v[OP_UNROLL];
+      constexpr int U = OpTune<T>::U;
+      for (int c = cg0 + warp; c < n; c += OP_WARPS * U) {
+        T v[U];
 #pragma unroll
-        for (int u = 0; u < OP_UNROLL; ++u) {
+        for (int u = 0; u < U; ++u) {
           const int cc = c + OP_WARPS * u;
           v[u] = (rok && cc < n) ? __ldcg(Tcm + (size_t)cc * n + r0 + row) : S::zero();
         }
 #pragma unroll
-        for (int u = 0; u < OP_UNROLL; ++u) {
+        for (int u = 0; u < U; ++u) {
           const int cc = c + OP_WARPS * u;
           if (cc < n) acc = S::add(acc, S::mul(v[u], d[cc]));
         }

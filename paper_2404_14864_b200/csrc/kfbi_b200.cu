@@ -608,7 +608,7 @@ kfbi_status build_operator_T(kfbi_plan *p, double kre, double kim, int bc_kind, 
 // T resident on chip (registers + shared memory) across the sweeps.
 template <typename T>
 kfbi_status op_solve(kfbi_plan *p, const kfbi_bvp *b, cudaStream_t s) {
-  constexpr int K = std::is_same<T, double2>::value ? 16 : 32;
+  constexpr int K = OpTune<T>::K;
   static int smem_optin = 0, sms = 0;
   if (!smem_optin) {
     cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, p->device);
