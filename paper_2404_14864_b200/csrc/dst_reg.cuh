@@ -37,7 +37,11 @@
 namespace kfbi {
 namespace reg {
 
-constexpr int E = 16;          // elements per thread
+#ifndef KFBI_E
+#define KFBI_E 16
+#endif
+constexpr int E = KFBI_E;      // elements per thread (16; 8 = more warps, one more pass)
+constexpr int LE = E == 16 ? 4 : 3;
 constexpr int CTA = 256;       // threads per CTA
 constexpr double RSQ2 = 0.70710678118654752440;
 
@@ -52,9 +56,9 @@ struct Cfg {
   static constexpr int CTA_T = T >= 256 ? (T > 512 ? 512 : T) : CTA;  // threads per CTA
   static constexpr int S = T >= 256 ? 1 : CTA / T;          // sequences per CTA
   static constexpr int LOCAL = CTA_T * E;                   // elements per CTA buffer
-  static constexpr int MINB = CTA_T == 256 ? 2 : 1;         // CTAs per SM
-  static constexpr int P = (LOGN + 3) / 4;        // Stockham passes
-  static constexpr int RLAST = 1 << (LOGN - 4 * (P - 1));
+  static constexpr int MINB = (CTA_T == 256 || E == 8) ? 2 : 1;  // CTAs per SM
+  static constexpr int P = (LOGN + LE - 1) / LE;  // Stockham passes
+  static constexpr int RLAST = 1 << (LOGN - LE * (P - 1));
   static_assert(LOGN >= 4 && LOGN <= 14, "DST length 16..16384");
 };
 
@@ -261,8 +265,8 @@ template <int LOGN, int PASS>
 KFBI_DEV void fft_passes(double2 (&v)[E], const View<LOGN> &sm, int t,
                          const double2 *__restrict__ twg) {
   using C = Cfg<LOGN>;
-  constexpr int R = (PASS < C::P - 1) ? 16 : C::RLAST;
-  constexpr int NS = 1 << (4 * PASS);
+  constexpr int R = (PASS < C::P - 1) ? E : C::RLAST;
+  constexpr int NS = 1 << (LE * PASS);
   stockham_pass<LOGN, R, NS>(v, sm, t, twg);
   if constexpr (PASS + 1 < C::P) {
     seq_sync<LOGN>();
@@ -313,8 +317,8 @@ KFBI_DEV void post(const View<LOGN> &sm, int t, double2 (&out)[E],
   constexpr int T = Cfg<LOGN>::T;
   double2 acc = make_double2(0.0, 0.0);
 #pragma unroll
-  for (int c = 0; c < 8; ++c) {
-    const int k = 8 * t + c;
+  for (int c = 0; c < E / 2; ++c) {
+    const int k = (E / 2) * t + c;
     const double2 zk = sm[k];
     const double2 zm = sm[(N - k) & (N - 1)];
     const double2 d = csub(zk, zm);
@@ -364,7 +368,7 @@ KFBI_DEV void post(const View<LOGN> &sm, int t, double2 (&out)[E],
     }
   }
 #pragma unroll
-  for (int c = 0; c < 8; ++c) out[2 * c + 1] = cadd(off, out[2 * c + 1]);
+  for (int c = 0; c < E / 2; ++c) out[2 * c + 1] = cadd(off, out[2 * c + 1]);
 }
 
 // Sum of v over the threads of the sequence, returned to every thread
