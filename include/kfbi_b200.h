@@ -76,7 +76,7 @@ typedef struct {
   int32_t n_edges;            /* unique sign-change edges (2 records each) */
   int32_t n_rec;              /* intersection records                    */
   int32_t n_groups;           /* owning irregular nodes                  */
-  const double *w_edges;      /* [n_edges][n_ctl] trig-interp rows       */
+  const double *w_edges;      /* [n_edges][n_ctl] trig-interp rows, or NULL */
   const int8_t *edge_axis;    /* [n_edges] 0 = horizontal, 1 = vertical  */
   const int32_t *rec_edge;    /* [n_rec] edge of each record             */
   const double *rec_d;        /* [n_rec] neighbour-minus-crossing offset */
@@ -93,6 +93,10 @@ typedef struct {
   const int32_t *stencil;     /* [n_ctl][6] flat node indices            */
   const double *ainv_rows;    /* [n_ctl][3][6] rows 0..2 of the 6x6 inverse */
   const double *jcoef;        /* [n_ctl][6][6] jump-shift coefficients   */
+  /* w_edges == NULL: build W on the device (trigonometric rows, even n_ctl
+   * >= 32, interface.py:38-52) from these parameters instead */
+  const double *edge_theta;   /* [n_edges] crossing parameter per edge   */
+  const double *ctl_theta;    /* [n_ctl] control parameters              */
 } kfbi_geometry;
 
 /* One Dirichlet or Neumann BVP solve by Richardson iteration (BvpProblem,
@@ -158,6 +162,9 @@ kfbi_status kfbi_box_solve_bc(kfbi_plan *plan, int32_t dtype, int32_t box_bc,
                               void *u, void *stream);
 
 kfbi_status kfbi_plan_set_geometry(kfbi_plan *plan, const kfbi_geometry *geo);
+
+/* Rows [row0, row0 + nrows) of the plan's W (n_ctl values each) to host. */
+kfbi_status kfbi_plan_copy_w(kfbi_plan *plan, int32_t row0, int32_t nrows, double *out);
 
 /* OneSidedExtractor tables (bvp.py:115-212), host pointers: stencil7
  * [n_ctl][7] flat node indices, rows [n_ctl][3][7] (rows 0..2 of inv(A)),

@@ -53,6 +53,7 @@ class Geometry(C.Structure):
         ("rec_sigma", vp), ("group_start", vp), ("group_node", vp), ("row_group", vp),
         ("deriv_col", vp), ("speed", vp), ("tangent", vp), ("normal", vp),
         ("dtan_ds", vp), ("inv3", vp), ("stencil", vp), ("ainv_rows", vp), ("jcoef", vp),
+        ("edge_theta", vp), ("ctl_theta", vp),
     ]
 
 
@@ -107,6 +108,7 @@ _SIGNATURES = {
                            C.POINTER(f64), vp], i32),
     "kfbi_mask_norm": ([vp, i32, i64, vp, vp, C.POINTER(f64), vp], i32),
     "kfbi_gather": ([vp, i32, i64, vp, vp, vp, vp], i32),
+    "kfbi_plan_copy_w": ([vp, i32, i32, vp], i32),
     "kfbi_slab_panel_bytes": ([vp, i32, i32, C.POINTER(i64)], i32),
     "kfbi_slab_rows_fwd": ([vp, i32, vp, vp, f64, vp, vp, vp], i32),
     "kfbi_slab_cols": ([vp, i32, vp, f64, f64, vp, vp], i32),

@@ -73,7 +73,6 @@ class Plan:
     def set_geometry(self, tables):
         """Upload the host tables built by InterfaceWorkspace (dict of numpy)."""
         t = {
-            "w_edges": _c(tables["w_edges"], _F64),
             "edge_axis": _c(tables["edge_axis"], np.int8),
             "rec_edge": _c(tables["rec_edge"], np.int32),
             "rec_d": _c(tables["rec_d"], _F64),
@@ -91,6 +90,13 @@ class Plan:
             "ainv_rows": _c(tables["ainv_rows"], _F64),
             "jcoef": _c(tables["jcoef"], _F64),
         }
+        # W: host rows when given, else built on the device from the crossing
+        # and control parameters (trigonometric interpolation)
+        if tables.get("w_edges") is not None:
+            t["w_edges"] = _c(tables["w_edges"], _F64)
+        else:
+            t["edge_theta"] = _c(tables["edge_theta"], _F64)
+            t["ctl_theta"] = _c(tables["ctl_theta"], _F64)
         g = N.Geometry(
             n_ctl=int(tables["n_ctl"]), n_edges=int(t["edge_axis"].size),
             n_rec=int(t["rec_edge"].size), n_groups=int(t["group_node"].size),
@@ -98,6 +104,12 @@ class Plan:
         N.check(self._lib.kfbi_plan_set_geometry(self.handle, C.byref(g)))
         self.n_ctl = int(tables["n_ctl"])
         self.has_geometry = True
+
+    def copy_w(self, row0, nrows):
+        """Rows of the device W (setup check)."""
+        out = np.empty((int(nrows), self.n_ctl))
+        N.check(self._lib.kfbi_plan_copy_w(self.handle, int(row0), int(nrows), out.ctypes.data))
+        return out
 
     # -- kernels --------------------------------------------------------------
     @staticmethod

@@ -164,6 +164,44 @@ __global__ void jumps_d2_kernel(CtlGeom g, const T *__restrict__ phi, const T *_
 }
 
 // ---------------------------------------------------------------------------
+// Device-side setup of W (InterfaceWorkspace.__init__, interface.py:161): the
+// cardinal trigonometric interpolation rows of _trig_rows (interface.py:38-52)
+//   x = mod(q - theta_p + pi, 2 pi) - pi   (numpy float mod: sign of divisor)
+//   D(x) = sin(m x / 2) cos(x / 2) / (m sin(x / 2)),  D = 1 where |x| < 1e-12
+// element-wise with the reference's operation order; the padding column of an
+// even-padded row stride is zero.  Differs from numpy only by libm rounding
+// (<= a few ulp).
+KFBI_DEV double np_mod(double a, double b) {
+  double r = fmod(a, b);
+  if (r != 0.0) {
+    if ((b < 0.0) != (r < 0.0)) r += b;
+  } else {
+    r = copysign(0.0, b);
+  }
+  return r;
+}
+
+__global__ void __launch_bounds__(256)
+w_build_kernel(int n_edges, int n_ctl, int ld, const double *__restrict__ edge_theta,
+               const double *__restrict__ ctl_theta, double *__restrict__ W) {
+  const double PI = 3.141592653589793;
+  const long total = (long)n_edges * ld;
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < total;
+       i += (long)gridDim.x * blockDim.x) {
+    const int e = (int)(i / ld), p = (int)(i - (long)e * ld);
+    double v = 0.0;
+    if (p < n_ctl) {
+      const double x = np_mod(edge_theta[e] - ctl_theta[p] + PI, 2.0 * PI) - PI;
+      const bool hit = fabs(x) < 1e-12;
+      const double xs = hit ? 1.0 : x;
+      const double r = sin(0.5 * n_ctl * xs) * cos(0.5 * xs) / (n_ctl * sin(0.5 * xs));
+      v = hit ? 1.0 : r;
+    }
+    W[i] = v;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // jv[e] = (W_e . JM_u, W_e . JM_a, W_e . JM_aa), a = x (horizontal) or y.
 // A warp owns EW consecutive edges and streams their W rows once.
 struct EdgeArgs {

@@ -793,13 +793,30 @@ kfbi_status kfbi_plan_set_geometry(kfbi_plan *p, const kfbi_geometry *g) {
   p->n_groups = g->n_groups;
   p->w_ld = (g->n_ctl + 1) & ~1;
   const int n = g->n_ctl;
-  std::vector<double> wpad((size_t)g->n_edges * p->w_ld, 0.0);
-  for (int e = 0; e < g->n_edges; ++e)
-    std::memcpy(&wpad[(size_t)e * p->w_ld], g->w_edges + (size_t)e * n, n * sizeof(double));
   cudaError_t e = cudaSuccess;
 #define UP(buf, ptr, cnt) \
   if (e == cudaSuccess) e = upload(p->buf, ptr, (size_t)(cnt))
-  UP(W, wpad.data(), wpad.size());
+  if (g->w_edges) {
+    std::vector<double> wpad((size_t)g->n_edges * p->w_ld, 0.0);
+    for (int ed = 0; ed < g->n_edges; ++ed)
+      std::memcpy(&wpad[(size_t)ed * p->w_ld], g->w_edges + (size_t)ed * n, n * sizeof(double));
+    UP(W, wpad.data(), wpad.size());
+  } else {
+    // device-side W build from the crossing and control parameters
+    if (!g->edge_theta || !g->ctl_theta || (n % 2) != 0 || n < 32)
+      return fail(KFBI_E_CONFIG, "device W build needs edge_theta / ctl_theta and an even n_ctl >= 32");
+    DevBuf<double> et, ct;
+    if (e == cudaSuccess) e = upload(et, g->edge_theta, (size_t)g->n_edges);
+    if (e == cudaSuccess) e = upload(ct, g->ctl_theta, (size_t)n);
+    if (e == cudaSuccess) e = p->W.ensure((size_t)g->n_edges * p->w_ld + 1);
+    if (e == cudaSuccess && g->n_edges > 0) {
+      w_build_kernel<<<148 * 16, 256>>>(g->n_edges, n, p->w_ld, et.p, ct.p, p->W.p);
+      e = cudaGetLastError();
+      if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    }
+    et.release();
+    ct.release();
+  }
   UP(edge_axis, reinterpret_cast<const signed char *>(g->edge_axis), g->n_edges);
   UP(rec_edge, g->rec_edge, g->n_rec);
   UP(rec_d, g->rec_d, g->n_rec);
@@ -824,6 +841,17 @@ kfbi_status kfbi_plan_set_geometry(kfbi_plan *p, const kfbi_geometry *g) {
   if (e != cudaSuccess) return fail(KFBI_E_CUDA, std::string("geometry upload: ") + cudaGetErrorString(e));
   p->has_geo = true;
   p->op_valid = false;
+  return KFBI_OK;
+}
+
+kfbi_status kfbi_plan_copy_w(kfbi_plan *p, int32_t row0, int32_t nrows, double *out) {
+  KFBI_TRY(check_geo(p));
+  if (!out || row0 < 0 || nrows < 0 || row0 + nrows > p->n_edges)
+    return fail(KFBI_E_CONFIG, "copy_w: bad row range");
+  cudaError_t e = cudaMemcpy2D(out, (size_t)p->n_ctl * sizeof(double), p->W.p + (size_t)row0 * p->w_ld,
+                               (size_t)p->w_ld * sizeof(double), (size_t)p->n_ctl * sizeof(double),
+                               (size_t)nrows, cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return fail(KFBI_E_CUDA, std::string("copy_w: ") + cudaGetErrorString(e));
   return KFBI_OK;
 }
 

@@ -166,8 +166,10 @@ class InterfaceWorkspace:
         self._inv3 = np.linalg.inv(a)
 
         # one interpolation row per unique sign-change edge; both records of
-        # an edge share theta (grid.py:243-254), so w_records = w_edges[edge]
-        self.w_edges = interp_rows(geometry.edge_theta, self.cps.theta)
+        # an edge share theta (grid.py:243-254), so w_records = w_edges[edge].
+        # Built lazily on the host (API views, tests); the device plan builds
+        # its own copy from the parameters (kfbi_plan_set_geometry)
+        self._w_edges = None
         self._box_solvers = {}
         self._plan = None
         self._trace = None
@@ -175,6 +177,18 @@ class InterfaceWorkspace:
         self._trace_error = None
 
     # -- host views kept for API compatibility --------------------------------
+    @property
+    def w_edges(self):
+        if self._w_edges is None:
+            self._w_edges = interp_rows(self.geometry.edge_theta, self.cps.theta)
+        return self._w_edges
+
+    @property
+    def device_w(self):
+        """W is built on the device when the trigonometric form applies."""
+        m = self.cps.m
+        return m >= TRIG_INTERP_MIN_M and m % 2 == 0
+
     @property
     def w_records(self):
         return self.w_edges[self.records.edge]
@@ -219,7 +233,9 @@ class InterfaceWorkspace:
         row_group = np.searchsorted(owner_row, np.arange(grid.m + 2), side="left")
         return {
             "n_ctl": n,
-            "w_edges": self.w_edges,
+            "w_edges": None if self.device_w else self.w_edges,
+            "edge_theta": self.geometry.edge_theta,
+            "ctl_theta": self.cps.theta,
             "edge_axis": self.geometry.edge_axis,
             "rec_edge": rec.edge,
             "rec_d": rec.d,

@@ -263,3 +263,13 @@ def test_runs_1024_vs_oracle_window(eq):
         res2 = k.run(k.ProblemSpec(**kw), geo, context=ctx, operator=True)
         assert res2.iterations == st.iterations
         assert rel_linf(res2.state.u, st.u) < TOL
+
+
+@pytest.mark.parametrize("name", ["flower128", "ellipse128", "pistar128"])
+def test_device_w_build_matches_host_rows(name):
+    # InterfaceWorkspace W (interface.py:161) built on the device vs numpy
+    box, m, curve = setup_cases()[name]
+    ws = k.InterfaceWorkspace(k.build_grid(box, m, curve))
+    assert ws.device_w
+    dev = ws.plan.copy_w(0, ws.w_edges.shape[0])
+    assert np.max(np.abs(dev - ws.w_edges)) < 1e-14
