@@ -304,6 +304,18 @@ def run_ours(args):
                               pin_memory=True) for eq in eqs}
     h2d = sum(ctxs[eq].n_ctl * (16 if eq == "schrodinger" else 8) for eq in eqs)
     d2h = sum(pinned[eq].numel() * pinned[eq].element_size() for eq in eqs)
+    # link probe (untimed): device -> pinned host bandwidth of this box
+    probe = torch.empty(max(p.numel() for p in pinned.values()) * 2 // 2, dtype=torch.float64,
+                        device=f"cuda:{local}")
+    host = torch.empty(probe.numel(), dtype=torch.float64, pin_memory=True)
+    host.copy_(probe)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(3):
+        host.copy_(probe)
+    torch.cuda.synchronize()
+    d2h_gbps = 3 * probe.numel() * 8 / (time.perf_counter() - t0) / 1e9
+    del probe, host
     _barrier(ws)
     torch.cuda.synchronize()
     s2 = torch.cuda.Event(enable_timing=True)
@@ -358,7 +370,8 @@ def run_ours(args):
                                              "c128": _bytes_cols(m, True)},
             "avg_launch_ms": cols_avg_ms,
         },
-        "e2e": {"value": e2e_value, "unit": "time steps/s", "h2d_bytes_per_step": h2d,
+        "e2e": {"value": e2e_value, "unit": "time steps/s", "d2h_link_GBps": d2h_gbps,
+                "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h},
         "gpu_launches": int(launches),
         "clocks": clocks,
