@@ -229,6 +229,28 @@ kfbi_status kfbi_slab_cols(kfbi_plan *plan, int32_t dtype, const kfbi_slab *slab
 kfbi_status kfbi_slab_rows_inv(kfbi_plan *plan, int32_t dtype, const kfbi_slab *slab,
                                const void *panels, void *u, void *stream);
 
+/* ---- slab-decomposed Richardson sweep (dist.py SlabRichardson) ----
+ * Per sweep on every rank: kfbi_jumps (replicated, O(n_ctl)) ->
+ * kfbi_edge_values (jv = W . JM, replicated) -> kfbi_slab_rows_fwd (with jv:
+ * the corrections of this slab's rows) -> all-to-all -> kfbi_slab_cols ->
+ * all-to-all -> kfbi_slab_rows_inv -> kfbi_slab_stencil_values (u at the
+ * extraction stencil nodes in this slab's rows, zero elsewhere;
+ * [n_ctl][13]) -> all-reduce(sum) of the values -> kfbi_slab_update
+ * (extraction + density update + residual, replicated, identical on every
+ * rank); kfbi_rich_begin / kfbi_rich_state open the solve and read its
+ * state (iterations, status 1 converged / 2 max_iter, residual, history). */
+kfbi_status kfbi_edge_values(kfbi_plan *plan, int32_t dtype, const void *jm, void *jv,
+                             void *stream);
+kfbi_status kfbi_slab_stencil_values(kfbi_plan *plan, int32_t dtype, int32_t bc_kind,
+                                     const kfbi_slab *slab, const void *u_slab, void *vals,
+                                     void *stream);
+kfbi_status kfbi_rich_begin(kfbi_plan *plan, int32_t max_iter, double tol, void *stream);
+kfbi_status kfbi_slab_update(kfbi_plan *plan, int32_t dtype, int32_t bc_kind, const void *vals,
+                             const void *jm, const void *g, void *density, void *trace_u,
+                             void *trace_un, double gamma, void *stream);
+kfbi_status kfbi_rich_state(kfbi_plan *plan, int32_t *iterations, int32_t *done,
+                            double *residual, double *history, void *stream);
+
 /* richardson_solve (bvp.py:276-351), device resident: one host sync per
  * batch of sweeps; history copied to result->history. */
 kfbi_status kfbi_richardson(kfbi_plan *plan, const kfbi_bvp *bvp,

@@ -108,6 +108,11 @@ _SIGNATURES = {
                            C.POINTER(f64), vp], i32),
     "kfbi_mask_norm": ([vp, i32, i64, vp, vp, C.POINTER(f64), vp], i32),
     "kfbi_gather": ([vp, i32, i64, vp, vp, vp, vp], i32),
+    "kfbi_edge_values": ([vp, i32, vp, vp, vp], i32),
+    "kfbi_slab_stencil_values": ([vp, i32, i32, vp, vp, vp, vp], i32),
+    "kfbi_rich_begin": ([vp, i32, f64, vp], i32),
+    "kfbi_slab_update": ([vp, i32, i32, vp, vp, vp, vp, vp, vp, f64, vp], i32),
+    "kfbi_rich_state": ([vp, C.POINTER(i32), C.POINTER(i32), C.POINTER(f64), vp, vp], i32),
     "kfbi_plan_copy_w": ([vp, i32, i32, vp], i32),
     "kfbi_slab_panel_bytes": ([vp, i32, i32, C.POINTER(i64)], i32),
     "kfbi_slab_rows_fwd": ([vp, i32, vp, vp, f64, vp, vp, vp], i32),

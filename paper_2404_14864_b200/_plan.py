@@ -144,6 +144,33 @@ class Plan:
         N.check(self._lib.kfbi_slab_rows_inv(self.handle, self._dt(cplx), C.byref(sl),
                                              panels.data_ptr(), u.data_ptr(), self.stream))
 
+    # -- slab-decomposed Richardson sweep (dist.py) -------------------------------
+    def edge_values(self, jm, jv):
+        N.check(self._lib.kfbi_edge_values(self.handle, self._dt(jm.is_complex()), jm.data_ptr(),
+                                           jv.data_ptr(), self.stream))
+
+    def slab_stencil_values(self, bc_kind, nranks, rank, u_slab, vals):
+        sl = N.Slab(int(nranks), int(rank))
+        N.check(self._lib.kfbi_slab_stencil_values(self.handle, self._dt(vals.is_complex()),
+                                                   _KIND[bc_kind], C.byref(sl), u_slab.data_ptr(),
+                                                   vals.data_ptr(), self.stream))
+
+    def rich_begin(self, max_iter, tol):
+        N.check(self._lib.kfbi_rich_begin(self.handle, int(max_iter), float(tol), self.stream))
+
+    def slab_update(self, bc_kind, vals, jm, g, density, trace_u, trace_un, gamma):
+        N.check(self._lib.kfbi_slab_update(self.handle, self._dt(vals.is_complex()), _KIND[bc_kind],
+                                           vals.data_ptr(), jm.data_ptr(), g.data_ptr(),
+                                           density.data_ptr(), trace_u.data_ptr(),
+                                           trace_un.data_ptr(), float(gamma), self.stream))
+
+    def rich_state(self, max_iter):
+        it, done, res = C.c_int32(0), C.c_int32(0), C.c_double(0.0)
+        hist = np.zeros(max(int(max_iter), 1))
+        N.check(self._lib.kfbi_rich_state(self.handle, C.byref(it), C.byref(done), C.byref(res),
+                                          hist.ctypes.data, self.stream))
+        return it.value, done.value, res.value, hist[: it.value].tolist()
+
     def jumps(self, kappa, phi, psi, f_gamma, jm, f_gamma_sign=1.0):
         k = complex(kappa)
         N.check(self._lib.kfbi_jumps(self.handle, self._dt(jm.is_complex()), k.real, k.imag,

@@ -298,10 +298,11 @@ struct ExtractArgs {
   const unsigned char *os_fb;     // [n] 1: fall back to the six-point stencil
 };
 
-// (u+, ux+, uy+) at control point p (bvp.py:98-104).
-template <typename T>
-KFBI_DEV void extract_point(const ExtractArgs &x, const T *__restrict__ u, const T *__restrict__ jm,
-                            int p, T &tu, T &tx, T &ty) {
+// (u+, ux+, uy+) at control point p (bvp.py:98-104) from the six stencil
+// values u6(s) of the straddling stencil.
+template <typename T, typename U6>
+KFBI_DEV void extract_point_v(const ExtractArgs &x, U6 u6, const T *__restrict__ jm, int p, T &tu,
+                              T &tx, T &ty) {
   using S = Sc<T>;
   T jp[6];
 #pragma unroll
@@ -313,7 +314,7 @@ KFBI_DEV void extract_point(const ExtractArgs &x, const T *__restrict__ u, const
     T corr = S::rmul(jp[0], jc[0]);
 #pragma unroll
     for (int k = 1; k < 6; ++k) corr = S::add(corr, S::rmul(jp[k], jc[k]));
-    vals[s] = S::add(u[x.stencil[6 * p + s]], corr);
+    vals[s] = S::add(u6(s), corr);
   }
   T c[3];
 #pragma unroll
@@ -329,18 +330,24 @@ KFBI_DEV void extract_point(const ExtractArgs &x, const T *__restrict__ u, const
   ty = rdiv(c[2], x.h);
 }
 
+template <typename T>
+KFBI_DEV void extract_point(const ExtractArgs &x, const T *__restrict__ u, const T *__restrict__ jm,
+                            int p, T &tu, T &tx, T &ty) {
+  extract_point_v<T>(x, [&](int s) { return u[x.stencil[6 * p + s]]; }, jm, p, tu, tx, ty);
+}
+
 // The extractor of the BVP kind: one-sided rows . u[7 nodes] (bvp.py:215-221)
 // with the straddling fallback (bvp.py:222-227: the fallback's gradient goes
 // through * h / h like the reference's coefficient array), or the six-point
-// straddling stencil.
-template <typename T>
-KFBI_DEV void extract_any(const ExtractArgs &x, const T *__restrict__ u, const T *__restrict__ jm,
-                          int p, T &tu, T &tx, T &ty) {
+// straddling stencil.  u6(s) / u7(k): field values at the stencil nodes.
+template <typename T, typename U6, typename U7>
+KFBI_DEV void extract_any_v(const ExtractArgs &x, U6 u6, U7 u7, const T *__restrict__ jm, int p,
+                            T &tu, T &tx, T &ty) {
   using S = Sc<T>;
   if (x.os_stencil && !x.os_fb[p]) {
     T v[7];
 #pragma unroll
-    for (int k = 0; k < 7; ++k) v[k] = u[x.os_stencil[7 * p + k]];
+    for (int k = 0; k < 7; ++k) v[k] = u7(k);
     T c[3];
 #pragma unroll
     for (int r = 0; r < 3; ++r) {
@@ -355,12 +362,52 @@ KFBI_DEV void extract_any(const ExtractArgs &x, const T *__restrict__ u, const T
     ty = rdiv(c[2], x.h);
     return;
   }
-  extract_point<T>(x, u, jm, p, tu, tx, ty);
+  extract_point_v<T>(x, u6, jm, p, tu, tx, ty);
   if (x.os_stencil) {
     tx = rdiv(S::rmul(tx, x.h), x.h);
     ty = rdiv(S::rmul(ty, x.h), x.h);
   }
 }
+
+template <typename T>
+KFBI_DEV void extract_any(const ExtractArgs &x, const T *__restrict__ u, const T *__restrict__ jm,
+                          int p, T &tu, T &tx, T &ty) {
+  extract_any_v<T>(
+      x, [&](int s) { return u[x.stencil[6 * p + s]]; },
+      [&](int k) { return u[x.os_stencil[7 * p + k]]; }, jm, p, tu, tx, ty);
+}
+
+// ---- slab-decomposed sweep (dist.py): stencil values of one row slab ----
+// vals[13 p + s] (six-point, s < 6) and vals[13 p + 6 + k] (one-sided) =
+// u at the node when its grid row lies in [row0, row0 + rows), else 0; the
+// sum over the ranks' buffers (all-reduce) is the full stencil data.
+constexpr int SLAB_VALS = 13;
+
+template <typename T>
+__global__ void __launch_bounds__(256)
+slab_stencil_kernel(ExtractArgs x, int row0, int rows, const T *__restrict__ u_slab, T *vals) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= x.n) return;
+  const int stride = x.m + 1;
+  auto pick = [&](int node) -> T {
+    const int j = node / stride;
+    if (j < row0 || j >= row0 + rows) return Sc<T>::zero();
+    return u_slab[(size_t)(j - row0) * stride + (node - j * stride)];
+  };
+#pragma unroll
+  for (int s = 0; s < 6; ++s) vals[SLAB_VALS * p + s] = pick(x.stencil[6 * p + s]);
+#pragma unroll
+  for (int k = 0; k < 7; ++k)
+    vals[SLAB_VALS * p + 6 + k] = x.os_stencil ? pick(x.os_stencil[7 * p + k]) : Sc<T>::zero();
+}
+
+// Extraction from reduced stencil values + density update + residual; the
+// last block closes the sweep (same arithmetic as extract_update_kernel).
+template <typename T>
+__global__ void __launch_bounds__(256)
+extract_update_vals_kernel(ExtractArgs x, const T *__restrict__ vals, const T *__restrict__ jm,
+                           const T *__restrict__ g, T *density, T *trace_u, T *trace_un,
+                           double gamma, int dirichlet, RichState *st, double *history);
 
 template <typename T>
 __global__ void __launch_bounds__(256)
@@ -421,6 +468,32 @@ extract_update_kernel(ExtractArgs x, const T *__restrict__ u, const T *__restric
   if (p < x.n) {
     T tu, tx, ty;
     extract_any<T>(x, u, jm, p, tu, tx, ty);
+    const double nx = x.normal[2 * p], ny = x.normal[2 * p + 1];
+    T tun = S::add(S::rmul(tx, nx), S::rmul(ty, ny));
+    T target = dirichlet ? tu : tun;
+    T upd = S::rmul(S::sub(g[p], target), gamma);
+    density[p] = S::add(density[p], upd);
+    trace_u[p] = tu;
+    trace_un[p] = tun;
+    mag = S::abs(upd);
+  }
+  sweep_close(mag, st, history);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256)
+extract_update_vals_kernel(ExtractArgs x, const T *__restrict__ vals, const T *__restrict__ jm,
+                           const T *__restrict__ g, T *density, T *trace_u, T *trace_un,
+                           double gamma, int dirichlet, RichState *st, double *history) {
+  using S = Sc<T>;
+  if (st->done) return;
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  double mag = 0.0;
+  if (p < x.n) {
+    T tu, tx, ty;
+    extract_any_v<T>(
+        x, [&](int s) { return vals[SLAB_VALS * p + s]; },
+        [&](int k) { return vals[SLAB_VALS * p + 6 + k]; }, jm, p, tu, tx, ty);
     const double nx = x.normal[2 * p], ny = x.normal[2 * p + 1];
     T tun = S::add(S::rmul(tx, nx), S::rmul(ty, ny));
     T target = dirichlet ? tu : tun;

@@ -750,6 +750,84 @@ kfbi_status kfbi_slab_rows_inv(kfbi_plan *p, int32_t dtype, const kfbi_slab *sl,
                    stream);
 }
 
+// ---- slab-decomposed Richardson sweep (dist.py SlabRichardson) ----
+kfbi_status kfbi_edge_values(kfbi_plan *p, int32_t dtype, const void *jm, void *jv, void *stream) {
+  KFBI_TRY(check_geo(p));
+  cudaStream_t s = (cudaStream_t)stream;
+  if (dtype == KFBI_C128) return edges_T<double2>(p, jm, jv, nullptr, s);
+  return edges_T<double>(p, jm, jv, nullptr, s);
+}
+
+kfbi_status kfbi_slab_stencil_values(kfbi_plan *p, int32_t dtype, int32_t bc_kind, const kfbi_slab *sl,
+                                     const void *u_slab, void *vals, void *stream) {
+  KFBI_TRY(check_geo(p));
+  if (!sl) return fail(KFBI_E_CONFIG, "slab: null argument");
+  if (bc_kind == 1 && !p->has_os) return fail(KFBI_E_CONFIG, "one-sided extraction tables missing");
+  BoxArgs a = box_args(p, 0.0, 0.0, nullptr);
+  KFBI_TRY(slab_args(p, dtype == KFBI_C128, sl->nranks, sl->rank, a));
+  ExtractArgs x = extract_args(p, bc_kind == 1);
+  cudaStream_t s = (cudaStream_t)stream;
+  const int blocks = (p->n_ctl + 255) / 256;
+  return launch(p, KFBI_K_EXTRACT, s, [&] {
+    if (dtype == KFBI_C128)
+      slab_stencil_kernel<double2><<<blocks, 256, 0, s>>>(x, a.row0, a.rows,
+                                                          static_cast<const double2 *>(u_slab),
+                                                          static_cast<double2 *>(vals));
+    else
+      slab_stencil_kernel<double><<<blocks, 256, 0, s>>>(x, a.row0, a.rows,
+                                                         static_cast<const double *>(u_slab),
+                                                         static_cast<double *>(vals));
+  });
+}
+
+kfbi_status kfbi_rich_begin(kfbi_plan *p, int32_t max_iter, double tol, void *stream) {
+  KFBI_TRY(check_geo(p));
+  if (max_iter < 1) return fail(KFBI_E_CONFIG, "max iterations must be >= 1");
+  cudaError_t e = p->history.ensure(max_iter);
+  if (e != cudaSuccess) return fail(KFBI_E_CUDA, "history allocation failed");
+  cudaStream_t s = (cudaStream_t)stream;
+  return launch(p, KFBI_K_DENSITY, s, [&] { rich_init_kernel<<<1, 1, 0, s>>>(p->st.p, max_iter, tol); });
+}
+
+kfbi_status kfbi_slab_update(kfbi_plan *p, int32_t dtype, int32_t bc_kind, const void *vals,
+                             const void *jm, const void *g, void *density, void *trace_u,
+                             void *trace_un, double gamma, void *stream) {
+  KFBI_TRY(check_geo(p));
+  ExtractArgs x = extract_args(p, bc_kind == 1);
+  cudaStream_t s = (cudaStream_t)stream;
+  const int blocks = (p->n_ctl + 255) / 256;
+  return launch(p, KFBI_K_DENSITY, s, [&] {
+    if (dtype == KFBI_C128)
+      extract_update_vals_kernel<double2><<<blocks, 256, 0, s>>>(
+          x, static_cast<const double2 *>(vals), static_cast<const double2 *>(jm),
+          static_cast<const double2 *>(g), static_cast<double2 *>(density),
+          static_cast<double2 *>(trace_u), static_cast<double2 *>(trace_un), gamma, bc_kind == 0,
+          p->st.p, p->history.p);
+    else
+      extract_update_vals_kernel<double><<<blocks, 256, 0, s>>>(
+          x, static_cast<const double *>(vals), static_cast<const double *>(jm),
+          static_cast<const double *>(g), static_cast<double *>(density),
+          static_cast<double *>(trace_u), static_cast<double *>(trace_un), gamma, bc_kind == 0,
+          p->st.p, p->history.p);
+  });
+}
+
+kfbi_status kfbi_rich_state(kfbi_plan *p, int32_t *iterations, int32_t *done, double *residual,
+                            double *history, void *stream) {
+  KFBI_TRY(check_geo(p));
+  cudaStream_t s = (cudaStream_t)stream;
+  KFBI_CUDA(cudaMemcpyAsync(p->st_host, p->st.p, sizeof(RichState), cudaMemcpyDeviceToHost, s),
+            "density-update");
+  KFBI_CUDA(cudaStreamSynchronize(s), "density-update");
+  if (iterations) *iterations = p->st_host->iters;
+  if (done) *done = p->st_host->done;
+  if (residual) *residual = p->st_host->last_res;
+  if (history && p->st_host->iters > 0)
+    KFBI_CUDA(cudaMemcpy(history, p->history.p, sizeof(double) * p->st_host->iters, cudaMemcpyDeviceToHost),
+              "density-update");
+  return KFBI_OK;
+}
+
 kfbi_status kfbi_plan_destroy(kfbi_plan *p) {
   if (!p) return KFBI_OK;
   cudaSetDevice(p->device);

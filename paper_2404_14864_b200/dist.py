@@ -166,3 +166,154 @@ def gather_rows(u_slab, m, group=None):
     full[:m] = torch.cat(parts, 0)
     return full
 
+
+
+# ---------------------------------------------------------------------------
+# slab-decomposed Richardson solve (bvp.py:276-351), dirichlet-zero box
+
+def _allreduce_sum(t, nranks, group=None):
+    if nranks == 1:
+        return t
+    dist = _dist()
+    if dist is None:
+        raise ConfigError("slab Richardson with nranks > 1 needs an initialised torch.distributed")
+    dist.all_reduce(t, group=group)
+    return t
+
+
+class SlabRichardson:
+    """The Richardson BVP solve of one rank of a slab-decomposed job.
+
+    Rank g holds rows ``slab_rows(m, P, g)`` of F and of the returned field.
+    Everything O(n_ctl) (density, jumps, edge values, traces, convergence) is
+    replicated and computed identically on every rank; per sweep the ranks
+    exchange the box-solve transposes (two all-to-alls) and one all-reduce of
+    13 n_ctl stencil values (include/kfbi_b200.h, kfbi_slab_*).  The field,
+    density and iteration counts are bit-identical to the one-GPU solve."""
+
+    def __init__(self, workspace, nranks=None, rank=None, group=None):
+        dist = _dist()
+        self.ws = workspace
+        self.nranks = int(nranks if nranks is not None else (dist.get_world_size(group) if dist else 1))
+        self.rank = int(rank if rank is not None else (dist.get_rank(group) if dist else 0))
+        self.group = group
+        self.rows = slab_rows(workspace.grid.m, self.nranks, self.rank)
+
+    def solve(self, *, kappa, F, f_gamma, g, density, F_sign=1.0, f_gamma_sign=1.0, gamma=0.8,
+              tol=1e-8, max_iter=200, bc_kind="dirichlet"):
+        """F: this rank's rows (rows, m+1); f_gamma, g, density: n_ctl device
+        vectors (density updated in place).  Returns (u_slab, trace_u,
+        trace_un, iterations, residual, history)."""
+        import torch
+
+        from .errors import ConvergenceError
+
+        if bc_kind != "dirichlet":
+            raise ConfigError("the slab-decomposed solve supports Dirichlet BVPs "
+                              "(dirichlet-zero box)")
+        ws, P, r = self.ws, self.nranks, self.rank
+        plan = ws.plan
+        ws.trace_tables()
+        cplx = F.is_complex() or isinstance(kappa, complex) and complex(kappa).imag != 0
+        dt = torch.complex128 if cplx else torch.float64
+        dev = F.device
+        n = ws.cps.m
+        jm = torch.empty(6 * n, dtype=dt, device=dev)
+        jv = torch.empty(3 * max(int(ws.geometry.edge_theta.size), 1), dtype=dt, device=dev)
+        vals = torch.empty(13 * n, dtype=dt, device=dev)
+        tu = torch.empty(n, dtype=dt, device=dev)
+        tn = torch.empty_like(tu)
+        u = torch.empty_like(F)
+        nbytes = plan.slab_panel_bytes(cplx, P)
+        a = torch.empty(nbytes // 8, dtype=torch.float64, device=dev)
+        b = torch.empty_like(a) if P > 1 else None
+        plan.rich_begin(max_iter, tol)
+        it = done = 0
+        res, hist = 0.0, []
+        for _ in range(max_iter):
+            plan.jumps(kappa, density, None, f_gamma, jm, f_gamma_sign)
+            plan.edge_values(jm, jv)
+            plan.slab_rows_fwd(cplx, P, r, F, a, sign=F_sign, jv=jv)
+            t = exchange_chunks(b, a, P, self.group)
+            plan.slab_cols(cplx, P, r, kappa, t)
+            t = exchange_chunks(a, t, P, self.group)
+            plan.slab_rows_inv(cplx, P, r, t, u)
+            plan.slab_stencil_values(bc_kind, P, r, u, vals)
+            _allreduce_sum(vals, P, self.group)
+            plan.slab_update(bc_kind, vals, jm, g, density, tu, tn, gamma)
+            it, done, res, hist = plan.rich_state(max_iter)
+            if done:
+                break
+        if done != 1:
+            raise ConvergenceError(
+                f"Richardson iteration did not reach tol={tol:g} within {max_iter} sweeps "
+                f"(last density update {res:.3e})", iterations=max_iter, last_residual=res)
+        return u, tu, tn, it, res, hist
+
+
+def richardson_virtual(workspace, nranks, *, kappa, F, f_gamma, g, density, F_sign=1.0,
+                       f_gamma_sign=1.0, gamma=0.8, tol=1e-8, max_iter=200):
+    """The P-slab Richardson solve on ONE device (every rank's passes in
+    turn, the exchanges as chunk copies, the all-reduce as a sum): the same
+    kernels and layouts as SlabRichardson.  F: full (m+1)^2 field.  Returns
+    (u full, trace_u, trace_un, iterations, residual, history)."""
+    import torch
+
+    from .errors import ConvergenceError
+
+    ws, P = workspace, int(nranks)
+    plan = ws.plan
+    ws.trace_tables()
+    m = ws.grid.m
+    F = F.reshape(m + 1, m + 1)
+    cplx = F.is_complex()
+    dt = F.dtype
+    dev = F.device
+    n = ws.cps.m
+    rows = [slab_rows(m, P, q) for q in range(P)]
+    jm = torch.empty(6 * n, dtype=dt, device=dev)
+    jv = torch.empty(3 * max(int(ws.geometry.edge_theta.size), 1), dtype=dt, device=dev)
+    vals = torch.empty(13 * n, dtype=dt, device=dev)
+    part = torch.empty_like(vals)
+    tu = torch.empty(n, dtype=dt, device=dev)
+    tn = torch.empty_like(tu)
+    nbytes = plan.slab_panel_bytes(cplx, P)
+    send = [torch.empty(nbytes // 8, dtype=torch.float64, device=dev) for _ in range(P)]
+    recv = [torch.empty_like(x) for x in send]
+    Fs = [F[r0:r1].contiguous() for r0, r1 in rows]
+    us = [torch.empty_like(f) for f in Fs]
+
+    def a2a(dst, src):
+        c = src[0].numel() // P
+        for q in range(P):
+            for h in range(P):
+                dst[q][h * c:(h + 1) * c].copy_(src[h][q * c:(q + 1) * c])
+
+    plan.rich_begin(max_iter, tol)
+    it = done = 0
+    res, hist = 0.0, []
+    for _ in range(max_iter):
+        plan.jumps(kappa, density, None, f_gamma, jm, f_gamma_sign)
+        plan.edge_values(jm, jv)
+        for q in range(P):
+            plan.slab_rows_fwd(cplx, P, q, Fs[q], send[q], sign=F_sign, jv=jv)
+        a2a(recv, send)
+        for q in range(P):
+            plan.slab_cols(cplx, P, q, kappa, recv[q])
+        a2a(send, recv)
+        vals.zero_()
+        for q in range(P):
+            plan.slab_rows_inv(cplx, P, q, send[q], us[q])
+            plan.slab_stencil_values("dirichlet", P, q, us[q], part)
+            vals += part
+        plan.slab_update("dirichlet", vals, jm, g, density, tu, tn, gamma)
+        it, done, res, hist = plan.rich_state(max_iter)
+        if done:
+            break
+    if done != 1:
+        raise ConvergenceError(f"no convergence in {max_iter} sweeps ({res:.3e})",
+                               iterations=max_iter, last_residual=res)
+    u = torch.zeros((m + 1, m + 1), dtype=dt, device=dev)
+    for (r0, r1), uq in zip(rows, us):
+        u[r0:r1] = uq
+    return u, tu, tn, it, res, hist

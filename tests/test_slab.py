@@ -219,3 +219,35 @@ def test_packed_field_to_host_roundtrip():
     ev.synchronize()
     full = ctx.unpack_interior(out.numpy())
     assert np.array_equal(full.ravel(), u.cpu().numpy())
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("m,kappa", [(64, 16.0), (128, 200.0), (128, 16j)])
+def test_slab_richardson_virtual_bit_identical(m, kappa):
+    # the slab-decomposed Richardson solve (stencil-value all-reduce) equals
+    # the one-GPU device solve bit for bit, for 1, 2 and 4 virtual ranks
+    import torch
+
+    from paper_2404_14864_b200.bvp import solve_device
+
+    box = BOX if not isinstance(kappa, complex) else (-np.pi, np.pi, -np.pi, np.pi)
+    curve = k.StarCurve(1.0, c=0.2, lobes=8) if m == 128 else k.CircleCurve(1.0)
+    ws = k.InterfaceWorkspace(k.build_grid(box, m, curve))
+    sol = k.StaticPlaneWave(kappa=abs(kappa))
+    cps = ws.cps
+    interior = ws.geometry.classification.interior
+    dt = torch.complex128 if isinstance(kappa, complex) else torch.float64
+    X, Y = ws.grid.X, ws.grid.Y
+    F = torch.from_numpy(np.where(interior, -(1.0 + kappa) * sol.u(X, Y), 0.0)).to("cuda", dt)
+    fg = torch.from_numpy(np.asarray(-(1.0 + kappa) * sol.u(cps.x, cps.y))).to("cuda", dt)
+    g = torch.from_numpy(np.asarray(sol.dirichlet(cps.x, cps.y))).to("cuda", dt)
+    ref = solve_device(ws, kappa=kappa, F=F.reshape(-1), f_gamma=fg, g=g,
+                       density=torch.zeros(cps.m, dtype=dt, device="cuda"))
+    for p in (1, 2, 4):
+        dens = torch.zeros(cps.m, dtype=dt, device="cuda")
+        u, tu, tn, it, res, hist = D.richardson_virtual(ws, p, kappa=kappa, F=F, f_gamma=fg, g=g,
+                                                        density=dens)
+        assert it == ref.iterations
+        assert torch.equal(u.reshape(-1), ref.u.reshape(-1)), p
+        assert torch.equal(dens, ref.density)
+        assert torch.equal(tu, ref.trace_u)
