@@ -71,38 +71,9 @@ KFBI_DEV T circ_deriv(const CtlGeom &g, const T *__restrict__ v, int i, int lane
   return acc[0];
 }
 
-// Warp dot product  sum_p row[p] (x[p] - x0[p])  with U independent partial
-// sums (U streaming row loads in flight per lane); result in every lane.
-template <typename T, int U>
-KFBI_DEV T warp_row_dot(const T *__restrict__ row, const T *__restrict__ x,
-                        const T *__restrict__ x0, int n, int lane);
-
 KFBI_DEV double warp_reduce_T(double v) { return warp_sum(v); }
 KFBI_DEV double2 warp_reduce_T(double2 v) {
   return make_double2(warp_sum(v.x), warp_sum(v.y));
-}
-
-template <typename T, int U>
-KFBI_DEV T warp_row_dot(const T *__restrict__ row, const T *__restrict__ x,
-                        const T *__restrict__ x0, int n, int lane) {
-  using S = Sc<T>;
-  T acc[U];
-#pragma unroll
-  for (int u = 0; u < U; ++u) acc[u] = S::zero();
-  int p = lane;
-  for (; p + 32 * (U - 1) < n; p += 32 * U) {
-    T r[U], d[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) r[u] = __ldcg(row + p + 32 * u);
-#pragma unroll
-    for (int u = 0; u < U; ++u) d[u] = S::sub(x[p + 32 * u], x0[p + 32 * u]);
-#pragma unroll
-    for (int u = 0; u < U; ++u) acc[u] = S::add(acc[u], S::mul(r[u], d[u]));
-  }
-  for (; p < n; p += 32) acc[0] = S::add(acc[0], S::mul(__ldcg(row + p), S::sub(x[p], x0[p])));
-#pragma unroll
-  for (int u = 1; u < U; ++u) acc[0] = S::add(acc[0], acc[u]);
-  return warp_reduce_T(acc[0]);
 }
 
 // phi_s (and psi_s when psi != nullptr).
