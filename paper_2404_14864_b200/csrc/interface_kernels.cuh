@@ -214,14 +214,33 @@ corr_edges_kernel(EdgeArgs ea, const T *__restrict__ jm, T *jv, const int *done)
   const int n2 = ea.ld >> 1;
   for (int i0 = lane; i0 < n2; i0 += 32 * U) {
     double2 w2[U][EW];
+    // one asm statement per 4 rows: the loads issue back to back, ahead of
+    // any use (ptxas otherwise interleaves them with the FMA chains)
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int i2 = i0 + 32 * u;
+      const int ii = i2 < n2 ? i2 : 0;
 #pragma unroll
-      for (int q = 0; q < EW; ++q)
-        w2[u][q] = i2 < n2 ? __ldcs(reinterpret_cast<const double2 *>(wr[q]) + i2)
-                           : make_double2(0.0, 0.0);
+      for (int q0 = 0; q0 < EW; q0 += 4) {
+        const double2 *a0 = reinterpret_cast<const double2 *>(wr[q0]) + ii;
+        const double2 *a1 = reinterpret_cast<const double2 *>(wr[q0 + 1]) + ii;
+        const double2 *a2 = reinterpret_cast<const double2 *>(wr[q0 + 2]) + ii;
+        const double2 *a3 = reinterpret_cast<const double2 *>(wr[q0 + 3]) + ii;
+        asm volatile(
+            "ld.global.cs.v2.f64 {%0,%1}, [%8];\n\t"
+            "ld.global.cs.v2.f64 {%2,%3}, [%9];\n\t"
+            "ld.global.cs.v2.f64 {%4,%5}, [%10];\n\t"
+            "ld.global.cs.v2.f64 {%6,%7}, [%11];"
+            : "=d"(w2[u][q0].x), "=d"(w2[u][q0].y), "=d"(w2[u][q0 + 1].x), "=d"(w2[u][q0 + 1].y),
+              "=d"(w2[u][q0 + 2].x), "=d"(w2[u][q0 + 2].y), "=d"(w2[u][q0 + 3].x),
+              "=d"(w2[u][q0 + 3].y)
+            : "l"(a0), "l"(a1), "l"(a2), "l"(a3));
+      }
+      if (i2 >= n2)
+#pragma unroll
+        for (int q = 0; q < EW; ++q) w2[u][q] = make_double2(0.0, 0.0);
     }
+
 #pragma unroll
     for (int u = 0; u < U; ++u) {
 #pragma unroll

@@ -13,13 +13,14 @@ out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--kernel-n
 lines = out.splitlines()
 rows = list(csv.reader(io.StringIO("\n".join(lines[1:]))))
 h = rows[0]
-ix = {n: h.index(n) for n in ("Address", "Source", "Warp Stall Sampling (All Samples)",
-                              "L1 Wavefronts Shared Excessive", "L1 Wavefronts Shared",
-                              "Instructions Executed")}
+ix = {n: (h.index(n) if n in h else None)
+      for n in ("Address", "Source", "Warp Stall Sampling (All Samples)",
+                "L1 Wavefronts Shared Excessive", "L1 Wavefronts Shared", "Instructions Executed")}
 data = rows[1:]
 def f(r, k):
     try: return float(r[ix[k]])
     except Exception: return 0.0
+data = [r for r in data if r and r[0].startswith("0x")]
 tot = sum(f(r, "Warp Stall Sampling (All Samples)") for r in data)
 print(f"total stall samples {tot:.0f}")
 for r in sorted(data, key=lambda r: -f(r, "Warp Stall Sampling (All Samples)"))[:top]:
