@@ -684,6 +684,144 @@ op_solve_kernel(OpSolveArgs a, const T *__restrict__ Tcm, T *A, T *B,
   }
 }
 
+// f64 operator sweeps with two rows per lane: half-warp h of warp w works on
+// columns 2w + h + 32 s, lane l of the half on rows (2l, 2l+1) of the CTA's
+// block, so every shared-memory and global load of T is a 16-byte pair and
+// each instruction covers two columns (half the instructions of the one-row
+// kernel above, which remains the complex / odd-n path).  Same sweep
+// semantics, same convergence protocol.  Requires n and R even.
+template <int K2>
+__global__ void __launch_bounds__(OP_THREADS, 1)
+op_solve_pair_kernel(OpSolveArgs a, const double *__restrict__ Tcm, double *A, double *B,
+                     const double *__restrict__ phi0, const double *__restrict__ trace1,
+                     const double *__restrict__ g) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ __align__(16) unsigned char op_smem[];
+  __shared__ double res_s;
+  const int n = a.n, R = a.rows, Cs = a.smem_cols;
+  double *d = reinterpret_cast<double *>(op_smem);       // phi_in - phi0, [n]
+  double *part = d + ((n + 1) & ~1);                     // [OP_WARPS][32]
+  double *cache = part + OP_WARPS * 32;                  // [Cs][R], column-major
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int hl = lane & 15, hf = lane >> 4;
+  const int r0 = blockIdx.x * R;
+  const int nr = max(0, min(R, n - r0));
+  const bool rok = 2 * hl < nr;
+  const int creg = min(n, 2 * OP_WARPS * K2);
+  const int cs0 = creg, cg0 = min(n, creg + Cs);
+  const int c_off = 2 * warp + hf;                       // first column of this half-warp
+
+  double2 treg[K2];
+#pragma unroll
+  for (int k = 0; k < K2; ++k) {
+    const int c = c_off + 2 * OP_WARPS * k;
+    treg[k] = (rok && c < creg) ? *reinterpret_cast<const double2 *>(Tcm + (size_t)c * n + r0 + 2 * hl)
+                                : make_double2(0.0, 0.0);
+  }
+  for (int i = tid; i < (cg0 - cs0) * R; i += OP_THREADS) {
+    const int c = cs0 + i / R, r = i - (i / R) * R;
+    cache[i] = r < nr ? Tcm[(size_t)c * n + r0 + r] : 0.0;
+  }
+  if (a.st->done) return;                       // uniform: set before launch
+
+  for (int idx = a.first_idx; idx < a.max_iter; ++idx) {
+    const double *in = (idx & 1) ? A : B;
+    double *out = (idx & 1) ? B : A;
+    for (int p0 = tid; p0 < n; p0 += OP_THREADS * 5) {
+      double vi[5], v0[5];
+#pragma unroll
+      for (int u = 0; u < 5; ++u) {
+        const int p = p0 + u * OP_THREADS;
+        vi[u] = p < n ? __ldcg(in + p) : 0.0;
+        v0[u] = p < n ? __ldg(phi0 + p) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 5; ++u) {
+        const int p = p0 + u * OP_THREADS;
+        if (p < n) d[p] = vi[u] - v0[u];
+      }
+    }
+    __syncthreads();
+    double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int k = 0; k < K2; ++k) {
+      const int c = c_off + 2 * OP_WARPS * k;
+      if (c < creg) {
+        const double dc = d[c];
+        acc.x = fma(treg[k].x, dc, acc.x);
+        acc.y = fma(treg[k].y, dc, acc.y);
+      }
+    }
+    if (rok)
+      for (int c = cs0 + c_off; c < cg0; c += 2 * OP_WARPS) {
+        const double2 t2 = *reinterpret_cast<const double2 *>(cache + (size_t)(c - cs0) * R + 2 * hl);
+        const double dc = d[c];
+        acc.x = fma(t2.x, dc, acc.x);
+        acc.y = fma(t2.y, dc, acc.y);
+      }
+    constexpr int U = 8;
+    for (int c = cg0 + c_off; c < n; c += 2 * OP_WARPS * U) {
+      double2 v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int cc = c + 2 * OP_WARPS * u;
+        v[u] = (rok && cc < n)
+                   ? __ldcg(reinterpret_cast<const double2 *>(Tcm + (size_t)cc * n + r0 + 2 * hl))
+                   : make_double2(0.0, 0.0);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int cc = c + 2 * OP_WARPS * u;
+        if (cc < n) {
+          const double dc = d[cc];
+          acc.x = fma(v[u].x, dc, acc.x);
+          acc.y = fma(v[u].y, dc, acc.y);
+        }
+      }
+    }
+    // the two column halves of the warp hold partial sums of the same rows
+    acc.x += __shfl_xor_sync(0xffffffffu, acc.x, 16);
+    acc.y += __shfl_xor_sync(0xffffffffu, acc.y, 16);
+    if (hf == 0) {
+      part[warp * 32 + 2 * hl] = acc.x;
+      part[warp * 32 + 2 * hl + 1] = acc.y;
+    }
+    __syncthreads();
+    double mag = 0.0;
+    if (tid < 32 && tid < nr) {
+      const int q = r0 + tid;
+      double s2 = part[tid];
+      for (int w = 1; w < OP_WARPS; ++w) s2 += part[w * 32 + tid];
+      const double trace = trace1[q] + s2;
+      const double upd = (g[q] - trace) * a.gamma;
+      out[q] = __ldcg(in + q) + upd;
+      mag = fabs(upd);
+    }
+    if (warp == 0) {
+      mag = warp_nanmax(mag);
+      if (lane == 0) {
+        atomic_max_nonneg(&a.slots[idx % 3], mag);
+        if (blockIdx.x == 0) a.slots[(idx + 1) % 3] = 0ull;
+      }
+    }
+    grid.sync();
+    if (tid == 0) res_s = __longlong_as_double((long long)__ldcg(&a.slots[idx % 3]));
+    __syncthreads();
+    const double res = res_s;
+    const bool conv = res <= a.tol;
+    const bool last = conv || idx + 1 >= a.max_iter;
+    if (blockIdx.x == 0 && tid == 0) {
+      a.history[idx] = res;
+      a.st->iters = idx + 1;
+      a.st->last_res = res;
+      if (conv) a.st->done = 1;
+      else if (idx + 1 >= a.max_iter) a.st->done = 2;
+    }
+    if (last) break;
+  }
+}
+
 // Extraction writing the BvpSolution traces (u+, d_n u+) of a final field.
 template <typename T>
 __global__ void __launch_bounds__(256)

@@ -618,6 +618,7 @@ kfbi_status op_solve(kfbi_plan *p, const kfbi_bvp *b, cudaStream_t s) {
   }
   const int n = p->n_ctl;
   int rows = (n + sms - 1) / sms;
+  rows += rows & 1;                       // even: 16-byte row pairs (pair kernel)
   const int grid = (n + rows - 1) / rows;
   const size_t fixed = op_smem_fixed<T>(n);
   const size_t avail = (size_t)(smem_optin - 1024) > fixed ? (size_t)(smem_optin - 1024) - fixed : 0;
@@ -646,6 +647,23 @@ kfbi_status op_solve(kfbi_plan *p, const kfbi_bvp *b, cudaStream_t s) {
   const T *tr1 = reinterpret_cast<const T *>(p->trace1.p);
   const T *g = static_cast<const T *>(b->g);
   void *args[] = {&a, (void *)&Tcm, &A, &B, (void *)&phi0, (void *)&tr1, (void *)&g};
+  if constexpr (std::is_same<T, double>::value) {
+    // two rows per lane (16-byte pairs) when n and R are even
+    constexpr int K2 = K / 2;
+    if (n % 2 == 0 && rows % 2 == 0) {
+      static bool pair_attr = false;
+      if (!pair_attr) {
+        KFBI_CUDA(cudaFuncSetAttribute(op_solve_pair_kernel<K2>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin - 1024),
+                  "density-update");
+        pair_attr = true;
+      }
+      return launch(p, KFBI_K_DENSITY, s, [&] {
+        return cudaLaunchCooperativeKernel((const void *)op_solve_pair_kernel<K2>, dim3(grid),
+                                           dim3(OP_THREADS), args, smem, s);
+      });
+    }
+  }
   return launch(p, KFBI_K_DENSITY, s, [&] {
     cudaLaunchCooperativeKernel((const void *)op_solve_kernel<T, K>, dim3(grid), dim3(OP_THREADS), args,
                                 smem, s);
