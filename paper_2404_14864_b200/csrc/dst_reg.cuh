@@ -235,7 +235,7 @@ KFBI_DEV void powers(double2 w1, double2 (&w)[R]) {
 
 // One Stockham pass: radix R, current span NS; thread t holds inputs
 // v[m] = x[t + m T]; writes the pass output to sm (swizzled).
-template <int LOGN, int R, int NS>
+template <int LOGN, int R, int NS, int TWS = 1>
 KFBI_DEV void stockham_pass(double2 (&v)[E], const View<LOGN> &sm, int t,
                             const double2 *__restrict__ twg) {
   constexpr int N = 1 << LOGN;
@@ -250,7 +250,7 @@ KFBI_DEV void stockham_pass(double2 (&v)[E], const View<LOGN> &sm, int t,
     for (int s = 0; s < R; ++s) a[s] = v[i + s * B];
     if constexpr (NS > 1) {
       double2 w[R];
-      powers<R>(__ldg(&twg[k * (N / (NS * R))]), w);
+      powers<R>(__ldg(&twg[k * (N / (NS * R)) * TWS]), w);
 #pragma unroll
       for (int s = 1; s < R; ++s) a[s] = cmul(a[s], w[s]);
     }
@@ -261,28 +261,29 @@ KFBI_DEV void stockham_pass(double2 (&v)[E], const View<LOGN> &sm, int t,
   }
 }
 
-template <int LOGN, int PASS>
+// TWS: stride into the twiddle table (2 when the table is for length 2N)
+template <int LOGN, int PASS, int TWS = 1>
 KFBI_DEV void fft_passes(double2 (&v)[E], const View<LOGN> &sm, int t,
                          const double2 *__restrict__ twg) {
   using C = Cfg<LOGN>;
   constexpr int R = (PASS < C::P - 1) ? E : C::RLAST;
   constexpr int NS = 1 << (LE * PASS);
-  stockham_pass<LOGN, R, NS>(v, sm, t, twg);
+  stockham_pass<LOGN, R, NS, TWS>(v, sm, t, twg);
   if constexpr (PASS + 1 < C::P) {
     seq_sync<LOGN>();
 #pragma unroll
     for (int m = 0; m < E; ++m) v[m] = sm[t + m * C::T];
     seq_sync<LOGN>();
-    fft_passes<LOGN, PASS + 1>(v, sm, t, twg);
+    fft_passes<LOGN, PASS + 1, TWS>(v, sm, t, twg);
   }
 }
 
 // Z = FFT_N(y): y in registers (v[m] = y_{t + m T}), Z left in sm in natural
 // order.  All threads of the CTA must call it; sm must be free on entry.
 // Returns after a sequence barrier (Z visible to all threads).
-template <int LOGN>
+template <int LOGN, int TWS = 1>
 KFBI_DEV void fft(double2 (&v)[E], const View<LOGN> &sm, int t, const double2 *__restrict__ twg) {
-  fft_passes<LOGN, 0>(v, sm, t, twg);
+  fft_passes<LOGN, 0, TWS>(v, sm, t, twg);
   seq_sync<LOGN>();
 }
 

@@ -17,6 +17,7 @@
 #include "box_kernels.cuh"
 #include "box_reg.cuh"
 #include "box_neu.cuh"
+#include "box_real.cuh"
 #include "interface_kernels.cuh"
 #include "stepping_kernels.cuh"
 
@@ -326,10 +327,45 @@ kfbi_status box_reg_launch(kfbi_plan *p, const BoxArgs &a, const void *rhs, doub
   return KFBI_OK;
 }
 
+// Real data at M = 16384: one real row / column per CTA on the length-8192
+// complex engine (box_real.cuh) instead of packed pairs on a two-CTA cluster.
+template <int LOGN>
+kfbi_status box_real_launch(kfbi_plan *p, const BoxArgs &a, const void *rhs, double sign,
+                            const CorrArgs<double> &c, void *u, int passes, cudaStream_t s) {
+  constexpr int LOGL = LOGN - 1;
+  static bool attr = false;
+  if (!attr) {
+    const int bytes = (int)reg::smem_bytes<LOGL>();
+    KFBI_CUDA(cudaFuncSetAttribute(rows_fwd_real<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes),
+              "transform-rows");
+    KFBI_CUDA(cudaFuncSetAttribute(rows_inv_real<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes),
+              "transform-rows");
+    KFBI_CUDA(cudaFuncSetAttribute(cols_real<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes),
+              "transform-cols");
+    attr = true;
+  }
+  const size_t smem = reg::smem_bytes<LOGL>();
+  constexpr int CT = reg::Cfg<LOGL>::CTA_T;
+  if (passes & 1)
+    KFBI_TRY(launch(p, KFBI_K_ROWS, s, [&] {
+      rows_fwd_real<LOGN><<<a.rows, CT, smem, s>>>(a, static_cast<const double *>(rhs), sign, c);
+    }));
+  if (passes & 2)
+    KFBI_TRY(launch(p, KFBI_K_COLS, s, [&] { cols_real<LOGN><<<4 * a.npl, CT, smem, s>>>(a); }));
+  if (passes & 4)
+    KFBI_TRY(launch(p, KFBI_K_ROWS, s, [&] {
+      rows_inv_real<LOGN><<<a.rows, CT, smem, s>>>(a, static_cast<double *>(u));
+    }));
+  return KFBI_OK;
+}
+
 template <bool CPLX>
 kfbi_status box_passes_reg(kfbi_plan *p, const BoxArgs &a, const void *rhs, double sign,
                            const CorrArgs<typename std::conditional<CPLX, double2, double>::type> &c,
                            void *u, cudaStream_t s, int passes = 7) {
+  if constexpr (!CPLX) {
+    if (p->logm == 14) return box_real_launch<14>(p, a, rhs, sign, c, u, passes, s);
+  }
   switch (p->logm) {
 #define KFBI_CASE(L) \
     case L: return box_reg_launch<CPLX, L>(p, a, rhs, sign, c, u, passes, s);
