@@ -203,14 +203,26 @@ __global__ void __launch_bounds__(reg::Cfg<LOGN>::CTA_T, reg::Cfg<LOGN>::MINB) c
   }
   if (t == 0) out[0] = make_double2(0.0, 0.0);   // x_0 = 0 for the second transform
   reg::seq_sync<LOGN>();
-  unstage<LOGN>(sm, out, t);
-  reg::seq_sync<LOGN>();
-  dst_staged<LOGN>(sm, t, a, out);
-  reg::seq_sync<LOGN>();
-  unstage<LOGN>(sm, out, t);
-  reg::seq_sync<LOGN>();
-  if (valid)
-    for (int n = t; n < M; n += TT) at(n) = sm[n];
+  if constexpr (C::CL == 1 && TT >= 32) {
+    // second transform in transposed form: its input is the first one's
+    // output layout and its output the column's row layout
+    reg::dst_transposed<LOGN>(sm, t, out, v, a.twg, a.sinv);
+    if (valid)
+#pragma unroll
+      for (int m = 0; m < reg::E; ++m) {
+        const int n = t + m * TT;
+        if (n >= 1) at(n) = v[m];
+      }
+  } else {
+    unstage<LOGN>(sm, out, t);
+    reg::seq_sync<LOGN>();
+    dst_staged<LOGN>(sm, t, a, out);
+    reg::seq_sync<LOGN>();
+    unstage<LOGN>(sm, out, t);
+    reg::seq_sync<LOGN>();
+    if (valid)
+      for (int n = t; n < M; n += TT) at(n) = sm[n];
+  }
   if constexpr (C::CL > 1) reg::seq_sync<LOGN>();
 }
 

@@ -235,7 +235,7 @@ KFBI_DEV void powers(double2 w1, double2 (&w)[R]) {
 
 // One Stockham pass: radix R, current span NS; thread t holds inputs
 // v[m] = x[t + m T]; writes the pass output to sm (swizzled).
-template <int LOGN, int R, int NS, int TWS = 1>
+template <int LOGN, int R, int NS, int TWS = 1, bool KEEP = false>
 KFBI_DEV void stockham_pass(double2 (&v)[E], const View<LOGN> &sm, int t,
                             const double2 *__restrict__ twg) {
   constexpr int N = 1 << LOGN;
@@ -255,27 +255,41 @@ KFBI_DEV void stockham_pass(double2 (&v)[E], const View<LOGN> &sm, int t,
       for (int s = 1; s < R; ++s) a[s] = cmul(a[s], w[s]);
     }
     dft<R>(a);
-    const int base = (b - k) * R + k;
+    if constexpr (KEEP) {
+      // last pass (NS = N / R): output b + r NS = t + (i + r B) T stays in v
 #pragma unroll
-    for (int r = 0; r < R; ++r) sm[base + r * NS] = a[r];
+      for (int r = 0; r < R; ++r) v[i + r * B] = a[r];
+    } else {
+      const int base = (b - k) * R + k;
+#pragma unroll
+      for (int r = 0; r < R; ++r) sm[base + r * NS] = a[r];
+    }
   }
 }
 
 // TWS: stride into the twiddle table (2 when the table is for length 2N)
-template <int LOGN, int PASS, int TWS = 1>
+template <int LOGN, int PASS, int TWS = 1, bool KEEP = false>
 KFBI_DEV void fft_passes(double2 (&v)[E], const View<LOGN> &sm, int t,
                          const double2 *__restrict__ twg) {
   using C = Cfg<LOGN>;
   constexpr int R = (PASS < C::P - 1) ? E : C::RLAST;
   constexpr int NS = 1 << (LE * PASS);
-  stockham_pass<LOGN, R, NS, TWS>(v, sm, t, twg);
+  constexpr bool LASTKEEP = KEEP && PASS + 1 == C::P;
+  stockham_pass<LOGN, R, NS, TWS, LASTKEEP>(v, sm, t, twg);
   if constexpr (PASS + 1 < C::P) {
     seq_sync<LOGN>();
 #pragma unroll
     for (int m = 0; m < E; ++m) v[m] = sm[t + m * C::T];
     seq_sync<LOGN>();
-    fft_passes<LOGN, PASS + 1, TWS>(v, sm, t, twg);
+    fft_passes<LOGN, PASS + 1, TWS, KEEP>(v, sm, t, twg);
   }
+}
+
+// FFT with the result left in registers: v[m] = Z_{t + m T}.  Entry: v holds
+// the input in the same layout and sm is free.  Exit: sm may still be read.
+template <int LOGN>
+KFBI_DEV void fft_keep(double2 (&v)[E], const View<LOGN> &sm, int t, const double2 *__restrict__ twg) {
+  fft_passes<LOGN, 0, 1, true>(v, sm, t, twg);
 }
 
 // Z = FFT_N(y): y in registers (v[m] = y_{t + m T}), Z left in sm in natural
@@ -370,6 +384,88 @@ KFBI_DEV void post(const View<LOGN> &sm, int t, double2 (&out)[E],
   }
 #pragma unroll
   for (int c = 0; c < E / 2; ++c) out[2 * c + 1] = cadd(off, out[2 * c + 1]);
+}
+
+// DST-I as the transpose of the forward factorisation, C = P F Q^T (P, F and
+// the DST-I matrix are symmetric), for an input in the post-processing
+// layout w[c] = w_{16 t + c}: Q^T w is a suffix scan of the odd entries plus
+// +-i times the even ones, zeta_j = S_j + i w_2j, zeta_{N-j} = S_j - i w_2j,
+// zeta_0 = S_0, zeta_{N/2} = 0, S_j = sum_{k >= j} w_{2k+1}; then one FFT
+// kept in registers and the symmetric pre-matrix P applied with the mirror
+// values from shared memory.  Output v[m] = C_{t + m T} (C_0 = 0): the layout
+// of a column's rows, stored without a further exchange.  Saves the staging
+// pair reads and the output exchange of the forward form.  Entry: sm free
+// (after a barrier).  Exit: sm may still be read.
+template <int LOGN>
+KFBI_DEV void dst_transposed(const View<LOGN> &sm, int t, const double2 (&w)[E], double2 (&v)[E],
+                             const double2 *__restrict__ twg, const double *__restrict__ sinv) {
+  constexpr int N = 1 << LOGN;
+  constexpr int T = Cfg<LOGN>::T;
+  static_assert(T >= 32 && Cfg<LOGN>::CL == 1, "transposed DST: one-CTA sequences, T >= 32");
+  // suffix sums of the odd entries: within the thread, then across threads
+  double2 suf[E / 2];
+  double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+  for (int c = E / 2 - 1; c >= 0; --c) {
+    acc = cadd(acc, w[2 * c + 1]);
+    suf[c] = acc;
+  }
+  const int lane = threadIdx.x & 31;
+  double2 inc = acc;                            // inclusive suffix over lanes >= lane
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const double ux = __shfl_down_sync(0xffffffffu, inc.x, o);
+    const double uy = __shfl_down_sync(0xffffffffu, inc.y, o);
+    if (lane + o < 32) {
+      inc.x += ux;
+      inc.y += uy;
+    }
+  }
+  double2 off = make_double2(__shfl_down_sync(0xffffffffu, inc.x, 1),
+                             __shfl_down_sync(0xffffffffu, inc.y, 1));
+  if (lane == 31) off = make_double2(0.0, 0.0);
+  if constexpr (T > 32) {
+    constexpr int WPC = Cfg<LOGN>::CTA_T / 32;
+    const int warp = t >> 5;
+    const int lw0 = (threadIdx.x >> 5) - (warp % WPC);
+    if (lane == 0) sm.scr[0][lw0 + warp] = inc;
+    seq_sync<LOGN>();
+    double2 pw = make_double2(0.0, 0.0);
+    for (int x = T / 32 - 1; x > warp; --x) pw = cadd(pw, sm.scr[0][lw0 + x]);
+    off = cadd(pw, off);
+  }
+  // zeta into shared memory (natural order)
+#pragma unroll
+  for (int c = 0; c < E / 2; ++c) {
+    const int j = (E / 2) * t + c;
+    const double2 sj = cadd(off, suf[c]);
+    const double2 iw = make_double2(-w[2 * c].y, w[2 * c].x);
+    if (j == 0) {
+      sm[0] = sj;
+    } else {
+      sm[j] = cadd(sj, iw);
+      sm[N - j] = csub(sj, iw);
+    }
+  }
+  if (t == 0) sm[N / 2] = make_double2(0.0, 0.0);
+  seq_sync<LOGN>();
+#pragma unroll
+  for (int m = 0; m < E; ++m) v[m] = sm[t + m * T];
+  seq_sync<LOGN>();
+  fft_keep<LOGN>(v, sm, t, twg);
+  // P: C_j = s_j (Y_j + Y_{N-j}) + (Y_j - Y_{N-j}) / 2
+  seq_sync<LOGN>();
+#pragma unroll
+  for (int m = 0; m < E; ++m) sm[t + m * T] = v[m];
+  seq_sync<LOGN>();
+#pragma unroll
+  for (int m = 0; m < E; ++m) {
+    const int j = t + m * T;
+    const double2 yr = sm[(N - j) & (N - 1)];
+    const double s = __ldg(&sinv[j]);
+    const double2 a = cadd(v[m], yr), d = csub(v[m], yr);
+    v[m] = make_double2(fma(s, a.x, 0.5 * d.x), fma(s, a.y, 0.5 * d.y));
+  }
 }
 
 // Sum of v over the threads of the sequence, returned to every thread
