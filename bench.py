@@ -424,7 +424,7 @@ def run_c5(args):
     wsp = k.InterfaceWorkspace(geo, backend=k.CudaBackend(local, timing=False))
     sol = k.StaticPlaneWave(kappa=kappa)
     cps = wsp.cps
-    solver = D.SlabRichardson(wsp, nranks=ws, rank=rank)
+    solver = D.SlabRichardson(wsp, nranks=ws, rank=rank, p2p=args.p2p)
     r0, r1 = solver.rows
     X, Y = geo.grid.X[r0:r1], geo.grid.Y[r0:r1]
     F = torch.from_numpy(np.where(geo.classification.interior[r0:r1], sol.f(X, Y), 0.0)).cuda()
@@ -464,7 +464,11 @@ def run_c5(args):
         "data": "synthetic: StaticPlaneWave manufactured solution (no RNG)",
         "config": {"workload": f"C5: one KFBI solve per step, {m}x{m}, flower star, kappa={kappa}",
                    "grid": m, "parallelism": f"slab{ws}",
-                   "transport": "NCCL all_to_all_single + all_reduce" if ws > 1 else "none (1 rank)"},
+                   "transport": ("none (1 rank)" if ws == 1 else
+                                 "transposes fused into the passes (CUDA IPC peer stores + "
+                                 "peer-flag barrier) + NCCL all_reduce" if args.p2p else
+                                 "NCCL all_to_all_single + all_reduce"),
+                   "p2p": bool(args.p2p)},
         "iterations": it, "residual": res, "max_err_interior": err, "setup_s": setup_s,
         "n_ctl": int(cps.m),
     }
@@ -617,6 +621,8 @@ def main(argv=None):
     ap.add_argument("--profile", action="store_true",
                     help="bracket the headline loop with cudaProfilerStart/Stop (for ncu "
                          "--profile-from-start off launch lists of the timed region only)")
+    ap.add_argument("--p2p", action="store_true",
+                    help="c5: fuse the slab transposes into the passes (peer-memory stores)")
     ap.add_argument("--pipeline", action="store_true",
                     help="run every Richardson sweep through the full pipeline (no trace operator)")
     args = ap.parse_args(argv)

@@ -229,6 +229,42 @@ kfbi_status kfbi_slab_cols(kfbi_plan *plan, int32_t dtype, const kfbi_slab *slab
 kfbi_status kfbi_slab_rows_inv(kfbi_plan *plan, int32_t dtype, const kfbi_slab *slab,
                                const void *panels, void *u, void *stream);
 
+/* ---- slab passes with the all-to-all fused into the stores ----
+ * Each rank holds two panel buffers in peer-addressable device memory
+ * (kfbi_ipc_alloc; the handles are exchanged once and opened with
+ * kfbi_ipc_open, or plain pointers of one device for virtual ranks):
+ * A (column-pass input) and B (row-pass input).  One solve is
+ *   kfbi_slab_rows_fwd_p2p(peer_panels = every rank's A)  -> barrier ->
+ *   kfbi_slab_cols_p2p(panels = own A, peer_panels = every rank's B) ->
+ *   barrier -> kfbi_slab_rows_inv(panels = own B)
+ * The forward row pass writes panel chunk h of its rows directly into rank
+ * h's A at the offset the all-to-all would have put it, and the column pass
+ * writes row chunk h of its panels into rank h's B: the exchange overlaps
+ * the transforms tile by tile and no separate collective runs.  The barrier
+ * is kfbi_p2p_barrier over per-rank flag arrays (KFBI_MAX_PEERS uint64 each,
+ * zero-initialised, epochs strictly increasing per call) or any stream-
+ * ordered collective.  Results are bit-identical to the all-to-all form. */
+#define KFBI_MAX_PEERS 8
+#define KFBI_IPC_HANDLE_BYTES 64
+
+kfbi_status kfbi_slab_rows_fwd_p2p(kfbi_plan *plan, int32_t dtype, const kfbi_slab *slab,
+                                   const void *rhs, double sign, const void *jv,
+                                   void *const *peer_panels, void *stream);
+kfbi_status kfbi_slab_cols_p2p(kfbi_plan *plan, int32_t dtype, const kfbi_slab *slab,
+                               double kappa_re, double kappa_im, const void *panels,
+                               void *const *peer_panels, void *stream);
+/* cudaMalloc'd, zeroed buffer + its IPC handle (KFBI_IPC_HANDLE_BYTES). */
+kfbi_status kfbi_ipc_alloc(int64_t bytes, void **ptr, void *handle);
+kfbi_status kfbi_ipc_free(void *ptr);
+kfbi_status kfbi_ipc_open(const void *handle, void **ptr);
+kfbi_status kfbi_ipc_close(void *ptr);
+/* Stream-ordered barrier of `nranks` ranks over peer flag arrays; after
+ * max_spins polls (<= 0: 2^28, tens of seconds) without every peer it gives
+ * up and sets *timed_out (device int, may be NULL) to 1 instead of hanging. */
+kfbi_status kfbi_p2p_barrier(void *const *peer_flags, int32_t nranks, int32_t rank,
+                             int64_t epoch, int64_t max_spins, int32_t *timed_out,
+                             void *stream);
+
 /* ---- slab-decomposed Richardson sweep (dist.py SlabRichardson) ----
  * Per sweep on every rank: kfbi_jumps (replicated, O(n_ctl)) ->
  * kfbi_edge_values (jv = W . JM, replicated) -> kfbi_slab_rows_fwd (with jv:

@@ -118,6 +118,13 @@ _SIGNATURES = {
     "kfbi_slab_rows_fwd": ([vp, i32, vp, vp, f64, vp, vp, vp], i32),
     "kfbi_slab_cols": ([vp, i32, vp, f64, f64, vp, vp], i32),
     "kfbi_slab_rows_inv": ([vp, i32, vp, vp, vp, vp], i32),
+    "kfbi_slab_rows_fwd_p2p": ([vp, i32, vp, vp, f64, vp, vp, vp], i32),
+    "kfbi_slab_cols_p2p": ([vp, i32, vp, f64, f64, vp, vp, vp], i32),
+    "kfbi_ipc_alloc": ([i64, C.POINTER(vp), vp], i32),
+    "kfbi_ipc_free": ([vp], i32),
+    "kfbi_ipc_open": ([vp, C.POINTER(vp)], i32),
+    "kfbi_ipc_close": ([vp], i32),
+    "kfbi_p2p_barrier": ([vp, i32, i32, i64, i64, vp, vp], i32),
     "kfbi_kernel_times": ([vp, C.POINTER(f64), C.POINTER(i64)], i32),
     "kfbi_reset_kernel_times": ([vp], i32),
     "kfbi_set_timing": ([vp, i32], i32),

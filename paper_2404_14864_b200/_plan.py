@@ -23,6 +23,16 @@ def _c(a, dtype):
     return np.ascontiguousarray(a, dtype=dtype)
 
 
+def _addr(x):
+    """Device address of a tensor or a raw integer pointer."""
+    return int(x) if isinstance(x, int) else x.data_ptr()
+
+
+def _ptr_table(bufs):
+    """C array of device addresses (tensors or raw integer pointers)."""
+    return (C.c_void_p * len(bufs))(*[_addr(b) for b in bufs])
+
+
 class Plan:
     def __init__(self, m, h, backend):
         self.m = int(m)
@@ -142,7 +152,30 @@ class Plan:
     def slab_rows_inv(self, cplx, nranks, rank, panels, u):
         sl = N.Slab(int(nranks), int(rank))
         N.check(self._lib.kfbi_slab_rows_inv(self.handle, self._dt(cplx), C.byref(sl),
-                                             panels.data_ptr(), u.data_ptr(), self.stream))
+                                             _addr(panels), u.data_ptr(), self.stream))
+
+    def slab_rows_fwd_p2p(self, cplx, nranks, rank, rhs, peers, sign=1.0, jv=None):
+        """Forward row pass storing panel chunk h into peers[h] (rank h's
+        column-pass buffer): the first all-to-all fused into the stores."""
+        sl = N.Slab(int(nranks), int(rank))
+        tab = _ptr_table(peers)
+        N.check(self._lib.kfbi_slab_rows_fwd_p2p(self.handle, self._dt(cplx), C.byref(sl),
+                                                 N.ptr(rhs), float(sign), N.ptr(jv), tab,
+                                                 self.stream))
+
+    def slab_cols_p2p(self, cplx, nranks, rank, kappa, panels, peers):
+        """Column pass on the own buffer, storing row chunk h into peers[h]
+        (rank h's row-pass buffer): the second all-to-all fused."""
+        k = complex(kappa)
+        sl = N.Slab(int(nranks), int(rank))
+        tab = _ptr_table(peers)
+        N.check(self._lib.kfbi_slab_cols_p2p(self.handle, self._dt(cplx), C.byref(sl), k.real,
+                                             k.imag, _addr(panels), tab, self.stream))
+
+    def p2p_barrier(self, flags, nranks, rank, epoch, timed_out=None, max_spins=0):
+        tab = _ptr_table(flags)
+        N.check(self._lib.kfbi_p2p_barrier(tab, int(nranks), int(rank), int(epoch),
+                                           int(max_spins), N.ptr(timed_out), self.stream))
 
     # -- slab-decomposed Richardson sweep (dist.py) -------------------------------
     def edge_values(self, jm, jv):

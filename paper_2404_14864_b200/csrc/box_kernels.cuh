@@ -22,7 +22,22 @@ struct BoxArgs {
   // [pp0, pp0 + npl) of every row, received as nranks blocks [rank][npl][rows][w].
   int rows, row0, pp0, npl;
   int ring_end;           // the field array also holds row m (zero ring)
+  // Transposes fused into the stores (slab_*_p2p): when dst[0] != null the
+  // forward row pass writes each panel chunk straight into the column-pass
+  // buffer of the panel's owner, and the column pass writes each row chunk
+  // into the row-pass buffer of the row's owner (peer device memory over
+  // NVLink, or other buffers of the same device); no all-to-all follows.
+  int nranks, rank;
+  void *dst[8];
 };
+
+// Destination of panel-row element (panel pp, slab row r, half w) written by
+// the forward row pass: own buffer [pp][R] or the owner's [rank][pl][R].
+KFBI_DEV double2 *rows_fwd_dst(const BoxArgs &a, int pp, int r, int w) {
+  if (!a.dst[0]) return static_cast<double2 *>(a.panels) + ((size_t)pp * a.rows + r) * 2 + w;
+  const int h = pp / a.npl, pl = pp - h * a.npl;
+  return static_cast<double2 *>(a.dst[h]) + (((size_t)a.rank * a.npl + pl) * a.rows + r) * 2 + w;
+}
 
 // Sparse right-hand-side corrections fused into the forward row pass.
 template <typename T>
@@ -62,3 +77,34 @@ __global__ void scatter_groups_kernel(CorrArgs<T> c, int n_groups, T *out) {
 }
 
 }  // namespace kfbi
+
+// ---------------------------------------------------------------------------
+// Peer-flag barrier between the fused slab passes (kfbi_p2p_barrier): rank r
+// publishes `epoch` into slot r of every rank's flag array (system-scope
+// release over NVLink), then waits until every slot of its own array holds
+// at least `epoch` (acquire).  One warp; lane h talks to rank h.  The spin is
+// bounded (max_spins polls): a missing peer sets *timed_out instead of hanging.
+struct P2pFlags {
+  unsigned long long *flags[8];
+};
+
+__global__ void p2p_barrier_kernel(P2pFlags f, int nranks, int rank, unsigned long long epoch,
+                                   long long max_spins, int *timed_out) {
+  const int h = threadIdx.x;
+  if (h >= nranks) return;
+  __threadfence_system();
+  unsigned long long *slot = f.flags[h] + rank;
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(slot), "l"(epoch) : "memory");
+  const unsigned long long *mine = f.flags[rank] + h;
+  for (long long it = 0;; ++it) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(mine) : "memory");
+    if (v >= epoch) break;
+    if (it >= max_spins) {
+      if (timed_out) atomicExch(timed_out, 1);
+      break;
+    }
+    __nanosleep(64);
+  }
+  __threadfence_system();
+}

@@ -144,9 +144,7 @@ rows_fwd_real(BoxArgs a, const double *__restrict__ rhs, double sign, CorrArgs<d
   unstage<LOGL>(sm, out, t);
   reg::seq_sync<LOGL>();
   // panel pp = slots 2pp, 2pp+1 of this row: 32 bytes
-  double2 *P2 = static_cast<double2 *>(a.panels);
-  const size_t R = a.rows;
-  for (int i = t; i < L; i += TT) P2[((size_t)(i >> 1) * R + r0) * 2 + (i & 1)] = sm[i];
+  for (int i = t; i < L; i += TT) *rows_fwd_dst(a, i >> 1, r0, i & 1) = sm[i];
 }
 
 // ---------------------------------------------------------------------------
@@ -194,10 +192,15 @@ __global__ void __launch_bounds__(reg::Cfg<LOGN - 1>::CTA_T, 1) cols_real(BoxArg
   reg::seq_sync<LOGL>();
   unstage<LOGL>(sm, out, t);
   reg::seq_sync<LOGL>();
+  // result element jj: in place, or into the row-pass buffer of its owner
+  auto out_at = [&](int jj) -> double & {
+    if (!a.dst[0]) return at(jj);
+    return static_cast<double *>(a.dst[jj >> lr])[((size_t)(a.pp0 + pl) * a.rows + (jj & (a.rows - 1))) * 4 + w];
+  };
   for (int qq = t; qq < M / 2; qq += TT) {
     const double2 s2 = sm[qq];
-    at(2 * qq) = s2.x;
-    at(2 * qq + 1) = s2.y;
+    out_at(2 * qq) = s2.x;
+    out_at(2 * qq + 1) = s2.y;
   }
 }
 

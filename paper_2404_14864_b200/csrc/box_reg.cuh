@@ -134,19 +134,17 @@ rows_fwd_reg(BoxArgs a, const void *__restrict__ rhs, double sign,
   if (valid) {
     // panel stores: consecutive lanes write consecutive 16-byte pieces of a
     // panel's (row j0, row j0+1) 64-byte chunk (real) / 32-byte row (complex)
-    double2 *P2 = static_cast<double2 *>(a.panels);
-    const size_t R = a.rows;
     if (!CPLX) {
       for (int i = t; i < M; i += TT) {          // M/4 panels x 4 pieces
         const int pp = i >> 2, part = i & 3, row = part >> 1;
         const int n0 = 4 * pp + 2 * (part & 1);
         const double2 v0 = sm[n0], v1 = sm[n0 + 1];
-        P2[(pp * R + r0 + row) * 2 + (part & 1)] =
+        *rows_fwd_dst(a, pp, r0 + row, part & 1) =
             row ? make_double2(v0.y, v1.y) : make_double2(v0.x, v1.x);
       }
     } else {
       for (int i = t; i < M; i += TT)            // M/2 panels x 2 pieces
-        P2[((i >> 1) * R + r0) * 2 + (i & 1)] = sm[i];
+        *rows_fwd_dst(a, i >> 1, r0, i & 1) = sm[i];
     }
   }
   if constexpr (C::CL > 1) reg::seq_sync<LOGN>();   // keep the cluster's smem alive
@@ -172,6 +170,11 @@ __global__ void __launch_bounds__(reg::Cfg<LOGN>::CTA_T, reg::Cfg<LOGN>::MINB) c
   auto at = [&](int j) -> double2 & {
     const size_t blk = (size_t)(j >> lr) * a.npl + pl;
     return P2[(blk * a.rows + (j & (a.rows - 1))) * 2 + half];
+  };
+  // result element j: in place, or into the row-pass buffer of row j's owner
+  auto out_at = [&](int j) -> double2 & {
+    if (!a.dst[0]) return at(j);
+    return static_cast<double2 *>(a.dst[j >> lr])[((size_t)pp * a.rows + (j & (a.rows - 1))) * 2 + half];
   };
 
   double2 v[reg::E];
@@ -211,7 +214,7 @@ __global__ void __launch_bounds__(reg::Cfg<LOGN>::CTA_T, reg::Cfg<LOGN>::MINB) c
 #pragma unroll
       for (int m = 0; m < reg::E; ++m) {
         const int n = t + m * TT;
-        if (n >= 1) at(n) = v[m];
+        out_at(n) = n >= 1 ? v[m] : make_double2(0.0, 0.0);   // row 0: zero ring
       }
   } else {
     unstage<LOGN>(sm, out, t);
@@ -221,7 +224,7 @@ __global__ void __launch_bounds__(reg::Cfg<LOGN>::CTA_T, reg::Cfg<LOGN>::MINB) c
     unstage<LOGN>(sm, out, t);
     reg::seq_sync<LOGN>();
     if (valid)
-      for (int n = t; n < M; n += TT) at(n) = sm[n];
+      for (int n = t; n < M; n += TT) out_at(n) = sm[n];
   }
   if constexpr (C::CL > 1) reg::seq_sync<LOGN>();
 }

@@ -208,6 +208,9 @@ BoxArgs box_args(kfbi_plan *p, double kre, double kim, const int *done) {
   a.pp0 = 0;
   a.npl = 0;                 // set per dtype by the launcher
   a.ring_end = 1;
+  a.nranks = 1;
+  a.rank = 0;
+  for (int h = 0; h < 8; ++h) a.dst[h] = nullptr;
   return a;
 }
 
@@ -224,6 +227,8 @@ kfbi_status slab_args(kfbi_plan *p, bool cplx, int nranks, int rank, BoxArgs &a)
   a.npl = npanels / nranks;
   a.pp0 = rank * a.npl;
   a.ring_end = 0;
+  a.nranks = nranks;
+  a.rank = rank;
   return KFBI_OK;
 }
 
@@ -390,17 +395,26 @@ kfbi_status box_passes(kfbi_plan *p, double kre, double kim, const void *rhs, do
 }
 
 // One pass of the slab-decomposed box solve (kfbi_slab_*).
+// peers != nullptr: the pass stores its output straight into peers[h], the
+// buffer of rank h (the all-to-all fused into the stores).
 kfbi_status slab_pass(kfbi_plan *p, int32_t dtype, const kfbi_slab *sl, int passes, double kre,
                       double kim, const void *rhs, double sign, const void *jv, void *panels,
-                      void *u, void *stream) {
+                      void *u, void *stream, void *const *peers = nullptr) {
   KFBI_TRY(check_plan(p));
-  if (!sl || !panels) return fail(KFBI_E_CONFIG, "slab: null argument");
+  if (!sl || (!panels && !(passes == 1 && peers))) return fail(KFBI_E_CONFIG, "slab: null argument");
   const bool cplx = dtype == KFBI_C128;
   if (!cplx && kim != 0.0) return fail(KFBI_E_CONFIG, "complex kappa requires the c128 path");
   if (jv && !p->has_geo) return fail(KFBI_E_CONFIG, "slab: corrections need the plan's geometry");
   BoxArgs a = box_args(p, kre, kim, nullptr);
   KFBI_TRY(slab_args(p, cplx, sl->nranks, sl->rank, a));
   a.panels = panels;
+  if (peers) {
+    if (sl->nranks > KFBI_MAX_PEERS) return fail(KFBI_E_CONFIG, "slab p2p: at most 8 ranks");
+    for (int h = 0; h < sl->nranks; ++h) {
+      if (!peers[h]) return fail(KFBI_E_CONFIG, "slab p2p: null peer buffer");
+      a.dst[h] = peers[h];
+    }
+  }
   cudaStream_t s = (cudaStream_t)stream;
   if (cplx) {
     CorrArgs<double2> c = corr_args<double2>(p, static_cast<const double2 *>(jv));
@@ -802,6 +816,68 @@ kfbi_status kfbi_slab_rows_inv(kfbi_plan *p, int32_t dtype, const kfbi_slab *sl,
                                void *u, void *stream) {
   return slab_pass(p, dtype, sl, 4, 0.0, 0.0, nullptr, 1.0, nullptr, const_cast<void *>(panels), u,
                    stream);
+}
+
+kfbi_status kfbi_slab_rows_fwd_p2p(kfbi_plan *p, int32_t dtype, const kfbi_slab *sl, const void *rhs,
+                                   double sign, const void *jv, void *const *peer_panels,
+                                   void *stream) {
+  if (!peer_panels) return fail(KFBI_E_CONFIG, "slab p2p: null peer table");
+  return slab_pass(p, dtype, sl, 1, 0.0, 0.0, rhs, sign, jv, nullptr, nullptr, stream, peer_panels);
+}
+
+kfbi_status kfbi_slab_cols_p2p(kfbi_plan *p, int32_t dtype, const kfbi_slab *sl, double kappa_re,
+                               double kappa_im, const void *panels, void *const *peer_panels,
+                               void *stream) {
+  if (!peer_panels) return fail(KFBI_E_CONFIG, "slab p2p: null peer table");
+  return slab_pass(p, dtype, sl, 2, kappa_re, kappa_im, nullptr, 1.0, nullptr,
+                   const_cast<void *>(panels), nullptr, stream, peer_panels);
+}
+
+// ---- peer memory (CUDA IPC) and the peer-flag barrier ----
+
+kfbi_status kfbi_ipc_alloc(int64_t bytes, void **ptr, void *handle) {
+  if (!ptr || !handle || bytes <= 0) return fail(KFBI_E_CONFIG, "ipc: bad argument");
+  KFBI_CUDA(cudaMalloc(ptr, (size_t)bytes), "ipc-alloc");
+  KFBI_CUDA(cudaMemset(*ptr, 0, (size_t)bytes), "ipc-alloc");
+  cudaIpcMemHandle_t h;
+  KFBI_CUDA(cudaIpcGetMemHandle(&h, *ptr), "ipc-alloc");
+  static_assert(sizeof(h) == KFBI_IPC_HANDLE_BYTES, "IPC handle size");
+  std::memcpy(handle, &h, sizeof(h));
+  return KFBI_OK;
+}
+
+kfbi_status kfbi_ipc_free(void *ptr) {
+  if (ptr) KFBI_CUDA(cudaFree(ptr), "ipc-free");
+  return KFBI_OK;
+}
+
+kfbi_status kfbi_ipc_open(const void *handle, void **ptr) {
+  if (!ptr || !handle) return fail(KFBI_E_CONFIG, "ipc: bad argument");
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, sizeof(h));
+  KFBI_CUDA(cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess), "ipc-open");
+  return KFBI_OK;
+}
+
+kfbi_status kfbi_ipc_close(void *ptr) {
+  if (ptr) KFBI_CUDA(cudaIpcCloseMemHandle(ptr), "ipc-close");
+  return KFBI_OK;
+}
+
+kfbi_status kfbi_p2p_barrier(void *const *peer_flags, int32_t nranks, int32_t rank, int64_t epoch,
+                             int64_t max_spins, int32_t *timed_out, void *stream) {
+  if (!peer_flags || nranks < 1 || nranks > KFBI_MAX_PEERS || rank < 0 || rank >= nranks || epoch < 1)
+    return fail(KFBI_E_CONFIG, "p2p barrier: bad argument");
+  P2pFlags f;
+  for (int h = 0; h < KFBI_MAX_PEERS; ++h) f.flags[h] = h < nranks ? (unsigned long long *)peer_flags[h] : nullptr;
+  for (int h = 0; h < nranks; ++h)
+    if (!f.flags[h]) return fail(KFBI_E_CONFIG, "p2p barrier: null flag buffer");
+  p2p_barrier_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(f, nranks, rank,
+                                                          (unsigned long long)epoch,
+                                                          max_spins > 0 ? (long long)max_spins : (1ll << 28),
+                                                          timed_out);
+  KFBI_CUDA(cudaGetLastError(), "p2p-barrier");
+  return KFBI_OK;
 }
 
 // ---- slab-decomposed Richardson sweep (dist.py SlabRichardson) ----

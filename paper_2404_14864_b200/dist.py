@@ -17,6 +17,13 @@ kernels, the collective is ``torch.distributed.all_to_all_single`` over NCCL
 (NVLink / NVSwitch).  With P = 1 the exchanges are identities and the solve
 is bit-identical to BoxSolver.solve.
 
+With ``p2p=True`` the two all-to-alls are fused into the transforms: the
+forward row pass stores each panel chunk straight into the owning rank's
+column-pass buffer and the column pass stores each row chunk into the owning
+rank's row-pass buffer (device memory of the peers, mapped once with CUDA
+IPC), with a peer-flag barrier kernel between the passes instead of a
+collective.  The exchange then overlaps the transforms tile by tile.
+
 ``solve_virtual`` runs P slabs one after the other on one GPU with the
 exchange done by device copies: the same kernels and layouts, used to
 validate the decomposition where only one GPU is available.
@@ -57,14 +64,126 @@ def exchange_chunks(dst, src, nranks, group=None):
     return dst
 
 
+class PeerBuffers:
+    """One device buffer per rank, addressable by every rank: allocated with
+    kfbi_ipc_alloc, handles exchanged once (all_gather_object) and opened with
+    kfbi_ipc_open.  ``ptrs[h]`` is rank h's buffer in this process."""
+
+    def __init__(self, nbytes, nranks, rank, group=None):
+        import ctypes as C
+
+        from . import _native as N
+
+        self._lib = N.lib()
+        self.nranks, self.rank = nranks, rank
+        own = C.c_void_p()
+        handle = (C.c_char * 64)()
+        N.check(self._lib.kfbi_ipc_alloc(int(nbytes), C.byref(own), handle))
+        self.own = int(own.value)
+        self._opened = []
+        if nranks == 1:
+            self.ptrs = [self.own]
+            return
+        dist = _dist()
+        if dist is None:
+            raise ConfigError("p2p slab solve with nranks > 1 needs an initialised torch.distributed")
+        handles = [None] * nranks
+        dist.all_gather_object(handles, bytes(handle), group=group)
+        self.ptrs = []
+        for h, hb in enumerate(handles):
+            if h == rank:
+                self.ptrs.append(self.own)
+                continue
+            q = C.c_void_p()
+            N.check(self._lib.kfbi_ipc_open(C.create_string_buffer(hb, 64), C.byref(q)))
+            self._opened.append(int(q.value))
+            self.ptrs.append(int(q.value))
+
+    def close(self):
+        for q in self._opened:
+            self._lib.kfbi_ipc_close(q)
+        self._opened = []
+        if self.own:
+            self._lib.kfbi_ipc_free(self.own)
+            self.own = 0
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # pragma: no cover - interpreter shutdown
+            pass
+
+
+class SlabPasses:
+    """The three box-solve passes of one rank with the two transposes
+    between them: NCCL all-to-alls (default) or, with p2p=True, fused into
+    the pass stores over CUDA-IPC peer buffers with a peer-flag barrier
+    kernel between the passes.  Buffers are allocated on first use per dtype
+    (the p2p ones collectively: every rank must make its first call)."""
+
+    def __init__(self, plan, nranks, rank, group=None, device=None, p2p=False):
+        self.plan, self.nranks, self.rank, self.group = plan, nranks, rank, group
+        self.device = device
+        self.p2p = bool(p2p)
+        self._bufs = {}
+        self._epoch = 0
+        self._timed_out = None
+
+    def _buffers(self, cplx):
+        import torch
+
+        key = bool(cplx)
+        if key not in self._bufs:
+            nbytes = self.plan.slab_panel_bytes(cplx, self.nranks)
+            P, g = self.nranks, self.rank
+            if self.p2p:
+                self._bufs[key] = (PeerBuffers(nbytes, P, g, self.group),
+                                   PeerBuffers(nbytes, P, g, self.group),
+                                   PeerBuffers(8 * 8, P, g, self.group))
+                if self._timed_out is None:
+                    self._timed_out = torch.zeros(1, dtype=torch.int32, device=self.device)
+            else:
+                mk = lambda: torch.empty(nbytes // 8, dtype=torch.float64, device=self.device)
+                self._bufs[key] = (mk(), mk() if P > 1 else None)
+        return self._bufs[key]
+
+    def _barrier(self, flags):
+        self._epoch += 1
+        self.plan.p2p_barrier(flags.ptrs, self.nranks, self.rank, self._epoch, self._timed_out)
+
+    def peers_ok(self):
+        """False if a p2p barrier ever gave up waiting for a peer (syncs)."""
+        return self._timed_out is None or int(self._timed_out.item()) == 0
+
+    def run(self, cplx, kappa, rhs, u, sign=1.0, jv=None):
+        """u (this rank's rows) = box solve of sign * rhs (+ corrections of jv)."""
+        p, P, g = self.plan, self.nranks, self.rank
+        if self.p2p:
+            A, B, F = self._buffers(cplx)
+            p.slab_rows_fwd_p2p(cplx, P, g, rhs, A.ptrs, sign=sign, jv=jv)
+            self._barrier(F)
+            p.slab_cols_p2p(cplx, P, g, kappa, A.own, B.ptrs)
+            self._barrier(F)
+            p.slab_rows_inv(cplx, P, g, B.own, u)
+            return u
+        a, b = self._buffers(cplx)
+        p.slab_rows_fwd(cplx, P, g, rhs, a, sign=sign, jv=jv)
+        t = exchange_chunks(b, a, P, self.group)
+        p.slab_cols(cplx, P, g, kappa, t)
+        t = exchange_chunks(a, t, P, self.group)
+        p.slab_rows_inv(cplx, P, g, t, u)
+        return u
+
+
 class SlabBoxSolver:
     """Slab-decomposed BoxSolver (dirichlet-zero) for the calling rank.
 
     rhs / u are this rank's rows ``slab_rows(m, nranks, rank)`` as CUDA
-    tensors of shape (rows, m + 1), float64 or complex128."""
+    tensors of shape (rows, m + 1), float64 or complex128.  p2p=True fuses
+    the transposes into the passes (SlabPasses)."""
 
     def __init__(self, grid, kappa, bc="dirichlet-zero", nranks=None, rank=None, group=None,
-                 backend=None):
+                 backend=None, p2p=False):
         _validate(bc, kappa)
         if bc != "dirichlet-zero":
             raise ConfigError("the slab-decomposed box solve supports the dirichlet-zero closure")
@@ -79,17 +198,11 @@ class SlabBoxSolver:
         self.backend = make_backend(backend) if backend is not None else default_backend()
         self.plan = _grid_plan(grid, self.backend)
         self.rows = slab_rows(grid.m, self.nranks, self.rank)
-        self._bufs = {}
+        self.passes = SlabPasses(self.plan, self.nranks, self.rank, group,
+                                 self.backend.torch_device, p2p)
 
-    def _panels(self, cplx):
-        import torch
-
-        key = bool(cplx)
-        if key not in self._bufs:
-            nbytes = self.plan.slab_panel_bytes(cplx, self.nranks)
-            mk = lambda: torch.empty(nbytes // 8, dtype=torch.float64, device=self.backend.torch_device)
-            self._bufs[key] = (mk(), mk() if self.nranks > 1 else None)
-        return self._bufs[key]
+    def peers_ok(self):
+        return self.passes.peers_ok()
 
     def solve(self, rhs):
         import torch
@@ -101,21 +214,15 @@ class SlabBoxSolver:
         cplx = rhs.is_complex() or isinstance(self.kappa, complex)
         dt = torch.complex128 if cplx else torch.float64
         rhs = rhs.to(dt).contiguous()
-        a, b = self._panels(cplx)
         u = torch.empty_like(rhs)
-        p, P, g = self.plan, self.nranks, self.rank
-        p.slab_rows_fwd(cplx, P, g, rhs, a)
-        t = exchange_chunks(b, a, P, self.group)
-        p.slab_cols(cplx, P, g, self.kappa, t)
-        t = exchange_chunks(a, t, P, self.group)
-        p.slab_rows_inv(cplx, P, g, t, u)
-        return u
+        return self.passes.run(cplx, self.kappa, rhs, u)
 
 
-def solve_virtual(grid, kappa, rhs, nranks, backend=None):
+def solve_virtual(grid, kappa, rhs, nranks, backend=None, p2p=False):
     """The P-slab solve of a full (m+1)^2 rhs on ONE device: every rank's
-    passes run in turn and the all-to-alls are chunk copies.  Returns the full
-    solution (row m = zero ring)."""
+    passes run in turn and the all-to-alls are chunk copies (p2p=True: the
+    fused passes store into the other virtual ranks' buffers directly).
+    Returns the full solution (row m = zero ring)."""
     import torch
 
     m = grid.m
@@ -135,6 +242,23 @@ def solve_virtual(grid, kappa, rhs, nranks, backend=None):
         for g in range(nranks):
             for h in range(nranks):
                 dst[g][h * c:(h + 1) * c].copy_(src[h][g * c:(g + 1) * c])
+
+    if p2p:
+        send.clear()
+        send.extend(torch.full_like(x, float("nan")) for x in recv)
+        recv[:] = [torch.full_like(x, float("nan")) for x in recv]
+        for g, s in enumerate(solvers):
+            r0, r1 = s.rows
+            plan.slab_rows_fwd_p2p(cplx, nranks, g, rhs[r0:r1].contiguous(), recv)
+        for g, s in enumerate(solvers):
+            plan.slab_cols_p2p(cplx, nranks, g, s.kappa, recv[g], send)
+        u = torch.zeros((m + 1, m + 1), dtype=dt, device=dev)
+        for g, s in enumerate(solvers):
+            r0, r1 = s.rows
+            out = torch.empty((r1 - r0, m + 1), dtype=dt, device=dev)
+            plan.slab_rows_inv(cplx, nranks, g, send[g], out)
+            u[r0:r1] = out
+        return u
 
     for g, s in enumerate(solvers):
         r0, r1 = s.rows
@@ -191,13 +315,15 @@ class SlabRichardson:
     13 n_ctl stencil values (include/kfbi_b200.h, kfbi_slab_*).  The field,
     density and iteration counts are bit-identical to the one-GPU solve."""
 
-    def __init__(self, workspace, nranks=None, rank=None, group=None):
+    def __init__(self, workspace, nranks=None, rank=None, group=None, p2p=False):
         dist = _dist()
         self.ws = workspace
         self.nranks = int(nranks if nranks is not None else (dist.get_world_size(group) if dist else 1))
         self.rank = int(rank if rank is not None else (dist.get_rank(group) if dist else 0))
         self.group = group
         self.rows = slab_rows(workspace.grid.m, self.nranks, self.rank)
+        self.passes = SlabPasses(workspace.plan, self.nranks, self.rank, group,
+                                 workspace.backend.torch_device, p2p)
 
     def solve(self, *, kappa, F, f_gamma, g, density, F_sign=1.0, f_gamma_sign=1.0, gamma=0.8,
               tol=1e-8, max_iter=200, bc_kind="dirichlet"):
@@ -224,20 +350,13 @@ class SlabRichardson:
         tu = torch.empty(n, dtype=dt, device=dev)
         tn = torch.empty_like(tu)
         u = torch.empty_like(F)
-        nbytes = plan.slab_panel_bytes(cplx, P)
-        a = torch.empty(nbytes // 8, dtype=torch.float64, device=dev)
-        b = torch.empty_like(a) if P > 1 else None
         plan.rich_begin(max_iter, tol)
         it = done = 0
         res, hist = 0.0, []
         for _ in range(max_iter):
             plan.jumps(kappa, density, None, f_gamma, jm, f_gamma_sign)
             plan.edge_values(jm, jv)
-            plan.slab_rows_fwd(cplx, P, r, F, a, sign=F_sign, jv=jv)
-            t = exchange_chunks(b, a, P, self.group)
-            plan.slab_cols(cplx, P, r, kappa, t)
-            t = exchange_chunks(a, t, P, self.group)
-            plan.slab_rows_inv(cplx, P, r, t, u)
+            self.passes.run(cplx, kappa, F, u, sign=F_sign, jv=jv)
             plan.slab_stencil_values(bc_kind, P, r, u, vals)
             _allreduce_sum(vals, P, self.group)
             plan.slab_update(bc_kind, vals, jm, g, density, tu, tn, gamma)

@@ -52,6 +52,9 @@ def test_virtual_slabs_bit_identical(m, cplx):
     for p in (1, 2, 4, 8):
         u = D.solve_virtual(grid, kappa, rhs, p)
         assert torch.equal(u, ref), (p, float((u - ref).abs().max()))
+        # the all-to-alls fused into the pass stores (peer-buffer addressing)
+        u = D.solve_virtual(grid, kappa, rhs, p, p2p=True)
+        assert torch.equal(u, ref), ("p2p", p, float((u - ref).abs().max()))
 
 
 @pytest.mark.gpu
@@ -71,6 +74,59 @@ def test_slab_solver_single_rank_and_oracle():
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("cplx", [False, True])
+def test_p2p_slab_solver_single_rank(cplx):
+    """SlabBoxSolver(p2p=True) at P = 1: IPC-allocated buffers, the fused
+    passes and the peer-flag barrier, bit-identical to BoxSolver.solve."""
+    import torch
+
+    m = 1024
+    grid = k.CartesianGrid(BOX, m)
+    kappa = 2j * m if cplx else 7.0
+    dt = torch.complex128 if cplx else torch.float64
+    g = torch.Generator(device="cuda").manual_seed(3)
+    s = D.SlabBoxSolver(grid, kappa, p2p=True)
+    box = k.BoxSolver(grid, kappa, "dirichlet-zero")
+    for it in range(3):
+        rhs = torch.randn((m + 1, m + 1), generator=g, device="cuda", dtype=dt)
+        rhs[m] = 0
+        u = s.solve(rhs[:m])
+        ref = box.solve(rhs)
+        assert torch.equal(D.gather_rows(u, m), ref), it
+    assert s.peers_ok()
+
+
+@pytest.mark.gpu
+def test_p2p_barrier_concurrent_ranks_and_timeout():
+    """kfbi_p2p_barrier: two virtual ranks on two streams of one GPU meet;
+    a rank whose peer never arrives gives up and reports it."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2404_14864_b200 import _native as N
+
+    lib = N.lib()
+    flags = [torch.zeros(8, dtype=torch.int64, device="cuda") for _ in range(2)]
+    tab = (C.c_void_p * 2)(*[f.data_ptr() for f in flags])
+    bad = torch.zeros(1, dtype=torch.int32, device="cuda")
+    streams = [torch.cuda.Stream() for _ in range(2)]
+    for epoch in (1, 2, 3):
+        for r in (1, 0):
+            N.check(lib.kfbi_p2p_barrier(tab, 2, r, epoch, 1 << 26, bad.data_ptr(),
+                                         streams[r].cuda_stream))
+        torch.cuda.synchronize()
+        assert int(bad.item()) == 0
+        assert flags[0][:2].tolist() == [epoch, epoch] and flags[1][:2].tolist() == [epoch, epoch]
+    # rank 0 alone at epoch 4: times out, does not hang
+    N.check(lib.kfbi_p2p_barrier(tab, 2, 0, 4, 1 << 16, bad.data_ptr(), streams[0].cuda_stream))
+    torch.cuda.synchronize()
+    assert int(bad.item()) == 1
+    with pytest.raises(k.ConfigError):
+        N.check(lib.kfbi_p2p_barrier(tab, 9, 0, 1, 0, None, None))
+
+
+@pytest.mark.gpu
 def test_virtual_slabs_16384():
     import torch
 
@@ -80,6 +136,9 @@ def test_virtual_slabs_16384():
     rhs = torch.randn((m + 1, m + 1), generator=g, device="cuda", dtype=torch.float64)
     ref = k.BoxSolver(grid, 1.0, "dirichlet-zero").solve(rhs)
     u = D.solve_virtual(grid, 1.0, rhs, 8)
+    assert torch.equal(u, ref)
+    del u
+    u = D.solve_virtual(grid, 1.0, rhs, 8, p2p=True)
     assert torch.equal(u, ref)
     # size-independent check: the five-point operator of the solution
     # returns the right-hand side (interior rows of a band); the stencil's
@@ -176,7 +235,7 @@ def _worker(rank, world, port, out):
         s.nranks, s.rank, s.group, s.grid, s.kappa = world, rank, None, grid, 2.5
         s.plan = NumpySlabPlan(m, grid.h)
         s.rows = D.slab_rows(m, world, rank)
-        s._bufs = {}
+        s.passes = D.SlabPasses(s.plan, world, rank, None, "cpu")
 
         class _B:
             torch_device = "cpu"
@@ -251,3 +310,12 @@ def test_slab_richardson_virtual_bit_identical(m, kappa):
         assert torch.equal(u.reshape(-1), ref.u.reshape(-1)), p
         assert torch.equal(dens, ref.density)
         assert torch.equal(tu, ref.trace_u)
+    # the real SlabRichardson at P = 1, transposes fused (p2p buffers + barrier)
+    solver = D.SlabRichardson(ws, p2p=True)
+    dens = torch.zeros(cps.m, dtype=dt, device="cuda")
+    m1 = ws.grid.m
+    u, tu, tn, it, res, hist = solver.solve(kappa=kappa, F=F[:m1].contiguous(), f_gamma=fg, g=g,
+                                            density=dens)
+    assert it == ref.iterations and solver.passes.peers_ok()
+    assert torch.equal(u.reshape(-1), ref.u.reshape(-1)[:m1 * (m1 + 1)])
+    assert torch.equal(dens, ref.density)
