@@ -40,6 +40,9 @@ namespace reg {
 #ifndef KFBI_E
 #define KFBI_E 16
 #endif
+#ifndef KFBI_MINB256
+#define KFBI_MINB256 2
+#endif
 constexpr int E = KFBI_E;      // elements per thread (16; 8 = more warps, one more pass)
 constexpr int LE = E == 16 ? 4 : 3;
 constexpr int CTA = 256;       // threads per CTA
@@ -56,7 +59,7 @@ struct Cfg {
   static constexpr int CTA_T = T >= 256 ? (T > 512 ? 512 : T) : CTA;  // threads per CTA
   static constexpr int S = T >= 256 ? 1 : CTA / T;          // sequences per CTA
   static constexpr int LOCAL = CTA_T * E;                   // elements per CTA buffer
-  static constexpr int MINB = (CTA_T == 256 || E == 8) ? 2 : 1;  // CTAs per SM
+  static constexpr int MINB = (CTA_T == 256 || E == 8) ? KFBI_MINB256 : 1;  // CTAs per SM
   static constexpr int P = (LOGN + LE - 1) / LE;  // Stockham passes
   static constexpr int RLAST = 1 << (LOGN - LE * (P - 1));
   static_assert(LOGN >= 4 && LOGN <= 14, "DST length 16..16384");

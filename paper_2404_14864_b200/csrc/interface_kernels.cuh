@@ -549,9 +549,30 @@ struct OpSolveArgs {
   RichState *st;
   double *history;
   unsigned long long *slots;      // [3]
+  unsigned int *bar;              // grid barrier counter, zero at launch
   int rows;                       // R, rows per CTA
   int smem_cols;                  // Cs
 };
+
+// Grid barrier of the cooperative sweep kernels (all CTAs co-resident): a
+// monotonically increasing arrival counter, release on arrival, acquire on
+// the spin; thread 0 then reads the sweep's max |update| into *res.
+// (~1.26 us per barrier on 148 CTAs against 1.67 us for cg::grid_group::sync,
+// tools/mb/gsync.cu.)
+KFBI_DEV void op_barrier(const OpSolveArgs &a, int sweep, double *res) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned int target = (unsigned int)(sweep - a.first_idx + 1) * gridDim.x;
+    unsigned int v;
+    __threadfence();
+    asm volatile("atom.add.release.gpu.u32 %0, [%1], 1;" : "=r"(v) : "l"(a.bar) : "memory");
+    do {
+      asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(v) : "l"(a.bar) : "memory");
+    } while (v < target);
+    *res = __longlong_as_double((long long)__ldcg(&a.slots[sweep % 3]));
+  }
+  __syncthreads();
+}
 
 constexpr int OP_THREADS = 512;
 constexpr int OP_WARPS = OP_THREADS / 32;
@@ -571,8 +592,6 @@ op_solve_kernel(OpSolveArgs a, const T *__restrict__ Tcm, T *A, T *B,
                 const T *__restrict__ phi0, const T *__restrict__ trace1,
                 const T *__restrict__ g) {
   using S = Sc<T>;
-  namespace cg = cooperative_groups;
-  cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(16) unsigned char op_smem[];
   __shared__ double res_s;
   const int n = a.n, R = a.rows, Cs = a.smem_cols;
@@ -602,16 +621,16 @@ op_solve_kernel(OpSolveArgs a, const T *__restrict__ Tcm, T *A, T *B,
     T *out = (idx & 1) ? B : A;
     // d = phi_in - phi0: all of a thread's loads in flight at once (a
     // dependent loop of L2 round trips dominated the sweep before)
-    for (int p0 = tid; p0 < n; p0 += OP_THREADS * 5) {
-      T vi[5], v0[5];
+    for (int p0 = tid; p0 < n; p0 += OP_THREADS * 4) {
+      T vi[4], v0[4];
 #pragma unroll
-      for (int u = 0; u < 5; ++u) {
+      for (int u = 0; u < 4; ++u) {
         const int p = p0 + u * OP_THREADS;
         vi[u] = p < n ? __ldcg(in + p) : S::zero();
         v0[u] = p < n ? __ldg(phi0 + p) : S::zero();
       }
 #pragma unroll
-      for (int u = 0; u < 5; ++u) {
+      for (int u = 0; u < 4; ++u) {
         const int p = p0 + u * OP_THREADS;
         if (p < n) d[p] = S::sub(vi[u], v0[u]);
       }
@@ -666,10 +685,8 @@ op_solve_kernel(OpSolveArgs a, const T *__restrict__ Tcm, T *A, T *B,
         if (blockIdx.x == 0) a.slots[(idx + 1) % 3] = 0ull;
       }
     }
-    grid.sync();
-    // one L2 read per block (an atomic per thread would serialise)
-    if (tid == 0) res_s = __longlong_as_double((long long)__ldcg(&a.slots[idx % 3]));
-    __syncthreads();
+    // one L2 read of the max per block (an atomic per thread would serialise)
+    op_barrier(a, idx, &res_s);
     const double res = res_s;
     const bool conv = res <= a.tol;
     const bool last = conv || idx + 1 >= a.max_iter;
@@ -695,8 +712,6 @@ __global__ void __launch_bounds__(OP_THREADS, 1)
 op_solve_pair_kernel(OpSolveArgs a, const double *__restrict__ Tcm, double *A, double *B,
                      const double *__restrict__ phi0, const double *__restrict__ trace1,
                      const double *__restrict__ g) {
-  namespace cg = cooperative_groups;
-  cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(16) unsigned char op_smem[];
   __shared__ double res_s;
   const int n = a.n, R = a.rows, Cs = a.smem_cols;
@@ -711,6 +726,13 @@ op_solve_pair_kernel(OpSolveArgs a, const double *__restrict__ Tcm, double *A, d
   const int creg = min(n, 2 * OP_WARPS * K2);
   const int cs0 = creg, cg0 = min(n, creg + Cs);
   const int c_off = 2 * warp + hf;                       // first column of this half-warp
+  constexpr int PD = 8;                                  // d entries per thread and round
+  double p0r[PD];                                        // phi0 of the first round, kept
+#pragma unroll
+  for (int u = 0; u < PD; ++u) {
+    const int p = tid + u * OP_THREADS;
+    p0r[u] = p < n ? phi0[p] : 0.0;
+  }
 
   double2 treg[K2];
 #pragma unroll
@@ -728,18 +750,18 @@ op_solve_pair_kernel(OpSolveArgs a, const double *__restrict__ Tcm, double *A, d
   for (int idx = a.first_idx; idx < a.max_iter; ++idx) {
     const double *in = (idx & 1) ? A : B;
     double *out = (idx & 1) ? B : A;
-    for (int p0 = tid; p0 < n; p0 += OP_THREADS * 5) {
-      double vi[5], v0[5];
+    // all of a thread's d loads in one round (n <= 4096: one L2 round trip)
+    for (int q0 = 0; q0 < n; q0 += OP_THREADS * PD) {
+      double vi[PD];
 #pragma unroll
-      for (int u = 0; u < 5; ++u) {
-        const int p = p0 + u * OP_THREADS;
+      for (int u = 0; u < PD; ++u) {
+        const int p = q0 + tid + u * OP_THREADS;
         vi[u] = p < n ? __ldcg(in + p) : 0.0;
-        v0[u] = p < n ? __ldg(phi0 + p) : 0.0;
       }
 #pragma unroll
-      for (int u = 0; u < 5; ++u) {
-        const int p = p0 + u * OP_THREADS;
-        if (p < n) d[p] = vi[u] - v0[u];
+      for (int u = 0; u < PD; ++u) {
+        const int p = q0 + tid + u * OP_THREADS;
+        if (p < n) d[p] = vi[u] - (q0 == 0 ? p0r[u] : __ldg(phi0 + p));
       }
     }
     __syncthreads();
@@ -805,9 +827,7 @@ op_solve_pair_kernel(OpSolveArgs a, const double *__restrict__ Tcm, double *A, d
         if (blockIdx.x == 0) a.slots[(idx + 1) % 3] = 0ull;
       }
     }
-    grid.sync();
-    if (tid == 0) res_s = __longlong_as_double((long long)__ldcg(&a.slots[idx % 3]));
-    __syncthreads();
+    op_barrier(a, idx, &res_s);
     const double res = res_s;
     const bool conv = res <= a.tol;
     const bool last = conv || idx + 1 >= a.max_iter;

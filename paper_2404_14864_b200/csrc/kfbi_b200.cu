@@ -678,8 +678,8 @@ kfbi_status op_solve(kfbi_plan *p, const kfbi_bvp *b, cudaStream_t s) {
   const size_t smem = fixed + cs * rows * sizeof(T);
   if (fixed > (size_t)(smem_optin - 1024))
     return fail(KFBI_E_CONFIG, "operator form: n_ctl too large for the on-chip sweep kernel");
-  unsigned long long *slots = p->red.p + 4;
-  KFBI_CUDA(cudaMemsetAsync(slots, 0, 3 * sizeof(unsigned long long), s), "density-update");
+  unsigned long long *slots = p->red.p + 4;        // [3] maxima + the barrier counter
+  KFBI_CUDA(cudaMemsetAsync(slots, 0, 4 * sizeof(unsigned long long), s), "density-update");
   OpSolveArgs a;
   a.n = n;
   a.first_idx = 1;
@@ -689,6 +689,7 @@ kfbi_status op_solve(kfbi_plan *p, const kfbi_bvp *b, cudaStream_t s) {
   a.st = p->st.p;
   a.history = p->history.p;
   a.slots = slots;
+  a.bar = reinterpret_cast<unsigned int *>(slots + 3);
   a.rows = rows;
   a.smem_cols = (int)cs;
   const T *Tcm = reinterpret_cast<const T *>(p->Top.p);
