@@ -238,9 +238,11 @@ KFBI_DEV void powers(double2 w1, double2 (&w)[R]) {
 
 // One Stockham pass: radix R, current span NS; thread t holds inputs
 // v[m] = x[t + m T]; writes the pass output to sm (swizzled).
+// w1pre: the pass's twiddle base, preloaded at FFT entry when the thread has
+// one butterfly (B = 1); otherwise read here.
 template <int LOGN, int R, int NS, int TWS = 1, bool KEEP = false>
 KFBI_DEV void stockham_pass(double2 (&v)[E], const View<LOGN> &sm, int t,
-                            const double2 *__restrict__ twg) {
+                            const double2 *__restrict__ twg, double2 w1pre) {
   constexpr int N = 1 << LOGN;
   constexpr int T = Cfg<LOGN>::T;
   constexpr int B = E / R;              // butterflies per thread
@@ -253,7 +255,7 @@ KFBI_DEV void stockham_pass(double2 (&v)[E], const View<LOGN> &sm, int t,
     for (int s = 0; s < R; ++s) a[s] = v[i + s * B];
     if constexpr (NS > 1) {
       double2 w[R];
-      powers<R>(__ldg(&twg[k * (N / (NS * R)) * TWS]), w);
+      powers<R>(B == 1 ? w1pre : __ldg(&twg[k * (N / (NS * R)) * TWS]), w);
 #pragma unroll
       for (int s = 1; s < R; ++s) a[s] = cmul(a[s], w[s]);
     }
@@ -273,18 +275,34 @@ KFBI_DEV void stockham_pass(double2 (&v)[E], const View<LOGN> &sm, int t,
 // TWS: stride into the twiddle table (2 when the table is for length 2N)
 template <int LOGN, int PASS, int TWS = 1, bool KEEP = false>
 KFBI_DEV void fft_passes(double2 (&v)[E], const View<LOGN> &sm, int t,
-                         const double2 *__restrict__ twg) {
+                         const double2 *__restrict__ twg, const double2 (&tw)[Cfg<LOGN>::P]) {
   using C = Cfg<LOGN>;
   constexpr int R = (PASS < C::P - 1) ? E : C::RLAST;
   constexpr int NS = 1 << (LE * PASS);
   constexpr bool LASTKEEP = KEEP && PASS + 1 == C::P;
-  stockham_pass<LOGN, R, NS, TWS, LASTKEEP>(v, sm, t, twg);
+  stockham_pass<LOGN, R, NS, TWS, LASTKEEP>(v, sm, t, twg, tw[PASS]);
   if constexpr (PASS + 1 < C::P) {
     seq_sync<LOGN>();
 #pragma unroll
     for (int m = 0; m < E; ++m) v[m] = sm[t + m * C::T];
     seq_sync<LOGN>();
-    fft_passes<LOGN, PASS + 1, TWS, KEEP>(v, sm, t, twg);
+    fft_passes<LOGN, PASS + 1, TWS, KEEP>(v, sm, t, twg, tw);
+  }
+}
+
+// Twiddle bases of the passes with one butterfly per thread, read at FFT
+// entry: the table reads then overlap the first pass instead of stalling
+// the twiddle products of later passes (a long-scoreboard stall in ncu).
+template <int LOGN, int TWS>
+KFBI_DEV void load_twiddles(double2 (&tw)[Cfg<LOGN>::P], int t, const double2 *__restrict__ twg) {
+  using C = Cfg<LOGN>;
+  constexpr int N = 1 << LOGN;
+  tw[0] = make_double2(1.0, 0.0);
+#pragma unroll
+  for (int pass = 1; pass < C::P; ++pass) {
+    const int R = (pass < C::P - 1) ? E : C::RLAST;
+    const int NS = 1 << (LE * pass);
+    tw[pass] = (R == E) ? __ldg(&twg[(t & (NS - 1)) * (N / (NS * R)) * TWS]) : make_double2(1.0, 0.0);
   }
 }
 
@@ -292,7 +310,9 @@ KFBI_DEV void fft_passes(double2 (&v)[E], const View<LOGN> &sm, int t,
 // the input in the same layout and sm is free.  Exit: sm may still be read.
 template <int LOGN>
 KFBI_DEV void fft_keep(double2 (&v)[E], const View<LOGN> &sm, int t, const double2 *__restrict__ twg) {
-  fft_passes<LOGN, 0, 1, true>(v, sm, t, twg);
+  double2 tw[Cfg<LOGN>::P];
+  load_twiddles<LOGN, 1>(tw, t, twg);
+  fft_passes<LOGN, 0, 1, true>(v, sm, t, twg, tw);
 }
 
 // Z = FFT_N(y): y in registers (v[m] = y_{t + m T}), Z left in sm in natural
@@ -300,7 +320,9 @@ KFBI_DEV void fft_keep(double2 (&v)[E], const View<LOGN> &sm, int t, const doubl
 // Returns after a sequence barrier (Z visible to all threads).
 template <int LOGN, int TWS = 1>
 KFBI_DEV void fft(double2 (&v)[E], const View<LOGN> &sm, int t, const double2 *__restrict__ twg) {
-  fft_passes<LOGN, 0, TWS>(v, sm, t, twg);
+  double2 tw[Cfg<LOGN>::P];
+  load_twiddles<LOGN, TWS>(tw, t, twg);
+  fft_passes<LOGN, 0, TWS>(v, sm, t, twg, tw);
   seq_sync<LOGN>();
 }
 
