@@ -164,6 +164,15 @@ kfbi_status kfbi_box_solve_bc(kfbi_plan *plan, int32_t dtype, int32_t box_bc,
 kfbi_status kfbi_plan_set_geometry(kfbi_plan *plan, const kfbi_geometry *geo);
 
 /* Rows [row0, row0 + nrows) of the plan's W (n_ctl values each) to host. */
+/* Edge values jv = W . JM (interface.py:206-238): the matrix-free spectral
+ * form applies when the controls are the reference's theta_j = 2 pi j / n
+ * with n even >= 32 (the trig branch of interp_rows, interface.py:38-52,
+ * 70-75).  Mode 0 (default) uses it when the W rows it replaces would exceed
+ * 192 MB and streams W rows (built on the device on first use) otherwise;
+ * 1 forces the W rows, 2 the spectral form.
+ * kfbi_plan_get_interp reports 1 when the spectral form is in use. */
+kfbi_status kfbi_plan_set_interp(kfbi_plan *plan, int32_t mode);
+kfbi_status kfbi_plan_get_interp(kfbi_plan *plan, int32_t *spectral);
 kfbi_status kfbi_plan_copy_w(kfbi_plan *plan, int32_t row0, int32_t nrows, double *out);
 
 /* OneSidedExtractor tables (bvp.py:115-212), host pointers: stencil7

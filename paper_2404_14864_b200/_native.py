@@ -118,6 +118,8 @@ _SIGNATURES = {
     "kfbi_slab_rows_fwd": ([vp, i32, vp, vp, f64, vp, vp, vp], i32),
     "kfbi_slab_cols": ([vp, i32, vp, f64, f64, vp, vp], i32),
     "kfbi_slab_rows_inv": ([vp, i32, vp, vp, vp, vp], i32),
+    "kfbi_plan_set_interp": ([vp, i32], i32),
+    "kfbi_plan_get_interp": ([vp, C.POINTER(i32)], i32),
     "kfbi_slab_rows_fwd_p2p": ([vp, i32, vp, vp, f64, vp, vp, vp], i32),
     "kfbi_slab_cols_p2p": ([vp, i32, vp, f64, f64, vp, vp, vp], i32),
     "kfbi_ipc_alloc": ([i64, C.POINTER(vp), vp], i32),

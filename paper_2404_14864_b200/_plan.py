@@ -115,6 +115,17 @@ class Plan:
         self.n_ctl = int(tables["n_ctl"])
         self.has_geometry = True
 
+    def set_interp(self, mode):
+        """Edge-value form: "auto" (spectral when it applies), "w" (W rows),
+        "spectral" (kfbi_plan_set_interp)."""
+        N.check(self._lib.kfbi_plan_set_interp(self.handle, {"auto": 0, "w": 1, "spectral": 2}[mode]))
+
+    @property
+    def spectral_edges(self):
+        v = C.c_int32(0)
+        N.check(self._lib.kfbi_plan_get_interp(self.handle, C.byref(v)))
+        return bool(v.value)
+
     def copy_w(self, row0, nrows):
         """Rows of the device W (setup check)."""
         out = np.empty((int(nrows), self.n_ctl))

@@ -275,6 +275,273 @@ corr_edges_kernel(EdgeArgs ea, const T *__restrict__ jm, T *jv, const int *done)
 }
 
 // ---------------------------------------------------------------------------
+// Matrix-free edge values (the trig branch of interp_rows, interface.py:38-52,
+// 70-75).  For the reference's equispaced controls theta_j = 2 pi j / n (n
+// even) the cardinal kernel D(x) = sin(n x/2) cos(x/2) / (n sin(x/2)) is the
+// trigonometric interpolant 1/n [1 + 2 sum_{k=1}^{n/2-1} cos(k x) + cos(n x/2)],
+// so with F_k = sum_j f_j e^{-2 pi i j k / n} (the DFT of a real column f)
+//   (W f)(theta) = 1/n [F_0 + 2 sum_{k=1}^{n/2-1} Re(e^{i k theta} F_k)
+//                       + cos(n theta / 2) F_{n/2}].
+// Two kernels replace the n_edges x n_ctl W stream (680 MB at 4096^2 flower in
+// the reference, 5.4 GB at 16384^2): the spectrum of the five used JM columns
+// (u, ux, uy, uxx, uyy; real and imaginary parts separately for c128) by a
+// direct DFT, then one sum over k per edge.  The exact angles k theta come
+// from an exact product (fma) and a first-order correction of sincos, the
+// in-between powers from one rotation per 32 k; deviation from W . JM is the
+// conditioning of the reference formula itself (k ulp(theta), <= 1e-12).
+constexpr int SPEC_COLS = 5;                     // JM columns u, ux, uy, uxx, uyy
+KFBI_DEV int spec_jm_col(int c) { return c < 4 ? c : 5; }
+
+// e^{i a b} for a large product a b: exact product p + e, sincos(p) corrected
+KFBI_DEV double2 cis_product(double a, double b) {
+  const double p = a * b;
+  const double e = fma(a, b, -p);
+  double sp, cp;
+  sincos(p, &sp, &cp);
+  return make_double2(fma(-e, sp, cp), fma(e, cp, sp));
+}
+
+// Spectrum F_k (k < K = n/2 + 1) of the used JM columns.  CTA (x, y): lane =
+// frequency k = 32 x + lane, warp w and split y cover the control range
+// [(y W + w) n / (W Y), ...).  e^{-2 pi i j k / n} is exact from the index
+// (j k mod n) every 32 controls and advanced by one rotation in between.  The
+// W partial sums of a CTA are added in warp order in shared memory, the Y
+// CTA partials of a frequency block by the last CTA to finish it, in split
+// order (deterministic; the block counter resets itself).
+template <typename T>
+__global__ void __launch_bounds__(512)
+spec_block_kernel(int n, int K, const T *__restrict__ jm, double2 *__restrict__ part,
+                  double2 *__restrict__ spec, unsigned int *counters) {
+  constexpr int NP = std::is_same<T, double2>::value ? 2 : 1;
+  constexpr int R = SPEC_COLS * NP;
+  extern __shared__ double2 red_sm[];                   // [W][R][32]
+  __shared__ bool last;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int Y = gridDim.y, y = blockIdx.y;
+  auto red = [&](int x, int r) -> double2 & { return red_sm[((size_t)x * R + r) * 32 + lane]; };
+  const int k = blockIdx.x * 32 + lane;
+  const long part_id = (long)y * nw + w, nparts = (long)Y * nw;
+  const int j0 = (int)(n * part_id / nparts), j1 = (int)(n * (part_id + 1) / nparts);
+  double2 acc[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) acc[r] = make_double2(0.0, 0.0);
+  if (k < K) {
+    double ss, cs;
+    sincospi(-2.0 * (double)k / n, &ss, &cs);
+    const double2 step = make_double2(cs, ss);
+    double2 wk = make_double2(1.0, 0.0);
+    for (int j = j0; j < j1; ++j) {
+      if (((j - j0) & 31) == 0) {
+        const long idx = ((long)j * k) % n;
+        double sw, cw;
+        sincospi(-2.0 * (double)idx / n, &sw, &cw);
+        wk = make_double2(cw, sw);
+      }
+#pragma unroll
+      for (int c = 0; c < SPEC_COLS; ++c) {
+        const T v = __ldg(&jm[(size_t)spec_jm_col(c) * n + j]);
+        if constexpr (NP == 1) {
+          acc[c].x = fma(v, wk.x, acc[c].x);
+          acc[c].y = fma(v, wk.y, acc[c].y);
+        } else {
+          acc[c].x = fma(v.x, wk.x, acc[c].x);
+          acc[c].y = fma(v.x, wk.y, acc[c].y);
+          acc[SPEC_COLS + c].x = fma(v.y, wk.x, acc[SPEC_COLS + c].x);
+          acc[SPEC_COLS + c].y = fma(v.y, wk.y, acc[SPEC_COLS + c].y);
+        }
+      }
+      wk = cmul(wk, step);
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < R; ++r) red(w, r) = acc[r];
+  __syncthreads();
+  if (w == 0 && k < K) {
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      double2 sum = red(0, r);
+      for (int x = 1; x < nw; ++x) sum = cadd(sum, red(x, r));
+      part[((size_t)y * R + r) * K + k] = sum;
+    }
+  }
+  if (Y == 1) {
+    if (w == 0 && k < K)
+#pragma unroll
+      for (int r = 0; r < R; ++r) spec[(size_t)r * K + k] = part[(size_t)r * K + k];
+    return;
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(&counters[blockIdx.x], 1u) == (unsigned)(Y - 1);
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  if (w == 0 && k < K) {
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      double2 sum = __ldcg(&part[(size_t)r * K + k]);
+      for (int x = 1; x < Y; ++x) sum = cadd(sum, __ldcg(&part[((size_t)x * R + r) * K + k]));
+      spec[(size_t)r * K + k] = sum;
+    }
+  }
+  if (threadIdx.x == 0) counters[blockIdx.x] = 0u;
+}
+
+// One group of EB edges of one axis (the host orders the edges by axis and
+// pads each class to whole groups; perm = -1 marks a pad): lane l sums
+// k = 1 + l + 32 i (k < n/2) over the three columns (u, u_a, u_aa) of the
+// group's axis.  F(col, k) returns the spectrum entry.
+template <typename T, int EB, typename FN>
+KFBI_DEV void edge_group(int g, int n, int K, const int *__restrict__ perm, const double *__restrict__ theta,
+                         const signed char *__restrict__ axis, int kbeg, int kend, double (&acc)[EB][6],
+                         double2 (&z)[EB], const double2 (&z32)[EB], int ca, FN F) {
+  constexpr int NP = std::is_same<T, double2>::value ? 2 : 1;
+  for (int k = kbeg; k < kend; k += 32) {
+    double2 f[NP][3];
+#pragma unroll
+    for (int h = 0; h < NP; ++h) {
+      f[h][0] = F(h * SPEC_COLS, k);
+      f[h][1] = F(h * SPEC_COLS + ca, k);
+      f[h][2] = F(h * SPEC_COLS + ca + 2, k);
+    }
+#pragma unroll
+    for (int q = 0; q < EB; ++q) {
+#pragma unroll
+      for (int h = 0; h < NP; ++h)
+#pragma unroll
+        for (int c = 0; c < 3; ++c)     // Re(z F) = z.x F.x - z.y F.y
+          acc[q][3 * h + c] = fma(z[q].x, f[h][c].x, fma(-z[q].y, f[h][c].y, acc[q][3 * h + c]));
+      z[q] = cmul(z[q], z32[q]);
+    }
+  }
+}
+
+template <typename T, int EB>
+KFBI_DEV void edge_group_begin(int g, const int *__restrict__ perm, const double *__restrict__ theta,
+                               const signed char *__restrict__ axis, int lane, int (&eid)[EB],
+                               double (&th)[EB], double2 (&z)[EB], double2 (&z32)[EB], int &ca,
+                               double (&acc)[EB][6]) {
+  ca = 1;
+#pragma unroll
+  for (int q = EB - 1; q >= 0; --q) {
+    eid[q] = perm[g * EB + q];
+    const int e = eid[q] >= 0 ? eid[q] : 0;
+    th[q] = theta[e];
+    if (eid[q] >= 0) ca = axis[e] != 0 ? 2 : 1;   // uniform over the group's real edges
+    z[q] = cis_product((double)(1 + lane), th[q]);
+    z32[q] = cis_product(32.0, th[q]);
+#pragma unroll
+    for (int c = 0; c < 6; ++c) acc[q][c] = 0.0;
+  }
+}
+
+template <typename T, int EB, typename FN>
+KFBI_DEV void edge_group_end(int n, int lane, const int (&eid)[EB], const double (&th)[EB], int ca,
+                             double (&acc)[EB][6], T *jv, FN F) {
+  constexpr int NP = std::is_same<T, double2>::value ? 2 : 1;
+#pragma unroll
+  for (int q = 0; q < EB; ++q)
+#pragma unroll
+    for (int c = 0; c < 3 * NP; ++c) acc[q][c] = warp_sum(acc[q][c]);
+  if (lane >= EB) return;
+  double out[6];
+  double tq = th[0];
+  int e = eid[0];
+#pragma unroll
+  for (int c = 0; c < 6; ++c) out[c] = acc[0][c];
+#pragma unroll
+  for (int q = 1; q < EB; ++q)
+    if (lane == q) {
+#pragma unroll
+      for (int c = 0; c < 6; ++c) out[c] = acc[q][c];
+      tq = th[q];
+      e = eid[q];
+    }
+  if (e < 0) return;
+  const double cn = cis_product(0.5 * n, tq).x;         // cos(n theta / 2)
+  const double inv_n = 1.0 / n;
+  const int cols[3] = {0, ca, ca + 2};
+  double res[6];
+#pragma unroll
+  for (int h = 0; h < NP; ++h)
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+      res[3 * h + c] = (F(h * SPEC_COLS + cols[c], 0).x + 2.0 * out[3 * h + c] +
+                        cn * F(h * SPEC_COLS + cols[c], n / 2).x) * inv_n;
+  T *o = jv + 3 * (size_t)e;
+  if constexpr (NP == 1) {
+    o[0] = res[0];
+    o[1] = res[1];
+    o[2] = res[2];
+  } else {
+    o[0] = make_double2(res[0], res[3]);
+    o[1] = make_double2(res[1], res[4]);
+    o[2] = make_double2(res[2], res[5]);
+  }
+}
+
+// Spectrum resident in shared memory (R K 16 bytes fit): one CTA per SM
+// loads it once; its warps walk the edge groups.
+template <typename T, int EB>
+__global__ void __launch_bounds__(512, 1)
+edges_spectral_res_kernel(int ngroups, int n, int K, const int *__restrict__ perm,
+                          const double *__restrict__ theta, const signed char *__restrict__ axis,
+                          const double2 *__restrict__ spec, T *jv, const int *done) {
+  constexpr int NP = std::is_same<T, double2>::value ? 2 : 1;
+  constexpr int R = SPEC_COLS * NP;
+  extern __shared__ double2 fsm[];                       // [R][K]
+  if (done && *done) return;
+  for (int i = threadIdx.x; i < R * K; i += blockDim.x) fsm[i] = spec[i];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+  auto F = [&](int r, int k) { return fsm[(size_t)r * K + k]; };
+  for (int g = blockIdx.x * nwarps + (threadIdx.x >> 5); g < ngroups; g += gridDim.x * nwarps) {
+    int eid[EB], ca;
+    double th[EB], acc[EB][6];
+    double2 z[EB], z32[EB];
+    edge_group_begin<T, EB>(g, perm, theta, axis, lane, eid, th, z, z32, ca, acc);
+    edge_group<T, EB>(g, n, K, perm, theta, axis, 1 + lane, n / 2, acc, z, z32, ca, F);
+    edge_group_end<T, EB>(n, lane, eid, th, ca, acc, jv, F);
+  }
+}
+
+// Large n (C5): one group per warp, the spectrum staged in chunks of
+// SPEC_KC frequencies shared by the CTA's warps.
+constexpr int SPEC_KC = 512;
+template <typename T, int EB>
+__global__ void __launch_bounds__(256)
+edges_spectral_kernel(int ngroups, int n, int K, const int *__restrict__ perm,
+                      const double *__restrict__ theta, const signed char *__restrict__ axis,
+                      const double2 *__restrict__ spec, T *jv, const int *done) {
+  constexpr int NP = std::is_same<T, double2>::value ? 2 : 1;
+  constexpr int R = SPEC_COLS * NP;
+  extern __shared__ double2 fsm[];                       // [R][SPEC_KC]
+  if (done && *done) return;
+  const int lane = threadIdx.x & 31;
+  const int g = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const bool active = g < ngroups;
+  int eid[EB], ca = 1;
+  double th[EB], acc[EB][6];
+  double2 z[EB], z32[EB];
+  if (active) edge_group_begin<T, EB>(g, perm, theta, axis, lane, eid, th, z, z32, ca, acc);
+  const int kmax = n / 2;
+  for (int kc0 = 1; kc0 < kmax; kc0 += SPEC_KC) {
+    const int kn = min(SPEC_KC, kmax - kc0);
+    __syncthreads();
+    for (int i = threadIdx.x; i < R * kn; i += blockDim.x) {
+      const int r = i / kn, kk = i - r * kn;
+      fsm[r * SPEC_KC + kk] = spec[(size_t)r * K + kc0 + kk];
+    }
+    __syncthreads();
+    auto F = [&](int r, int k) { return fsm[r * SPEC_KC + (k - kc0)]; };
+    if (active) edge_group<T, EB>(g, n, K, perm, theta, axis, kc0 + lane, kc0 + kn, acc, z, z32, ca, F);
+  }
+  if (!active) return;
+  auto FG = [&](int r, int k) { return spec[(size_t)r * K + k]; };
+  edge_group_end<T, EB>(n, lane, eid, th, ca, acc, jv, FG);
+}
+
+// ---------------------------------------------------------------------------
 struct ExtractArgs {
   int n, m;
   double h, inv_h;

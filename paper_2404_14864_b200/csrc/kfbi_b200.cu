@@ -92,6 +92,16 @@ struct kfbi_plan {
   bool has_geo = false;
   int n_ctl = 0, n_edges = 0, n_rec = 0, n_groups = 0, w_ld = 0;
   DevBuf<double> W;
+  // edge values: W rows (streamed) or the matrix-free spectral form
+  int interp_mode = 0;              // 0 auto, 1 W rows, 2 spectral
+  bool spec_ok = false;             // equispaced controls, even n >= 32
+  bool w_ready = false;             // W built / uploaded
+  bool w_explicit = false;          // W given by the caller (cubic rows)
+  DevBuf<double> edge_theta_d, ctl_theta_d;
+  DevBuf<double2> spec, spec_part;
+  DevBuf<int> edge_perm;            // edges grouped by axis, 4 per group, -1 pads
+  int n_perm = 0;
+  DevBuf<unsigned int> spec_ctr;    // per frequency block, self-resetting
   DevBuf<signed char> edge_axis;
   DevBuf<int> rec_edge, group_start, group_node, row_group, stencil;
   DevBuf<double> rec_d, rec_sigma, deriv_col, speed, tangent, normal, dtan_ds, inv3;
@@ -510,8 +520,96 @@ kfbi_status jumps_T(kfbi_plan *p, double kre, double kim, const void *phi, const
   return KFBI_OK;
 }
 
+// W rows built on the device from the crossing and control parameters
+// (interp_rows trig branch) when first needed: the W-row path of edges_T,
+// kfbi_plan_copy_w.  The spectral path never builds them.
+kfbi_status ensure_w(kfbi_plan *p) {
+  if (p->w_ready) return KFBI_OK;
+  if (!p->edge_theta_d.p || !p->ctl_theta_d.p) return fail(KFBI_E_CONFIG, "W rows: no crossing parameters");
+  cudaError_t e = p->W.ensure((size_t)p->n_edges * p->w_ld + 1);
+  if (e == cudaSuccess && p->n_edges > 0) {
+    w_build_kernel<<<148 * 16, 256>>>(p->n_edges, p->n_ctl, p->w_ld, p->edge_theta_d.p, p->ctl_theta_d.p,
+                                      p->W.p);
+    e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  }
+  if (e != cudaSuccess) return fail(KFBI_E_CUDA, std::string("W build: ") + cudaGetErrorString(e));
+  p->w_ready = true;
+  return KFBI_OK;
+}
+
+
+// Matrix-free edge values: the spectrum of the used JM columns, then one
+// k-sum per edge (interface_kernels.cuh).  The spectrum stays resident in
+// shared memory when it fits (one CTA per SM); otherwise it is staged in
+// chunks (C5-size n_ctl).
+template <typename T>
+kfbi_status edges_spectral(kfbi_plan *p, const void *jm, void *jv, const int *done, cudaStream_t s) {
+  constexpr int NP = std::is_same<T, double2>::value ? 2 : 1;
+  constexpr int R = SPEC_COLS * NP;
+  constexpr int EB = NP == 1 ? 4 : 2;          // edges per group (perm groups of 4)
+  static int sms = 0, optin = 0;
+  static bool attr = false;
+  if (!attr) {
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->device);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, p->device);
+    KFBI_CUDA(cudaFuncSetAttribute(edges_spectral_kernel<T, EB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)(R * SPEC_KC * sizeof(double2))), "jumps-and-corrections");
+    KFBI_CUDA(cudaFuncSetAttribute(edges_spectral_res_kernel<T, EB>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, optin), "jumps-and-corrections");
+    KFBI_CUDA(cudaFuncSetAttribute(spec_block_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)(16 * R * 32 * sizeof(double2))), "jumps-and-corrections");
+    attr = true;
+  }
+  const int n = p->n_ctl, K = n / 2 + 1;
+  const int kb = (K + 31) / 32;
+  int Y = (2 * sms) / kb;
+  Y = Y < 1 ? 1 : (Y > 8 ? 8 : Y);
+  cudaError_t e = p->spec.ensure((size_t)2 * SPEC_COLS * K);
+  if (e == cudaSuccess) e = p->spec_part.ensure((size_t)8 * 2 * SPEC_COLS * K);
+  if (e == cudaSuccess && p->spec_ctr.n < (size_t)kb) {
+    e = p->spec_ctr.ensure((size_t)kb);
+    if (e == cudaSuccess) e = cudaMemset(p->spec_ctr.p, 0, (size_t)kb * sizeof(unsigned int));
+  }
+  if (e != cudaSuccess) return fail(KFBI_E_CUDA, std::string("spectral edges: ") + cudaGetErrorString(e));
+  if (p->n_edges == 0) return KFBI_OK;
+  KFBI_TRY(launch(p, KFBI_K_JUMPS, s, [&] {
+    spec_block_kernel<T><<<dim3(kb, Y), 512, 16 * R * 32 * sizeof(double2), s>>>(
+        n, K, static_cast<const T *>(jm), p->spec_part.p, p->spec.p, p->spec_ctr.p);
+  }));
+  const int ngroups = p->n_perm / EB;
+  const size_t res_bytes = (size_t)R * K * sizeof(double2);
+  if (res_bytes <= (size_t)optin) {
+    return launch(p, KFBI_K_JUMPS, s, [&] {
+      edges_spectral_res_kernel<T, EB><<<sms, 512, res_bytes, s>>>(
+          ngroups, n, K, p->edge_perm.p, p->edge_theta_d.p, p->edge_axis.p, p->spec.p,
+          static_cast<T *>(jv), done);
+    });
+  }
+  return launch(p, KFBI_K_JUMPS, s, [&] {
+    edges_spectral_kernel<T, EB><<<(ngroups + 7) / 8, 256, R * SPEC_KC * sizeof(double2), s>>>(
+        ngroups, n, K, p->edge_perm.p, p->edge_theta_d.p, p->edge_axis.p, p->spec.p,
+        static_cast<T *>(jv), done);
+  });
+}
+
+// Auto mode: the spectral form when the W stream it replaces is large (its
+// cost is fp64 work ~ n_edges n_ctl, the stream's HBM bytes 8 n_edges n_ctl;
+// measured at 4096^2: spectral 59 us vs W 80 us for the 340 MB flower rows,
+// 69 us vs 61 us for the 116 MB star rows), always when forced (mode 2).
+#ifndef KFBI_SPEC_MIN_BYTES
+#define KFBI_SPEC_MIN_BYTES (192ull << 20)
+#endif
+bool use_spectral(const kfbi_plan *p) {
+  if (!p->spec_ok || p->w_explicit || p->interp_mode == 1) return false;
+  if (p->interp_mode == 2) return true;
+  return (unsigned long long)p->n_edges * p->n_ctl * 8ull >= KFBI_SPEC_MIN_BYTES;
+}
+
 template <typename T>
 kfbi_status edges_T(kfbi_plan *p, const void *jm, void *jv, const int *done, cudaStream_t s) {
+  if (use_spectral(p)) return edges_spectral<T>(p, jm, jv, done, s);
+  KFBI_TRY(ensure_w(p));
   // one wave of 2 CTAs per SM, the edges spread evenly over its warps in
   // contiguous ranges of at most EW (a partial second wave ran on half the
   // SMs); larger problems use more waves of full ranges
@@ -969,7 +1067,8 @@ kfbi_status kfbi_plan_destroy(kfbi_plan *p) {
   }
   for (auto e : p->pool) cudaEventDestroy(e);
   p->lam.release(); p->panels.release(); p->twg.release(); p->sinv.release();
-  p->W.release(); p->edge_axis.release(); p->rec_edge.release(); p->group_start.release();
+  p->W.release(); p->edge_theta_d.release(); p->ctl_theta_d.release(); p->spec.release();
+  p->spec_part.release(); p->edge_perm.release(); p->spec_ctr.release(); p->edge_axis.release(); p->rec_edge.release(); p->group_start.release();
   p->group_node.release(); p->row_group.release(); p->stencil.release(); p->rec_d.release();
   p->rec_sigma.release(); p->deriv_col.release(); p->speed.release(); p->tangent.release();
   p->normal.release(); p->dtan_ds.release(); p->inv3.release(); p->ainv_rows.release();
@@ -1005,26 +1104,37 @@ kfbi_status kfbi_plan_set_geometry(kfbi_plan *p, const kfbi_geometry *g) {
   cudaError_t e = cudaSuccess;
 #define UP(buf, ptr, cnt) \
   if (e == cudaSuccess) e = upload(p->buf, ptr, (size_t)(cnt))
+  p->W.release();
+  p->w_ready = p->w_explicit = false;
+  p->spec_ok = false;
+  if (g->edge_theta && g->ctl_theta) {
+    UP(edge_theta_d, g->edge_theta, g->n_edges > 0 ? g->n_edges : 1);
+    UP(ctl_theta_d, g->ctl_theta, n);
+    // the spectral form needs the reference's controls theta_j = 2 pi j / n
+    // (geometry.py:393, same operation order) and the trig branch (even n >= 32)
+    bool eq = (n % 2) == 0 && n >= 32;
+    for (int j = 0; eq && j < n; ++j) eq = g->ctl_theta[j] == 2.0 * 3.141592653589793 * j / n;
+    p->spec_ok = eq;
+    // edge groups of one axis for the spectral kernels: axis-0 edges, then
+    // axis-1 edges, each class padded to a multiple of 4 with -1
+    std::vector<int> perm;
+    for (int ax = 0; ax < 2; ++ax) {
+      for (int ed = 0; ed < g->n_edges; ++ed)
+        if ((g->edge_axis[ed] != 0) == (ax == 1)) perm.push_back(ed);
+      while (perm.size() % 4) perm.push_back(-1);
+    }
+    if (perm.empty()) perm.assign(4, -1);
+    p->n_perm = (int)perm.size();
+    UP(edge_perm, perm.data(), perm.size());
+  }
   if (g->w_edges) {
     std::vector<double> wpad((size_t)g->n_edges * p->w_ld, 0.0);
     for (int ed = 0; ed < g->n_edges; ++ed)
       std::memcpy(&wpad[(size_t)ed * p->w_ld], g->w_edges + (size_t)ed * n, n * sizeof(double));
     UP(W, wpad.data(), wpad.size());
-  } else {
-    // device-side W build from the crossing and control parameters
-    if (!g->edge_theta || !g->ctl_theta || (n % 2) != 0 || n < 32)
-      return fail(KFBI_E_CONFIG, "device W build needs edge_theta / ctl_theta and an even n_ctl >= 32");
-    DevBuf<double> et, ct;
-    if (e == cudaSuccess) e = upload(et, g->edge_theta, (size_t)g->n_edges);
-    if (e == cudaSuccess) e = upload(ct, g->ctl_theta, (size_t)n);
-    if (e == cudaSuccess) e = p->W.ensure((size_t)g->n_edges * p->w_ld + 1);
-    if (e == cudaSuccess && g->n_edges > 0) {
-      w_build_kernel<<<148 * 16, 256>>>(g->n_edges, n, p->w_ld, et.p, ct.p, p->W.p);
-      e = cudaGetLastError();
-      if (e == cudaSuccess) e = cudaDeviceSynchronize();
-    }
-    et.release();
-    ct.release();
+    p->w_ready = p->w_explicit = true;
+  } else if (!g->edge_theta || !g->ctl_theta || (n % 2) != 0 || n < 32) {
+    return fail(KFBI_E_CONFIG, "device W build needs edge_theta / ctl_theta and an even n_ctl >= 32");
   }
   UP(edge_axis, reinterpret_cast<const signed char *>(g->edge_axis), g->n_edges);
   UP(rec_edge, g->rec_edge, g->n_rec);
@@ -1053,8 +1163,25 @@ kfbi_status kfbi_plan_set_geometry(kfbi_plan *p, const kfbi_geometry *g) {
   return KFBI_OK;
 }
 
+kfbi_status kfbi_plan_set_interp(kfbi_plan *p, int32_t mode) {
+  KFBI_TRY(check_plan(p));
+  if (mode < 0 || mode > 2) return fail(KFBI_E_CONFIG, "interp mode: 0 auto, 1 W rows, 2 spectral");
+  if (mode == 2 && p->has_geo && (!p->spec_ok || p->w_explicit))
+    return fail(KFBI_E_CONFIG, "spectral edge values need the reference's equispaced controls and even n >= 32");
+  p->interp_mode = mode;
+  return KFBI_OK;
+}
+
+kfbi_status kfbi_plan_get_interp(kfbi_plan *p, int32_t *spectral) {
+  KFBI_TRY(check_geo(p));
+  if (!spectral) return fail(KFBI_E_CONFIG, "null argument");
+  *spectral = use_spectral(p) ? 1 : 0;
+  return KFBI_OK;
+}
+
 kfbi_status kfbi_plan_copy_w(kfbi_plan *p, int32_t row0, int32_t nrows, double *out) {
   KFBI_TRY(check_geo(p));
+  KFBI_TRY(ensure_w(p));
   if (!out || row0 < 0 || nrows < 0 || row0 + nrows > p->n_edges)
     return fail(KFBI_E_CONFIG, "copy_w: bad row range");
   cudaError_t e = cudaMemcpy2D(out, (size_t)p->n_ctl * sizeof(double), p->W.p + (size_t)row0 * p->w_ld,

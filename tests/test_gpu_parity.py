@@ -273,3 +273,37 @@ def test_device_w_build_matches_host_rows(name):
     assert ws.device_w
     dev = ws.plan.copy_w(0, ws.w_edges.shape[0])
     assert np.max(np.abs(dev - ws.w_edges)) < 1e-14
+
+
+@pytest.mark.parametrize("cplx", [False, True], ids=["f64", "c128"])
+@pytest.mark.parametrize("name", ["flower128", "ellipse128", "pistar128"])
+def test_spectral_edge_values_match_w_rows(name, cplx):
+    # matrix-free edge values (kfbi_plan_set_interp auto = spectral) against
+    # the W rows on the device and W . JM on the host (interface.py:224)
+    import torch
+
+    box, m, curve = setup_cases()[name]
+    ws = k.InterfaceWorkspace(k.build_grid(box, m, curve))
+    plan = ws.plan
+    plan.set_interp("spectral")
+    assert plan.spectral_edges
+    n, ne = ws.cps.m, ws.w_edges.shape[0]
+    rng = np.random.default_rng(7)
+    jm = rng.standard_normal((6, n)) * np.array([1, 10, 10, 100, 100, 100])[:, None]
+    if cplx:
+        jm = jm + 1j * rng.standard_normal((6, n))
+    jm_d = torch.from_numpy(np.ascontiguousarray(jm)).cuda()
+    out = {}
+    for mode in ("spectral", "w"):
+        plan.set_interp(mode)
+        jv = torch.empty(3 * ne, dtype=jm_d.dtype, device="cuda")
+        plan.edge_values(jm_d, jv)
+        out[mode] = jv.cpu().numpy().reshape(ne, 3)
+    plan.set_interp("auto")
+    axis = ws.geometry.edge_axis
+    host = np.empty((ne, 3), dtype=jm.dtype)
+    host[:, 0] = ws.w_edges @ jm[0]
+    host[:, 1] = np.where(axis == 0, ws.w_edges @ jm[1], ws.w_edges @ jm[2])
+    host[:, 2] = np.where(axis == 0, ws.w_edges @ jm[3], ws.w_edges @ jm[5])
+    assert rel_linf(out["w"], host) < 1e-13
+    assert rel_linf(out["spectral"], host) < 1e-12
