@@ -37,14 +37,14 @@ namespace kfbi {
 template <int LOGN>
 KFBI_DEV void stage(const reg::View<LOGN> &sm, const double2 (&v)[reg::E], int t) {
 #pragma unroll
-  for (int m = 0; m < reg::E; ++m) sm[t + m * reg::Cfg<LOGN>::T] = v[m];
+  for (int m = 0; m < reg::E; ++m) sm.xc(t, reg::sw(t), m * reg::Cfg<LOGN>::T) = v[m];
 }
 
 // write out[c] (index 16 t + c) to the sequence's smem in natural order
 template <int LOGN>
 KFBI_DEV void unstage(const reg::View<LOGN> &sm, const double2 (&out)[reg::E], int t) {
 #pragma unroll
-  for (int c = 0; c < reg::E; ++c) sm[reg::E * t + c] = out[c];
+  for (int c = 0; c < reg::E; ++c) sm.xc(reg::E * t, reg::sw(reg::E * t), c) = out[c];
 }
 
 // x staged in sm -> C = DST-I(x) in out[c] (index 16 t + c).  Entry: staged
@@ -134,17 +134,34 @@ rows_fwd_reg(BoxArgs a, const void *__restrict__ rhs, double sign,
   if (valid) {
     // panel stores: consecutive lanes write consecutive 16-byte pieces of a
     // panel's (row j0, row j0+1) 64-byte chunk (real) / 32-byte row (complex)
+    // (i = t + kk TT: the shared-memory slots are t's plus a constant)
+    const int ts = reg::sw(t);
     if (!CPLX) {
-      for (int i = t; i < M; i += TT) {          // M/4 panels x 4 pieces
+      const int n0t = (t & ~3) | ((t & 1) << 1);   // slot pair of piece t
+      const int s0 = reg::sw(n0t), s1 = reg::sw(n0t + 1);
+#pragma unroll
+      for (int kk = 0; kk < M / TT; ++kk) {      // M/4 panels x 4 pieces
+        const int i = t + kk * TT;
         const int pp = i >> 2, part = i & 3, row = part >> 1;
-        const int n0 = 4 * pp + 2 * (part & 1);
-        const double2 v0 = sm[n0], v1 = sm[n0 + 1];
+        // n0(i) = n0(t) + kk TT needs TT % 4 == 0 (M >= 64); else the plain index
+        double2 v0, v1;
+        if constexpr (TT % 4 == 0) {
+          v0 = sm.xc(n0t, s0, kk * TT);
+          v1 = sm.xc(n0t + 1, s1, kk * TT);
+        } else {
+          const int n0 = 4 * pp + 2 * (part & 1);
+          v0 = sm[n0];
+          v1 = sm[n0 + 1];
+        }
         *rows_fwd_dst(a, pp, r0 + row, part & 1) =
             row ? make_double2(v0.y, v1.y) : make_double2(v0.x, v1.x);
       }
     } else {
-      for (int i = t; i < M; i += TT)            // M/2 panels x 2 pieces
-        *rows_fwd_dst(a, i >> 1, r0, i & 1) = sm[i];
+#pragma unroll
+      for (int kk = 0; kk < M / TT; ++kk) {      // M/2 panels x 2 pieces
+        const int i = t + kk * TT;
+        *rows_fwd_dst(a, i >> 1, r0, i & 1) = sm.xc(t, ts, kk * TT);
+      }
     }
   }
   if constexpr (C::CL > 1) reg::seq_sync<LOGN>();   // keep the cluster's smem alive
@@ -224,7 +241,8 @@ __global__ void __launch_bounds__(reg::Cfg<LOGN>::CTA_T, reg::Cfg<LOGN>::MINB) c
     unstage<LOGN>(sm, out, t);
     reg::seq_sync<LOGN>();
     if (valid)
-      for (int n = t; n < M; n += TT) out_at(n) = sm[n];
+#pragma unroll
+      for (int kk = 0; kk < M / TT; ++kk) out_at(t + kk * TT) = sm.xc(t, reg::sw(t), kk * TT);
   }
   if constexpr (C::CL > 1) reg::seq_sync<LOGN>();
 }
@@ -289,10 +307,13 @@ rows_inv_reg(BoxArgs a, void *__restrict__ u) {
       double *U = static_cast<double *>(u);
       double *u0 = U + (size_t)r0 * stride;
       double *u1 = u0 + stride;
-      for (int n = t; n <= M; n += TT) {
+#pragma unroll
+      for (int kk = 0; kk <= M / TT; ++kk) {
+        const int n = t + kk * TT;
+        if (n > M) break;
         double x = 0.0, y = 0.0;
         if (n >= 1 && n < M) {
-          const double2 w = sm[n];
+          const double2 w = sm.xc(t, reg::sw(t), kk * TT);
           x = j0 ? w.x : 0.0;
           y = w.y;
         }
@@ -303,8 +324,11 @@ rows_inv_reg(BoxArgs a, void *__restrict__ u) {
     } else {
       double2 *U = static_cast<double2 *>(u);
       double2 *u0 = U + (size_t)r0 * stride;
-      for (int n = t; n <= M; n += TT) {
-        u0[n] = (n >= 1 && n < M && j0) ? sm[n] : make_double2(0.0, 0.0);
+#pragma unroll
+      for (int kk = 0; kk <= M / TT; ++kk) {
+        const int n = t + kk * TT;
+        if (n > M) break;
+        u0[n] = (n >= 1 && n < M && j0) ? sm.xc(t, reg::sw(t), kk * TT) : make_double2(0.0, 0.0);
         if (last) u0[stride + n] = make_double2(0.0, 0.0);
       }
     }

@@ -90,6 +90,16 @@ struct View {
     if constexpr (C::CL == 1) return p[0][sw(i)];
     else return p[i / C::LOCAL][sw(i & (C::LOCAL - 1))];
   }
+  // Element x + c for a per-thread x (xs = sw(x)) and a c that is constant
+  // after unrolling, with disjoint bits (x + c = x ^ c).  sw is linear over
+  // GF(2), so sw(x + c) = xs ^ sw(c), and above bit 2 the XOR is an add: one
+  // XOR with a small constant and an immediate offset instead of the full
+  // swizzle per access (the integer work was ~40 % of the DST kernels'
+  // instructions).
+  KFBI_DEV double2 &xc(int x, int xs, int c) const {
+    if constexpr (C::CL == 1) return p[0][(xs ^ ((((c >> 3) ^ (c >> 6)) & 7) ^ (c & 7))) + (c & ~7)];
+    else return (*this)[x + c];
+  }
 };
 
 // View of the calling thread's sequence and its logical thread index t.
@@ -266,8 +276,9 @@ KFBI_DEV void stockham_pass(double2 (&v)[E], const View<LOGN> &sm, int t,
       for (int r = 0; r < R; ++r) v[i + r * B] = a[r];
     } else {
       const int base = (b - k) * R + k;
+      const int bs = sw(base);
 #pragma unroll
-      for (int r = 0; r < R; ++r) sm[base + r * NS] = a[r];
+      for (int r = 0; r < R; ++r) sm.xc(base, bs, r * NS) = a[r];
     }
   }
 }
@@ -284,7 +295,7 @@ KFBI_DEV void fft_passes(double2 (&v)[E], const View<LOGN> &sm, int t,
   if constexpr (PASS + 1 < C::P) {
     seq_sync<LOGN>();
 #pragma unroll
-    for (int m = 0; m < E; ++m) v[m] = sm[t + m * C::T];
+    for (int m = 0; m < E; ++m) v[m] = sm.xc(t, sw(t), m * C::T);
     seq_sync<LOGN>();
     fft_passes<LOGN, PASS + 1, TWS, KEEP>(v, sm, t, twg, tw);
   }
@@ -335,7 +346,7 @@ KFBI_DEV void pre_from_smem(double2 (&v)[E], const View<LOGN> &sm, int t,
 #pragma unroll
   for (int m = 0; m < E; ++m) {
     const int j = t + m * T;
-    const double2 xj = sm[j];
+    const double2 xj = sm.xc(t, sw(t), m * T);
     const double2 xr = sm[(N - j) & (N - 1)];       // j = 0 -> x_0 = 0
     const double s = __ldg(&sinv[j]);
     const double2 a = cadd(xj, xr), d = csub(xj, xr);
@@ -359,7 +370,7 @@ KFBI_DEV void post(const View<LOGN> &sm, int t, double2 (&out)[E],
 #pragma unroll
   for (int c = 0; c < E / 2; ++c) {
     const int k = (E / 2) * t + c;
-    const double2 zk = sm[k];
+    const double2 zk = sm.xc((E / 2) * t, sw((E / 2) * t), c);
     const double2 zm = sm[(N - k) & (N - 1)];
     const double2 d = csub(zk, zm);
     const double2 id = make_double2(-d.y, d.x);        // i (Z_k - Z_{N-k})
@@ -468,20 +479,20 @@ KFBI_DEV void dst_transposed(const View<LOGN> &sm, int t, const double2 (&w)[E],
     if (j == 0) {
       sm[0] = sj;
     } else {
-      sm[j] = cadd(sj, iw);
+      sm.xc((E / 2) * t, sw((E / 2) * t), c) = cadd(sj, iw);
       sm[N - j] = csub(sj, iw);
     }
   }
   if (t == 0) sm[N / 2] = make_double2(0.0, 0.0);
   seq_sync<LOGN>();
 #pragma unroll
-  for (int m = 0; m < E; ++m) v[m] = sm[t + m * T];
+  for (int m = 0; m < E; ++m) v[m] = sm.xc(t, sw(t), m * T);
   seq_sync<LOGN>();
   fft_keep<LOGN>(v, sm, t, twg);
   // P: C_j = s_j (Y_j + Y_{N-j}) + (Y_j - Y_{N-j}) / 2
   seq_sync<LOGN>();
 #pragma unroll
-  for (int m = 0; m < E; ++m) sm[t + m * T] = v[m];
+  for (int m = 0; m < E; ++m) sm.xc(t, sw(t), m * T) = v[m];
   seq_sync<LOGN>();
 #pragma unroll
   for (int m = 0; m < E; ++m) {
@@ -533,7 +544,7 @@ KFBI_DEV double2 pre_dct(double2 (&v)[E], const View<LOGN> &sm, int t,
 #pragma unroll
   for (int m = 0; m < E; ++m) {
     const int j = t + m * T;
-    const double2 xj = sm[j];
+    const double2 xj = sm.xc(t, sw(t), m * T);
     const double2 xr = j == 0 ? xN : sm[N - j];
     const double s = __ldg(&sinv[j]);
     const double2 a = cadd(xj, xr), d = csub(xj, xr);
