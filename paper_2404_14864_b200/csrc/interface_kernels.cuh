@@ -76,6 +76,123 @@ KFBI_DEV double2 warp_reduce_T(double2 v) {
   return make_double2(warp_sum(v.x), warp_sum(v.y));
 }
 
+// Jump system of control point i given phi_ss (the epilogue of jumps_d2).
+template <typename T>
+struct JumpArgs {
+  const T *phi, *psi, *phi_s, *psi_s, *f_gamma;
+  double fg_sign, kre, kim;
+  T *jm;
+};
+
+template <typename T>
+KFBI_DEV void jump_system(const CtlGeom &g, const JumpArgs<T> &a, int i, T pss) {
+  using S = Sc<T>;
+  const T ju = a.phi ? a.phi[i] : S::zero();
+  const T ps = a.phi ? a.phi_s[i] : S::zero();
+  const T pv = a.psi ? a.psi[i] : S::zero();
+  const T pvs = a.psi ? a.psi_s[i] : S::zero();
+  const double t1 = g.tangent[2 * i], t2 = g.tangent[2 * i + 1];
+  const double dt1 = g.dtan_ds[2 * i], dt2 = g.dtan_ds[2 * i + 1];
+  const T jx = S::add(S::rmul(ps, t1), S::rmul(pv, t2));
+  const T jy = S::sub(S::rmul(ps, t2), S::rmul(pv, t1));
+  const T r0 = S::sub(S::sub(pss, S::rmul(jx, dt1)), S::rmul(jy, dt2));
+  const T r1 = S::add(S::sub(pvs, S::rmul(jx, dt2)), S::rmul(jy, dt1));
+  const T r2 = S::add(S::rmul(a.f_gamma[i], a.fg_sign), S::kmul(a.kre, a.kim, ju));
+  const double *A = g.inv3 + 9 * i;
+  const int n = g.n;
+  T *jm = a.jm;
+  jm[i] = ju;
+  jm[n + i] = jx;
+  jm[2 * n + i] = jy;
+#pragma unroll
+  for (int r = 0; r < 3; ++r) {
+    T v = S::add(S::add(S::rmul(r0, A[3 * r]), S::rmul(r1, A[3 * r + 1])), S::rmul(r2, A[3 * r + 2]));
+    jm[(3 + r) * n + i] = v;
+  }
+}
+
+// Circulant derivatives through shared memory: out_i = (sum_j D[(i-j) mod n]
+// v_j) / speed_i for NV vectors (the spectral d/dtheta of geometry.py:415-426
+// as its circulant column).  CTA = CIRC_OUT outputs x CIRC_CH control chunks;
+// a thread keeps 4 consecutive outputs of one chunk with a sliding window of
+// D (one D and NV v reads per 4 NV FMAs); the chunk partials are added in
+// chunk order.  JUMPS: the jump system runs as the epilogue (jumps_d2).
+constexpr int CIRC_OUT = 16, CIRC_CH = 64;
+template <typename T>
+inline size_t circ_smem_bytes(int n, int nv) {
+  return ((size_t)((n + 1) & ~1)) * sizeof(double) + (size_t)nv * n * sizeof(T) +
+         (size_t)CIRC_CH * nv * CIRC_OUT * sizeof(T);
+}
+
+template <typename T, int NV, bool JUMPS>
+__global__ void __launch_bounds__(256)
+circ_block_kernel(CtlGeom g, const T *__restrict__ v0, const T *__restrict__ v1, T *o0, T *o1,
+                  JumpArgs<T> ja, const int *done) {
+  using S = Sc<T>;
+  extern __shared__ __align__(16) unsigned char circ_sm[];
+  if (done && *done) return;
+  const int n = g.n, tid = threadIdx.x;
+  double *Ds = reinterpret_cast<double *>(circ_sm);
+  T *vs = reinterpret_cast<T *>(Ds + ((n + 1) & ~1));
+  T *red = vs + NV * n;
+  const bool have = v0 != nullptr;
+  for (int i = tid; i < n; i += blockDim.x) {
+    Ds[i] = g.deriv_col[i];
+    if (have) {
+      vs[i] = v0[i];
+      if (NV == 2) vs[n + i] = v1[i];
+    }
+  }
+  __syncthreads();
+  const int q = tid & 3, c = tid >> 2;
+  const int i0 = blockIdx.x * CIRC_OUT, ib = i0 + 4 * q;
+  const int j0 = (int)((long)n * c / CIRC_CH), j1 = (int)((long)n * (c + 1) / CIRC_CH);
+  T acc[NV][4];
+#pragma unroll
+  for (int v = 0; v < NV; ++v)
+#pragma unroll
+    for (int r = 0; r < 4; ++r) acc[v][r] = S::zero();
+  if (have) {
+    double w[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) w[r] = Ds[(((ib + r - j0) % n) + n) % n];
+    for (int j = j0; j < j1; ++j) {
+      const T x0 = vs[j];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) acc[0][r] = S::add(acc[0][r], S::rmul(x0, w[r]));
+      if constexpr (NV == 2) {
+        const T x1 = vs[n + j];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) acc[1][r] = S::add(acc[1][r], S::rmul(x1, w[r]));
+      }
+      w[3] = w[2];
+      w[2] = w[1];
+      w[1] = w[0];
+      int idx = ib - j - 1;
+      if (idx < 0) idx += n;
+      w[0] = Ds[idx];
+    }
+  }
+#pragma unroll
+  for (int v = 0; v < NV; ++v)
+#pragma unroll
+    for (int r = 0; r < 4; ++r) red[(c * NV + v) * CIRC_OUT + 4 * q + r] = acc[v][r];
+  __syncthreads();
+  if (tid < NV * CIRC_OUT) {
+    const int v = tid / CIRC_OUT, o = tid - v * CIRC_OUT, i = i0 + o;
+    if (i < n) {
+      T sum = red[v * CIRC_OUT + o];
+      for (int cc = 1; cc < CIRC_CH; ++cc) sum = S::add(sum, red[(cc * NV + v) * CIRC_OUT + o]);
+      sum = rdiv(sum, g.speed[i]);
+      if constexpr (JUMPS) {
+        jump_system<T>(g, ja, i, have ? sum : S::zero());
+      } else {
+        (v == 0 ? o0 : o1)[i] = sum;
+      }
+    }
+  }
+}
+
 // phi_s (and psi_s when psi != nullptr).
 template <typename T>
 __global__ void jumps_d1_kernel(CtlGeom g, const T *__restrict__ phi, const T *__restrict__ psi,

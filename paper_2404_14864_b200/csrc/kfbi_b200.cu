@@ -509,6 +509,39 @@ kfbi_status jumps_T(kfbi_plan *p, double kre, double kim, const void *phi, const
   T *ps = reinterpret_cast<T *>(p->psi_s.p);
   const T *ph = static_cast<const T *>(phi);
   const T *pv = static_cast<const T *>(psi);
+  // shared-memory circulant kernels when both vectors and D fit (n_ctl up to
+  // ~5,000); the warp-per-output kernels otherwise (C5)
+  static int optin = 0;
+  static bool attr = false;
+  if (!attr) {
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, p->device);
+    KFBI_CUDA(cudaFuncSetAttribute(circ_block_kernel<T, 2, false>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, optin), "jumps-and-corrections");
+    KFBI_CUDA(cudaFuncSetAttribute(circ_block_kernel<T, 1, false>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, optin), "jumps-and-corrections");
+    KFBI_CUDA(cudaFuncSetAttribute(circ_block_kernel<T, 1, true>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, optin), "jumps-and-corrections");
+    attr = true;
+  }
+  const int n = p->n_ctl;
+  if (circ_smem_bytes<T>(n, 2) <= (size_t)optin) {
+    const int cb = (n + CIRC_OUT - 1) / CIRC_OUT;
+    JumpArgs<T> ja{ph, pv, d1, ps, static_cast<const T *>(fg), fg_sign, kre, kim, static_cast<T *>(jm)};
+    if (ph && pv) {
+      KFBI_TRY(launch(p, KFBI_K_JUMPS, s, [&] {
+        circ_block_kernel<T, 2, false><<<cb, 256, circ_smem_bytes<T>(n, 2), s>>>(g, ph, pv, d1, ps, ja, done);
+      }));
+    } else if (ph || pv) {
+      KFBI_TRY(launch(p, KFBI_K_JUMPS, s, [&] {
+        circ_block_kernel<T, 1, false><<<cb, 256, circ_smem_bytes<T>(n, 1), s>>>(
+            g, ph ? ph : pv, nullptr, ph ? d1 : ps, nullptr, ja, done);
+      }));
+    }
+    return launch(p, KFBI_K_JUMPS, s, [&] {
+      circ_block_kernel<T, 1, true><<<cb, 256, circ_smem_bytes<T>(n, 1), s>>>(
+          g, ph ? d1 : nullptr, nullptr, nullptr, nullptr, ja, done);
+    });
+  }
   KFBI_TRY(launch(p, KFBI_K_JUMPS, s, [&] {
     jumps_d1_kernel<T><<<blocks, 32 * warps_per_block, 0, s>>>(g, ph, pv, d1, ps, done);
   }));
