@@ -1226,6 +1226,119 @@ op_solve_pair_kernel(OpSolveArgs a, const double *__restrict__ Tcm, double *A, d
   }
 }
 
+// c128 operator sweeps for R <= 16 rows per CTA: half-warp h of warp w works
+// on columns 2w + h + 32 s, lane l of the half on row l (one 16-byte complex),
+// so 16 lanes stay busy where the one-row-per-lane kernel above keeps R of 32.
+// Same accumulation order per row as op_solve_kernel<double2> (register,
+// shared, streamed columns in increasing order within a lane's column set);
+// same sweep semantics and convergence protocol.
+template <int K>
+__global__ void __launch_bounds__(OP_THREADS, 1)
+op_solve_half_kernel(OpSolveArgs a, const double2 *__restrict__ Tcm, double2 *A, double2 *B,
+                     const double2 *__restrict__ phi0, const double2 *__restrict__ trace1,
+                     const double2 *__restrict__ g) {
+  extern __shared__ __align__(16) unsigned char op_smem[];
+  __shared__ double res_s;
+  const int n = a.n, R = a.rows, Cs = a.smem_cols;
+  double2 *d = reinterpret_cast<double2 *>(op_smem);     // phi_in - phi0, [n]
+  double2 *part = d + ((n + 1) & ~1);                    // [OP_WARPS][32]
+  double2 *cache = part + OP_WARPS * 32;                 // [Cs][R], column-major
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int hl = lane & 15, hf = lane >> 4;
+  const int r0 = blockIdx.x * R;
+  const int nr = max(0, min(R, n - r0));
+  const bool rok = hl < nr;
+  const int creg = min(n, 2 * OP_WARPS * K);
+  const int cs0 = creg, cg0 = min(n, creg + Cs);
+  const int c_off = 2 * warp + hf;
+  double2 treg[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const int c = c_off + 2 * OP_WARPS * k;
+    treg[k] = (rok && c < creg) ? Tcm[(size_t)c * n + r0 + hl] : make_double2(0.0, 0.0);
+  }
+  for (int i = tid; i < (cg0 - cs0) * R; i += OP_THREADS) {
+    const int c = cs0 + i / R, r = i - (i / R) * R;
+    cache[i] = r < nr ? Tcm[(size_t)c * n + r0 + r] : make_double2(0.0, 0.0);
+  }
+  if (a.st->done) return;
+  for (int idx = a.first_idx; idx < a.max_iter; ++idx) {
+    const double2 *in = (idx & 1) ? A : B;
+    double2 *out = (idx & 1) ? B : A;
+    for (int q0 = 0; q0 < n; q0 += OP_THREADS * 4) {
+      double2 vi[4], v0[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int p = q0 + tid + u * OP_THREADS;
+        vi[u] = p < n ? __ldcg(in + p) : make_double2(0.0, 0.0);
+        v0[u] = p < n ? __ldg(phi0 + p) : make_double2(0.0, 0.0);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int p = q0 + tid + u * OP_THREADS;
+        if (p < n) d[p] = csub(vi[u], v0[u]);
+      }
+    }
+    __syncthreads();
+    double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const int c = c_off + 2 * OP_WARPS * k;
+      if (c < creg) acc = cadd(acc, cmul(treg[k], d[c]));
+    }
+    if (rok)
+      for (int c = cs0 + c_off; c < cg0; c += 2 * OP_WARPS)
+        acc = cadd(acc, cmul(cache[(size_t)(c - cs0) * R + hl], d[c]));
+    constexpr int U = 8;
+    for (int c = cg0 + c_off; c < n; c += 2 * OP_WARPS * U) {
+      double2 v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int cc = c + 2 * OP_WARPS * u;
+        v[u] = (rok && cc < n) ? __ldcg(Tcm + (size_t)cc * n + r0 + hl) : make_double2(0.0, 0.0);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int cc = c + 2 * OP_WARPS * u;
+        if (cc < n) acc = cadd(acc, cmul(v[u], d[cc]));
+      }
+    }
+    acc.x += __shfl_xor_sync(0xffffffffu, acc.x, 16);
+    acc.y += __shfl_xor_sync(0xffffffffu, acc.y, 16);
+    if (hf == 0) part[warp * 32 + hl] = acc;
+    __syncthreads();
+    double mag = 0.0;
+    if (tid < 32 && tid < nr) {
+      const int q = r0 + tid;
+      double2 s2 = part[tid];
+      for (int w = 1; w < OP_WARPS; ++w) s2 = cadd(s2, part[w * 32 + tid]);
+      const double2 trace = cadd(trace1[q], s2);
+      const double2 upd = cscale(csub(g[q], trace), a.gamma);
+      out[q] = cadd(__ldcg(in + q), upd);
+      mag = hypot(upd.x, upd.y);
+    }
+    if (warp == 0) {
+      mag = warp_nanmax(mag);
+      if (lane == 0) {
+        atomic_max_nonneg(&a.slots[idx % 3], mag);
+        if (blockIdx.x == 0) a.slots[(idx + 1) % 3] = 0ull;
+      }
+    }
+    op_barrier(a, idx, &res_s);
+    const double res = res_s;
+    const bool conv = res <= a.tol;
+    const bool last = conv || idx + 1 >= a.max_iter;
+    if (blockIdx.x == 0 && tid == 0) {
+      a.history[idx] = res;
+      a.st->iters = idx + 1;
+      a.st->last_res = res;
+      if (conv) a.st->done = 1;
+      else if (idx + 1 >= a.max_iter) a.st->done = 2;
+    }
+    if (last) break;
+  }
+}
+
 // Extraction writing the BvpSolution traces (u+, d_n u+) of a final field.
 template <typename T>
 __global__ void __launch_bounds__(256)
