@@ -431,14 +431,21 @@ spec_block_kernel(int n, int K, const T *__restrict__ jm, double2 *__restrict__ 
                   double2 *__restrict__ spec, unsigned int *counters) {
   constexpr int NP = std::is_same<T, double2>::value ? 2 : 1;
   constexpr int R = SPEC_COLS * NP;
-  extern __shared__ double2 red_sm[];                   // [W][R][32]
+  extern __shared__ double2 red_sm[];                   // [W][R][32], then the staged columns
   __shared__ bool last;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int Y = gridDim.y, y = blockIdx.y;
   auto red = [&](int x, int r) -> double2 & { return red_sm[((size_t)x * R + r) * 32 + lane]; };
   const int k = blockIdx.x * 32 + lane;
-  const long part_id = (long)y * nw + w, nparts = (long)Y * nw;
-  const int j0 = (int)(n * part_id / nparts), j1 = (int)(n * (part_id + 1) / nparts);
+  // the CTA's control range, staged column-major [SPEC_COLS][jn] in shared memory
+  const int cj0 = (int)((long)n * y / Y), cj1 = (int)((long)n * (y + 1) / Y), jn = cj1 - cj0;
+  T *fs = reinterpret_cast<T *>(red_sm + (size_t)nw * R * 32);
+  for (int i = threadIdx.x; i < SPEC_COLS * jn; i += blockDim.x) {
+    const int c = i / jn, j = i - c * jn;
+    fs[i] = jm[(size_t)spec_jm_col(c) * n + cj0 + j];
+  }
+  __syncthreads();
+  const int j0 = cj0 + (int)((long)jn * w / nw), j1 = cj0 + (int)((long)jn * (w + 1) / nw);
   double2 acc[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) acc[r] = make_double2(0.0, 0.0);
@@ -447,16 +454,16 @@ spec_block_kernel(int n, int K, const T *__restrict__ jm, double2 *__restrict__ 
     sincospi(-2.0 * (double)k / n, &ss, &cs);
     const double2 step = make_double2(cs, ss);
     double2 wk = make_double2(1.0, 0.0);
+    int idx = (int)(((long)j0 * k) % n);                 // j k mod n, advanced by k per control
     for (int j = j0; j < j1; ++j) {
       if (((j - j0) & 31) == 0) {
-        const long idx = ((long)j * k) % n;
         double sw, cw;
         sincospi(-2.0 * (double)idx / n, &sw, &cw);
         wk = make_double2(cw, sw);
       }
 #pragma unroll
       for (int c = 0; c < SPEC_COLS; ++c) {
-        const T v = __ldg(&jm[(size_t)spec_jm_col(c) * n + j]);
+        const T v = fs[c * jn + (j - cj0)];
         if constexpr (NP == 1) {
           acc[c].x = fma(v, wk.x, acc[c].x);
           acc[c].y = fma(v, wk.y, acc[c].y);
@@ -468,6 +475,8 @@ spec_block_kernel(int n, int K, const T *__restrict__ jm, double2 *__restrict__ 
         }
       }
       wk = cmul(wk, step);
+      idx += k;
+      if (idx >= n) idx -= n;
     }
   }
 #pragma unroll

@@ -591,15 +591,24 @@ kfbi_status edges_spectral(kfbi_plan *p, const void *jm, void *jv, const int *do
     KFBI_CUDA(cudaFuncSetAttribute(edges_spectral_res_kernel<T, EB>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, optin), "jumps-and-corrections");
     KFBI_CUDA(cudaFuncSetAttribute(spec_block_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)(16 * R * 32 * sizeof(double2))), "jumps-and-corrections");
+                                   optin - 1024), "jumps-and-corrections");
     attr = true;
   }
   const int n = p->n_ctl, K = n / 2 + 1;
   const int kb = (K + 31) / 32;
+#ifdef KFBI_SPEC_Y
+  int Y = KFBI_SPEC_Y;
+#else
   int Y = (2 * sms) / kb;
   Y = Y < 1 ? 1 : (Y > 8 ? 8 : Y);
+#endif
+  // the staged control range of a CTA must fit next to the reduction buffer
+  const size_t red_bytes = (size_t)16 * R * 32 * sizeof(double2);
+  while ((size_t)SPEC_COLS * ((n + Y - 1) / Y + 1) * sizeof(T) + red_bytes > (size_t)(optin - 1024) && Y < 64)
+    ++Y;
+  const size_t spec_smem = red_bytes + (size_t)SPEC_COLS * ((n + Y - 1) / Y + 1) * sizeof(T);
   cudaError_t e = p->spec.ensure((size_t)2 * SPEC_COLS * K);
-  if (e == cudaSuccess) e = p->spec_part.ensure((size_t)8 * 2 * SPEC_COLS * K);
+  if (e == cudaSuccess) e = p->spec_part.ensure((size_t)Y * 2 * SPEC_COLS * K);
   if (e == cudaSuccess && p->spec_ctr.n < (size_t)kb) {
     e = p->spec_ctr.ensure((size_t)kb);
     if (e == cudaSuccess) e = cudaMemset(p->spec_ctr.p, 0, (size_t)kb * sizeof(unsigned int));
@@ -607,7 +616,7 @@ kfbi_status edges_spectral(kfbi_plan *p, const void *jm, void *jv, const int *do
   if (e != cudaSuccess) return fail(KFBI_E_CUDA, std::string("spectral edges: ") + cudaGetErrorString(e));
   if (p->n_edges == 0) return KFBI_OK;
   KFBI_TRY(launch(p, KFBI_K_JUMPS, s, [&] {
-    spec_block_kernel<T><<<dim3(kb, Y), 512, 16 * R * 32 * sizeof(double2), s>>>(
+    spec_block_kernel<T><<<dim3(kb, Y), 512, spec_smem, s>>>(
         n, K, static_cast<const T *>(jm), p->spec_part.p, p->spec.p, p->spec_ctr.p);
   }));
   const int ngroups = p->n_perm / EB;
