@@ -1100,7 +1100,7 @@ op_solve_kernel(OpSolveArgs a, const T *__restrict__ Tcm, T *A, T *B,
 // each instruction covers two columns (half the instructions of the one-row
 // kernel above, which remains the complex / odd-n path).  Same sweep
 // semantics, same convergence protocol.  Requires n and R even.
-template <int K2>
+template <int K2, int G>
 __global__ void __launch_bounds__(OP_THREADS, 1)
 op_solve_pair_kernel(OpSolveArgs a, const double *__restrict__ Tcm, double *A, double *B,
                      const double *__restrict__ phi0, const double *__restrict__ trace1,
@@ -1112,13 +1112,16 @@ op_solve_pair_kernel(OpSolveArgs a, const double *__restrict__ Tcm, double *A, d
   double *part = d + ((n + 1) & ~1);                     // [OP_WARPS][32]
   double *cache = part + OP_WARPS * 32;                  // [Cs][R], column-major
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int hl = lane & 15, hf = lane >> 4;
+  // G column groups per warp, RPL = 32 / G row pairs per group: lane l is
+  // row pair hl of group hf (G = 2: half-warps; G = 3: 10 pairs, lanes 30-31 idle)
+  constexpr int RPL = 32 / G;
+  const int hf = lane / RPL, hl = lane - hf * RPL;
   const int r0 = blockIdx.x * R;
   const int nr = max(0, min(R, n - r0));
-  const bool rok = 2 * hl < nr;
-  const int creg = min(n, 2 * OP_WARPS * K2);
+  const bool rok = hf < G && 2 * hl < nr;
+  const int creg = min(n, G * OP_WARPS * K2);
   const int cs0 = creg, cg0 = min(n, creg + Cs);
-  const int c_off = 2 * warp + hf;                       // first column of this half-warp
+  const int c_off = G * warp + hf;                       // first column of this lane group
   constexpr int PD = 8;                                  // d entries per thread and round
   double p0r[PD];                                        // phi0 of the first round, kept
 #pragma unroll
@@ -1130,7 +1133,7 @@ op_solve_pair_kernel(OpSolveArgs a, const double *__restrict__ Tcm, double *A, d
   double2 treg[K2];
 #pragma unroll
   for (int k = 0; k < K2; ++k) {
-    const int c = c_off + 2 * OP_WARPS * k;
+    const int c = c_off + G * OP_WARPS * k;
     treg[k] = (rok && c < creg) ? *reinterpret_cast<const double2 *>(Tcm + (size_t)c * n + r0 + 2 * hl)
                                 : make_double2(0.0, 0.0);
   }
@@ -1161,33 +1164,33 @@ op_solve_pair_kernel(OpSolveArgs a, const double *__restrict__ Tcm, double *A, d
     double2 acc = make_double2(0.0, 0.0);
 #pragma unroll
     for (int k = 0; k < K2; ++k) {
-      const int c = c_off + 2 * OP_WARPS * k;
-      if (c < creg) {
+      const int c = c_off + G * OP_WARPS * k;
+      if (rok && c < creg) {
         const double dc = d[c];
         acc.x = fma(treg[k].x, dc, acc.x);
         acc.y = fma(treg[k].y, dc, acc.y);
       }
     }
     if (rok)
-      for (int c = cs0 + c_off; c < cg0; c += 2 * OP_WARPS) {
+      for (int c = cs0 + c_off; c < cg0; c += G * OP_WARPS) {
         const double2 t2 = *reinterpret_cast<const double2 *>(cache + (size_t)(c - cs0) * R + 2 * hl);
         const double dc = d[c];
         acc.x = fma(t2.x, dc, acc.x);
         acc.y = fma(t2.y, dc, acc.y);
       }
     constexpr int U = 8;
-    for (int c = cg0 + c_off; c < n; c += 2 * OP_WARPS * U) {
+    for (int c = cg0 + c_off; c < n; c += G * OP_WARPS * U) {
       double2 v[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        const int cc = c + 2 * OP_WARPS * u;
+        const int cc = c + G * OP_WARPS * u;
         v[u] = (rok && cc < n)
                    ? __ldcg(reinterpret_cast<const double2 *>(Tcm + (size_t)cc * n + r0 + 2 * hl))
                    : make_double2(0.0, 0.0);
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        const int cc = c + 2 * OP_WARPS * u;
+        const int cc = c + G * OP_WARPS * u;
         if (cc < n) {
           const double dc = d[cc];
           acc.x = fma(v[u].x, dc, acc.x);
@@ -1195,9 +1198,20 @@ op_solve_pair_kernel(OpSolveArgs a, const double *__restrict__ Tcm, double *A, d
         }
       }
     }
-    // the two column halves of the warp hold partial sums of the same rows
-    acc.x += __shfl_xor_sync(0xffffffffu, acc.x, 16);
-    acc.y += __shfl_xor_sync(0xffffffffu, acc.y, 16);
+    // the G column groups of the warp hold partial sums of the same rows
+    if constexpr (G == 2) {
+      acc.x += __shfl_xor_sync(0xffffffffu, acc.x, 16);
+      acc.y += __shfl_xor_sync(0xffffffffu, acc.y, 16);
+    } else {
+      double2 tot = acc;
+#pragma unroll
+      for (int gg = 1; gg < G; ++gg) {
+        const int src = min(lane + gg * RPL, 31);
+        tot.x += __shfl_sync(0xffffffffu, acc.x, src);
+        tot.y += __shfl_sync(0xffffffffu, acc.y, src);
+      }
+      acc = tot;
+    }
     if (hf == 0) {
       part[warp * 32 + 2 * hl] = acc.x;
       part[warp * 32 + 2 * hl + 1] = acc.y;

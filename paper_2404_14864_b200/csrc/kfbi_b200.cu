@@ -844,14 +844,25 @@ kfbi_status op_solve(kfbi_plan *p, const kfbi_bvp *b, cudaStream_t s) {
     if (n % 2 == 0 && rows % 2 == 0) {
       static bool pair_attr = false;
       if (!pair_attr) {
-        KFBI_CUDA(cudaFuncSetAttribute(op_solve_pair_kernel<K2>,
+        KFBI_CUDA(cudaFuncSetAttribute(op_solve_pair_kernel<K2, 2>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin - 1024),
+                  "density-update");
+        KFBI_CUDA(cudaFuncSetAttribute(op_solve_pair_kernel<K2, 3>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin - 1024),
                   "density-update");
         pair_attr = true;
       }
+      // three column groups per warp when a CTA owns <= 20 rows (30 busy lanes
+      // instead of rows / 2 of 32); the register-cached columns grow with G
+      const int G = rows <= 20 ? 3 : 2;
+      const int cregG = n < G * OP_WARPS * K2 ? n : G * OP_WARPS * K2;
+      size_t csG = avail / ((size_t)rows * sizeof(T));
+      if (csG > (size_t)(n - cregG)) csG = (size_t)(n - cregG);
+      a.smem_cols = (int)csG;
+      const size_t smemG = fixed + csG * rows * sizeof(T);
+      const void *fn = G == 3 ? (const void *)op_solve_pair_kernel<K2, 3> : (const void *)op_solve_pair_kernel<K2, 2>;
       return launch(p, KFBI_K_DENSITY, s, [&] {
-        return cudaLaunchCooperativeKernel((const void *)op_solve_pair_kernel<K2>, dim3(grid),
-                                           dim3(OP_THREADS), args, smem, s);
+        return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(OP_THREADS), args, smemG, s);
       });
     }
   }
