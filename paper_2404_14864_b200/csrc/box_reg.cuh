@@ -195,15 +195,40 @@ __global__ void __launch_bounds__(reg::Cfg<LOGN>::CTA_T, reg::Cfg<LOGN>::MINB) c
   };
 
   double2 v[reg::E];
-#pragma unroll
-  for (int m = 0; m < reg::E; ++m) {
-    const int n = t + m * TT;
-    v[m] = (valid && n >= 1) ? at(n) : make_double2(0.0, 0.0);
-  }
-  stage<LOGN>(sm, v, t);
-  reg::seq_sync<LOGN>();
   double2 out[reg::E];
-  dst_staged<LOGN>(sm, t, a, out);
+  if constexpr (C::CL == 1) {
+    // DST-I pre-processing straight from global memory: element n and its
+    // mirror M - n (the same strip, an L2 hit for one of the two loads)
+    // instead of staging the column through shared memory
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      double2 x[reg::E / 2], xr[reg::E / 2];
+#pragma unroll
+      for (int mm = 0; mm < reg::E / 2; ++mm) {
+        const int n = t + (h * (reg::E / 2) + mm) * TT;
+        x[mm] = (valid && n >= 1) ? at(n) : make_double2(0.0, 0.0);
+        xr[mm] = (valid && n >= 1) ? at(M - n) : make_double2(0.0, 0.0);
+      }
+#pragma unroll
+      for (int mm = 0; mm < reg::E / 2; ++mm) {
+        const int n = t + (h * (reg::E / 2) + mm) * TT;
+        const double sj = __ldg(&a.sinv[n]);
+        const double2 ad = cadd(x[mm], xr[mm]), df = csub(x[mm], xr[mm]);
+        v[h * (reg::E / 2) + mm] = make_double2(fma(sj, ad.x, 0.5 * df.x), fma(sj, ad.y, 0.5 * df.y));
+      }
+    }
+    reg::fft<LOGN>(v, sm, t, a.twg);
+    reg::post<LOGN>(sm, t, out);
+  } else {
+#pragma unroll
+    for (int m = 0; m < reg::E; ++m) {
+      const int n = t + m * TT;
+      v[m] = (valid && n >= 1) ? at(n) : make_double2(0.0, 0.0);
+    }
+    stage<LOGN>(sm, v, t);
+    reg::seq_sync<LOGN>();
+    dst_staged<LOGN>(sm, t, a, out);
+  }
 
   // spectral division (boxsolve.py:74-76): (v / (lam_p + lam_q - kappa)) / (4 M^2)
 #pragma unroll
