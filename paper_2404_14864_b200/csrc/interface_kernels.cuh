@@ -971,7 +971,13 @@ constexpr int OP_THREADS = 512;
 constexpr int OP_WARPS = OP_THREADS / 32;
 template <typename T>
 struct OpTune;                    // register cache K and streamed loads in flight U
-template <> struct OpTune<double> { static constexpr int K = 24, U = 16; };
+#ifndef KFBI_OP_K_F64
+#define KFBI_OP_K_F64 24
+#endif
+#ifndef KFBI_OP_K_HALF
+#define KFBI_OP_K_HALF 12
+#endif
+template <> struct OpTune<double> { static constexpr int K = KFBI_OP_K_F64, U = 16; };
 template <> struct OpTune<double2> { static constexpr int K = 12, U = 8; };
 
 template <typename T>

@@ -869,20 +869,21 @@ kfbi_status op_solve(kfbi_plan *p, const kfbi_bvp *b, cudaStream_t s) {
   if constexpr (std::is_same<T, double2>::value) {
     // complex rows on half-warps (16 busy lanes) when a CTA owns <= 16 rows
     if (rows <= 16) {
+      constexpr int KH = KFBI_OP_K_HALF;
       static bool half_attr = false;
       if (!half_attr) {
-        KFBI_CUDA(cudaFuncSetAttribute(op_solve_half_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        KFBI_CUDA(cudaFuncSetAttribute(op_solve_half_kernel<KH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        smem_optin - 1024), "density-update");
         half_attr = true;
       }
       // twice the register-cached columns per row set: re-split the rest
-      const int creg2 = n < 2 * OP_WARPS * K ? n : 2 * OP_WARPS * K;
+      const int creg2 = n < 2 * OP_WARPS * KH ? n : 2 * OP_WARPS * KH;
       size_t cs2 = avail / ((size_t)rows * sizeof(T));
       if (cs2 > (size_t)(n - creg2)) cs2 = (size_t)(n - creg2);
       a.smem_cols = (int)cs2;
       const size_t smem2 = fixed + cs2 * rows * sizeof(T);
       return launch(p, KFBI_K_DENSITY, s, [&] {
-        return cudaLaunchCooperativeKernel((const void *)op_solve_half_kernel<K>, dim3(grid),
+        return cudaLaunchCooperativeKernel((const void *)op_solve_half_kernel<KH>, dim3(grid),
                                            dim3(OP_THREADS), args, smem2, s);
       });
     }
