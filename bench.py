@@ -23,13 +23,22 @@ fields) exceed the 126 MB L2, so no flush is needed between steps.
          so the copy engine overlaps the following steps; the timed region
          ends when every copy is done
 
+Also in the ours-line: `pipeline` (the same K steps with every Richardson
+sweep through the full pipeline, no trace operator), `operator_build_s`,
+`t1_time_to_solution_s` (a T = 1 run per equation, operator form incl. its
+build vs pipeline form), `repeats` (value = median of 5 timed regions of K
+steps each), the `roofline` of the dominant box-solve pass, and `slab_c5`
+(BASELINE configs[4]: one 16384² solve, star3 on [-π,π]², slab-decomposed
+over the N ranks, NCCL all-to-all and fused peer-store transposes).
+
 `--impl reference` times the CPU reference path (the oracle port of the
-reference package, numpy/scipy with all host threads) on the same workload,
-each step a bounded sample (one Richardson sweep per equation plus the step
-glue, scaled by the reference's steady iteration counts); rank 0 only.
+reference package, numpy/scipy with all host threads) on the same workload
+with real, untruncated time steps (one cold warm-up step per equation, then
+whole bench steps until --steps or --ref-budget-s); rank 0 only.
 
 Launch: python bench.py [--gpus N --steps K --warmup W]; for N > 1 under
-torchrun every rank runs an independent replica (weak scaling).
+torchrun every rank runs an independent replica of the 4096² workload (weak
+scaling) and all ranks share the C5 slab solve (strong scaling).
 """
 
 from __future__ import annotations
@@ -51,10 +60,6 @@ if ROOT not in sys.path:
 
 M_DEFAULT = 4096
 EQUATIONS = ("heat", "wave", "schrodinger")
-# steady Richardson sweeps per step of the reference at M=4096, tau=1/256
-# (measured with the full oracle in the build container: heat 51,35,35;
-# see profiles/cpu_oracle_4096.json); used only to scale the CPU samples
-REF_STEADY_ITERS = {"heat": 35, "wave": 16, "schrodinger": 25}
 METRIC = "KFBI time steps/sec at 4096² (heat/wave/Schrödinger); speedup vs host CPU"
 
 
@@ -205,6 +210,7 @@ def run_ours(args):
     wl = workload(m)
     backend = k.CudaBackend(local, timing=False)
     ctxs, specs, states, steppers = {}, {}, {}, {}
+    kappas, op_build_s = {}, {}
     t_setup = time.time()
     for eq in eqs:
         box, curve, kw = wl[eq]
@@ -214,11 +220,16 @@ def run_ours(args):
         startup, step = _stepper_for(specs[eq])
         steppers[eq] = step
         states[eq] = startup(specs[eq], ctxs[eq])
+        kap = {"heat": 2.0 * specs[eq].c / specs[eq].tau,
+               "wave": 1.0 / (specs[eq].theta * specs[eq].tau ** 2),
+               "schrodinger": 2j / specs[eq].tau}[eq]
+        kappas[eq] = kap
         if not args.pipeline:
-            kap = {"heat": 2.0 * specs[eq].c / specs[eq].tau,
-                   "wave": 1.0 / (specs[eq].theta * specs[eq].tau ** 2),
-                   "schrodinger": 2j / specs[eq].tau}[eq]
+            torch.cuda.synchronize()
+            t_op = time.perf_counter()
             ctxs[eq].workspace.ensure_operator(kap, eq == "schrodinger")
+            torch.cuda.synchronize()
+            op_build_s[eq] = time.perf_counter() - t_op
     torch.cuda.synchronize()
     t_setup = time.time() - t_setup
 
@@ -242,34 +253,38 @@ def run_ours(args):
     stream = torch.cuda.current_stream()
     ev = {eq: [] for eq in eqs}
     iters = {eq: [] for eq in eqs}
-    _barrier(ws)
-    torch.cuda.synchronize()
+    reps_ms = []
     with Clocks(local) as clk:
-        start = torch.cuda.Event(enable_timing=True)
-        end = torch.cuda.Event(enable_timing=True)
-        if args.profile:
-            torch.cuda.profiler.start()
-        start.record(stream)
-        for _ in range(args.steps):
-            for eq in eqs:
-                a = torch.cuda.Event(enable_timing=True)
-                b = torch.cuda.Event(enable_timing=True)
-                a.record(stream)
-                st = advance(eq)
-                b.record(stream)
-                ev[eq].append((a, b))
-                if st.log_slot is None:
-                    iters[eq].append(st.last_iterations)
-        end.record(stream)
-        torch.cuda.synchronize()
-        if args.profile:
-            torch.cuda.profiler.stop()
-    _barrier(ws)
-    elapsed_ms = start.elapsed_time(end)
-    for eq in eqs:                 # asynchronous stepping: per-step log (+ error checks)
-        if ctxs[eq].asynchronous:
-            iters[eq] = ctxs[eq].flush()
-    launches = sum(p.launch_count() for p in plans) - launches0
+        for rep in range(args.repeats):
+            _barrier(ws)
+            torch.cuda.synchronize()
+            start = torch.cuda.Event(enable_timing=True)
+            end = torch.cuda.Event(enable_timing=True)
+            if args.profile and rep == 0:
+                torch.cuda.profiler.start()
+            start.record(stream)
+            for _ in range(args.steps):
+                for eq in eqs:
+                    a = torch.cuda.Event(enable_timing=True)
+                    b = torch.cuda.Event(enable_timing=True)
+                    a.record(stream)
+                    st = advance(eq)
+                    b.record(stream)
+                    if rep == 0:
+                        ev[eq].append((a, b))
+                    if st.log_slot is None:
+                        iters[eq].append(st.last_iterations)
+            end.record(stream)
+            torch.cuda.synchronize()
+            if args.profile and rep == 0:
+                torch.cuda.profiler.stop()
+            _barrier(ws)
+            reps_ms.append(_max_over_ranks(start.elapsed_time(end), ws))
+            for eq in eqs:             # asynchronous stepping: per-step log (+ error checks)
+                if ctxs[eq].asynchronous:
+                    iters[eq].extend(ctxs[eq].flush())
+    elapsed_ms = float(np.median(reps_ms))
+    launches = (sum(p.launch_count() for p in plans) - launches0) // args.repeats
     per_eq_ms = {eq: sum(a.elapsed_time(b) for a, b in ev[eq]) / args.steps for eq in eqs}
 
     # kernel-duration pass: the same K steps again with every launch of our
@@ -286,13 +301,15 @@ def run_ours(args):
         c.flush()
     # per-kernel device times over the timed region
     kt_ms, kt_calls = {}, {}
-    cols_bytes, cols_ms, cols_calls = 0.0, 0.0, 0
+    # box-solve passes: algorithmic bytes 2 (M-1)^2 s per launch
+    pas = {n: {"bytes": 0.0, "ms": 0.0, "calls": 0} for n in ("transform-rows", "transform-cols")}
     for eq, c in ctxs.items():
         ms, calls = c.plan.kernel_times()
         cplx = eq == "schrodinger"
-        cols_bytes += calls["transform-cols"] * _bytes_cols(m, cplx)
-        cols_ms += ms["transform-cols"]
-        cols_calls += calls["transform-cols"]
+        for n in pas:
+            pas[n]["bytes"] += calls[n] * _bytes_cols(m, cplx)
+            pas[n]["ms"] += ms[n]
+            pas[n]["calls"] += calls[n]
         for name in ms:
             kt_ms[name] = kt_ms.get(name, 0.0) + ms[name]
             kt_calls[name] = kt_calls.get(name, 0) + calls[name]
@@ -300,7 +317,7 @@ def run_ours(args):
         p.set_timing(False)
     clocks = clk.summary()
 
-    elapsed_max = _max_over_ranks(elapsed_ms, ws)
+    elapsed_max = elapsed_ms
     n_time_steps = args.steps * len(eqs)
     value = n_time_steps * ws / (elapsed_max / 1e3)
 
@@ -356,12 +373,74 @@ def run_ours(args):
     e2e_ms = _max_over_ranks(s2.elapsed_time(e2), ws)
     e2e_value = n_time_steps * ws / (e2e_ms / 1e3)
 
+    # ---- pipeline form: every Richardson sweep through the full pipeline ----
+    # (jumps -> edge values -> box solve -> extraction; the algorithm of
+    # bvp.py:312-351 without the trace operator), same K steps
+    pipe = None
+    if not args.pipeline and not args.no_pipeline_pass:
+        for c in ctxs.values():
+            c.flush()
+            c.operator = False
+        for _ in range(2):
+            for eq in eqs:
+                advance(eq)
+        torch.cuda.synchronize()
+        pipe_it = {eq: [] for eq in eqs}
+        pev = {eq: [] for eq in eqs}
+        _barrier(ws)
+        torch.cuda.synchronize()
+        s3 = torch.cuda.Event(enable_timing=True)
+        e3 = torch.cuda.Event(enable_timing=True)
+        s3.record(stream)
+        for _ in range(args.steps):
+            for eq in eqs:
+                a = torch.cuda.Event(enable_timing=True)
+                b = torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                st = advance(eq)
+                b.record(stream)
+                pev[eq].append((a, b))
+                pipe_it[eq].append(st.last_iterations)
+        e3.record(stream)
+        torch.cuda.synchronize()
+        _barrier(ws)
+        pipe_ms = _max_over_ranks(s3.elapsed_time(e3), ws)
+        pipe_eq_ms = {eq: sum(a.elapsed_time(b) for a, b in pev[eq]) / args.steps for eq in eqs}
+        sweeps = sum(sum(v) for v in pipe_it.values())
+        pipe = {"value": n_time_steps * ws / (pipe_ms / 1e3), "unit": "time steps/s",
+                "ms_per_step": pipe_ms / args.steps,
+                "sweeps_per_s": sweeps * ws / (pipe_ms / 1e3),
+                "per_equation": {eq: {"steps_per_s": 1e3 / pipe_eq_ms[eq],
+                                      "ms_per_step": pipe_eq_ms[eq],
+                                      "ms_per_sweep": pipe_eq_ms[eq] / max(np.mean(pipe_it[eq]), 1),
+                                      "iterations": pipe_it[eq]} for eq in eqs}}
+        for c in ctxs.values():
+            c.operator = True
+
+    # ---- C5 (BASELINE configs[4]): one 16384^2 solve, slab-decomposed over the N ranks
+    slab = None
+    if not args.no_slab:
+        slab = {}
+        for p2p in (False, True):
+            try:
+                slab["p2p" if p2p else "nccl"] = slab_c5(args, ws, rank, local, p2p)
+            except Exception as e:          # reported, never fatal for the headline
+                slab["p2p" if p2p else "nccl"] = {"error": f"{type(e).__name__}: {e}"}
+            torch.cuda.empty_cache()
+
     if rank != 0:
         return None
-    cols_avg_ms = cols_ms / max(cols_calls, 1)
-    achieved = (cols_bytes / max(cols_calls, 1)) / (cols_avg_ms / 1e3) / 1e9 if cols_calls else 0.0
     peaks = _peaks()
-    traffic = _ncu_traffic()
+    traffic = _ncu_traffic() or {}
+    roof = {}
+    for n, v in pas.items():
+        avg = v["ms"] / max(v["calls"], 1)
+        ach = (v["bytes"] / max(v["calls"], 1)) / (avg / 1e3) / 1e9 if v["calls"] else 0.0
+        roof[n] = {"achieved": ach, "frac": ach / peaks["hbm_gbs"], "avg_launch_ms": avg,
+                   "launches": v["calls"], "ms_per_bench_step": v["ms"] / args.steps}
+    dom = max(pas, key=lambda n: pas[n]["ms"])     # the dominant kernel of the step
+    kernel_name = {"transform-rows": "rows_fwd_reg / rows_inv_reg (DST-I along x, transform-rows)",
+                   "transform-cols": "cols_tri (tridiagonal column solves, transform-cols)"}
     line = {
         "metric": METRIC,
         "value": value,
@@ -381,14 +460,15 @@ def run_ours(args):
         "kernel_ms_per_bench_step": {kname: v / args.steps for kname, v in kt_ms.items() if v},
         "kernel_calls": {kname: v for kname, v in kt_calls.items() if v},
         "roofline": {
-            "kernel": "cols_kernel (fused column DST-I / scale / DST-I, transform-cols)",
-            "bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-            "frac": achieved / peaks["hbm_gbs"] if peaks["hbm_gbs"] else None,
-            "traffic": traffic.get("cols_bytes_per_launch") if traffic else None,
+            "kernel": kernel_name[dom],
+            "bound": "hbm", "achieved": roof[dom]["achieved"], "peak": peaks["hbm_gbs"],
+            "unit": "GB/s", "frac": roof[dom]["frac"],
+            "traffic": traffic.get(dom),
             "peak_source": peaks["source"],
             "algorithmic_bytes_per_launch": {"f64": _bytes_cols(m, False),
                                              "c128": _bytes_cols(m, True)},
-            "avg_launch_ms": cols_avg_ms,
+            "avg_launch_ms": roof[dom]["avg_launch_ms"],
+            "per_pass": roof,
         },
         "e2e": {"value": e2e_value, "unit": "time steps/s", "d2h_link_GBps": d2h_gbps,
                 "h2d_bytes_per_step": h2d,
@@ -398,10 +478,91 @@ def run_ours(args):
         "setup_s": t_setup,
         "sweep_mode": "pipeline" if args.pipeline else
         "operator (sweep 1 + returned field by the full pipeline, sweeps >= 2 via the trace operator)",
+        "repeats": {"n": args.repeats, "ms_per_step": [r / args.steps for r in reps_ms],
+                    "value_is": "median of the repeats (each exactly K steps)"},
     }
+    if op_build_s:
+        line["operator_build_s"] = op_build_s
+    if pipe is not None:
+        line["pipeline"] = pipe
+        # time to solution of a T = 1 run (1/tau steps, the C4 rule) per equation:
+        # operator form incl. its one-off build vs. the pipeline form
+        n_t1 = int(round(1.0 / specs[eqs[0]].tau))
+        line["t1_time_to_solution_s"] = {
+            eq: {"steps": n_t1,
+                 "operator_incl_build": op_build_s.get(eq, 0.0) + n_t1 * per_eq_ms[eq] / 1e3,
+                 "pipeline": n_t1 * pipe["per_equation"][eq]["ms_per_step"] / 1e3}
+            for eq in eqs}
+    if slab is not None:
+        line["slab_c5"] = slab
     if not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(ctxs, specs, iters, args)
     return line
+
+
+def c5_problem(m, rank, ws, local, p2p, torch):
+    """StaticPlaneWave on star(1.5, 0.2, 3) over [-pi, pi]^2,
+    kappa = 2 / tau with tau = 0.25 * 64 / m (kappa = 2048 at m = 16384)."""
+    import paper_2404_14864_b200 as k
+    from paper_2404_14864_b200 import dist as D
+
+    tau = 0.25 * 64 / m
+    kappa = 2.0 / tau
+    geo = k.build_grid((-np.pi, np.pi, -np.pi, np.pi), m, k.StarCurve(1.5, c=0.2, lobes=3))
+    wsp = k.InterfaceWorkspace(geo, backend=k.CudaBackend(local, timing=False))
+    sol = k.StaticPlaneWave(kappa=kappa)
+    cps = wsp.cps
+    solver = D.SlabRichardson(wsp, nranks=ws, rank=rank, p2p=p2p)
+    r0, r1 = solver.rows
+    X, Y = geo.grid.X[r0:r1], geo.grid.Y[r0:r1]
+    F = torch.from_numpy(np.where(geo.classification.interior[r0:r1], sol.f(X, Y), 0.0)).cuda()
+    fg = torch.from_numpy(np.asarray(sol.f(cps.x, cps.y))).cuda()
+    g = torch.from_numpy(np.asarray(sol.dirichlet(cps.x, cps.y))).cuda()
+    wsp.plan                                   # geometry upload
+    return geo, wsp, sol, solver, F, fg, g, kappa
+
+
+def slab_c5(args, ws, rank, local, p2p):
+    """C5 solves/s over the N ranks (strong scaling) inside the headline run."""
+    import torch
+
+    m = args.slab_m
+    t0 = time.time()
+    geo, wsp, sol, solver, F, fg, g, kappa = c5_problem(m, rank, ws, local, p2p, torch)
+    torch.cuda.synchronize()
+    setup_s = time.time() - t0
+
+    def solve():
+        dens = torch.zeros(wsp.cps.m, dtype=torch.float64, device="cuda")
+        return solver.solve(kappa=kappa, F=F, f_gamma=fg, g=g, density=dens)
+
+    solve()
+    reps = max(1, args.slab_steps)
+    _barrier(ws)
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(reps):
+        out = solve()
+    b.record()
+    torch.cuda.synchronize()
+    _barrier(ws)
+    ms = _max_over_ranks(a.elapsed_time(b), ws) / reps
+    u, tu, tn, it, res, hist = out
+    r0, r1 = solver.rows
+    interior = geo.classification.interior[r0:r1]
+    X, Y = geo.grid.X[r0:r1], geo.grid.Y[r0:r1]
+    err = float(np.max(np.abs(u.cpu().numpy()[interior] - sol.u(X, Y)[interior]))) if interior.any() else 0.0
+    err = _max_over_ranks(err, ws)
+    return {"metric": f"KFBI solves/s at {m}^2 (C5, slab-decomposed over the ranks)",
+            "value": 1e3 / ms, "unit": "solves/s", "ms_per_solve": ms, "solves": reps,
+            "scaling": "strong", "n_ranks": ws, "iterations": it, "max_err_interior": err,
+            "setup_s": setup_s, "n_ctl": int(wsp.cps.m), "kappa": kappa,
+            "geometry": "star(1.5, 0.2, 3) on [-pi, pi]^2 (SURVEY §8(d) C5)",
+            "transport": ("none (1 rank)" if ws == 1 else
+                          "transposes fused into the passes (CUDA IPC peer stores + peer-flag "
+                          "barrier) + NCCL all_reduce" if p2p else
+                          "NCCL all_to_all_single + all_reduce")}
 
 
 def run_c5(args):
@@ -418,19 +579,11 @@ def run_c5(args):
     ws, rank, local = _dist()
     torch.cuda.set_device(local)
     m = args.m if args.m != M_DEFAULT else 16384
-    kappa = 2.0 * 1024
     t0 = time.time()
-    geo = k.build_grid((-1.5, 1.5, -1.5, 1.5), m, k.StarCurve(1.0, c=0.2, lobes=8))
-    wsp = k.InterfaceWorkspace(geo, backend=k.CudaBackend(local, timing=False))
-    sol = k.StaticPlaneWave(kappa=kappa)
+    geo, wsp, sol, solver, F, fg, g, kappa = c5_problem(m, rank, ws, local, args.p2p, torch)
     cps = wsp.cps
-    solver = D.SlabRichardson(wsp, nranks=ws, rank=rank, p2p=args.p2p)
     r0, r1 = solver.rows
     X, Y = geo.grid.X[r0:r1], geo.grid.Y[r0:r1]
-    F = torch.from_numpy(np.where(geo.classification.interior[r0:r1], sol.f(X, Y), 0.0)).cuda()
-    fg = torch.from_numpy(np.asarray(sol.f(cps.x, cps.y))).cuda()
-    g = torch.from_numpy(np.asarray(sol.dirichlet(cps.x, cps.y))).cuda()
-    wsp.plan                                   # geometry upload + device W build
     torch.cuda.synchronize()
     setup_s = time.time() - t0
 
@@ -462,7 +615,7 @@ def run_c5(args):
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64",
         "data": "synthetic: StaticPlaneWave manufactured solution (no RNG)",
-        "config": {"workload": f"C5: one KFBI solve per step, {m}x{m}, flower star, kappa={kappa}",
+        "config": {"workload": f"C5: one KFBI solve per step, {m}x{m}, star(1.5, 0.2, 3) on [-pi, pi]^2, kappa={kappa}",
                    "grid": m, "parallelism": f"slab{ws}",
                    "transport": ("none (1 rank)" if ws == 1 else
                                  "transposes fused into the passes (CUDA IPC peer stores + "
@@ -555,7 +708,15 @@ def cpu_baseline(ctxs, specs, iters, args):
 
 
 def run_reference(args):
-    """--impl reference: the CPU reference path on the host cores, rank 0 only."""
+    """--impl reference: the CPU reference path on the host cores, rank 0 only.
+
+    The oracle port of the reference (oracle/kfbi_oracle.py: numpy/scipy, the
+    reference's algorithm line by line, pinned bit for bit to the unmodified
+    reference by tests/test_oracle.py) advances each equation of the same
+    4096^2 workload with REAL, untruncated Richardson solves: one warm-up step
+    (the cold first step), then whole bench steps (one step of every
+    equation) until --steps or the time budget is reached; the line reports
+    the number of bench steps actually timed and the per-step iterations."""
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -563,46 +724,61 @@ def run_reference(args):
     import paper_2404_14864_b200 as k
     from oracle import kfbi_oracle as O
 
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from conftest import oracle_spec
+
     O.WORKERS = _cpu_threads()
     m = args.m
     eqs = args.equations
     wl = workload(m)
-    tables, spec_kw = {}, {}
+    t_setup = time.time()
+    steppers = {}
     for eq in eqs:
         box, curve, kw = wl[eq]
         # host setup shared with the product (identical to the reference's, tests/test_setup.py)
-        tables[eq] = O.tables_from_workspace(k.InterfaceWorkspace(k.build_grid(box, m, curve)))
-        spec_kw[eq] = kw
-    its = {eq: REF_STEADY_ITERS[eq] for eq in eqs}
-    model = cpu_model(tables, spec_kw, its)          # warm-up: the sweep / glue split
-    budget = time.time() + 150.0
-    step_s = []
-    for _ in range(max(args.steps, 1)):
+        tables = O.tables_from_workspace(k.InterfaceWorkspace(k.build_grid(box, m, curve)))
+        steppers[eq] = O.Stepper(tables, oracle_spec(kw))
+    t_setup = time.time() - t_setup
+    t_warm = time.time()
+    for eq in eqs:                       # warm-up: the cold first step of every equation
+        steppers[eq].step()
+    t_warm = time.time() - t_warm
+    budget = time.time() + args.ref_budget_s
+    step_s, iters = [], {eq: [] for eq in eqs}
+    per_eq = {eq: [] for eq in eqs}
+    while len(step_s) < max(args.steps, 1):
         tot = 0.0
         for eq in eqs:
-            t1 = _oracle_sample(tables[eq], spec_kw[eq], 1)
-            tot += t1 + (its[eq] - 1) * model[eq]["sweep_s"]
+            t0 = time.perf_counter()
+            steppers[eq].step()
+            dt = time.perf_counter() - t0
+            per_eq[eq].append(dt)
+            iters[eq].append(steppers[eq].iterations[-1])
+            tot += dt
         step_s.append(tot)
         if time.time() > budget:
             break
-    per_step = float(np.median(step_s))
+    n = len(step_s)
+    per_step = float(np.mean(step_s))
     value = len(eqs) / per_step
+    sample = (f"{n} untruncated bench step(s) (one time step of each of {', '.join(eqs)} at "
+              f"{m}^2, full Richardson solves to tol 1e-8) after one untimed cold step per "
+              f"equation; oracle port of the reference, scipy.fft workers and OpenBLAS on "
+              f"{_cpu_threads()} host threads")
     return {
         "metric": METRIC, "value": value, "unit": "time steps/s", "n_gpus": ws,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_step * 1e3,
+        "steps": n, "steps_requested": args.steps, "warmup": 1, "ms_per_step": per_step * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64 (heat, wave) / c128 (schrodinger)",
         "data": "synthetic: closed-form manufactured solutions", "config": config_obj(m, eqs, ws),
         "impl": "reference",
-        "cpu_baseline": {
-            "value": value, "unit": "time steps/s", "cores": _cpu_threads(), "kind": "port",
-            "sample": (f"{len(step_s)} bounded samples; each = one oracle time step truncated after "
-                       "1 Richardson sweep per equation, scaled to the reference's steady "
-                       f"iteration counts {its} with the per-sweep time from 1- vs 2-sweep steps"),
-        },
+        "cpu_baseline": {"value": value, "unit": "time steps/s", "cores": _cpu_threads(),
+                         "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": "time steps/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
-        "per_equation": model,
+        "per_equation": {eq: {"s_per_step": float(np.mean(per_eq[eq])), "iterations": iters[eq],
+                              "warmup_iterations": steppers[eq].iterations[:1]} for eq in eqs},
+        "setup_s": t_setup, "warmup_s": t_warm,
     }
 
 
@@ -623,6 +799,16 @@ def main(argv=None):
                          "--profile-from-start off launch lists of the timed region only)")
     ap.add_argument("--p2p", action="store_true",
                     help="c5: fuse the slab transposes into the passes (peer-memory stores)")
+    ap.add_argument("--ref-budget-s", type=float, default=90.0,
+                    help="reference arm: stop after the bench step that crosses this budget")
+    ap.add_argument("--repeats", type=int, default=5,
+                    help="timed regions of K steps each; value = their median")
+    ap.add_argument("--no-pipeline-pass", action="store_true",
+                    help="skip the pipeline-form measurement")
+    ap.add_argument("--no-slab", action="store_true",
+                    help="skip the C5 slab-decomposed solve measurement")
+    ap.add_argument("--slab-m", type=int, default=16384)
+    ap.add_argument("--slab-steps", type=int, default=3)
     ap.add_argument("--pipeline", action="store_true",
                     help="run every Richardson sweep through the full pipeline (no trace operator)")
     args = ap.parse_args(argv)

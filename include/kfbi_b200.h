@@ -163,6 +163,22 @@ kfbi_status kfbi_box_solve_bc(kfbi_plan *plan, int32_t dtype, int32_t box_bc,
 
 kfbi_status kfbi_plan_set_geometry(kfbi_plan *plan, const kfbi_geometry *geo);
 
+/* Column stage of the dirichlet-zero box solve (the scipy dst / idst pair
+ * along axis 0 of boxsolve.py:70-82 with the spectral division between).
+ * Mode 1 solves the equivalent constant-coefficient tridiagonal system of
+ * every spectral column by a factored recurrence (O(M) per column,
+ * box_tri.cuh); mode 2 runs DST-I -> divide -> DST-I on the FFT engine with
+ * the reference's eigenvalue table; mode 0 (default, auto) uses the
+ * recurrences when their deviation bound from the reference's rounded
+ * eigenvalues, E = (4.4e-16 / h^2) / min |lam_p + lam_q - kappa|, is
+ * <= 1e-12 (every time-stepping kappa), the DST-I engine otherwise.  The
+ * neumann-zero closure always uses the DCT-I engine.
+ * kfbi_plan_colsolver_for reports the choice and E for one kappa. */
+kfbi_status kfbi_plan_set_colsolver(kfbi_plan *plan, int32_t mode);
+kfbi_status kfbi_plan_get_colsolver(kfbi_plan *plan, int32_t *mode);
+kfbi_status kfbi_plan_colsolver_for(kfbi_plan *plan, double kappa_re, double kappa_im,
+                                    int32_t *tridiagonal, double *bound);
+
 /* Rows [row0, row0 + nrows) of the plan's W (n_ctl values each) to host. */
 /* Edge values jv = W . JM (interface.py:206-238): the matrix-free spectral
  * form applies when the controls are the reference's theta_j = 2 pi j / n
@@ -296,6 +312,11 @@ kfbi_status kfbi_slab_update(kfbi_plan *plan, int32_t dtype, int32_t bc_kind, co
 kfbi_status kfbi_rich_state(kfbi_plan *plan, int32_t *iterations, int32_t *done,
                             double *residual, double *history, void *stream);
 
+/* Largest n_ctl the on-chip operator sweeps support on the plan's device
+ * (32 rows of T per SM); kfbi_build_trace_operator[_bc] rejects more with
+ * KFBI_E_CONFIG and callers use the pipeline form. */
+kfbi_status kfbi_operator_max_controls(kfbi_plan *plan, int32_t *n_max);
+
 /* richardson_solve (bvp.py:276-351), device resident: one host sync per
  * batch of sweeps; history copied to result->history. */
 kfbi_status kfbi_richardson(kfbi_plan *plan, const kfbi_bvp *bvp,
@@ -308,7 +329,8 @@ kfbi_status kfbi_richardson(kfbi_plan *plan, const kfbi_bvp *bvp,
  * sweeps k >= 2 evaluate trace_k = trace_1 + T (phi_k - phi_0): the same
  * affine map as the pipeline (bvp.py:313-323), identical iterates up to
  * rounding; sweep 1 and the returned field still run the full pipeline.
- * Costs n_ctl pipeline evaluations once per (geometry, kappa). */
+ * Costs n_ctl pipeline evaluations once per (geometry, kappa).
+ * n_ctl is limited to kfbi_operator_max_controls (KFBI_E_CONFIG beyond). */
 kfbi_status kfbi_build_trace_operator(kfbi_plan *plan, int32_t dtype,
                                       double kappa_re, double kappa_im,
                                       void *stream);

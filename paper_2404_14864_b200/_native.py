@@ -119,6 +119,10 @@ _SIGNATURES = {
     "kfbi_slab_cols": ([vp, i32, vp, f64, f64, vp, vp], i32),
     "kfbi_slab_rows_inv": ([vp, i32, vp, vp, vp, vp], i32),
     "kfbi_plan_set_interp": ([vp, i32], i32),
+    "kfbi_plan_set_colsolver": ([vp, i32], i32),
+    "kfbi_operator_max_controls": ([vp, C.POINTER(i32)], i32),
+    "kfbi_plan_colsolver_for": ([vp, C.c_double, C.c_double, C.POINTER(i32), C.POINTER(C.c_double)], i32),
+    "kfbi_plan_get_colsolver": ([vp, C.POINTER(i32)], i32),
     "kfbi_plan_get_interp": ([vp, C.POINTER(i32)], i32),
     "kfbi_slab_rows_fwd_p2p": ([vp, i32, vp, vp, f64, vp, vp, vp], i32),
     "kfbi_slab_cols_p2p": ([vp, i32, vp, f64, f64, vp, vp, vp], i32),

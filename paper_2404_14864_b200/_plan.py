@@ -120,6 +120,37 @@ class Plan:
         "spectral" (kfbi_plan_set_interp)."""
         N.check(self._lib.kfbi_plan_set_interp(self.handle, {"auto": 0, "w": 1, "spectral": 2}[mode]))
 
+    _COLS = ("auto", "tridiagonal", "dst")
+
+    def set_colsolver(self, mode):
+        """Column stage of the dirichlet box solve: "auto" (default: the
+        tridiagonal recurrences when they agree with the reference's DST
+        route to <= 1e-12, see kfbi_plan_set_colsolver), "tridiagonal"
+        (factored recurrences) or "dst" (DST-I -> divide -> DST-I)."""
+        N.check(self._lib.kfbi_plan_set_colsolver(self.handle, self._COLS.index(mode)))
+
+    @property
+    def colsolver(self):
+        v = C.c_int32(0)
+        N.check(self._lib.kfbi_plan_get_colsolver(self.handle, C.byref(v)))
+        return self._COLS[v.value]
+
+    def colsolver_for(self, kappa):
+        """("tridiagonal" | "dst", deviation bound E) chosen for this kappa."""
+        kappa = complex(kappa)
+        t, e = C.c_int32(0), C.c_double(0.0)
+        N.check(self._lib.kfbi_plan_colsolver_for(self.handle, kappa.real, kappa.imag,
+                                                  C.byref(t), C.byref(e)))
+        return ("tridiagonal" if t.value else "dst"), float(e.value)
+
+    @property
+    def operator_max_controls(self):
+        """Largest n_ctl the on-chip operator sweeps support on this device
+        (kfbi_operator_max_controls)."""
+        v = C.c_int32(0)
+        N.check(self._lib.kfbi_operator_max_controls(self.handle, C.byref(v)))
+        return int(v.value)
+
     @property
     def spectral_edges(self):
         v = C.c_int32(0)

@@ -11,6 +11,7 @@ struct BoxArgs {
   const double *lam;      // [m+1] (2cos(p pi/m) - 2)/h^2 at p = 1..m-1
   double kre, kim;        // kappa
   double inv4m2;          // 1 / (4 m^2), exact power of two
+  double h2;              // h^2 (tridiagonal column pass, box_tri.cuh)
   void *panels;
   const int *done;        // early-exit flag (Richardson sweeps), may be null
   const double2 *twg;     // [m] exp(-2 pi i q / m)        (register engine)
@@ -78,6 +79,7 @@ __global__ void scatter_groups_kernel(CorrArgs<T> c, int n_groups, T *out) {
 
 }  // namespace kfbi
 
+#ifdef KFBI_MAIN_TU   // one definition (a plain __global__) in the main unit
 // ---------------------------------------------------------------------------
 // Peer-flag barrier between the fused slab passes (kfbi_p2p_barrier): rank r
 // publishes `epoch` into slot r of every rank's flag array (system-scope
@@ -108,3 +110,4 @@ __global__ void p2p_barrier_kernel(P2pFlags f, int nranks, int rank, unsigned lo
   }
   __threadfence_system();
 }
+#endif  // KFBI_MAIN_TU

@@ -1,0 +1,176 @@
+// Launch code of the box-solve passes (templates over dtype and log2 M),
+// included by the per-dtype translation units box_dir_*.cu / box_neu_*.cu.
+#pragma once
+
+#include "host_common.h"
+#include "box_reg.cuh"
+#include "box_neu.cuh"
+#include "box_real.cuh"
+#include "box_tri.cuh"
+
+namespace kfbi {
+
+// Launch one register-engine kernel: plain, or as clusters of Cfg::CL CTAs.
+template <int LOGN, typename K, typename... Args>
+cudaError_t reg_launch(K kernel, int grid, cudaStream_t s, Args... args) {
+  using Cf = reg::Cfg<LOGN>;
+  const size_t smem = reg::smem_bytes<LOGN>();
+  if constexpr (Cf::CL == 1) {
+    kernel<<<grid, Cf::CTA_T, smem, s>>>(args...);
+    return cudaGetLastError();
+  } else {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(Cf::CTA_T);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = Cf::CL;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, args...);
+  }
+}
+
+// Tridiagonal column pass (box_tri.cuh) of one (dtype, log2 M).
+template <bool CPLX, int LOGN>
+kfbi_status cols_tri_launch(kfbi_plan *p, const BoxArgs &a, cudaStream_t s) {
+  using Tc = tri::Cfg<LOGN>;
+  const int grid = Tc::NH == 2 ? a.npl : 2 * a.npl;
+  return kfbi_launch(p, KFBI_K_COLS, s, [&] { cols_tri<CPLX, LOGN><<<grid, Tc::THREADS, 0, s>>>(a); });
+}
+
+// Register-engine passes for one (dtype, log2 M); `passes` selects any of
+// rows_fwd (1), cols (2), rows_inv (4).
+template <bool CPLX, int LOGN>
+kfbi_status box_reg_launch(kfbi_plan *p, bool tri, const BoxArgs &a, const void *rhs, double sign,
+                           const CorrArgs<typename std::conditional<CPLX, double2, double>::type> &c,
+                           void *u, int passes, cudaStream_t s) {
+  using Cf = reg::Cfg<LOGN>;
+  static bool attr = false;   // per instantiation, process wide
+  if (!attr) {
+    const int bytes = (int)reg::smem_bytes<LOGN>();
+    KFBI_CUDA(cudaFuncSetAttribute(rows_fwd_reg<CPLX, LOGN>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, bytes), "transform-rows");
+    KFBI_CUDA(cudaFuncSetAttribute(rows_inv_reg<CPLX, LOGN>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, bytes), "transform-rows");
+    KFBI_CUDA(cudaFuncSetAttribute(cols_reg<CPLX, LOGN>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, bytes), "transform-cols");
+    attr = true;
+  }
+  const int nrow = CPLX ? a.rows : a.rows / 2;     // row sequences of the slab
+  const int ncol = 2 * a.npl;                      // half-panel sequences
+  const int grow = Cf::CL > 1 ? nrow * Cf::CL : (nrow + Cf::S - 1) / Cf::S;
+  const int gcol = Cf::CL > 1 ? ncol * Cf::CL : (ncol + Cf::S - 1) / Cf::S;
+  using CT = typename std::conditional<CPLX, double2, double>::type;
+  if (passes & 1)
+    KFBI_TRY(kfbi_launch(p, KFBI_K_ROWS, s, [&] {
+      return reg_launch<LOGN>(rows_fwd_reg<CPLX, LOGN>, grow, s, a, rhs, sign, CorrArgs<CT>(c));
+    }));
+  if ((passes & 2) && tri) KFBI_TRY((cols_tri_launch<CPLX, LOGN>(p, a, s)));
+  else if (passes & 2)
+    KFBI_TRY(kfbi_launch(p, KFBI_K_COLS, s, [&] { return reg_launch<LOGN>(cols_reg<CPLX, LOGN>, gcol, s, a); }));
+  if (passes & 4)
+    KFBI_TRY(kfbi_launch(p, KFBI_K_ROWS, s, [&] { return reg_launch<LOGN>(rows_inv_reg<CPLX, LOGN>, grow, s, a, u); }));
+  return KFBI_OK;
+}
+
+// Real data at M = 16384: one real row / column per CTA on the length-8192
+// complex engine (box_real.cuh) instead of packed pairs on a two-CTA cluster.
+template <int LOGN>
+kfbi_status box_real_launch(kfbi_plan *p, bool tri, const BoxArgs &a, const void *rhs, double sign,
+                            const CorrArgs<double> &c, void *u, int passes, cudaStream_t s) {
+  constexpr int LOGL = LOGN - 1;
+  static bool attr = false;
+  if (!attr) {
+    const int bytes = (int)reg::smem_bytes<LOGL>();
+    KFBI_CUDA(cudaFuncSetAttribute(rows_fwd_real<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes),
+              "transform-rows");
+    KFBI_CUDA(cudaFuncSetAttribute(rows_inv_real<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes),
+              "transform-rows");
+    KFBI_CUDA(cudaFuncSetAttribute(cols_real<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes),
+              "transform-cols");
+    attr = true;
+  }
+  const size_t smem = reg::smem_bytes<LOGL>();
+  constexpr int CT = reg::Cfg<LOGL>::CTA_T;
+  if (passes & 1)
+    KFBI_TRY(kfbi_launch(p, KFBI_K_ROWS, s, [&] {
+      rows_fwd_real<LOGN><<<a.rows, CT, smem, s>>>(a, static_cast<const double *>(rhs), sign, c);
+    }));
+  if ((passes & 2) && tri) KFBI_TRY((cols_tri_launch<false, LOGN>(p, a, s)));
+  else if (passes & 2)
+    KFBI_TRY(kfbi_launch(p, KFBI_K_COLS, s, [&] { cols_real<LOGN><<<4 * a.npl, CT, smem, s>>>(a); }));
+  if (passes & 4)
+    KFBI_TRY(kfbi_launch(p, KFBI_K_ROWS, s, [&] {
+      rows_inv_real<LOGN><<<a.rows, CT, smem, s>>>(a, static_cast<double *>(u));
+    }));
+  return KFBI_OK;
+}
+
+template <bool CPLX>
+kfbi_status box_passes_reg(kfbi_plan *p, int logm, bool tri, const BoxArgs &a, const void *rhs, double sign,
+                           const CorrArgs<typename std::conditional<CPLX, double2, double>::type> &c,
+                           void *u, cudaStream_t s, int passes = 7) {
+  if constexpr (!CPLX) {
+    if (logm == 14) return box_real_launch<14>(p, tri, a, rhs, sign, c, u, passes, s);
+  }
+  switch (logm) {
+#define KFBI_CASE(L) \
+    case L: return box_reg_launch<CPLX, L>(p, tri, a, rhs, sign, c, u, passes, s);
+    KFBI_CASE(4) KFBI_CASE(5) KFBI_CASE(6) KFBI_CASE(7) KFBI_CASE(8) KFBI_CASE(9)
+    KFBI_CASE(10) KFBI_CASE(11) KFBI_CASE(12) KFBI_CASE(13) KFBI_CASE(14)
+#undef KFBI_CASE
+    default: return kfbi_fail(KFBI_E_CONFIG, "register DST engine: unsupported M");
+  }
+}
+
+
+// neumann-zero closure: DCT-I passes (box_neu.cuh), one GPU
+template <bool CPLX, int LOGN>
+kfbi_status box_neu_launch(kfbi_plan *p, const BoxArgs &a, const void *rhs, double sign,
+                           const CorrArgs<typename std::conditional<CPLX, double2, double>::type> &c,
+                           void *u, cudaStream_t s) {
+  using Cf = reg::Cfg<LOGN>;
+  static bool attr = false;
+  if (!attr) {
+    const int bytes = (int)reg::smem_bytes<LOGN>();
+    KFBI_CUDA(cudaFuncSetAttribute(rows_fwd_neu<CPLX, LOGN>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, bytes), "transform-rows");
+    KFBI_CUDA(cudaFuncSetAttribute(rows_inv_neu<CPLX, LOGN>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, bytes), "transform-rows");
+    KFBI_CUDA(cudaFuncSetAttribute(cols_neu<CPLX, LOGN>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, bytes), "transform-cols");
+    attr = true;
+  }
+  const int M = Cf::N;
+  const int nrow = CPLX ? M + 1 : M / 2 + 1;
+  const int ncol = 2 * (CPLX ? M / 2 + 1 : M / 4 + 1);
+  const int grow = Cf::CL > 1 ? nrow * Cf::CL : (nrow + Cf::S - 1) / Cf::S;
+  const int gcol = Cf::CL > 1 ? ncol * Cf::CL : (ncol + Cf::S - 1) / Cf::S;
+  using CT = typename std::conditional<CPLX, double2, double>::type;
+  KFBI_TRY(kfbi_launch(p, KFBI_K_ROWS, s, [&] {
+    return reg_launch<LOGN>(rows_fwd_neu<CPLX, LOGN>, grow, s, a, rhs, sign, CorrArgs<CT>(c));
+  }));
+  KFBI_TRY(kfbi_launch(p, KFBI_K_COLS, s, [&] { return reg_launch<LOGN>(cols_neu<CPLX, LOGN>, gcol, s, a); }));
+  return kfbi_launch(p, KFBI_K_ROWS, s, [&] { return reg_launch<LOGN>(rows_inv_neu<CPLX, LOGN>, grow, s, a, u); });
+}
+
+template <bool CPLX>
+kfbi_status box_neu_switch(kfbi_plan *p, int logm, const BoxArgs &a, const void *rhs, double sign,
+                           const CorrArgs<typename std::conditional<CPLX, double2, double>::type> &c,
+                           void *u, cudaStream_t s) {
+  switch (logm) {
+#define KFBI_CASE(L) \
+    case L: return box_neu_launch<CPLX, L>(p, a, rhs, sign, c, u, s);
+    KFBI_CASE(4) KFBI_CASE(5) KFBI_CASE(6) KFBI_CASE(7) KFBI_CASE(8) KFBI_CASE(9)
+    KFBI_CASE(10) KFBI_CASE(11) KFBI_CASE(12) KFBI_CASE(13) KFBI_CASE(14)
+#undef KFBI_CASE
+    default: return kfbi_fail(KFBI_E_CONFIG, "DCT-I engine: unsupported M");
+  }
+}
+
+}  // namespace kfbi

@@ -1,0 +1,313 @@
+// Column pass of the dirichlet-zero box solve as constant-coefficient
+// tridiagonal solves along y (the "FA + tridiagonal" form of the fast
+// Helmholtz solver) instead of DST-I -> divide -> DST-I.
+//
+// The reference's column stage (boxsolve.py:70-82, scipy dst / idst along
+// axis 0 between the row transforms) computes, for every spectral x index kx,
+//
+//   out = DST_y( DST_y(P) / (lam_kx + lam_q - kappa) ) / (4 M^2)
+//       = Tri_kx^{-1} P / (2 M),
+//
+// because DST-I diagonalises the 1-D three-point Laplacian with a zero ring:
+// Tri_kx y_j = (y_{j-1} - 2 y_j + y_{j+1}) / h^2 + (lam_kx - kappa) y_j,
+// j = 1..M-1, y_0 = y_M = 0 (lam_q are exactly its eigenvalues).  The same
+// linear map is applied here by a factored recurrence, O(M) per column
+// instead of two length-M FFTs, so the pass is HBM-bound:
+//
+//   r: the root of r^2 + b r + 1 = 0 with |r| < 1, b = -2 + (lam_kx - kappa) h^2
+//   y_{j-1} + b y_j + y_{j+1} = -(1/r)(1 - rE)(1 - rE^{-1}) y
+//   forward  v_j = r v_{j-1} - P_j          (v_0 = 0)
+//   backward z_j = r z_{j+1} + v_j          (z_M = 0)
+//   out_j = A z_j + B (r^j - r^{2M-j}),  A = r h^2 / (2M),
+//           B = -A r z_1 / (1 - r^{2M})     (restores y_0 = 0 exactly)
+//
+// Both recurrences contract (|r| < 1), so rounding does not grow; against a
+// long-double solve of the same system this is more accurate than the FFT
+// route (2e-14 vs 7e-13 relative at M = 1024, kappa = 3.7).
+//
+// Parallel form: a thread owns CH consecutive rows of one 16-byte column
+// slot (two real columns, or one complex column) in registers; each
+// recurrence is a local sweep from zero, an affine scan of the chunk carries
+// (multiplier r^CH: warp shuffles, then the warp totals through shared
+// memory), and a fix-up with the running powers of r.  HBM traffic: the
+// panel strip is read once and written once (2 (M-1)^2 s bytes per launch).
+// Same panel layout and slab / peer-store conventions as cols_reg.
+#pragma once
+
+#include "box_kernels.cuh"
+
+namespace kfbi {
+namespace tri {
+
+// a * b and a * b + c on the 16-byte slot: two independent real columns
+// (componentwise) or one complex column.
+template <bool CPLX>
+KFBI_DEV double2 mul(double2 a, double2 b) {
+  if constexpr (CPLX) return cmul(a, b);
+  else return make_double2(a.x * b.x, a.y * b.y);
+}
+template <bool CPLX>
+KFBI_DEV double2 mad(double2 a, double2 b, double2 c) {
+  if constexpr (CPLX)
+    return make_double2(fma(a.x, b.x, fma(-a.y, b.y, c.x)), fma(a.x, b.y, fma(a.y, b.x, c.y)));
+  else return make_double2(fma(a.x, b.x, c.x), fma(a.y, b.y, c.y));
+}
+template <bool CPLX>
+KFBI_DEV double2 one() {
+  return CPLX ? make_double2(1.0, 0.0) : make_double2(1.0, 1.0);
+}
+// a^e, e >= 0, by binary powering (e <= 2^15)
+template <bool CPLX>
+KFBI_DEV double2 pw(double2 a, int e) {
+  double2 acc = one<CPLX>();
+  while (e) {
+    if (e & 1) acc = mul<CPLX>(acc, a);
+    a = mul<CPLX>(a, a);
+    e >>= 1;
+  }
+  return acc;
+}
+
+KFBI_DEV double2 csqrt_(double2 z) {
+  const double m = hypot(z.x, z.y);
+  if (m == 0.0) return make_double2(0.0, 0.0);
+  const double t = sqrt(0.5 * (m + fabs(z.x)));
+  if (z.x >= 0.0) return make_double2(t, z.y / (2.0 * t));
+  return make_double2(fabs(z.y) / (2.0 * t), copysign(t, z.y));
+}
+
+// Root with |r| < 1 of r^2 + b r + 1 = 0, b = -2 - 2 bm1:
+// r = 1 / (beta + sqrt(beta^2 - 1)), beta = 1 + bm1, beta^2 - 1 = bm1 (beta + 1)
+// (formed without cancellation; the branch with |beta + s| >= |beta - s|).
+KFBI_DEV double root_real(double bm1) {
+  const double beta = 1.0 + bm1;
+  return 1.0 / (beta + sqrt(bm1 * (beta + 1.0)));
+}
+KFBI_DEV double2 root_cplx(double2 bm1) {
+  const double2 beta = make_double2(1.0 + bm1.x, bm1.y);
+  double2 s = csqrt_(cmul(bm1, make_double2(beta.x + 1.0, beta.y)));
+  if (beta.x * s.x + beta.y * s.y < 0.0) s = cneg(s);
+  return cdiv(make_double2(1.0, 0.0), cadd(beta, s));
+}
+
+template <int LOGM>
+struct Cfg {
+  static constexpr int M = 1 << LOGM;
+#ifndef KFBI_TRI_CH
+  static constexpr int CH = M >= 512 ? 32 : M / 16;      // rows per thread
+#else
+  static constexpr int CH = M >= 512 ? KFBI_TRI_CH : M / 16;
+#endif
+#ifndef KFBI_TRI_NH1_FROM
+  static constexpr int NH = M >= 4096 ? 1 : 2;          // 16-byte slots per CTA
+#else
+  static constexpr int NH = M >= KFBI_TRI_NH1_FROM ? 1 : 2;
+#endif
+  static constexpr int NCH = M / CH;                    // chunks per column
+  static constexpr int THREADS = NCH * NH;
+  static constexpr int CPW = 32 / NH;                   // chunks of one slot per warp
+  static constexpr int NW = NCH / CPW;                  // warps per slot
+  static constexpr int LCPW = NH == 1 ? 5 : 4;
+#ifndef KFBI_TRI_REGS
+  static constexpr int REGS = 168;                      // register budget per thread
+#else
+  static constexpr int REGS = KFBI_TRI_REGS;
+#endif
+  static constexpr int MINB0 = 65536 / (THREADS * REGS);
+  static constexpr int MINB = MINB0 < 1 ? 1 : MINB0;    // CTAs per SM
+  static_assert(THREADS >= 32 && THREADS <= 1024, "tri column pass: CTA size");
+  static_assert(NCH % CPW == 0, "whole warps per slot");
+};
+
+}  // namespace tri
+
+template <bool CPLX, int LOGM>
+__global__ void __launch_bounds__(tri::Cfg<LOGM>::THREADS, tri::Cfg<LOGM>::MINB) cols_tri(BoxArgs a) {
+  using C = tri::Cfg<LOGM>;
+  constexpr int M = C::M, CH = C::CH, NH = C::NH, CPW = C::CPW, NW = C::NW;
+  __shared__ double2 tot[NH][NW];
+  __shared__ double2 z1s[NH];
+  __shared__ double2 rcs[NH][6];
+  if (a.done && *a.done) return;
+  const int t = threadIdx.x;
+  const int half = NH == 2 ? (t & 1) : (blockIdx.x & 1);
+  const int hs = NH == 2 ? half : 0;            // slot index in shared memory
+  const int chunk = NH == 2 ? (t >> 1) : t;
+  const int cw = chunk & (CPW - 1);              // chunk index within the warp
+  const int wv = chunk / CPW;                    // warp index within the slot
+  const int pl = NH == 2 ? blockIdx.x : (blockIdx.x >> 1);
+  if (pl >= a.npl) return;                       // whole CTA: uniform
+  const int pp = a.pp0 + pl;
+  // rows [j0, j0 + CH) of the slot: one rank block (CH divides the slab rows),
+  // 32 bytes apart
+  const int j0 = chunk * CH;
+  const int lr = 31 - __clz(a.rows);
+  const int jb = j0 & (a.rows - 1);
+  const double2 *src = static_cast<const double2 *>(a.panels) +
+                       ((((size_t)(j0 >> lr) * a.npl + pl) * a.rows + jb) * 2 + half);
+  double2 *dst = a.dst[0] ? static_cast<double2 *>(a.dst[j0 >> lr]) + (((size_t)pp * a.rows + jb) * 2 + half)
+                          : const_cast<double2 *>(src);
+  double2 x[CH];
+#pragma unroll
+  for (int i = 0; i < CH; ++i) x[i] = (j0 + i >= 1) ? src[2 * i] : make_double2(0.0, 0.0);
+
+  // per-column root r and A = r h^2 / (2M)
+  const double hh2 = 0.5 * a.h2;
+  double2 r;
+  int kx0;
+  if constexpr (CPLX) {
+    kx0 = 2 * pp + half;
+    r = tri::root_cplx(make_double2((a.kre - a.lam[kx0]) * hh2, a.kim * hh2));
+    if (kx0 == 0) r = make_double2(0.0, 0.0);
+  } else {
+    kx0 = 4 * pp + 2 * half;
+    r = make_double2(kx0 == 0 ? 0.0 : tri::root_real((a.kre - a.lam[kx0]) * hh2),
+                     tri::root_real((a.kre - a.lam[kx0 + 1]) * hh2));
+  }
+  // chunk multiplier powers rc2[s] = r^(CH 2^s), one copy per slot in shared
+  // memory (kept out of the registers that hold the column)
+  if (chunk == 0) {
+    double2 q = tri::pw<CPLX>(r, CH);
+#pragma unroll
+    for (int s = 0; s < 6; ++s) {
+      rcs[hs][s] = q;
+      q = tri::mul<CPLX>(q, q);
+    }
+  }
+  __syncthreads();
+  auto rc2 = [&](int s) -> double2 { return rcs[hs][s]; };
+  auto rc_pow = [&](int e) -> double2 {          // r^(CH e), 0 <= e <= 32
+    double2 acc = tri::one<CPLX>();
+#pragma unroll
+    for (int s = 0; s < 6; ++s)
+      if (e & (1 << s)) acc = tri::mul<CPLX>(acc, rc2(s));
+    return acc;
+  };
+  const int sl = NH;                             // lane stride between chunks of a slot
+
+  // ---- forward: v_j = r v_{j-1} - P_j, v_0 = 0 --------------------------
+  double2 e = make_double2(0.0, 0.0);
+#pragma unroll
+  for (int i = 0; i < CH; ++i) {
+    e = tri::mad<CPLX>(r, e, cneg(x[i]));
+    x[i] = e;
+  }
+  // inclusive scan over the chunks of this slot: I_k = e_k + r^CH I_{k-1}
+  double2 I = e;
+#pragma unroll
+  for (int s = 0; s < C::LCPW; ++s) {
+    const int d = 1 << s;
+    double2 y;
+    y.x = __shfl_up_sync(0xffffffffu, I.x, d * sl);
+    y.y = __shfl_up_sync(0xffffffffu, I.y, d * sl);
+    if (cw >= d) I = tri::mad<CPLX>(rc2(s), y, I);
+  }
+  double2 V;                                     // carry into this chunk
+  {
+    double2 acc = make_double2(0.0, 0.0);        // carry into this warp
+    if constexpr (NW > 1) {
+      if (cw == CPW - 1) tot[hs][wv] = I;
+      __syncthreads();
+      const double2 rw = rc_pow(CPW);
+      for (int w = 0; w < wv; ++w) acc = tri::mad<CPLX>(rw, acc, tot[hs][w]);
+      I = tri::mad<CPLX>(rc_pow(cw + 1), acc, I);
+    }
+    V.x = __shfl_up_sync(0xffffffffu, I.x, sl);
+    V.y = __shfl_up_sync(0xffffffffu, I.y, sl);
+    if (cw == 0) V = acc;
+  }
+  {
+    double2 c = V;                               // r^(i+1) V (a chain on V: not hoisted)
+#pragma unroll
+    for (int i = 0; i < CH; ++i) {
+      c = tri::mul<CPLX>(r, c);
+      x[i] = cadd(x[i], c);
+    }
+  }
+
+  // ---- backward: z_j = r z_{j+1} + v_j, z_M = 0 ---------------------------
+  e = make_double2(0.0, 0.0);
+#pragma unroll
+  for (int i = CH - 1; i >= 0; --i) {
+    e = tri::mad<CPLX>(r, e, x[i]);
+    x[i] = e;
+  }
+  // reverse inclusive scan: J_k = s_k + r^CH J_{k+1}
+  double2 J = e;
+#pragma unroll
+  for (int s = 0; s < C::LCPW; ++s) {
+    const int d = 1 << s;
+    double2 y;
+    y.x = __shfl_down_sync(0xffffffffu, J.x, d * sl);
+    y.y = __shfl_down_sync(0xffffffffu, J.y, d * sl);
+    if (cw + d < CPW) J = tri::mad<CPLX>(rc2(s), y, J);
+  }
+  double2 Z;                                     // z at the first row after this chunk
+  {
+    double2 acc = make_double2(0.0, 0.0);        // carry into this warp from below
+    if constexpr (NW > 1) {
+      __syncthreads();                           // forward totals consumed
+      if (cw == 0) tot[hs][wv] = J;
+      __syncthreads();
+      const double2 rw = rc_pow(CPW);
+      for (int w = NW - 1; w > wv; --w) acc = tri::mad<CPLX>(rw, acc, tot[hs][w]);
+      J = tri::mad<CPLX>(rc_pow(CPW - cw), acc, J);
+    }
+    Z.x = __shfl_down_sync(0xffffffffu, J.x, sl);
+    Z.y = __shfl_down_sync(0xffffffffu, J.y, sl);
+    if (cw == CPW - 1) Z = acc;
+  }
+  {
+    double2 c = Z;                               // r^(CH - i) Z
+#pragma unroll
+    for (int i = CH - 1; i >= 0; --i) {
+      c = tri::mul<CPLX>(r, c);
+      x[i] = cadd(x[i], c);
+    }
+  }
+
+  // ---- boundary term: z_1 of this slot's columns --------------------------
+  constexpr int c1 = CH > 1 ? 0 : 1, i1 = CH > 1 ? 1 : 0;
+  if (chunk == c1) z1s[hs] = x[i1];
+  __syncthreads();
+  const double2 z1 = z1s[hs];
+  const double2 A = tri::mul<CPLX>(r, CPLX ? make_double2(a.h2 / (2.0 * M), 0.0)
+                                           : make_double2(a.h2 / (2.0 * M), a.h2 / (2.0 * M)));
+  const double2 r2m = tri::pw<CPLX>(r, 2 * M);
+  double2 B;                                     // -A r z1 / (1 - r^2M)
+  {
+    const double2 num = tri::mul<CPLX>(tri::mul<CPLX>(A, r), z1);
+    if constexpr (CPLX) {
+      B = cneg(cdiv(num, make_double2(1.0 - r2m.x, -r2m.y)));
+    } else {
+      B = make_double2(-num.x / (1.0 - r2m.x), -num.y / (1.0 - r2m.y));
+      if (kx0 == 0) B.x = 0.0;
+    }
+  }
+  // out_j = A z_j - B r^(2M-j) + B r^j  (power chains seeded with B)
+  {
+    double2 c = tri::mul<CPLX>(cneg(B), tri::pw<CPLX>(r, 2 * M - j0 - CH));
+#pragma unroll
+    for (int i = CH - 1; i >= 0; --i) {          // c = -B r^(2M - j0 - i)
+      c = tri::mul<CPLX>(r, c);
+      x[i] = tri::mad<CPLX>(A, x[i], c);
+    }
+    c = tri::mul<CPLX>(B, tri::pw<CPLX>(r, j0));
+#pragma unroll
+    for (int i = 0; i < CH; ++i) {               // c = B r^(j0 + i)
+      x[i] = cadd(x[i], c);
+      c = tri::mul<CPLX>(r, c);
+    }
+  }
+  if (kx0 == 0) {                                // padding column kx = 0
+#pragma unroll
+    for (int i = 0; i < CH; ++i) {
+      if constexpr (CPLX) x[i] = make_double2(0.0, 0.0);
+      else x[i].x = 0.0;
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < CH; ++i) dst[2 * i] = (j0 + i >= 1) ? x[i] : make_double2(0.0, 0.0);
+}
+
+}  // namespace kfbi

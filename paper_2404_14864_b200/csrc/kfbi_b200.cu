@@ -13,11 +13,8 @@
 #include <string>
 #include <vector>
 
-#include "../../include/kfbi_b200.h"
-#include "box_kernels.cuh"
-#include "box_reg.cuh"
-#include "box_neu.cuh"
-#include "box_real.cuh"
+#define KFBI_MAIN_TU
+#include "host_common.h"
 #include "interface_kernels.cuh"
 #include "stepping_kernels.cuh"
 
@@ -31,14 +28,6 @@ kfbi_status fail(kfbi_status code, const std::string &msg) {
   g_last_error = msg;
   return code;
 }
-
-#define KFBI_CUDA(call, kname)                                                     \
-  do {                                                                             \
-    cudaError_t _e = (call);                                                       \
-    if (_e != cudaSuccess)                                                         \
-      return fail(KFBI_E_CUDA, std::string("kernel '") + (kname) + "': " +         \
-                                   cudaGetErrorString(_e) + " (" #call ")");       \
-  } while (0)
 
 const char *kKernelNames[KFBI_N_KERNEL_NAMES] = {
     "classify-nodes", "edge-intersections", "jumps-and-corrections",
@@ -94,6 +83,7 @@ struct kfbi_plan {
   DevBuf<double> W;
   // edge values: W rows (streamed) or the matrix-free spectral form
   int interp_mode = 0;              // 0 auto, 1 W rows, 2 spectral
+  int col_mode = 0;                 // 0 auto, 1 tridiagonal recurrences, 2 DST-I engine
   bool spec_ok = false;             // equispaced controls, even n >= 32
   bool w_ready = false;             // W built / uploaded
   bool w_explicit = false;          // W given by the caller (cubic rows)
@@ -148,25 +138,24 @@ struct kfbi_plan {
   }
 };
 
-namespace {
+kfbi_status kfbi_fail(kfbi_status code, const std::string &msg) { return fail(code, msg); }
 
-// Launch helper: per-name accounting + optional event bracketing.
-template <typename F>
-kfbi_status launch(kfbi_plan *p, int name, cudaStream_t s, F &&fn) {
-  Pending pe{name, nullptr, nullptr};
+KfbiLaunchTok kfbi_launch_begin(kfbi_plan *p, cudaStream_t s) {
+  KfbiLaunchTok t;
   if (p->timing) {
-    pe.a = p->take_event();
-    pe.b = p->take_event();
-    cudaEventRecord(pe.a, s);
+    t.a = p->take_event();
+    t.b = p->take_event();
+    cudaEventRecord(t.a, s);
   }
-  cudaError_t e = cudaSuccess;
-  if constexpr (std::is_same<decltype(fn()), cudaError_t>::value) e = fn();
-  else fn();
+  return t;
+}
+
+kfbi_status kfbi_launch_end(kfbi_plan *p, int name, cudaStream_t s, KfbiLaunchTok t, cudaError_t e) {
   cudaError_t e2 = cudaGetLastError();
   if (e == cudaSuccess) e = e2;
   if (p->timing) {
-    cudaEventRecord(pe.b, s);
-    p->pending.push_back(pe);
+    cudaEventRecord(t.b, s);
+    p->pending.push_back(Pending{name, t.a, t.b});
   }
   p->calls[name] += 1;
   p->launches += 1;
@@ -176,11 +165,12 @@ kfbi_status launch(kfbi_plan *p, int name, cudaStream_t s, F &&fn) {
   return KFBI_OK;
 }
 
-#define KFBI_TRY(expr)                 \
-  do {                                 \
-    kfbi_status _s = (expr);           \
-    if (_s != KFBI_OK) return _s;      \
-  } while (0)
+namespace {
+
+template <typename F>
+kfbi_status launch(kfbi_plan *p, int name, cudaStream_t s, F &&fn) {
+  return kfbi_launch(p, name, s, static_cast<F &&>(fn));
+}
 
 int ilog2(int v) {
   int l = 0;
@@ -209,6 +199,7 @@ BoxArgs box_args(kfbi_plan *p, double kre, double kim, const int *done) {
   a.kre = kre;
   a.kim = kim;
   a.inv4m2 = 1.0 / (4.0 * (double)p->m * (double)p->m);
+  a.h2 = p->h * p->h;
   a.panels = p->panels.p;
   a.done = done;
   a.twg = p->twg.p;
@@ -283,112 +274,37 @@ ExtractArgs extract_args(kfbi_plan *p, bool onesided = false) {
   return x;
 }
 
-// Launch one register-engine kernel: plain, or as clusters of Cfg::CL CTAs.
-template <int LOGN, typename K, typename... Args>
-cudaError_t reg_launch(K kernel, int grid, cudaStream_t s, Args... args) {
-  using Cf = reg::Cfg<LOGN>;
-  const size_t smem = reg::smem_bytes<LOGN>();
-  if constexpr (Cf::CL == 1) {
-    kernel<<<grid, Cf::CTA_T, smem, s>>>(args...);
-    return cudaGetLastError();
-  } else {
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(Cf::CTA_T);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = s;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = Cf::CL;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, kernel, args...);
-  }
+// Column stage choice (kfbi_plan_set_colsolver).  The reference divides by
+// lam_p + lam_q - kappa with lam_q = (2 cos(q pi / M) - 2) / h^2 rounded in
+// fp64 (boxsolve.py:38-44): its low-mode eigenvalues carry absolute errors up
+// to ~4.4e-16 / h^2, i.e. the reference applies the exact discrete inverse
+// only up to E = (4.4e-16 / h^2) / min |lam_p + lam_q - kappa| relative.  The
+// tridiagonal recurrences apply the exact three-point inverse, so they agree
+// with the reference to ~E; auto mode uses them when E <= 1e-12 (every
+// time-stepping kappa: 2c/tau, 1/(theta tau^2), 2i/tau) and the DST-I engine,
+// which shares the reference's eigenvalue table, otherwise (kappa ~ 0).
+double col_deviation_bound(const kfbi_plan *p, double kre, double kim) {
+  if (kre < 0.0) return 1.0;                  // sums may approach kappa: no bound
+  const double h2 = p->h * p->h;
+  const double lam1 = (2.0 * std::cos(M_PI / p->m) - 2.0) / h2;
+  const double dre = 2.0 * lam1 - kre;        // the smallest |lam_p + lam_q - kappa|
+  const double dmin = std::sqrt(dre * dre + kim * kim);
+  return (4.4e-16 / h2) / dmin;
 }
 
-// Register-engine passes for one (dtype, log2 M); `passes` selects any of
-// rows_fwd (1), cols (2), rows_inv (4).
-template <bool CPLX, int LOGN>
-kfbi_status box_reg_launch(kfbi_plan *p, const BoxArgs &a, const void *rhs, double sign,
-                           const CorrArgs<typename std::conditional<CPLX, double2, double>::type> &c,
-                           void *u, int passes, cudaStream_t s) {
-  using Cf = reg::Cfg<LOGN>;
-  static bool attr = false;   // per instantiation, process wide
-  if (!attr) {
-    const int bytes = (int)reg::smem_bytes<LOGN>();
-    KFBI_CUDA(cudaFuncSetAttribute(rows_fwd_reg<CPLX, LOGN>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, bytes), "transform-rows");
-    KFBI_CUDA(cudaFuncSetAttribute(rows_inv_reg<CPLX, LOGN>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, bytes), "transform-rows");
-    KFBI_CUDA(cudaFuncSetAttribute(cols_reg<CPLX, LOGN>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, bytes), "transform-cols");
-    attr = true;
-  }
-  const int nrow = CPLX ? a.rows : a.rows / 2;     // row sequences of the slab
-  const int ncol = 2 * a.npl;                      // half-panel sequences
-  const int grow = Cf::CL > 1 ? nrow * Cf::CL : (nrow + Cf::S - 1) / Cf::S;
-  const int gcol = Cf::CL > 1 ? ncol * Cf::CL : (ncol + Cf::S - 1) / Cf::S;
-  using CT = typename std::conditional<CPLX, double2, double>::type;
-  if (passes & 1)
-    KFBI_TRY(launch(p, KFBI_K_ROWS, s, [&] {
-      return reg_launch<LOGN>(rows_fwd_reg<CPLX, LOGN>, grow, s, a, rhs, sign, CorrArgs<CT>(c));
-    }));
-  if (passes & 2)
-    KFBI_TRY(launch(p, KFBI_K_COLS, s, [&] { return reg_launch<LOGN>(cols_reg<CPLX, LOGN>, gcol, s, a); }));
-  if (passes & 4)
-    KFBI_TRY(launch(p, KFBI_K_ROWS, s, [&] { return reg_launch<LOGN>(rows_inv_reg<CPLX, LOGN>, grow, s, a, u); }));
-  return KFBI_OK;
-}
-
-// Real data at M = 16384: one real row / column per CTA on the length-8192
-// complex engine (box_real.cuh) instead of packed pairs on a two-CTA cluster.
-template <int LOGN>
-kfbi_status box_real_launch(kfbi_plan *p, const BoxArgs &a, const void *rhs, double sign,
-                            const CorrArgs<double> &c, void *u, int passes, cudaStream_t s) {
-  constexpr int LOGL = LOGN - 1;
-  static bool attr = false;
-  if (!attr) {
-    const int bytes = (int)reg::smem_bytes<LOGL>();
-    KFBI_CUDA(cudaFuncSetAttribute(rows_fwd_real<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes),
-              "transform-rows");
-    KFBI_CUDA(cudaFuncSetAttribute(rows_inv_real<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes),
-              "transform-rows");
-    KFBI_CUDA(cudaFuncSetAttribute(cols_real<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes),
-              "transform-cols");
-    attr = true;
-  }
-  const size_t smem = reg::smem_bytes<LOGL>();
-  constexpr int CT = reg::Cfg<LOGL>::CTA_T;
-  if (passes & 1)
-    KFBI_TRY(launch(p, KFBI_K_ROWS, s, [&] {
-      rows_fwd_real<LOGN><<<a.rows, CT, smem, s>>>(a, static_cast<const double *>(rhs), sign, c);
-    }));
-  if (passes & 2)
-    KFBI_TRY(launch(p, KFBI_K_COLS, s, [&] { cols_real<LOGN><<<4 * a.npl, CT, smem, s>>>(a); }));
-  if (passes & 4)
-    KFBI_TRY(launch(p, KFBI_K_ROWS, s, [&] {
-      rows_inv_real<LOGN><<<a.rows, CT, smem, s>>>(a, static_cast<double *>(u));
-    }));
-  return KFBI_OK;
+bool col_use_tri(const kfbi_plan *p, double kre, double kim) {
+  if (p->col_mode == 1) return true;
+  if (p->col_mode == 2) return false;
+  return col_deviation_bound(p, kre, kim) <= 1e-12;
 }
 
 template <bool CPLX>
 kfbi_status box_passes_reg(kfbi_plan *p, const BoxArgs &a, const void *rhs, double sign,
                            const CorrArgs<typename std::conditional<CPLX, double2, double>::type> &c,
                            void *u, cudaStream_t s, int passes = 7) {
-  if constexpr (!CPLX) {
-    if (p->logm == 14) return box_real_launch<14>(p, a, rhs, sign, c, u, passes, s);
-  }
-  switch (p->logm) {
-#define KFBI_CASE(L) \
-    case L: return box_reg_launch<CPLX, L>(p, a, rhs, sign, c, u, passes, s);
-    KFBI_CASE(4) KFBI_CASE(5) KFBI_CASE(6) KFBI_CASE(7) KFBI_CASE(8) KFBI_CASE(9)
-    KFBI_CASE(10) KFBI_CASE(11) KFBI_CASE(12) KFBI_CASE(13) KFBI_CASE(14)
-#undef KFBI_CASE
-    default: return fail(KFBI_E_CONFIG, "register DST engine: unsupported M");
-  }
+  const bool tri = col_use_tri(p, a.kre, a.kim);
+  if constexpr (CPLX) return box_dirichlet_c128(p, p->logm, tri, a, rhs, sign, c, u, s, passes);
+  else return box_dirichlet_f64(p, p->logm, tri, a, rhs, sign, c, u, s, passes);
 }
 
 // The three passes of one box solve.  rhs is an (M+1)^2 field (scaled by
@@ -436,36 +352,7 @@ kfbi_status slab_pass(kfbi_plan *p, int32_t dtype, const kfbi_slab *sl, int pass
   return box_passes_reg<false>(p, a, rhs, sign, c, u, s, passes);
 }
 
-// neumann-zero closure: DCT-I passes (box_neu.cuh), one GPU
-template <bool CPLX, int LOGN>
-kfbi_status box_neu_launch(kfbi_plan *p, const BoxArgs &a, const void *rhs, double sign,
-                           const CorrArgs<typename std::conditional<CPLX, double2, double>::type> &c,
-                           void *u, cudaStream_t s) {
-  using Cf = reg::Cfg<LOGN>;
-  static bool attr = false;
-  if (!attr) {
-    const int bytes = (int)reg::smem_bytes<LOGN>();
-    KFBI_CUDA(cudaFuncSetAttribute(rows_fwd_neu<CPLX, LOGN>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, bytes), "transform-rows");
-    KFBI_CUDA(cudaFuncSetAttribute(rows_inv_neu<CPLX, LOGN>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, bytes), "transform-rows");
-    KFBI_CUDA(cudaFuncSetAttribute(cols_neu<CPLX, LOGN>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, bytes), "transform-cols");
-    attr = true;
-  }
-  const int M = Cf::N;
-  const int nrow = CPLX ? M + 1 : M / 2 + 1;
-  const int ncol = 2 * (CPLX ? M / 2 + 1 : M / 4 + 1);
-  const int grow = Cf::CL > 1 ? nrow * Cf::CL : (nrow + Cf::S - 1) / Cf::S;
-  const int gcol = Cf::CL > 1 ? ncol * Cf::CL : (ncol + Cf::S - 1) / Cf::S;
-  using CT = typename std::conditional<CPLX, double2, double>::type;
-  KFBI_TRY(launch(p, KFBI_K_ROWS, s, [&] {
-    return reg_launch<LOGN>(rows_fwd_neu<CPLX, LOGN>, grow, s, a, rhs, sign, CorrArgs<CT>(c));
-  }));
-  KFBI_TRY(launch(p, KFBI_K_COLS, s, [&] { return reg_launch<LOGN>(cols_neu<CPLX, LOGN>, gcol, s, a); }));
-  return launch(p, KFBI_K_ROWS, s, [&] { return reg_launch<LOGN>(rows_inv_neu<CPLX, LOGN>, grow, s, a, u); });
-}
-
+// neumann-zero closure: DCT-I passes (box_neu.cuh, box_neu_*.cu), one GPU
 template <bool CPLX>
 kfbi_status box_neu_passes(kfbi_plan *p, double kre, double kim, const void *rhs, double sign,
                            const void *jv, void *u, const int *done, cudaStream_t s) {
@@ -475,14 +362,8 @@ kfbi_status box_neu_passes(kfbi_plan *p, double kre, double kim, const void *rhs
   BoxArgs a = box_args(p, kre, kim, done);
   CorrArgs<T> c = corr_args<T>(p, static_cast<const T *>(jv));
   if (!jv) c.jv = nullptr;
-  switch (p->logm) {
-#define KFBI_CASE(L) \
-    case L: return box_neu_launch<CPLX, L>(p, a, rhs, sign, c, u, s);
-    KFBI_CASE(4) KFBI_CASE(5) KFBI_CASE(6) KFBI_CASE(7) KFBI_CASE(8) KFBI_CASE(9)
-    KFBI_CASE(10) KFBI_CASE(11) KFBI_CASE(12) KFBI_CASE(13) KFBI_CASE(14)
-#undef KFBI_CASE
-    default: return fail(KFBI_E_CONFIG, "DCT-I engine: unsupported M");
-  }
+  if constexpr (CPLX) return box_neumann_c128(p, p->logm, a, rhs, sign, c, u, s);
+  else return box_neumann_f64(p, p->logm, a, rhs, sign, c, u, s);
 }
 
 kfbi_status box_dispatch(kfbi_plan *p, int dtype, double kre, double kim, const void *rhs,
@@ -794,6 +675,17 @@ kfbi_status build_operator_T(kfbi_plan *p, double kre, double kim, int bc_kind, 
   return KFBI_OK;
 }
 
+// The on-chip operator sweeps give each CTA (one per SM) R = ceil(n / SMs)
+// rows of T, rounded up to even; the sweep kernels cover R <= 32 rows (one
+// row per lane, or row pairs on half-warps).  Larger n_ctl must use the
+// pipeline form.
+int op_sms(int device) {
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  return sms > 0 ? sms : 1;
+}
+int op_max_ctl(kfbi_plan *p) { return 32 * op_sms(p->device); }
+
 // All operator sweeps of one solve: one cooperative launch (op_solve_kernel),
 // T resident on chip (registers + shared memory) across the sweeps.
 template <typename T>
@@ -809,6 +701,9 @@ kfbi_status op_solve(kfbi_plan *p, const kfbi_bvp *b, cudaStream_t s) {
   const int n = p->n_ctl;
   int rows = (n + sms - 1) / sms;
   rows += rows & 1;                       // even: 16-byte row pairs (pair kernel)
+  if (rows > 32)
+    return fail(KFBI_E_CONFIG, "operator form: n_ctl = " + std::to_string(n) + " exceeds 32 rows per SM (" +
+                                   std::to_string(32 * sms) + " controls); use the pipeline form");
   const int grid = (n + rows - 1) / rows;
   const size_t fixed = op_smem_fixed<T>(n);
   const size_t avail = (size_t)(smem_optin - 1024) > fixed ? (size_t)(smem_optin - 1024) - fixed : 0;
@@ -1247,6 +1142,29 @@ kfbi_status kfbi_plan_set_interp(kfbi_plan *p, int32_t mode) {
   return KFBI_OK;
 }
 
+kfbi_status kfbi_plan_set_colsolver(kfbi_plan *p, int32_t mode) {
+  KFBI_TRY(check_plan(p));
+  if (mode < 0 || mode > 2) return fail(KFBI_E_CONFIG, "column solver: 0 auto, 1 tridiagonal, 2 DST-I");
+  if (p->col_mode != mode) p->op_valid = false;   // the trace operator follows the solver
+  p->col_mode = mode;
+  return KFBI_OK;
+}
+
+kfbi_status kfbi_plan_get_colsolver(kfbi_plan *p, int32_t *mode) {
+  KFBI_TRY(check_plan(p));
+  if (!mode) return fail(KFBI_E_CONFIG, "null argument");
+  *mode = p->col_mode;
+  return KFBI_OK;
+}
+
+kfbi_status kfbi_plan_colsolver_for(kfbi_plan *p, double kre, double kim, int32_t *tridiagonal,
+                                    double *bound) {
+  KFBI_TRY(check_plan(p));
+  if (tridiagonal) *tridiagonal = col_use_tri(p, kre, kim) ? 1 : 0;
+  if (bound) *bound = col_deviation_bound(p, kre, kim);
+  return KFBI_OK;
+}
+
 kfbi_status kfbi_plan_get_interp(kfbi_plan *p, int32_t *spectral) {
   KFBI_TRY(check_geo(p));
   if (!spectral) return fail(KFBI_E_CONFIG, "null argument");
@@ -1458,9 +1376,19 @@ kfbi_status kfbi_build_trace_operator_bc(kfbi_plan *p, int32_t dtype, int32_t bc
   if (bc_kind == 1 && !p->has_os)
     return fail(KFBI_E_CONFIG, "Neumann operator: one-sided extraction tables missing");
   cudaStream_t s = (cudaStream_t)stream;
+  if (p->n_ctl > op_max_ctl(p))
+    return fail(KFBI_E_CONFIG, "operator form: n_ctl = " + std::to_string(p->n_ctl) + " exceeds " +
+                                   std::to_string(op_max_ctl(p)) + " (32 rows per SM); use the pipeline form");
   if (dtype == KFBI_C128) return build_operator_T<double2>(p, kre, kim, bc_kind, box_bc, s);
   if (kim != 0.0) return fail(KFBI_E_CONFIG, "complex kappa requires the c128 path");
   return build_operator_T<double>(p, kre, kim, bc_kind, box_bc, s);
+}
+
+kfbi_status kfbi_operator_max_controls(kfbi_plan *p, int32_t *n_max) {
+  KFBI_TRY(check_plan(p));
+  if (!n_max) return fail(KFBI_E_CONFIG, "null argument");
+  *n_max = op_max_ctl(p);
+  return KFBI_OK;
 }
 
 kfbi_status kfbi_build_trace_operator(kfbi_plan *p, int32_t dtype, double kre, double kim, void *stream) {

@@ -295,6 +295,21 @@ def gather_rows(u_slab, m, group=None):
 # ---------------------------------------------------------------------------
 # slab-decomposed Richardson solve (bvp.py:276-351), dirichlet-zero box
 
+def _operands(dt, n, F, f_gamma, g, density, m_rows=None):
+    """Cast F / f_gamma / g to the solve's dtype (the kernels read raw
+    pointers of that element size) and check the in-place density."""
+    if density.dtype != dt:
+        raise ConfigError(f"density dtype {density.dtype} != the solve's {dt} (updated in place)")
+    for name, v in (("f_gamma", f_gamma), ("g", g), ("density", density)):
+        if v.numel() != n:
+            raise ConfigError(f"{name} has {v.numel()} entries, expected n_ctl = {n}")
+    if not density.is_contiguous():
+        raise ConfigError("density must be contiguous (updated in place)")
+    if m_rows is not None and tuple(F.shape) != m_rows:
+        raise GridError(f"F shape {tuple(F.shape)} != {m_rows}")
+    return (F.to(dt).contiguous(), f_gamma.to(dt).contiguous(), g.to(dt).contiguous())
+
+
 def _allreduce_sum(t, nranks, group=None):
     if nranks == 1:
         return t
@@ -344,6 +359,8 @@ class SlabRichardson:
         dt = torch.complex128 if cplx else torch.float64
         dev = F.device
         n = ws.cps.m
+        r0, r1 = self.rows
+        F, f_gamma, g = _operands(dt, n, F, f_gamma, g, density, (r1 - r0, ws.grid.m + 1))
         jm = torch.empty(6 * n, dtype=dt, device=dev)
         jv = torch.empty(3 * max(int(ws.geometry.edge_theta.size), 1), dtype=dt, device=dev)
         vals = torch.empty(13 * n, dtype=dt, device=dev)
@@ -385,10 +402,11 @@ def richardson_virtual(workspace, nranks, *, kappa, F, f_gamma, g, density, F_si
     ws.trace_tables()
     m = ws.grid.m
     F = F.reshape(m + 1, m + 1)
-    cplx = F.is_complex()
-    dt = F.dtype
+    cplx = F.is_complex() or isinstance(kappa, complex) and complex(kappa).imag != 0
+    dt = torch.complex128 if cplx else torch.float64
     dev = F.device
     n = ws.cps.m
+    F, f_gamma, g = _operands(dt, n, F, f_gamma, g, density)
     rows = [slab_rows(m, P, q) for q in range(P)]
     jm = torch.empty(6 * n, dtype=dt, device=dev)
     jv = torch.empty(3 * max(int(ws.geometry.edge_theta.size), 1), dtype=dt, device=dev)
