@@ -171,7 +171,7 @@ kfbi_status kfbi_plan_set_geometry(kfbi_plan *plan, const kfbi_geometry *geo);
  * the reference's eigenvalue table; mode 0 (default, auto) uses the
  * recurrences when their deviation bound from the reference's rounded
  * eigenvalues, E = (4.4e-16 / h^2) / min |lam_p + lam_q - kappa|, is
- * <= 1e-12 (every time-stepping kappa), the DST-I engine otherwise.  The
+ * <= 1e-11 (every time-stepping kappa), the DST-I engine otherwise.  The
  * neumann-zero closure always uses the DCT-I engine.
  * kfbi_plan_colsolver_for reports the choice and E for one kappa. */
 kfbi_status kfbi_plan_set_colsolver(kfbi_plan *plan, int32_t mode);

@@ -125,7 +125,7 @@ class Plan:
     def set_colsolver(self, mode):
         """Column stage of the dirichlet box solve: "auto" (default: the
         tridiagonal recurrences when they agree with the reference's DST
-        route to <= 1e-12, see kfbi_plan_set_colsolver), "tridiagonal"
+        route to <= 1e-11, see kfbi_plan_set_colsolver), "tridiagonal"
         (factored recurrences) or "dst" (DST-I -> divide -> DST-I)."""
         N.check(self._lib.kfbi_plan_set_colsolver(self.handle, self._COLS.index(mode)))
 

@@ -35,10 +35,27 @@ cudaError_t reg_launch(K kernel, int grid, cudaStream_t s, Args... args) {
   }
 }
 
-// Tridiagonal column pass (box_tri.cuh) of one (dtype, log2 M).
+// Tridiagonal column pass (box_tri.cuh) of one (dtype, log2 M); M = 4096 on
+// the persistent bulk-copy kernel (one CTA per SM).
 template <bool CPLX, int LOGN>
 kfbi_status cols_tri_launch(kfbi_plan *p, const BoxArgs &a, cudaStream_t s) {
   using Tc = tri::Cfg<LOGN>;
+#ifndef KFBI_TRI_NO_TMA
+  if constexpr (LOGN == tri::TMA_LOGM) {
+    static int sms = 0;
+    if (!sms) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      KFBI_CUDA(cudaFuncSetAttribute(cols_tri_tma<CPLX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     tri::TMA_SMEM), "transform-cols");
+    }
+    const int grid = a.npl < sms ? a.npl : sms;
+    return kfbi_launch(p, KFBI_K_COLS, s, [&] {
+      cols_tri_tma<CPLX><<<grid, Tc::THREADS, tri::TMA_SMEM, s>>>(a);
+    });
+  }
+#endif
   const int grid = Tc::NH == 2 ? a.npl : 2 * a.npl;
   return kfbi_launch(p, KFBI_K_COLS, s, [&] { cols_tri<CPLX, LOGN><<<grid, Tc::THREADS, 0, s>>>(a); });
 }

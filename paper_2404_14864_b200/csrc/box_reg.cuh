@@ -236,12 +236,12 @@ __global__ void __launch_bounds__(reg::Cfg<LOGN>::CTA_T, reg::Cfg<LOGN>::MINB) c
     const int p = reg::E * t + c;
     const double lp = a.lam[p];
     if (!CPLX) {
-      const int kx = 4 * pp + 2 * half;
+      const int kx = valid ? 4 * pp + 2 * half : 0;   // idle sequences stay in bounds
       const double da = (lp + a.lam[kx]) - a.kre;
       const double db = (lp + a.lam[kx + 1]) - a.kre;
       out[c] = make_double2((out[c].x / da) * a.inv4m2, (out[c].y / db) * a.inv4m2);
     } else {
-      const int kx = 2 * pp + half;
+      const int kx = valid ? 2 * pp + half : 0;
       const double2 d = make_double2((lp + a.lam[kx]) - a.kre, -a.kim);
       out[c] = cscale(cdiv(out[c], d), a.inv4m2);
     }

@@ -99,7 +99,7 @@ struct Cfg {
   static constexpr int CH = M >= 512 ? KFBI_TRI_CH : M / 16;
 #endif
 #ifndef KFBI_TRI_NH1_FROM
-  static constexpr int NH = M >= 4096 ? 1 : 2;          // 16-byte slots per CTA
+  static constexpr int NH = M >= 8192 ? 1 : 2;          // 16-byte slots per CTA
 #else
   static constexpr int NH = M >= KFBI_TRI_NH1_FROM ? 1 : 2;
 #endif
@@ -121,36 +121,29 @@ struct Cfg {
 
 }  // namespace tri
 
+// Shared memory of the scans of one CTA (NH slots, NW warps per slot).
+template <int NH, int NW>
+struct TriSmem {
+  double2 tot[NH][NW];
+  double2 z1s[NH];
+  double2 rcs[NH][6];
+};
+
+// The recurrences of one thread's CH rows [j0, j0 + CH) of column slot
+// (pp, half) held in x (in place): forward sweep + carry scan + fix-up,
+// backward sweep + carry scan + fix-up, boundary term and scale.  Every
+// thread of the CTA calls it (CTA barriers inside).
 template <bool CPLX, int LOGM>
-__global__ void __launch_bounds__(tri::Cfg<LOGM>::THREADS, tri::Cfg<LOGM>::MINB) cols_tri(BoxArgs a) {
+KFBI_DEV void tri_solve(double2 (&x)[tri::Cfg<LOGM>::CH], const BoxArgs &a, int pp, int half, int hs,
+                        int chunk, TriSmem<tri::Cfg<LOGM>::NH, tri::Cfg<LOGM>::NW> &sh) {
   using C = tri::Cfg<LOGM>;
   constexpr int M = C::M, CH = C::CH, NH = C::NH, CPW = C::CPW, NW = C::NW;
-  __shared__ double2 tot[NH][NW];
-  __shared__ double2 z1s[NH];
-  __shared__ double2 rcs[NH][6];
-  if (a.done && *a.done) return;
-  const int t = threadIdx.x;
-  const int half = NH == 2 ? (t & 1) : (blockIdx.x & 1);
-  const int hs = NH == 2 ? half : 0;            // slot index in shared memory
-  const int chunk = NH == 2 ? (t >> 1) : t;
+  auto &tot = sh.tot;
+  auto &z1s = sh.z1s;
+  auto &rcs = sh.rcs;
   const int cw = chunk & (CPW - 1);              // chunk index within the warp
   const int wv = chunk / CPW;                    // warp index within the slot
-  const int pl = NH == 2 ? blockIdx.x : (blockIdx.x >> 1);
-  if (pl >= a.npl) return;                       // whole CTA: uniform
-  const int pp = a.pp0 + pl;
-  // rows [j0, j0 + CH) of the slot: one rank block (CH divides the slab rows),
-  // 32 bytes apart
   const int j0 = chunk * CH;
-  const int lr = 31 - __clz(a.rows);
-  const int jb = j0 & (a.rows - 1);
-  const double2 *src = static_cast<const double2 *>(a.panels) +
-                       ((((size_t)(j0 >> lr) * a.npl + pl) * a.rows + jb) * 2 + half);
-  double2 *dst = a.dst[0] ? static_cast<double2 *>(a.dst[j0 >> lr]) + (((size_t)pp * a.rows + jb) * 2 + half)
-                          : const_cast<double2 *>(src);
-  double2 x[CH];
-#pragma unroll
-  for (int i = 0; i < CH; ++i) x[i] = (j0 + i >= 1) ? src[2 * i] : make_double2(0.0, 0.0);
-
   // per-column root r and A = r h^2 / (2M)
   const double hh2 = 0.5 * a.h2;
   double2 r;
@@ -306,8 +299,131 @@ __global__ void __launch_bounds__(tri::Cfg<LOGM>::THREADS, tri::Cfg<LOGM>::MINB)
       else x[i].x = 0.0;
     }
   }
+}
+
+template <bool CPLX, int LOGM>
+__global__ void __launch_bounds__(tri::Cfg<LOGM>::THREADS, tri::Cfg<LOGM>::MINB) cols_tri(BoxArgs a) {
+  using C = tri::Cfg<LOGM>;
+  constexpr int CH = C::CH, NH = C::NH;
+  __shared__ TriSmem<NH, C::NW> sh;
+  if (a.done && *a.done) return;
+  const int t = threadIdx.x;
+  const int half = NH == 2 ? (t & 1) : (blockIdx.x & 1);
+  const int hs = NH == 2 ? half : 0;            // slot index in shared memory
+  const int chunk = NH == 2 ? (t >> 1) : t;
+  const int pl = NH == 2 ? blockIdx.x : (blockIdx.x >> 1);
+  if (pl >= a.npl) return;                       // whole CTA: uniform
+  const int pp = a.pp0 + pl;
+  // rows [j0, j0 + CH) of the slot: one rank block (CH divides the slab rows),
+  // 32 bytes apart
+  const int j0 = chunk * CH;
+  const int lr = 31 - __clz(a.rows);
+  const int jb = j0 & (a.rows - 1);
+  const double2 *src = static_cast<const double2 *>(a.panels) +
+                       ((((size_t)(j0 >> lr) * a.npl + pl) * a.rows + jb) * 2 + half);
+  double2 *dst = a.dst[0] ? static_cast<double2 *>(a.dst[j0 >> lr]) + (((size_t)pp * a.rows + jb) * 2 + half)
+                          : const_cast<double2 *>(src);
+  double2 x[CH];
+#pragma unroll
+  for (int i = 0; i < CH; ++i) x[i] = (j0 + i >= 1) ? src[2 * i] : make_double2(0.0, 0.0);
+  tri_solve<CPLX, LOGM>(x, a, pp, half, hs, chunk, sh);
 #pragma unroll
   for (int i = 0; i < CH; ++i) dst[2 * i] = (j0 + i >= 1) ? x[i] : make_double2(0.0, 0.0);
+}
+
+// ---------------------------------------------------------------------------
+// M = 4096: one persistent CTA per SM walks the strips; while it solves strip
+// s from registers, the bulk-copy engine (cp.async.bulk, mbarrier completion)
+// already streams strip s + grid into shared memory, so HBM reads overlap the
+// recurrences and the stores.  The strip (M rows x 32 bytes, contiguous) is
+// copied as 1 KB chunks (the 32 rows of one thread pair) to 1056-byte slots:
+// the 16-byte reads of a quarter warp then hit 8 distinct bank groups.
+namespace tri {
+constexpr int TMA_LOGM = 12;
+constexpr int TMA_SLOT = 1056;                      // bytes per 32-row chunk in smem
+constexpr int TMA_SMEM = (1 << TMA_LOGM) / 32 * TMA_SLOT;
+
+KFBI_DEV uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+KFBI_DEV void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+KFBI_DEV void mbar_arrive_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+KFBI_DEV void mbar_wait(uint64_t *bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+KFBI_DEV void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+}  // namespace tri
+
+template <bool CPLX>
+__global__ void __launch_bounds__(tri::Cfg<tri::TMA_LOGM>::THREADS, 1) cols_tri_tma(BoxArgs a) {
+  constexpr int LOGM = tri::TMA_LOGM;
+  using C = tri::Cfg<LOGM>;
+  constexpr int CH = C::CH, NH = C::NH, NCH = C::NCH;
+  static_assert(NH == 2 && CH == 32, "bulk-copy column pass: thread pairs own 32-row chunks");
+  extern __shared__ __align__(128) unsigned char tbuf[];
+  __shared__ TriSmem<NH, C::NW> sh;
+  __shared__ __align__(8) uint64_t bar;
+  if (a.done && *a.done) return;
+  const int t = threadIdx.x;
+  const int half = t & 1, chunk = t >> 1;
+  const int lr = 31 - __clz(a.rows);
+  auto chunk_src = [&](int pl, int k) -> const unsigned char * {
+    const int j = k * CH;
+    const size_t blk = (size_t)(j >> lr) * a.npl + pl;
+    return reinterpret_cast<const unsigned char *>(a.panels) + ((blk * a.rows + (j & (a.rows - 1))) * 32);
+  };
+  auto issue = [&](int pl) {                     // warp 0: 128 chunk copies of 1 KB
+    if (t < 32) {
+      if (t == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        tri::mbar_arrive_tx(&bar, NCH * 1024);
+      }
+      __syncwarp();
+      for (int k = t; k < NCH; k += 32) tri::bulk_g2s(tbuf + k * tri::TMA_SLOT, chunk_src(pl, k), 1024, &bar);
+    }
+  };
+  if (t == 0) {
+    tri::mbar_init(&bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  uint32_t parity = 0;
+  int pl = blockIdx.x;
+  if (pl < a.npl) issue(pl);
+  for (; pl < a.npl; pl += gridDim.x) {
+    tri::mbar_wait(&bar, parity);
+    parity ^= 1;
+    double2 x[CH];
+    const unsigned char *mine = tbuf + chunk * tri::TMA_SLOT + half * 16;
+#pragma unroll
+    for (int i = 0; i < CH; ++i) x[i] = *reinterpret_cast<const double2 *>(mine + i * 32);
+    if (chunk == 0) x[0] = make_double2(0.0, 0.0);   // row 0: the zero ring
+    __syncthreads();                             // the buffer is free again
+    if (pl + (int)gridDim.x < a.npl) issue(pl + gridDim.x);
+    const int pp = a.pp0 + pl;
+    tri_solve<CPLX, LOGM>(x, a, pp, half, half, chunk, sh);
+    const int j0 = chunk * CH, jb = j0 & (a.rows - 1);
+    double2 *dst = a.dst[0] ? static_cast<double2 *>(a.dst[j0 >> lr]) + (((size_t)pp * a.rows + jb) * 2 + half)
+                            : static_cast<double2 *>(a.panels) +
+                                  ((((size_t)(j0 >> lr) * a.npl + pl) * a.rows + jb) * 2 + half);
+#pragma unroll
+    for (int i = 0; i < CH; ++i) dst[2 * i] = (j0 + i >= 1) ? x[i] : make_double2(0.0, 0.0);
+  }
 }
 
 }  // namespace kfbi

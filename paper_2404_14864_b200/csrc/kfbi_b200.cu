@@ -280,7 +280,7 @@ ExtractArgs extract_args(kfbi_plan *p, bool onesided = false) {
 // to ~4.4e-16 / h^2, i.e. the reference applies the exact discrete inverse
 // only up to E = (4.4e-16 / h^2) / min |lam_p + lam_q - kappa| relative.  The
 // tridiagonal recurrences apply the exact three-point inverse, so they agree
-// with the reference to ~E; auto mode uses them when E <= 1e-12 (every
+// with the reference to ~E; auto mode uses them when E <= 1e-11 (every
 // time-stepping kappa: 2c/tau, 1/(theta tau^2), 2i/tau) and the DST-I engine,
 // which shares the reference's eigenvalue table, otherwise (kappa ~ 0).
 double col_deviation_bound(const kfbi_plan *p, double kre, double kim) {
@@ -295,7 +295,7 @@ double col_deviation_bound(const kfbi_plan *p, double kre, double kim) {
 bool col_use_tri(const kfbi_plan *p, double kre, double kim) {
   if (p->col_mode == 1) return true;
   if (p->col_mode == 2) return false;
-  return col_deviation_bound(p, kre, kim) <= 1e-12;
+  return col_deviation_bound(p, kre, kim) <= 1e-11;
 }
 
 template <bool CPLX>
