@@ -35,12 +35,13 @@ cudaError_t reg_launch(K kernel, int grid, cudaStream_t s, Args... args) {
   }
 }
 
-// Tridiagonal column pass (box_tri.cuh) of one (dtype, log2 M); M = 4096 on
-// the persistent bulk-copy kernel (one CTA per SM).
+// Tridiagonal column pass (box_tri.cuh) of one (dtype, log2 M).  The
+// persistent bulk-copy variant (KFBI_TRI_TMA) measured 2-9 % slower than the
+// register kernel at M = 4096 (profiles/r2_v7_ab_tri.log) and is opt-in.
 template <bool CPLX, int LOGN>
 kfbi_status cols_tri_launch(kfbi_plan *p, const BoxArgs &a, cudaStream_t s) {
   using Tc = tri::Cfg<LOGN>;
-#ifndef KFBI_TRI_NO_TMA
+#ifdef KFBI_TRI_TMA
   if constexpr (LOGN == tri::TMA_LOGM) {
     static int sms = 0;
     if (!sms) {

@@ -122,29 +122,36 @@ struct Cfg {
 }  // namespace tri
 
 // Shared memory of the scans of one CTA (NH slots, NW warps per slot).
+constexpr int TRI_NPOW = 12;                     // r^(CH 2^s), s < 12 (exponents < 2^12 CH)
 template <int NH, int NW>
 struct TriSmem {
   double2 tot[NH][NW];
   double2 z1s[NH];
-  double2 rcs[NH][6];
+  double2 rcs[NH][TRI_NPOW];
+  double2 w0s[NH];
 };
 
 // The recurrences of one thread's CH rows [j0, j0 + CH) of column slot
-// (pp, half) held in x (in place): forward sweep + carry scan + fix-up,
-// backward sweep + carry scan + fix-up, boundary term and scale.  Every
-// thread of the CTA calls it (CTA barriers inside).
+// (pp, half) held in x (in place).  Every thread of the CTA calls it (CTA
+// barriers inside).  With local sweeps from zero
+//   vL_i = r vL_{i-1} - P_i,   zL_i = r zL_{i+1} + vL_i
+// the exact chunk values are v_i = vL_i + r^{i+1} V and
+// z_i = zL_i + V w_i + Z r^{CH-i}, w_i = sum_{m>=i} r^{2m-i+1}
+// = (r^{i+1} - r^{2CH-i+1}) / (1 - r^2), where V (true v at row j0 - 1) and
+// Z (true z at row j0 + CH) come from two affine scans over the chunks: the
+// forward one of the local ends vL_{CH-1}, the backward one of the chunk
+// starts zL_0 + V w_0.  Both local sweeps run back to back; the epilogue
+//   out_i = A z_i + B (r^j - r^{2M-j}) = A zL_i + alpha r^i + gamma r^{CH-1-i}
+// is two multiply chains.
 template <bool CPLX, int LOGM>
 KFBI_DEV void tri_solve(double2 (&x)[tri::Cfg<LOGM>::CH], const BoxArgs &a, int pp, int half, int hs,
                         int chunk, TriSmem<tri::Cfg<LOGM>::NH, tri::Cfg<LOGM>::NW> &sh) {
   using C = tri::Cfg<LOGM>;
-  constexpr int M = C::M, CH = C::CH, NH = C::NH, CPW = C::CPW, NW = C::NW;
-  auto &tot = sh.tot;
-  auto &z1s = sh.z1s;
-  auto &rcs = sh.rcs;
+  constexpr int CH = C::CH, NH = C::NH, CPW = C::CPW, NW = C::NW, NCH = C::NCH;
+  static_assert(2 * NCH < (1 << TRI_NPOW), "power table");
   const int cw = chunk & (CPW - 1);              // chunk index within the warp
   const int wv = chunk / CPW;                    // warp index within the slot
-  const int j0 = chunk * CH;
-  // per-column root r and A = r h^2 / (2M)
+  // per-column root r
   const double hh2 = 0.5 * a.h2;
   double2 r;
   int kx0;
@@ -157,116 +164,111 @@ KFBI_DEV void tri_solve(double2 (&x)[tri::Cfg<LOGM>::CH], const BoxArgs &a, int 
     r = make_double2(kx0 == 0 ? 0.0 : tri::root_real((a.kre - a.lam[kx0]) * hh2),
                      tri::root_real((a.kre - a.lam[kx0 + 1]) * hh2));
   }
-  // chunk multiplier powers rc2[s] = r^(CH 2^s), one copy per slot in shared
-  // memory (kept out of the registers that hold the column)
+  const double2 zero = make_double2(0.0, 0.0);
+
+  // ---- local sweeps (no dependence on other chunks) ------------------------
+  double2 e = zero;
+#pragma unroll
+  for (int i = 0; i < CH; ++i) {
+    e = tri::mad<CPLX>(r, e, cneg(x[i]));
+    x[i] = e;                                    // vL
+  }
+  const double2 eF = e;                          // vL_{CH-1}
+  e = zero;
+#pragma unroll
+  for (int i = CH - 1; i >= 0; --i) {
+    e = tri::mad<CPLX>(r, e, x[i]);
+    x[i] = e;                                    // zL
+  }
+  const double2 sL = e;                          // zL_0
+
+  // per-slot powers r^(CH 2^s) and w_0 = sum_{m<CH} r^{2m+1} (chunk 0, shared)
   if (chunk == 0) {
     double2 q = tri::pw<CPLX>(r, CH);
 #pragma unroll
-    for (int s = 0; s < 6; ++s) {
-      rcs[hs][s] = q;
+    for (int s2 = 0; s2 < TRI_NPOW; ++s2) {
+      sh.rcs[hs][s2] = q;
       q = tri::mul<CPLX>(q, q);
     }
+    const double2 r2 = tri::mul<CPLX>(r, r);
+    double2 w = zero;
+#pragma unroll 4
+    for (int m = CH - 1; m >= 0; --m) w = tri::mad<CPLX>(r2, w, r);   // Horner: r sum r^{2m}
+    sh.w0s[hs] = w;
   }
   __syncthreads();
-  auto rc2 = [&](int s) -> double2 { return rcs[hs][s]; };
-  auto rc_pow = [&](int e) -> double2 {          // r^(CH e), 0 <= e <= 32
+  auto rc2 = [&](int s2) -> double2 { return sh.rcs[hs][s2]; };
+  auto rc_pow = [&](int ex) -> double2 {        // r^(CH ex), 0 <= ex < 2^TRI_NPOW
     double2 acc = tri::one<CPLX>();
 #pragma unroll
-    for (int s = 0; s < 6; ++s)
-      if (e & (1 << s)) acc = tri::mul<CPLX>(acc, rc2(s));
+    for (int s2 = 0; s2 < TRI_NPOW; ++s2)
+      if (ex & (1 << s2)) acc = tri::mul<CPLX>(acc, rc2(s2));
     return acc;
   };
   const int sl = NH;                             // lane stride between chunks of a slot
 
-  // ---- forward: v_j = r v_{j-1} - P_j, v_0 = 0 --------------------------
-  double2 e = make_double2(0.0, 0.0);
+  // ---- forward carries: I_k = eF_k + r^CH I_{k-1}, V_k = I_{k-1} ----------
+  double2 I = eF;
 #pragma unroll
-  for (int i = 0; i < CH; ++i) {
-    e = tri::mad<CPLX>(r, e, cneg(x[i]));
-    x[i] = e;
-  }
-  // inclusive scan over the chunks of this slot: I_k = e_k + r^CH I_{k-1}
-  double2 I = e;
-#pragma unroll
-  for (int s = 0; s < C::LCPW; ++s) {
-    const int d = 1 << s;
+  for (int s2 = 0; s2 < C::LCPW; ++s2) {
+    const int d = 1 << s2;
     double2 y;
     y.x = __shfl_up_sync(0xffffffffu, I.x, d * sl);
     y.y = __shfl_up_sync(0xffffffffu, I.y, d * sl);
-    if (cw >= d) I = tri::mad<CPLX>(rc2(s), y, I);
+    if (cw >= d) I = tri::mad<CPLX>(rc2(s2), y, I);
   }
-  double2 V;                                     // carry into this chunk
+  double2 V;
   {
-    double2 acc = make_double2(0.0, 0.0);        // carry into this warp
+    double2 acc = zero;                          // carry into this warp
     if constexpr (NW > 1) {
-      if (cw == CPW - 1) tot[hs][wv] = I;
+      if (cw == CPW - 1) sh.tot[hs][wv] = I;
       __syncthreads();
       const double2 rw = rc_pow(CPW);
-      for (int w = 0; w < wv; ++w) acc = tri::mad<CPLX>(rw, acc, tot[hs][w]);
+      for (int w = 0; w < wv; ++w) acc = tri::mad<CPLX>(rw, acc, sh.tot[hs][w]);
       I = tri::mad<CPLX>(rc_pow(cw + 1), acc, I);
     }
     V.x = __shfl_up_sync(0xffffffffu, I.x, sl);
     V.y = __shfl_up_sync(0xffffffffu, I.y, sl);
     if (cw == 0) V = acc;
   }
-  {
-    double2 c = V;                               // r^(i+1) V (a chain on V: not hoisted)
-#pragma unroll
-    for (int i = 0; i < CH; ++i) {
-      c = tri::mul<CPLX>(r, c);
-      x[i] = cadd(x[i], c);
-    }
-  }
 
-  // ---- backward: z_j = r z_{j+1} + v_j, z_M = 0 ---------------------------
-  e = make_double2(0.0, 0.0);
+  // ---- backward carries: J_k = s_k + r^CH J_{k+1}, s_k = zL_0 + V w_0 -----
+  double2 J = tri::mad<CPLX>(V, sh.w0s[hs], sL);
 #pragma unroll
-  for (int i = CH - 1; i >= 0; --i) {
-    e = tri::mad<CPLX>(r, e, x[i]);
-    x[i] = e;
-  }
-  // reverse inclusive scan: J_k = s_k + r^CH J_{k+1}
-  double2 J = e;
-#pragma unroll
-  for (int s = 0; s < C::LCPW; ++s) {
-    const int d = 1 << s;
+  for (int s2 = 0; s2 < C::LCPW; ++s2) {
+    const int d = 1 << s2;
     double2 y;
     y.x = __shfl_down_sync(0xffffffffu, J.x, d * sl);
     y.y = __shfl_down_sync(0xffffffffu, J.y, d * sl);
-    if (cw + d < CPW) J = tri::mad<CPLX>(rc2(s), y, J);
+    if (cw + d < CPW) J = tri::mad<CPLX>(rc2(s2), y, J);
   }
-  double2 Z;                                     // z at the first row after this chunk
+  double2 Z;                                     // true z at row j0 + CH
   {
-    double2 acc = make_double2(0.0, 0.0);        // carry into this warp from below
+    double2 acc = zero;                          // carry into this warp from below
     if constexpr (NW > 1) {
       __syncthreads();                           // forward totals consumed
-      if (cw == 0) tot[hs][wv] = J;
+      if (cw == 0) sh.tot[hs][wv] = J;
       __syncthreads();
       const double2 rw = rc_pow(CPW);
-      for (int w = NW - 1; w > wv; --w) acc = tri::mad<CPLX>(rw, acc, tot[hs][w]);
+      for (int w = NW - 1; w > wv; --w) acc = tri::mad<CPLX>(rw, acc, sh.tot[hs][w]);
       J = tri::mad<CPLX>(rc_pow(CPW - cw), acc, J);
     }
     Z.x = __shfl_down_sync(0xffffffffu, J.x, sl);
     Z.y = __shfl_down_sync(0xffffffffu, J.y, sl);
     if (cw == CPW - 1) Z = acc;
   }
-  {
-    double2 c = Z;                               // r^(CH - i) Z
-#pragma unroll
-    for (int i = CH - 1; i >= 0; --i) {
-      c = tri::mul<CPLX>(r, c);
-      x[i] = cadd(x[i], c);
-    }
-  }
 
-  // ---- boundary term: z_1 of this slot's columns --------------------------
-  constexpr int c1 = CH > 1 ? 0 : 1, i1 = CH > 1 ? 1 : 0;
-  if (chunk == c1) z1s[hs] = x[i1];
+  // ---- boundary term: true z_1 of this slot --------------------------------
+  // z_1 = zL_1 + V_0 w_1 + Z_0 r^{CH-1} with V_0 = 0 (chunk 0), or z_1 = zL_0
+  // + Z r (CH = 1: row 1 is chunk 1's only row)
+  const double2 rch = rc2(0);                    // r^CH
+  if (CH > 1 && chunk == 0) sh.z1s[hs] = tri::mad<CPLX>(Z, tri::pw<CPLX>(r, CH - 1), x[CH > 1 ? 1 : 0]);
+  if (CH == 1 && chunk == 1) sh.z1s[hs] = tri::mad<CPLX>(V, sh.w0s[hs], tri::mad<CPLX>(Z, r, x[0]));
   __syncthreads();
-  const double2 z1 = z1s[hs];
-  const double2 A = tri::mul<CPLX>(r, CPLX ? make_double2(a.h2 / (2.0 * M), 0.0)
-                                           : make_double2(a.h2 / (2.0 * M), a.h2 / (2.0 * M)));
-  const double2 r2m = tri::pw<CPLX>(r, 2 * M);
+  const double2 z1 = sh.z1s[hs];
+  const double sc = a.h2 / (2.0 * C::M);
+  const double2 A = tri::mul<CPLX>(r, CPLX ? make_double2(sc, 0.0) : make_double2(sc, sc));
+  const double2 r2m = rc_pow(2 * NCH);           // r^{2M}
   double2 B;                                     // -A r z1 / (1 - r^2M)
   {
     const double2 num = tri::mul<CPLX>(tri::mul<CPLX>(A, r), z1);
@@ -277,25 +279,39 @@ KFBI_DEV void tri_solve(double2 (&x)[tri::Cfg<LOGM>::CH], const BoxArgs &a, int 
       if (kx0 == 0) B.x = 0.0;
     }
   }
-  // out_j = A z_j - B r^(2M-j) + B r^j  (power chains seeded with B)
+  // alpha = A V r / (1 - r^2) + B r^{j0}
+  // gamma = -A V r^{CH+2} / (1 - r^2) + A Z r - B r^{2M - j0 - CH + 1}
+  double2 inv1mr2;                               // 1 / ((1 - r)(1 + r))
   {
-    double2 c = tri::mul<CPLX>(cneg(B), tri::pw<CPLX>(r, 2 * M - j0 - CH));
+    const double2 d = tri::mul<CPLX>(make_double2(1.0 - r.x, -r.y),
+                                     CPLX ? make_double2(1.0 + r.x, r.y) : make_double2(1.0 + r.y, 0.0));
+    if constexpr (CPLX) inv1mr2 = cdiv(make_double2(1.0, 0.0), d);
+    else inv1mr2 = make_double2(1.0 / ((1.0 - r.x) * (1.0 + r.x)), 1.0 / ((1.0 - r.y) * (1.0 + r.y)));
+  }
+  const double2 AVq = tri::mul<CPLX>(tri::mul<CPLX>(A, V), inv1mr2);          // A V / (1 - r^2)
+  const double2 alpha = tri::mad<CPLX>(AVq, r, tri::mul<CPLX>(B, rc_pow(chunk)));
+  const double2 rch1 = tri::mul<CPLX>(rch, r);   // r^{CH+1}
+  double2 gamma = tri::mul<CPLX>(tri::mul<CPLX>(AVq, rch1), r);                 // A V r^{CH+2} / (1 - r^2)
+  gamma = tri::mad<CPLX>(tri::mul<CPLX>(A, Z), r, cneg(gamma));
+  gamma = tri::mad<CPLX>(cneg(B), tri::mul<CPLX>(rc_pow(2 * NCH - chunk - 1), r), gamma);
+  {
+    double2 c = alpha;                           // alpha r^i
 #pragma unroll
-    for (int i = CH - 1; i >= 0; --i) {          // c = -B r^(2M - j0 - i)
-      c = tri::mul<CPLX>(r, c);
+    for (int i = 0; i < CH; ++i) {
       x[i] = tri::mad<CPLX>(A, x[i], c);
+      c = tri::mul<CPLX>(c, r);
     }
-    c = tri::mul<CPLX>(B, tri::pw<CPLX>(r, j0));
+    c = gamma;                                   // gamma r^{CH-1-i}
 #pragma unroll
-    for (int i = 0; i < CH; ++i) {               // c = B r^(j0 + i)
+    for (int i = CH - 1; i >= 0; --i) {
       x[i] = cadd(x[i], c);
-      c = tri::mul<CPLX>(r, c);
+      c = tri::mul<CPLX>(c, r);
     }
   }
   if (kx0 == 0) {                                // padding column kx = 0
 #pragma unroll
     for (int i = 0; i < CH; ++i) {
-      if constexpr (CPLX) x[i] = make_double2(0.0, 0.0);
+      if constexpr (CPLX) x[i] = zero;
       else x[i].x = 0.0;
     }
   }
