@@ -210,7 +210,7 @@ def run_ours(args):
     wl = workload(m)
     backend = k.CudaBackend(local, timing=False)
     ctxs, specs, states, steppers = {}, {}, {}, {}
-    kappas, op_build_s = {}, {}
+    kappas, op_build_s, startups = {}, {}, {}
     t_setup = time.time()
     for eq in eqs:
         box, curve, kw = wl[eq]
@@ -219,6 +219,7 @@ def run_ours(args):
         specs[eq] = k.ProblemSpec(**kw)
         startup, step = _stepper_for(specs[eq])
         steppers[eq] = step
+        startups[eq] = startup
         states[eq] = startup(specs[eq], ctxs[eq])
         kap = {"heat": 2.0 * specs[eq].c / specs[eq].tau,
                "wave": 1.0 / (specs[eq].theta * specs[eq].tau ** 2),
@@ -239,12 +240,25 @@ def run_ours(args):
         states[eq] = st
         return st
 
-    for _ in range(args.warmup):
+    def fresh():
+        # every timed region starts from t = 0: startup + W untimed warm-up
+        # steps (the cold first step included), so the timed window is
+        # steps W+1..W+K of each equation, the same early regime the
+        # reference arm times (the wave iteration counts grow later in the
+        # run)
+        torch.cuda.synchronize()
+        for c in ctxs.values():
+            c.flush()
         for eq in eqs:
-            advance(eq)
-    torch.cuda.synchronize()
-    for c in ctxs.values():
-        c.flush()
+            states[eq] = startups[eq](specs[eq], ctxs[eq])
+        for _ in range(args.warmup):
+            for eq in eqs:
+                advance(eq)
+        torch.cuda.synchronize()
+        for c in ctxs.values():
+            c.flush()
+
+    fresh()
 
     plans = [c.plan for c in ctxs.values()]
     for p in plans:
@@ -256,6 +270,8 @@ def run_ours(args):
     reps_ms = []
     with Clocks(local) as clk:
         for rep in range(args.repeats):
+            if rep:
+                fresh()
             _barrier(ws)
             torch.cuda.synchronize()
             start = torch.cuda.Event(enable_timing=True)
@@ -290,6 +306,7 @@ def run_ours(args):
     # kernel-duration pass: the same K steps again with every launch of our
     # kernels bracketed by CUDA events on the launching stream (kept out of
     # the headline pass, whose host side it would slow down)
+    fresh()
     for p in plans:
         p.reset_kernel_times()
         p.set_timing(True)
@@ -344,6 +361,7 @@ def run_ours(args):
     del probe, host
     # warm-up of the e2e path (untimed): first DMA into fresh pinned pages and
     # the staging buffers' first use cost ~2x a steady step
+    fresh()
     for _ in range(args.warmup):
         for eq in eqs:
             st = advance(eq)
@@ -351,8 +369,7 @@ def run_ours(args):
     for c in ctxs.values():
         c.host_sync()
     torch.cuda.synchronize()
-    for c in ctxs.values():
-        c.flush()
+    fresh()
     _barrier(ws)
     torch.cuda.synchronize()
     s2 = torch.cuda.Event(enable_timing=True)
@@ -381,9 +398,7 @@ def run_ours(args):
         for c in ctxs.values():
             c.flush()
             c.operator = False
-        for _ in range(2):
-            for eq in eqs:
-                advance(eq)
+        fresh()
         torch.cuda.synchronize()
         pipe_it = {eq: [] for eq in eqs}
         pev = {eq: [] for eq in eqs}
@@ -416,6 +431,11 @@ def run_ours(args):
                                       "iterations": pipe_it[eq]} for eq in eqs}}
         for c in ctxs.values():
             c.operator = True
+
+    # ---- BASELINE configs[0..2] (C1-C3) through run(), rank-local
+    configs = None
+    if not args.no_configs:
+        configs = run_configs(args, local, with_cpu=(rank == 0 and ws == 1 and not args.no_cpu_baseline))
 
     # ---- C5 (BASELINE configs[4]): one 16384^2 solve, slab-decomposed over the N ranks
     slab = None
@@ -493,11 +513,92 @@ def run_ours(args):
                  "operator_incl_build": op_build_s.get(eq, 0.0) + n_t1 * per_eq_ms[eq] / 1e3,
                  "pipeline": n_t1 * pipe["per_equation"][eq]["ms_per_step"] / 1e3}
             for eq in eqs}
+    if configs is not None:
+        line["configs"] = configs
     if slab is not None:
         line["slab_c5"] = slab
     if not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(ctxs, specs, iters, args)
     return line
+
+
+def config_cases():
+    """BASELINE.json configs[0..2] as run() specs."""
+    import paper_2404_14864_b200 as k
+
+    box = (-1.5, 1.5, -1.5, 1.5)
+    pibox = (-np.pi, np.pi, -np.pi, np.pi)
+    heat, wave, schr = k.HeatPlaneDecay(1.0), k.WaveStanding(0.0), k.SchrodingerPhaseRotation()
+    return {
+        "C1": ("heat CN, flower star(1, 0.2, 8), 128^2, tau 0.01, T 1 (100 steps)",
+               box, 128, k.StarCurve(1.0, c=0.2, lobes=8),
+               dict(equation="heat", bc_kind="dirichlet", g=heat.dirichlet, u0=heat.u0,
+                    lap_u0=heat.lap_u0, tau=0.01, t_final=1.0, c=1.0)),
+        "C2": ("wave theta 1/4, ellipse (1.2, 0.8), 1024^2, tau 1/64, T 1 (64 steps)",
+               box, 1024, k.EllipseCurve(1.2, 0.8),
+               dict(equation="wave", bc_kind="dirichlet", g=wave.dirichlet, u0=wave.u0,
+                    lap_u0=wave.lap_u0, v0=wave.v0, lap_v0=wave.lap_v0, tau=1 / 64, t_final=1.0,
+                    theta=0.25)),
+        "C3": ("Schrodinger Strang (c128), star(1.5, 0.2, 3) on [-pi, pi]^2, 2048^2, tau 1/128, "
+               "T 1 (128 steps)", pibox, 2048, k.StarCurve(1.5, c=0.2, lobes=3),
+               dict(equation="schrodinger", bc_kind="dirichlet", g=schr.dirichlet, u0=schr.u0,
+                    lap_u0=schr.lap_u0, potential=schr.potential, w=1.0, tau=1 / 128, t_final=1.0)),
+    }
+
+
+def run_configs(args, local, with_cpu):
+    """Each config end to end through the public run() API (numpy in, numpy
+    out: setup, operator build when run(operator="auto") picks it, every
+    step, the final field copied to the host), wall-clocked after a warm-up
+    run; C1 also on the host CPU with the oracle port (the reference's own
+    size)."""
+    import torch
+
+    import paper_2404_14864_b200 as k
+
+    out = {}
+    backend = k.CudaBackend(local, timing=False)
+    for name, (desc, box, m, curve, kw) in config_cases().items():
+        geo = k.build_grid(box, m, curve)
+        spec = k.ProblemSpec(**kw)
+        k.run(spec, geo, backend=backend)              # warm-up (first-use allocations)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        res = k.run(spec, geo, backend=backend)
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+        ctx = k.StepContext(geo, backend=backend)
+        n = spec.n_steps()
+        from paper_2404_14864_b200.timestepping import operator_pays
+        row = {"workload": desc, "steps": n, "run_wall_s": wall, "steps_per_s_run": n / wall,
+               "iterations_total": int(sum(res.iterations)),
+               "operator_form": bool(operator_pays(ctx, n)), "n_ctl": int(ctx.n_ctl)}
+        # steady stepping rate: the same run() with the context (setup) reused
+        k.run(spec, geo, context=ctx)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        res2 = k.run(spec, geo, context=ctx)
+        torch.cuda.synchronize()
+        row["steps_per_s_steady"] = n / (time.perf_counter() - t0)
+        row["iterations_match"] = res2.iterations == res.iterations
+        if with_cpu and name == "C1":
+            from oracle import kfbi_oracle as O
+            sys.path.insert(0, os.path.join(ROOT, "tests"))
+            from conftest import oracle_spec
+
+            O.WORKERS = _cpu_threads()
+            tabs = O.tables_from_workspace(ctx.workspace)
+            t0 = time.perf_counter()
+            st = O.run(tabs, oracle_spec(kw))
+            cpu = time.perf_counter() - t0
+            row["cpu_oracle"] = {"wall_s": cpu, "steps_per_s": n / cpu, "cores": _cpu_threads(),
+                                 "iterations_match": list(st.iterations) == list(res.iterations),
+                                 "max_rel_diff": float(np.max(np.abs(res.state.u - st.u))
+                                                       / np.max(np.abs(st.u)))}
+        out[name] = row
+        del ctx
+        torch.cuda.empty_cache()
+    return out
 
 
 def c5_problem(m, rank, ws, local, p2p, torch):
@@ -563,6 +664,83 @@ def slab_c5(args, ws, rank, local, p2p):
                           "transposes fused into the passes (CUDA IPC peer stores + peer-flag "
                           "barrier) + NCCL all_reduce" if p2p else
                           "NCCL all_to_all_single + all_reduce")}
+
+
+def c4_cases():
+    """SURVEY §6.3 / BASELINE configs[3]: the reference CLI's convergence
+    geometries (heat star k=5, wave ellipse, Schrodinger star3 on [-pi, pi]^2)."""
+    import paper_2404_14864_b200 as k
+
+    box = (-1.5, 1.5, -1.5, 1.5)
+    pibox = (-np.pi, np.pi, -np.pi, np.pi)
+    heat, wave, schr = k.HeatPlaneDecay(1.0), k.WaveStanding(0.0), k.SchrodingerPhaseRotation()
+    return {
+        "heat": (box, k.StarCurve(1.0, c=0.2, lobes=5), heat, dict(
+            equation="heat", bc_kind="dirichlet", g=heat.dirichlet, u0=heat.u0,
+            lap_u0=heat.lap_u0, c=1.0)),
+        "wave": (box, k.EllipseCurve(1.2, 0.8), wave, dict(
+            equation="wave", bc_kind="dirichlet", g=wave.dirichlet, u0=wave.u0,
+            lap_u0=wave.lap_u0, v0=wave.v0, lap_v0=wave.lap_v0, theta=0.25)),
+        "schrodinger": (pibox, k.StarCurve(1.5, c=0.2, lobes=3), schr, dict(
+            equation="schrodinger", bc_kind="dirichlet", g=schr.dirichlet, u0=schr.u0,
+            lap_u0=schr.lap_u0, potential=schr.potential, w=1.0)),
+    }
+
+
+def run_c4(args):
+    """--workload c4 (BASELINE configs[3], report.py:183-225 convergence_study):
+    every equation at M = 256..4096, tau = 0.25 * 64 / M, T = 1, errors
+    against the exact solution over the interior nodes, orders log2(e_M /
+    e_2M), and the steady steps/s of each size (run() with the context
+    reused, after one untimed run)."""
+    import torch
+
+    import paper_2404_14864_b200 as k
+
+    ws, rank, local = _dist()
+    torch.cuda.set_device(local)
+    sizes = [int(x) for x in args.c4_sizes.split(",")]
+    backend = k.CudaBackend(local, timing=False)
+    table = {}
+    t_all = time.time()
+    for eq, (box, curve, sol, kw) in c4_cases().items():
+        rows = []
+        for m in sizes:
+            t0 = time.time()
+            geo = k.build_grid(box, m, curve)
+            spec = k.ProblemSpec(tau=0.25 * 64 / m, t_final=1.0, **kw)
+            ctx = k.StepContext(geo, backend=backend)
+            setup = time.time() - t0
+            t0 = time.perf_counter()
+            res = k.run(spec, geo, context=ctx)        # incl. the operator build
+            torch.cuda.synchronize()
+            first = time.perf_counter() - t0
+            t0 = time.perf_counter()
+            res = k.run(spec, geo, context=ctx)
+            torch.cuda.synchronize()
+            steady = time.perf_counter() - t0
+            e_inf, e_2 = k.compute_errors(res.state.u, lambda x, y: sol.u(x, y, 1.0), geo.grid,
+                                          geo.classification)
+            n = spec.n_steps()
+            rows.append({"m": m, "steps": n, "e_inf": float(e_inf), "e_2": float(e_2),
+                         "mean_iterations": float(np.mean(res.iterations)),
+                         "steps_per_s": n / steady, "first_run_s": first, "setup_s": setup,
+                         "operator_form": bool(ctx.operator)})
+            del ctx
+            torch.cuda.empty_cache()
+        for a, b in zip(rows[:-1], rows[1:]):
+            b["order_inf"] = float(np.log2(a["e_inf"] / b["e_inf"]))
+            b["order_2"] = float(np.log2(a["e_2"] / b["e_2"]))
+        table[eq] = rows
+    if rank != 0:
+        return None
+    return {"metric": "KFBI convergence sweep (C4): errors, orders and steps/s per size",
+            "value": min(r["steps_per_s"] for rows in table.values() for r in rows if r["m"] == sizes[-1]),
+            "unit": f"time steps/s at {sizes[-1]}^2 (slowest equation)", "n_gpus": ws,
+            "higher_is_better": True, "dtype": "f64 (heat, wave) / c128 (schrodinger)",
+            "data": "synthetic: closed-form manufactured solutions",
+            "config": {"workload": "C4: heat star5, wave ellipse, Schrodinger star3; tau = 16/M, T = 1",
+                       "sizes": sizes}, "table": table, "wall_s": time.time() - t_all}
 
 
 def run_c5(args):
@@ -791,7 +969,7 @@ def main(argv=None):
     ap.add_argument("--m", type=int, default=M_DEFAULT)
     ap.add_argument("--equations", default=",".join(EQUATIONS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--workload", choices=["steps", "c5"], default="steps",
+    ap.add_argument("--workload", choices=["steps", "c4", "c5"], default="steps",
                     help="steps: the 4096^2 time-step metric (default); c5: one 16384^2 "
                          "KFBI solve per step, slab-decomposed over the ranks")
     ap.add_argument("--profile", action="store_true",
@@ -805,9 +983,12 @@ def main(argv=None):
                     help="timed regions of K steps each; value = their median")
     ap.add_argument("--no-pipeline-pass", action="store_true",
                     help="skip the pipeline-form measurement")
+    ap.add_argument("--no-configs", action="store_true",
+                    help="skip the C1-C3 run() measurements")
     ap.add_argument("--no-slab", action="store_true",
                     help="skip the C5 slab-decomposed solve measurement")
     ap.add_argument("--slab-m", type=int, default=16384)
+    ap.add_argument("--c4-sizes", default="256,512,1024,2048,4096")
     ap.add_argument("--slab-steps", type=int, default=3)
     ap.add_argument("--pipeline", action="store_true",
                     help="run every Richardson sweep through the full pipeline (no trace operator)")
@@ -819,6 +1000,8 @@ def main(argv=None):
         line = run_reference(args)
     elif args.workload == "c5":
         line = run_c5(args)
+    elif args.workload == "c4":
+        line = run_c4(args)
     else:
         line = run_ours(args)
     if line is not None:

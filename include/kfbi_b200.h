@@ -163,6 +163,18 @@ kfbi_status kfbi_box_solve_bc(kfbi_plan *plan, int32_t dtype, int32_t box_bc,
 
 kfbi_status kfbi_plan_set_geometry(kfbi_plan *plan, const kfbi_geometry *geo);
 
+/* classify (grid.py:122-155): interior[j*(m+1)+i] = level(x[i], y[j]) <= tol
+ * on the device (host in/out arrays).  kind 0 circle (params cx, cy, r),
+ * 1 ellipse (cx, cy, a, b), 2 star (cx, cy, scale, c, lobes).  Circle and
+ * ellipse levels are evaluated exactly as numpy does (no contraction); for
+ * the star the flat indices of nodes with |level - tol| <= 1e-12 are
+ * returned in ambiguous[0 .. min(*n_ambiguous, cap)) for the caller to
+ * re-evaluate with the reference formula. */
+kfbi_status kfbi_classify_nodes(int32_t device, int32_t kind, const double *params,
+                                const double *x, const double *y, int32_t m, double tol,
+                                uint8_t *interior, int32_t *n_ambiguous, int64_t *ambiguous,
+                                int32_t cap);
+
 /* Column stage of the dirichlet-zero box solve (the scipy dst / idst pair
  * along axis 0 of boxsolve.py:70-82 with the spectral division between).
  * Mode 1 solves the equivalent constant-coefficient tridiagonal system of
@@ -311,6 +323,20 @@ kfbi_status kfbi_slab_update(kfbi_plan *plan, int32_t dtype, int32_t bc_kind, co
                              void *trace_un, double gamma, void *stream);
 kfbi_status kfbi_rich_state(kfbi_plan *plan, int32_t *iterations, int32_t *done,
                             double *residual, double *history, void *stream);
+
+/* Opt-in restarted GMRES(restart) on the same boundary integral equation
+ * (PAPER.md:768, SPEC.md:349 name Krylov solvers as the follow-up to the
+ * reference's Richardson iteration): solves T phi = g - t_F for the density,
+ * where trace(phi) = t_F + T phi is the affine sweep map of bvp.py:312-323.
+ * Krylov vectors come from the pipeline with F = 0, f_gamma = 0, or from the
+ * plan's trace operator when use_operator = 1; stopping rule
+ * gamma ||g - trace(phi)||_2 <= tol (implies the reference's max-norm rule).
+ * Same kfbi_bvp fields as kfbi_richardson (gamma only scales the stopping
+ * test); u / traces are the field of the final density; iterations counts
+ * matvecs plus full sweeps.  Results differ from Richardson's at the level
+ * of tol (a different iterate converging to the same fixed point). */
+kfbi_status kfbi_gmres(kfbi_plan *plan, const kfbi_bvp *bvp, int32_t restart,
+                       kfbi_bvp_result *result, void *stream);
 
 /* Largest n_ctl the on-chip operator sweeps support on the plan's device
  * (32 rows of T per SM); kfbi_build_trace_operator[_bc] rejects more with

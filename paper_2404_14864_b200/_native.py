@@ -90,6 +90,8 @@ _SIGNATURES = {
     "kfbi_interface_solve": ([vp, i32, f64, f64, vp, vp, vp, vp], i32),
     "kfbi_extract": ([vp, i32, vp, vp, vp, vp], i32),
     "kfbi_richardson": ([vp, C.POINTER(Bvp), C.POINTER(BvpResult), vp], i32),
+    "kfbi_gmres": ([vp, C.POINTER(Bvp), i32, C.POINTER(BvpResult), vp], i32),
+    "kfbi_classify_nodes": ([i32, i32, vp, vp, vp, i32, C.c_double, vp, C.POINTER(i32), vp, i32], i32),
     "kfbi_build_trace_operator": ([vp, i32, f64, f64, vp], i32),
     "kfbi_build_trace_operator_bc": ([vp, i32, i32, i32, f64, f64, vp], i32),
     "kfbi_box_solve_bc": ([vp, i32, i32, f64, f64, vp, vp, vp], i32),

@@ -313,6 +313,28 @@ class Plan:
         N.check(status, iterations=int(max_iter), last_residual=last)
         return res.iterations, res.residual, history
 
+    def gmres(self, *, kappa, F, F_sign, f_gamma, f_gamma_sign, g, density, gamma, tol, max_iter,
+              u, trace_u, trace_un, restart=40, use_operator=False, bc_kind="dirichlet",
+              box_bc=None):
+        """Opt-in restarted GMRES on the same BIE (kfbi_gmres); density in place."""
+        k = complex(kappa)
+        box_bc = box_bc or ("dirichlet-zero" if bc_kind == "dirichlet" else "neumann-zero")
+        b = N.Bvp(dtype=self._dt(u.is_complex()), kappa_re=k.real, kappa_im=k.imag,
+                  F=F.data_ptr(), F_sign=float(F_sign), f_gamma=f_gamma.data_ptr(),
+                  f_gamma_sign=float(f_gamma_sign), g=g.data_ptr(), density=density.data_ptr(),
+                  gamma=float(gamma), tol=float(tol), max_iter=int(max_iter), sweeps_hint=0,
+                  u=u.data_ptr(), trace_u=trace_u.data_ptr(), trace_un=trace_un.data_ptr(),
+                  use_operator=int(bool(use_operator)), log_slot=-1, bc_kind=_KIND[bc_kind],
+                  box_bc=_BOX[box_bc])
+        hist = np.zeros(max(int(max_iter), 1))
+        res = N.BvpResult(history=hist.ctypes.data_as(C.POINTER(C.c_double)))
+        status = self._lib.kfbi_gmres(self.handle, C.byref(b), int(restart), C.byref(res),
+                                      self.stream)
+        n_hist = max(0, min(int(max_iter), res.iterations))
+        history = [h for h in hist[:n_hist].tolist()]
+        N.check(status, iterations=int(max_iter), last_residual=res.residual)
+        return res.iterations, res.residual, history
+
     # -- asynchronous step log ----------------------------------------------
     def log_reserve(self, count):
         N.check(self._lib.kfbi_log_reserve(self.handle, int(count)))

@@ -215,7 +215,8 @@ class DeviceBvp:
 
 def solve_device(ws, *, kappa, F, f_gamma, g, density, F_sign=1.0, f_gamma_sign=1.0,
                  gamma=0.8, tol=1e-8, max_iter=200, sweeps_hint=0, u_out=None,
-                 use_operator=False, log_slot=-1, bc_kind="dirichlet", box_bc=None):
+                 use_operator=False, log_slot=-1, bc_kind="dirichlet", box_bc=None,
+                 method="richardson", restart=40):
     """Richardson solve on device tensors (the inner loop of every time step).
 
     `density` is updated in place (it carries the warm start); F and f_gamma
@@ -232,6 +233,16 @@ def solve_device(ws, *, kappa, F, f_gamma, g, density, F_sign=1.0, f_gamma_sign=
     u = u_out if u_out is not None else torch.empty_like(F)
     tu = torch.empty(n, dtype=F.dtype, device=F.device)
     tn = torch.empty_like(tu)
+    if method == "gmres":
+        it, res, hist = ws.plan.gmres(
+            kappa=kappa, F=F, F_sign=F_sign, f_gamma=f_gamma, f_gamma_sign=f_gamma_sign, g=g,
+            density=density, gamma=gamma, tol=tol, max_iter=max_iter, u=u, trace_u=tu,
+            trace_un=tn, restart=restart, use_operator=use_operator, bc_kind=bc_kind,
+            box_bc=box_bc)
+        return DeviceBvp(u=u, density=density, trace_u=tu, trace_un=tn, iterations=it,
+                         residual=res, residual_history=hist)
+    if method != "richardson":
+        raise ConfigError(f"unknown BIE solver {method!r}; expected 'richardson' or 'gmres'")
     it, res, hist = ws.plan.richardson(
         kappa=kappa, F=F, F_sign=F_sign, f_gamma=f_gamma, f_gamma_sign=f_gamma_sign, g=g,
         density=density, gamma=gamma, tol=tol, max_iter=max_iter, u=u, trace_u=tu,
@@ -242,22 +253,34 @@ def solve_device(ws, *, kappa, F, f_gamma, g, density, F_sign=1.0, f_gamma_sign=
                      residual=res, residual_history=hist)
 
 
+def gmres_solve(problem, workspace, backend=None, restart=40):
+    """Opt-in restarted GMRES on the same boundary integral equation as
+    richardson_solve: the density solves T phi = g - t_F with
+    T the trace operator; stops when gamma ||g - trace||_2 <= tol.  The field
+    agrees with richardson_solve's to about tol (a different iterate of the
+    same fixed point).  `iterations` counts matvecs plus full sweeps."""
+    return _solve_problem(problem, workspace, method="gmres", restart=restart)
+
+
 def richardson_solve(problem, workspace, backend=None, extractor=None):
     """Damped fixed-point iteration on the density (bvp.py:276-351), with
     every sweep on the device.  numpy in, numpy out."""
-    from .device import to_device
-
-    ws = workspace
-    m_ctl = ws.cps.m
-    if np.shape(problem.bc_values) != (m_ctl,):
-        raise ConfigError(f"boundary data must have shape ({m_ctl},), got "
-                          f"{np.shape(problem.bc_values)}")
     dirichlet = problem.bc_kind == "dirichlet"
     want = TraceExtractor if dirichlet else OneSidedExtractor
     if extractor is not None and not isinstance(extractor, want):
         raise ConfigError(f"the device Richardson solve of a {problem.bc_kind} BVP uses the "
                           f"{want.__name__}")
-    if dirichlet:
+    return _solve_problem(problem, workspace, method="richardson")
+
+
+def _solve_problem(problem, ws, method, restart=40):
+    from .device import to_device
+
+    m_ctl = ws.cps.m
+    if np.shape(problem.bc_values) != (m_ctl,):
+        raise ConfigError(f"boundary data must have shape ({m_ctl},), got "
+                          f"{np.shape(problem.bc_values)}")
+    if problem.bc_kind == "dirichlet":
         ws.trace_tables()
     dtype = np.result_type(np.asarray(problem.F).dtype, np.asarray(problem.kappa).dtype,
                            np.asarray(problem.bc_values).dtype)
@@ -271,7 +294,8 @@ def richardson_solve(problem, workspace, backend=None, extractor=None):
     density = to_device(dens0, dt, ws.backend).clone()
     sol = solve_device(ws, kappa=problem.kappa, F=F, f_gamma=fg, g=g, density=density,
                        gamma=problem.gamma, tol=problem.tol, max_iter=problem.max_iter,
-                       bc_kind=problem.bc_kind, box_bc=problem.box_bc)
+                       bc_kind=problem.bc_kind, box_bc=problem.box_bc, method=method,
+                       restart=restart)
     return BvpSolution(
         u=sol.u.cpu().numpy().reshape(mg + 1, mg + 1),
         density=sol.density.cpu().numpy(),

@@ -18,13 +18,14 @@ kfbi_status kfbi_fail(kfbi_status code, const std::string &msg);
 struct KfbiLaunchTok {
   cudaEvent_t a = nullptr, b = nullptr;
 };
-KfbiLaunchTok kfbi_launch_begin(kfbi_plan *p, cudaStream_t s);
+KfbiLaunchTok kfbi_launch_begin(kfbi_plan *p, int name, cudaStream_t s);
 kfbi_status kfbi_launch_end(kfbi_plan *p, int name, cudaStream_t s, KfbiLaunchTok t, cudaError_t e);
 
-// Launch helper: per-name accounting + optional event bracketing.
+// Launch helper: per-name accounting, optional event bracketing and an NVTX
+// range named after the kernel family (engine.py:23-35 names).
 template <typename F>
 kfbi_status kfbi_launch(kfbi_plan *p, int name, cudaStream_t s, F &&fn) {
-  KfbiLaunchTok t = kfbi_launch_begin(p, s);
+  KfbiLaunchTok t = kfbi_launch_begin(p, name, s);
   cudaError_t e = cudaSuccess;
   if constexpr (std::is_same<decltype(fn()), cudaError_t>::value) e = fn();
   else fn();

@@ -5,6 +5,7 @@
 // per-kernel-name CUDA-event timing (the Backend.timings contract of
 // engine.py:84-95) and error reporting.
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <cmath>
 #include <cstdio>
@@ -16,6 +17,8 @@
 #define KFBI_MAIN_TU
 #include "host_common.h"
 #include "interface_kernels.cuh"
+#include "gmres.cuh"
+#include "classify.cuh"
 #include "stepping_kernels.cuh"
 
 using namespace kfbi;
@@ -34,6 +37,12 @@ const char *kKernelNames[KFBI_N_KERNEL_NAMES] = {
     "transform-rows", "transform-cols",     "diagonal-scale",
     "extract-traces", "density-update",     "rhs-update"};
 
+// NVTX ranges (nsys / ncu --nvtx) carry the reference's kernel names
+const char *kNvtxNames[KFBI_N_KERNEL_NAMES] = {
+    "kfbi:classify-nodes", "kfbi:edge-intersections", "kfbi:jumps-and-corrections",
+    "kfbi:transform-rows", "kfbi:transform-cols",     "kfbi:diagonal-scale",
+    "kfbi:extract-traces", "kfbi:density-update",     "kfbi:rhs-update"};
+
 struct Pending {
   int name;
   cudaEvent_t a, b;
@@ -49,6 +58,9 @@ struct DevBuf {
     p = nullptr;
     n = 0;
     cudaError_t e = cudaMalloc(&p, count * sizeof(T));
+    // defined contents from the start (state structs are copied to the host
+    // whole, padding included; compute-sanitizer initcheck clean)
+    if (e == cudaSuccess) e = cudaMemset(p, 0, count * sizeof(T));
     if (e == cudaSuccess) n = count;
     return e;
   }
@@ -108,6 +120,10 @@ struct kfbi_plan {
   // operator form (trace operator T of one kappa / dtype)
   DevBuf<double2> Top, phi0, phi_prev, trace1, trace_tmp, zvec, evec, out3, ufield;
   DevBuf<double2> phik1;
+  // GMRES (gmres.cuh) scratch
+  DevBuf<double2> gm_V, gm_w, gm_H, gm_sn, gm_g, gm_y, gm_part, gm_tr;
+  DevBuf<double> gm_cs, gm_np;
+  DevBuf<GmresState> gm_st;
   DevBuf<int> skip;
   DevBuf<StepLog> log;
   int log_cap = 0;
@@ -140,8 +156,9 @@ struct kfbi_plan {
 
 kfbi_status kfbi_fail(kfbi_status code, const std::string &msg) { return fail(code, msg); }
 
-KfbiLaunchTok kfbi_launch_begin(kfbi_plan *p, cudaStream_t s) {
+KfbiLaunchTok kfbi_launch_begin(kfbi_plan *p, int name, cudaStream_t s) {
   KfbiLaunchTok t;
+  nvtxRangePushA(kNvtxNames[name]);
   if (p->timing) {
     t.a = p->take_event();
     t.b = p->take_event();
@@ -151,6 +168,7 @@ KfbiLaunchTok kfbi_launch_begin(kfbi_plan *p, cudaStream_t s) {
 }
 
 kfbi_status kfbi_launch_end(kfbi_plan *p, int name, cudaStream_t s, KfbiLaunchTok t, cudaError_t e) {
+  nvtxRangePop();
   cudaError_t e2 = cudaGetLastError();
   if (e == cudaSuccess) e = e2;
   if (p->timing) {
@@ -810,6 +828,121 @@ kfbi_status final_pipeline(kfbi_plan *p, const kfbi_bvp *b, const void *phi_befo
   });
 }
 
+// w = T v: the pipeline with F = 0, f_gamma = 0 applied to the density v
+// (the column map of build_operator_T), or the plan's explicit operator.
+template <typename T>
+kfbi_status gm_matvec(kfbi_plan *p, const kfbi_bvp *b, const T *v, T *w, bool op, cudaStream_t s) {
+  constexpr bool CPLX = std::is_same<T, double2>::value;
+  const int n = p->n_ctl;
+  GmresState *st = p->gm_st.p;
+  const int *done = &st->done;
+  if (op) {
+    T *part = reinterpret_cast<T *>(p->gm_tr.p);
+    KFBI_TRY(launch(p, KFBI_K_DENSITY, s, [&] {
+      gm_gemv_kernel<T><<<dim3((n + GM_T - 1) / GM_T, GM_JS), GM_T, 0, s>>>(
+          n, reinterpret_cast<const T *>(p->Top.p), v, part, st);
+    }));
+    return launch(p, KFBI_K_DENSITY, s, [&] {
+      gm_gemv_sum_kernel<T><<<(n + GM_T - 1) / GM_T, GM_T, 0, s>>>(n, part, w, st);
+    });
+  }
+  const bool dir = b->bc_kind == 0;
+  T *z = reinterpret_cast<T *>(p->zvec.p);
+  KFBI_TRY(jumps_T<T>(p, b->kappa_re, b->kappa_im, dir ? v : nullptr, dir ? nullptr : v, z, 1.0, p->jm.p,
+                      done, s));
+  KFBI_TRY(edges_T<T>(p, p->jm.p, p->jv.p, done, s));
+  KFBI_TRY(box_dispatch(p, CPLX ? KFBI_C128 : KFBI_F64, b->kappa_re, b->kappa_im, nullptr, 1.0, p->jv.p,
+                        p->ufield.p, done, s, b->box_bc));
+  ExtractArgs x = extract_args(p, !dir);
+  T *other = reinterpret_cast<T *>(p->gm_tr.p);
+  return launch(p, KFBI_K_EXTRACT, s, [&] {
+    extract_traces_kernel<T><<<(n + 255) / 256, 256, 0, s>>>(
+        x, reinterpret_cast<const T *>(p->ufield.p), reinterpret_cast<const T *>(p->jm.p),
+        dir ? w : other, dir ? other : w, done);
+  });
+}
+
+// Restarted GMRES(m) on T phi = g - t_F (gmres.cuh); one host sync per cycle.
+template <typename T>
+kfbi_status gmres_T(kfbi_plan *p, const kfbi_bvp *b, int m, kfbi_bvp_result *res, cudaStream_t s) {
+  const int n = p->n_ctl;
+  const size_t nf = (size_t)(p->m + 1) * (p->m + 1);
+  const bool op = b->use_operator != 0;
+  cudaError_t e = cudaSuccess;
+  DevBuf<double2> *vb[] = {&p->gm_w, &p->gm_g, &p->gm_sn, &p->gm_y};
+  for (auto *q : vb)
+    if (e == cudaSuccess) e = q->ensure((size_t)m + 1 > (size_t)n ? (size_t)m + 1 : (size_t)n);
+  if (e == cudaSuccess) e = p->gm_V.ensure((size_t)(m + 1) * n);
+  if (e == cudaSuccess) e = p->gm_H.ensure((size_t)(m + 1) * m);
+  if (e == cudaSuccess) e = p->gm_part.ensure((size_t)(m + 1) * GM_NB);
+  if (e == cudaSuccess) e = p->gm_tr.ensure((size_t)GM_JS * n > (size_t)n ? (size_t)GM_JS * n : (size_t)n);
+  if (e == cudaSuccess) e = p->gm_cs.ensure((size_t)m + 1);
+  if (e == cudaSuccess) e = p->gm_np.ensure(GM_NB);
+  if (e == cudaSuccess) e = p->gm_st.ensure(1);
+  if (e == cudaSuccess) e = p->ufield.ensure(nf);
+  if (e != cudaSuccess) return fail(KFBI_E_CUDA, std::string("gmres scratch: ") + cudaGetErrorString(e));
+  KFBI_TRY(ensure_op_scratch(p));
+  KFBI_CUDA(cudaMemsetAsync(p->zvec.p, 0, n * sizeof(double2), s), "density-update");
+  T *V = reinterpret_cast<T *>(p->gm_V.p), *w = reinterpret_cast<T *>(p->gm_w.p);
+  T *H = reinterpret_cast<T *>(p->gm_H.p), *sn = reinterpret_cast<T *>(p->gm_sn.p);
+  T *gv = reinterpret_cast<T *>(p->gm_g.p), *y = reinterpret_cast<T *>(p->gm_y.p);
+  T *part = reinterpret_cast<T *>(p->gm_part.p), *x = static_cast<T *>(b->density);
+  GmresState *st = p->gm_st.p;
+  double *np = p->gm_np.p, *cs = p->gm_cs.p;
+  const bool dir = b->bc_kind == 0;
+  KFBI_TRY(launch(p, KFBI_K_DENSITY, s, [&] { gm_init_kernel<<<1, 1, 0, s>>>(st, b->max_iter, b->tol, b->gamma); }));
+  GmresState hs{};
+  int cycles = 0;
+  for (;;) {
+    // r0 = g - trace(x): one full sweep (F, f_gamma) from the current density
+    KFBI_TRY(final_pipeline<T>(p, b, x, s));
+    const T *tr = static_cast<const T *>(dir ? b->trace_u : b->trace_un);
+    KFBI_TRY(launch(p, KFBI_K_DENSITY, s, [&] {
+      gm_start_kernel<T><<<GM_NB, GM_T, 0, s>>>(n, static_cast<const T *>(b->g), tr, w, np, st);
+    }));
+    KFBI_TRY(launch(p, KFBI_K_DENSITY, s, [&] { gm_begin_kernel<T><<<1, 32, 0, s>>>(np, gv, st, p->history.p); }));
+    KFBI_TRY(launch(p, KFBI_K_DENSITY, s, [&] { gm_scale_kernel<T><<<GM_NB, GM_T, 0, s>>>(n, w, V, st); }));
+    for (int j = 0; j < m; ++j) {
+      KFBI_TRY(gm_matvec<T>(p, b, V + (size_t)j * n, w, op, s));
+      for (int pass = 0; pass < 2; ++pass) {       // classical Gram-Schmidt, twice
+        KFBI_TRY(launch(p, KFBI_K_DENSITY, s, [&] { gm_dots_kernel<T><<<GM_NB, GM_T, 0, s>>>(n, j, V, w, part, st); }));
+        KFBI_TRY(launch(p, KFBI_K_DENSITY, s, [&] {
+          gm_orth_kernel<T><<<GM_NB, GM_T, 0, s>>>(n, j, m, V, w, part, H, pass, np, st);
+        }));
+      }
+      KFBI_TRY(launch(p, KFBI_K_DENSITY, s, [&] {
+        gm_givens_kernel<T><<<1, 32, 0, s>>>(j, m, np, H, cs, sn, gv, st, p->history.p);
+      }));
+      KFBI_TRY(launch(p, KFBI_K_DENSITY, s, [&] {
+        gm_scale_kernel<T><<<GM_NB, GM_T, 0, s>>>(n, w, V + (size_t)(j + 1) * n, st);
+      }));
+    }
+    KFBI_TRY(launch(p, KFBI_K_DENSITY, s, [&] { gm_backsolve_kernel<T><<<1, 32, 0, s>>>(m, H, gv, y, st); }));
+    KFBI_TRY(launch(p, KFBI_K_DENSITY, s, [&] { gm_update_kernel<T><<<GM_NB, GM_T, 0, s>>>(n, V, y, x, st); }));
+    KFBI_CUDA(cudaMemcpyAsync(&hs, st, sizeof(GmresState), cudaMemcpyDeviceToHost, s), "density-update");
+    KFBI_CUDA(cudaStreamSynchronize(s), "density-update");
+    ++cycles;
+    if (hs.done || hs.iters >= b->max_iter) break;
+    // next cycle: rotation state restarts, the density carries over
+  }
+  // the returned field and traces: one full sweep from the final density
+  KFBI_TRY(final_pipeline<T>(p, b, x, s));
+  res->iterations = hs.iters + cycles + 1;        // matvecs + full sweeps
+  res->converged = hs.done == 1 ? 1 : 0;
+  res->residual = b->gamma * hs.resid;
+  if (res->history) {
+    const int nh = hs.iters < b->max_iter ? hs.iters : b->max_iter;
+    if (nh > 0)
+      KFBI_CUDA(cudaMemcpy(res->history, p->history.p, nh * sizeof(double), cudaMemcpyDeviceToHost),
+                "density-update");
+  }
+  KFBI_CUDA(cudaStreamSynchronize(s), "density-update");
+  if (hs.done != 1)
+    return fail(KFBI_E_NOCONV, "GMRES did not reach tol within max_iter matvecs (last gamma*||r|| " +
+                                   std::to_string(b->gamma * hs.resid) + ")");
+  return KFBI_OK;
+}
+
 }  // namespace
 
 // ===========================================================================
@@ -1242,6 +1375,77 @@ kfbi_status kfbi_extract(kfbi_plan *p, int32_t dtype, const void *u, const void 
                                                   static_cast<const double *>(jm),
                                                   static_cast<double *>(out));
   });
+}
+
+kfbi_status kfbi_classify_nodes(int32_t device, int32_t kind, const double *params, const double *x,
+                                const double *y, int32_t m, double tol, uint8_t *interior,
+                                int32_t *n_ambiguous, int64_t *ambiguous, int32_t cap) {
+  if (!params || !x || !y || !interior || !n_ambiguous || m < 1 || cap < 0)
+    return fail(KFBI_E_CONFIG, "classify: null argument");
+  if (kind < 0 || kind > 2) return fail(KFBI_E_CONFIG, "classify: curve kind 0 circle, 1 ellipse, 2 star");
+  KFBI_CUDA(cudaSetDevice(device), "classify-nodes");
+  CurveDesc c;
+  c.kind = kind;
+  c.cx = params[0];
+  c.cy = params[1];
+  c.p0 = params[2];
+  c.p1 = kind >= 1 ? params[3] : 0.0;
+  c.p2 = kind == 2 ? params[4] : 0.0;
+  const size_t n1 = (size_t)m + 1, total = n1 * n1;
+  double *dx = nullptr, *dy = nullptr;
+  unsigned char *dint = nullptr;
+  int *dn = nullptr;
+  long long *damb = nullptr;
+  cudaError_t e = cudaMalloc(&dx, n1 * sizeof(double));
+  if (e == cudaSuccess) e = cudaMalloc(&dy, n1 * sizeof(double));
+  if (e == cudaSuccess) e = cudaMalloc(&dint, total);
+  if (e == cudaSuccess) e = cudaMalloc(&dn, sizeof(int));
+  if (e == cudaSuccess) e = cudaMalloc(&damb, (size_t)(cap > 0 ? cap : 1) * sizeof(long long));
+  if (e == cudaSuccess) e = cudaMemcpy(dx, x, n1 * sizeof(double), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(dy, y, n1 * sizeof(double), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemset(dn, 0, sizeof(int));
+  if (e == cudaSuccess) {
+    const double band = kind == 2 ? 1e-12 : 0.0;    // polynomials are exact
+    classify_kernel<<<148 * 8, 256>>>(c, dx, dy, m, tol, band, dint, dn, damb, cap);
+    e = cudaGetLastError();
+  }
+  int nh = 0;
+  if (e == cudaSuccess) e = cudaMemcpy(interior, dint, total, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess) e = cudaMemcpy(&nh, dn, sizeof(int), cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess && nh > 0 && cap > 0)
+    e = cudaMemcpy(ambiguous, damb, (size_t)(nh < cap ? nh : cap) * sizeof(long long), cudaMemcpyDeviceToHost);
+  cudaFree(dx);
+  cudaFree(dy);
+  cudaFree(dint);
+  cudaFree(dn);
+  cudaFree(damb);
+  if (e != cudaSuccess) return fail(KFBI_E_CUDA, std::string("kernel 'classify-nodes': ") + cudaGetErrorString(e));
+  *n_ambiguous = nh;
+  return KFBI_OK;
+}
+
+kfbi_status kfbi_gmres(kfbi_plan *p, const kfbi_bvp *b, int32_t restart, kfbi_bvp_result *res,
+                       void *stream) {
+  KFBI_TRY(check_geo(p));
+  if (!b || !res) return fail(KFBI_E_CONFIG, "null argument");
+  if (b->max_iter < 1) return fail(KFBI_E_CONFIG, "max iterations must be >= 1");
+  if (!(b->gamma > 0.0 && b->gamma < 1.0)) return fail(KFBI_E_CONFIG, "gamma must lie in (0,1)");
+  if (!(b->tol > 0.0)) return fail(KFBI_E_CONFIG, "tolerance must be positive");
+  if (restart < 1 || restart > 64) return fail(KFBI_E_CONFIG, "GMRES restart must lie in 1..64");
+  const bool cplx = b->dtype == KFBI_C128;
+  if (!cplx && b->kappa_im != 0.0) return fail(KFBI_E_CONFIG, "complex kappa requires the c128 path");
+  if (b->bc_kind != 0 && b->bc_kind != 1) return fail(KFBI_E_CONFIG, "unknown boundary condition kind");
+  if (b->bc_kind == 1 && !p->has_os)
+    return fail(KFBI_E_CONFIG, "Neumann BVP: one-sided extraction tables missing (kfbi_plan_set_onesided)");
+  if (b->use_operator &&
+      (!p->op_valid || p->op_dtype != b->dtype || p->op_kre != b->kappa_re || p->op_kim != b->kappa_im ||
+       p->op_bc != b->bc_kind * 2 + b->box_bc))
+    return fail(KFBI_E_CONFIG, "trace operator not built for this kappa / dtype (kfbi_build_trace_operator)");
+  cudaError_t e = p->history.ensure(b->max_iter);
+  if (e != cudaSuccess) return fail(KFBI_E_CUDA, "history allocation failed");
+  cudaStream_t s = (cudaStream_t)stream;
+  if (cplx) return gmres_T<double2>(p, b, restart, res, s);
+  return gmres_T<double>(p, b, restart, res, s);
 }
 
 kfbi_status kfbi_richardson(kfbi_plan *p, const kfbi_bvp *b, kfbi_bvp_result *res, void *stream) {
