@@ -441,11 +441,12 @@ def run_ours(args):
     slab = None
     if not args.no_slab:
         slab = {}
-        for p2p in (False, True):
+        for mode in ("carry", "a2a", "p2p"):
+            name = {"a2a": "nccl", "p2p": "p2p", "carry": "carry"}[mode]
             try:
-                slab["p2p" if p2p else "nccl"] = slab_c5(args, ws, rank, local, p2p)
+                slab[name] = slab_c5(args, ws, rank, local, mode)
             except Exception as e:          # reported, never fatal for the headline
-                slab["p2p" if p2p else "nccl"] = {"error": f"{type(e).__name__}: {e}"}
+                slab[name] = {"error": f"{type(e).__name__}: {e}"}
             torch.cuda.empty_cache()
 
     if rank != 0:
@@ -601,7 +602,7 @@ def run_configs(args, local, with_cpu):
     return out
 
 
-def c5_problem(m, rank, ws, local, p2p, torch):
+def c5_problem(m, rank, ws, local, mode, torch):
     """StaticPlaneWave on star(1.5, 0.2, 3) over [-pi, pi]^2,
     kappa = 2 / tau with tau = 0.25 * 64 / m (kappa = 2048 at m = 16384)."""
     import paper_2404_14864_b200 as k
@@ -613,7 +614,7 @@ def c5_problem(m, rank, ws, local, p2p, torch):
     wsp = k.InterfaceWorkspace(geo, backend=k.CudaBackend(local, timing=False))
     sol = k.StaticPlaneWave(kappa=kappa)
     cps = wsp.cps
-    solver = D.SlabRichardson(wsp, nranks=ws, rank=rank, p2p=p2p)
+    solver = D.SlabRichardson(wsp, nranks=ws, rank=rank, mode=mode)
     r0, r1 = solver.rows
     X, Y = geo.grid.X[r0:r1], geo.grid.Y[r0:r1]
     F = torch.from_numpy(np.where(geo.classification.interior[r0:r1], sol.f(X, Y), 0.0)).cuda()
@@ -623,13 +624,13 @@ def c5_problem(m, rank, ws, local, p2p, torch):
     return geo, wsp, sol, solver, F, fg, g, kappa
 
 
-def slab_c5(args, ws, rank, local, p2p):
+def slab_c5(args, ws, rank, local, mode):
     """C5 solves/s over the N ranks (strong scaling) inside the headline run."""
     import torch
 
     m = args.slab_m
     t0 = time.time()
-    geo, wsp, sol, solver, F, fg, g, kappa = c5_problem(m, rank, ws, local, p2p, torch)
+    geo, wsp, sol, solver, F, fg, g, kappa = c5_problem(m, rank, ws, local, mode, torch)
     torch.cuda.synchronize()
     setup_s = time.time() - t0
 
@@ -660,10 +661,14 @@ def slab_c5(args, ws, rank, local, p2p):
             "scaling": "strong", "n_ranks": ws, "iterations": it, "max_err_interior": err,
             "setup_s": setup_s, "n_ctl": int(wsp.cps.m), "kappa": kappa,
             "geometry": "star(1.5, 0.2, 3) on [-pi, pi]^2 (SURVEY §8(d) C5)",
-            "transport": ("none (1 rank)" if ws == 1 else
-                          "transposes fused into the passes (CUDA IPC peer stores + peer-flag "
-                          "barrier) + NCCL all_reduce" if p2p else
-                          "NCCL all_to_all_single + all_reduce")}
+            "mode": mode,
+            "transport": {"a2a": "NCCL all_to_all_single x2 + all_reduce per sweep",
+                          "p2p": "transposes fused into the passes (CUDA IPC peer stores + "
+                                 "peer-flag barrier) + NCCL all_reduce",
+                          "carry": "no transposes: tridiagonal column stage pushes 3 values per "
+                                   "column to every rank over CUDA IPC peer memory inside the "
+                                   "kernel + NCCL all_reduce"}[mode]
+                         + (" (1 rank: no traffic)" if ws == 1 else "")}
 
 
 def c4_cases():
@@ -758,7 +763,7 @@ def run_c5(args):
     torch.cuda.set_device(local)
     m = args.m if args.m != M_DEFAULT else 16384
     t0 = time.time()
-    geo, wsp, sol, solver, F, fg, g, kappa = c5_problem(m, rank, ws, local, args.p2p, torch)
+    geo, wsp, sol, solver, F, fg, g, kappa = c5_problem(m, rank, ws, local, args.slab_mode or ("p2p" if args.p2p else "a2a"), torch)
     cps = wsp.cps
     r0, r1 = solver.rows
     X, Y = geo.grid.X[r0:r1], geo.grid.Y[r0:r1]
@@ -990,6 +995,8 @@ def main(argv=None):
     ap.add_argument("--slab-m", type=int, default=16384)
     ap.add_argument("--c4-sizes", default="256,512,1024,2048,4096")
     ap.add_argument("--slab-steps", type=int, default=3)
+    ap.add_argument("--slab-mode", choices=["a2a", "p2p", "carry"], default=None,
+                    help="c5: slab exchange (default a2a, or p2p with --p2p)")
     ap.add_argument("--pipeline", action="store_true",
                     help="run every Richardson sweep through the full pipeline (no trace operator)")
     args = ap.parse_args(argv)

@@ -258,6 +258,35 @@ typedef struct {
 
 kfbi_status kfbi_slab_panel_bytes(kfbi_plan *plan, int32_t dtype, int32_t nranks,
                                   int64_t *bytes);
+
+/* Transpose-free column stage of the slab-decomposed dirichlet box solve
+ * (tridiagonal recurrences, box_tri.cuh cols_tri_dist).  Rank g keeps its
+ * rows of every spectral column in the row pass's own buffer ([panel][R][w],
+ * kfbi_slab_rows_fwd with no exchange), solves them with zero carries at the
+ * slab ends, and exchanges three values per column with every rank over peer
+ * memory INSIDE the kernel (pushes into agg[h] / flags[h] of every rank h,
+ * waits on its own flags for `epoch`); then kfbi_slab_rows_inv reads the same
+ * buffer.  Replaces both all-to-alls: 3 P values per column cross NVLink
+ * instead of 2 M^2 s / P bytes per rank.  Equal to the one-GPU solve to
+ * rounding (the carries are combined in a different order).
+ * virt = 1: all ranks in ONE launch on one device (panels[h] = every rank's
+ * buffer), for tests.  Buffer sizes from kfbi_slab_tri_bytes. */
+typedef struct {
+  int32_t nranks, rank, virt;
+  int32_t pad;
+  uint64_t epoch;              /* > every earlier epoch on these flags          */
+  int64_t max_spins;           /* bounded wait; a missing peer sets *timed_out */
+  int32_t *timed_out;          /* device int, may be NULL                      */
+  void *panels[8];             /* virt: every rank's panel buffer              */
+  void *agg[8];                /* every rank's aggregate buffer, as mapped here */
+  void *flags[8];              /* every rank's flag buffer (zeroed once)       */
+} kfbi_tri_dist;
+
+kfbi_status kfbi_slab_tri_bytes(kfbi_plan *plan, int32_t dtype, int32_t nranks,
+                                int64_t *agg_bytes, int64_t *flag_bytes);
+kfbi_status kfbi_slab_cols_tri(kfbi_plan *plan, int32_t dtype, int32_t nranks, int32_t rank,
+                               double kappa_re, double kappa_im, void *panels,
+                               const kfbi_tri_dist *dist, void *stream);
 kfbi_status kfbi_slab_rows_fwd(kfbi_plan *plan, int32_t dtype, const kfbi_slab *slab,
                                const void *rhs, double sign, const void *jv,
                                void *panels, void *stream);

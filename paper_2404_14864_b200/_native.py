@@ -46,6 +46,12 @@ class Slab(C.Structure):
     _fields_ = [("nranks", i32), ("rank", i32)]
 
 
+class TriDist(C.Structure):
+    _fields_ = [("nranks", i32), ("rank", i32), ("virt", i32), ("pad", i32),
+                ("epoch", C.c_uint64), ("max_spins", C.c_int64), ("timed_out", vp),
+                ("panels", vp * 8), ("agg", vp * 8), ("flags", vp * 8)]
+
+
 class Geometry(C.Structure):
     _fields_ = [
         ("n_ctl", i32), ("n_edges", i32), ("n_rec", i32), ("n_groups", i32),
@@ -91,6 +97,8 @@ _SIGNATURES = {
     "kfbi_extract": ([vp, i32, vp, vp, vp, vp], i32),
     "kfbi_richardson": ([vp, C.POINTER(Bvp), C.POINTER(BvpResult), vp], i32),
     "kfbi_gmres": ([vp, C.POINTER(Bvp), i32, C.POINTER(BvpResult), vp], i32),
+    "kfbi_slab_tri_bytes": ([vp, i32, i32, C.POINTER(C.c_int64), C.POINTER(C.c_int64)], i32),
+    "kfbi_slab_cols_tri": ([vp, i32, i32, i32, C.c_double, C.c_double, vp, C.POINTER(TriDist), vp], i32),
     "kfbi_classify_nodes": ([i32, i32, vp, vp, vp, i32, C.c_double, vp, C.POINTER(i32), vp, i32], i32),
     "kfbi_build_trace_operator": ([vp, i32, f64, f64, vp], i32),
     "kfbi_build_trace_operator_bc": ([vp, i32, i32, i32, f64, f64, vp], i32),

@@ -214,6 +214,30 @@ class Plan:
         N.check(self._lib.kfbi_slab_cols_p2p(self.handle, self._dt(cplx), C.byref(sl), k.real,
                                              k.imag, _addr(panels), tab, self.stream))
 
+    def slab_tri_bytes(self, cplx, nranks):
+        a, f = C.c_int64(0), C.c_int64(0)
+        N.check(self._lib.kfbi_slab_tri_bytes(self.handle, self._dt(cplx), int(nranks), C.byref(a),
+                                              C.byref(f)))
+        return a.value, f.value
+
+    def slab_cols_tri(self, cplx, nranks, rank, kappa, panels, agg, flags, epoch, timed_out=None,
+                      max_spins=1 << 26, virt_panels=None):
+        """Transpose-free column stage (kfbi_slab_cols_tri): agg / flags are
+        every rank's buffers as mapped here; virt_panels: all ranks in one
+        launch on this device."""
+        k = complex(kappa)
+        d = N.TriDist(nranks=int(nranks), rank=int(rank), virt=int(virt_panels is not None),
+                      epoch=int(epoch), max_spins=int(max_spins),
+                      timed_out=N.ptr(timed_out) if timed_out is not None else None)
+        for h in range(int(nranks)):
+            d.agg[h] = _addr(agg[h])
+            d.flags[h] = _addr(flags[h])
+            if virt_panels is not None:
+                d.panels[h] = _addr(virt_panels[h])
+        N.check(self._lib.kfbi_slab_cols_tri(self.handle, self._dt(cplx), int(nranks), int(rank),
+                                             k.real, k.imag, _addr(panels) if panels is not None else None,
+                                             C.byref(d), self.stream))
+
     def p2p_barrier(self, flags, nranks, rank, epoch, timed_out=None, max_spins=0):
         tab = _ptr_table(flags)
         N.check(self._lib.kfbi_p2p_barrier(tab, int(nranks), int(rank), int(epoch),

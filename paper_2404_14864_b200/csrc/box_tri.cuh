@@ -143,9 +143,27 @@ struct TriSmem {
 // starts zL_0 + V w_0.  Both local sweeps run back to back; the epilogue
 //   out_i = A z_i + B (r^j - r^{2M-j}) = A zL_i + alpha r^i + gamma r^{CH-1-i}
 // is two multiply chains.
-template <bool CPLX, int LOGM>
+// Row slabs across ranks (cols_tri_dist): the rank's R = 2^LOGM rows are
+// solved with zero carries at the slab ends, the three slab aggregates of
+// every column (v at the last row, z at the first row, z at global row 1)
+// are pushed to every rank over peer memory, and each rank folds the other
+// slabs' carries into its epilogue.  nullptr: one slab holds all rows.
+struct TriDist {
+  int P, g;                                   // ranks, this rank
+  int units;                                  // column units (strips or half strips)
+  int virt;                                   // 1: all ranks in one launch (blockIdx.y = rank)
+  unsigned long long epoch;
+  long long max_spins;
+  int *timed_out;
+  void *vpanels[8];                           // virt: every rank's panel buffer
+  double2 *agg[8];                            // [unit][P][NH][3] of rank h, as mapped here
+  unsigned long long *flg[8];                 // [unit][P] of rank h, as mapped here
+};
+
+template <bool CPLX, int LOGM, bool DIST = false>
 KFBI_DEV void tri_solve(double2 (&x)[tri::Cfg<LOGM>::CH], const BoxArgs &a, int pp, int half, int hs,
-                        int chunk, TriSmem<tri::Cfg<LOGM>::NH, tri::Cfg<LOGM>::NW> &sh) {
+                        int chunk, TriSmem<tri::Cfg<LOGM>::NH, tri::Cfg<LOGM>::NW> &sh,
+                        const TriDist *dd = nullptr, int unit = 0, int g = 0) {
   using C = tri::Cfg<LOGM>;
   constexpr int CH = C::CH, NH = C::NH, CPW = C::CPW, NW = C::NW, NCH = C::NCH;
   static_assert(2 * NCH < (1 << TRI_NPOW), "power table");
@@ -258,17 +276,93 @@ KFBI_DEV void tri_solve(double2 (&x)[tri::Cfg<LOGM>::CH], const BoxArgs &a, int 
     if (cw == CPW - 1) Z = acc;
   }
 
-  // ---- boundary term: true z_1 of this slot --------------------------------
-  // z_1 = zL_1 + V_0 w_1 + Z_0 r^{CH-1} with V_0 = 0 (chunk 0), or z_1 = zL_0
-  // + Z r (CH = 1: row 1 is chunk 1's only row)
+  // ---- slab carries (DIST) and the boundary term ---------------------------
+  // z_i = zL_i + Vc w_i + Zc r^{CH-i} + Vg W_i + Zg r^{R-iota}, iota = chunk CH + i
+  // (w, W: the chunk / slab sums r^{2m-i+1}); single slab: Vg = Zg = 0.
   const double2 rch = rc2(0);                    // r^CH
+  const int P = DIST ? dd->P : 1;
+  const int NT = P * NCH;                        // chunks of the whole column (M / CH)
+  double2 Vg = zero, Zg = zero, z1;
+  double2 inv1mr2;                               // 1 / ((1 - r)(1 + r))
+  {
+    const double2 d = tri::mul<CPLX>(make_double2(1.0 - r.x, -r.y),
+                                     CPLX ? make_double2(1.0 + r.x, r.y) : make_double2(1.0 + r.y, 0.0));
+    if constexpr (CPLX) inv1mr2 = cdiv(make_double2(1.0, 0.0), d);
+    else inv1mr2 = make_double2(1.0 / ((1.0 - r.x) * (1.0 + r.x)), 1.0 / ((1.0 - r.y) * (1.0 + r.y)));
+  }
+  // rank-local z at row 1 of this slab's chunk 0 (global row 1 on rank 0)
   if (CH > 1 && chunk == 0) sh.z1s[hs] = tri::mad<CPLX>(Z, tri::pw<CPLX>(r, CH - 1), x[CH > 1 ? 1 : 0]);
   if (CH == 1 && chunk == 1) sh.z1s[hs] = tri::mad<CPLX>(V, sh.w0s[hs], tri::mad<CPLX>(Z, r, x[0]));
-  __syncthreads();
-  const double2 z1 = sh.z1s[hs];
-  const double sc = a.h2 / (2.0 * C::M);
+  if constexpr (DIST) {
+    // slab aggregates: v at the last row (inclusive forward carry of the last
+    // chunk), z at the first row (backward carry of chunk 0), z at row 1
+    __shared__ double2 aggs[2][2];
+    if (chunk == NCH - 1) aggs[hs][0] = I;
+    if (chunk == 0) aggs[hs][1] = J;
+    __syncthreads();
+    if (threadIdx.x < NH) {                      // one thread per half: push to every rank
+      const int h2 = threadIdx.x;
+      const double2 v3[3] = {aggs[h2][0], aggs[h2][1], sh.z1s[h2]};
+      for (int q = 0; q < P; ++q) {
+        double2 *dst = dd->agg[q] + (((size_t)unit * P + g) * NH + h2) * 3;
+        for (int k3 = 0; k3 < 3; ++k3) dst[k3] = v3[k3];
+      }
+      __threadfence_system();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence_system();
+      for (int q = 0; q < P; ++q) {
+        unsigned long long *f = dd->flg[q] + (size_t)unit * P + g;
+        asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(f), "l"(dd->epoch) : "memory");
+      }
+      const unsigned long long *mine = dd->flg[g] + (size_t)unit * P;
+      for (int q = 0; q < P; ++q) {
+        for (long long it = 0;; ++it) {
+          unsigned long long v;
+          asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(mine + q) : "memory");
+          if (v >= dd->epoch) break;
+          if (it >= dd->max_spins) {
+            if (dd->timed_out) atomicExch(dd->timed_out, 1);
+            break;
+          }
+          __nanosleep(32);
+        }
+      }
+      __threadfence();
+    }
+    __syncthreads();
+    // carries across slabs from the P aggregates of this column (own buffer)
+    const double2 *ag = dd->agg[g] + (size_t)unit * P * NH * 3;
+    const double2 rR = rc_pow(NCH);              // r^R
+    // W_0 = (r - r^{2R+1}) / (1 - r^2)
+    const double2 W0 = tri::mul<CPLX>(tri::mad<CPLX>(cneg(rc_pow(2 * NCH)), r, r), inv1mr2);
+    double2 Vq = zero;                           // forward carry into slab q
+    double2 sq[8];
+    for (int q = 0; q < P; ++q) {
+      const double2 eq = __ldcg(&ag[((size_t)q * NH + hs) * 3 + 0]);
+      const double2 sLq = __ldcg(&ag[((size_t)q * NH + hs) * 3 + 1]);
+      if (q == g) Vg = Vq;
+      sq[q] = tri::mad<CPLX>(Vq, W0, sLq);      // z at slab q's first row without Z_q
+      Vq = tri::mad<CPLX>(rR, Vq, eq);
+    }
+    double2 Zq = zero;                           // backward carry into slab q from below
+    double2 Z0 = zero;
+    for (int q = P - 1; q >= 0; --q) {
+      if (q == g) Zg = Zq;
+      if (q == 0) Z0 = Zq;
+      Zq = tri::mad<CPLX>(rR, Zq, sq[q]);
+    }
+    // z_1 = zl1(slab 0) + Z_0 r^{R-1}
+    z1 = tri::mad<CPLX>(Z0, tri::mul<CPLX>(rc_pow(NCH - 1), tri::pw<CPLX>(r, CH - 1)),
+                        __ldcg(&ag[(size_t)hs * 3 + 2]));
+  } else {
+    __syncthreads();
+    z1 = sh.z1s[hs];
+  }
+  const double sc = a.h2 / (2.0 * a.m);
   const double2 A = tri::mul<CPLX>(r, CPLX ? make_double2(sc, 0.0) : make_double2(sc, sc));
-  const double2 r2m = rc_pow(2 * NCH);           // r^{2M}
+  const double2 r2m = rc_pow(2 * NT);            // r^{2M}
   double2 B;                                     // -A r z1 / (1 - r^2M)
   {
     const double2 num = tri::mul<CPLX>(tri::mul<CPLX>(A, r), z1);
@@ -279,21 +373,21 @@ KFBI_DEV void tri_solve(double2 (&x)[tri::Cfg<LOGM>::CH], const BoxArgs &a, int 
       if (kx0 == 0) B.x = 0.0;
     }
   }
-  // alpha = A V r / (1 - r^2) + B r^{j0}
-  // gamma = -A V r^{CH+2} / (1 - r^2) + A Z r - B r^{2M - j0 - CH + 1}
-  double2 inv1mr2;                               // 1 / ((1 - r)(1 + r))
-  {
-    const double2 d = tri::mul<CPLX>(make_double2(1.0 - r.x, -r.y),
-                                     CPLX ? make_double2(1.0 + r.x, r.y) : make_double2(1.0 + r.y, 0.0));
-    if constexpr (CPLX) inv1mr2 = cdiv(make_double2(1.0, 0.0), d);
-    else inv1mr2 = make_double2(1.0 / ((1.0 - r.x) * (1.0 + r.x)), 1.0 / ((1.0 - r.y) * (1.0 + r.y)));
-  }
-  const double2 AVq = tri::mul<CPLX>(tri::mul<CPLX>(A, V), inv1mr2);          // A V / (1 - r^2)
-  const double2 alpha = tri::mad<CPLX>(AVq, r, tri::mul<CPLX>(B, rc_pow(chunk)));
-  const double2 rch1 = tri::mul<CPLX>(rch, r);   // r^{CH+1}
-  double2 gamma = tri::mul<CPLX>(tri::mul<CPLX>(AVq, rch1), r);                 // A V r^{CH+2} / (1 - r^2)
-  gamma = tri::mad<CPLX>(tri::mul<CPLX>(A, Z), r, cneg(gamma));
-  gamma = tri::mad<CPLX>(cneg(B), tri::mul<CPLX>(rc_pow(2 * NCH - chunk - 1), r), gamma);
+  // alpha = A (Vc r + Vg r^{iota0+1}) / (1 - r^2) + B r^{j0}
+  // gamma = A [-(Vc r^{CH+2} + Vg r^{2R-iota0-CH+2}) / (1 - r^2) + Zc r + Zg r^{R-iota0-CH+1}]
+  //         - B r^{2M-j0-CH+1},   iota0 = chunk CH, j0 = g R + iota0
+  const int gch = g * NCH + chunk;               // global chunk index
+  const double2 Aq = tri::mul<CPLX>(A, inv1mr2);
+  double2 Vsum = tri::mad<CPLX>(Vg, tri::mul<CPLX>(rc_pow(chunk), r), tri::mul<CPLX>(V, r));
+  const double2 alpha = tri::mad<CPLX>(Aq, Vsum, tri::mul<CPLX>(B, rc_pow(gch)));
+  const double2 r2 = tri::mul<CPLX>(r, r);
+  double2 Vg2 = tri::mad<CPLX>(Vg, tri::mul<CPLX>(rc_pow(2 * NCH - chunk - 1), r2),
+                               tri::mul<CPLX>(V, tri::mul<CPLX>(tri::mul<CPLX>(rch, r), r)));
+  double2 gamma = tri::mul<CPLX>(Aq, Vg2);
+  gamma = tri::mad<CPLX>(tri::mul<CPLX>(A, tri::mad<CPLX>(Zg, tri::mul<CPLX>(rc_pow(NCH - chunk - 1), r),
+                                                          tri::mul<CPLX>(Z, r))),
+                         tri::one<CPLX>(), cneg(gamma));
+  gamma = tri::mad<CPLX>(cneg(B), tri::mul<CPLX>(rc_pow(2 * NT - gch - 1), r), gamma);
   {
     double2 c = alpha;                           // alpha r^i
 #pragma unroll
@@ -345,6 +439,41 @@ __global__ void __launch_bounds__(tri::Cfg<LOGM>::THREADS, tri::Cfg<LOGM>::MINB)
   tri_solve<CPLX, LOGM>(x, a, pp, half, hs, chunk, sh);
 #pragma unroll
   for (int i = 0; i < CH; ++i) dst[2 * i] = (j0 + i >= 1) ? x[i] : make_double2(0.0, 0.0);
+}
+
+// ---------------------------------------------------------------------------
+// Column stage of the slab-decomposed box solve WITHOUT transposes: rank g
+// keeps its R = 2^LOGR rows of every spectral column (the row pass's own
+// panel layout [pp][R][w]), solves them with zero carries at the slab ends
+// and exchanges three values per column with the other ranks over peer
+// memory inside the kernel (TriDist).  Persistent CTAs walk the column units
+// in the same order on every rank, so the partner CTAs of a unit are always
+// resident (cooperative launch) and the per-unit flag waits cannot deadlock.
+// Traffic between GPUs: 3 P values per column instead of two all-to-alls of
+// M^2 s / P bytes per rank.
+template <bool CPLX, int LOGR>
+__global__ void __launch_bounds__(tri::Cfg<LOGR>::THREADS, 1) cols_tri_dist(BoxArgs a, TriDist d) {
+  using C = tri::Cfg<LOGR>;
+  constexpr int CH = C::CH, NH = C::NH, R = C::M;
+  __shared__ TriSmem<NH, C::NW> sh;
+  if (a.done && *a.done) return;
+  const int t = threadIdx.x;
+  const int g = d.virt ? (int)blockIdx.y : d.g;
+  const int chunk = NH == 2 ? (t >> 1) : t;
+  const int j0 = chunk * CH;
+  double2 *panels = static_cast<double2 *>(d.virt ? d.vpanels[g] : a.panels);
+  for (int unit = blockIdx.x; unit < d.units; unit += gridDim.x) {
+    const int half = NH == 2 ? (t & 1) : (unit & 1);
+    const int pl = NH == 2 ? unit : (unit >> 1);
+    double2 *col = panels + (((size_t)pl * R + j0) * 2 + half);
+    double2 x[CH];
+#pragma unroll
+    for (int i = 0; i < CH; ++i) x[i] = (g == 0 && j0 + i == 0) ? make_double2(0.0, 0.0) : col[2 * i];
+    tri_solve<CPLX, LOGR, true>(x, a, pl, half, NH == 2 ? half : 0, chunk, sh, &d, unit, g);
+#pragma unroll
+    for (int i = 0; i < CH; ++i) col[2 * i] = (g == 0 && j0 + i == 0) ? make_double2(0.0, 0.0) : x[i];
+    __syncthreads();                             // shared scan state reused by the next unit
+  }
 }
 
 // ---------------------------------------------------------------------------

@@ -54,6 +54,10 @@ kfbi_status box_dirichlet_f64(kfbi_plan *p, int logm, bool tri, const kfbi::BoxA
 kfbi_status box_dirichlet_c128(kfbi_plan *p, int logm, bool tri, const kfbi::BoxArgs &a,
                                const void *rhs, double sign, const kfbi::CorrArgs<double2> &c,
                                void *u, cudaStream_t s, int passes);
+// Transpose-free slab column stage (box_tri.cuh cols_tri_dist); logr = log2
+// of the slab rows, units = column units of the dtype.
+kfbi_status box_cols_dist(kfbi_plan *p, bool cplx, int logr, const kfbi::BoxArgs &a,
+                          const kfbi_tri_dist *d, cudaStream_t s);
 kfbi_status box_neumann_f64(kfbi_plan *p, int logm, const kfbi::BoxArgs &a, const void *rhs,
                             double sign, const kfbi::CorrArgs<double> &c, void *u, cudaStream_t s);
 kfbi_status box_neumann_c128(kfbi_plan *p, int logm, const kfbi::BoxArgs &a, const void *rhs,

@@ -1004,6 +1004,39 @@ kfbi_status kfbi_slab_panel_bytes(kfbi_plan *p, int32_t dtype, int32_t nranks, i
   return KFBI_OK;
 }
 
+kfbi_status kfbi_slab_tri_bytes(kfbi_plan *p, int32_t dtype, int32_t nranks, int64_t *agg_bytes,
+                                int64_t *flag_bytes) {
+  KFBI_TRY(check_plan(p));
+  if (!agg_bytes || !flag_bytes || nranks < 1 || nranks > KFBI_MAX_PEERS)
+    return fail(KFBI_E_CONFIG, "slab: bad argument");
+  // units x P x NH x 3 double2 (NH x units = 2 x panels either way), units x P flags
+  const int64_t npl = dtype == KFBI_C128 ? p->m / 2 : p->m / 4;
+  *agg_bytes = 2 * npl * nranks * 3 * 16;
+  *flag_bytes = 2 * npl * nranks * 8;
+  return KFBI_OK;
+}
+
+kfbi_status kfbi_slab_cols_tri(kfbi_plan *p, int32_t dtype, int32_t nranks, int32_t rank, double kre,
+                               double kim, void *panels, const kfbi_tri_dist *d, void *stream) {
+  KFBI_TRY(check_plan(p));
+  if (!d || (!panels && !d->virt)) return fail(KFBI_E_CONFIG, "slab: null argument");
+  const bool cplx = dtype == KFBI_C128;
+  if (!cplx && kim != 0.0) return fail(KFBI_E_CONFIG, "complex kappa requires the c128 path");
+  if (nranks != d->nranks || rank != d->rank || nranks < 1 || nranks > KFBI_MAX_PEERS ||
+      (nranks & (nranks - 1)) != 0 || rank < 0 || rank >= nranks || p->m / nranks < 16)
+    return fail(KFBI_E_CONFIG, "slab column stage: nranks a power of two <= 8, M / nranks >= 16");
+  for (int h = 0; h < nranks; ++h)
+    if (!d->agg[h] || !d->flags[h] || (d->virt && !d->panels[h]))
+      return fail(KFBI_E_CONFIG, "slab column stage: null peer buffer");
+  if (d->epoch < 1) return fail(KFBI_E_CONFIG, "slab column stage: epoch must be >= 1");
+  BoxArgs a = box_args(p, kre, kim, nullptr);
+  a.rows = p->m / nranks;
+  a.row0 = rank * a.rows;
+  a.panels = panels;
+  const int logr = ilog2(a.rows);
+  return box_cols_dist(p, cplx, logr, a, d, (cudaStream_t)stream);
+}
+
 kfbi_status kfbi_slab_rows_fwd(kfbi_plan *p, int32_t dtype, const kfbi_slab *sl, const void *rhs,
                                double sign, const void *jv, void *panels, void *stream) {
   return slab_pass(p, dtype, sl, 1, 0.0, 0.0, rhs, sign, jv, panels, nullptr, stream);
@@ -1040,6 +1073,7 @@ kfbi_status kfbi_slab_cols_p2p(kfbi_plan *p, int32_t dtype, const kfbi_slab *sl,
 kfbi_status kfbi_ipc_alloc(int64_t bytes, void **ptr, void *handle) {
   if (!ptr || !handle || bytes <= 0) return fail(KFBI_E_CONFIG, "ipc: bad argument");
   KFBI_CUDA(cudaMalloc(ptr, (size_t)bytes), "ipc-alloc");
+  KFBI_CUDA(cudaMemset(*ptr, 0, (size_t)bytes), "ipc-alloc");   // flags start at epoch 0
   KFBI_CUDA(cudaMemset(*ptr, 0, (size_t)bytes), "ipc-alloc");
   cudaIpcMemHandle_t h;
   KFBI_CUDA(cudaIpcGetMemHandle(&h, *ptr), "ipc-alloc");

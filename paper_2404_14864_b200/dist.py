@@ -121,10 +121,16 @@ class SlabPasses:
     kernel between the passes.  Buffers are allocated on first use per dtype
     (the p2p ones collectively: every rank must make its first call)."""
 
-    def __init__(self, plan, nranks, rank, group=None, device=None, p2p=False):
+    def __init__(self, plan, nranks, rank, group=None, device=None, p2p=False, mode=None):
         self.plan, self.nranks, self.rank, self.group = plan, nranks, rank, group
         self.device = device
-        self.p2p = bool(p2p)
+        # "a2a": NCCL all-to-all transposes; "p2p": transposes fused into the
+        # pass stores; "carry": no transposes at all, the tridiagonal column
+        # stage exchanges three values per column over peer memory
+        self.mode = mode or ("p2p" if p2p else "a2a")
+        if self.mode not in ("a2a", "p2p", "carry"):
+            raise ConfigError(f"unknown slab mode {self.mode!r}")
+        self.p2p = self.mode == "p2p"
         self._bufs = {}
         self._epoch = 0
         self._timed_out = None
@@ -136,7 +142,14 @@ class SlabPasses:
         if key not in self._bufs:
             nbytes = self.plan.slab_panel_bytes(cplx, self.nranks)
             P, g = self.nranks, self.rank
-            if self.p2p:
+            if self.mode == "carry":
+                agg_b, flag_b = self.plan.slab_tri_bytes(cplx, P)
+                own = torch.empty(nbytes // 8, dtype=torch.float64, device=self.device)
+                self._bufs[key] = (own, PeerBuffers(agg_b, P, g, self.group),
+                                   PeerBuffers(flag_b, P, g, self.group))
+                if self._timed_out is None:
+                    self._timed_out = torch.zeros(1, dtype=torch.int32, device=self.device)
+            elif self.p2p:
                 self._bufs[key] = (PeerBuffers(nbytes, P, g, self.group),
                                    PeerBuffers(nbytes, P, g, self.group),
                                    PeerBuffers(8 * 8, P, g, self.group))
@@ -158,6 +171,14 @@ class SlabPasses:
     def run(self, cplx, kappa, rhs, u, sign=1.0, jv=None):
         """u (this rank's rows) = box solve of sign * rhs (+ corrections of jv)."""
         p, P, g = self.plan, self.nranks, self.rank
+        if self.mode == "carry":
+            own, agg, flags = self._buffers(cplx)
+            p.slab_rows_fwd(cplx, P, g, rhs, own, sign=sign, jv=jv)
+            self._epoch += 1
+            p.slab_cols_tri(cplx, P, g, kappa, own, agg.ptrs, flags.ptrs, self._epoch,
+                            self._timed_out)
+            p.slab_rows_inv(cplx, P, g, own, u)
+            return u
         if self.p2p:
             A, B, F = self._buffers(cplx)
             p.slab_rows_fwd_p2p(cplx, P, g, rhs, A.ptrs, sign=sign, jv=jv)
@@ -183,7 +204,7 @@ class SlabBoxSolver:
     the transposes into the passes (SlabPasses)."""
 
     def __init__(self, grid, kappa, bc="dirichlet-zero", nranks=None, rank=None, group=None,
-                 backend=None, p2p=False):
+                 backend=None, p2p=False, mode=None):
         _validate(bc, kappa)
         if bc != "dirichlet-zero":
             raise ConfigError("the slab-decomposed box solve supports the dirichlet-zero closure")
@@ -199,7 +220,7 @@ class SlabBoxSolver:
         self.plan = _grid_plan(grid, self.backend)
         self.rows = slab_rows(grid.m, self.nranks, self.rank)
         self.passes = SlabPasses(self.plan, self.nranks, self.rank, group,
-                                 self.backend.torch_device, p2p)
+                                 self.backend.torch_device, p2p, mode)
 
     def peers_ok(self):
         return self.passes.peers_ok()
@@ -218,7 +239,7 @@ class SlabBoxSolver:
         return self.passes.run(cplx, self.kappa, rhs, u)
 
 
-def solve_virtual(grid, kappa, rhs, nranks, backend=None, p2p=False):
+def solve_virtual(grid, kappa, rhs, nranks, backend=None, p2p=False, mode=None):
     """The P-slab solve of a full (m+1)^2 rhs on ONE device: every rank's
     passes run in turn and the all-to-alls are chunk copies (p2p=True: the
     fused passes store into the other virtual ranks' buffers directly).
@@ -242,6 +263,24 @@ def solve_virtual(grid, kappa, rhs, nranks, backend=None, p2p=False):
         for g in range(nranks):
             for h in range(nranks):
                 dst[g][h * c:(h + 1) * c].copy_(src[h][g * c:(g + 1) * c])
+
+    if mode == "carry":
+        # transpose-free: every rank's own buffer, one column launch for all
+        agg_b, flag_b = plan.slab_tri_bytes(cplx, nranks)
+        agg = [torch.zeros(max(agg_b // 8, 1), dtype=torch.float64, device=dev) for _ in range(nranks)]
+        flg = [torch.zeros(max(flag_b // 8, 1), dtype=torch.int64, device=dev) for _ in range(nranks)]
+        for g, s in enumerate(solvers):
+            r0, r1 = s.rows
+            plan.slab_rows_fwd(cplx, nranks, g, rhs[r0:r1].contiguous(), send[g])
+        plan.slab_cols_tri(cplx, nranks, 0, solvers[0].kappa, None, agg, flg, 1,
+                           virt_panels=send)
+        u = torch.zeros((m + 1, m + 1), dtype=dt, device=dev)
+        for g, s in enumerate(solvers):
+            r0, r1 = s.rows
+            out = torch.empty((r1 - r0, m + 1), dtype=dt, device=dev)
+            plan.slab_rows_inv(cplx, nranks, g, send[g], out)
+            u[r0:r1] = out
+        return u
 
     if p2p:
         send.clear()
@@ -330,7 +369,7 @@ class SlabRichardson:
     13 n_ctl stencil values (include/kfbi_b200.h, kfbi_slab_*).  The field,
     density and iteration counts are bit-identical to the one-GPU solve."""
 
-    def __init__(self, workspace, nranks=None, rank=None, group=None, p2p=False):
+    def __init__(self, workspace, nranks=None, rank=None, group=None, p2p=False, mode=None):
         dist = _dist()
         self.ws = workspace
         self.nranks = int(nranks if nranks is not None else (dist.get_world_size(group) if dist else 1))
@@ -338,7 +377,7 @@ class SlabRichardson:
         self.group = group
         self.rows = slab_rows(workspace.grid.m, self.nranks, self.rank)
         self.passes = SlabPasses(workspace.plan, self.nranks, self.rank, group,
-                                 workspace.backend.torch_device, p2p)
+                                 workspace.backend.torch_device, p2p, mode)
 
     def solve(self, *, kappa, F, f_gamma, g, density, F_sign=1.0, f_gamma_sign=1.0, gamma=0.8,
               tol=1e-8, max_iter=200, bc_kind="dirichlet"):
@@ -388,7 +427,7 @@ class SlabRichardson:
 
 
 def richardson_virtual(workspace, nranks, *, kappa, F, f_gamma, g, density, F_sign=1.0,
-                       f_gamma_sign=1.0, gamma=0.8, tol=1e-8, max_iter=200):
+                       f_gamma_sign=1.0, gamma=0.8, tol=1e-8, max_iter=200, mode="a2a"):
     """The P-slab Richardson solve on ONE device (every rank's passes in
     turn, the exchanges as chunk copies, the all-reduce as a sum): the same
     kernels and layouts as SlabRichardson.  F: full (m+1)^2 field.  Returns
@@ -426,6 +465,11 @@ def richardson_virtual(workspace, nranks, *, kappa, F, f_gamma, g, density, F_si
             for h in range(P):
                 dst[q][h * c:(h + 1) * c].copy_(src[h][q * c:(q + 1) * c])
 
+    if mode == "carry":
+        agg_b, flag_b = plan.slab_tri_bytes(cplx, P)
+        agg = [torch.zeros(max(agg_b // 8, 1), dtype=torch.float64, device=dev) for _ in range(P)]
+        flg = [torch.zeros(max(flag_b // 8, 1), dtype=torch.int64, device=dev) for _ in range(P)]
+        epoch = 0
     plan.rich_begin(max_iter, tol)
     it = done = 0
     res, hist = 0.0, []
@@ -434,10 +478,14 @@ def richardson_virtual(workspace, nranks, *, kappa, F, f_gamma, g, density, F_si
         plan.edge_values(jm, jv)
         for q in range(P):
             plan.slab_rows_fwd(cplx, P, q, Fs[q], send[q], sign=F_sign, jv=jv)
-        a2a(recv, send)
-        for q in range(P):
-            plan.slab_cols(cplx, P, q, kappa, recv[q])
-        a2a(send, recv)
+        if mode == "carry":
+            epoch += 1
+            plan.slab_cols_tri(cplx, P, 0, kappa, None, agg, flg, epoch, virt_panels=send)
+        else:
+            a2a(recv, send)
+            for q in range(P):
+                plan.slab_cols(cplx, P, q, kappa, recv[q])
+            a2a(send, recv)
         vals.zero_()
         for q in range(P):
             plan.slab_rows_inv(cplx, P, q, send[q], us[q])

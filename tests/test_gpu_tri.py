@@ -95,3 +95,83 @@ def test_tri_slab_virtual_ranks_bit_identical(p2p):
     for p in (2, 4, 8):
         got = D.solve_virtual(grid, 40.0, rhs, p, p2p=p2p)
         assert torch.equal(got, one), p
+
+
+@pytest.mark.parametrize("m,cplx", [(256, False), (1024, False), (1024, True), (4096, False),
+                                    (4096, True)])
+def test_slab_carry_matches_one_gpu(m, cplx):
+    # transpose-free slab column stage (kfbi_slab_cols_tri): P virtual ranks
+    # in one launch exchange three values per column; equal to the one-slab
+    # solve up to the order the carries are combined in
+    import torch
+
+    from paper_2404_14864_b200 import dist as D
+
+    grid = k.CartesianGrid(BOX, m)
+    g = torch.Generator(device="cuda").manual_seed(m)
+    dt = torch.complex128 if cplx else torch.float64
+    rhs = torch.randn((m + 1, m + 1), generator=g, device="cuda", dtype=dt)
+    kappa = 2j * m if cplx else 2.0 * m
+    ref = k.BoxSolver(grid, kappa, "dirichlet-zero").solve(rhs)
+    scale = float(ref.abs().max())
+    for p in (1, 2, 4, 8):
+        u = D.solve_virtual(grid, kappa, rhs, p, mode="carry")
+        err = float((u - ref).abs().max()) / scale
+        assert err < 1e-13, (p, err)
+        for edge in (u[0], u[-1], u[:, 0], u[:, -1]):
+            assert bool((edge == 0).all())
+
+
+def test_slab_carry_16384():
+    import torch
+
+    from paper_2404_14864_b200 import dist as D
+
+    m = 16384
+    grid = k.CartesianGrid(PI_BOX, m)
+    g = torch.Generator(device="cuda").manual_seed(1)
+    rhs = torch.randn((m + 1, m + 1), generator=g, device="cuda", dtype=torch.float64)
+    ref = k.BoxSolver(grid, 2048.0, "dirichlet-zero").solve(rhs)
+    u = D.solve_virtual(grid, 2048.0, rhs, 8, mode="carry")
+    assert float((u - ref).abs().max()) / float(ref.abs().max()) < 1e-13
+    del u, ref, rhs
+    torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("kappa", [200.0, 16j])
+def test_slab_carry_richardson(kappa):
+    # the slab Richardson solve with the transpose-free column stage: same
+    # iterations as the one-GPU device solve, field within rounding
+    import torch
+
+    from paper_2404_14864_b200 import dist as D
+    from paper_2404_14864_b200.bvp import solve_device
+
+    box = BOX if not isinstance(kappa, complex) else PI_BOX
+    ws = k.InterfaceWorkspace(k.build_grid(box, 256, k.StarCurve(1.0, c=0.2, lobes=8)))
+    sol = k.StaticPlaneWave(kappa=abs(kappa))
+    cps = ws.cps
+    interior = ws.geometry.classification.interior
+    dt = torch.complex128 if isinstance(kappa, complex) else torch.float64
+    X, Y = ws.grid.X, ws.grid.Y
+    F = torch.from_numpy(np.where(interior, -(1.0 + kappa) * sol.u(X, Y), 0.0)).to("cuda", dt)
+    fg = torch.from_numpy(np.asarray(-(1.0 + kappa) * sol.u(cps.x, cps.y))).to("cuda", dt)
+    gb = torch.from_numpy(np.asarray(sol.dirichlet(cps.x, cps.y))).to("cuda", dt)
+    ref = solve_device(ws, kappa=kappa, F=F.reshape(-1), f_gamma=fg, g=gb,
+                       density=torch.zeros(cps.m, dtype=dt, device="cuda"))
+    for p in (2, 4):
+        dens = torch.zeros(cps.m, dtype=dt, device="cuda")
+        u, tu, tn, it, res, hist = D.richardson_virtual(ws, p, kappa=kappa, F=F, f_gamma=fg, g=gb,
+                                                        density=dens, mode="carry")
+        assert it == ref.iterations
+        err = float((u.reshape(-1) - ref.u.reshape(-1)).abs().max()) / float(ref.u.abs().max())
+        assert err < 1e-11, (p, err)
+    # the real SlabRichardson at P = 1 in carry mode (IPC buffers, in-kernel exchange)
+    solver = D.SlabRichardson(ws, mode="carry")
+    dens = torch.zeros(cps.m, dtype=dt, device="cuda")
+    m1 = ws.grid.m
+    u, tu, tn, it, res, hist = solver.solve(kappa=kappa, F=F[:m1].contiguous(), f_gamma=fg, g=gb,
+                                            density=dens)
+    assert it == ref.iterations and solver.passes.peers_ok()
+    err = float((u.reshape(-1) - ref.u.reshape(-1)[:m1 * (m1 + 1)]).abs().max()) / float(ref.u.abs().max())
+    assert err < 1e-11
