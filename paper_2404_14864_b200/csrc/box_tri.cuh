@@ -572,3 +572,85 @@ __global__ void __launch_bounds__(tri::Cfg<tri::TMA_LOGM>::THREADS, 1) cols_tri_
 }
 
 }  // namespace kfbi
+
+namespace kfbi {
+
+// ---------------------------------------------------------------------------
+// The inverse row transform evaluated only where the trace extraction reads
+// it (sweep 1 of the operator form needs the trace, not the field): for the
+// stencil nodes (i, j) of one grid row j,
+//   u(i, j) = 2 sum_{kx=1}^{M-1} P[kx][j] sin(pi kx i / M)
+// (the DST-I of rows_inv_reg, boxsolve.py:90-93) as a direct sum over the
+// column-stage output of row j.  One CTA per row with stencil nodes: the row
+// and the sine table sit in shared memory, one fixed-order block reduction
+// per node.  Reads each needed row once, writes nothing but the node values.
+template <bool CPLX>
+__global__ void __launch_bounds__(256) stencil_eval_kernel(BoxArgs a, const int *__restrict__ rows,
+                                                           const int *__restrict__ rowptr,
+                                                           const int *__restrict__ cols,
+                                                           typename std::conditional<CPLX, double2, double>::type *vals) {
+  using T = typename std::conditional<CPLX, double2, double>::type;
+  using S = Sc<T>;
+  extern __shared__ double2 sraw[];
+  const int M = a.m;
+  T *row = reinterpret_cast<T *>(sraw);                       // [M]
+  double *sn = reinterpret_cast<double *>(row + M);           // [M] sin(pi n / M)
+  __shared__ T red[8];
+  const int j = rows[blockIdx.x];
+  const int t = threadIdx.x;
+  for (int kx = t; kx < M; kx += blockDim.x) {
+    sn[kx] = a.sinv[kx];
+    T v = S::zero();
+    if (kx >= 1) {
+      if constexpr (CPLX) {
+        v = static_cast<const double2 *>(a.panels)[((size_t)(kx >> 1) * a.rows + j) * 2 + (kx & 1)];
+      } else {
+        v = static_cast<const double *>(a.panels)[((size_t)(kx >> 2) * a.rows + j) * 4 + (kx & 3)];
+      }
+    }
+    row[kx] = v;
+  }
+  __syncthreads();
+  const int twoM = 2 * M;
+  for (int q = rowptr[blockIdx.x]; q < rowptr[blockIdx.x + 1]; ++q) {
+    const int i = cols[q];
+    T acc = S::zero();
+    int n = (int)(((long long)t * i) % twoM);
+    const int dn = (int)(((long long)blockDim.x * i) % twoM);
+    for (int kx = t; kx < M; kx += blockDim.x) {
+      const double sv = n < M ? sn[n] : -sn[n - M];
+      acc = S::add(acc, S::rmul(row[kx], sv));
+      n += dn;
+      if (n >= twoM) n -= twoM;
+    }
+    // fixed-order block sum
+    if constexpr (CPLX) {
+      acc.x = warp_sum(acc.x);
+      acc.y = warp_sum(acc.y);
+    } else {
+      acc = warp_sum(acc);
+    }
+    if ((t & 31) == 0) red[t >> 5] = acc;
+    __syncthreads();
+    if (t == 0) {
+      T s2 = S::zero();
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s2 = S::add(s2, red[w]);
+      vals[q] = S::rmul(s2, 2.0);
+    }
+    __syncthreads();
+  }
+}
+
+// vals[13 p + s] = node value of stencil entry (p, s) (the slab extraction layout)
+template <typename T>
+__global__ void __launch_bounds__(256) stencil_vals_kernel(int n, const int *__restrict__ map,
+                                                           const T *__restrict__ nodevals, T *vals) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+#pragma unroll
+  for (int s = 0; s < 6; ++s) vals[13 * p + s] = nodevals[map[6 * p + s]];
+#pragma unroll
+  for (int s = 6; s < 13; ++s) vals[13 * p + s] = Sc<T>::zero();
+}
+
+}  // namespace kfbi

@@ -1399,7 +1399,9 @@ struct StepLog {
 //   op_solve_kernel); the step log entry.
 template <typename T>
 __global__ void op_finalize_kernel(const RichState *st, int n, T *A, const T *B, T *phik1,
-                                   int *skip, StepLog *log) {
+                                   int *skip, StepLog *log, const T *phi0 = nullptr) {
+  // phi0 != null: sweep 1 formed only its trace, so a solve converging at
+  // sweep 1 also needs the field, from phi_0
   const int K = st->iters, done = st->done;
   const bool odd = (K & 1) != 0;
   for (int p = threadIdx.x; p < n; p += blockDim.x) {
@@ -1407,10 +1409,12 @@ __global__ void op_finalize_kernel(const RichState *st, int n, T *A, const T *B,
       const T a = A[p], b = B[p];
       phik1[p] = odd ? b : a;       // phi_(K-1)
       if (!odd) A[p] = b;           // phi_K into the density buffer
+    } else if (phi0) {
+      phik1[p] = phi0[p];
     }
   }
   if (threadIdx.x == 0) {
-    skip[0] = (K >= 2 && done == 1) ? 0 : 1;
+    skip[0] = ((K >= 2 || phi0) && done == 1) ? 0 : 1;
     if (log) {
       log->iterations = K;
       log->status = done;

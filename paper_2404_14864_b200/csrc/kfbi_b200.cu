@@ -10,6 +10,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <algorithm>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -19,6 +20,7 @@
 #include "interface_kernels.cuh"
 #include "gmres.cuh"
 #include "classify.cuh"
+#include "box_tri.cuh"
 #include "stepping_kernels.cuh"
 
 using namespace kfbi;
@@ -124,6 +126,11 @@ struct kfbi_plan {
   DevBuf<double2> gm_V, gm_w, gm_H, gm_sn, gm_g, gm_y, gm_part, gm_tr;
   DevBuf<double> gm_cs, gm_np;
   DevBuf<GmresState> gm_st;
+  // stencil nodes grouped by grid row (trace-only sweep 1 of the operator form)
+  DevBuf<int> sn_rows, sn_rowptr, sn_cols, sn_map;
+  int sn_nrows = 0, sn_nodes = 0;
+  bool trace_sweep = true;          // kfbi_plan_set_trace_sweep
+  DevBuf<double2> sn_vals, sn_v13;
   DevBuf<int> skip;
   DevBuf<StepLog> log;
   int log_cap = 0;
@@ -807,6 +814,52 @@ kfbi_status op_solve(kfbi_plan *p, const kfbi_bvp *b, cudaStream_t s) {
   });
 }
 
+// Sweep 1 of the operator form when only its trace is needed (Dirichlet,
+// one slab): rows_fwd + column stage, then the inverse row transform only at
+// the stencil nodes (stencil_eval_kernel) instead of the whole field; the
+// extraction and density update read those values (the slab update kernel).
+bool trace_sweep_ok(kfbi_plan *p, const kfbi_bvp *b) {
+  // the row and the sine table of one grid row in shared memory: M <= 8192
+  return p->trace_sweep && b->bc_kind == 0 && b->box_bc == KFBI_DIRICHLET_ZERO && p->sn_nrows > 0 &&
+         p->m <= 8192;
+}
+
+template <typename T>
+kfbi_status sweep1_trace(kfbi_plan *p, const kfbi_bvp *b, cudaStream_t s) {
+  constexpr bool CPLX = std::is_same<T, double2>::value;
+  const int *done = &p->st.p->done;
+  KFBI_TRY(jumps_T<T>(p, b->kappa_re, b->kappa_im, b->density, nullptr, b->f_gamma, b->f_gamma_sign,
+                      p->jm.p, done, s));
+  KFBI_TRY(edges_T<T>(p, p->jm.p, p->jv.p, done, s));
+  BoxArgs a = box_args(p, b->kappa_re, b->kappa_im, done);
+  a.npl = CPLX ? p->m / 2 : p->m / 4;
+  CorrArgs<T> c = corr_args<T>(p, reinterpret_cast<const T *>(p->jv.p));
+  KFBI_TRY(box_passes_reg<CPLX>(p, a, b->F, b->F_sign, c, nullptr, s, 3));
+  T *nv = reinterpret_cast<T *>(p->sn_vals.p);
+  const size_t smem = (size_t)p->m * (sizeof(T) + sizeof(double));
+  static size_t attr[2] = {0, 0};
+  if (smem > attr[CPLX] && smem > 48 * 1024) {
+    KFBI_CUDA(cudaFuncSetAttribute(stencil_eval_kernel<CPLX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)smem), "extract-traces");
+    attr[CPLX] = smem;
+  }
+  KFBI_TRY(launch(p, KFBI_K_EXTRACT, s, [&] {
+    stencil_eval_kernel<CPLX><<<p->sn_nrows, 256, smem, s>>>(a, p->sn_rows.p, p->sn_rowptr.p, p->sn_cols.p, nv);
+  }));
+  T *v13 = reinterpret_cast<T *>(p->sn_v13.p);
+  const int blocks = (p->n_ctl + 255) / 256;
+  KFBI_TRY(launch(p, KFBI_K_EXTRACT, s, [&] {
+    stencil_vals_kernel<T><<<blocks, 256, 0, s>>>(p->n_ctl, p->sn_map.p, nv, v13);
+  }));
+  ExtractArgs x = extract_args(p, false);
+  return launch(p, KFBI_K_DENSITY, s, [&] {
+    extract_update_vals_kernel<T><<<blocks, 256, 0, s>>>(
+        x, v13, reinterpret_cast<const T *>(p->jm.p), static_cast<const T *>(b->g),
+        static_cast<T *>(b->density), static_cast<T *>(b->trace_u), static_cast<T *>(b->trace_un),
+        b->gamma, 1, p->st.p, p->history.p);
+  });
+}
+
 // Full pipeline from the density before the converging update: the field and
 // traces the reference returns (bvp.py:319-323, 336-344).
 template <typename T>
@@ -1290,6 +1343,38 @@ kfbi_status kfbi_plan_set_geometry(kfbi_plan *p, const kfbi_geometry *g) {
   UP(ainv_rows, g->ainv_rows, 18 * n);
   UP(jcoef, g->jcoef, 36 * n);
 #undef UP
+  // unique six-point stencil nodes grouped by row (trace-only sweep 1)
+  if (e == cudaSuccess) {
+    std::vector<std::pair<int, int>> nodes;       // (flat node, entry)
+    nodes.reserve(6 * (size_t)n);
+    for (int q = 0; q < 6 * n; ++q) nodes.emplace_back(g->stencil[q], q);
+    std::sort(nodes.begin(), nodes.end());
+    std::vector<int> rows, rowptr, cols, map(6 * (size_t)n);
+    int last = -1, uniq = -1, lastrow = -1;
+    for (const auto &pr : nodes) {
+      if (pr.first != last) {
+        last = pr.first;
+        ++uniq;
+        const int j = pr.first / (m + 1), i = pr.first - j * (m + 1);
+        if (j != lastrow) {
+          rows.push_back(j);
+          rowptr.push_back(uniq);
+          lastrow = j;
+        }
+        cols.push_back(i);
+      }
+      map[pr.second] = uniq;
+    }
+    rowptr.push_back(uniq + 1);
+    p->sn_nrows = (int)rows.size();
+    p->sn_nodes = uniq + 1;
+    if ((e = upload(p->sn_rows, rows.data(), rows.size())) == cudaSuccess &&
+        (e = upload(p->sn_rowptr, rowptr.data(), rowptr.size())) == cudaSuccess &&
+        (e = upload(p->sn_cols, cols.data(), cols.size())) == cudaSuccess &&
+        (e = upload(p->sn_map, map.data(), map.size())) == cudaSuccess &&
+        (e = p->sn_vals.ensure((size_t)p->sn_nodes)) == cudaSuccess)
+      e = p->sn_v13.ensure(13 * (size_t)n);
+  }
   if (e == cudaSuccess) e = p->d1.ensure(n);
   if (e == cudaSuccess) e = p->psi_s.ensure(n);
   if (e == cudaSuccess) e = p->jm.ensure(6 * (size_t)n);
@@ -1321,6 +1406,12 @@ kfbi_status kfbi_plan_get_colsolver(kfbi_plan *p, int32_t *mode) {
   KFBI_TRY(check_plan(p));
   if (!mode) return fail(KFBI_E_CONFIG, "null argument");
   *mode = p->col_mode;
+  return KFBI_OK;
+}
+
+kfbi_status kfbi_plan_set_trace_sweep(kfbi_plan *p, int32_t on) {
+  KFBI_TRY(check_plan(p));
+  p->trace_sweep = on != 0;
   return KFBI_OK;
 }
 
@@ -1499,6 +1590,7 @@ kfbi_status kfbi_richardson(kfbi_plan *p, const kfbi_bvp *b, kfbi_bvp_result *re
   if (b->bc_kind == 1 && !p->has_os)
     return fail(KFBI_E_CONFIG, "Neumann BVP: one-sided extraction tables missing (kfbi_plan_set_onesided)");
   const bool use_op = b->use_operator != 0;
+  bool sync_trace_only = false;
   const size_t es = cplx ? sizeof(double2) : sizeof(double);
   if (use_op) {
     if (!p->op_valid || p->op_dtype != b->dtype || p->op_kre != b->kappa_re || p->op_kim != b->kappa_im ||
@@ -1515,7 +1607,10 @@ kfbi_status kfbi_richardson(kfbi_plan *p, const kfbi_bvp *b, kfbi_bvp_result *re
     // whether the full pipeline must recompute the field and logs the step
     if (b->log_slot >= p->log_cap) return fail(KFBI_E_CONFIG, "log slot out of range (kfbi_log_reserve)");
     KFBI_TRY(ensure_async_scratch(p));
-    if (cplx) KFBI_TRY(sweep<double2>(p, b, s));
+    const bool tr = trace_sweep_ok(p, b);
+    if (tr && cplx) KFBI_TRY(sweep1_trace<double2>(p, b, s));
+    else if (tr) KFBI_TRY(sweep1_trace<double>(p, b, s));
+    else if (cplx) KFBI_TRY(sweep<double2>(p, b, s));
     else KFBI_TRY(sweep<double>(p, b, s));
     KFBI_CUDA(cudaMemcpyAsync(p->trace1.p, b->bc_kind ? b->trace_un : b->trace_u, p->n_ctl * es, cudaMemcpyDeviceToDevice, s),
               "density-update");
@@ -1528,7 +1623,8 @@ kfbi_status kfbi_richardson(kfbi_plan *p, const kfbi_bvp *b, kfbi_bvp_result *re
     if (cplx) {
       KFBI_TRY(launch(p, KFBI_K_DENSITY, s, [&] {
         op_finalize_kernel<double2><<<1, 256, 0, s>>>(p->st.p, p->n_ctl, static_cast<double2 *>(b->density),
-                                                      p->phi_prev.p, p->phik1.p, skip, entry);
+                                                      p->phi_prev.p, p->phik1.p, skip, entry,
+                                                      tr ? p->phi0.p : nullptr);
       }));
       KFBI_TRY(final_pipeline<double2>(p, b, p->phik1.p, s, skip));
     } else {
@@ -1536,7 +1632,7 @@ kfbi_status kfbi_richardson(kfbi_plan *p, const kfbi_bvp *b, kfbi_bvp_result *re
         op_finalize_kernel<double><<<1, 256, 0, s>>>(
             p->st.p, p->n_ctl, static_cast<double *>(b->density),
             reinterpret_cast<const double *>(p->phi_prev.p), reinterpret_cast<double *>(p->phik1.p),
-            skip, entry);
+            skip, entry, tr ? reinterpret_cast<const double *>(p->phi0.p) : nullptr);
       }));
       KFBI_TRY(final_pipeline<double>(p, b, p->phik1.p, s, skip));
     }
@@ -1548,8 +1644,12 @@ kfbi_status kfbi_richardson(kfbi_plan *p, const kfbi_bvp *b, kfbi_bvp_result *re
   if (use_op) {
     // sweep 1 through the pipeline, then every further sweep inside one
     // cooperative launch; a single host sync per solve
-    if (cplx) KFBI_TRY(sweep<double2>(p, b, s));
+    const bool tr = trace_sweep_ok(p, b);
+    if (tr && cplx) KFBI_TRY(sweep1_trace<double2>(p, b, s));
+    else if (tr) KFBI_TRY(sweep1_trace<double>(p, b, s));
+    else if (cplx) KFBI_TRY(sweep<double2>(p, b, s));
     else KFBI_TRY(sweep<double>(p, b, s));
+    sync_trace_only = tr;
     KFBI_CUDA(cudaMemcpyAsync(p->trace1.p, b->bc_kind ? b->trace_un : b->trace_u, p->n_ctl * es, cudaMemcpyDeviceToDevice, s),
               "density-update");
     if (b->max_iter > 1) {
@@ -1576,6 +1676,11 @@ kfbi_status kfbi_richardson(kfbi_plan *p, const kfbi_bvp *b, kfbi_bvp_result *re
       if (p->st_host->done != 0 || enqueued >= b->max_iter) break;
       batch = 2;
     }
+  }
+  if (use_op && sync_trace_only && p->st_host->iters == 1 && p->st_host->done == 1) {
+    // converged at sweep 1, whose field was not formed: recompute it from phi_0
+    if (cplx) KFBI_TRY(final_pipeline<double2>(p, b, p->phi0.p, s));
+    else KFBI_TRY(final_pipeline<double>(p, b, p->phi0.p, s));
   }
   if (use_op && p->st_host->iters >= 2) {
     // after K sweeps: phi_K sits in density when K is odd, in phi_prev when

@@ -292,3 +292,40 @@ def test_operator_form_capacity():
     # below the cap the same decision builds the operator for long runs
     small = k.StepContext(k.build_grid(BOX, 1024, k.StarCurve(1.0, c=0.2, lobes=8)))
     assert small.n_ctl <= cap and operator_pays(small, 10**4)
+
+
+@pytest.mark.parametrize("cplx", [False, True], ids=["f64", "c128"])
+def test_trace_only_first_sweep(cplx):
+    # operator form: sweep 1 forms only its trace at the stencil nodes
+    # (kfbi_plan_set_trace_sweep); same iterations and field (to rounding)
+    # as the full first sweep, including a solve converging at sweep 1
+    import torch
+
+    from paper_2404_14864_b200.bvp import solve_device
+
+    box = PI_BOX if cplx else BOX
+    ws = k.InterfaceWorkspace(k.build_grid(box, 512, k.StarCurve(1.0, c=0.2, lobes=8)))
+    kappa = 512j if cplx else 512.0
+    sol = k.StaticPlaneWave(kappa=abs(kappa))
+    cps = ws.cps
+    dt = torch.complex128 if cplx else torch.float64
+    X, Y = ws.grid.X, ws.grid.Y
+    F = torch.from_numpy(np.where(ws.geometry.classification.interior, -(1.0 + kappa) * sol.u(X, Y),
+                                  0.0)).to("cuda", dt).reshape(-1)
+    fg = torch.from_numpy(np.asarray(-(1.0 + kappa) * sol.u(cps.x, cps.y))).to("cuda", dt)
+    g = torch.from_numpy(np.asarray(sol.dirichlet(cps.x, cps.y))).to("cuda", dt)
+    ws.ensure_operator(kappa, cplx)
+    out = {}
+    for tol in (1e-8, 1e3):
+        for on in (True, False):
+            ws.plan.set_trace_sweep(on)
+            r = solve_device(ws, kappa=kappa, F=F, f_gamma=fg, g=g, tol=tol, use_operator=True,
+                             density=torch.zeros(cps.m, dtype=dt, device="cuda"))
+            out[(tol, on)] = (r.iterations, r.u.clone(), r.density.clone())
+        ws.plan.set_trace_sweep(True)
+        (i1, u1, d1), (i0, u0, d0) = out[(tol, True)], out[(tol, False)]
+        assert i1 == i0
+        scale = float(u0.abs().max())
+        assert float((u1 - u0).abs().max()) / scale < 1e-12
+        assert float((d1 - d0).abs().max()) / float(d0.abs().max()) < 1e-12
+    assert out[(1e3, True)][0] == 1
