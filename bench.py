@@ -168,8 +168,13 @@ def _dist():
     if ws > 1 and not dist.is_initialized():
         import torch
 
+        from datetime import timedelta
+
         backend = "nccl" if torch.cuda.is_available() else "gloo"
-        dist.init_process_group(backend=backend)
+        if backend == "nccl":
+            torch.cuda.set_device(local)
+        # a stuck collective fails the run after 5 minutes instead of hanging it
+        dist.init_process_group(backend=backend, timeout=timedelta(seconds=300))
     return ws, rank, local
 
 

@@ -584,58 +584,77 @@ namespace kfbi {
 // column-stage output of row j.  One CTA per row with stencil nodes: the row
 // and the sine table sit in shared memory, one fixed-order block reduction
 // per node.  Reads each needed row once, writes nothing but the node values.
+constexpr int SEVAL_E = 16;                    // row elements per thread (blockDim = M / 16)
+constexpr int SEVAL_NB = 32;                   // nodes per reduction batch
+
 template <bool CPLX>
-__global__ void __launch_bounds__(256) stencil_eval_kernel(BoxArgs a, const int *__restrict__ rows,
-                                                           const int *__restrict__ rowptr,
+__global__ void __launch_bounds__(512) stencil_eval_kernel(BoxArgs a, const int *__restrict__ pairs,
+                                                           const int *__restrict__ pairptr,
                                                            const int *__restrict__ cols,
                                                            typename std::conditional<CPLX, double2, double>::type *vals) {
+  // One CTA per row pair (2q, 2q + 1): the two rows are adjacent 32-byte
+  // sectors of every strip, so they are read together.  Node entries encode
+  // the column in bits 1.. and the row of the pair in bit 0.
   using T = typename std::conditional<CPLX, double2, double>::type;
   using S = Sc<T>;
-  extern __shared__ double2 sraw[];
+  __shared__ T red[SEVAL_NB][16];
   const int M = a.m;
-  T *row = reinterpret_cast<T *>(sraw);                       // [M]
-  double *sn = reinterpret_cast<double *>(row + M);           // [M] sin(pi n / M)
-  __shared__ T red[8];
-  const int j = rows[blockIdx.x];
-  const int t = threadIdx.x;
-  for (int kx = t; kx < M; kx += blockDim.x) {
-    sn[kx] = a.sinv[kx];
-    T v = S::zero();
-    if (kx >= 1) {
-      if constexpr (CPLX) {
-        v = static_cast<const double2 *>(a.panels)[((size_t)(kx >> 1) * a.rows + j) * 2 + (kx & 1)];
-      } else {
-        v = static_cast<const double *>(a.panels)[((size_t)(kx >> 2) * a.rows + j) * 4 + (kx & 3)];
-      }
-    }
-    row[kx] = v;
-  }
-  __syncthreads();
-  const int twoM = 2 * M;
-  for (int q = rowptr[blockIdx.x]; q < rowptr[blockIdx.x + 1]; ++q) {
-    const int i = cols[q];
-    T acc = S::zero();
-    int n = (int)(((long long)t * i) % twoM);
-    const int dn = (int)(((long long)blockDim.x * i) % twoM);
-    for (int kx = t; kx < M; kx += blockDim.x) {
-      const double sv = n < M ? sn[n] : -sn[n - M];
-      acc = S::add(acc, S::rmul(row[kx], sv));
-      n += dn;
-      if (n >= twoM) n -= twoM;
-    }
-    // fixed-order block sum
+  const int j0 = 2 * pairs[blockIdx.x];
+  const int t = threadIdx.x, nt = blockDim.x;  // nt = M / 16
+  const int lane = t & 31, warp = t >> 5, nw = nt >> 5;
+  T x0[SEVAL_E], x1[SEVAL_E];
+#pragma unroll
+  for (int e = 0; e < SEVAL_E; ++e) {
+    const int kx = t + nt * e;
     if constexpr (CPLX) {
-      acc.x = warp_sum(acc.x);
-      acc.y = warp_sum(acc.y);
+      const double2 *P2 = static_cast<const double2 *>(a.panels) + ((size_t)(kx >> 1) * a.rows + j0) * 2 + (kx & 1);
+      x0[e] = P2[0];
+      x1[e] = j0 + 1 < M ? P2[2] : S::zero();
     } else {
-      acc = warp_sum(acc);
+      const double *P = static_cast<const double *>(a.panels) + ((size_t)(kx >> 2) * a.rows + j0) * 4 + (kx & 3);
+      x0[e] = P[0];
+      x1[e] = j0 + 1 < M ? P[4] : S::zero();
     }
-    if ((t & 31) == 0) red[t >> 5] = acc;
+  }
+  if (t == 0) {                                 // kx = 0: padding column
+    x0[0] = S::zero();
+    x1[0] = S::zero();
+  }
+  const int mask2 = 2 * M - 1;                  // M is a power of two
+  // sin(pi n / M) for 0 <= n < 2M from the table sin(pi n / M), n < M
+  auto sin_n = [&](int n) -> double { return n < M ? __ldg(&a.sinv[n]) : -__ldg(&a.sinv[n - M]); };
+  const int q0 = pairptr[blockIdx.x], q1 = pairptr[blockIdx.x + 1];
+  for (int qb = q0; qb < q1; qb += SEVAL_NB) {
+    const int nq = min(SEVAL_NB, q1 - qb);
+    for (int k = 0; k < nq; ++k) {
+      const int code = cols[qb + k], i = code >> 1, odd = code & 1;
+      // sin((t + nt e) pi i / M), e = 0..15: exact first two terms, then the
+      // three-term recurrence s_{e+1} = 2 cos(d) s_e - s_{e-1}, d = pi nt i / M
+      double sm = sin_n((t * i) & mask2);
+      double s0 = sin_n(((t + nt) * i) & mask2);
+      const double c2 = 2.0 * sin_n(((nt * i) + (M >> 1)) & mask2);   // 2 cos(d)
+      T acc = S::rmul(odd ? x1[0] : x0[0], sm);
+      acc = S::add(acc, S::rmul(odd ? x1[1] : x0[1], s0));
+#pragma unroll
+      for (int e = 2; e < SEVAL_E; ++e) {
+        const double sn = fma(c2, s0, -sm);
+        sm = s0;
+        s0 = sn;
+        acc = S::add(acc, S::rmul(odd ? x1[e] : x0[e], sn));
+      }
+      if constexpr (CPLX) {
+        acc.x = warp_sum(acc.x);
+        acc.y = warp_sum(acc.y);
+      } else {
+        acc = warp_sum(acc);
+      }
+      if (lane == 0) red[k][warp] = acc;
+    }
     __syncthreads();
-    if (t == 0) {
+    if (t < nq) {                                 // fixed-order sum over the warps
       T s2 = S::zero();
-      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s2 = S::add(s2, red[w]);
-      vals[q] = S::rmul(s2, 2.0);
+      for (int w = 0; w < nw; ++w) s2 = S::add(s2, red[t][w]);
+      vals[qb + t] = S::rmul(s2, 2.0);
     }
     __syncthreads();
   }

@@ -129,7 +129,7 @@ struct kfbi_plan {
   // stencil nodes grouped by grid row (trace-only sweep 1 of the operator form)
   DevBuf<int> sn_rows, sn_rowptr, sn_cols, sn_map;
   int sn_nrows = 0, sn_nodes = 0;
-  bool trace_sweep = true;          // kfbi_plan_set_trace_sweep
+  bool trace_sweep = false;         // kfbi_plan_set_trace_sweep (opt-in: measured no gain)
   DevBuf<double2> sn_vals, sn_v13;
   DevBuf<int> skip;
   DevBuf<StepLog> log;
@@ -819,9 +819,9 @@ kfbi_status op_solve(kfbi_plan *p, const kfbi_bvp *b, cudaStream_t s) {
 // the stencil nodes (stencil_eval_kernel) instead of the whole field; the
 // extraction and density update read those values (the slab update kernel).
 bool trace_sweep_ok(kfbi_plan *p, const kfbi_bvp *b) {
-  // the row and the sine table of one grid row in shared memory: M <= 8192
+  // one grid row per CTA, 16 elements per thread: 512 <= M <= 8192
   return p->trace_sweep && b->bc_kind == 0 && b->box_bc == KFBI_DIRICHLET_ZERO && p->sn_nrows > 0 &&
-         p->m <= 8192;
+         p->m >= 512 && p->m <= 8192;
 }
 
 template <typename T>
@@ -836,15 +836,9 @@ kfbi_status sweep1_trace(kfbi_plan *p, const kfbi_bvp *b, cudaStream_t s) {
   CorrArgs<T> c = corr_args<T>(p, reinterpret_cast<const T *>(p->jv.p));
   KFBI_TRY(box_passes_reg<CPLX>(p, a, b->F, b->F_sign, c, nullptr, s, 3));
   T *nv = reinterpret_cast<T *>(p->sn_vals.p);
-  const size_t smem = (size_t)p->m * (sizeof(T) + sizeof(double));
-  static size_t attr[2] = {0, 0};
-  if (smem > attr[CPLX] && smem > 48 * 1024) {
-    KFBI_CUDA(cudaFuncSetAttribute(stencil_eval_kernel<CPLX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)smem), "extract-traces");
-    attr[CPLX] = smem;
-  }
   KFBI_TRY(launch(p, KFBI_K_EXTRACT, s, [&] {
-    stencil_eval_kernel<CPLX><<<p->sn_nrows, 256, smem, s>>>(a, p->sn_rows.p, p->sn_rowptr.p, p->sn_cols.p, nv);
+    stencil_eval_kernel<CPLX><<<p->sn_nrows, p->m / SEVAL_E, 0, s>>>(a, p->sn_rows.p, p->sn_rowptr.p,
+                                                                     p->sn_cols.p, nv);
   }));
   T *v13 = reinterpret_cast<T *>(p->sn_v13.p);
   const int blocks = (p->n_ctl + 255) / 256;
@@ -1349,19 +1343,20 @@ kfbi_status kfbi_plan_set_geometry(kfbi_plan *p, const kfbi_geometry *g) {
     nodes.reserve(6 * (size_t)n);
     for (int q = 0; q < 6 * n; ++q) nodes.emplace_back(g->stencil[q], q);
     std::sort(nodes.begin(), nodes.end());
+    // grouped by row PAIR (2q, 2q+1); node code = 2 column + (row & 1)
     std::vector<int> rows, rowptr, cols, map(6 * (size_t)n);
-    int last = -1, uniq = -1, lastrow = -1;
+    int last = -1, uniq = -1, lastpair = -1;
     for (const auto &pr : nodes) {
       if (pr.first != last) {
         last = pr.first;
         ++uniq;
         const int j = pr.first / (m + 1), i = pr.first - j * (m + 1);
-        if (j != lastrow) {
-          rows.push_back(j);
+        if ((j >> 1) != lastpair) {
+          rows.push_back(j >> 1);
           rowptr.push_back(uniq);
-          lastrow = j;
+          lastpair = j >> 1;
         }
-        cols.push_back(i);
+        cols.push_back(2 * i + (j & 1));
       }
       map[pr.second] = uniq;
     }

@@ -322,7 +322,7 @@ def test_trace_only_first_sweep(cplx):
             r = solve_device(ws, kappa=kappa, F=F, f_gamma=fg, g=g, tol=tol, use_operator=True,
                              density=torch.zeros(cps.m, dtype=dt, device="cuda"))
             out[(tol, on)] = (r.iterations, r.u.clone(), r.density.clone())
-        ws.plan.set_trace_sweep(True)
+        ws.plan.set_trace_sweep(False)
         (i1, u1, d1), (i0, u0, d0) = out[(tol, True)], out[(tol, False)]
         assert i1 == i0
         scale = float(u0.abs().max())
