@@ -196,6 +196,13 @@ kfbi_status kfbi_plan_get_colsolver(kfbi_plan *plan, int32_t *mode);
  * 100-200 us for the full inverse row pass.  The returned field
  * is the final pipeline's either way. */
 kfbi_status kfbi_plan_set_trace_sweep(kfbi_plan *plan, int32_t on);
+/* Dirichlet box solves on one slab, 64 <= M <= 8192, tridiagonal-eligible
+ * kappa: one level of cyclic reduction in y (box_facr.cuh) — the even rows
+ * by DST-I x tridiagonal recurrences with root r^2 on M/2 rows, the odd rows
+ * by recurrences along x — half the row transforms, 5 instead of 6 field
+ * sweeps of HBM.  Default on (environment KFBI_FACR=0 at plan creation: off);
+ * 0 restores the three-pass solve. */
+kfbi_status kfbi_plan_set_facr(kfbi_plan *plan, int32_t on);
 kfbi_status kfbi_plan_colsolver_for(kfbi_plan *plan, double kappa_re, double kappa_im,
                                     int32_t *tridiagonal, double *bound);
 

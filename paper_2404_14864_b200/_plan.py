@@ -129,6 +129,11 @@ class Plan:
         (factored recurrences) or "dst" (DST-I -> divide -> DST-I)."""
         N.check(self._lib.kfbi_plan_set_colsolver(self.handle, self._COLS.index(mode)))
 
+    def set_facr(self, on):
+        """Cyclic-reduction (FACR(1)) form of the dirichlet box solve
+        (kfbi_plan_set_facr, default on where it applies)."""
+        N.check(self._lib.kfbi_plan_set_facr(self.handle, int(bool(on))))
+
     def set_trace_sweep(self, on):
         """Operator form, Dirichlet: sweep 1 forms only its trace (stencil
         nodes) instead of the whole field (kfbi_plan_set_trace_sweep)."""

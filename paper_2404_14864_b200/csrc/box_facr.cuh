@@ -1,0 +1,366 @@
+// Box solve by one level of cyclic reduction in y (FACR(1)): the same
+// dirichlet-zero solve of boxsolve.py:46-94 with HALF the row transforms.
+//
+// With g = sign F + corrections on the interior rows and B the x operator
+// (B v)_i = v_{i-1} - (4 + kappa h^2) v_i + v_{i+1} (zero ends), the 5-point
+// system is u_{j-1} + B u_j + u_{j+1} = h^2 g_j.  Eliminating the odd rows,
+// the even rows satisfy
+//   u_{j-2} + (2 I - B^2) u_j + u_{j+2} = h^2 (g_{j-1} + g_{j+1} - B g_j)
+// (u_0 = u_M = 0), which the DST along x diagonalises exactly like the full
+// system: in mode kx the columns are y_{m-1} + (2 - b^2) y_m + y_{m+1} with
+// b = 2 cos(pi kx / M) - 4 - kappa h^2, whose small root is r^2 (r the full
+// system's root), so the tridiagonal column stage runs on M / 2 rows with
+// r^2 (BoxArgs.red).  The odd rows follow from B u_j = h^2 g_j - u_{j-1} -
+// u_{j+1}: one constant-coefficient tridiagonal solve along x per row
+// (BoxArgs.trow, the same recurrence kernel along the row).
+//
+//   rows_fwd_facr : rows j-1, j, j+1 (+ corrections) -> w_j = g_{j-1} + g_{j+1}
+//                   - B g_j -> DST-I(x) -> panels of the M/2 even rows
+//   cols_tri (red): the even-row column systems (M/2 rows, root r^2)
+//   rows_inv_reg  : panels -> DST-I(x) -> u on the even rows (row_step 2)
+//   rows_odd_facr : the odd rows by x recurrences
+//
+// HBM traffic 5 (M-1)^2 s instead of 6 (M-1)^2 s, and half the row FFTs.
+#pragma once
+
+#include "box_reg.cuh"
+#include "box_tri.cuh"
+
+namespace kfbi {
+namespace facr {
+
+// add the sparse corrections of grid row j to a thread's elements
+// n = t + m TT (m < E) (interface.py:235-238, the owner of node column i)
+template <typename T, int E, int TT>
+KFBI_DEV void add_row_corr(const CorrArgs<T> &c, int j, int stride, int t, T (&v)[E]) {
+  if (!c.jv) return;
+  const int g0 = c.row_group[j], g1 = c.row_group[j + 1];
+  for (int g = g0; g < g1; ++g) {
+    const int i = c.group_node[g] - j * stride;
+    if (i < t || ((i - t) % TT) != 0) continue;
+    const int m = (i - t) / TT;
+    const T cv = group_correction<T>(c, g);
+#pragma unroll
+    for (int mm = 0; mm < E; ++mm)
+      if (mm == m) v[mm] = Sc<T>::add(v[mm], cv);
+  }
+}
+
+// The grid-row configuration of the x recurrence (one slot per CTA).
+template <int LOGM>
+struct CfgRow {
+  static constexpr int M = 1 << LOGM;
+  static constexpr int CH = M >= 1024 ? 32 : M / 32;
+  static constexpr int NH = 1;
+  static constexpr int NCH = M / CH;
+  static constexpr int THREADS = NCH;
+  static constexpr int CPW = 32;
+  static constexpr int NW = NCH / 32;
+  static constexpr int LCPW = 5;
+  static constexpr int MINB = THREADS * 255 <= 65536 / 2 ? 2 : 1;
+  static_assert(NCH >= 32 && NCH % 32 == 0 && THREADS <= 1024, "row recurrence: CTA size");
+};
+
+}  // namespace facr
+
+// ---------------------------------------------------------------------------
+template <bool CPLX, int LOGN>
+__global__ void __launch_bounds__(reg::Cfg<LOGN>::CTA_T, reg::Cfg<LOGN>::MINB)
+rows_fwd_facr(BoxArgs a, const void *__restrict__ rhs, double sign,
+              CorrArgs<typename std::conditional<CPLX, double2, double>::type> corr) {
+  using T = typename std::conditional<CPLX, double2, double>::type;
+  using S = Sc<T>;
+  using C = reg::Cfg<LOGN>;
+  constexpr int M = C::N, TT = C::T, E = reg::E;
+  extern __shared__ double2 smem[];
+  if (a.done && *a.done) return;
+  int seq, t;
+  const reg::View<LOGN> sm = reg::make_view<LOGN>(smem, seq, t);
+  const int stride = M + 1;
+  const int q = seq_index<LOGN>(seq);
+  const int nseq = CPLX ? a.rows : a.rows / 2;   // a.rows = M / 2 even rows
+  const bool valid = q < nseq;
+  const int r0 = CPLX ? q : 2 * q;               // even-row index (row 0: the zero ring)
+  const int J0 = 2 * r0;                         // grid rows 2 r0 (and 2 r0 + 2)
+  // g = sign F + corrections of one grid row at this thread's elements
+  auto row = [&](int j, T (&v)[E]) {
+#pragma unroll
+    for (int m = 0; m < E; ++m) {
+      const int n = t + m * TT;
+      T val = S::zero();
+      if (valid && j >= 1 && j <= M - 1 && n >= 1 && rhs != nullptr)
+        val = S::rmul(static_cast<const T *>(rhs)[(size_t)j * stride + n], sign);
+      v[m] = val;
+    }
+  };
+  // add the corrections of grid row j (coefficient k) into component `comp`
+  // of the staged sequence: distinct nodes of one row, one thread each
+  // (interface.py:235-238); callers separate rows that share a slot by barriers
+  auto scatter = [&](int j, int comp, double k) {
+    if (!corr.jv || !valid || j < 1 || j > M - 1) return;
+    const int g0 = corr.row_group[j], g1 = corr.row_group[j + 1];
+    for (int g = g0 + t; g < g1; g += TT) {
+      const T cv = S::rmul(group_correction<T>(corr, g), k);
+      const int i = corr.group_node[g] - j * stride;
+      if constexpr (CPLX) {
+        double2 &slot = sm[i];
+        slot = cadd(slot, cv);
+      } else {
+        double *slot = reinterpret_cast<double *>(&sm[i]) + comp;
+        *slot += cv;
+      }
+    }
+  };
+  // the even rows' g in shared memory (the stencil reads neighbours)
+  T ga[E], gb[E];
+  row(J0, ga);
+  if constexpr (!CPLX) row(J0 + 2, gb);
+  {
+    double2 v[E];
+#pragma unroll
+    for (int m = 0; m < E; ++m) {
+      if constexpr (CPLX) v[m] = ga[m];
+      else v[m] = make_double2(ga[m], gb[m]);
+    }
+    stage<LOGN>(sm, v, t);
+  }
+  reg::seq_sync<LOGN>();
+  scatter(J0, 0, 1.0);                           // the even rows' own corrections
+  if constexpr (!CPLX) scatter(J0 + 2, 1, 1.0);
+  reg::seq_sync<LOGN>();
+  // w = g_{j-1} + g_{j+1} - B g_j  (B g_j = g_{j,i-1} + g_{j,i+1} - c4 g_{j,i})
+  const double2 c4 = make_double2(4.0 + a.kre * a.h2, a.kim * a.h2);
+  double2 w[E];
+  {
+    T lo[E], hi[E];
+    row(J0 - 1, lo);
+    row(J0 + 1, hi);
+    T hi2[E];
+    if constexpr (!CPLX) row(J0 + 3, hi2);
+#pragma unroll
+    for (int m = 0; m < E; ++m) {
+      const int n = t + m * TT;
+      const double2 l = n >= 1 ? sm[n - 1] : make_double2(0.0, 0.0);
+      const double2 rr = n + 1 <= M - 1 ? sm[n + 1] : make_double2(0.0, 0.0);
+      const double2 cc = sm.xc(t, reg::sw(t), m * TT);
+      double2 bg;                                // B g_j at n
+      if constexpr (CPLX) bg = csub(cadd(l, rr), cmul(c4, cc));
+      else bg = make_double2(l.x + rr.x - c4.x * cc.x, l.y + rr.y - c4.x * cc.y);
+      if constexpr (CPLX) {
+        w[m] = csub(cadd(lo[m], hi[m]), bg);
+      } else {
+        w[m] = make_double2(lo[m] + hi[m] - bg.x, hi[m] + hi2[m] - bg.y);
+      }
+      if (n == 0 || !valid) w[m] = make_double2(0.0, 0.0);
+    }
+    if (J0 == 0) {                               // even row 0: the zero ring
+#pragma unroll
+      for (int m = 0; m < E; ++m) w[m].x = 0.0;
+      if constexpr (CPLX) {
+#pragma unroll
+        for (int m = 0; m < E; ++m) w[m].y = 0.0;
+      }
+    }
+  }
+  reg::seq_sync<LOGN>();                         // neighbours read before overwrite
+  stage<LOGN>(sm, w, t);
+  reg::seq_sync<LOGN>();
+  // the odd rows' corrections enter w with coefficient 1; rows sharing a
+  // component are separated by a barrier
+  if (corr.jv) {
+    if (J0 > 0) scatter(J0 - 1, 0, 1.0);
+    if constexpr (!CPLX) scatter(J0 + 3, 1, 1.0);
+    reg::seq_sync<LOGN>();
+    if (J0 > 0) scatter(J0 + 1, 0, 1.0);
+    reg::seq_sync<LOGN>();
+    if constexpr (!CPLX) {
+      scatter(J0 + 1, 1, 1.0);
+      reg::seq_sync<LOGN>();
+    }
+  }
+  double2 out[E];
+  dst_staged<LOGN>(sm, t, a, out);
+  reg::seq_sync<LOGN>();
+  unstage<LOGN>(sm, out, t);
+  reg::seq_sync<LOGN>();
+  if (valid) {
+    const int ts = reg::sw(t);
+    if (!CPLX) {
+      const int n0t = (t & ~3) | ((t & 1) << 1);
+      const int s0 = reg::sw(n0t), s1 = reg::sw(n0t + 1);
+#pragma unroll
+      for (int kk = 0; kk < M / TT; ++kk) {
+        const int i = t + kk * TT;
+        const int pp = i >> 2, part = i & 3, rw = part >> 1;
+        double2 v0, v1;
+        if constexpr (TT % 4 == 0) {
+          v0 = sm.xc(n0t, s0, kk * TT);
+          v1 = sm.xc(n0t + 1, s1, kk * TT);
+        } else {
+          const int n0 = 4 * pp + 2 * (part & 1);
+          v0 = sm[n0];
+          v1 = sm[n0 + 1];
+        }
+        *rows_fwd_dst(a, pp, r0 + rw, part & 1) = rw ? make_double2(v0.y, v1.y) : make_double2(v0.x, v1.x);
+      }
+    } else {
+#pragma unroll
+      for (int kk = 0; kk < M / TT; ++kk) {
+        const int i = t + kk * TT;
+        *rows_fwd_dst(a, i >> 1, r0, i & 1) = sm.xc(t, ts, kk * TT);
+      }
+    }
+  }
+  if constexpr (C::CL > 1) reg::seq_sync<LOGN>();
+}
+
+// ---------------------------------------------------------------------------
+// The odd rows: B u_j = h^2 g_j - u_{j-1} - u_{j+1} along x.  Real data: two
+// odd rows (j, j + 2) per CTA as the two components of a slot; complex: one.
+//
+// B's factored recurrences have the root rho of rho + 1/rho = 4 + kappa h^2:
+// |rho| <= 2 - sqrt(3) = 0.268 whenever Re kappa >= 0 (every FACR kappa), so
+// an element's influence decays below 1e-22 within W = 40 neighbours.  Each
+// thread therefore solves its CH-element chunk on its own: the forward sweep
+// starts W elements before the chunk and the backward sweep W elements after
+// it (exact where the window reaches the ends x = 0 / x = M), with no carries
+// and no scan; the boundary term at x = 0 (rho^n) needs z_1 from thread 0.
+// The right-hand side is formed with coalesced loads into shared memory and
+// the solution leaves the same way (padded: conflict-free chunk accesses).
+constexpr int ODD_W = 40;
+
+template <int LOGM>
+struct OddCfg {
+  static constexpr int M = 1 << LOGM;
+  static constexpr int CH = M >= 512 ? 16 : M / 32;
+  static constexpr int NT = M / CH;
+};
+
+template <int LOGM>
+constexpr size_t odd_smem_bytes() {
+  return ((size_t)(1 << LOGM) + (1 << LOGM) / 16 + 1) * sizeof(double2);
+}
+
+template <bool CPLX, int LOGM>
+__global__ void __launch_bounds__(OddCfg<LOGM>::NT)
+rows_odd_facr(BoxArgs a, const void *__restrict__ rhs, double sign,
+              CorrArgs<typename std::conditional<CPLX, double2, double>::type> corr, void *u) {
+  using T = typename std::conditional<CPLX, double2, double>::type;
+  using S = Sc<T>;
+  constexpr int M = OddCfg<LOGM>::M, CH = OddCfg<LOGM>::CH, NT = OddCfg<LOGM>::NT;
+  extern __shared__ double2 rbuf[];              // rhs then solution, padded by one slot per 16
+  __shared__ double2 z1s;
+  if (a.done && *a.done) return;
+  const int t = threadIdx.x;
+  const int stride = M + 1;
+  const int j = CPLX ? 2 * blockIdx.x + 1 : 4 * blockIdx.x + 1;   // odd row (and j + 2)
+  const double h2 = a.h2;
+  auto pos = [](int n) { return n + (n >> 4); };
+  // rhs_n = h^2 g_j - u_{j-1} - u_{j+1} (u_0 = u_M = 0), coalesced over n = t + NT e
+  auto form = [&](int jj, int comp) {
+    const T *U = static_cast<const T *>(u);
+    const T *Fr = static_cast<const T *>(rhs) + (size_t)jj * stride;
+    const T *Ul = U + (size_t)(jj - 1) * stride, *Uh = U + (size_t)(jj + 1) * stride;
+    const bool hasl = jj - 1 >= 1, hash = jj + 1 <= M - 1;
+    T f[CH], l[CH], hv[CH];                      // every load in flight before any use
+#pragma unroll
+    for (int e = 0; e < CH; ++e) {
+      const int n = t + NT * e;
+      f[e] = rhs ? Fr[n] : S::zero();
+      l[e] = hasl ? Ul[n] : S::zero();
+      hv[e] = hash ? Uh[n] : S::zero();
+    }
+#pragma unroll
+    for (int e = 0; e < CH; ++e) {
+      const int n = t + NT * e;
+      T val = S::sub(S::sub(S::rmul(f[e], sign * h2), l[e]), hv[e]);
+      if (n == 0) val = S::zero();
+      if constexpr (CPLX) rbuf[pos(n)] = val;
+      else reinterpret_cast<double *>(&rbuf[pos(n)])[comp] = val;
+    }
+  };
+  form(j, 0);
+  if constexpr (!CPLX) form(j + 2, 1);
+  __syncthreads();
+  if (corr.jv) {                                 // corrections of the row(s), h^2 scaled:
+    for (int k2 = 0; k2 < (CPLX ? 1 : 2); ++k2) {  // distinct nodes, one thread each
+      const int jj = j + 2 * k2;
+      const int g0 = corr.row_group[jj], g1 = corr.row_group[jj + 1];
+      for (int g = g0 + t; g < g1; g += NT) {
+        const int i = corr.group_node[g] - jj * stride;
+        const T cv = S::rmul(group_correction<T>(corr, g), h2);
+        if constexpr (CPLX) rbuf[pos(i)] = cadd(rbuf[pos(i)], cv);
+        else reinterpret_cast<double *>(&rbuf[pos(i)])[k2] += cv;
+      }
+      __syncthreads();
+    }
+  }
+  __syncthreads();
+  // this thread's chunk [s, s + CH) with windows
+  const double2 r = tri::root_cplx(make_double2(a.tb_re, a.tb_im));   // rho (imag 0 for real kappa)
+  double2 rr;                                    // the slot multiplier
+  if constexpr (CPLX) rr = r;
+  else rr = make_double2(r.x, r.x);
+  const int s0 = t * CH;
+  const int lo = s0 - ODD_W < 1 ? 1 : s0 - ODD_W;               // exact start at x = 1 (v_0 = 0)
+  const int hi = s0 + CH + ODD_W > M - 1 ? M - 1 : s0 + CH + ODD_W;  // exact end at x = M - 1 (z_M = 0)
+  // forward v_n = rho v_{n-1} - rhs_n over [lo, hi]: v kept on the chunk; after
+  // it only z at the chunk end, z_end = sum_{n >= end} rho^{n - end} v_n
+  double2 zch[CH];
+  double2 v = make_double2(0.0, 0.0);
+#pragma unroll 8
+  for (int n = lo; n < s0; ++n) v = tri::mad<CPLX>(rr, v, cneg(rbuf[pos(n)]));
+#pragma unroll
+  for (int e = 0; e < CH; ++e) {
+    const int n = s0 + e;
+    if (n >= 1) v = tri::mad<CPLX>(rr, v, cneg(rbuf[pos(n)]));
+    zch[e] = v;                                  // n = 0: v_0 = 0
+  }
+  double2 z = make_double2(0.0, 0.0), pw1 = tri::one<CPLX>();
+#pragma unroll 8
+  for (int n = s0 + CH; n <= hi; ++n) {
+    v = tri::mad<CPLX>(rr, v, cneg(rbuf[pos(n)]));
+    z = tri::mad<CPLX>(pw1, v, z);
+    pw1 = tri::mul<CPLX>(pw1, rr);
+  }
+  // backward z_n = rho z_{n+1} + v_n through the chunk (in place)
+#pragma unroll
+  for (int e = CH - 1; e >= 0; --e) {
+    z = tri::mad<CPLX>(rr, z, zch[e]);
+    zch[e] = z;
+  }
+  if (t == 0) z1s = zch[CH > 1 ? 1 : 0];          // z_1 (CH >= 2 always here)
+  __syncthreads();                               // rhs reads done; z_1 visible
+  // y_n = rho z_n + B rho^n, B = -rho^2 z_1 (rho^{2M} terms < 1e-300)
+  const double2 Bc = cneg(tri::mul<CPLX>(tri::mul<CPLX>(rr, rr), z1s));
+  double2 pw = tri::pw<CPLX>(rr, s0);            // rho^n
+#pragma unroll
+  for (int e = 0; e < CH; ++e) {
+    const double2 y = tri::mad<CPLX>(Bc, pw, tri::mul<CPLX>(rr, zch[e]));
+    rbuf[pos(s0 + e)] = y;
+    pw = tri::mul<CPLX>(pw, rr);
+  }
+  __syncthreads();
+  T *U = static_cast<T *>(u);
+#pragma unroll
+  for (int e = 0; e < CH; ++e) {
+    const int n = t + NT * e;
+    const double2 y = rbuf[pos(n)];
+    if constexpr (CPLX) {
+      U[(size_t)j * stride + n] = n >= 1 ? y : S::zero();
+    } else {
+      U[(size_t)j * stride + n] = n >= 1 ? y.x : 0.0;
+      U[(size_t)(j + 2) * stride + n] = n >= 1 ? y.y : 0.0;
+    }
+  }
+  if (t == 0) {                                  // x = M: the zero ring column
+    U[(size_t)j * stride + M] = S::zero();
+    if constexpr (!CPLX) U[(size_t)(j + 2) * stride + M] = S::zero();
+  }
+  // the zero ring row M, written by the CTA of the last odd row
+  const int last = CPLX ? M - 1 : M - 3;
+  if (j == last)
+    for (int i = t; i <= M; i += NT) U[(size_t)M * stride + i] = S::zero();
+}
+
+}  // namespace kfbi

@@ -12,6 +12,13 @@ struct BoxArgs {
   double kre, kim;        // kappa
   double inv4m2;          // 1 / (4 m^2), exact power of two
   double h2;              // h^2 (tridiagonal column pass, box_tri.cuh)
+  // cyclic-reduction (FACR) form of the box solve, box_tri.cuh / box_facr.cuh:
+  int red;                // column stage on the even-row system (root r^2)
+  int trow;               // recurrence along x of one grid row (odd rows)
+  int row_step;           // grid rows per slab row of the inverse row pass (1, or 2)
+  double tb_re, tb_im;    // trow: beta - 1 of the x recurrence (1 + kappa h^2 / 2)
+  double tscale;          // trow: output scale (1)
+  void *gsum;             // scratch for the group sums (n_groups slots of 16 bytes)
   void *panels;
   const int *done;        // early-exit flag (Richardson sweeps), may be null
   const double2 *twg;     // [m] exp(-2 pi i q / m)        (register engine)
@@ -50,6 +57,7 @@ struct CorrArgs {
   const int *rec_edge;
   const double *rec_d;
   const double *rec_sigma;
+  const T *cval = nullptr;  // precomputed group sums (the FACR passes), or null
 };
 
 // Correction at one irregular node: sum over its arm records, in record
@@ -57,6 +65,7 @@ struct CorrArgs {
 template <typename T>
 KFBI_DEV T group_correction(const CorrArgs<T> &c, int g) {
   using S = Sc<T>;
+  if (c.cval) return c.cval[g];
   const int r0 = c.group_start[g], r1 = c.group_start[g + 1];
   T acc = S::zero();
   for (int r = r0; r < r1; ++r) {
@@ -68,6 +77,15 @@ KFBI_DEV T group_correction(const CorrArgs<T> &c, int g) {
     acc = (r == r0) ? v : S::add(acc, v);
   }
   return acc;
+}
+
+// The group sums into a compact array (the FACR passes read each one once
+// instead of re-walking the records in every thread that needs it).
+template <typename T>
+__global__ void __launch_bounds__(256) group_sums_kernel(CorrArgs<T> c, int m, T *out) {
+  const int n_groups = c.row_group[m + 1];
+  for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < n_groups; g += gridDim.x * blockDim.x)
+    out[g] = group_correction<T>(c, g);
 }
 
 // Dense scatter of the group sums (the standalone corrections() API).

@@ -7,6 +7,7 @@
 #include "box_neu.cuh"
 #include "box_real.cuh"
 #include "box_tri.cuh"
+#include "box_facr.cuh"
 
 namespace kfbi {
 
@@ -59,6 +60,72 @@ kfbi_status cols_tri_launch(kfbi_plan *p, const BoxArgs &a, cudaStream_t s) {
 #endif
   const int grid = Tc::NH == 2 ? a.npl : 2 * a.npl;
   return kfbi_launch(p, KFBI_K_COLS, s, [&] { cols_tri<CPLX, LOGN><<<grid, Tc::THREADS, 0, s>>>(a); });
+}
+
+// FACR(1) box solve (box_facr.cuh) of one (dtype, log2 M), one slab.
+template <bool CPLX, int LOGN>
+kfbi_status box_facr_launch(kfbi_plan *p, const BoxArgs &a0, const void *rhs, double sign,
+                            const CorrArgs<typename std::conditional<CPLX, double2, double>::type> &c,
+                            void *u, cudaStream_t s) {
+  if constexpr (LOGN < 6 || LOGN > 13) {
+    return kfbi_fail(KFBI_E_CONFIG, "FACR box solve: 64 <= M <= 8192");
+  } else {
+    using Cf = reg::Cfg<LOGN>;
+    using CT = typename std::conditional<CPLX, double2, double>::type;
+    constexpr int M = 1 << LOGN;
+    static bool attr = false;
+    if (!attr) {
+      const int bytes = (int)reg::smem_bytes<LOGN>();
+      KFBI_CUDA(cudaFuncSetAttribute(rows_fwd_facr<CPLX, LOGN>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, bytes), "transform-rows");
+      KFBI_CUDA(cudaFuncSetAttribute(rows_inv_reg<CPLX, LOGN>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, bytes), "transform-rows");
+      attr = true;
+    }
+    // the group sums once (every FACR pass reads each correction several times)
+    CorrArgs<CT> cc = c;
+    if (c.jv && a0.gsum) {
+      CT *gs = static_cast<CT *>(a0.gsum);
+      KFBI_TRY(kfbi_launch(p, KFBI_K_JUMPS, s, [&] {
+        group_sums_kernel<CT><<<148 * 2, 256, 0, s>>>(c, M, gs);
+      }));
+      cc.cval = gs;
+    }
+    BoxArgs a = a0;
+    a.rows = M / 2;                                 // the even rows
+    a.npl = CPLX ? M / 2 : M / 4;
+    a.ring_end = 0;                                 // row M: written by the odd-row pass
+    const int nseq = CPLX ? M / 2 : M / 4;
+    const int grow = Cf::CL > 1 ? nseq * Cf::CL : (nseq + Cf::S - 1) / Cf::S;
+    KFBI_TRY(kfbi_launch(p, KFBI_K_ROWS, s, [&] {
+      return reg_launch<LOGN>(rows_fwd_facr<CPLX, LOGN>, grow, s, a, rhs, sign, cc);
+    }));
+    BoxArgs ar = a;
+    ar.red = 1;
+    KFBI_TRY((cols_tri_launch<CPLX, LOGN - 1>(p, ar, s)));
+    BoxArgs ai = a;
+    ai.row_step = 2;
+    KFBI_TRY(kfbi_launch(p, KFBI_K_ROWS, s, [&] {
+      return reg_launch<LOGN>(rows_inv_reg<CPLX, LOGN>, grow, s, ai, u);
+    }));
+    BoxArgs ao = a0;
+    ao.trow = 1;
+    ao.tb_re = 1.0 + 0.5 * a0.kre * a0.h2;          // beta - 1, beta = 2 + kappa h^2 / 2
+    ao.tb_im = 0.5 * a0.kim * a0.h2;
+    ao.tscale = 1.0;
+    using Rc = OddCfg<LOGN>;
+    const int nodd = CPLX ? M / 2 : M / 4;
+    constexpr size_t osm = odd_smem_bytes<LOGN>();
+    static bool oattr = false;
+    if (!oattr && osm > 48 * 1024) {
+      KFBI_CUDA(cudaFuncSetAttribute(rows_odd_facr<CPLX, LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)osm), "diagonal-scale");
+      oattr = true;
+    }
+    return kfbi_launch(p, KFBI_K_SCALE, s, [&] {
+      rows_odd_facr<CPLX, LOGN><<<nodd, Rc::NT, osm, s>>>(ao, rhs, sign, cc, u);
+    });
+  }
 }
 
 // Register-engine passes for one (dtype, log2 M); `passes` selects any of
@@ -130,9 +197,23 @@ kfbi_status box_real_launch(kfbi_plan *p, bool tri, const BoxArgs &a, const void
 }
 
 template <bool CPLX>
+kfbi_status box_facr_switch(kfbi_plan *p, int logm, const BoxArgs &a, const void *rhs, double sign,
+                            const CorrArgs<typename std::conditional<CPLX, double2, double>::type> &c,
+                            void *u, cudaStream_t s) {
+  switch (logm) {
+#define KFBI_CASE(L) \
+    case L: return box_facr_launch<CPLX, L>(p, a, rhs, sign, c, u, s);
+    KFBI_CASE(6) KFBI_CASE(7) KFBI_CASE(8) KFBI_CASE(9) KFBI_CASE(10) KFBI_CASE(11) KFBI_CASE(12) KFBI_CASE(13)
+#undef KFBI_CASE
+    default: return kfbi_fail(KFBI_E_CONFIG, "FACR box solve: 64 <= M <= 8192");
+  }
+}
+
+template <bool CPLX>
 kfbi_status box_passes_reg(kfbi_plan *p, int logm, bool tri, const BoxArgs &a, const void *rhs, double sign,
                            const CorrArgs<typename std::conditional<CPLX, double2, double>::type> &c,
                            void *u, cudaStream_t s, int passes = 7) {
+  if (passes == 8) return box_facr_switch<CPLX>(p, logm, a, rhs, sign, c, u, s);   // FACR(1)
   if constexpr (!CPLX) {
     if (logm == 14) return box_real_launch<14>(p, tri, a, rhs, sign, c, u, passes, s);
   }

@@ -330,8 +330,8 @@ rows_inv_reg(BoxArgs a, void *__restrict__ u) {
     const bool last = a.ring_end && q == nseq - 1;   // also write ring row M
     if (!CPLX) {
       double *U = static_cast<double *>(u);
-      double *u0 = U + (size_t)r0 * stride;
-      double *u1 = u0 + stride;
+      double *u0 = U + (size_t)r0 * a.row_step * stride;   // row_step 2: FACR even rows
+      double *u1 = u0 + (size_t)a.row_step * stride;
 #pragma unroll
       for (int kk = 0; kk <= M / TT; ++kk) {
         const int n = t + kk * TT;
@@ -348,7 +348,7 @@ rows_inv_reg(BoxArgs a, void *__restrict__ u) {
       }
     } else {
       double2 *U = static_cast<double2 *>(u);
-      double2 *u0 = U + (size_t)r0 * stride;
+      double2 *u0 = U + (size_t)r0 * a.row_step * stride;
 #pragma unroll
       for (int kk = 0; kk <= M / TT; ++kk) {
         const int n = t + kk * TT;

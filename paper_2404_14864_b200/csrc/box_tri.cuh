@@ -160,20 +160,27 @@ struct TriDist {
   unsigned long long *flg[8];                 // [unit][P] of rank h, as mapped here
 };
 
-template <bool CPLX, int LOGM, bool DIST = false>
-KFBI_DEV void tri_solve(double2 (&x)[tri::Cfg<LOGM>::CH], const BoxArgs &a, int pp, int half, int hs,
-                        int chunk, TriSmem<tri::Cfg<LOGM>::NH, tri::Cfg<LOGM>::NW> &sh,
-                        const TriDist *dd = nullptr, int unit = 0, int g = 0) {
-  using C = tri::Cfg<LOGM>;
+template <bool CPLX, class C, bool DIST = false>
+KFBI_DEV void tri_solve_c(double2 (&x)[C::CH], const BoxArgs &a, int pp, int half, int hs, int chunk,
+                          TriSmem<C::NH, C::NW> &sh, const TriDist *dd = nullptr, int unit = 0,
+                          int g = 0) {
   constexpr int CH = C::CH, NH = C::NH, CPW = C::CPW, NW = C::NW, NCH = C::NCH;
   static_assert(2 * NCH < (1 << TRI_NPOW), "power table");
   const int cw = chunk & (CPW - 1);              // chunk index within the warp
   const int wv = chunk / CPW;                    // warp index within the slot
-  // per-column root r
+  // per-column root r (a.trow: one root for the x recurrence of a grid row;
+  // a.red: the even-row system's root r^2)
   const double hh2 = 0.5 * a.h2;
   double2 r;
   int kx0;
-  if constexpr (CPLX) {
+  if (a.trow) {
+    kx0 = 1;
+    if constexpr (CPLX) r = tri::root_cplx(make_double2(a.tb_re, a.tb_im));
+    else {
+      const double rr = tri::root_real(a.tb_re);
+      r = make_double2(rr, rr);
+    }
+  } else if constexpr (CPLX) {
     kx0 = 2 * pp + half;
     r = tri::root_cplx(make_double2((a.kre - a.lam[kx0]) * hh2, a.kim * hh2));
     if (kx0 == 0) r = make_double2(0.0, 0.0);
@@ -182,6 +189,7 @@ KFBI_DEV void tri_solve(double2 (&x)[tri::Cfg<LOGM>::CH], const BoxArgs &a, int 
     r = make_double2(kx0 == 0 ? 0.0 : tri::root_real((a.kre - a.lam[kx0]) * hh2),
                      tri::root_real((a.kre - a.lam[kx0 + 1]) * hh2));
   }
+  if (a.red) r = tri::mul<CPLX>(r, r);
   const double2 zero = make_double2(0.0, 0.0);
 
   // ---- local sweeps (no dependence on other chunks) ------------------------
@@ -360,7 +368,7 @@ KFBI_DEV void tri_solve(double2 (&x)[tri::Cfg<LOGM>::CH], const BoxArgs &a, int 
     __syncthreads();
     z1 = sh.z1s[hs];
   }
-  const double sc = a.h2 / (2.0 * a.m);
+  const double sc = a.trow ? a.tscale : a.h2 / (2.0 * a.m);
   const double2 A = tri::mul<CPLX>(r, CPLX ? make_double2(sc, 0.0) : make_double2(sc, sc));
   const double2 r2m = rc_pow(2 * NT);            // r^{2M}
   double2 B;                                     // -A r z1 / (1 - r^2M)
@@ -409,6 +417,13 @@ KFBI_DEV void tri_solve(double2 (&x)[tri::Cfg<LOGM>::CH], const BoxArgs &a, int 
       else x[i].x = 0.0;
     }
   }
+}
+
+template <bool CPLX, int LOGM, bool DIST = false>
+KFBI_DEV void tri_solve(double2 (&x)[tri::Cfg<LOGM>::CH], const BoxArgs &a, int pp, int half, int hs,
+                        int chunk, TriSmem<tri::Cfg<LOGM>::NH, tri::Cfg<LOGM>::NW> &sh,
+                        const TriDist *dd = nullptr, int unit = 0, int g = 0) {
+  tri_solve_c<CPLX, tri::Cfg<LOGM>, DIST>(x, a, pp, half, hs, chunk, sh, dd, unit, g);
 }
 
 template <bool CPLX, int LOGM>

@@ -128,8 +128,10 @@ struct kfbi_plan {
   DevBuf<GmresState> gm_st;
   // stencil nodes grouped by grid row (trace-only sweep 1 of the operator form)
   DevBuf<int> sn_rows, sn_rowptr, sn_cols, sn_map;
+  DevBuf<double2> gsum;             // group sums of the FACR passes
   int sn_nrows = 0, sn_nodes = 0;
   bool trace_sweep = false;         // kfbi_plan_set_trace_sweep (opt-in: measured no gain)
+  bool facr = true;                 // kfbi_plan_set_facr: cyclic-reduction box solve
   DevBuf<double2> sn_vals, sn_v13;
   DevBuf<int> skip;
   DevBuf<StepLog> log;
@@ -225,6 +227,12 @@ BoxArgs box_args(kfbi_plan *p, double kre, double kim, const int *done) {
   a.kim = kim;
   a.inv4m2 = 1.0 / (4.0 * (double)p->m * (double)p->m);
   a.h2 = p->h * p->h;
+  a.red = 0;
+  a.trow = 0;
+  a.row_step = 1;
+  a.tb_re = a.tb_im = 0.0;
+  a.tscale = 1.0;
+  a.gsum = p->gsum.p;
   a.panels = p->panels.p;
   a.done = done;
   a.twg = p->twg.p;
@@ -328,6 +336,11 @@ kfbi_status box_passes_reg(kfbi_plan *p, const BoxArgs &a, const void *rhs, doub
                            const CorrArgs<typename std::conditional<CPLX, double2, double>::type> &c,
                            void *u, cudaStream_t s, int passes = 7) {
   const bool tri = col_use_tri(p, a.kre, a.kim);
+  // one level of cyclic reduction (box_facr.cuh): half the row transforms;
+  // single slab, full solve, tridiagonal-eligible kappa, 64 <= M <= 8192
+  if (passes == 7 && tri && p->facr && a.nranks == 1 && !a.dst[0] && a.rows == p->m && p->m >= 64 &&
+      p->m <= 8192)
+    passes = 8;
   if constexpr (CPLX) return box_dirichlet_c128(p, p->logm, tri, a, rhs, sign, c, u, s, passes);
   else return box_dirichlet_f64(p, p->logm, tri, a, rhs, sign, c, u, s, passes);
 }
@@ -1009,6 +1022,10 @@ kfbi_status kfbi_plan_create(const kfbi_grid_desc *desc, kfbi_plan **out) {
   p->m = m;
   p->logm = ilog2(m);
   p->h = desc->h;
+  {
+    const char *f = std::getenv("KFBI_FACR");      // "0": three-pass box solves by default
+    if (f && f[0] == '0') p->facr = false;
+  }
   cudaError_t e = cudaSetDevice(p->device);
   if (e != cudaSuccess) {
     delete p;
@@ -1370,6 +1387,7 @@ kfbi_status kfbi_plan_set_geometry(kfbi_plan *p, const kfbi_geometry *g) {
         (e = p->sn_vals.ensure((size_t)p->sn_nodes)) == cudaSuccess)
       e = p->sn_v13.ensure(13 * (size_t)n);
   }
+  if (e == cudaSuccess) e = p->gsum.ensure((size_t)(g->n_groups > 0 ? g->n_groups : 1));
   if (e == cudaSuccess) e = p->d1.ensure(n);
   if (e == cudaSuccess) e = p->psi_s.ensure(n);
   if (e == cudaSuccess) e = p->jm.ensure(6 * (size_t)n);
@@ -1401,6 +1419,13 @@ kfbi_status kfbi_plan_get_colsolver(kfbi_plan *p, int32_t *mode) {
   KFBI_TRY(check_plan(p));
   if (!mode) return fail(KFBI_E_CONFIG, "null argument");
   *mode = p->col_mode;
+  return KFBI_OK;
+}
+
+kfbi_status kfbi_plan_set_facr(kfbi_plan *p, int32_t on) {
+  KFBI_TRY(check_plan(p));
+  if (p->facr != (on != 0)) p->op_valid = false;   // the trace operator follows the solver
+  p->facr = on != 0;
   return KFBI_OK;
 }
 

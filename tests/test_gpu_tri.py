@@ -80,6 +80,7 @@ def test_tri_large_residual(m):
         torch.cuda.empty_cache()
 
 
+@pytest.mark.usefixtures("_three_pass_reference")
 @pytest.mark.parametrize("p2p", [False, True])
 def test_tri_slab_virtual_ranks_bit_identical(p2p):
     # the slab layout ([rank][panels][rows][w] blocks, or the peer stores of
@@ -175,3 +176,64 @@ def test_slab_carry_richardson(kappa):
     assert it == ref.iterations and solver.passes.peers_ok()
     err = float((u.reshape(-1) - ref.u.reshape(-1)[:m1 * (m1 + 1)]).abs().max()) / float(ref.u.abs().max())
     assert err < 1e-11
+
+
+@pytest.mark.parametrize("m", [64, 256, 1024, 4096, 8192])
+@pytest.mark.parametrize("kappa", [2048.0, 262144.0, 512j])
+def test_facr_box_solve(m, kappa):
+    # one level of cyclic reduction (box_facr.cuh, default where it applies)
+    # against the three-pass solve and the oracle
+    import torch
+
+    grid = k.CartesianGrid(BOX, m)
+    cplx = isinstance(kappa, complex)
+    g = torch.Generator(device="cuda").manual_seed(m + 3)
+    dt = torch.complex128 if cplx else torch.float64
+    rhs = torch.randn((m + 1, m + 1), generator=g, device="cuda", dtype=dt)
+    s = k.BoxSolver(grid, kappa, "dirichlet-zero")
+    u_f = s.solve(rhs)
+    s.plan.set_facr(False)
+    try:
+        u_3 = s.solve(rhs)
+    finally:
+        s.plan.set_facr(True)
+    scale = float(u_3.abs().max())
+    assert float((u_f - u_3).abs().max()) / scale < 1e-12
+    for edge in (u_f[0], u_f[-1], u_f[:, 0], u_f[:, -1]):
+        assert bool((edge == 0).all())
+    if m <= 1024:
+        ref = O.box_solve(m, grid.h, kappa, rhs.cpu().numpy())
+        assert rel_linf(u_f.cpu().numpy(), ref) < 1e-11
+
+
+def test_facr_richardson_same_iterations():
+    # the Richardson solve through the FACR box solve (corrections on even and
+    # odd rows): same sweeps and field as the three-pass solve
+    geo = k.build_grid(BOX, 1024, k.StarCurve(1.0, c=0.2, lobes=8))
+    ws = k.InterfaceWorkspace(geo)
+    sol = k.StaticPlaneWave(kappa=2048.0)
+    cps = ws.cps
+    F = np.where(geo.classification.interior, sol.f(geo.grid.X, geo.grid.Y), 0.0)
+    prob = k.BvpProblem(kappa=2048.0, F=F, f_gamma=sol.f(cps.x, cps.y), bc_kind="dirichlet",
+                        bc_values=sol.dirichlet(cps.x, cps.y))
+    a = k.richardson_solve(prob, ws)
+    ws.plan.set_facr(False)
+    try:
+        b = k.richardson_solve(prob, ws)
+    finally:
+        ws.plan.set_facr(True)
+    assert a.iterations == b.iterations
+    assert rel_linf(a.u, b.u) < 1e-12
+
+
+@pytest.fixture
+def _three_pass_reference(monkeypatch):
+    # bit-identity with the slab passes is defined against the three-pass
+    # one-GPU box solve (the FACR form is compared to rounding in
+    # test_gpu_tri.py::test_facr_*); plans created here start with FACR off
+    from paper_2404_14864_b200 import boxsolve
+
+    monkeypatch.setenv("KFBI_FACR", "0")
+    boxsolve._GRID_PLANS.clear()
+    yield
+    boxsolve._GRID_PLANS.clear()

@@ -319,3 +319,16 @@ def test_slab_richardson_virtual_bit_identical(m, kappa):
     assert it == ref.iterations and solver.passes.peers_ok()
     assert torch.equal(u.reshape(-1), ref.u.reshape(-1)[:m1 * (m1 + 1)])
     assert torch.equal(dens, ref.density)
+
+
+@pytest.fixture(autouse=True)
+def _three_pass_reference(monkeypatch):
+    # bit-identity with the slab passes is defined against the three-pass
+    # one-GPU box solve (the FACR form is compared to rounding in
+    # test_gpu_tri.py::test_facr_*); plans created here start with FACR off
+    from paper_2404_14864_b200 import boxsolve
+
+    monkeypatch.setenv("KFBI_FACR", "0")
+    boxsolve._GRID_PLANS.clear()
+    yield
+    boxsolve._GRID_PLANS.clear()
