@@ -323,13 +323,21 @@ def run_ours(args):
         c.flush()
     # per-kernel device times over the timed region
     kt_ms, kt_calls = {}, {}
-    # box-solve passes: algorithmic bytes 2 (M-1)^2 s per launch
-    pas = {n: {"bytes": 0.0, "ms": 0.0, "calls": 0} for n in ("transform-rows", "transform-cols")}
+    # box-solve passes, algorithmic bytes per launch in units of (M-1)^2 s
+    # (SURVEY §8(d)): three-pass solve 2 per row pass and 2 for the column
+    # stage; FACR(1) rows_fwd 1.5 / rows_inv 1 (average 1.25 over
+    # the alternating launches), column stage 1 (M/2 rows), odd rows 1.5
+    pas = {n: {"bytes": 0.0, "ms": 0.0, "calls": 0}
+           for n in ("transform-rows", "transform-cols", "diagonal-scale")}
     for eq, c in ctxs.items():
         ms, calls = c.plan.kernel_times()
         cplx = eq == "schrodinger"
+        unit = _bytes_cols(m, cplx) / 2.0
+        facr = c.plan.facr_for(kappas[eq])
+        per = ({"transform-rows": 1.25, "transform-cols": 1.0, "diagonal-scale": 1.5} if facr
+               else {"transform-rows": 2.0, "transform-cols": 2.0, "diagonal-scale": 0.0})
         for n in pas:
-            pas[n]["bytes"] += calls[n] * _bytes_cols(m, cplx)
+            pas[n]["bytes"] += calls[n] * per[n] * unit
             pas[n]["ms"] += ms[n]
             pas[n]["calls"] += calls[n]
         for name in ms:
@@ -459,14 +467,17 @@ def run_ours(args):
     peaks = _peaks()
     traffic = _ncu_traffic() or {}
     roof = {}
+    pas = {n: v for n, v in pas.items() if v["calls"]}
     for n, v in pas.items():
         avg = v["ms"] / max(v["calls"], 1)
         ach = (v["bytes"] / max(v["calls"], 1)) / (avg / 1e3) / 1e9 if v["calls"] else 0.0
         roof[n] = {"achieved": ach, "frac": ach / peaks["hbm_gbs"], "avg_launch_ms": avg,
                    "launches": v["calls"], "ms_per_bench_step": v["ms"] / args.steps}
     dom = max(pas, key=lambda n: pas[n]["ms"])     # the dominant kernel of the step
-    kernel_name = {"transform-rows": "rows_fwd_reg / rows_inv_reg (DST-I along x, transform-rows)",
-                   "transform-cols": "cols_tri (tridiagonal column solves, transform-cols)"}
+    kernel_name = {"transform-rows": "rows_fwd_facr / rows_inv_reg (DST-I along x of the even rows, "
+                                     "transform-rows)",
+                   "transform-cols": "cols_tri (tridiagonal column solves, transform-cols)",
+                   "diagonal-scale": "rows_odd_facr (odd rows by x recurrences)"}
     line = {
         "metric": METRIC,
         "value": value,
@@ -491,8 +502,9 @@ def run_ours(args):
             "unit": "GB/s", "frac": roof[dom]["frac"],
             "traffic": traffic.get(dom),
             "peak_source": peaks["source"],
-            "algorithmic_bytes_per_launch": {"f64": _bytes_cols(m, False),
-                                             "c128": _bytes_cols(m, True)},
+            "algorithmic_bytes_per_launch": "transform-rows under FACR(1): 1.5 (forward) / 1.0 "
+                                            "(inverse) x (M-1)^2 s, averaged over the alternating "
+                                            "launches; three-pass: 2 (M-1)^2 s",
             "avg_launch_ms": roof[dom]["avg_launch_ms"],
             "per_pass": roof,
         },

@@ -203,6 +203,8 @@ kfbi_status kfbi_plan_set_trace_sweep(kfbi_plan *plan, int32_t on);
  * sweeps of HBM.  Default on (environment KFBI_FACR=0 at plan creation: off);
  * 0 restores the three-pass solve. */
 kfbi_status kfbi_plan_set_facr(kfbi_plan *plan, int32_t on);
+/* 1 when a single-slab dirichlet box solve with this kappa uses FACR(1). */
+kfbi_status kfbi_plan_facr_for(kfbi_plan *plan, double kappa_re, double kappa_im, int32_t *on);
 kfbi_status kfbi_plan_colsolver_for(kfbi_plan *plan, double kappa_re, double kappa_im,
                                     int32_t *tridiagonal, double *bound);
 

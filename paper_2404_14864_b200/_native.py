@@ -132,6 +132,7 @@ _SIGNATURES = {
     "kfbi_plan_set_colsolver": ([vp, i32], i32),
     "kfbi_plan_set_trace_sweep": ([vp, i32], i32),
     "kfbi_plan_set_facr": ([vp, i32], i32),
+    "kfbi_plan_facr_for": ([vp, C.c_double, C.c_double, C.POINTER(i32)], i32),
     "kfbi_operator_max_controls": ([vp, C.POINTER(i32)], i32),
     "kfbi_plan_colsolver_for": ([vp, C.c_double, C.c_double, C.POINTER(i32), C.POINTER(C.c_double)], i32),
     "kfbi_plan_get_colsolver": ([vp, C.POINTER(i32)], i32),

@@ -134,6 +134,13 @@ class Plan:
         (kfbi_plan_set_facr, default on where it applies)."""
         N.check(self._lib.kfbi_plan_set_facr(self.handle, int(bool(on))))
 
+    def facr_for(self, kappa):
+        """True when a single-slab dirichlet box solve with kappa uses FACR(1)."""
+        kappa = complex(kappa)
+        v = C.c_int32(0)
+        N.check(self._lib.kfbi_plan_facr_for(self.handle, kappa.real, kappa.imag, C.byref(v)))
+        return bool(v.value)
+
     def set_trace_sweep(self, on):
         """Operator form, Dirichlet: sweep 1 forms only its trace (stencil
         nodes) instead of the whole field (kfbi_plan_set_trace_sweep)."""

@@ -242,7 +242,7 @@ constexpr size_t odd_smem_bytes() {
 }
 
 template <bool CPLX, int LOGM>
-__global__ void __launch_bounds__(OddCfg<LOGM>::NT)
+__global__ void __launch_bounds__(OddCfg<LOGM>::NT, OddCfg<LOGM>::NT <= 256 ? 2 : 1)
 rows_odd_facr(BoxArgs a, const void *__restrict__ rhs, double sign,
               CorrArgs<typename std::conditional<CPLX, double2, double>::type> corr, void *u) {
   using T = typename std::conditional<CPLX, double2, double>::type;

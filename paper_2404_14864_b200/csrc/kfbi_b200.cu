@@ -1429,6 +1429,13 @@ kfbi_status kfbi_plan_set_facr(kfbi_plan *p, int32_t on) {
   return KFBI_OK;
 }
 
+kfbi_status kfbi_plan_facr_for(kfbi_plan *p, double kre, double kim, int32_t *on) {
+  KFBI_TRY(check_plan(p));
+  if (!on) return fail(KFBI_E_CONFIG, "null argument");
+  *on = (p->facr && col_use_tri(p, kre, kim) && p->m >= 64 && p->m <= 8192) ? 1 : 0;
+  return KFBI_OK;
+}
+
 kfbi_status kfbi_plan_set_trace_sweep(kfbi_plan *p, int32_t on) {
   KFBI_TRY(check_plan(p));
   p->trace_sweep = on != 0;

@@ -10,13 +10,16 @@ import json
 import sys
 
 dst, srcs = sys.argv[1], sys.argv[2:]
-acc = {"transform-rows": {"f64": [], "c128": []}, "transform-cols": {"f64": [], "c128": []}}
+acc = {"transform-rows": {"f64": [], "c128": []}, "transform-cols": {"f64": [], "c128": []},
+       "diagonal-scale": {"f64": [], "c128": []}}
 for src in srcs:
     for ks in json.load(open(src)).values():
         for k in ks:
             name = k["kernel"]
-            if "rows_fwd_reg" in name or "rows_inv_reg" in name:
+            if "rows_fwd_reg" in name or "rows_inv_reg" in name or "rows_fwd_facr" in name:
                 pas = "transform-rows"
+            elif "rows_odd_facr" in name:
+                pas = "diagonal-scale"
             elif "cols_tri" in name or "cols_reg" in name:
                 pas = "transform-cols"
             else:
