@@ -132,11 +132,26 @@ rows_fwd_facr(BoxArgs a, const void *__restrict__ rhs, double sign,
   const double2 c4 = make_double2(4.0 + a.kre * a.h2, a.kim * a.h2);
   double2 w[E];
   {
-    T lo[E], hi[E];
-    row(J0 - 1, lo);
-    row(J0 + 1, hi);
-    T hi2[E];
-    if constexpr (!CPLX) row(J0 + 3, hi2);
+    // g_{j-1} + g_{j+1} summed as loaded (one register set for the odd rows)
+    double2 os[E];
+    {
+      const T *R = static_cast<const T *>(rhs);
+      const bool ok = valid && rhs != nullptr;
+#pragma unroll
+      for (int m = 0; m < E; ++m) {
+        const int n = t + m * TT;
+        const bool nn = ok && n >= 1;
+        auto ld = [&](int j) -> T {
+          return (nn && j >= 1 && j <= M - 1) ? R[(size_t)j * stride + n] : S::zero();
+        };
+        if constexpr (CPLX) {
+          os[m] = cscale(cadd(ld(J0 - 1), ld(J0 + 1)), sign);
+        } else {
+          const double mid = ld(J0 + 1);
+          os[m] = make_double2((ld(J0 - 1) + mid) * sign, (mid + ld(J0 + 3)) * sign);
+        }
+      }
+    }
 #pragma unroll
     for (int m = 0; m < E; ++m) {
       const int n = t + m * TT;
@@ -146,11 +161,7 @@ rows_fwd_facr(BoxArgs a, const void *__restrict__ rhs, double sign,
       double2 bg;                                // B g_j at n
       if constexpr (CPLX) bg = csub(cadd(l, rr), cmul(c4, cc));
       else bg = make_double2(l.x + rr.x - c4.x * cc.x, l.y + rr.y - c4.x * cc.y);
-      if constexpr (CPLX) {
-        w[m] = csub(cadd(lo[m], hi[m]), bg);
-      } else {
-        w[m] = make_double2(lo[m] + hi[m] - bg.x, hi[m] + hi2[m] - bg.y);
-      }
+      w[m] = csub(os[m], bg);
       if (n == 0 || !valid) w[m] = make_double2(0.0, 0.0);
     }
     if (J0 == 0) {                               // even row 0: the zero ring
