@@ -216,16 +216,26 @@ def run_ours(args):
     backend = k.CudaBackend(local, timing=False)
     ctxs, specs, states, steppers = {}, {}, {}, {}
     kappas, op_build_s, startups = {}, {}, {}
+    setup_parts = {}
     t_setup = time.time()
     for eq in eqs:
         box, curve, kw = wl[eq]
+        part = {}
+        t_p = time.perf_counter()
         geo = k.build_grid(box, m, curve)
+        part["build_grid"] = time.perf_counter() - t_p
+        t_p = time.perf_counter()
         ctxs[eq] = k.StepContext(geo, backend=backend, operator=not args.pipeline)
         specs[eq] = k.ProblemSpec(**kw)
         startup, step = _stepper_for(specs[eq])
         steppers[eq] = step
         startups[eq] = startup
+        part["context"] = time.perf_counter() - t_p
+        t_p = time.perf_counter()
         states[eq] = startup(specs[eq], ctxs[eq])
+        torch.cuda.synchronize()
+        part["startup"] = time.perf_counter() - t_p
+        setup_parts[eq] = part
         kap = {"heat": 2.0 * specs[eq].c / specs[eq].tau,
                "wave": 1.0 / (specs[eq].theta * specs[eq].tau ** 2),
                "schrodinger": 2j / specs[eq].tau}[eq]
@@ -514,6 +524,7 @@ def run_ours(args):
         "gpu_launches": int(launches),
         "clocks": clocks,
         "setup_s": t_setup,
+        "setup_parts_s": setup_parts,
         "sweep_mode": "pipeline" if args.pipeline else
         "operator (sweep 1 + returned field by the full pipeline, sweeps >= 2 via the trace operator)",
         "repeats": {"n": args.repeats, "ms_per_step": [r / args.steps for r in reps_ms],

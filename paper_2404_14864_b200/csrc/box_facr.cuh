@@ -24,6 +24,7 @@
 #pragma once
 
 #include "box_reg.cuh"
+#include "box_real.cuh"
 #include "box_tri.cuh"
 
 namespace kfbi {
@@ -372,6 +373,185 @@ rows_odd_facr(BoxArgs a, const void *__restrict__ rhs, double sign,
   const int last = CPLX ? M - 1 : M - 3;
   if (j == last)
     for (int i = t; i <= M; i += NT) U[(size_t)M * stride + i] = S::zero();
+}
+
+}  // namespace kfbi
+
+namespace kfbi {
+
+// ---------------------------------------------------------------------------
+// FACR(1) for REAL data at M = 16384 on the one-real-row-per-CTA engine of
+// box_real.cuh (length-8192 complex FFT with the real split).
+
+// even grid row j = 2 r0 (r0 = blockIdx.x, reduced row): w_j = g_{j-1} +
+// g_{j+1} - B g_j, staged as pairs (x_2q, x_2q+1), then the real DST-I
+template <int LOGN>
+__global__ void __launch_bounds__(reg::Cfg<LOGN - 1>::CTA_T, 1)
+rows_fwd_facr_real(BoxArgs a, const double *__restrict__ rhs, double sign, CorrArgs<double> corr) {
+  constexpr int LOGL = LOGN - 1;
+  using C = reg::Cfg<LOGL>;
+  static_assert(C::S == 1 && C::CL == 1, "one sequence per CTA");
+  constexpr int M = 1 << LOGN, L = C::N, TT = C::T, E = reg::E;
+  extern __shared__ double2 smem[];
+  if (a.done && *a.done) return;
+  int seq, t;
+  const reg::View<LOGL> sm = reg::make_view<LOGL>(smem, seq, t);
+  const int stride = M + 1;
+  const int r0 = blockIdx.x;                     // reduced (even) row
+  const int j = 2 * r0;                          // grid row
+  auto ldrow = [&](int jj, int q, double &x0, double &x1) {
+    x0 = x1 = 0.0;
+    if (jj >= 1 && jj <= M - 1 && rhs != nullptr) {
+      const double *row = rhs + (size_t)jj * stride;
+      if (q >= 1) x0 = row[2 * q] * sign;
+      x1 = row[2 * q + 1] * sign;
+    }
+  };
+  auto scatter = [&](int jj) {                   // corrections of grid row jj into the staged pairs
+    if (!corr.jv || jj < 1 || jj > M - 1) return;
+    const int g0 = corr.row_group[jj], g1 = corr.row_group[jj + 1];
+    for (int g = g0 + t; g < g1; g += TT) {
+      const double cv = group_correction<double>(corr, g);
+      const int i = corr.group_node[g] - jj * stride;
+      reinterpret_cast<double *>(&sm[i >> 1])[i & 1] += cv;
+    }
+  };
+  {
+    double2 v[E];
+#pragma unroll
+    for (int m = 0; m < E; ++m) ldrow(j, t + m * TT, v[m].x, v[m].y);
+    stage<LOGL>(sm, v, t);
+  }
+  reg::seq_sync<LOGL>();
+  scatter(j);
+  reg::seq_sync<LOGL>();
+  const double c4 = 4.0 + a.kre * a.h2;
+  double2 w[E];
+#pragma unroll
+  for (int m = 0; m < E; ++m) {
+    const int q = t + m * TT;                    // elements 2q, 2q + 1
+    double l0, l1, h0, h1;
+    ldrow(j - 1, q, l0, l1);
+    ldrow(j + 1, q, h0, h1);
+    const double2 c = sm[q];
+    const double left = q >= 1 ? sm[q - 1].y : 0.0;           // g[2q - 1]
+    const double right = q + 1 < L ? sm[q + 1].x : 0.0;       // g[2q + 2] (g[M] = 0)
+    const double b0 = left + c.y - c4 * c.x;                  // (B g)[2q]
+    const double b1 = c.x + right - c4 * c.y;                 // (B g)[2q + 1]
+    w[m] = make_double2(q >= 1 ? l0 + h0 - b0 : 0.0, l1 + h1 - b1);
+    if (j == 0) w[m] = make_double2(0.0, 0.0);
+  }
+  reg::seq_sync<LOGL>();
+  stage<LOGL>(sm, w, t);
+  reg::seq_sync<LOGL>();
+  if (j > 0) {                                   // odd rows' corrections, one row per barrier
+    scatter(j - 1);
+    reg::seq_sync<LOGL>();
+    scatter(j + 1);
+    reg::seq_sync<LOGL>();
+  }
+  double2 out[E];
+  realdst::dst_staged<LOGL>(sm, t, a, out);
+  reg::seq_sync<LOGL>();
+  unstage<LOGL>(sm, out, t);
+  reg::seq_sync<LOGL>();
+  for (int i = t; i < L; i += TT) *rows_fwd_dst(a, i >> 1, r0, i & 1) = sm[i];
+}
+
+// odd grid row j (one real row per CTA): B u_j = h^2 g_j - u_{j-1} - u_{j+1}
+// by windowed recurrences (|rho| <= 0.268), as rows_odd_facr
+template <int LOGM>
+constexpr size_t odd1_smem_bytes() {
+  return ((size_t)(1 << LOGM) + (1 << LOGM) / 16 + 1) * sizeof(double);
+}
+
+template <int LOGM>
+__global__ void __launch_bounds__(1024, 1)
+rows_odd_facr_real1(BoxArgs a, const double *__restrict__ rhs, double sign, CorrArgs<double> corr,
+                    double *u) {
+  constexpr int M = 1 << LOGM, CH = 16, NT = M / CH;
+  static_assert(NT <= 1024, "one chunk of 16 per thread");
+  extern __shared__ double rb1[];
+  __shared__ double z1s;
+  if (a.done && *a.done) return;
+  const int t = threadIdx.x;
+  const int stride = M + 1;
+  const int j = 2 * blockIdx.x + 1;
+  const double h2 = a.h2;
+  auto pos = [](int n) { return n + (n >> 4); };
+  {
+    const double *Fr = rhs + (size_t)j * stride;
+    const double *Ul = u + (size_t)(j - 1) * stride, *Uh = u + (size_t)(j + 1) * stride;
+    const bool hasl = j - 1 >= 1, hash = j + 1 <= M - 1;
+    double f[CH], l[CH], hv[CH];
+#pragma unroll
+    for (int e = 0; e < CH; ++e) {
+      const int n = t + NT * e;
+      f[e] = rhs ? Fr[n] : 0.0;
+      l[e] = hasl ? Ul[n] : 0.0;
+      hv[e] = hash ? Uh[n] : 0.0;
+    }
+#pragma unroll
+    for (int e = 0; e < CH; ++e) {
+      const int n = t + NT * e;
+      rb1[pos(n)] = n >= 1 ? f[e] * (sign * h2) - l[e] - hv[e] : 0.0;
+    }
+  }
+  __syncthreads();
+  if (corr.jv) {
+    const int g0 = corr.row_group[j], g1 = corr.row_group[j + 1];
+    for (int g = g0 + t; g < g1; g += NT) {
+      const int i = corr.group_node[g] - j * stride;
+      rb1[pos(i)] += group_correction<double>(corr, g) * h2;
+    }
+    __syncthreads();
+  }
+  const double r = tri::root_real(a.tb_re);
+  const int s0 = t * CH;
+  const int lo = s0 - ODD_W < 1 ? 1 : s0 - ODD_W;
+  const int hi = s0 + CH + ODD_W > M - 1 ? M - 1 : s0 + CH + ODD_W;
+  double zc[CH];
+  double v = 0.0;
+#pragma unroll 8
+  for (int n = lo; n < s0; ++n) v = fma(r, v, -rb1[pos(n)]);
+#pragma unroll
+  for (int e = 0; e < CH; ++e) {
+    const int n = s0 + e;
+    if (n >= 1) v = fma(r, v, -rb1[pos(n)]);
+    zc[e] = v;
+  }
+  double z = 0.0, pw1 = 1.0;
+#pragma unroll 8
+  for (int n = s0 + CH; n <= hi; ++n) {
+    v = fma(r, v, -rb1[pos(n)]);
+    z = fma(pw1, v, z);
+    pw1 *= r;
+  }
+#pragma unroll
+  for (int e = CH - 1; e >= 0; --e) {
+    z = fma(r, z, zc[e]);
+    zc[e] = z;
+  }
+  if (t == 0) z1s = zc[1];
+  __syncthreads();
+  const double Bc = -(r * r) * z1s;
+  double pw = 1.0;
+  for (int k = 0; k < s0 && pw != 0.0; ++k) pw *= r;   // r^s0 (underflows to 0 quickly)
+#pragma unroll
+  for (int e = 0; e < CH; ++e) {
+    rb1[pos(s0 + e)] = fma(Bc, pw, r * zc[e]);
+    pw *= r;
+  }
+  __syncthreads();
+  double *urow = u + (size_t)j * stride;
+#pragma unroll
+  for (int e = 0; e < CH; ++e) {
+    const int n = t + NT * e;
+    urow[n] = n >= 1 ? rb1[pos(n)] : 0.0;
+  }
+  if (t == 0) urow[M] = 0.0;
+  if (j == M - 1)
+    for (int i = t; i <= M; i += NT) u[(size_t)M * stride + i] = 0.0;
 }
 
 }  // namespace kfbi

@@ -196,6 +196,56 @@ kfbi_status box_real_launch(kfbi_plan *p, bool tri, const BoxArgs &a, const void
   return KFBI_OK;
 }
 
+// FACR(1) for real data at M = 16384 on the one-real-row engine (box_real.cuh).
+template <int LOGN>
+kfbi_status box_facr_real_launch(kfbi_plan *p, const BoxArgs &a0, const void *rhs, double sign,
+                                 const CorrArgs<double> &c, void *u, cudaStream_t s) {
+  constexpr int LOGL = LOGN - 1, M = 1 << LOGN;
+  static bool attr = false;
+  const int bytes = (int)reg::smem_bytes<LOGL>();
+  constexpr size_t osm = odd1_smem_bytes<LOGN>();
+  if (!attr) {
+    KFBI_CUDA(cudaFuncSetAttribute(rows_fwd_facr_real<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes),
+              "transform-rows");
+    KFBI_CUDA(cudaFuncSetAttribute(rows_inv_real<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes),
+              "transform-rows");
+    KFBI_CUDA(cudaFuncSetAttribute(rows_odd_facr_real1<LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)osm), "diagonal-scale");
+    attr = true;
+  }
+  CorrArgs<double> cc = c;
+  if (c.jv && a0.gsum) {
+    double *gs = static_cast<double *>(a0.gsum);
+    KFBI_TRY(kfbi_launch(p, KFBI_K_JUMPS, s, [&] { group_sums_kernel<double><<<148 * 2, 256, 0, s>>>(c, M, gs); }));
+    cc.cval = gs;
+  }
+  BoxArgs a = a0;
+  a.rows = M / 2;
+  a.npl = M / 4;
+  a.ring_end = 0;
+  constexpr int CT = reg::Cfg<LOGL>::CTA_T;
+  KFBI_TRY(kfbi_launch(p, KFBI_K_ROWS, s, [&] {
+    rows_fwd_facr_real<LOGN><<<M / 2, CT, bytes, s>>>(a, static_cast<const double *>(rhs), sign, cc);
+  }));
+  BoxArgs ar = a;
+  ar.red = 1;
+  KFBI_TRY((cols_tri_launch<false, LOGN - 1>(p, ar, s)));
+  BoxArgs ai = a;
+  ai.row_step = 2;
+  KFBI_TRY(kfbi_launch(p, KFBI_K_ROWS, s, [&] {
+    rows_inv_real<LOGN><<<M / 2, CT, bytes, s>>>(ai, static_cast<double *>(u));
+  }));
+  BoxArgs ao = a0;
+  ao.trow = 1;
+  ao.tb_re = 1.0 + 0.5 * a0.kre * a0.h2;
+  ao.tb_im = 0.0;
+  ao.tscale = 1.0;
+  return kfbi_launch(p, KFBI_K_SCALE, s, [&] {
+    rows_odd_facr_real1<LOGN><<<M / 2, M / 16, osm, s>>>(ao, static_cast<const double *>(rhs), sign, cc,
+                                                         static_cast<double *>(u));
+  });
+}
+
 template <bool CPLX>
 kfbi_status box_facr_switch(kfbi_plan *p, int logm, const BoxArgs &a, const void *rhs, double sign,
                             const CorrArgs<typename std::conditional<CPLX, double2, double>::type> &c,
@@ -205,7 +255,10 @@ kfbi_status box_facr_switch(kfbi_plan *p, int logm, const BoxArgs &a, const void
     case L: return box_facr_launch<CPLX, L>(p, a, rhs, sign, c, u, s);
     KFBI_CASE(6) KFBI_CASE(7) KFBI_CASE(8) KFBI_CASE(9) KFBI_CASE(10) KFBI_CASE(11) KFBI_CASE(12) KFBI_CASE(13)
 #undef KFBI_CASE
-    default: return kfbi_fail(KFBI_E_CONFIG, "FACR box solve: 64 <= M <= 8192");
+    case 14:
+      if constexpr (!CPLX) return box_facr_real_launch<14>(p, a, rhs, sign, c, u, s);
+      return kfbi_fail(KFBI_E_CONFIG, "FACR box solve: complex data at M = 16384 not supported");
+    default: return kfbi_fail(KFBI_E_CONFIG, "FACR box solve: 64 <= M <= 8192 (16384 real)");
   }
 }
 

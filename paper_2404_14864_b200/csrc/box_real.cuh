@@ -230,7 +230,7 @@ __global__ void __launch_bounds__(reg::Cfg<LOGN - 1>::CTA_T, 1) rows_inv_real(Bo
   reg::seq_sync<LOGL>();
   unstage<LOGL>(sm, out, t);
   reg::seq_sync<LOGL>();
-  double *urow = u + (size_t)r0 * stride;
+  double *urow = u + (size_t)r0 * a.row_step * stride;   // row_step 2: FACR even rows
   for (int n = t; n <= M; n += TT) {
     double val = 0.0;
     if (j >= 1 && n >= 1 && n < M) {

@@ -339,7 +339,7 @@ kfbi_status box_passes_reg(kfbi_plan *p, const BoxArgs &a, const void *rhs, doub
   // one level of cyclic reduction (box_facr.cuh): half the row transforms;
   // single slab, full solve, tridiagonal-eligible kappa, 64 <= M <= 8192
   if (passes == 7 && tri && p->facr && a.nranks == 1 && !a.dst[0] && a.rows == p->m && p->m >= 64 &&
-      p->m <= 8192)
+      (p->m <= 8192 || (!CPLX && p->m == 16384)))
     passes = 8;
   if constexpr (CPLX) return box_dirichlet_c128(p, p->logm, tri, a, rhs, sign, c, u, s, passes);
   else return box_dirichlet_f64(p, p->logm, tri, a, rhs, sign, c, u, s, passes);
@@ -1432,7 +1432,8 @@ kfbi_status kfbi_plan_set_facr(kfbi_plan *p, int32_t on) {
 kfbi_status kfbi_plan_facr_for(kfbi_plan *p, double kre, double kim, int32_t *on) {
   KFBI_TRY(check_plan(p));
   if (!on) return fail(KFBI_E_CONFIG, "null argument");
-  *on = (p->facr && col_use_tri(p, kre, kim) && p->m >= 64 && p->m <= 8192) ? 1 : 0;
+  *on = (p->facr && col_use_tri(p, kre, kim) && p->m >= 64 &&
+         (p->m <= 8192 || (kim == 0.0 && p->m == 16384))) ? 1 : 0;
   return KFBI_OK;
 }
 

@@ -206,6 +206,35 @@ def test_facr_box_solve(m, kappa):
         assert rel_linf(u_f.cpu().numpy(), ref) < 1e-11
 
 
+@pytest.mark.parametrize("kappa", [2048.0, 32768.0, 8j])
+def test_facr_16384(kappa):
+    # M = 16384: real data runs FACR on the one-real-row engine (box_real.cuh,
+    # rows_odd_facr_real1); complex data stays on the three-pass solve
+    import torch
+
+    m = 16384
+    grid = k.CartesianGrid(PI_BOX, m)
+    cplx = isinstance(kappa, complex)
+    s = k.BoxSolver(grid, kappa, "dirichlet-zero")
+    assert s.plan.facr_for(kappa) == (not cplx)
+    if cplx:
+        return
+    g = torch.Generator(device="cuda").manual_seed(5)
+    rhs = torch.randn((m + 1, m + 1), generator=g, device="cuda", dtype=torch.float64)
+    u_f = s.solve(rhs)
+    s.plan.set_facr(False)
+    try:
+        u_3 = s.solve(rhs)
+    finally:
+        s.plan.set_facr(True)
+    scale = float(u_3.abs().max())
+    assert float((u_f - u_3).abs().max()) / scale < 1e-12
+    for edge in (u_f[0], u_f[-1], u_f[:, 0], u_f[:, -1]):
+        assert bool((edge == 0).all())
+    del u_f, u_3, rhs
+    torch.cuda.empty_cache()
+
+
 def test_facr_richardson_same_iterations():
     # the Richardson solve through the FACR box solve (corrections on even and
     # odd rows): same sweeps and field as the three-pass solve
