@@ -471,6 +471,12 @@ def run_ours(args):
             except Exception as e:          # reported, never fatal for the headline
                 slab[name] = {"error": f"{type(e).__name__}: {e}"}
             torch.cuda.empty_cache()
+        if ws == 1:
+            try:
+                slab["one_gpu"] = c5_one_gpu(args, local)
+            except Exception as e:
+                slab["one_gpu"] = {"error": f"{type(e).__name__}: {e}"}
+            torch.cuda.empty_cache()
 
     if rank != 0:
         return None
@@ -650,6 +656,55 @@ def c5_problem(m, rank, ws, local, mode, torch):
     g = torch.from_numpy(np.asarray(sol.dirichlet(cps.x, cps.y))).cuda()
     wsp.plan                                   # geometry upload
     return geo, wsp, sol, solver, F, fg, g, kappa
+
+
+def c5_one_gpu(args, local):
+    """C5 on one GPU through the plan's own device Richardson solve
+    (bvp.solve_device: FACR(1) box solve, no slab layout)."""
+    import torch
+
+    import paper_2404_14864_b200 as k
+    from paper_2404_14864_b200.bvp import solve_device
+
+    m = args.slab_m
+    t0 = time.time()
+    tau = 0.25 * 64 / m
+    kappa = 2.0 / tau
+    geo = k.build_grid((-np.pi, np.pi, -np.pi, np.pi), m, k.StarCurve(1.5, c=0.2, lobes=3))
+    wsp = k.InterfaceWorkspace(geo, backend=k.CudaBackend(local, timing=False))
+    sol = k.StaticPlaneWave(kappa=kappa)
+    cps = wsp.cps
+    X, Y = geo.grid.X, geo.grid.Y
+    interior = geo.classification.interior
+    F = torch.from_numpy(np.where(interior, sol.f(X, Y), 0.0).reshape(-1)).cuda()
+    fg = torch.from_numpy(np.asarray(sol.f(cps.x, cps.y))).cuda()
+    g = torch.from_numpy(np.asarray(sol.dirichlet(cps.x, cps.y))).cuda()
+    wsp.plan
+    torch.cuda.synchronize()
+    setup_s = time.time() - t0
+
+    def solve():
+        dens = torch.zeros(cps.m, dtype=torch.float64, device="cuda")
+        return solve_device(wsp, kappa=kappa, F=F, f_gamma=fg, g=g, density=dens)
+
+    solve()
+    reps = max(1, args.slab_steps)
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(reps):
+        out = solve()
+    b.record()
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / reps
+    u = out.u.reshape(m + 1, m + 1).cpu().numpy()
+    err = float(np.max(np.abs(u[interior] - sol.u(X, Y)[interior])))
+    return {"metric": f"KFBI solves/s at {m}^2 (C5, one GPU, plan box solve)",
+            "value": 1e3 / ms, "unit": "solves/s", "ms_per_solve": ms, "solves": reps,
+            "n_ranks": 1, "iterations": out.iterations, "max_err_interior": err,
+            "setup_s": setup_s, "n_ctl": int(cps.m), "kappa": kappa,
+            "facr": bool(wsp.plan.facr_for(kappa)),
+            "geometry": "star(1.5, 0.2, 3) on [-pi, pi]^2 (SURVEY §8(d) C5)", "mode": "plan"}
 
 
 def slab_c5(args, ws, rank, local, mode):

@@ -391,6 +391,103 @@ corr_edges_kernel(EdgeArgs ea, const T *__restrict__ jm, T *jv, const int *done)
   }
 }
 
+// Same product with the jump matrix staged in shared memory: a CTA of
+// CE_WARPS warps owns a contiguous block of edges and walks the controls in
+// chunks of CE_CK; each chunk of the five used JM columns is read from L2
+// ONCE per CTA (the per-warp form above re-reads all of JM per warp: 16x the W
+// bytes of L2 traffic at star3 c128) and kept de-interleaved by parity so the
+// lanes' pair reads are conflict free.  The chunk's W loads are issued before
+// the staging, so HBM latency overlaps it.
+constexpr int CE_WARPS = 16;
+
+template <typename T, int EW>
+__global__ void __launch_bounds__(CE_WARPS * 32, 1)
+corr_edges_smem_kernel(EdgeArgs ea, const T *__restrict__ jm, T *jv, const int *done) {
+  using S = Sc<T>;
+  // control pairs per lane per chunk: UP * EW 16-byte W loads in flight per
+  // lane within the 128-register budget of 16 warps per SM
+  constexpr int UP = sizeof(T) == 16 && EW >= 4 ? 2 : 4;
+  constexpr int CE_CK = 64 * UP;
+  __shared__ T js[5][2][CE_CK / 2];
+  if (done && *done) return;
+  const int lane = threadIdx.x & 31;
+  const int gw = blockIdx.x * CE_WARPS + (threadIdx.x >> 5);
+  const int e0 = gw * ea.per_warp;
+  const int e_end = min(e0 + ea.per_warp, ea.n_edges);
+  const int nq = e_end - e0;                     // edges of this warp (<= 0: staging only)
+  const int n = ea.n_ctl;
+  bool vert[EW];
+  const double2 *wr[EW];
+#pragma unroll
+  for (int q = 0; q < EW; ++q) {
+    const int e = nq > 0 ? e0 + min(q, nq - 1) : 0;
+    vert[q] = ea.axis[e] != 0;
+    wr[q] = reinterpret_cast<const double2 *>(ea.W + (size_t)e * ea.ld);
+  }
+  T acc[EW][3];
+#pragma unroll
+  for (int q = 0; q < EW; ++q) acc[q][0] = acc[q][1] = acc[q][2] = S::zero();
+  const int n2 = ea.ld >> 1;
+  for (int c0 = 0; c0 < n; c0 += CE_CK) {
+    double2 w2[UP][EW];
+#pragma unroll
+    for (int u = 0; u < UP; ++u) {
+      const int i2 = (c0 >> 1) + lane + 32 * u;
+      const bool ok = i2 < n2;
+#pragma unroll
+      for (int q = 0; q < EW; ++q) {
+        if (ok && q < nq) {
+          asm volatile("ld.global.cs.v2.f64 {%0,%1}, [%2];"
+                       : "=d"(w2[u][q].x), "=d"(w2[u][q].y) : "l"(wr[q] + i2));
+        } else {
+          w2[u][q] = make_double2(0.0, 0.0);
+        }
+      }
+    }
+    __syncthreads();                             // the previous chunk's reads are done
+    for (int idx = threadIdx.x; idx < 5 * CE_CK; idx += CE_WARPS * 32) {
+      const int col = idx / CE_CK, k = idx - col * CE_CK, i = c0 + k;
+      const int off = col == 4 ? 5 : col;        // u, u_x, u_y, u_xx, u_yy
+      js[col][k & 1][k >> 1] = i < n ? jm[(size_t)off * n + i] : S::zero();
+    }
+    __syncthreads();
+    if (nq > 0) {
+#pragma unroll
+      for (int u = 0; u < UP; ++u) {
+        const int k2 = lane + 32 * u;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const T a0 = js[0][h][k2], ax = js[1][h][k2], ay = js[2][h][k2], axx = js[3][h][k2],
+                  ayy = js[4][h][k2];
+#pragma unroll
+          for (int q = 0; q < EW; ++q) {
+            const double w = h ? w2[u][q].y : w2[u][q].x;
+            acc[q][0] = S::add(acc[q][0], S::rmul(a0, w));
+            acc[q][1] = S::add(acc[q][1], S::rmul(vert[q] ? ay : ax, w));
+            acc[q][2] = S::add(acc[q][2], S::rmul(vert[q] ? ayy : axx, w));
+          }
+        }
+      }
+    }
+  }
+  if (nq <= 0) return;
+#pragma unroll
+  for (int q = 0; q < EW; ++q) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) acc[q][c] = warp_reduce_T(acc[q][c]);
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int q = 0; q < EW; ++q) {
+      if (q < nq) {
+        jv[3 * (e0 + q)] = acc[q][0];
+        jv[3 * (e0 + q) + 1] = acc[q][1];
+        jv[3 * (e0 + q) + 2] = acc[q][2];
+      }
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Matrix-free edge values (the trig branch of interp_rows, interface.py:38-52,
 // 70-75).  For the reference's equispaced controls theta_j = 2 pi j / n (n

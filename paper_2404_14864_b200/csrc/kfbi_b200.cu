@@ -132,6 +132,7 @@ struct kfbi_plan {
   int sn_nrows = 0, sn_nodes = 0;
   bool trace_sweep = false;         // kfbi_plan_set_trace_sweep (opt-in: measured no gain)
   bool facr = true;                 // kfbi_plan_set_facr: cyclic-reduction box solve
+  bool edges_smem = true;           // W-row edge values with JM staged per CTA (env KFBI_EDGES_SMEM=0: per warp)
   DevBuf<double2> sn_vals, sn_v13;
   DevBuf<int> skip;
   DevBuf<StepLog> log;
@@ -577,6 +578,29 @@ kfbi_status edges_T(kfbi_plan *p, const void *jm, void *jv, const int *done, cud
   constexpr int EW = std::is_same<T, double2>::value ? 4 : 8, U = 2;
   static int sms = 0;
   if (!sms) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->device);
+  if (p->n_edges == 0) return KFBI_OK;
+  // JM staged per CTA (corr_edges_smem_kernel, one CTA of CE_WARPS warps per SM)
+  // when a wave of warps covers the edges with <= 4 rows each: 61 -> 46 us for
+  // the star3 c128 rows at 4096^2, 22 -> 16 us at 1024^2; with more rows per
+  // warp the per-warp form's deeper load queue wins (flower f64 at 4096^2:
+  // 79 vs 92 us; profiles/r2_v31_edges.log)
+  const int wave_s = sms * CE_WARPS;
+  const int pw_s = (p->n_edges + wave_s - 1) / wave_s;
+  if (p->edges_smem && pw_s <= 4) {
+    const int pw = pw_s;
+    auto go = [&](auto ew) {
+      constexpr int E = decltype(ew)::value;
+      EdgeArgs ea{p->n_edges, p->n_ctl, p->w_ld, pw, p->W.p, p->edge_axis.p};
+      const int warps = (p->n_edges + pw - 1) / pw;
+      const int blocks = (warps + CE_WARPS - 1) / CE_WARPS;
+      return launch(p, KFBI_K_JUMPS, s, [&] {
+        corr_edges_smem_kernel<T, E><<<blocks, CE_WARPS * 32, 0, s>>>(
+            ea, static_cast<const T *>(jm), static_cast<T *>(jv), done);
+      });
+    };
+    if (pw <= 2) return go(std::integral_constant<int, 2>());
+    return go(std::integral_constant<int, 4>());
+  }
   const int wave_warps = sms * 2 * 8;
   int per_warp = (p->n_edges + wave_warps - 1) / wave_warps;
   if (per_warp > EW) per_warp = EW;
@@ -1025,6 +1049,8 @@ kfbi_status kfbi_plan_create(const kfbi_grid_desc *desc, kfbi_plan **out) {
   {
     const char *f = std::getenv("KFBI_FACR");      // "0": three-pass box solves by default
     if (f && f[0] == '0') p->facr = false;
+    const char *es = std::getenv("KFBI_EDGES_SMEM");
+    if (es && es[0] == '0') p->edges_smem = false;
   }
   cudaError_t e = cudaSetDevice(p->device);
   if (e != cudaSuccess) {
