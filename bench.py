@@ -1054,7 +1054,7 @@ def main(argv=None):
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--m", type=int, default=M_DEFAULT)
+    ap.add_argument("--m", "--grid", dest="m", type=int, default=M_DEFAULT)
     ap.add_argument("--equations", default=",".join(EQUATIONS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--workload", choices=["steps", "c4", "c5"], default="steps",

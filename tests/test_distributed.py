@@ -51,3 +51,25 @@ def test_two_rank_gloo_reduction_and_rank0_only_reference():
         assert p.exitcode == 0
     assert out[0][0] == pytest.approx(2.5) and out[1][0] == pytest.approx(2.5)
     assert out[1][1] is None          # non-zero ranks do no reference work
+
+
+def test_torchrun_two_ranks_reference_arm_contract():
+    # the driver's exact launch (torch.distributed.run, 127.0.0.1) of the
+    # reference arm on CPU: rank 0 prints ONE JSON line, rank 1 exits 0 silently
+    import json
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), "bench.py",
+           "--impl", "reference", "--gpus", "2", "--steps", "1", "--warmup", "3", "--grid", "64",
+           "--equations", "heat", "--ref-budget-s", "20"]
+    env = dict(os.environ, OMP_NUM_THREADS="1", CUDA_VISIBLE_DEVICES="")
+    r = subprocess.run(cmd, cwd=root, capture_output=True, text=True, timeout=600, env=env)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["value"] > 0 and d["n_gpus"] == 2
+    assert d["e2e"]["h2d_bytes_per_step"] == 0
