@@ -68,6 +68,35 @@ KFBI_DEV T group_correction(const CorrArgs<T> &c, int g) {
   if (c.cval) return c.cval[g];
   const int r0 = c.group_start[g], r1 = c.group_start[g + 1];
   T acc = S::zero();
+  if (r1 - r0 <= 4) {
+    // a node has at most four crossing edges: every gather in flight at once,
+    // then the same ordered sum as the loop below
+    const int cnt = r1 - r0;
+    int e[4];
+    double d[4], sg[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      e[k] = k < cnt ? c.rec_edge[r0 + k] : 0;
+      d[k] = k < cnt ? c.rec_d[r0 + k] : 0.0;
+      sg[k] = k < cnt ? c.rec_sigma[r0 + k] : 0.0;
+    }
+    T j0[4], j1[4], j2[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      j0[k] = k < cnt ? c.jv[3 * e[k]] : S::zero();
+      j1[k] = k < cnt ? c.jv[3 * e[k] + 1] : S::zero();
+      j2[k] = k < cnt ? c.jv[3 * e[k] + 2] : S::zero();
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (k < cnt) {
+        T v = S::add(S::add(j0[k], S::rmul(j1[k], d[k])), S::rmul(S::rmul(j2[k], 0.5), d[k] * d[k]));
+        v = S::rmul(v, sg[k]);
+        acc = k == 0 ? v : S::add(acc, v);
+      }
+    }
+    return acc;
+  }
   for (int r = r0; r < r1; ++r) {
     const int e = c.rec_edge[r];
     const T j0 = c.jv[3 * e], j1 = c.jv[3 * e + 1], j2 = c.jv[3 * e + 2];

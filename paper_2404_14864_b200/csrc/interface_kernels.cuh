@@ -71,6 +71,26 @@ KFBI_DEV T circ_deriv(const CtlGeom &g, const T *__restrict__ v, int i, int lane
   return acc[0];
 }
 
+// Block-wide copy global -> shared with U loads in flight per thread before
+// any store (a plain strided loop waits out one L2 round trip per element).
+template <int U, typename LD, typename ST>
+KFBI_DEV void stage_batched(int count, LD ld, ST st) {
+  const int nt = blockDim.x, tid = threadIdx.x;
+  for (int base = 0; base < count; base += U * nt) {
+    decltype(ld(0)) v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = base + u * nt + tid;
+      if (i < count) v[u] = ld(i);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = base + u * nt + tid;
+      if (i < count) st(i, v[u]);
+    }
+  }
+}
+
 KFBI_DEV double warp_reduce_T(double v) { return warp_sum(v); }
 KFBI_DEV double2 warp_reduce_T(double2 v) {
   return make_double2(warp_sum(v.x), warp_sum(v.y));
@@ -136,12 +156,10 @@ circ_block_kernel(CtlGeom g, const T *__restrict__ v0, const T *__restrict__ v1,
   T *vs = reinterpret_cast<T *>(Ds + ((n + 1) & ~1));
   T *red = vs + NV * n;
   const bool have = v0 != nullptr;
-  for (int i = tid; i < n; i += blockDim.x) {
-    Ds[i] = g.deriv_col[i];
-    if (have) {
-      vs[i] = v0[i];
-      if (NV == 2) vs[n + i] = v1[i];
-    }
+  stage_batched<8>(n, [&](int i) { return g.deriv_col[i]; }, [&](int i, double x) { Ds[i] = x; });
+  if (have) {
+    stage_batched<8>(n, [&](int i) { return v0[i]; }, [&](int i, T x) { vs[i] = x; });
+    if (NV == 2) stage_batched<8>(n, [&](int i) { return v1[i]; }, [&](int i, T x) { vs[n + i] = x; });
   }
   __syncthreads();
   const int q = tid & 3, c = tid >> 2;
@@ -178,11 +196,32 @@ circ_block_kernel(CtlGeom g, const T *__restrict__ v0, const T *__restrict__ v1,
 #pragma unroll
     for (int r = 0; r < 4; ++r) red[(c * NV + v) * CIRC_OUT + 4 * q + r] = acc[v][r];
   __syncthreads();
-  if (tid < NV * CIRC_OUT) {
-    const int v = tid / CIRC_OUT, o = tid - v * CIRC_OUT, i = i0 + o;
+  // the CIRC_CH chunk partials of an output: 8 threads sum 8 chunks each (in
+  // chunk order), then a fixed shuffle tree (deterministic)
+  T sum;
+  {
+    const int ov = tid >> 3, part = tid & 7;     // ov = v * CIRC_OUT + o
+    sum = S::zero();
+    if (ov < NV * CIRC_OUT) {
+      const int v = ov / CIRC_OUT, o = ov - v * CIRC_OUT;
+      constexpr int PER = CIRC_CH / 8;
+      sum = red[((part * PER) * NV + v) * CIRC_OUT + o];
+#pragma unroll
+      for (int cc = 1; cc < PER; ++cc) sum = S::add(sum, red[((part * PER + cc) * NV + v) * CIRC_OUT + o]);
+    }
+#pragma unroll
+    for (int off = 4; off >= 1; off >>= 1) {
+      if constexpr (std::is_same<T, double>::value) sum += __shfl_down_sync(0xffffffffu, sum, off, 8);
+      else {
+        sum.x += __shfl_down_sync(0xffffffffu, sum.x, off, 8);
+        sum.y += __shfl_down_sync(0xffffffffu, sum.y, off, 8);
+      }
+    }
+  }
+  static_assert(NV * CIRC_OUT * 8 <= 256 && CIRC_CH % 8 == 0, "circ reduction layout");
+  if ((tid & 7) == 0 && (tid >> 3) < NV * CIRC_OUT) {
+    const int v = (tid >> 3) / CIRC_OUT, o = (tid >> 3) - v * CIRC_OUT, i = i0 + o;
     if (i < n) {
-      T sum = red[v * CIRC_OUT + o];
-      for (int cc = 1; cc < CIRC_CH; ++cc) sum = S::add(sum, red[(cc * NV + v) * CIRC_OUT + o]);
       sum = rdiv(sum, g.speed[i]);
       if constexpr (JUMPS) {
         jump_system<T>(g, ja, i, have ? sum : S::zero());
@@ -537,10 +576,10 @@ spec_block_kernel(int n, int K, const T *__restrict__ jm, double2 *__restrict__ 
   // the CTA's control range, staged column-major [SPEC_COLS][jn] in shared memory
   const int cj0 = (int)((long)n * y / Y), cj1 = (int)((long)n * (y + 1) / Y), jn = cj1 - cj0;
   T *fs = reinterpret_cast<T *>(red_sm + (size_t)nw * R * 32);
-  for (int i = threadIdx.x; i < SPEC_COLS * jn; i += blockDim.x) {
+  stage_batched<4>(SPEC_COLS * jn, [&](int i) {
     const int c = i / jn, j = i - c * jn;
-    fs[i] = jm[(size_t)spec_jm_col(c) * n + cj0 + j];
-  }
+    return jm[(size_t)spec_jm_col(c) * n + cj0 + j];
+  }, [&](int i, T x) { fs[i] = x; });
   __syncthreads();
   const int j0 = cj0 + (int)((long)jn * w / nw), j1 = cj0 + (int)((long)jn * (w + 1) / nw);
   double2 acc[R];
@@ -714,7 +753,7 @@ edges_spectral_res_kernel(int ngroups, int n, int K, const int *__restrict__ per
   constexpr int R = SPEC_COLS * NP;
   extern __shared__ double2 fsm[];                       // [R][K]
   if (done && *done) return;
-  for (int i = threadIdx.x; i < R * K; i += blockDim.x) fsm[i] = spec[i];
+  stage_batched<8>(R * K, [&](int i) { return spec[i]; }, [&](int i, double2 x) { fsm[i] = x; });
   __syncthreads();
   const int lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
   auto F = [&](int r, int k) { return fsm[(size_t)r * K + k]; };
