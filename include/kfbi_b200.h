@@ -476,6 +476,11 @@ kfbi_status kfbi_log_reserve(kfbi_plan *plan, int32_t count);
 kfbi_status kfbi_log_norm(kfbi_plan *plan, int32_t slot, int32_t which, void *stream);
 kfbi_status kfbi_log_fetch(kfbi_plan *plan, int32_t first, int32_t count,
                            kfbi_step_log *out, void *stream);
+/* Stream-ordered log maintenance for CUDA-graph replays of a step (the
+ * graph logs into a fixed slot): zero `count` entries from `slot`, copy
+ * `count` entries from `src` to `dst`. */
+kfbi_status kfbi_log_clear(kfbi_plan *plan, int32_t slot, int32_t count, void *stream);
+kfbi_status kfbi_log_copy(kfbi_plan *plan, int32_t src, int32_t dst, int32_t count, void *stream);
 
 /* Per-kernel-name device time (ms) and call counts since the last reset
  * (Backend.timings / calls, engine.py:84-95).  Syncs the plan's events. */

@@ -383,6 +383,12 @@ class Plan:
     def log_norm(self, slot, which=0):
         N.check(self._lib.kfbi_log_norm(self.handle, int(slot), int(which), self.stream))
 
+    def log_clear(self, slot, count=1):
+        N.check(self._lib.kfbi_log_clear(self.handle, int(slot), int(count), self.stream))
+
+    def log_copy(self, src, dst, count=1):
+        N.check(self._lib.kfbi_log_copy(self.handle, int(src), int(dst), int(count), self.stream))
+
     def log_fetch(self, first, count):
         out = (N.StepLog * max(int(count), 1))()
         N.check(self._lib.kfbi_log_fetch(self.handle, int(first), int(count), out, self.stream))

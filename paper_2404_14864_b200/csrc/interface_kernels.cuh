@@ -1236,6 +1236,104 @@ op_solve_kernel(OpSolveArgs a, const T *__restrict__ Tcm, T *A, T *B,
   }
 }
 
+// Small n_ctl (the latency path of small grids, C1: n = 88): every sweep
+// inside ONE CTA, T transposed into shared memory (row-major: a warp reads
+// one row's columns conflict free), the iterates ping-pong in shared memory,
+// no grid barrier (1.3 us per sweep on the cooperative kernels, more than the
+// sweep's work at this size).  Same sweep semantics and state protocol as
+// op_solve_kernel: each sweep's iterate also goes to A / B by parity (the
+// finaliser reads the last two), the history and RichState as there.
+constexpr int OPC_THREADS = 1024;
+template <typename T>
+inline size_t op_cta_smem(int n) {
+  return ((size_t)n * n + 6 * (size_t)n) * sizeof(T);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(OPC_THREADS, 1)
+op_solve_cta_kernel(OpSolveArgs a, const T *__restrict__ Tcm, T *A, T *B,
+                    const T *__restrict__ phi0, const T *__restrict__ trace1,
+                    const T *__restrict__ g) {
+  using S = Sc<T>;
+  extern __shared__ __align__(16) unsigned char opc_smem[];
+  __shared__ double wmax[OPC_THREADS / 32];
+  const int n = a.n;
+  T *Ts = reinterpret_cast<T *>(opc_smem);               // [n][n], Ts[q n + c] = T(q, c)
+  T *ph = Ts + (size_t)n * n;                            // [2][n] iterates
+  T *d = ph + 2 * n, *p0 = d + n, *t1 = p0 + n, *gs = t1 + n;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int NW = OPC_THREADS / 32;
+  if (a.st->done) return;                       // uniform: set before launch
+  for (int i = tid; i < n * n; i += OPC_THREADS) {   // Ts[q n + c] = Tcm[c n + q]
+    const int q = i / n, c = i - q * n;
+    Ts[i] = __ldg(&Tcm[(size_t)c * n + q]);
+  }
+  for (int i = tid; i < n; i += OPC_THREADS) {
+    p0[i] = phi0[i];
+    t1[i] = trace1[i];
+    gs[i] = g[i];
+    ph[((a.first_idx & 1) ^ 1) * n + i] = (a.first_idx & 1) ? A[i] : B[i];   // the first input
+  }
+  __syncthreads();
+  // 8 lanes per row (four rows per warp at once), shuffle sums within the
+  // group; the sweep max by one warp
+  constexpr int GL = 8;
+  const int sub = lane & (GL - 1), grp = tid / GL;
+  constexpr int NG = OPC_THREADS / GL;
+  for (int idx = a.first_idx; idx < a.max_iter; ++idx) {
+    const T *in = ph + ((idx & 1) ^ 1) * n;     // A-side iterate for odd idx (as op_solve_kernel)
+    T *outs = ph + (idx & 1) * n;
+    T *outg = (idx & 1) ? B : A;
+    for (int i = tid; i < n; i += OPC_THREADS) d[i] = S::sub(in[i], p0[i]);
+    __syncthreads();
+    double mag = 0.0;
+    for (int q0 = 0; q0 < n; q0 += NG) {
+      const int q = q0 + grp;
+      T acc = S::zero();
+      if (q < n) {
+        const T *row = Ts + (size_t)q * n;
+        for (int c = sub; c < n; c += GL) acc = S::add(acc, S::mul(row[c], d[c]));
+      }
+#pragma unroll
+      for (int off = GL / 2; off >= 1; off >>= 1) {
+        if constexpr (std::is_same<T, double>::value) acc += __shfl_down_sync(0xffffffffu, acc, off, GL);
+        else {
+          acc.x += __shfl_down_sync(0xffffffffu, acc.x, off, GL);
+          acc.y += __shfl_down_sync(0xffffffffu, acc.y, off, GL);
+        }
+      }
+      if (sub == 0 && q < n) {
+        const T trace = S::add(t1[q], acc);
+        const T upd = S::rmul(S::sub(gs[q], trace), a.gamma);
+        const T o = S::add(in[q], upd);
+        outs[q] = o;
+        outg[q] = o;
+        mag = nanmax(mag, S::abs(upd));
+      }
+    }
+    mag = warp_nanmax(mag);
+    if (lane == 0) wmax[warp] = mag;
+    __syncthreads();
+    if (warp == 0) {
+      double v = warp_nanmax(wmax[lane]);
+      if (lane == 0) wmax[0] = v;
+    }
+    __syncthreads();
+    const double res = wmax[0];
+    const bool conv = res <= a.tol;
+    const bool last = conv || idx + 1 >= a.max_iter;
+    if (tid == 0) {
+      a.history[idx] = res;
+      a.st->iters = idx + 1;
+      a.st->last_res = res;
+      if (conv) a.st->done = 1;
+      else if (idx + 1 >= a.max_iter) a.st->done = 2;
+    }
+    __syncthreads();                            // wmax / d reused by the next sweep
+    if (last) break;
+  }
+}
+
 // f64 operator sweeps with two rows per lane: half-warp h of warp w works on
 // columns 2w + h + 32 s, lane l of the half on rows (2l, 2l+1) of the CTA's
 // block, so every shared-memory and global load of T is a 16-byte pair and

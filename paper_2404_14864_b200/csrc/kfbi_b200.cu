@@ -133,6 +133,7 @@ struct kfbi_plan {
   bool trace_sweep = false;         // kfbi_plan_set_trace_sweep (opt-in: measured no gain)
   bool facr = true;                 // kfbi_plan_set_facr: cyclic-reduction box solve
   bool edges_smem = true;           // W-row edge values with JM staged per CTA (env KFBI_EDGES_SMEM=0: per warp)
+  bool op_cta = true;               // operator sweeps of n_ctl <= 160 in one CTA (env KFBI_OP_CTA=0: grid kernels)
   DevBuf<double2> sn_vals, sn_v13;
   DevBuf<int> skip;
   DevBuf<StepLog> log;
@@ -795,6 +796,19 @@ kfbi_status op_solve(kfbi_plan *p, const kfbi_bvp *b, cudaStream_t s) {
   const T *tr1 = reinterpret_cast<const T *>(p->trace1.p);
   const T *g = static_cast<const T *>(b->g);
   void *args[] = {&a, (void *)&Tcm, &A, &B, (void *)&phi0, (void *)&tr1, (void *)&g};
+  // small n: all sweeps in one CTA, no grid barrier (op_solve_cta_kernel)
+  if (n <= 160 && op_cta_smem<T>(n) <= (size_t)(smem_optin - 1024) && p->op_cta) {
+    static bool cta_attr = false;
+    if (!cta_attr) {
+      KFBI_CUDA(cudaFuncSetAttribute(op_solve_cta_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     smem_optin - 1024), "density-update");
+      cta_attr = true;
+    }
+    const size_t smc = op_cta_smem<T>(n);
+    return launch(p, KFBI_K_DENSITY, s, [&] {
+      op_solve_cta_kernel<T><<<1, OPC_THREADS, smc, s>>>(a, Tcm, A, B, phi0, tr1, g);
+    });
+  }
   if constexpr (std::is_same<T, double>::value) {
     // two rows per lane (16-byte pairs) when n and R are even
     constexpr int K2 = K / 2;
@@ -1051,6 +1065,8 @@ kfbi_status kfbi_plan_create(const kfbi_grid_desc *desc, kfbi_plan **out) {
     if (f && f[0] == '0') p->facr = false;
     const char *es = std::getenv("KFBI_EDGES_SMEM");
     if (es && es[0] == '0') p->edges_smem = false;
+    const char *oc = std::getenv("KFBI_OP_CTA");
+    if (oc && oc[0] == '0') p->op_cta = false;
   }
   cudaError_t e = cudaSetDevice(p->device);
   if (e != cudaSuccess) {
@@ -1878,6 +1894,23 @@ kfbi_status kfbi_log_fetch(kfbi_plan *p, int32_t first, int32_t count, kfbi_step
   KFBI_CUDA(cudaMemcpyAsync(out, p->log.p + first, sizeof(StepLog) * count, cudaMemcpyDeviceToHost, s),
             "density-update");
   KFBI_CUDA(cudaStreamSynchronize(s), "density-update");
+  return KFBI_OK;
+}
+
+kfbi_status kfbi_log_clear(kfbi_plan *p, int32_t slot, int32_t count, void *stream) {
+  KFBI_TRY(check_plan(p));
+  if (slot < 0 || count < 0 || slot + count > p->log_cap) return fail(KFBI_E_CONFIG, "log range out of bounds");
+  KFBI_CUDA(cudaMemsetAsync(p->log.p + slot, 0, sizeof(StepLog) * count, (cudaStream_t)stream),
+            "rhs-update");
+  return KFBI_OK;
+}
+
+kfbi_status kfbi_log_copy(kfbi_plan *p, int32_t src, int32_t dst, int32_t count, void *stream) {
+  KFBI_TRY(check_plan(p));
+  if (src < 0 || dst < 0 || count < 0 || src + count > p->log_cap || dst + count > p->log_cap)
+    return fail(KFBI_E_CONFIG, "log range out of bounds");
+  KFBI_CUDA(cudaMemcpyAsync(p->log.p + dst, p->log.p + src, sizeof(StepLog) * count,
+                            cudaMemcpyDeviceToDevice, (cudaStream_t)stream), "rhs-update");
   return KFBI_OK;
 }
 

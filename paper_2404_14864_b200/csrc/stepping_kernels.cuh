@@ -2,6 +2,14 @@
 // the (M+1)^2 grid (with the interior mask) or the n_ctl control points (no
 // mask).  Each kernel folds in the blow-up norm max|u| of
 // StepContext.check_stable (timestepping.py:172-175).
+//
+// Exterior nodes: every state field the steppers carry (u, F, F_prev, the
+// Strang carry) is zero outside the mask — the startups build them from
+// interior_field (timestepping.py:203-209, 243-274, 366-368) and every step
+// masks what it returns — so at a masked-off node the recurrences give exactly
+// 0 from zero inputs.  The kernels load the mask first and skip the field
+// loads (and the Newton solve) there: only the zero stores remain (the
+// exterior is 65-82 % of the grid in the bench geometries).
 #pragma once
 
 #include "common.cuh"
@@ -52,16 +60,21 @@ struct MaskNormOp {
     T v[K][2];
     uchar2 mk[K];
 #pragma unroll
-    for (int k = 0; k < K; ++k) {
-      if constexpr (std::is_same<T, double>::value) {
-        const double2 w = reinterpret_cast<const double2 *>(u)[ii[k]];
-        v[k][0] = w.x;
-        v[k][1] = w.y;
-      } else {
-        v[k][0] = u[2 * ii[k]];
-        v[k][1] = u[2 * ii[k] + 1];
-      }
+    for (int k = 0; k < K; ++k)
       mk[k] = mask ? reinterpret_cast<const uchar2 *>(mask)[ii[k]] : make_uchar2(1, 1);
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      v[k][0] = v[k][1] = Sc<T>::zero();
+      if (mk[k].x | mk[k].y) {                   // exterior pairs: zero stores only
+        if constexpr (std::is_same<T, double>::value) {
+          const double2 w = reinterpret_cast<const double2 *>(u)[ii[k]];
+          v[k][0] = w.x;
+          v[k][1] = w.y;
+        } else {
+          v[k][0] = u[2 * ii[k]];
+          v[k][1] = u[2 * ii[k] + 1];
+        }
+      }
     }
 #pragma unroll
     for (int k = 0; k < K; ++k) {
@@ -98,10 +111,15 @@ struct HeatOp {
     double2 v[K], fo[K];
     uchar2 mk[K];
 #pragma unroll
-    for (int k = 0; k < K; ++k) {
-      v[k] = reinterpret_cast<const double2 *>(u)[ii[k]];
-      fo[k] = reinterpret_cast<const double2 *>(F_old)[ii[k]];
+    for (int k = 0; k < K; ++k)
       mk[k] = mask ? reinterpret_cast<const uchar2 *>(mask)[ii[k]] : make_uchar2(1, 1);
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      v[k] = fo[k] = make_double2(0.0, 0.0);
+      if (mk[k].x | mk[k].y) {
+        v[k] = reinterpret_cast<const double2 *>(u)[ii[k]];
+        fo[k] = reinterpret_cast<const double2 *>(F_old)[ii[k]];
+      }
     }
 #pragma unroll
     for (int k = 0; k < K; ++k) {
@@ -148,12 +166,17 @@ struct WaveOp {
     double2 v[K], c[K], a[K], b[K];
     uchar2 mk[K];
 #pragma unroll
-    for (int k = 0; k < K; ++k) {
-      v[k] = reinterpret_cast<const double2 *>(un)[ii[k]];
-      c[k] = reinterpret_cast<const double2 *>(uc)[ii[k]];
-      a[k] = reinterpret_cast<const double2 *>(fc)[ii[k]];
-      b[k] = reinterpret_cast<const double2 *>(fp)[ii[k]];
+    for (int k = 0; k < K; ++k)
       mk[k] = mask ? reinterpret_cast<const uchar2 *>(mask)[ii[k]] : make_uchar2(1, 1);
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      v[k] = c[k] = a[k] = b[k] = make_double2(0.0, 0.0);
+      if (mk[k].x | mk[k].y) {
+        v[k] = reinterpret_cast<const double2 *>(un)[ii[k]];
+        c[k] = reinterpret_cast<const double2 *>(uc)[ii[k]];
+        a[k] = reinterpret_cast<const double2 *>(fc)[ii[k]];
+        b[k] = reinterpret_cast<const double2 *>(fp)[ii[k]];
+      }
     }
 #pragma unroll
     for (int k = 0; k < K; ++k) {
@@ -272,6 +295,11 @@ nonlinear_phase_kernel(long n, const double2 *__restrict__ ustar, const double2 
   double worst = 0.0;
   for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n;
        i += (long)gridDim.x * blockDim.x) {
+    if (mask && !mask[i]) {                      // u* = 0 there: Newton returns 0, residual 0
+      out[i] = make_double2(0.0, 0.0);
+      if (F) F[i] = make_double2(0.0, 0.0);
+      continue;
+    }
     double r;
     const double2 us = other ? ustar_of(mode, ustar[i], other[i], tau) : ustar[i];
     double2 z = newton_node(us, v[i], w, c, r);

@@ -329,3 +329,41 @@ def test_trace_only_first_sweep(cplx):
         assert float((u1 - u0).abs().max()) / scale < 1e-12
         assert float((d1 - d0).abs().max()) / float(d0.abs().max()) < 1e-12
     assert out[(1e3, True)][0] == 1
+
+
+@pytest.mark.parametrize("eq", ["heat", "wave", "schrodinger"])
+def test_state_fields_zero_outside_mask(eq):
+    # the right-hand-side kernels skip the field loads at masked-off nodes
+    # (stepping_kernels.cuh): valid because every state field the steppers
+    # carry is exactly zero there (timestepping.py:203-300, 366-400)
+    import torch
+
+    from paper_2404_14864_b200.timestepping import _stepper_for
+
+    heat, wave, schr = k.HeatPlaneDecay(), k.WaveStanding(), k.SchrodingerPhaseRotation()
+    if eq == "heat":
+        box, curve = BOX, k.StarCurve(1.0, c=0.2, lobes=8)
+        kw = dict(equation="heat", bc_kind="dirichlet", g=heat.dirichlet, u0=heat.u0,
+                  lap_u0=heat.lap_u0, tau=1 / 64, t_final=1.0)
+    elif eq == "wave":
+        box, curve = BOX, k.EllipseCurve(1.2, 0.8)
+        kw = dict(equation="wave", bc_kind="dirichlet", g=wave.dirichlet, u0=wave.u0,
+                  lap_u0=wave.lap_u0, v0=wave.v0, lap_v0=wave.lap_v0, tau=1 / 64, t_final=1.0)
+    else:
+        box, curve = PI_BOX, k.StarCurve(1.5, c=0.2, lobes=3)
+        kw = dict(equation="schrodinger", bc_kind="dirichlet", g=schr.dirichlet, u0=schr.u0,
+                  lap_u0=schr.lap_u0, potential=schr.potential, tau=1 / 64, t_final=1.0)
+    geo = k.build_grid(box, 256, curve)
+    ctx = k.StepContext(geo)
+    spec = k.ProblemSpec(**kw)
+    startup, step = _stepper_for(spec)
+    st = startup(spec, ctx)
+    ext = torch.from_numpy(~geo.classification.interior.reshape(-1)).cuda()
+    for _ in range(4):
+        st = step(st, spec, ctx)
+        for name in ("u", "F", "F_prev", "u_prev", "carry"):
+            v = getattr(st, name)
+            if v is None or not hasattr(v, "reshape"):
+                continue
+            assert bool((v.reshape(-1)[ext] == 0).all()), (eq, name)
+    torch.cuda.synchronize()

@@ -1,0 +1,3 @@
+set -x
+timeout 900 python -m pytest tests/test_gpu_graph.py -m gpu -q --tb=short -p no:cacheprovider > gpurun_out/pytest_r2v39.log 2>&1; echo rc=$? >> gpurun_out/pytest_r2v39.log
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_headline.py tests/test_slab.py -m gpu -q --tb=short -p no:cacheprovider >> gpurun_out/pytest_r2v39.log 2>&1; echo rc=$? >> gpurun_out/pytest_r2v39.log

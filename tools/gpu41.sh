@@ -1,0 +1,4 @@
+set -x
+timeout 900 python -m pytest tests/test_gpu_graph.py tests/test_gpu_parity.py tests/test_gpu_neumann.py tests/test_gpu_gmres.py -m gpu -q --tb=short -p no:cacheprovider > gpurun_out/pytest_r2v41.log 2>&1; echo rc=$? >> gpurun_out/pytest_r2v41.log
+timeout 600 python tools/graph_probe.py > gpurun_out/graph_probe_r2v41.log 2>&1
+KFBI_OP_CTA=0 timeout 600 python tools/graph_probe.py > gpurun_out/graph_probe_r2v41_grid.log 2>&1
