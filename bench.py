@@ -15,7 +15,9 @@ synchronize, max over ranks.  Per-equation working sets (W rows, panels,
 fields) exceed the 126 MB L2, so no flush is needed between steps.
 
   value  time steps/s, device-resident (the public per-step API, boundary
-         data evaluated and uploaded by it every step)
+         data evaluated and uploaded by it every step); the three equations
+         are independent problems, each stepped on its own CUDA stream
+         (`sequential` in the line: the same steps on one stream)
   e2e    same loop plus a device->host copy of every step's solution field
          into pinned memory (what a user saving each step pays): its interior
          values (the masked exterior is zero by construction), packed by a
@@ -249,11 +251,26 @@ def run_ours(args):
     torch.cuda.synchronize()
     t_setup = time.time() - t_setup
 
+    # the three equations are independent problems: each steps on its own
+    # CUDA stream (their latency-bound phases overlap the others' kernels);
+    # --sequential puts them on one stream
+    main_stream = torch.cuda.current_stream()
+    eq_stream = {eq: (main_stream if args.sequential else torch.cuda.Stream()) for eq in eqs}
+
     def advance(eq):
-        st = steppers[eq](states[eq], specs[eq], ctxs[eq])
-        ctxs[eq].check_stable(st, specs[eq])
+        with torch.cuda.stream(eq_stream[eq]):
+            st = steppers[eq](states[eq], specs[eq], ctxs[eq])
+            ctxs[eq].check_stable(st, specs[eq])
         states[eq] = st
         return st
+
+    def fork():
+        for eq in eqs:
+            eq_stream[eq].wait_stream(main_stream)
+
+    def join():
+        for eq in eqs:
+            main_stream.wait_stream(eq_stream[eq])
 
     def fresh():
         # every timed region starts from t = 0: startup + W untimed warm-up
@@ -265,10 +282,31 @@ def run_ours(args):
         for c in ctxs.values():
             c.flush()
         for eq in eqs:
-            states[eq] = startups[eq](specs[eq], ctxs[eq])
+            with torch.cuda.stream(eq_stream[eq]):
+                states[eq] = startups[eq](specs[eq], ctxs[eq])
         for _ in range(args.warmup):
             for eq in eqs:
                 advance(eq)
+        torch.cuda.synchronize()
+        for c in ctxs.values():
+            c.flush()
+
+    def seq_advance(eq):
+        st = steppers[eq](states[eq], specs[eq], ctxs[eq])
+        ctxs[eq].check_stable(st, specs[eq])
+        states[eq] = st
+        return st
+
+    def fresh_seq():
+        # as fresh(), everything on the launching stream
+        torch.cuda.synchronize()
+        for c in ctxs.values():
+            c.flush()
+        for eq in eqs:
+            states[eq] = startups[eq](specs[eq], ctxs[eq])
+        for _ in range(args.warmup):
+            for eq in eqs:
+                seq_advance(eq)
         torch.cuda.synchronize()
         for c in ctxs.values():
             c.flush()
@@ -294,17 +332,13 @@ def run_ours(args):
             if args.profile and rep == 0:
                 torch.cuda.profiler.start()
             start.record(stream)
+            fork()
             for _ in range(args.steps):
                 for eq in eqs:
-                    a = torch.cuda.Event(enable_timing=True)
-                    b = torch.cuda.Event(enable_timing=True)
-                    a.record(stream)
                     st = advance(eq)
-                    b.record(stream)
-                    if rep == 0:
-                        ev[eq].append((a, b))
                     if st.log_slot is None:
                         iters[eq].append(st.last_iterations)
+            join()
             end.record(stream)
             torch.cuda.synchronize()
             if args.profile and rep == 0:
@@ -316,18 +350,37 @@ def run_ours(args):
                     iters[eq].extend(ctxs[eq].flush())
     elapsed_ms = float(np.median(reps_ms))
     launches = (sum(p.launch_count() for p in plans) - launches0) // args.repeats
+
+    # per-equation rates and the one-stream rate: the same K steps with the
+    # equations one after another on one stream, each bracketed by events
+    fresh_seq()
+    s0 = torch.cuda.Event(enable_timing=True)
+    s1 = torch.cuda.Event(enable_timing=True)
+    s0.record(stream)
+    for _ in range(args.steps):
+        for eq in eqs:
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            seq_advance(eq)
+            b.record(stream)
+            ev[eq].append((a, b))
+    s1.record(stream)
+    torch.cuda.synchronize()
+    seq_iters = {eq: ctxs[eq].flush() for eq in eqs}
+    seq_ms = _max_over_ranks(s0.elapsed_time(s1), ws)
     per_eq_ms = {eq: sum(a.elapsed_time(b) for a, b in ev[eq]) / args.steps for eq in eqs}
 
-    # kernel-duration pass: the same K steps again with every launch of our
-    # kernels bracketed by CUDA events on the launching stream (kept out of
-    # the headline pass, whose host side it would slow down)
-    fresh()
+    # kernel-duration pass: the same K steps again, one stream, with every
+    # launch of our kernels bracketed by CUDA events on the launching stream
+    # (kept out of the headline pass, whose host side it would slow down)
+    fresh_seq()
     for p in plans:
         p.reset_kernel_times()
         p.set_timing(True)
     for _ in range(args.steps):
         for eq in eqs:
-            advance(eq)
+            seq_advance(eq)
     torch.cuda.synchronize()
     for c in ctxs.values():
         c.flush()
@@ -401,13 +454,17 @@ def run_ours(args):
         s2 = torch.cuda.Event(enable_timing=True)
         e2 = torch.cuda.Event(enable_timing=True)
         s2.record(stream)
+        fork()
         for _ in range(args.steps):
             for eq in eqs:
                 st = advance(eq)
                 # D2H on the context's copy stream, overlapping the next steps
-                ctxs[eq].field_to_host(st.u, pinned[eq], packed=True)
-        for c in ctxs.values():
-            c.host_sync()
+                with torch.cuda.stream(eq_stream[eq]):
+                    ctxs[eq].field_to_host(st.u, pinned[eq], packed=True)
+        for eq, c in ctxs.items():
+            with torch.cuda.stream(eq_stream[eq]):
+                c.host_sync()
+        join()
         e2.record(stream)
         torch.cuda.synchronize()
         for c in ctxs.values():
@@ -425,7 +482,7 @@ def run_ours(args):
         for c in ctxs.values():
             c.flush()
             c.operator = False
-        fresh()
+        fresh_seq()
         torch.cuda.synchronize()
         pipe_it = {eq: [] for eq in eqs}
         pev = {eq: [] for eq in eqs}
@@ -439,7 +496,7 @@ def run_ours(args):
                 a = torch.cuda.Event(enable_timing=True)
                 b = torch.cuda.Event(enable_timing=True)
                 a.record(stream)
-                st = advance(eq)
+                st = seq_advance(eq)
                 b.record(stream)
                 pev[eq].append((a, b))
                 pipe_it[eq].append(st.last_iterations)
@@ -512,8 +569,15 @@ def run_ours(args):
         "dtype": "f64 (heat, wave) / c128 (schrodinger)",
         "data": "synthetic: closed-form manufactured solutions (no RNG), random-free geometry",
         "config": config_obj(m, eqs, ws),
+        "schedule": ("one CUDA stream per equation (the three problems are independent; "
+                     "their latency-bound phases overlap)" if not args.sequential else
+                     "one stream (equations one after another)"),
+        "sequential": {"value": n_time_steps * ws / (seq_ms / 1e3), "ms_per_step": seq_ms / args.steps,
+                       "note": "the same K steps on one stream, equations one after another"},
         "per_equation": {eq: {"steps_per_s": 1e3 / per_eq_ms[eq], "ms_per_step": per_eq_ms[eq],
-                              "iterations": iters[eq]} for eq in eqs},
+                              "iterations": iters[eq],
+                              "iterations_one_stream_equal": seq_iters[eq] == iters[eq][:len(seq_iters[eq])]}
+                         for eq in eqs},
         "kernel_ms_per_bench_step": {kname: v / args.steps for kname, v in kt_ms.items() if v},
         "kernel_calls": {kname: v for kname, v in kt_calls.items() if v},
         "roofline": {
@@ -1085,6 +1149,8 @@ def main(argv=None):
     ap.add_argument("--slab-steps", type=int, default=3)
     ap.add_argument("--slab-mode", choices=["a2a", "p2p", "carry"], default=None,
                     help="c5: slab exchange (default a2a, or p2p with --p2p)")
+    ap.add_argument("--sequential", action="store_true",
+                    help="step the three equations on one stream (default: one stream each)")
     ap.add_argument("--pipeline", action="store_true",
                     help="run every Richardson sweep through the full pipeline (no trace operator)")
     args = ap.parse_args(argv)

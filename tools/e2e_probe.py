@@ -38,13 +38,33 @@ def adv(eq):
 pinned = {eq: torch.empty(ctxs[eq].interior_index.numel(),
                           dtype=torch.complex128 if eq == "schrodinger" else torch.float64,
                           pin_memory=True) for eq in eqs}
-for _ in range(4):
+startups = {eq: _stepper_for(specs[eq])[0] for eq in eqs}
+
+
+def fresh():
+    # every loop from t = 0 (+ 3 warm steps), as bench.py: the same steps timed
+    for c in ctxs.values():
+        c.flush()
     for eq in eqs:
-        adv(eq)
-torch.cuda.synchronize()
+        states[eq] = startups[eq](specs[eq], ctxs[eq])
+    for _ in range(3):
+        for eq in eqs:
+            adv(eq)
+    torch.cuda.synchronize()
+    for c in ctxs.values():
+        c.flush()
+
+
+fresh()
+
+
+full = {eq: torch.empty((4097 * 4097,), dtype=torch.complex128 if eq == "schrodinger" else torch.float64,
+                        pin_memory=True) for eq in eqs}
+side = torch.cuda.Stream()
 
 
 def loop(mode):
+    fresh()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
@@ -58,6 +78,8 @@ def loop(mode):
                 c.plan.gather(c.interior_index, s.u, buf)
             elif mode == "copy":
                 ctxs[eq].field_to_host(s.u, pinned[eq], packed=True)
+            elif mode == "fullcopy":
+                ctxs[eq].field_to_host(s.u, full[eq], packed=False)
     for c in ctxs.values():
         c.host_sync()
     b.record()
@@ -69,6 +91,6 @@ def loop(mode):
 
 
 for rep in range(2):
-    for mode in ("plain", "gather", "copy", "plain"):
+    for mode in ("plain", "gather", "copy", "fullcopy", "plain"):
         dev, wall = loop(mode)
         print(f"{mode:7s} device {dev:7.3f} ms / bench step   host wall {wall:7.3f} ms", flush=True)
