@@ -410,6 +410,33 @@ def run_ours(args):
         p.set_timing(False)
     clocks = clk.summary()
 
+    # matrix-free edge values (fp64-bound): spec_block (DFT of
+    # the five used jump columns) + edges_spectral_res (one frequency sum per
+    # crossing) on the heat geometry, event-timed; flops counted per (control,
+    # frequency) and per (crossing, frequency)
+    mf = None
+    hp = ctxs.get("heat")
+    if hp is not None and hp.plan.spectral_edges:
+        n = hp.plan.n_ctl
+        jm = torch.randn((6, n), dtype=torch.float64, device=f"cuda:{local}")
+        jv = torch.empty(3 * hp.plan.n_edges, dtype=torch.float64, device=f"cuda:{local}")
+        hp.plan.edge_values(jm, jv)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(20):
+            hp.plan.edge_values(jm, jv)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        t_ms = e0.elapsed_time(e1) / 20
+        K = n // 2 + 1
+        flops = 26.0 * n * K + 18.0 * hp.plan.n_edges * (n // 2 - 1)
+        mf = {"kernels": "spec_block_kernel + edges_spectral_res_kernel (heat, flower8)",
+              "n_ctl": n, "n_edges": hp.plan.n_edges, "flops_per_call": flops, "ms_per_call": t_ms,
+              "achieved_tflops": flops / (t_ms / 1e3) / 1e12, "peak_tflops": FP64_PEAK_TFLOPS,
+              "peak_source": "measured fp64 FMA peak (tools/mb/dfma.cu, DESIGN.md §4)",
+              "frac": flops / (t_ms / 1e3) / 1e12 / FP64_PEAK_TFLOPS, "bound": "fp64"}
+
     elapsed_max = elapsed_ms
     n_time_steps = args.steps * len(eqs)
     value = n_time_steps * ws / (elapsed_max / 1e3)
@@ -581,6 +608,7 @@ def run_ours(args):
         "kernel_ms_per_bench_step": {kname: v / args.steps for kname, v in kt_ms.items() if v},
         "kernel_calls": {kname: v for kname, v in kt_calls.items() if v},
         "roofline": {
+            "matrix_free_edges": mf,
             "kernel": kernel_name[dom],
             "bound": "hbm", "achieved": roof[dom]["achieved"], "peak": peaks["hbm_gbs"],
             "unit": "GB/s", "frac": roof[dom]["frac"],
@@ -960,6 +988,9 @@ def run_c5(args):
         "iterations": it, "residual": res, "max_err_interior": err, "setup_s": setup_s,
         "n_ctl": int(cps.m),
     }
+
+
+FP64_PEAK_TFLOPS = 33.7     # measured DFMA throughput, tools/mb/dfma.cu
 
 
 def _peaks():

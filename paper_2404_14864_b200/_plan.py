@@ -113,6 +113,7 @@ class Plan:
             **{k: v.ctypes.data for k, v in t.items()})
         N.check(self._lib.kfbi_plan_set_geometry(self.handle, C.byref(g)))
         self.n_ctl = int(tables["n_ctl"])
+        self.n_edges = int(t["edge_axis"].size)
         self.has_geometry = True
 
     def set_interp(self, mode):

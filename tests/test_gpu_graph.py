@@ -90,3 +90,47 @@ def test_graph_reuse_and_log_ring_wrap(monkeypatch):
     assert ctx._step_graph is sg                     # reused, not recaptured
     assert first.iterations == g and second.iterations == g
     assert np.array_equal(first.state.u, second.state.u)
+
+
+@pytest.mark.parametrize("cplx", [False, True], ids=["f64", "c128"])
+def test_one_cta_operator_sweeps_match_grid_kernels(monkeypatch, cplx):
+    # op_solve_cta_kernel (n_ctl <= 160, no grid barrier) against the
+    # cooperative grid kernels (KFBI_OP_CTA=0): same sweeps, same field to
+    # rounding (the row sums are ordered differently)
+    from paper_2404_14864_b200 import boxsolve
+
+    res = {}
+    for flag in ("1", "0"):
+        monkeypatch.setenv("KFBI_OP_CTA", flag)
+        boxsolve._GRID_PLANS.clear()
+        box, curve, kw = _spec("schrodinger" if cplx else "heat", 1 / 64, 8 / 64)
+        geo = k.build_grid(box, 128, curve)
+        ctx = k.StepContext(geo, backend=k.CudaBackend(0, timing=False))
+        assert ctx.n_ctl <= 160
+        res[flag] = k.run(k.ProblemSpec(**kw), geo, context=ctx, operator=True, graph=False)
+    boxsolve._GRID_PLANS.clear()
+    assert res["1"].iterations == res["0"].iterations
+    a, b = np.asarray(res["1"].state.u), np.asarray(res["0"].state.u)
+    assert np.max(np.abs(a - b)) <= 1e-12 * np.max(np.abs(b))
+
+
+def test_staged_edge_values_bit_identical(monkeypatch):
+    # corr_edges_smem_kernel (JM staged per CTA) against the per-warp W-row
+    # kernel: the same per-lane summation order, so the same bits
+    import torch
+
+    from paper_2404_14864_b200 import boxsolve
+
+    out = {}
+    for flag in ("1", "0"):
+        monkeypatch.setenv("KFBI_EDGES_SMEM", flag)
+        boxsolve._GRID_PLANS.clear()
+        ws = k.InterfaceWorkspace(k.build_grid(PI_BOX, 512, k.StarCurve(1.5, c=0.2, lobes=3)))
+        ws.plan.set_interp("w")
+        g = torch.Generator(device="cuda").manual_seed(3)
+        jm = torch.randn((6, ws.cps.m), generator=g, device="cuda", dtype=torch.complex128)
+        jv = torch.zeros(3 * ws.plan.n_edges, device="cuda", dtype=torch.complex128)
+        ws.plan.edge_values(jm, jv)
+        out[flag] = jv.cpu()
+    boxsolve._GRID_PLANS.clear()
+    assert torch.equal(out["1"], out["0"])
