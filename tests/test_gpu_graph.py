@@ -134,3 +134,28 @@ def test_staged_edge_values_bit_identical(monkeypatch):
         out[flag] = jv.cpu()
     boxsolve._GRID_PLANS.clear()
     assert torch.equal(out["1"], out["0"])
+
+
+@pytest.mark.parametrize("eq", ["heat", "wave"])
+def test_graph_replay_neumann(eq):
+    # Neumann runs close the recurrences with the extracted trace (the step's
+    # output, not host data): the captured step carries it through its state
+    heat, wave = k.HeatPlaneDecay(c=1.0), k.WaveStanding(phase=0.0)
+    if eq == "heat":
+        box, curve, kw = BOX, k.StarCurve(1.0, c=0.2, lobes=5), dict(
+            equation="heat", bc_kind="neumann", g=heat.neumann, u0=heat.u0,
+            lap_u0=heat.lap_u0, tau=1 / 32, t_final=10 / 32, c=1.0)
+    else:
+        box, curve, kw = BOX, k.EllipseCurve(1.2, 0.8), dict(
+            equation="wave", bc_kind="neumann", g=wave.neumann, u0=wave.u0,
+            lap_u0=wave.lap_u0, v0=wave.v0, lap_v0=wave.lap_v0, tau=1 / 32, t_final=10 / 32)
+    geo = k.build_grid(box, 64, curve)
+    spec = k.ProblemSpec(**kw)
+    be = k.CudaBackend(0, timing=False)
+    ctx = k.StepContext(geo, operator=True, backend=be)
+    b = k.run(spec, geo, context=ctx, operator=True, graph=True)
+    assert ctx._step_graph is not None
+    a = k.run(spec, geo, context=k.StepContext(geo, operator=True, backend=be), operator=True,
+              graph=False)
+    assert a.iterations == b.iterations
+    assert np.array_equal(a.state.u, b.state.u)
