@@ -148,7 +148,9 @@ def test_graph_replay_neumann(eq):
     else:
         box, curve, kw = BOX, k.EllipseCurve(1.2, 0.8), dict(
             equation="wave", bc_kind="neumann", g=wave.neumann, u0=wave.u0,
-            lap_u0=wave.lap_u0, v0=wave.v0, lap_v0=wave.lap_v0, tau=1 / 32, t_final=10 / 32)
+            lap_u0=wave.lap_u0, v0=wave.v0, lap_v0=wave.lap_v0, tau=0.25, t_final=2.5)
+        # (tau 1/32 does not converge within max_iter for Neumann wave on 64^2
+        # in the reference's Richardson either)
     geo = k.build_grid(box, 64, curve)
     spec = k.ProblemSpec(**kw)
     be = k.CudaBackend(0, timing=False)

@@ -6,6 +6,7 @@ independent problems): device ms per bench step.
 """
 import os
 import sys
+import time
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
@@ -50,10 +51,12 @@ def fresh(conc):
         c.flush()
 
 
-def loop(conc):
-    fresh(conc)
+def loop(conc, do_fresh=True):
+    if do_fresh:
+        fresh(conc)
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record(main)
+    t0 = time.perf_counter()
     if conc:
         for s in streams.values():
             s.wait_stream(main)
@@ -68,9 +71,10 @@ def loop(conc):
         for s in streams.values():
             main.wait_stream(s)
     b.record(main)
+    host = (time.perf_counter() - t0) / K * 1e3
     torch.cuda.synchronize()
     its = {eq: ctxs[eq].flush() for eq in eqs}
-    return a.elapsed_time(b) / K, its
+    return a.elapsed_time(b) / K, its, host
 
 
 if __name__ == "__main__":
@@ -83,8 +87,9 @@ if __name__ == "__main__":
     ref = None
     for rep in range(3):
         for conc in (False, True):
-            ms, its = loop(conc)
+            ms, its, host = loop(conc)
             if ref is None:
                 ref = its
             print(f"{'3 streams' if conc else '1 stream '}: {ms:.3f} ms per bench step "
-                  f"({3000.0 / ms:.1f} time steps/s)  iterations equal: {its == ref}", flush=True)
+                  f"({3000.0 / ms:.1f} time steps/s), host issue {host:.3f} ms per bench step, "
+                  f"iterations equal: {its == ref}", flush=True)
