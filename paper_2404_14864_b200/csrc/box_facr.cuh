@@ -104,10 +104,10 @@ rows_fwd_facr(BoxArgs a, const void *__restrict__ rhs, double sign,
       const T cv = S::rmul(group_correction<T>(corr, g), k);
       const int i = corr.group_node[g] - j * stride;
       if constexpr (CPLX) {
-        double2 &slot = sm[i];
+        double2 &slot = sm.lin(i);
         slot = cadd(slot, cv);
       } else {
-        double *slot = reinterpret_cast<double *>(&sm[i]) + comp;
+        double *slot = reinterpret_cast<double *>(&sm.lin(i)) + comp;
         *slot += cv;
       }
     }
@@ -118,14 +118,12 @@ rows_fwd_facr(BoxArgs a, const void *__restrict__ rhs, double sign,
   T ga[E], gb[E];
   row(J0, ga);
   if constexpr (!CPLX) row(J0 + 2, gb);
-  {
-    double2 v[E];
+  // (linear layout until the FFT: the stencil and the DST pre-processing
+  // read shifted / mirrored windows)
 #pragma unroll
-    for (int m = 0; m < E; ++m) {
-      if constexpr (CPLX) v[m] = ga[m];
-      else v[m] = make_double2(ga[m], gb[m]);
-    }
-    stage<LOGN>(sm, v, t);
+  for (int m = 0; m < E; ++m) {
+    if constexpr (CPLX) sm.lin(t + m * TT) = ga[m];
+    else sm.lin(t + m * TT) = make_double2(ga[m], gb[m]);
   }
   double2 os[E];
   auto load_os = [&] {
@@ -159,9 +157,9 @@ rows_fwd_facr(BoxArgs a, const void *__restrict__ rhs, double sign,
 #pragma unroll
     for (int m = 0; m < E; ++m) {
       const int n = t + m * TT;
-      const double2 l = n >= 1 ? sm[n - 1] : make_double2(0.0, 0.0);
-      const double2 rr = n + 1 <= M - 1 ? sm[n + 1] : make_double2(0.0, 0.0);
-      const double2 cc = sm.xc(t, reg::sw(t), m * TT);
+      const double2 l = n >= 1 ? sm.lin(n - 1) : make_double2(0.0, 0.0);
+      const double2 rr = n + 1 <= M - 1 ? sm.lin(n + 1) : make_double2(0.0, 0.0);
+      const double2 cc = sm.lin(n);
       double2 bg;                                // B g_j at n
       if constexpr (CPLX) bg = csub(cadd(l, rr), cmul(c4, cc));
       else bg = make_double2(l.x + rr.x - c4.x * cc.x, l.y + rr.y - c4.x * cc.y);
@@ -178,7 +176,8 @@ rows_fwd_facr(BoxArgs a, const void *__restrict__ rhs, double sign,
     }
   }
   reg::seq_sync<LOGN>();                         // neighbours read before overwrite
-  stage<LOGN>(sm, w, t);
+#pragma unroll
+  for (int m = 0; m < E; ++m) sm.lin(t + m * TT) = w[m];
   reg::seq_sync<LOGN>();
   // the odd rows' corrections enter w with coefficient 1; rows sharing a
   // component are separated by a barrier
@@ -194,7 +193,23 @@ rows_fwd_facr(BoxArgs a, const void *__restrict__ rhs, double sign,
     }
   }
   double2 out[E];
-  dst_staged<LOGN>(sm, t, a, out);
+  {
+    // DST pre-processing from the linear layout (reg::pre_from_smem with
+    // unswizzled reads), then the FFT and post-processing as dst_staged
+    double2 v[E];
+#pragma unroll
+    for (int m = 0; m < E; ++m) {
+      const int j = t + m * TT;
+      const double2 xj = sm.lin(j);
+      const double2 xr = sm.lin((M - j) & (M - 1));   // j = 0 -> x_0 = 0
+      const double s = __ldg(&a.sinv[j]);
+      const double2 ap = cadd(xj, xr), dm = csub(xj, xr);
+      v[m] = make_double2(fma(s, ap.x, 0.5 * dm.x), fma(s, ap.y, 0.5 * dm.y));
+    }
+    reg::seq_sync<LOGN>();
+    reg::fft<LOGN>(v, sm, t, a.twg);
+    reg::post<LOGN>(sm, t, out);
+  }
   reg::seq_sync<LOGN>();
   unstage<LOGN>(sm, out, t);
   reg::seq_sync<LOGN>();
@@ -294,8 +309,41 @@ rows_odd_facr(BoxArgs a, const void *__restrict__ rhs, double sign,
       else reinterpret_cast<double *>(&rbuf[pos(n)])[comp] = val;
     }
   };
-  form(j, 0);
-  if constexpr (!CPLX) form(j + 2, 1);
+  if constexpr (CPLX) {
+    form(j, 0);
+  } else {
+    // both rows per slot in one 16-byte store (8-byte stores into 16-byte
+    // slots were 2-way bank conflicts): rows j, j + 2 share row j + 1, so
+    // five row loads per element, eight elements in flight
+    const double *R = static_cast<const double *>(rhs);
+    const double *U = static_cast<const double *>(u);
+    const double *F0 = R + (size_t)j * stride, *F1 = F0 + 2 * (size_t)stride;
+    const double *Ua = U + (size_t)(j - 1) * stride;     // u_{j-1}
+    const double *Ub = Ua + 2 * (size_t)stride;          // u_{j+1}
+    const double *Uc = Ub + 2 * (size_t)stride;          // u_{j+3}
+    const bool ha = j - 1 >= 1, hc = j + 3 <= M - 1;
+    constexpr int HB = CH >= 8 ? 8 : CH;
+#pragma unroll
+    for (int e0 = 0; e0 < CH; e0 += HB) {
+      double f0[HB], f1[HB], la[HB], lb[HB], lc[HB];
+#pragma unroll
+      for (int e = 0; e < HB; ++e) {
+        const int n = t + NT * (e0 + e);
+        f0[e] = rhs ? F0[n] : 0.0;
+        f1[e] = rhs ? F1[n] : 0.0;
+        la[e] = ha ? Ua[n] : 0.0;
+        lb[e] = Ub[n];
+        lc[e] = hc ? Uc[n] : 0.0;
+      }
+#pragma unroll
+      for (int e = 0; e < HB; ++e) {
+        const int n = t + NT * (e0 + e);
+        const double v0 = f0[e] * (sign * h2) - la[e] - lb[e];
+        const double v1 = f1[e] * (sign * h2) - lb[e] - lc[e];
+        rbuf[pos(n)] = n == 0 ? make_double2(0.0, 0.0) : make_double2(v0, v1);
+      }
+    }
+  }
   __syncthreads();
   if (corr.jv) {                                 // corrections of the row(s), h^2 scaled:
     for (int k2 = 0; k2 < (CPLX ? 1 : 2); ++k2) {  // distinct nodes, one thread each

@@ -282,6 +282,11 @@ rows_inv_reg(BoxArgs a, void *__restrict__ u) {
   if (a.done && *a.done) return;
   int seq, t;
   const reg::View<LOGN> sm = reg::make_view<LOGN>(smem, seq, t);
+  // staging slot of element n: linear for one-CTA sequences (see View::lin)
+  auto stg = [&](int n) -> double2 & {
+    if constexpr (C::CL == 1) return sm.lin(n);
+    else return sm[n];
+  };
   const int stride = M + 1;
   const int q = seq_index<LOGN>(seq);
   const int nseq = CPLX ? a.rows : a.rows / 2;
@@ -304,8 +309,8 @@ rows_inv_reg(BoxArgs a, void *__restrict__ u) {
     for (int m = 0; m < reg::E; ++m) {
       const int i = t + m * TT, pp = i >> 2, part = i & 3, row = part >> 1;
       const int n0 = 4 * pp + 2 * (part & 1);
-      double *s0 = reinterpret_cast<double *>(&sm[n0]) + row;
-      double *s1 = reinterpret_cast<double *>(&sm[n0 + 1]) + row;
+      double *s0 = reinterpret_cast<double *>(&stg(n0)) + row;
+      double *s1 = reinterpret_cast<double *>(&stg(n0 + 1)) + row;
       *s0 = n0 == 0 ? 0.0 : v[m].x;            // x_0 = 0
       *s1 = v[m].y;
     }
@@ -316,11 +321,30 @@ rows_inv_reg(BoxArgs a, void *__restrict__ u) {
       const int n = t + m * TT;
       v[m] = (valid && n >= 1) ? P2[((n >> 1) * R + r0) * 2 + (n & 1)] : make_double2(0.0, 0.0);
     }
-    stage<LOGN>(sm, v, t);
+#pragma unroll
+    for (int m = 0; m < reg::E; ++m) stg(t + m * TT) = v[m];
   }
   reg::seq_sync<LOGN>();
   double2 out[reg::E];
-  dst_staged<LOGN>(sm, t, a, out);
+  if constexpr (C::CL == 1) {
+    // pre-processing from the linear staging (mirror reads without the
+    // swizzle-group conflicts), then the FFT and post-processing
+    double2 v[reg::E];
+#pragma unroll
+    for (int m = 0; m < reg::E; ++m) {
+      const int j = t + m * TT;
+      const double2 xj = sm.lin(j);
+      const double2 xr = sm.lin((M - j) & (M - 1));
+      const double s = __ldg(&a.sinv[j]);
+      const double2 ap = cadd(xj, xr), dm = csub(xj, xr);
+      v[m] = make_double2(fma(s, ap.x, 0.5 * dm.x), fma(s, ap.y, 0.5 * dm.y));
+    }
+    reg::seq_sync<LOGN>();
+    reg::fft<LOGN>(v, sm, t, a.twg);
+    reg::post<LOGN>(sm, t, out);
+  } else {
+    dst_staged<LOGN>(sm, t, a, out);
+  }
   reg::seq_sync<LOGN>();
   unstage<LOGN>(sm, out, t);
   reg::seq_sync<LOGN>();

@@ -96,6 +96,13 @@ struct View {
   // XOR with a small constant and an immediate offset instead of the full
   // swizzle per access (the integer work was ~40 % of the DST kernels'
   // instructions).
+  // unswizzled slot i (one-CTA sequences): for stencil and mirror reads,
+  // whose shifted windows straddle swizzle groups (2-way conflicts of the
+  // 16-byte accesses per quarter warp); a linear window never conflicts
+  KFBI_DEV double2 &lin(int i) const {
+    static_assert(C::CL == 1, "linear view: one-CTA sequences");
+    return p[0][i];
+  }
   KFBI_DEV double2 &xc(int x, int xs, int c) const {
     if constexpr (C::CL == 1) return p[0][(xs ^ ((((c >> 3) ^ (c >> 6)) & 7) ^ (c & 7))) + (c & ~7)];
     else return (*this)[x + c];

@@ -1262,7 +1262,6 @@ op_solve_cta_kernel(OpSolveArgs a, const T *__restrict__ Tcm, T *A, T *B,
   T *ph = Ts + (size_t)n * n;                            // [2][n] iterates
   T *d = ph + 2 * n, *p0 = d + n, *t1 = p0 + n, *gs = t1 + n;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  constexpr int NW = OPC_THREADS / 32;
   if (a.st->done) return;                       // uniform: set before launch
   for (int i = tid; i < n * n; i += OPC_THREADS) {   // Ts[q n + c] = Tcm[c n + q]
     const int q = i / n, c = i - q * n;
