@@ -480,6 +480,11 @@ kfbi_status kfbi_log_fetch(kfbi_plan *plan, int32_t first, int32_t count,
  * graph logs into a fixed slot): zero `count` entries from `slot`, copy
  * `count` entries from `src` to `dst`. */
 kfbi_status kfbi_log_clear(kfbi_plan *plan, int32_t slot, int32_t count, void *stream);
+/* The caller guarantees that the F_new / out / F buffers it passes with a
+ * mask to kfbi_heat_rhs, kfbi_wave_rhs, kfbi_nonlinear_phase and
+ * kfbi_strang_phase already hold zeros outside the mask (the stepper's
+ * zero-initialised buffer rings): the kernels then skip those stores. */
+kfbi_status kfbi_plan_set_exterior_zero(kfbi_plan *plan, int32_t on);
 kfbi_status kfbi_log_copy(kfbi_plan *plan, int32_t src, int32_t dst, int32_t count, void *stream);
 
 /* Per-kernel-name device time (ms) and call counts since the last reset

@@ -384,6 +384,11 @@ class Plan:
     def log_norm(self, slot, which=0):
         N.check(self._lib.kfbi_log_norm(self.handle, int(slot), int(which), self.stream))
 
+    def set_exterior_zero(self, on):
+        """The masked outputs of the right-hand-side kernels are zero outside
+        the mask already (kfbi_plan_set_exterior_zero)."""
+        N.check(self._lib.kfbi_plan_set_exterior_zero(self.handle, int(bool(on))))
+
     def log_clear(self, slot, count=1):
         N.check(self._lib.kfbi_log_clear(self.handle, int(slot), int(count), self.stream))
 

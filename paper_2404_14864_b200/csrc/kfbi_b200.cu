@@ -134,6 +134,7 @@ struct kfbi_plan {
   bool facr = true;                 // kfbi_plan_set_facr: cyclic-reduction box solve
   bool edges_smem = true;           // W-row edge values with JM staged per CTA (env KFBI_EDGES_SMEM=0: per warp)
   bool op_cta = true;               // operator sweeps of n_ctl <= 160 in one CTA (env KFBI_OP_CTA=0: grid kernels)
+  bool ext_zero = false;            // kfbi_plan_set_exterior_zero: masked outputs already zero outside the mask
   DevBuf<double2> sn_vals, sn_v13;
   DevBuf<int> skip;
   DevBuf<StepLog> log;
@@ -1897,6 +1898,12 @@ kfbi_status kfbi_log_fetch(kfbi_plan *p, int32_t first, int32_t count, kfbi_step
   return KFBI_OK;
 }
 
+kfbi_status kfbi_plan_set_exterior_zero(kfbi_plan *p, int32_t on) {
+  KFBI_TRY(check_plan(p));
+  p->ext_zero = on != 0;
+  return KFBI_OK;
+}
+
 kfbi_status kfbi_log_clear(kfbi_plan *p, int32_t slot, int32_t count, void *stream) {
   KFBI_TRY(check_plan(p));
   if (slot < 0 || count < 0 || slot + count > p->log_cap) return fail(KFBI_E_CONFIG, "log range out of bounds");
@@ -1924,9 +1931,9 @@ kfbi_status kfbi_heat_rhs(kfbi_plan *p, int64_t n, const uint8_t *mask, void *u,
     auto *fo = static_cast<const double *>(F_old);
     auto *fn = static_cast<double *>(F_new);
     if (aligned16({uu, fo, fn}) && !((uintptr_t)mask & 1))
-      heat_rhs_kernel<true><<<pair_blocks(n), 256, 0, s>>>(n, mask, uu, fo, fn, a, p->red.p);
+      heat_rhs_kernel<true><<<pair_blocks(n), 256, 0, s>>>(n, mask, uu, fo, fn, a, p->red.p, p->ext_zero);
     else
-      heat_rhs_kernel<false><<<elem_blocks(n), 256, 0, s>>>(n, mask, uu, fo, fn, a, p->red.p);
+      heat_rhs_kernel<false><<<elem_blocks(n), 256, 0, s>>>(n, mask, uu, fo, fn, a, p->red.p, p->ext_zero);
   }));
   return norm_out ? read_norm(p, s, norm_out) : KFBI_OK;
 }
@@ -1944,9 +1951,9 @@ kfbi_status kfbi_wave_rhs(kfbi_plan *p, int64_t n, const uint8_t *mask, void *u_
     auto *fp = static_cast<const double *>(F_prev);
     auto *fn = static_cast<double *>(F_new);
     if (aligned16({un, uc, fc, fp, fn}) && !((uintptr_t)mask & 1))
-      wave_rhs_kernel<true><<<pair_blocks(n), 256, 0, s>>>(n, mask, un, uc, fc, fp, fn, kw, coef, p->red.p);
+      wave_rhs_kernel<true><<<pair_blocks(n), 256, 0, s>>>(n, mask, un, uc, fc, fp, fn, kw, coef, p->red.p, p->ext_zero);
     else
-      wave_rhs_kernel<false><<<elem_blocks(n), 256, 0, s>>>(n, mask, un, uc, fc, fp, fn, kw, coef, p->red.p);
+      wave_rhs_kernel<false><<<elem_blocks(n), 256, 0, s>>>(n, mask, un, uc, fc, fp, fn, kw, coef, p->red.p, p->ext_zero);
   }));
   return norm_out ? read_norm(p, s, norm_out) : KFBI_OK;
 }
@@ -1971,7 +1978,7 @@ kfbi_status kfbi_nonlinear_phase(kfbi_plan *p, int64_t n, const void *ustar, con
   KFBI_TRY(launch(p, KFBI_K_RHS, s, [&] {
     nonlinear_phase_kernel<<<elem_blocks(n), 256, 0, s>>>(
         n, static_cast<const double2 *>(ustar), nullptr, 0, 0.0, v, w, half_tau, mask,
-        static_cast<double2 *>(out), kre, kim, static_cast<double2 *>(F), p->red.p);
+        static_cast<double2 *>(out), kre, kim, static_cast<double2 *>(F), p->red.p, p->ext_zero);
   }));
   if (!max_res) return KFBI_OK;    // asynchronous: the caller logs red[0] (kfbi_log_norm)
   double r = 0.0;
@@ -1996,7 +2003,8 @@ kfbi_status kfbi_strang_phase(kfbi_plan *p, int64_t n, int32_t mode, const void 
   KFBI_TRY(launch(p, KFBI_K_RHS, s, [&] {
     nonlinear_phase_kernel<<<elem_blocks(n), 256, 0, s>>>(
         n, static_cast<const double2 *>(u), static_cast<const double2 *>(other), mode, tau, v, w,
-        half_tau, mask, static_cast<double2 *>(out), kre, kim, static_cast<double2 *>(F), p->red.p);
+        half_tau, mask, static_cast<double2 *>(out), kre, kim, static_cast<double2 *>(F), p->red.p,
+        p->ext_zero);
   }));
   if (!max_res) return KFBI_OK;
   double r = 0.0;

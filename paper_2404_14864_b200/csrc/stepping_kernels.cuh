@@ -105,6 +105,7 @@ struct HeatOp {
   const double *__restrict__ F_old;
   double *__restrict__ F_new;
   double a, mag;
+  bool ext_zero;                  // F_new is already zero outside the mask
   template <int K>
   KFBI_DEV void pair(long i0, long i1) {
     const long ii[2] = {i0, i1};
@@ -128,7 +129,8 @@ struct HeatOp {
         if (!mk[k].y) v[k].y = 0.0;
         reinterpret_cast<double2 *>(u)[ii[k]] = v[k];
       }
-      reinterpret_cast<double2 *>(F_new)[ii[k]] = make_double2(a * v[k].x - fo[k].x, a * v[k].y - fo[k].y);
+      if (!ext_zero || (mk[k].x | mk[k].y))
+        reinterpret_cast<double2 *>(F_new)[ii[k]] = make_double2(a * v[k].x - fo[k].x, a * v[k].y - fo[k].y);
       mag = nanmax(mag, nanmax(fabs(v[k].x), fabs(v[k].y)));
     }
   }
@@ -143,8 +145,8 @@ struct HeatOp {
 template <bool VEC>
 __global__ void __launch_bounds__(256) heat_rhs_kernel(long n, const unsigned char *mask, double *u,
                                                        const double *F_old, double *F_new, double a,
-                                                       unsigned long long *norm) {
-  HeatOp op{mask, u, F_old, F_new, a, 0.0};
+                                                       unsigned long long *norm, bool ext_zero) {
+  HeatOp op{mask, u, F_old, F_new, a, 0.0, ext_zero && mask != nullptr};
   elementwise_pairs<VEC>(n, op);
   block_nanmax_to(norm, op.mag);
 }
@@ -157,6 +159,7 @@ struct WaveOp {
   const double *__restrict__ uc, *__restrict__ fc, *__restrict__ fp;
   double *__restrict__ F_new;
   double kw, coef, mag;
+  bool ext_zero;                  // F_new is already zero outside the mask
   KFBI_DEV double f(double v, double c, double fcv, double fpv) const {
     return (2.0 * v - c) * kw + coef * (kw * v - fcv) + (kw * c - fpv);
   }
@@ -185,8 +188,9 @@ struct WaveOp {
         if (!mk[k].y) v[k].y = 0.0;
         reinterpret_cast<double2 *>(un)[ii[k]] = v[k];
       }
-      reinterpret_cast<double2 *>(F_new)[ii[k]] =
-          make_double2(f(v[k].x, c[k].x, a[k].x, b[k].x), f(v[k].y, c[k].y, a[k].y, b[k].y));
+      if (!ext_zero || (mk[k].x | mk[k].y))
+        reinterpret_cast<double2 *>(F_new)[ii[k]] =
+            make_double2(f(v[k].x, c[k].x, a[k].x, b[k].x), f(v[k].y, c[k].y, a[k].y, b[k].y));
       mag = nanmax(mag, nanmax(fabs(v[k].x), fabs(v[k].y)));
     }
   }
@@ -202,8 +206,9 @@ template <bool VEC>
 __global__ void __launch_bounds__(256) wave_rhs_kernel(long n, const unsigned char *mask, double *un,
                                                        const double *uc, const double *fc,
                                                        const double *fp, double *F_new, double kw,
-                                                       double coef, unsigned long long *norm) {
-  WaveOp op{mask, un, uc, fc, fp, F_new, kw, coef, 0.0};
+                                                       double coef, unsigned long long *norm,
+                                                       bool ext_zero) {
+  WaveOp op{mask, un, uc, fc, fp, F_new, kw, coef, 0.0, ext_zero && mask != nullptr};
   elementwise_pairs<VEC>(n, op);
   block_nanmax_to(norm, op.mag);
 }
@@ -291,13 +296,15 @@ nonlinear_phase_kernel(long n, const double2 *__restrict__ ustar, const double2 
                        int mode, double tau, const double *__restrict__ v, double w, double c,
                        const unsigned char *__restrict__ mask, double2 *__restrict__ out,
                        double kre, double kim, double2 *__restrict__ F,
-                       unsigned long long *max_res) {
+                       unsigned long long *max_res, bool ext_zero = false) {
   double worst = 0.0;
   for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n;
        i += (long)gridDim.x * blockDim.x) {
     if (mask && !mask[i]) {                      // u* = 0 there: Newton returns 0, residual 0
-      out[i] = make_double2(0.0, 0.0);
-      if (F) F[i] = make_double2(0.0, 0.0);
+      if (!ext_zero) {                           // (ext_zero: out / F already hold the zeros)
+        out[i] = make_double2(0.0, 0.0);
+        if (F) F[i] = make_double2(0.0, 0.0);
+      }
       continue;
     }
     double r;
