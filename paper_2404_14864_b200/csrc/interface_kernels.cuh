@@ -527,6 +527,96 @@ corr_edges_smem_kernel(EdgeArgs ea, const T *__restrict__ jm, T *jv, const int *
   }
 }
 
+// The same with ALL of the five used JM columns staged once per CTA (when
+// they fit in shared memory: n_ctl <= ~2,800 complex / ~5,600 real): no
+// barrier inside the control loop, so the warps drift apart and one warp's
+// W loads overlap another's FMAs.
+template <typename T, int EW>
+__global__ void __launch_bounds__(CE_WARPS * 32, 1)
+corr_edges_full_kernel(EdgeArgs ea, const T *__restrict__ jm, T *jv, const int *done) {
+  using S = Sc<T>;
+  constexpr int UP = sizeof(T) == 16 && EW >= 4 ? 2 : 4;
+  extern __shared__ __align__(16) unsigned char ce_smem[];
+  if (done && *done) return;
+  const int n = ea.n_ctl;
+  const int nh = (n + 1) >> 1;                   // pairs per parity
+  T *js = reinterpret_cast<T *>(ce_smem);        // [5][2][nh]
+  for (int idx = threadIdx.x; idx < 5 * 2 * nh; idx += CE_WARPS * 32) {
+    const int col = idx / (2 * nh), r = idx - col * 2 * nh, h = r / nh, k2 = r - h * nh;
+    const int i = 2 * k2 + h;
+    const int off = col == 4 ? 5 : col;          // u, u_x, u_y, u_xx, u_yy
+    js[idx] = i < n ? jm[(size_t)off * n + i] : S::zero();
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int gw = blockIdx.x * CE_WARPS + (threadIdx.x >> 5);
+  const int e0 = gw * ea.per_warp;
+  const int e_end = min(e0 + ea.per_warp, ea.n_edges);
+  const int nq = e_end - e0;
+  if (nq <= 0) return;
+  bool vert[EW];
+  const double2 *wr[EW];
+#pragma unroll
+  for (int q = 0; q < EW; ++q) {
+    const int e = e0 + min(q, nq - 1);
+    vert[q] = ea.axis[e] != 0;
+    wr[q] = reinterpret_cast<const double2 *>(ea.W + (size_t)e * ea.ld);
+  }
+  T acc[EW][3];
+#pragma unroll
+  for (int q = 0; q < EW; ++q) acc[q][0] = acc[q][1] = acc[q][2] = S::zero();
+  const int n2 = ea.ld >> 1;
+  auto J = [&](int col, int h, int k2) -> T { return js[(col * 2 + h) * nh + k2]; };
+  for (int c2 = 0; c2 < n2; c2 += 32 * UP) {     // control pairs c2 + lane + 32 u
+    double2 w2[UP][EW];
+#pragma unroll
+    for (int u = 0; u < UP; ++u) {
+      const int i2 = c2 + lane + 32 * u;
+      const bool ok = i2 < n2;
+#pragma unroll
+      for (int q = 0; q < EW; ++q) {
+        if (ok && q < nq) {
+          asm volatile("ld.global.cs.v2.f64 {%0,%1}, [%2];"
+                       : "=d"(w2[u][q].x), "=d"(w2[u][q].y) : "l"(wr[q] + i2));
+        } else {
+          w2[u][q] = make_double2(0.0, 0.0);
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < UP; ++u) {
+      const int k2 = min(c2 + lane + 32 * u, nh - 1);   // pairs past n: W is zero there
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const T a0 = J(0, h, k2), ax = J(1, h, k2), ay = J(2, h, k2), axx = J(3, h, k2),
+                ayy = J(4, h, k2);
+#pragma unroll
+        for (int q = 0; q < EW; ++q) {
+          const double w = h ? w2[u][q].y : w2[u][q].x;
+          acc[q][0] = S::add(acc[q][0], S::rmul(a0, w));
+          acc[q][1] = S::add(acc[q][1], S::rmul(vert[q] ? ay : ax, w));
+          acc[q][2] = S::add(acc[q][2], S::rmul(vert[q] ? ayy : axx, w));
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < EW; ++q) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) acc[q][c] = warp_reduce_T(acc[q][c]);
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int q = 0; q < EW; ++q) {
+      if (q < nq) {
+        jv[3 * (e0 + q)] = acc[q][0];
+        jv[3 * (e0 + q) + 1] = acc[q][1];
+        jv[3 * (e0 + q) + 2] = acc[q][2];
+      }
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Matrix-free edge values (the trig branch of interp_rows, interface.py:38-52,
 // 70-75).  For the reference's equispaced controls theta_j = 2 pi j / n (n

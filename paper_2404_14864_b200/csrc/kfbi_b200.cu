@@ -134,6 +134,7 @@ struct kfbi_plan {
   bool facr = true;                 // kfbi_plan_set_facr: cyclic-reduction box solve
   bool edges_smem = true;           // W-row edge values with JM staged per CTA (env KFBI_EDGES_SMEM=0: per warp)
   bool op_cta = true;               // operator sweeps of n_ctl <= 160 in one CTA (env KFBI_OP_CTA=0: grid kernels)
+  bool edges_full = true;           // staged edge values with all of JM in shared memory (env KFBI_EDGES_FULL=0)
   bool ext_zero = false;            // kfbi_plan_set_exterior_zero: masked outputs already zero outside the mask
   DevBuf<double2> sn_vals, sn_v13;
   DevBuf<int> skip;
@@ -590,11 +591,28 @@ kfbi_status edges_T(kfbi_plan *p, const void *jm, void *jv, const int *done, cud
   const int pw_s = (p->n_edges + wave_s - 1) / wave_s;
   if (p->edges_smem && pw_s <= 4) {
     const int pw = pw_s;
+    static int optin_ce = 0;
+    if (!optin_ce) cudaDeviceGetAttribute(&optin_ce, cudaDevAttrMaxSharedMemoryPerBlockOptin, p->device);
+    const size_t full_bytes = (size_t)5 * 2 * ((p->n_ctl + 1) / 2) * sizeof(T);
     auto go = [&](auto ew) {
       constexpr int E = decltype(ew)::value;
       EdgeArgs ea{p->n_edges, p->n_ctl, p->w_ld, pw, p->W.p, p->edge_axis.p};
       const int warps = (p->n_edges + pw - 1) / pw;
       const int blocks = (warps + CE_WARPS - 1) / CE_WARPS;
+      if (p->edges_full && full_bytes <= (size_t)optin_ce - 2048) {
+        // the whole JM in shared memory: no barrier inside the control loop
+        static bool fattr = false;
+        if (!fattr) {
+          KFBI_CUDA(cudaFuncSetAttribute(corr_edges_full_kernel<T, E>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, optin_ce - 2048),
+                    "jumps-and-corrections");
+          fattr = true;
+        }
+        return launch(p, KFBI_K_JUMPS, s, [&] {
+          corr_edges_full_kernel<T, E><<<blocks, CE_WARPS * 32, full_bytes, s>>>(
+              ea, static_cast<const T *>(jm), static_cast<T *>(jv), done);
+        });
+      }
       return launch(p, KFBI_K_JUMPS, s, [&] {
         corr_edges_smem_kernel<T, E><<<blocks, CE_WARPS * 32, 0, s>>>(
             ea, static_cast<const T *>(jm), static_cast<T *>(jv), done);
@@ -1068,6 +1086,8 @@ kfbi_status kfbi_plan_create(const kfbi_grid_desc *desc, kfbi_plan **out) {
     if (es && es[0] == '0') p->edges_smem = false;
     const char *oc = std::getenv("KFBI_OP_CTA");
     if (oc && oc[0] == '0') p->op_cta = false;
+    const char *ef = std::getenv("KFBI_EDGES_FULL");
+    if (ef && ef[0] == '0') p->edges_full = false;
   }
   cudaError_t e = cudaSetDevice(p->device);
   if (e != cudaSuccess) {
