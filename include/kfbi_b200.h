@@ -485,6 +485,11 @@ kfbi_status kfbi_log_clear(kfbi_plan *plan, int32_t slot, int32_t count, void *s
  * kfbi_strang_phase already hold zeros outside the mask (the stepper's
  * zero-initialised buffer rings): the kernels then skip those stores. */
 kfbi_status kfbi_plan_set_exterior_zero(kfbi_plan *plan, int32_t on);
+/* The mask's interior nodes (increasing flat indices, caller-owned device
+ * array that must outlive its use): with the exterior-zero promise the
+ * masked Newton passes (kfbi_nonlinear_phase, kfbi_strang_phase) then visit
+ * only these nodes.  idx = NULL clears it. */
+kfbi_status kfbi_plan_set_interior_list(kfbi_plan *plan, const int32_t *idx, int64_t count);
 kfbi_status kfbi_log_copy(kfbi_plan *plan, int32_t src, int32_t dst, int32_t count, void *stream);
 
 /* Per-kernel-name device time (ms) and call counts since the last reset

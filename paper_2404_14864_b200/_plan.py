@@ -389,6 +389,14 @@ class Plan:
         the mask already (kfbi_plan_set_exterior_zero)."""
         N.check(self._lib.kfbi_plan_set_exterior_zero(self.handle, int(bool(on))))
 
+    def set_interior_list(self, idx):
+        """Interior node list (device int32 tensor, kept alive by the
+        caller) for the masked Newton passes; None clears it."""
+        if idx is None:
+            N.check(self._lib.kfbi_plan_set_interior_list(self.handle, None, 0))
+        else:
+            N.check(self._lib.kfbi_plan_set_interior_list(self.handle, idx.data_ptr(), int(idx.numel())))
+
     def log_clear(self, slot, count=1):
         N.check(self._lib.kfbi_log_clear(self.handle, int(slot), int(count), self.stream))
 

@@ -136,6 +136,8 @@ struct kfbi_plan {
   bool op_cta = true;               // operator sweeps of n_ctl <= 160 in one CTA (env KFBI_OP_CTA=0: grid kernels)
   bool edges_full = true;           // staged edge values with all of JM in shared memory (env KFBI_EDGES_FULL=0)
   bool ext_zero = false;            // kfbi_plan_set_exterior_zero: masked outputs already zero outside the mask
+  const int *int_idx = nullptr;     // kfbi_plan_set_interior_list: the mask's interior nodes (caller-owned)
+  int64_t n_int = 0;
   DevBuf<double2> sn_vals, sn_v13;
   DevBuf<int> skip;
   DevBuf<StepLog> log;
@@ -1924,6 +1926,14 @@ kfbi_status kfbi_plan_set_exterior_zero(kfbi_plan *p, int32_t on) {
   return KFBI_OK;
 }
 
+kfbi_status kfbi_plan_set_interior_list(kfbi_plan *p, const int32_t *idx, int64_t count) {
+  KFBI_TRY(check_plan(p));
+  if (count < 0 || (count > 0 && !idx)) return fail(KFBI_E_CONFIG, "interior list: bad arguments");
+  p->int_idx = idx;
+  p->n_int = idx ? count : 0;
+  return KFBI_OK;
+}
+
 kfbi_status kfbi_log_clear(kfbi_plan *p, int32_t slot, int32_t count, void *stream) {
   KFBI_TRY(check_plan(p));
   if (slot < 0 || count < 0 || slot + count > p->log_cap) return fail(KFBI_E_CONFIG, "log range out of bounds");
@@ -1996,9 +2006,14 @@ kfbi_status kfbi_nonlinear_phase(kfbi_plan *p, int64_t n, const void *ustar, con
   cudaStream_t s = (cudaStream_t)stream;
   KFBI_CUDA(cudaMemsetAsync(p->red.p, 0, sizeof(unsigned long long), s), "rhs-update");
   KFBI_TRY(launch(p, KFBI_K_RHS, s, [&] {
-    nonlinear_phase_kernel<<<elem_blocks(n), 256, 0, s>>>(
-        n, static_cast<const double2 *>(ustar), nullptr, 0, 0.0, v, w, half_tau, mask,
-        static_cast<double2 *>(out), kre, kim, static_cast<double2 *>(F), p->red.p, p->ext_zero);
+    if (mask && p->ext_zero && p->int_idx)
+      nonlinear_phase_list_kernel<<<elem_blocks(p->n_int), 256, 0, s>>>(
+          p->n_int, p->int_idx, static_cast<const double2 *>(ustar), nullptr, 0, 0.0, v, w, half_tau,
+          static_cast<double2 *>(out), kre, kim, static_cast<double2 *>(F), p->red.p);
+    else
+      nonlinear_phase_kernel<<<elem_blocks(n), 256, 0, s>>>(
+          n, static_cast<const double2 *>(ustar), nullptr, 0, 0.0, v, w, half_tau, mask,
+          static_cast<double2 *>(out), kre, kim, static_cast<double2 *>(F), p->red.p, p->ext_zero);
   }));
   if (!max_res) return KFBI_OK;    // asynchronous: the caller logs red[0] (kfbi_log_norm)
   double r = 0.0;
@@ -2021,10 +2036,16 @@ kfbi_status kfbi_strang_phase(kfbi_plan *p, int64_t n, int32_t mode, const void 
   cudaStream_t s = (cudaStream_t)stream;
   KFBI_CUDA(cudaMemsetAsync(p->red.p, 0, sizeof(unsigned long long), s), "rhs-update");
   KFBI_TRY(launch(p, KFBI_K_RHS, s, [&] {
-    nonlinear_phase_kernel<<<elem_blocks(n), 256, 0, s>>>(
-        n, static_cast<const double2 *>(u), static_cast<const double2 *>(other), mode, tau, v, w,
-        half_tau, mask, static_cast<double2 *>(out), kre, kim, static_cast<double2 *>(F), p->red.p,
-        p->ext_zero);
+    if (mask && p->ext_zero && p->int_idx)
+      nonlinear_phase_list_kernel<<<elem_blocks(p->n_int), 256, 0, s>>>(
+          p->n_int, p->int_idx, static_cast<const double2 *>(u), static_cast<const double2 *>(other),
+          mode, tau, v, w, half_tau, static_cast<double2 *>(out), kre, kim, static_cast<double2 *>(F),
+          p->red.p);
+    else
+      nonlinear_phase_kernel<<<elem_blocks(n), 256, 0, s>>>(
+          n, static_cast<const double2 *>(u), static_cast<const double2 *>(other), mode, tau, v, w,
+          half_tau, mask, static_cast<double2 *>(out), kre, kim, static_cast<double2 *>(F), p->red.p,
+          p->ext_zero);
   }));
   if (!max_res) return KFBI_OK;
   double r = 0.0;

@@ -318,4 +318,31 @@ nonlinear_phase_kernel(long n, const double2 *__restrict__ ustar, const double2 
   block_nanmax_to(max_res, worst);
 }
 
+// The same over an explicit list of the interior nodes (increasing flat
+// indices) when the outputs' exterior is zero already
+// (kfbi_plan_set_exterior_zero + kfbi_plan_set_interior_list): the Newton
+// work is spread evenly over the threads instead of concentrating in the
+// warps that cover the domain (the full-grid pass spent most of its time with
+// exterior warps idle at the block reduction).
+__global__ void __launch_bounds__(256)
+nonlinear_phase_list_kernel(long n_int, const int *__restrict__ idx, const double2 *__restrict__ ustar,
+                            const double2 *__restrict__ other, int mode, double tau,
+                            const double *__restrict__ v, double w, double c,
+                            double2 *__restrict__ out, double kre, double kim, double2 *__restrict__ F,
+                            unsigned long long *max_res) {
+  double worst = 0.0;
+  const double2 kap = make_double2(kre, kim);
+  for (long q = blockIdx.x * (long)blockDim.x + threadIdx.x; q < n_int;
+       q += (long)gridDim.x * blockDim.x) {
+    const long i = idx[q];
+    double r;
+    const double2 us = other ? ustar_of(mode, ustar[i], other[i], tau) : ustar[i];
+    const double2 z = newton_node(us, v[i], w, c, r);
+    worst = nanmax(worst, r);
+    out[i] = z;
+    if (F) F[i] = cmul(kap, z);
+  }
+  block_nanmax_to(max_res, worst);
+}
+
 }  // namespace kfbi
