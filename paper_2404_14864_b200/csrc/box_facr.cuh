@@ -431,6 +431,93 @@ rows_odd_facr(BoxArgs a, const void *__restrict__ rhs, double sign,
 namespace kfbi {
 
 // ---------------------------------------------------------------------------
+// The odd rows of a trace-only first sweep: only the 16-element chunks that
+// hold six-point stencil nodes (BoxArgs.oc_list, built with the geometry).
+// One warp per chunk: the lanes stage the chunk's right-hand side over its
+// windows [s0 - W, s0 + 16 + W] (h^2 g - u_{j-1} - u_{j+1} + corrections, as
+// rows_odd_facr forms it), then lane 0 runs exactly rows_odd_facr's
+// recurrences for that chunk.  The chunks never reach x = 0, where the one
+// boundary term of the full row lives (rho^n z_1 with n >= 64: below the
+// rounding of y).
+constexpr int OS_WARPS = 4;
+template <bool CPLX, int LOGM>
+__global__ void __launch_bounds__(OS_WARPS * 32)
+rows_odd_facr_sparse(BoxArgs a, const void *__restrict__ rhs, double sign,
+                     CorrArgs<typename std::conditional<CPLX, double2, double>::type> corr, void *u) {
+  using T = typename std::conditional<CPLX, double2, double>::type;
+  using S = Sc<T>;
+  constexpr int M = 1 << LOGM, CH = 16, WIN = CH + 2 * ODD_W + 1;
+  __shared__ double2 win[OS_WARPS][WIN];
+  if (a.done && *a.done) return;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int q = blockIdx.x * OS_WARPS + w;
+  if (q >= a.n_oc) return;
+  const int2 jc = a.oc_list[q];
+  const int j = jc.x, s0 = CH * jc.y;
+  const int stride = M + 1;
+  const int lo = s0 - ODD_W, hi = s0 + CH + ODD_W;     // interior windows (checked at build)
+  const double h2 = a.h2;
+  const T *F = static_cast<const T *>(rhs);
+  const T *U = static_cast<const T *>(u);
+  double2 *wb = win[w];
+  for (int k = lane; k <= hi - lo; k += 32) {
+    const int n = lo + k;
+    const T f = rhs ? F[(size_t)j * stride + n] : S::zero();
+    const T l = U[(size_t)(j - 1) * stride + n];
+    const T h = j + 1 <= M - 1 ? U[(size_t)(j + 1) * stride + n] : S::zero();
+    const T val = S::sub(S::sub(S::rmul(f, sign * h2), l), h);
+    if constexpr (CPLX) wb[k] = val;
+    else wb[k] = make_double2(val, 0.0);
+  }
+  __syncwarp();
+  if (corr.jv) {                                 // the row's corrections inside the window
+    const int g0 = corr.row_group[j], g1 = corr.row_group[j + 1];
+    for (int g = g0 + lane; g < g1; g += 32) {
+      const int i = corr.group_node[g] - j * stride;
+      if (i >= lo && i <= hi) {
+        const T cv = S::rmul(group_correction<T>(corr, g), h2);
+        if constexpr (CPLX) wb[i - lo] = cadd(wb[i - lo], cv);
+        else wb[i - lo].x += cv;
+      }
+    }
+  }
+  __syncwarp();
+  if (lane == 0) {
+    const double2 r = tri::root_cplx(make_double2(a.tb_re, a.tb_im));
+    double2 rr;
+    if constexpr (CPLX) rr = r;
+    else rr = make_double2(r.x, r.x);
+    auto x = [&](int n) { return wb[n - lo]; };
+    double2 zch[CH];
+    double2 v = make_double2(0.0, 0.0);
+    for (int n = lo; n < s0; ++n) v = tri::mad<CPLX>(rr, v, cneg(x(n)));
+#pragma unroll
+    for (int e = 0; e < CH; ++e) {
+      v = tri::mad<CPLX>(rr, v, cneg(x(s0 + e)));
+      zch[e] = v;
+    }
+    double2 z = make_double2(0.0, 0.0), pw1 = tri::one<CPLX>();
+    for (int n = s0 + CH; n <= hi; ++n) {
+      v = tri::mad<CPLX>(rr, v, cneg(x(n)));
+      z = tri::mad<CPLX>(pw1, v, z);
+      pw1 = tri::mul<CPLX>(pw1, rr);
+    }
+#pragma unroll
+    for (int e = CH - 1; e >= 0; --e) {
+      z = tri::mad<CPLX>(rr, z, zch[e]);
+      zch[e] = z;
+    }
+    T *Uo = static_cast<T *>(u) + (size_t)j * stride;
+#pragma unroll
+    for (int e = 0; e < CH; ++e) {
+      const double2 y = tri::mul<CPLX>(rr, zch[e]);
+      if constexpr (CPLX) Uo[s0 + e] = y;
+      else Uo[s0 + e] = y.x;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // FACR(1) for REAL data at M = 16384 on the one-real-row-per-CTA engine of
 // box_real.cuh (length-8192 complex FFT with the real split).
 

@@ -19,6 +19,8 @@ struct BoxArgs {
   double tb_re, tb_im;    // trow: beta - 1 of the x recurrence (1 + kappa h^2 / 2)
   double tscale;          // trow: output scale (1)
   void *gsum;             // scratch for the group sums (n_groups slots of 16 bytes)
+  const int2 *oc_list;    // FACR: solve only these (odd row, 16-chunk) pieces of the odd rows
+  int n_oc;               // (trace-only first sweep; nullptr: every odd row)
   void *panels;
   const int *done;        // early-exit flag (Richardson sweeps), may be null
   const double2 *twg;     // [m] exp(-2 pi i q / m)        (register engine)

@@ -122,6 +122,13 @@ kfbi_status box_facr_launch(kfbi_plan *p, const BoxArgs &a0, const void *rhs, do
                                      (int)osm), "diagonal-scale");
       oattr = true;
     }
+    if (a0.oc_list) {                                // trace-only first sweep: the stencil chunks
+      if (a0.n_oc == 0) return KFBI_OK;
+      return kfbi_launch(p, KFBI_K_SCALE, s, [&] {
+        rows_odd_facr_sparse<CPLX, LOGN><<<(a0.n_oc + OS_WARPS - 1) / OS_WARPS, OS_WARPS * 32, 0, s>>>(
+            ao, rhs, sign, cc, u);
+      });
+    }
     return kfbi_launch(p, KFBI_K_SCALE, s, [&] {
       rows_odd_facr<CPLX, LOGN><<<nodd, Rc::NT, osm, s>>>(ao, rhs, sign, cc, u);
     });
@@ -240,6 +247,13 @@ kfbi_status box_facr_real_launch(kfbi_plan *p, const BoxArgs &a0, const void *rh
   ao.tb_re = 1.0 + 0.5 * a0.kre * a0.h2;
   ao.tb_im = 0.0;
   ao.tscale = 1.0;
+  if (a0.oc_list) {                                  // trace-only first sweep: the stencil chunks
+    if (a0.n_oc == 0) return KFBI_OK;
+    return kfbi_launch(p, KFBI_K_SCALE, s, [&] {
+      rows_odd_facr_sparse<false, LOGN><<<(a0.n_oc + OS_WARPS - 1) / OS_WARPS, OS_WARPS * 32, 0, s>>>(
+          ao, rhs, sign, cc, u);
+    });
+  }
   return kfbi_launch(p, KFBI_K_SCALE, s, [&] {
     rows_odd_facr_real1<LOGN><<<M / 2, M / 16, osm, s>>>(ao, static_cast<const double *>(rhs), sign, cc,
                                                          static_cast<double *>(u));

@@ -128,6 +128,9 @@ struct kfbi_plan {
   DevBuf<GmresState> gm_st;
   // stencil nodes grouped by grid row (trace-only sweep 1 of the operator form)
   DevBuf<int> sn_rows, sn_rowptr, sn_cols, sn_map;
+  DevBuf<int2> oc_list;             // (odd row, 16-element chunk) pairs holding stencil nodes
+  int n_oc = 0;                     // 0: the sparse odd-row pass does not apply
+  bool facr_trace = true;           // env KFBI_FACR_TRACE=0: sweep 1 forms the whole field
   DevBuf<double2> gsum;             // group sums of the FACR passes
   int sn_nrows = 0, sn_nodes = 0;
   bool trace_sweep = false;         // kfbi_plan_set_trace_sweep (opt-in: measured no gain)
@@ -251,6 +254,8 @@ BoxArgs box_args(kfbi_plan *p, double kre, double kim, const int *done) {
   a.nranks = 1;
   a.rank = 0;
   for (int h = 0; h < 8; ++h) a.dst[h] = nullptr;
+  a.oc_list = nullptr;
+  a.n_oc = 0;
   return a;
 }
 
@@ -886,6 +891,41 @@ kfbi_status op_solve(kfbi_plan *p, const kfbi_bvp *b, cudaStream_t s) {
   });
 }
 
+// Sweep 1 of the operator form through the FACR box solve with only the
+// stencil chunks of the odd rows (rows_odd_facr_sparse): the even rows come
+// out whole, the odd rows only where the six-point stencils read them; the
+// field is recomputed from phi_0 if the solve converges at sweep 1.
+bool facr_trace_ok(kfbi_plan *p, const kfbi_bvp *b) {
+  if (!p->facr_trace || !p->facr || p->n_oc <= 0 || b->bc_kind != 0 || b->box_bc != KFBI_DIRICHLET_ZERO)
+    return false;
+  if (!col_use_tri(p, b->kappa_re, b->kappa_im)) return false;
+  const bool cplx = b->dtype == KFBI_C128;
+  return p->m >= 512 && (p->m <= 8192 || (!cplx && p->m == 16384));
+}
+
+template <typename T>
+kfbi_status sweep1_facr_trace(kfbi_plan *p, const kfbi_bvp *b, cudaStream_t s) {
+  constexpr bool CPLX = std::is_same<T, double2>::value;
+  const int *done = &p->st.p->done;
+  KFBI_TRY(jumps_T<T>(p, b->kappa_re, b->kappa_im, b->density, nullptr, b->f_gamma, b->f_gamma_sign,
+                      p->jm.p, done, s));
+  KFBI_TRY(edges_T<T>(p, p->jm.p, p->jv.p, done, s));
+  BoxArgs a = box_args(p, b->kappa_re, b->kappa_im, done);
+  a.npl = CPLX ? p->m / 2 : p->m / 4;
+  a.oc_list = p->oc_list.p;
+  a.n_oc = p->n_oc;
+  CorrArgs<T> c = corr_args<T>(p, reinterpret_cast<const T *>(p->jv.p));
+  KFBI_TRY(box_passes_reg<CPLX>(p, a, b->F, b->F_sign, c, b->u, s));
+  ExtractArgs x = extract_args(p, false);
+  const int blocks = (p->n_ctl + 255) / 256;
+  return launch(p, KFBI_K_DENSITY, s, [&] {
+    extract_update_kernel<T><<<blocks, 256, 0, s>>>(
+        x, static_cast<const T *>(b->u), reinterpret_cast<const T *>(p->jm.p),
+        static_cast<const T *>(b->g), static_cast<T *>(b->density), static_cast<T *>(b->trace_u),
+        static_cast<T *>(b->trace_un), b->gamma, 1, p->st.p, p->history.p);
+  });
+}
+
 // Sweep 1 of the operator form when only its trace is needed (Dirichlet,
 // one slab): rows_fwd + column stage, then the inverse row transform only at
 // the stencil nodes (stencil_eval_kernel) instead of the whole field; the
@@ -1090,6 +1130,8 @@ kfbi_status kfbi_plan_create(const kfbi_grid_desc *desc, kfbi_plan **out) {
     if (oc && oc[0] == '0') p->op_cta = false;
     const char *ef = std::getenv("KFBI_EDGES_FULL");
     if (ef && ef[0] == '0') p->edges_full = false;
+    const char *ft = std::getenv("KFBI_FACR_TRACE");
+    if (ft && ft[0] == '0') p->facr_trace = false;
   }
   cudaError_t e = cudaSetDevice(p->device);
   if (e != cudaSuccess) {
@@ -1452,6 +1494,31 @@ kfbi_status kfbi_plan_set_geometry(kfbi_plan *p, const kfbi_geometry *g) {
         (e = p->sn_vals.ensure((size_t)p->sn_nodes)) == cudaSuccess)
       e = p->sn_v13.ensure(13 * (size_t)n);
   }
+  // odd grid rows x 16-element chunks holding six-point stencil nodes: the
+  // trace-only first sweep solves only these chunks of the FACR odd rows
+  // (rows_odd_facr_sparse); every chunk's 32-element windows must stay
+  // clear of x = 0 and x = M (the chunk never needs the x = 0 boundary term)
+  if (e == cudaSuccess) {
+    std::vector<long long> keys;
+    bool ok = m >= 512;
+    for (int q = 0; q < 6 * n && ok; ++q) {
+      const int node = g->stencil[q];
+      const int j = node / (m + 1), i = node - j * (m + 1);
+      if (!(j & 1)) continue;
+      const int ch = i / 16, s0 = 16 * ch;
+      if (s0 < 64 || s0 + 16 + 32 > m - 1) ok = false;   // windows of ODD_W = 32
+      keys.push_back((long long)j * (m / 16 + 1) + ch);
+    }
+    p->n_oc = 0;
+    if (ok && !keys.empty()) {
+      std::sort(keys.begin(), keys.end());
+      keys.erase(std::unique(keys.begin(), keys.end()), keys.end());
+      std::vector<int2> lst;
+      lst.reserve(keys.size());
+      for (long long k : keys) lst.push_back(make_int2((int)(k / (m / 16 + 1)), (int)(k % (m / 16 + 1))));
+      if ((e = upload(p->oc_list, lst.data(), lst.size())) == cudaSuccess) p->n_oc = (int)lst.size();
+    }
+  }
   if (e == cudaSuccess) e = p->gsum.ensure((size_t)(g->n_groups > 0 ? g->n_groups : 1));
   if (e == cudaSuccess) e = p->d1.ensure(n);
   if (e == cudaSuccess) e = p->psi_s.ensure(n);
@@ -1700,8 +1767,11 @@ kfbi_status kfbi_richardson(kfbi_plan *p, const kfbi_bvp *b, kfbi_bvp_result *re
     // whether the full pipeline must recompute the field and logs the step
     if (b->log_slot >= p->log_cap) return fail(KFBI_E_CONFIG, "log slot out of range (kfbi_log_reserve)");
     KFBI_TRY(ensure_async_scratch(p));
-    const bool tr = trace_sweep_ok(p, b);
-    if (tr && cplx) KFBI_TRY(sweep1_trace<double2>(p, b, s));
+    const bool ft = facr_trace_ok(p, b);
+    const bool tr = ft || trace_sweep_ok(p, b);
+    if (ft && cplx) KFBI_TRY(sweep1_facr_trace<double2>(p, b, s));
+    else if (ft) KFBI_TRY(sweep1_facr_trace<double>(p, b, s));
+    else if (tr && cplx) KFBI_TRY(sweep1_trace<double2>(p, b, s));
     else if (tr) KFBI_TRY(sweep1_trace<double>(p, b, s));
     else if (cplx) KFBI_TRY(sweep<double2>(p, b, s));
     else KFBI_TRY(sweep<double>(p, b, s));
@@ -1737,8 +1807,11 @@ kfbi_status kfbi_richardson(kfbi_plan *p, const kfbi_bvp *b, kfbi_bvp_result *re
   if (use_op) {
     // sweep 1 through the pipeline, then every further sweep inside one
     // cooperative launch; a single host sync per solve
-    const bool tr = trace_sweep_ok(p, b);
-    if (tr && cplx) KFBI_TRY(sweep1_trace<double2>(p, b, s));
+    const bool ft = facr_trace_ok(p, b);
+    const bool tr = ft || trace_sweep_ok(p, b);
+    if (ft && cplx) KFBI_TRY(sweep1_facr_trace<double2>(p, b, s));
+    else if (ft) KFBI_TRY(sweep1_facr_trace<double>(p, b, s));
+    else if (tr && cplx) KFBI_TRY(sweep1_trace<double2>(p, b, s));
     else if (tr) KFBI_TRY(sweep1_trace<double>(p, b, s));
     else if (cplx) KFBI_TRY(sweep<double2>(p, b, s));
     else KFBI_TRY(sweep<double>(p, b, s));

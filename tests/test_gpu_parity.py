@@ -367,3 +367,32 @@ def test_state_fields_zero_outside_mask(eq):
                 continue
             assert bool((v.reshape(-1)[ext] == 0).all()), (eq, name)
     torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("eq", ["heat", "schrodinger"])
+def test_facr_trace_first_sweep_matches_full(monkeypatch, eq):
+    # the operator form's first sweep solves only the stencil chunks of the
+    # FACR odd rows (rows_odd_facr_sparse): same iteration lists and field as
+    # with the whole first-sweep field (KFBI_FACR_TRACE=0)
+    from paper_2404_14864_b200 import boxsolve
+
+    heat, schr = k.HeatPlaneDecay(), k.SchrodingerPhaseRotation()
+    if eq == "heat":
+        box, curve, kw = BOX, k.StarCurve(1.0, c=0.2, lobes=8), dict(
+            equation="heat", bc_kind="dirichlet", g=heat.dirichlet, u0=heat.u0,
+            lap_u0=heat.lap_u0, tau=1 / 256, t_final=6 / 256)
+    else:
+        box, curve, kw = PI_BOX, k.StarCurve(1.5, c=0.2, lobes=3), dict(
+            equation="schrodinger", bc_kind="dirichlet", g=schr.dirichlet, u0=schr.u0,
+            lap_u0=schr.lap_u0, potential=schr.potential, tau=1 / 128, t_final=6 / 128)
+    res = {}
+    for flag in ("1", "0"):
+        monkeypatch.setenv("KFBI_FACR_TRACE", flag)
+        boxsolve._GRID_PLANS.clear()
+        geo = k.build_grid(box, 1024, curve)
+        ctx = k.StepContext(geo, backend=k.CudaBackend(0, timing=False))
+        res[flag] = k.run(k.ProblemSpec(**kw), geo, context=ctx, operator=True, graph=False)
+    boxsolve._GRID_PLANS.clear()
+    assert res["1"].iterations == res["0"].iterations
+    a, b = np.asarray(res["1"].state.u), np.asarray(res["0"].state.u)
+    assert np.max(np.abs(a - b)) <= 1e-13 * np.max(np.abs(b))
