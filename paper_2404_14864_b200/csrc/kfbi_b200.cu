@@ -715,6 +715,8 @@ kfbi_status ensure_async_scratch(kfbi_plan *p) {
 }
 
 // Column p of T = trace of the pipeline applied to e_p with F = 0, f_gamma = 0.
+bool facr_trace_applies(kfbi_plan *p, double kre, double kim, bool cplx, int bc_kind, int box_bc);
+
 template <typename T>
 kfbi_status build_operator_T(kfbi_plan *p, double kre, double kim, int bc_kind, int box_bc,
                              cudaStream_t s) {
@@ -734,15 +736,26 @@ kfbi_status build_operator_T(kfbi_plan *p, double kre, double kim, int bc_kind, 
   const int eb = (n + 255) / 256;
   const bool timing = p->timing;
   p->timing = false;
+  const bool sparse = facr_trace_applies(p, kre, kim, CPLX, bc_kind, box_bc);
   kfbi_status st = KFBI_OK;
   for (int col = 0; col < n && st == KFBI_OK; ++col) {
     st = launch(p, KFBI_K_JUMPS, s, [&] { unit_vector_kernel<T><<<eb, 256, 0, s>>>(ev, n, col); });
     if (st == KFBI_OK)
       st = jumps_T<T>(p, kre, kim, dir ? ev : nullptr, dir ? nullptr : ev, z, 1.0, p->jm.p, nullptr, s);
     if (st == KFBI_OK) st = edges_T<T>(p, p->jm.p, p->jv.p, nullptr, s);
-    if (st == KFBI_OK)
-      st = box_dispatch(p, CPLX ? KFBI_C128 : KFBI_F64, kre, kim, nullptr, 1.0, p->jv.p, p->ufield.p,
-                        nullptr, s, box_bc);
+    if (st == KFBI_OK) {
+      if (sparse) {                              // only the trace is needed: stencil chunks of the odd rows
+        BoxArgs a = box_args(p, kre, kim, nullptr);
+        a.npl = CPLX ? p->m / 2 : p->m / 4;
+        a.oc_list = p->oc_list.p;
+        a.n_oc = p->n_oc;
+        CorrArgs<T> c = corr_args<T>(p, reinterpret_cast<const T *>(p->jv.p));
+        st = box_passes_reg<CPLX>(p, a, nullptr, 1.0, c, p->ufield.p, s);
+      } else {
+        st = box_dispatch(p, CPLX ? KFBI_C128 : KFBI_F64, kre, kim, nullptr, 1.0, p->jv.p, p->ufield.p,
+                          nullptr, s, box_bc);
+      }
+    }
     if (st == KFBI_OK)
       st = launch(p, KFBI_K_EXTRACT, s, [&] {
         extract_kernel<T><<<eb, 256, 0, s>>>(x, reinterpret_cast<const T *>(p->ufield.p),
@@ -895,12 +908,15 @@ kfbi_status op_solve(kfbi_plan *p, const kfbi_bvp *b, cudaStream_t s) {
 // stencil chunks of the odd rows (rows_odd_facr_sparse): the even rows come
 // out whole, the odd rows only where the six-point stencils read them; the
 // field is recomputed from phi_0 if the solve converges at sweep 1.
-bool facr_trace_ok(kfbi_plan *p, const kfbi_bvp *b) {
-  if (!p->facr_trace || !p->facr || p->n_oc <= 0 || b->bc_kind != 0 || b->box_bc != KFBI_DIRICHLET_ZERO)
+bool facr_trace_applies(kfbi_plan *p, double kre, double kim, bool cplx, int bc_kind, int box_bc) {
+  if (!p->facr_trace || !p->facr || p->n_oc <= 0 || bc_kind != 0 || box_bc != KFBI_DIRICHLET_ZERO)
     return false;
-  if (!col_use_tri(p, b->kappa_re, b->kappa_im)) return false;
-  const bool cplx = b->dtype == KFBI_C128;
+  if (!col_use_tri(p, kre, kim)) return false;
   return p->m >= 512 && (p->m <= 8192 || (!cplx && p->m == 16384));
+}
+
+bool facr_trace_ok(kfbi_plan *p, const kfbi_bvp *b) {
+  return facr_trace_applies(p, b->kappa_re, b->kappa_im, b->dtype == KFBI_C128, b->bc_kind, b->box_bc);
 }
 
 template <typename T>
