@@ -124,6 +124,10 @@ typedef struct {
                              (density = psi, trace d_n u+, one-sided
                              extraction; bvp.py:313-323) */
   int32_t box_bc;         /* kfbi_box_bc closure of the box solves          */
+  int32_t field_chunks;   /* 1: the caller reads the returned field only at
+                             the nodes covered by kfbi_plan_set_field_chunks
+                             (the steppers mask it); the FACR odd rows of the
+                             final sweep are solved only there               */
 } kfbi_bvp;
 
 /* One entry of the plan's device-side step log (asynchronous stepping). */
@@ -490,6 +494,11 @@ kfbi_status kfbi_plan_set_exterior_zero(kfbi_plan *plan, int32_t on);
  * masked Newton passes (kfbi_nonlinear_phase, kfbi_strang_phase) then visit
  * only these nodes.  idx = NULL clears it. */
 kfbi_status kfbi_plan_set_interior_list(kfbi_plan *plan, const int32_t *idx, int64_t count);
+/* (odd grid row, 16-node chunk) pairs, host int32[2 * count], covering every
+ * node the caller reads of a field returned with kfbi_bvp.field_chunks = 1
+ * (interior nodes and six-point stencil nodes); each chunk's windows must
+ * lie inside the box (16 chunk >= 64, 16 chunk + 48 <= M - 1). */
+kfbi_status kfbi_plan_set_field_chunks(kfbi_plan *plan, const int32_t *pairs, int64_t count);
 kfbi_status kfbi_log_copy(kfbi_plan *plan, int32_t src, int32_t dst, int32_t count, void *stream);
 
 /* Per-kernel-name device time (ms) and call counts since the last reset

@@ -70,7 +70,7 @@ class Bvp(C.Structure):
         ("g", vp), ("density", vp), ("gamma", f64), ("tol", f64),
         ("max_iter", i32), ("sweeps_hint", i32),
         ("u", vp), ("trace_u", vp), ("trace_un", vp), ("use_operator", i32),
-        ("log_slot", i32), ("bc_kind", i32), ("box_bc", i32),
+        ("log_slot", i32), ("bc_kind", i32), ("box_bc", i32), ("field_chunks", i32),
     ]
 
 
@@ -112,6 +112,7 @@ _SIGNATURES = {
     "kfbi_log_clear": ([vp, i32, i32, vp], i32),
     "kfbi_plan_set_exterior_zero": ([vp, i32], i32),
     "kfbi_plan_set_interior_list": ([vp, vp, i64], i32),
+    "kfbi_plan_set_field_chunks": ([vp, vp, i64], i32),
     "kfbi_log_copy": ([vp, i32, i32, i32, vp], i32),
     "kfbi_heat_rhs": ([vp, i64, vp, vp, vp, vp, f64, C.POINTER(f64), vp], i32),
     "kfbi_wave_rhs": ([vp, i64, vp, vp, vp, vp, vp, vp, f64, f64, C.POINTER(f64), vp], i32),

@@ -334,7 +334,7 @@ class Plan:
 
     def richardson(self, *, kappa, F, F_sign, f_gamma, f_gamma_sign, g, density, gamma, tol,
                    max_iter, u, trace_u, trace_un, sweeps_hint=0, use_operator=False,
-                   log_slot=-1, bc_kind="dirichlet", box_bc=None):
+                   log_slot=-1, bc_kind="dirichlet", box_bc=None, field_chunks=False):
         k = complex(kappa)
         box_bc = box_bc or ("dirichlet-zero" if bc_kind == "dirichlet" else "neumann-zero")
         b = N.Bvp(dtype=self._dt(u.is_complex()), kappa_re=k.real, kappa_im=k.imag,
@@ -343,7 +343,8 @@ class Plan:
                   gamma=float(gamma), tol=float(tol), max_iter=int(max_iter),
                   sweeps_hint=int(sweeps_hint), u=u.data_ptr(), trace_u=trace_u.data_ptr(),
                   trace_un=trace_un.data_ptr(), use_operator=int(bool(use_operator)),
-                  log_slot=int(log_slot), bc_kind=_KIND[bc_kind], box_bc=_BOX[box_bc])
+                  log_slot=int(log_slot), bc_kind=_KIND[bc_kind], box_bc=_BOX[box_bc],
+                  field_chunks=int(bool(field_chunks)))
         hist = np.zeros(max(int(max_iter), 1))
         res = N.BvpResult(history=hist.ctypes.data_as(C.POINTER(C.c_double)))
         status = self._lib.kfbi_richardson(self.handle, C.byref(b), C.byref(res), self.stream)
@@ -388,6 +389,12 @@ class Plan:
         """The masked outputs of the right-hand-side kernels are zero outside
         the mask already (kfbi_plan_set_exterior_zero)."""
         N.check(self._lib.kfbi_plan_set_exterior_zero(self.handle, int(bool(on))))
+
+    def set_field_chunks(self, pairs):
+        """(odd row, 16-node chunk) pairs covering the nodes a caller reads
+        of fields returned with field_chunks=True (kfbi_plan_set_field_chunks)."""
+        arr = np.ascontiguousarray(pairs, dtype=np.int32).reshape(-1, 2)
+        N.check(self._lib.kfbi_plan_set_field_chunks(self.handle, arr.ctypes.data, int(arr.shape[0])))
 
     def set_interior_list(self, idx):
         """Interior node list (device int32 tensor, kept alive by the

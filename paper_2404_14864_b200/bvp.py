@@ -216,7 +216,7 @@ class DeviceBvp:
 def solve_device(ws, *, kappa, F, f_gamma, g, density, F_sign=1.0, f_gamma_sign=1.0,
                  gamma=0.8, tol=1e-8, max_iter=200, sweeps_hint=0, u_out=None,
                  use_operator=False, log_slot=-1, bc_kind="dirichlet", box_bc=None,
-                 method="richardson", restart=40):
+                 method="richardson", restart=40, field_chunks=False):
     """Richardson solve on device tensors (the inner loop of every time step).
 
     `density` is updated in place (it carries the warm start); F and f_gamma
@@ -247,7 +247,7 @@ def solve_device(ws, *, kappa, F, f_gamma, g, density, F_sign=1.0, f_gamma_sign=
         kappa=kappa, F=F, F_sign=F_sign, f_gamma=f_gamma, f_gamma_sign=f_gamma_sign, g=g,
         density=density, gamma=gamma, tol=tol, max_iter=max_iter, u=u, trace_u=tu,
         trace_un=tn, sweeps_hint=sweeps_hint, use_operator=use_operator, log_slot=log_slot,
-        bc_kind=bc_kind, box_bc=box_bc)
+        bc_kind=bc_kind, box_bc=box_bc, field_chunks=field_chunks)
     del cplx
     return DeviceBvp(u=u, density=density, trace_u=tu, trace_un=tn, iterations=it,
                      residual=res, residual_history=hist)

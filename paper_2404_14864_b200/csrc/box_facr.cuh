@@ -286,6 +286,24 @@ rows_odd_facr(BoxArgs a, const void *__restrict__ rhs, double sign,
   const int j = CPLX ? 2 * blockIdx.x + 1 : 4 * blockIdx.x + 1;   // odd row (and j + 2)
   const double h2 = a.h2;
   auto pos = [](int n) { return n + (n >> 4); };
+  // a.span (the final field of a masked caller, kfbi_plan_set_field_chunks):
+  // only the chunks [c_lo, c_hi] of this row (pair) are needed; loads outside
+  // their windows and the x = 0 boundary term (rho^n z_1, n >= 64: below the
+  // rounding of y) are skipped
+  int c_lo = 0, c_hi = NT - 1, nlo = 0, nhi = M;
+  if (a.span) {
+    int2 sp = a.span[(j - 1) >> 1];
+    if constexpr (!CPLX) {                     // rows j and j + 2: the union of the ranges
+      const int2 s2 = a.span[(j + 1) >> 1];
+      const bool e1 = sp.x <= sp.y;
+      if (s2.x <= s2.y) sp = e1 ? make_int2(min(sp.x, s2.x), max(sp.y, s2.y)) : s2;
+    }
+    if (sp.x > sp.y) return;                     // nothing of this row (pair) is read
+    c_lo = sp.x;
+    c_hi = sp.y;
+    nlo = CH * c_lo - ODD_W - 1;
+    nhi = CH * (c_hi + 1) + ODD_W;
+  }
   // rhs_n = h^2 g_j - u_{j-1} - u_{j+1} (u_0 = u_M = 0), coalesced over n = t + NT e
   auto form = [&](int jj, int comp) {
     const T *U = static_cast<const T *>(u);
@@ -296,9 +314,10 @@ rows_odd_facr(BoxArgs a, const void *__restrict__ rhs, double sign,
 #pragma unroll
     for (int e = 0; e < CH; ++e) {
       const int n = t + NT * e;
-      f[e] = rhs ? Fr[n] : S::zero();
-      l[e] = hasl ? Ul[n] : S::zero();
-      hv[e] = hash ? Uh[n] : S::zero();
+      const bool w = n >= nlo && n <= nhi;
+      f[e] = (rhs && w) ? Fr[n] : S::zero();
+      l[e] = (hasl && w) ? Ul[n] : S::zero();
+      hv[e] = (hash && w) ? Uh[n] : S::zero();
     }
 #pragma unroll
     for (int e = 0; e < CH; ++e) {
@@ -329,11 +348,12 @@ rows_odd_facr(BoxArgs a, const void *__restrict__ rhs, double sign,
 #pragma unroll
       for (int e = 0; e < HB; ++e) {
         const int n = t + NT * (e0 + e);
-        f0[e] = rhs ? F0[n] : 0.0;
-        f1[e] = rhs ? F1[n] : 0.0;
-        la[e] = ha ? Ua[n] : 0.0;
-        lb[e] = Ub[n];
-        lc[e] = hc ? Uc[n] : 0.0;
+        const bool w = n >= nlo && n <= nhi;
+        f0[e] = (rhs && w) ? F0[n] : 0.0;
+        f1[e] = (rhs && w) ? F1[n] : 0.0;
+        la[e] = (ha && w) ? Ua[n] : 0.0;
+        lb[e] = w ? Ub[n] : 0.0;
+        lc[e] = (hc && w) ? Uc[n] : 0.0;
       }
 #pragma unroll
       for (int e = 0; e < HB; ++e) {
@@ -369,10 +389,11 @@ rows_odd_facr(BoxArgs a, const void *__restrict__ rhs, double sign,
   const int hi = s0 + CH + ODD_W > M - 1 ? M - 1 : s0 + CH + ODD_W;  // exact end at x = M - 1 (z_M = 0)
   // forward v_n = rho v_{n-1} - rhs_n over [lo, hi]: v kept on the chunk; after
   // it only z at the chunk end, z_end = sum_{n >= end} rho^{n - end} v_n
+  const bool act = t >= c_lo && t <= c_hi;       // (always, without a span)
   double2 zch[CH];
   double2 v = make_double2(0.0, 0.0);
 #pragma unroll 8
-  for (int n = lo; n < s0; ++n) v = tri::mad<CPLX>(rr, v, cneg(rbuf[pos(n)]));
+  for (int n = lo; n < (act ? s0 : lo); ++n) v = tri::mad<CPLX>(rr, v, cneg(rbuf[pos(n)]));
 #pragma unroll
   for (int e = 0; e < CH; ++e) {
     const int n = s0 + e;
@@ -381,7 +402,7 @@ rows_odd_facr(BoxArgs a, const void *__restrict__ rhs, double sign,
   }
   double2 z = make_double2(0.0, 0.0), pw1 = tri::one<CPLX>();
 #pragma unroll 8
-  for (int n = s0 + CH; n <= hi; ++n) {
+  for (int n = s0 + CH; n <= (act ? hi : s0); ++n) {
     v = tri::mad<CPLX>(rr, v, cneg(rbuf[pos(n)]));
     z = tri::mad<CPLX>(pw1, v, z);
     pw1 = tri::mul<CPLX>(pw1, rr);
@@ -395,7 +416,7 @@ rows_odd_facr(BoxArgs a, const void *__restrict__ rhs, double sign,
   if (t == 0) z1s = zch[CH > 1 ? 1 : 0];          // z_1 (CH >= 2 always here)
   __syncthreads();                               // rhs reads done; z_1 visible
   // y_n = rho z_n + B rho^n, B = -rho^2 z_1 (rho^{2M} terms < 1e-300)
-  const double2 Bc = cneg(tri::mul<CPLX>(tri::mul<CPLX>(rr, rr), z1s));
+  const double2 Bc = a.span ? make_double2(0.0, 0.0) : cneg(tri::mul<CPLX>(tri::mul<CPLX>(rr, rr), z1s));
   double2 pw = tri::pw<CPLX>(rr, s0);            // rho^n
 #pragma unroll
   for (int e = 0; e < CH; ++e) {
@@ -405,9 +426,11 @@ rows_odd_facr(BoxArgs a, const void *__restrict__ rhs, double sign,
   }
   __syncthreads();
   T *U = static_cast<T *>(u);
+  const int olo = a.span ? CH * c_lo : 0, ohi = a.span ? CH * (c_hi + 1) - 1 : M;
 #pragma unroll
   for (int e = 0; e < CH; ++e) {
     const int n = t + NT * e;
+    if (n < olo || n > ohi) continue;
     const double2 y = rbuf[pos(n)];
     if constexpr (CPLX) {
       U[(size_t)j * stride + n] = n >= 1 ? y : S::zero();
@@ -416,6 +439,7 @@ rows_odd_facr(BoxArgs a, const void *__restrict__ rhs, double sign,
       U[(size_t)(j + 2) * stride + n] = n >= 1 ? y.y : 0.0;
     }
   }
+  if (a.span) return;                            // (ring column / row: exterior, never read)
   if (t == 0) {                                  // x = M: the zero ring column
     U[(size_t)j * stride + M] = S::zero();
     if constexpr (!CPLX) U[(size_t)(j + 2) * stride + M] = S::zero();

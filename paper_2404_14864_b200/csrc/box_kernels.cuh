@@ -21,6 +21,8 @@ struct BoxArgs {
   void *gsum;             // scratch for the group sums (n_groups slots of 16 bytes)
   const int2 *oc_list;    // FACR: solve only these (odd row, 16-chunk) pieces of the odd rows
   int n_oc;               // (trace-only first sweep; nullptr: every odd row)
+  const int2 *span;       // FACR: per odd row (j - 1) / 2, the chunk range [x, y] the caller
+                          // reads (x > y: none); nullptr: whole rows
   void *panels;
   const int *done;        // early-exit flag (Richardson sweeps), may be null
   const double2 *twg;     // [m] exp(-2 pi i q / m)        (register engine)

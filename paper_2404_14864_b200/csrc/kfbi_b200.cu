@@ -129,6 +129,8 @@ struct kfbi_plan {
   // stencil nodes grouped by grid row (trace-only sweep 1 of the operator form)
   DevBuf<int> sn_rows, sn_rowptr, sn_cols, sn_map;
   DevBuf<int2> oc_list;             // (odd row, 16-element chunk) pairs holding stencil nodes
+  DevBuf<int2> fc_span;             // kfbi_plan_set_field_chunks: per odd row, the chunk range read
+  int n_fc = 0;
   int n_oc = 0;                     // 0: the sparse odd-row pass does not apply
   bool facr_trace = true;           // env KFBI_FACR_TRACE=0: sweep 1 forms the whole field
   DevBuf<double2> gsum;             // group sums of the FACR passes
@@ -256,6 +258,7 @@ BoxArgs box_args(kfbi_plan *p, double kre, double kim, const int *done) {
   for (int h = 0; h < 8; ++h) a.dst[h] = nullptr;
   a.oc_list = nullptr;
   a.n_oc = 0;
+  a.span = nullptr;
   return a;
 }
 
@@ -993,8 +996,19 @@ kfbi_status final_pipeline(kfbi_plan *p, const kfbi_bvp *b, const void *phi_befo
   KFBI_TRY(jumps_T<T>(p, b->kappa_re, b->kappa_im, dir ? phi_before : nullptr,
                       dir ? nullptr : phi_before, b->f_gamma, b->f_gamma_sign, p->jm.p, skip, s));
   KFBI_TRY(edges_T<T>(p, p->jm.p, p->jv.p, skip, s));
-  KFBI_TRY(box_dispatch(p, CPLX ? KFBI_C128 : KFBI_F64, b->kappa_re, b->kappa_im, b->F, b->F_sign,
-                        p->jv.p, b->u, skip, s, b->box_bc));
+  if (b->field_chunks && p->n_fc > 0 &&
+      facr_trace_applies(p, b->kappa_re, b->kappa_im, CPLX, b->bc_kind, b->box_bc)) {
+    // the caller reads the field only at the interior and stencil nodes
+    // (kfbi_plan_set_field_chunks): odd rows only at their chunks
+    BoxArgs a = box_args(p, b->kappa_re, b->kappa_im, skip);
+    a.npl = CPLX ? p->m / 2 : p->m / 4;
+    a.span = p->fc_span.p;
+    CorrArgs<T> c = corr_args<T>(p, reinterpret_cast<const T *>(p->jv.p));
+    KFBI_TRY(box_passes_reg<CPLX>(p, a, b->F, b->F_sign, c, b->u, s));
+  } else {
+    KFBI_TRY(box_dispatch(p, CPLX ? KFBI_C128 : KFBI_F64, b->kappa_re, b->kappa_im, b->F, b->F_sign,
+                          p->jv.p, b->u, skip, s, b->box_bc));
+  }
   ExtractArgs x = extract_args(p, !dir);
   return launch(p, KFBI_K_EXTRACT, s, [&] {
     extract_traces_kernel<T><<<(n + 255) / 256, 256, 0, s>>>(
@@ -2012,6 +2026,33 @@ kfbi_status kfbi_log_fetch(kfbi_plan *p, int32_t first, int32_t count, kfbi_step
 kfbi_status kfbi_plan_set_exterior_zero(kfbi_plan *p, int32_t on) {
   KFBI_TRY(check_plan(p));
   p->ext_zero = on != 0;
+  return KFBI_OK;
+}
+
+kfbi_status kfbi_plan_set_field_chunks(kfbi_plan *p, const int32_t *pairs, int64_t count) {
+  KFBI_TRY(check_plan(p));
+  if (count < 0 || (count > 0 && !pairs)) return fail(KFBI_E_CONFIG, "field chunks: bad arguments");
+  const int nch = p->m / 16;
+  for (int64_t q = 0; q < count; ++q) {
+    const int j = pairs[2 * q], ch = pairs[2 * q + 1], s0 = 16 * ch;
+    if (j < 1 || j > p->m - 1 || !(j & 1) || ch < 0 || ch >= nch || s0 < 64 || s0 + 16 + 32 > p->m - 1)
+      return fail(KFBI_E_CONFIG, "field chunks: (odd row, chunk) pairs with windows inside the box");
+  }
+  p->n_fc = 0;
+  if (count > 0) {
+    // per odd row the covering chunk range (the odd-row pass keeps its
+    // thread-per-chunk layout and skips the rest of the row)
+    std::vector<int2> span((size_t)p->m / 2, make_int2(1, 0));
+    for (int64_t q = 0; q < count; ++q) {
+      int2 &sp = span[(size_t)(pairs[2 * q] - 1) / 2];
+      const int ch = pairs[2 * q + 1];
+      if (sp.x > sp.y) sp = make_int2(ch, ch);
+      else sp = make_int2(std::min(sp.x, ch), std::max(sp.y, ch));
+    }
+    cudaError_t e = upload(p->fc_span, span.data(), span.size());
+    if (e != cudaSuccess) return fail(KFBI_E_CUDA, std::string("field chunks: ") + cudaGetErrorString(e));
+    p->n_fc = (int)count;
+  }
   return KFBI_OK;
 }
 
