@@ -392,13 +392,21 @@ def run_ours(args):
     # the alternating launches), column stage 1 (M/2 rows), odd rows 1.5
     pas = {n: {"bytes": 0.0, "ms": 0.0, "calls": 0}
            for n in ("transform-rows", "transform-cols", "diagonal-scale")}
+    work_fr = {}
     for eq, c in ctxs.items():
         ms, calls = c.plan.kernel_times()
         cplx = eq == "schrodinger"
         unit = _bytes_cols(m, cplx) / 2.0
         facr = c.plan.facr_for(kappas[eq])
-        per = ({"transform-rows": 1.25, "transform-cols": 1.0, "diagonal-scale": 1.5} if facr
+        # FACR per step: the trace-only first sweep (inverse of the even rows
+        # its stencils read, odd-row chunks of the stencils) and the masked
+        # final sweep (even rows of the domain's band, odd-row chunk ranges of
+        # the interior): the plan's work fractions scale those launches' bytes
+        fr = c.plan.work_fractions() if facr else (1.0, 1.0, 1.0, 1.0)
+        per = ({"transform-rows": (1.5 + fr[0] + 1.5 + fr[1]) / 4.0, "transform-cols": 1.0,
+                "diagonal-scale": 1.5 * (fr[2] + fr[3]) / 2.0} if facr
                else {"transform-rows": 2.0, "transform-cols": 2.0, "diagonal-scale": 0.0})
+        work_fr[eq] = fr
         for n in pas:
             pas[n]["bytes"] += calls[n] * per[n] * unit
             pas[n]["ms"] += ms[n]
@@ -614,9 +622,12 @@ def run_ours(args):
             "unit": "GB/s", "frac": roof[dom]["frac"],
             "traffic": traffic.get(dom),
             "peak_source": peaks["source"],
-            "algorithmic_bytes_per_launch": "transform-rows under FACR(1): 1.5 (forward) / 1.0 "
-                                            "(inverse) x (M-1)^2 s, averaged over the alternating "
-                                            "launches; three-pass: 2 (M-1)^2 s",
+            "algorithmic_bytes_per_launch": "transform-rows under FACR(1): 1.5 (forward) / 1.0 x f "
+                                            "(inverse, f = the fraction of even rows the trace-only "
+                                            "first sweep / the masked final sweep transform) x "
+                                            "(M-1)^2 s, averaged over the alternating launches; "
+                                            "three-pass: 2 (M-1)^2 s",
+            "work_fractions": work_fr,
             "avg_launch_ms": roof[dom]["avg_launch_ms"],
             "per_pass": roof,
         },

@@ -499,6 +499,11 @@ kfbi_status kfbi_plan_set_interior_list(kfbi_plan *plan, const int32_t *idx, int
  * (interior nodes and six-point stencil nodes); each chunk's windows must
  * lie inside the box (16 chunk >= 64, 16 chunk + 48 <= M - 1). */
 kfbi_status kfbi_plan_set_field_chunks(kfbi_plan *plan, const int32_t *pairs, int64_t count);
+/* Fractions of the FACR work the reduced solves still do (for roofline
+ * accounting): out[0] / out[1] even rows inverse-transformed by a trace-only
+ * first sweep / a masked final sweep, out[2] / out[3] odd-row chunks solved
+ * by each (1 where the reduction does not apply). */
+kfbi_status kfbi_plan_work_fractions(kfbi_plan *plan, double *out);
 kfbi_status kfbi_log_copy(kfbi_plan *plan, int32_t src, int32_t dst, int32_t count, void *stream);
 
 /* Per-kernel-name device time (ms) and call counts since the last reset

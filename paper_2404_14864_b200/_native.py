@@ -113,6 +113,7 @@ _SIGNATURES = {
     "kfbi_plan_set_exterior_zero": ([vp, i32], i32),
     "kfbi_plan_set_interior_list": ([vp, vp, i64], i32),
     "kfbi_plan_set_field_chunks": ([vp, vp, i64], i32),
+    "kfbi_plan_work_fractions": ([vp, C.POINTER(f64)], i32),
     "kfbi_log_copy": ([vp, i32, i32, i32, vp], i32),
     "kfbi_heat_rhs": ([vp, i64, vp, vp, vp, vp, f64, C.POINTER(f64), vp], i32),
     "kfbi_wave_rhs": ([vp, i64, vp, vp, vp, vp, vp, vp, f64, f64, C.POINTER(f64), vp], i32),

@@ -396,6 +396,13 @@ class Plan:
         arr = np.ascontiguousarray(pairs, dtype=np.int32).reshape(-1, 2)
         N.check(self._lib.kfbi_plan_set_field_chunks(self.handle, arr.ctypes.data, int(arr.shape[0])))
 
+    def work_fractions(self):
+        """(even rows trace, even rows field, odd chunks trace, odd chunks
+        field) fractions of the reduced FACR solves (kfbi_plan_work_fractions)."""
+        out = (C.c_double * 4)()
+        N.check(self._lib.kfbi_plan_work_fractions(self.handle, out))
+        return tuple(out)
+
     def set_interior_list(self, idx):
         """Interior node list (device int32 tensor, kept alive by the
         caller) for the masked Newton passes; None clears it."""

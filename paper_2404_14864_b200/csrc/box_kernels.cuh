@@ -23,6 +23,7 @@ struct BoxArgs {
   int n_oc;               // (trace-only first sweep; nullptr: every odd row)
   const int2 *span;       // FACR: per odd row (j - 1) / 2, the chunk range [x, y] the caller
                           // reads (x > y: none); nullptr: whole rows
+  const unsigned char *row_need;  // FACR inverse pass: per even row j / 2, 0 = nobody reads it
   void *panels;
   const int *done;        // early-exit flag (Richardson sweeps), may be null
   const double2 *twg;     // [m] exp(-2 pi i q / m)        (register engine)

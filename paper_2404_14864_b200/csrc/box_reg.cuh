@@ -294,6 +294,11 @@ rows_inv_reg(BoxArgs a, void *__restrict__ u) {
   const int r0 = CPLX ? q : 2 * q;               // slab row of the sequence
   const int j0 = a.row0 + r0;                    // grid row (row 0: zero ring)
   const size_t R = a.rows;
+  // rows nobody reads (trace-only / masked FACR solves, outside the domain's
+  // rows): the whole sequence is skipped (one sequence per CTA only)
+  if constexpr (C::S == 1 && C::CL == 1) {
+    if (a.row_need && valid && !a.row_need[r0] && (CPLX || !a.row_need[r0 + 1])) return;
+  }
 
   const double2 *P2 = static_cast<const double2 *>(a.panels);
   if (!CPLX) {

@@ -131,6 +131,8 @@ struct kfbi_plan {
   DevBuf<int2> oc_list;             // (odd row, 16-element chunk) pairs holding stencil nodes
   DevBuf<int2> fc_span;             // kfbi_plan_set_field_chunks: per odd row, the chunk range read
   int n_fc = 0;
+  DevBuf<unsigned char> need_trace, need_field;   // per even row j / 2: read by a trace sweep / a masked field
+  double frac[4] = {1.0, 1.0, 1.0, 1.0};         // kfbi_plan_work_fractions
   int n_oc = 0;                     // 0: the sparse odd-row pass does not apply
   bool facr_trace = true;           // env KFBI_FACR_TRACE=0: sweep 1 forms the whole field
   DevBuf<double2> gsum;             // group sums of the FACR passes
@@ -259,6 +261,7 @@ BoxArgs box_args(kfbi_plan *p, double kre, double kim, const int *done) {
   a.oc_list = nullptr;
   a.n_oc = 0;
   a.span = nullptr;
+  a.row_need = nullptr;
   return a;
 }
 
@@ -752,6 +755,7 @@ kfbi_status build_operator_T(kfbi_plan *p, double kre, double kim, int bc_kind, 
         a.npl = CPLX ? p->m / 2 : p->m / 4;
         a.oc_list = p->oc_list.p;
         a.n_oc = p->n_oc;
+        a.row_need = p->need_trace.p;
         CorrArgs<T> c = corr_args<T>(p, reinterpret_cast<const T *>(p->jv.p));
         st = box_passes_reg<CPLX>(p, a, nullptr, 1.0, c, p->ufield.p, s);
       } else {
@@ -933,6 +937,7 @@ kfbi_status sweep1_facr_trace(kfbi_plan *p, const kfbi_bvp *b, cudaStream_t s) {
   a.npl = CPLX ? p->m / 2 : p->m / 4;
   a.oc_list = p->oc_list.p;
   a.n_oc = p->n_oc;
+  a.row_need = p->need_trace.p;
   CorrArgs<T> c = corr_args<T>(p, reinterpret_cast<const T *>(p->jv.p));
   KFBI_TRY(box_passes_reg<CPLX>(p, a, b->F, b->F_sign, c, b->u, s));
   ExtractArgs x = extract_args(p, false);
@@ -1003,6 +1008,7 @@ kfbi_status final_pipeline(kfbi_plan *p, const kfbi_bvp *b, const void *phi_befo
     BoxArgs a = box_args(p, b->kappa_re, b->kappa_im, skip);
     a.npl = CPLX ? p->m / 2 : p->m / 4;
     a.span = p->fc_span.p;
+    a.row_need = p->need_field.p;
     CorrArgs<T> c = corr_args<T>(p, reinterpret_cast<const T *>(p->jv.p));
     KFBI_TRY(box_passes_reg<CPLX>(p, a, b->F, b->F_sign, c, b->u, s));
   } else {
@@ -1547,6 +1553,23 @@ kfbi_status kfbi_plan_set_geometry(kfbi_plan *p, const kfbi_geometry *g) {
       lst.reserve(keys.size());
       for (long long k : keys) lst.push_back(make_int2((int)(k / (m / 16 + 1)), (int)(k % (m / 16 + 1))));
       if ((e = upload(p->oc_list, lst.data(), lst.size())) == cudaSuccess) p->n_oc = (int)lst.size();
+      // even rows a trace sweep reads: stencil rows and the neighbours of
+      // the odd stencil rows (their windows)
+      std::vector<unsigned char> need((size_t)m / 2 + 1, 0);
+      for (int q = 0; q < 6 * n; ++q) {
+        const int j = g->stencil[q] / (m + 1);
+        if (j & 1) {
+          need[(size_t)(j - 1) / 2] = 1;
+          need[(size_t)(j + 1) / 2] = 1;
+        } else {
+          need[(size_t)j / 2] = 1;
+        }
+      }
+      if (e == cudaSuccess) e = upload(p->need_trace, need.data(), need.size());
+      size_t cnt = 0;
+      for (unsigned char c : need) cnt += c;
+      p->frac[0] = (double)cnt / (double)need.size();
+      p->frac[2] = (double)lst.size() / ((double)(m / 2) * (m / 16));
     }
   }
   if (e == cudaSuccess) e = p->gsum.ensure((size_t)(g->n_groups > 0 ? g->n_groups : 1));
@@ -2050,9 +2073,36 @@ kfbi_status kfbi_plan_set_field_chunks(kfbi_plan *p, const int32_t *pairs, int64
       else sp = make_int2(std::min(sp.x, ch), std::max(sp.y, ch));
     }
     cudaError_t e = upload(p->fc_span, span.data(), span.size());
+    // even rows the masked caller (or the odd rows' windows) read: between
+    // the first and last odd row with chunks, one row beyond each (the
+    // interior and the stencils of a closed curve occupy a contiguous band
+    // of rows; an even row inside the band next to no chunk row still holds
+    // interior nodes, so the whole band is kept)
+    std::vector<unsigned char> need((size_t)p->m / 2 + 1, 0);
+    int jlo = p->m, jhi = -1;
+    for (int64_t q = 0; q < count; ++q) {
+      jlo = std::min(jlo, (int)pairs[2 * q]);
+      jhi = std::max(jhi, (int)pairs[2 * q]);
+    }
+    for (int j = std::max(jlo - 1, 0); j <= std::min(jhi + 1, p->m); ++j)
+      if (!(j & 1)) need[(size_t)j / 2] = 1;
+    if (e == cudaSuccess) e = upload(p->need_field, need.data(), need.size());
     if (e != cudaSuccess) return fail(KFBI_E_CUDA, std::string("field chunks: ") + cudaGetErrorString(e));
     p->n_fc = (int)count;
+    size_t cnt = 0, chunks = 0;
+    for (unsigned char c : need) cnt += c;
+    for (const int2 &sp : span)
+      if (sp.x <= sp.y) chunks += (size_t)(sp.y - sp.x + 1);
+    p->frac[1] = (double)cnt / (double)need.size();
+    p->frac[3] = (double)chunks / ((double)(p->m / 2) * (p->m / 16));
   }
+  return KFBI_OK;
+}
+
+kfbi_status kfbi_plan_work_fractions(kfbi_plan *p, double *out) {
+  KFBI_TRY(check_plan(p));
+  if (!out) return fail(KFBI_E_CONFIG, "work fractions: null output");
+  for (int q = 0; q < 4; ++q) out[q] = p->frac[q];
   return KFBI_OK;
 }
 
