@@ -120,10 +120,16 @@ rows_fwd_facr(BoxArgs a, const void *__restrict__ rhs, double sign,
   if constexpr (!CPLX) row(J0 + 2, gb);
   // (linear layout until the FFT: the stencil and the DST pre-processing
   // read shifted / mirrored windows)
+  bool nzl = false;                              // any source in rows J0-1 .. J0+3 (below)
 #pragma unroll
   for (int m = 0; m < E; ++m) {
-    if constexpr (CPLX) sm.lin(t + m * TT) = ga[m];
-    else sm.lin(t + m * TT) = make_double2(ga[m], gb[m]);
+    if constexpr (CPLX) {
+      sm.lin(t + m * TT) = ga[m];
+      nzl |= (ga[m].x != 0.0) | (ga[m].y != 0.0);
+    } else {
+      sm.lin(t + m * TT) = make_double2(ga[m], gb[m]);
+      nzl |= (ga[m] != 0.0) | (gb[m] != 0.0);
+    }
   }
   double2 os[E];
   auto load_os = [&] {
@@ -150,6 +156,36 @@ rows_fwd_facr(BoxArgs a, const void *__restrict__ rhs, double sign,
   if constexpr (!CPLX) scatter(J0 + 2, 1, 1.0);
   reg::seq_sync<LOGN>();
   if constexpr (CPLX) load_os();
+  if constexpr (C::S == 1 && C::CL == 1) {
+    // rows with no source and no corrections (outside the domain's band for
+    // a masked source): w = 0, whose DST is exactly 0 — write the zeros and
+    // skip the stencil and the transform
+#pragma unroll
+    for (int m = 0; m < E; ++m) nzl |= (os[m].x != 0.0) | (os[m].y != 0.0);
+    if (corr.jv && valid && t == 0) {
+      for (int jj = J0 - 1; jj <= J0 + (CPLX ? 1 : 3); ++jj)
+        if (jj >= 1 && jj <= M - 1 && corr.row_group[jj + 1] > corr.row_group[jj]) nzl = true;
+    }
+    if (!__syncthreads_or(nzl)) {
+      if (valid) {
+        const double2 z = make_double2(0.0, 0.0);
+        if constexpr (!CPLX) {
+#pragma unroll
+          for (int kk = 0; kk < M / TT; ++kk) {
+            const int i = t + kk * TT;
+            *rows_fwd_dst(a, i >> 2, r0 + ((i & 3) >> 1), i & 1) = z;
+          }
+        } else {
+#pragma unroll
+          for (int kk = 0; kk < M / TT; ++kk) {
+            const int i = t + kk * TT;
+            *rows_fwd_dst(a, i >> 1, r0, i & 1) = z;
+          }
+        }
+      }
+      return;
+    }
+  }
   // w = g_{j-1} + g_{j+1} - B g_j  (B g_j = g_{j,i-1} + g_{j,i+1} - c4 g_{j,i})
   const double2 c4 = make_double2(4.0 + a.kre * a.h2, a.kim * a.h2);
   double2 w[E];
