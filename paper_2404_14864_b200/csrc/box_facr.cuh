@@ -166,8 +166,13 @@ rows_fwd_facr(BoxArgs a, const void *__restrict__ rhs, double sign,
       for (int jj = J0 - 1; jj <= J0 + (CPLX ? 1 : 3); ++jj)
         if (jj >= 1 && jj <= M - 1 && corr.row_group[jj + 1] > corr.row_group[jj]) nzl = true;
     }
-    if (!__syncthreads_or(nzl)) {
-      if (valid) {
+    const bool any = __syncthreads_or(nzl);
+    if (a.rowz && valid && t == 0) {             // the column pass skips the loads of zero rows
+      a.rowz[r0] = any ? 0 : 1;
+      if constexpr (!CPLX) a.rowz[r0 + 1] = any ? 0 : 1;
+    }
+    if (!any) {
+      if (valid && !a.rowz) {                    // (without the flags: explicit zero panels)
         const double2 z = make_double2(0.0, 0.0);
         if constexpr (!CPLX) {
 #pragma unroll

@@ -24,6 +24,9 @@ struct BoxArgs {
   const int2 *span;       // FACR: per odd row (j - 1) / 2, the chunk range [x, y] the caller
                           // reads (x > y: none); nullptr: whole rows
   const unsigned char *row_need;  // FACR inverse pass: per even row j / 2, 0 = nobody reads it
+  unsigned char *rowz;    // FACR: per reduced row, 1 = its forward output is zero (written by the
+                          // forward pass, which then skips the panel stores; read by the columns)
+  unsigned char *zbuf;    // the plan's flag buffer (the FACR launcher sets rowz = zbuf)
   void *panels;
   const int *done;        // early-exit flag (Richardson sweeps), may be null
   const double2 *twg;     // [m] exp(-2 pi i q / m)        (register engine)

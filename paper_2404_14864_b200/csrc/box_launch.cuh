@@ -95,6 +95,9 @@ kfbi_status box_facr_launch(kfbi_plan *p, const BoxArgs &a0, const void *rhs, do
     a.rows = M / 2;                                 // the even rows
     a.npl = CPLX ? M / 2 : M / 4;
     a.ring_end = 0;                                 // row M: written by the odd-row pass
+    // zero-row flags need the one-sequence-per-CTA forward kernel
+    a.rowz = (Cf::S == 1 && Cf::CL == 1) ? a0.zbuf : nullptr;
+
     const int nseq = CPLX ? M / 2 : M / 4;
     const int grow = Cf::CL > 1 ? nseq * Cf::CL : (nseq + Cf::S - 1) / Cf::S;
     KFBI_TRY(kfbi_launch(p, KFBI_K_ROWS, s, [&] {
@@ -230,6 +233,7 @@ kfbi_status box_facr_real_launch(kfbi_plan *p, const BoxArgs &a0, const void *rh
   a.rows = M / 2;
   a.npl = M / 4;
   a.ring_end = 0;
+  a.rowz = nullptr;                                 // (the 16384 forward kernel writes every panel)
   constexpr int CT = reg::Cfg<LOGL>::CTA_T;
   KFBI_TRY(kfbi_launch(p, KFBI_K_ROWS, s, [&] {
     rows_fwd_facr_real<LOGN><<<M / 2, CT, bytes, s>>>(a, static_cast<const double *>(rhs), sign, cc);

@@ -449,8 +449,12 @@ __global__ void __launch_bounds__(tri::Cfg<LOGM>::THREADS, tri::Cfg<LOGM>::MINB)
   double2 *dst = a.dst[0] ? static_cast<double2 *>(a.dst[j0 >> lr]) + (((size_t)pp * a.rows + jb) * 2 + half)
                           : const_cast<double2 *>(src);
   double2 x[CH];
+  // FACR: rows flagged zero by the forward pass are not loaded (their panels
+  // were not written)
+  const unsigned char *rz = a.rowz;
 #pragma unroll
-  for (int i = 0; i < CH; ++i) x[i] = (j0 + i >= 1) ? src[2 * i] : make_double2(0.0, 0.0);
+  for (int i = 0; i < CH; ++i)
+    x[i] = (j0 + i >= 1 && !(rz && rz[j0 + i])) ? src[2 * i] : make_double2(0.0, 0.0);
   tri_solve<CPLX, LOGM>(x, a, pp, half, hs, chunk, sh);
 #pragma unroll
   for (int i = 0; i < CH; ++i) dst[2 * i] = (j0 + i >= 1) ? x[i] : make_double2(0.0, 0.0);

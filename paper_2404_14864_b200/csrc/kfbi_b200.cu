@@ -132,6 +132,7 @@ struct kfbi_plan {
   DevBuf<int2> fc_span;             // kfbi_plan_set_field_chunks: per odd row, the chunk range read
   int n_fc = 0;
   DevBuf<unsigned char> need_trace, need_field;   // per even row j / 2: read by a trace sweep / a masked field
+  DevBuf<unsigned char> rowz;                     // FACR zero-row flags (per reduced row)
   double frac[4] = {1.0, 1.0, 1.0, 1.0};         // kfbi_plan_work_fractions
   int n_oc = 0;                     // 0: the sparse odd-row pass does not apply
   bool facr_trace = true;           // env KFBI_FACR_TRACE=0: sweep 1 forms the whole field
@@ -262,6 +263,8 @@ BoxArgs box_args(kfbi_plan *p, double kre, double kim, const int *done) {
   a.n_oc = 0;
   a.span = nullptr;
   a.row_need = nullptr;
+  a.rowz = nullptr;          // set by the FACR launcher only
+  a.zbuf = p->rowz.p;
   return a;
 }
 
@@ -1193,6 +1196,7 @@ kfbi_status kfbi_plan_create(const kfbi_grid_desc *desc, kfbi_plan **out) {
       (e = upload(p->sinv, sinv.data(), sinv.size())) != cudaSuccess ||
       (e = upload(p->lam, lam.data(), lam.size())) != cudaSuccess ||
       (e = p->panels.ensure((size_t)(m + 2) * (m + 2))) != cudaSuccess ||
+      (e = p->rowz.ensure((size_t)m / 2 + 2)) != cudaSuccess ||
       (e = p->st.ensure(1)) != cudaSuccess || (e = p->red.ensure(8)) != cudaSuccess) {
     kfbi_plan_destroy(p);
     return fail(KFBI_E_CUDA, std::string("plan allocation: ") + cudaGetErrorString(e));
