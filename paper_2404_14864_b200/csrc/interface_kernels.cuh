@@ -1746,6 +1746,14 @@ __global__ void op_finalize_kernel(const RichState *st, int n, T *A, const T *B,
   }
 }
 
+// dst = src while the Richardson solve runs: keeps phi_(K-1), the density the
+// converging sweep started from (the pipeline form with trace-only sweeps)
+template <typename T>
+__global__ void copy_running_kernel(const RichState *st, int n, const T *src, T *dst) {
+  if (st->done) return;
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x) dst[p] = src[p];
+}
+
 __global__ void log_norm_kernel(const unsigned long long *norm_bits, StepLog *log, int which) {
   const double v = __longlong_as_double((long long)*norm_bits);
   if (which == 0) log->norm = v;

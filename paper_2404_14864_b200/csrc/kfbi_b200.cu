@@ -914,10 +914,11 @@ kfbi_status op_solve(kfbi_plan *p, const kfbi_bvp *b, cudaStream_t s) {
   });
 }
 
-// Sweep 1 of the operator form through the FACR box solve with only the
-// stencil chunks of the odd rows (rows_odd_facr_sparse): the even rows come
-// out whole, the odd rows only where the six-point stencils read them; the
-// field is recomputed from phi_0 if the solve converges at sweep 1.
+// A trace-only sweep through the FACR box solve (sweep 1 of the operator
+// form, every sweep of the pipeline form) with only the stencil chunks of the
+// odd rows (rows_odd_facr_sparse): the even rows come out whole, the odd rows
+// only where the six-point stencils read them; the field of the converging
+// sweep comes from one full pipeline (final_pipeline) from its start density.
 bool facr_trace_applies(kfbi_plan *p, double kre, double kim, bool cplx, int bc_kind, int box_bc) {
   if (!p->facr_trace || !p->facr || p->n_oc <= 0 || bc_kind != 0 || box_bc != KFBI_DIRICHLET_ZERO)
     return false;
@@ -1883,12 +1884,32 @@ kfbi_status kfbi_richardson(kfbi_plan *p, const kfbi_bvp *b, kfbi_bvp_result *re
               "density-update");
     KFBI_CUDA(cudaStreamSynchronize(s), "density-update");
   } else {
+    // trace-only sweeps (FACR with the stencil chunks of the odd rows): each
+    // sweep keeps the density it started from, the field comes from one full
+    // pipeline after the loop
+    const bool ft = facr_trace_ok(p, b);
+    if (ft) KFBI_TRY(ensure_op_scratch(p));
     int enqueued = 0;
     int batch = b->sweeps_hint > 0 ? b->sweeps_hint : 4;
     for (;;) {
       int nb = batch;
       if (nb > b->max_iter - enqueued) nb = b->max_iter - enqueued;
       for (int k = 0; k < nb; ++k) {
+        if (ft) {
+          KFBI_TRY(launch(p, KFBI_K_DENSITY, s, [&] {
+            if (cplx)
+              copy_running_kernel<double2><<<64, 256, 0, s>>>(p->st.p, p->n_ctl,
+                                                             static_cast<const double2 *>(b->density),
+                                                             p->phi_prev.p);
+            else
+              copy_running_kernel<double><<<64, 256, 0, s>>>(p->st.p, p->n_ctl,
+                                                            static_cast<const double *>(b->density),
+                                                            reinterpret_cast<double *>(p->phi_prev.p));
+          }));
+          if (cplx) KFBI_TRY(sweep1_facr_trace<double2>(p, b, s));
+          else KFBI_TRY(sweep1_facr_trace<double>(p, b, s));
+          continue;
+        }
         if (cplx) KFBI_TRY(sweep<double2>(p, b, s));
         else KFBI_TRY(sweep<double>(p, b, s));
       }
@@ -1898,6 +1919,11 @@ kfbi_status kfbi_richardson(kfbi_plan *p, const kfbi_bvp *b, kfbi_bvp_result *re
       KFBI_CUDA(cudaStreamSynchronize(s), "density-update");
       if (p->st_host->done != 0 || enqueued >= b->max_iter) break;
       batch = 2;
+    }
+    if (ft) {
+      // the field and traces of the last sweep, from the density it started from
+      if (cplx) KFBI_TRY(final_pipeline<double2>(p, b, p->phi_prev.p, s));
+      else KFBI_TRY(final_pipeline<double>(p, b, p->phi_prev.p, s));
     }
   }
   if (use_op && sync_trace_only && p->st_host->iters == 1 && p->st_host->done == 1) {

@@ -369,11 +369,13 @@ def test_state_fields_zero_outside_mask(eq):
     torch.cuda.synchronize()
 
 
+@pytest.mark.parametrize("operator", [True, False], ids=["operator", "pipeline"])
 @pytest.mark.parametrize("eq", ["heat", "schrodinger"])
-def test_facr_trace_first_sweep_matches_full(monkeypatch, eq):
-    # the operator form's first sweep solves only the stencil chunks of the
-    # FACR odd rows (rows_odd_facr_sparse): same iteration lists and field as
-    # with the whole first-sweep field (KFBI_FACR_TRACE=0)
+def test_facr_trace_first_sweep_matches_full(monkeypatch, eq, operator):
+    # the operator form's first sweep (every sweep of the pipeline form) solves
+    # only the stencil chunks of the FACR odd rows (rows_odd_facr_sparse), the
+    # returned field comes from one full pipeline: same iteration lists and
+    # field as with whole-field sweeps (KFBI_FACR_TRACE=0)
     from paper_2404_14864_b200 import boxsolve
 
     heat, schr = k.HeatPlaneDecay(), k.SchrodingerPhaseRotation()
@@ -390,9 +392,47 @@ def test_facr_trace_first_sweep_matches_full(monkeypatch, eq):
         monkeypatch.setenv("KFBI_FACR_TRACE", flag)
         boxsolve._GRID_PLANS.clear()
         geo = k.build_grid(box, 1024, curve)
-        ctx = k.StepContext(geo, backend=k.CudaBackend(0, timing=False))
-        res[flag] = k.run(k.ProblemSpec(**kw), geo, context=ctx, operator=True, graph=False)
+        ctx = k.StepContext(geo, backend=k.CudaBackend(0, timing=False), operator=operator)
+        res[flag] = k.run(k.ProblemSpec(**kw), geo, context=ctx, operator=operator, graph=False)
     boxsolve._GRID_PLANS.clear()
     assert res["1"].iterations == res["0"].iterations
     a, b = np.asarray(res["1"].state.u), np.asarray(res["0"].state.u)
     assert np.max(np.abs(a - b)) <= 1e-13 * np.max(np.abs(b))
+
+
+@pytest.mark.parametrize("m", [2048, 16384])
+def test_facr_trace_pipeline_solve(monkeypatch, m):
+    # the device Richardson solve of the pipeline form (C5's one-GPU path):
+    # trace-only sweeps + one full pipeline give the same sweeps, density and
+    # field as whole-field sweeps; at 16384 on the one-real-row FACR engine
+    import torch
+
+    from paper_2404_14864_b200 import boxsolve
+    from paper_2404_14864_b200.bvp import solve_device
+
+    tau = 0.25 * 64 / m
+    kappa = 2.0 / tau
+    sol = k.StaticPlaneWave(kappa=kappa)
+    out = {}
+    for flag in ("1", "0"):
+        monkeypatch.setenv("KFBI_FACR_TRACE", flag)
+        boxsolve._GRID_PLANS.clear()
+        geo = k.build_grid(PI_BOX, m, k.StarCurve(1.5, c=0.2, lobes=3))
+        wsp = k.InterfaceWorkspace(geo, backend=k.CudaBackend(0, timing=False))
+        cps = wsp.cps
+        interior = geo.classification.interior
+        F = torch.from_numpy(np.where(interior, sol.f(geo.grid.X, geo.grid.Y), 0.0).reshape(-1)).cuda()
+        fg = torch.from_numpy(np.asarray(sol.f(cps.x, cps.y))).cuda()
+        g = torch.from_numpy(np.asarray(sol.dirichlet(cps.x, cps.y))).cuda()
+        dens = torch.zeros(cps.m, dtype=torch.float64, device="cuda")
+        r = solve_device(wsp, kappa=kappa, F=F, f_gamma=fg, g=g, density=dens)
+        out[flag] = (r.iterations, r.u.cpu(), dens.cpu())
+        del F, r, wsp
+        torch.cuda.empty_cache()
+    boxsolve._GRID_PLANS.clear()
+    assert out["1"][0] == out["0"][0]
+    # the sparse odd-row kernel rounds differently from the whole-row engine:
+    # ulp-level trace differences, 1.3e-13 after 36 sweeps at 16384
+    for i in (1, 2):
+        a, b = out["1"][i], out["0"][i]
+        assert float((a - b).abs().max()) <= 1e-12 * float(b.abs().max())
