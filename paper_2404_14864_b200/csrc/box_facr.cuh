@@ -644,6 +644,20 @@ rows_fwd_facr_real(BoxArgs a, const double *__restrict__ rhs, double sign, CorrA
     w[m] = make_double2(q >= 1 ? l0 + h0 - b0 : 0.0, l1 + h1 - b1);
     if (j == 0) w[m] = make_double2(0.0, 0.0);
   }
+  if (a.rowz) {
+    // no source and no corrections in rows j-1 .. j+1 (outside the domain's
+    // band for a masked source): the DST of w = 0 is exactly 0, the column
+    // pass skips the row (rowz) and no panel is written
+    bool nzl = false;
+#pragma unroll
+    for (int m = 0; m < E; ++m) nzl |= (w[m].x != 0.0) | (w[m].y != 0.0);
+    if (corr.jv && t == 0 && j > 0)
+      for (int jj = j - 1; jj <= j + 1; jj += 2)
+        if (jj <= M - 1 && corr.row_group[jj + 1] > corr.row_group[jj]) nzl = true;
+    const bool any = __syncthreads_or(nzl);
+    if (t == 0) a.rowz[r0] = any ? 0 : 1;
+    if (!any) return;
+  }
   reg::seq_sync<LOGL>();
   stage<LOGL>(sm, w, t);
   reg::seq_sync<LOGL>();

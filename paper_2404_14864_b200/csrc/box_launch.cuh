@@ -233,7 +233,7 @@ kfbi_status box_facr_real_launch(kfbi_plan *p, const BoxArgs &a0, const void *rh
   a.rows = M / 2;
   a.npl = M / 4;
   a.ring_end = 0;
-  a.rowz = nullptr;                                 // (the 16384 forward kernel writes every panel)
+  a.rowz = a0.zbuf;                                 // zero even rows: flagged, no panels written
   constexpr int CT = reg::Cfg<LOGL>::CTA_T;
   KFBI_TRY(kfbi_launch(p, KFBI_K_ROWS, s, [&] {
     rows_fwd_facr_real<LOGN><<<M / 2, CT, bytes, s>>>(a, static_cast<const double *>(rhs), sign, cc);

@@ -217,6 +217,8 @@ __global__ void __launch_bounds__(reg::Cfg<LOGN - 1>::CTA_T, 1) rows_inv_real(Bo
   const int stride = M + 1;
   const int r0 = blockIdx.x;
   const int j = a.row0 + r0;
+  // FACR even rows nobody reads (trace-only / masked solves, per even row)
+  if (a.row_step == 2 && a.row_need && !a.row_need[r0]) return;
   const double2 *P2 = static_cast<const double2 *>(a.panels);
   const size_t R = a.rows;
   for (int i = t; i < L; i += TT) {

@@ -414,8 +414,11 @@ def test_facr_trace_pipeline_solve(monkeypatch, m):
     kappa = 2.0 / tau
     sol = k.StaticPlaneWave(kappa=kappa)
     out = {}
-    for flag in ("1", "0"):
-        monkeypatch.setenv("KFBI_FACR_TRACE", flag)
+    # "1": trace-only sweeps; "0": whole-field FACR sweeps; "3p": the
+    # three-pass box solve (no FACR: no zero-row flags, no row skipping)
+    for flag in ("1", "0", "3p"):
+        monkeypatch.setenv("KFBI_FACR_TRACE", "0" if flag == "0" else "1")
+        monkeypatch.setenv("KFBI_FACR", "0" if flag == "3p" else "1")
         boxsolve._GRID_PLANS.clear()
         geo = k.build_grid(PI_BOX, m, k.StarCurve(1.5, c=0.2, lobes=3))
         wsp = k.InterfaceWorkspace(geo, backend=k.CudaBackend(0, timing=False))
@@ -430,9 +433,10 @@ def test_facr_trace_pipeline_solve(monkeypatch, m):
         del F, r, wsp
         torch.cuda.empty_cache()
     boxsolve._GRID_PLANS.clear()
-    assert out["1"][0] == out["0"][0]
+    assert out["1"][0] == out["0"][0] == out["3p"][0]
     # the sparse odd-row kernel rounds differently from the whole-row engine:
     # ulp-level trace differences, 1.3e-13 after 36 sweeps at 16384
     for i in (1, 2):
-        a, b = out["1"][i], out["0"][i]
-        assert float((a - b).abs().max()) <= 1e-12 * float(b.abs().max())
+        b = out["0"][i]
+        for f in ("1", "3p"):
+            assert float((out[f][i] - b).abs().max()) <= 1e-12 * float(b.abs().max()), (f, i)
