@@ -1727,7 +1727,7 @@ __global__ void op_finalize_kernel(const RichState *st, int n, T *A, const T *B,
   // sweep 1 also needs the field, from phi_0
   const int K = st->iters, done = st->done;
   const bool odd = (K & 1) != 0;
-  for (int p = threadIdx.x; p < n; p += blockDim.x) {
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x) {
     if (K >= 2) {
       const T a = A[p], b = B[p];
       phik1[p] = odd ? b : a;       // phi_(K-1)
@@ -1736,7 +1736,7 @@ __global__ void op_finalize_kernel(const RichState *st, int n, T *A, const T *B,
       phik1[p] = phi0[p];
     }
   }
-  if (threadIdx.x == 0) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
     skip[0] = ((K >= 2 || phi0) && done == 1) ? 0 : 1;
     if (log) {
       log->iterations = K;

@@ -1843,14 +1843,14 @@ kfbi_status kfbi_richardson(kfbi_plan *p, const kfbi_bvp *b, kfbi_bvp_result *re
     int *skip = p->skip.p;
     if (cplx) {
       KFBI_TRY(launch(p, KFBI_K_DENSITY, s, [&] {
-        op_finalize_kernel<double2><<<1, 256, 0, s>>>(p->st.p, p->n_ctl, static_cast<double2 *>(b->density),
+        op_finalize_kernel<double2><<<(p->n_ctl + 255) / 256, 256, 0, s>>>(p->st.p, p->n_ctl, static_cast<double2 *>(b->density),
                                                       p->phi_prev.p, p->phik1.p, skip, entry,
                                                       tr ? p->phi0.p : nullptr);
       }));
       KFBI_TRY(final_pipeline<double2>(p, b, p->phik1.p, s, skip));
     } else {
       KFBI_TRY(launch(p, KFBI_K_DENSITY, s, [&] {
-        op_finalize_kernel<double><<<1, 256, 0, s>>>(
+        op_finalize_kernel<double><<<(p->n_ctl + 255) / 256, 256, 0, s>>>(
             p->st.p, p->n_ctl, static_cast<double *>(b->density),
             reinterpret_cast<const double *>(p->phi_prev.p), reinterpret_cast<double *>(p->phik1.p),
             skip, entry, tr ? reinterpret_cast<const double *>(p->phi0.p) : nullptr);
