@@ -3,7 +3,8 @@
 stages, DCT-I), a Dirichlet Richardson solve, heat and Schrodinger runs in
 the operator form (op_solve_* kernels and the hand-rolled grid barrier), a
 Neumann heat run, GMRES, the slab passes with fused peer stores and the
-peer-flag barrier (two virtual ranks on two streams)."""
+peer-flag barrier (two virtual ranks on two streams), and the reduced-work
+FACR paths at 512² (trace-only and masked sweeps, graphs, one-CTA sweeps)."""
 import ctypes as C
 import os
 import sys
@@ -54,6 +55,24 @@ sspec = k.ProblemSpec(equation="schrodinger", bc_kind="dirichlet", g=schr.dirich
                       lap_u0=schr.lap_u0, potential=schr.potential, w=1.0, tau=1 / 32, t_final=2 / 32)
 k.run(sspec, pgeo, operator=True)
 print("runs ok", flush=True)
+
+# the reduced-work FACR paths need M >= 512: trace-only sweeps
+# (rows_odd_facr_sparse, row_need, zero-row flags), the masked final sweep
+# (field chunks), zero-exterior rings, CUDA-graph steps, one-CTA operator
+# sweeps, and the pipeline form's trace-only sweeps + final pipeline
+m2 = int(os.environ.get("SAN_M2", "512"))
+geo2 = k.build_grid(BOX, m2, k.StarCurve(1.0, c=0.2, lobes=8))
+spec2 = k.ProblemSpec(equation="heat", bc_kind="dirichlet", g=heat.dirichlet, u0=heat.u0,
+                      lap_u0=heat.lap_u0, tau=1 / 256, t_final=4 / 256)
+for op in (True, False):
+    ctx2 = k.StepContext(geo2, backend=k.CudaBackend(0, timing=False), operator=op)
+    k.run(spec2, geo2, context=ctx2, operator=op, graph="auto" if op else False)
+pgeo2 = k.build_grid(PI_BOX, m2, k.StarCurve(1.5, c=0.2, lobes=3))
+sspec2 = k.ProblemSpec(equation="schrodinger", bc_kind="dirichlet", g=schr.dirichlet, u0=schr.u0,
+                       lap_u0=schr.lap_u0, potential=schr.potential, w=1.0, tau=1 / 128, t_final=3 / 128)
+ctx3 = k.StepContext(pgeo2, backend=k.CudaBackend(0, timing=False), operator=True)
+k.run(sspec2, pgeo2, context=ctx3, operator=True, graph="auto")
+print("reduced-work runs ok", flush=True)
 
 rhs = torch.from_numpy(rng.standard_normal((m + 1, m + 1))).cuda()
 D.solve_virtual(grid, 40.0, rhs, 2, p2p=True)
