@@ -70,9 +70,9 @@ struct MaskNormOp {
           const double2 w = reinterpret_cast<const double2 *>(u)[ii[k]];
           v[k][0] = w.x;
           v[k][1] = w.y;
-        } else {
-          v[k][0] = u[2 * ii[k]];
-          v[k][1] = u[2 * ii[k] + 1];
+        } else {                                 // complex: one 16-byte load per element
+          if (mk[k].x) v[k][0] = u[2 * ii[k]];
+          if (mk[k].y) v[k][1] = u[2 * ii[k] + 1];
         }
       }
     }
@@ -84,8 +84,9 @@ struct MaskNormOp {
     }
   }
   KFBI_DEV void one(long i) {
-    T v = u[i];
-    if (mask && !mask[i]) { v = Sc<T>::zero(); u[i] = v; }
+    const bool in = !mask || mask[i];           // (exterior values are not read)
+    T v = in ? u[i] : Sc<T>::zero();
+    if (!in) u[i] = v;
     mag = nanmax(mag, Sc<T>::abs(v));
   }
 };
@@ -135,8 +136,9 @@ struct HeatOp {
     }
   }
   KFBI_DEV void one(long i) {
-    double v = u[i];
-    if (mask && !mask[i]) { v = 0.0; u[i] = v; }
+    const bool in = !mask || mask[i];
+    const double v = in ? u[i] : 0.0;
+    if (!in) u[i] = v;
     F_new[i] = a * v - F_old[i];
     mag = nanmax(mag, fabs(v));
   }
@@ -195,8 +197,9 @@ struct WaveOp {
     }
   }
   KFBI_DEV void one(long i) {
-    double v = un[i];
-    if (mask && !mask[i]) { v = 0.0; un[i] = v; }
+    const bool in = !mask || mask[i];
+    const double v = in ? un[i] : 0.0;
+    if (!in) un[i] = v;
     F_new[i] = f(v, uc[i], fc[i], fp[i]);
     mag = nanmax(mag, fabs(v));
   }
