@@ -156,10 +156,37 @@ circ_block_kernel(CtlGeom g, const T *__restrict__ v0, const T *__restrict__ v1,
   T *vs = reinterpret_cast<T *>(Ds + ((n + 1) & ~1));
   T *red = vs + NV * n;
   const bool have = v0 != nullptr;
-  stage_batched<8>(n, [&](int i) { return g.deriv_col[i]; }, [&](int i, double x) { Ds[i] = x; });
-  if (have) {
-    stage_batched<8>(n, [&](int i) { return v0[i]; }, [&](int i, T x) { vs[i] = x; });
-    if (NV == 2) stage_batched<8>(n, [&](int i) { return v1[i]; }, [&](int i, T x) { vs[n + i] = x; });
+  {
+    // D and the NV vectors in the same rounds: U elements of each in flight
+    // per thread (one L2 round trip per round instead of one per array)
+    constexpr int U = std::is_same<T, double>::value && NV == 1 ? 12 : 6;
+    const int nt = blockDim.x;
+    for (int base = 0; base < n; base += U * nt) {
+      double dv[U];
+      T xv[NV][U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int i = base + u * nt + tid;
+        if (i < n) {
+          dv[u] = g.deriv_col[i];
+          if (have) {
+            xv[0][u] = v0[i];
+            if constexpr (NV == 2) xv[NV - 1][u] = v1[i];
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int i = base + u * nt + tid;
+        if (i < n) {
+          Ds[i] = dv[u];
+          if (have) {
+            vs[i] = xv[0][u];
+            if constexpr (NV == 2) vs[n + i] = xv[NV - 1][u];
+          }
+        }
+      }
+    }
   }
   __syncthreads();
   const int q = tid & 3, c = tid >> 2;
