@@ -693,7 +693,7 @@ spec_block_kernel(int n, int K, const T *__restrict__ jm, double2 *__restrict__ 
   // the CTA's control range, staged column-major [SPEC_COLS][jn] in shared memory
   const int cj0 = (int)((long)n * y / Y), cj1 = (int)((long)n * (y + 1) / Y), jn = cj1 - cj0;
   T *fs = reinterpret_cast<T *>(red_sm + (size_t)nw * R * 32);
-  stage_batched<4>(SPEC_COLS * jn, [&](int i) {
+  stage_batched<8>(SPEC_COLS * jn, [&](int i) {
     const int c = i / jn, j = i - c * jn;
     return jm[(size_t)spec_jm_col(c) * n + cj0 + j];
   }, [&](int i, T x) { fs[i] = x; });
@@ -870,7 +870,7 @@ edges_spectral_res_kernel(int ngroups, int n, int K, const int *__restrict__ per
   constexpr int R = SPEC_COLS * NP;
   extern __shared__ double2 fsm[];                       // [R][K]
   if (done && *done) return;
-  stage_batched<8>(R * K, [&](int i) { return spec[i]; }, [&](int i, double2 x) { fsm[i] = x; });
+  stage_batched<16>(R * K, [&](int i) { return spec[i]; }, [&](int i, double2 x) { fsm[i] = x; });
   __syncthreads();
   const int lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
   auto F = [&](int r, int k) { return fsm[(size_t)r * K + k]; };
