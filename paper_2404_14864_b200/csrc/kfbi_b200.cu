@@ -535,12 +535,13 @@ kfbi_status edges_spectral(kfbi_plan *p, const void *jm, void *jv, const int *do
   }
   const int n = p->n_ctl, K = n / 2 + 1;
   const int kb = (K + 31) / 32;
-#ifdef KFBI_SPEC_Y
-  int Y = KFBI_SPEC_Y;
-#else
+  static const int y_env = [] {
+    const char *e = std::getenv("KFBI_SPEC_Y");        // control splits per frequency block
+    return e ? std::atoi(e) : 0;
+  }();
   int Y = (2 * sms) / kb;
   Y = Y < 1 ? 1 : (Y > 8 ? 8 : Y);
-#endif
+  if (y_env > 0) Y = y_env;
   // the staged control range of a CTA must fit next to the reduction buffer
   const size_t red_bytes = (size_t)16 * R * 32 * sizeof(double2);
   while ((size_t)SPEC_COLS * ((n + Y - 1) / Y + 1) * sizeof(T) + red_bytes > (size_t)(optin - 1024) && Y < 64)
