@@ -205,12 +205,19 @@ def test_convergence_error_fields():
     assert ei.value.iterations == 3 and ei.value.last_residual > 0.0
 
 
+@pytest.mark.parametrize("interp", ["auto", "spectral"])
 @pytest.mark.parametrize("operator", [False, True], ids=["pipeline", "operator"])
 @pytest.mark.parametrize("name", list(run_cases()))
-def test_full_runs_vs_reference(name, operator):
+def test_full_runs_vs_reference(name, operator, interp):
+    # "spectral": the matrix-free edge values (the form the 4096^2 bench runs)
+    # forced at the golden sizes, against the same reference goldens
     box, m, curve, kw = run_cases()[name]
     geo = k.build_grid(box, m, curve)
-    res = k.run(k.ProblemSpec(**kw), geo, operator=operator)
+    ctx = k.StepContext(geo, operator=operator)
+    if interp == "spectral":
+        ctx.plan.set_interp("spectral")
+        assert ctx.plan.spectral_edges
+    res = k.run(k.ProblemSpec(**kw), geo, context=ctx, operator=operator)
     g = golden("runs")
     assert res.iterations == list(g[name + "__iterations"])
     assert rel_linf(res.state.u, g[name + "__u"]) < TOL
