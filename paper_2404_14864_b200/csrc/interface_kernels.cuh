@@ -735,34 +735,27 @@ spec_block_kernel(int n, int K, const T *__restrict__ jm, double2 *__restrict__ 
 #pragma unroll
   for (int r = 0; r < R; ++r) red(w, r) = acc[r];
   __syncthreads();
-  if (w == 0 && k < K) {
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
+  // column r's warp partials summed by warp r (warp order: deterministic)
+  if (k < K)
+    for (int r = w; r < R; r += nw) {
       double2 sum = red(0, r);
       for (int x = 1; x < nw; ++x) sum = cadd(sum, red(x, r));
-      part[((size_t)y * R + r) * K + k] = sum;
+      if (Y == 1) spec[(size_t)r * K + k] = sum;
+      else part[((size_t)y * R + r) * K + k] = sum;
     }
-  }
-  if (Y == 1) {
-    if (w == 0 && k < K)
-#pragma unroll
-      for (int r = 0; r < R; ++r) spec[(size_t)r * K + k] = part[(size_t)r * K + k];
-    return;
-  }
+  if (Y == 1) return;
   __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) last = atomicAdd(&counters[blockIdx.x], 1u) == (unsigned)(Y - 1);
   __syncthreads();
   if (!last) return;
   __threadfence();
-  if (w == 0 && k < K) {
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
+  if (k < K)
+    for (int r = w; r < R; r += nw) {
       double2 sum = __ldcg(&part[(size_t)r * K + k]);
       for (int x = 1; x < Y; ++x) sum = cadd(sum, __ldcg(&part[((size_t)x * R + r) * K + k]));
       spec[(size_t)r * K + k] = sum;
     }
-  }
   if (threadIdx.x == 0) counters[blockIdx.x] = 0u;
 }
 
