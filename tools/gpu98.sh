@@ -1,0 +1,4 @@
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_r2v98.log 2>&1; echo rc=$? >> gpurun_out/smoke_r2v98.log
+timeout 1500 python -m pytest tests -m gpu -q --tb=short -p no:cacheprovider > gpurun_out/pytest_r2v98.log 2>&1; echo rc=$? >> gpurun_out/pytest_r2v98.log
+timeout 1500 python bench.py > gpurun_out/bench_r2v98.log 2>&1; echo rc=$? >> gpurun_out/bench_r2v98.log
+timeout 900 python bench.py --impl reference > gpurun_out/bench_ref_r2v98.log 2>&1; echo rc=$? >> gpurun_out/bench_ref_r2v98.log
