@@ -447,3 +447,33 @@ def test_facr_trace_pipeline_solve(monkeypatch, m):
         b = out["0"][i]
         for f in ("1", "3p"):
             assert float((out[f][i] - b).abs().max()) <= 1e-12 * float(b.abs().max()), (f, i)
+
+
+@pytest.mark.parametrize("flag", ["1", "0"])
+def test_facr_trace_pipeline_max_iter(monkeypatch, flag):
+    # a pipeline-form solve that stops at max_iter with trace-only sweeps
+    # raises the reference's ConvergenceError with the same sweep count and
+    # last update as with whole-field sweeps (bvp.py:346-351)
+    from paper_2404_14864_b200 import boxsolve
+
+    monkeypatch.setenv("KFBI_FACR_TRACE", flag)
+    boxsolve._GRID_PLANS.clear()
+    try:
+        geo = k.build_grid(BOX, 1024, k.StarCurve(1.0, c=0.2, lobes=5))
+        ws = k.InterfaceWorkspace(geo)
+        sol = k.StaticPlaneWave(kappa=512.0)
+        cps = ws.cps
+        F = np.where(geo.classification.interior, sol.f(geo.grid.X, geo.grid.Y), 0.0)
+        prob = k.BvpProblem(kappa=512.0, F=F, f_gamma=sol.f(cps.x, cps.y), bc_kind="dirichlet",
+                            bc_values=sol.dirichlet(cps.x, cps.y), max_iter=3)
+        with pytest.raises(k.ConvergenceError) as ei:
+            k.richardson_solve(prob, ws)
+        assert ei.value.iterations == 3
+        prob_full = k.BvpProblem(kappa=512.0, F=F, f_gamma=sol.f(cps.x, cps.y), bc_kind="dirichlet",
+                                 bc_values=sol.dirichlet(cps.x, cps.y))
+        s = k.richardson_solve(prob_full, ws)
+        assert s.iterations > 3
+        # the residual history's third entry is the update the error reports
+        assert abs(ei.value.last_residual - s.residual_history[2]) <= 1e-12 * s.residual_history[2]
+    finally:
+        boxsolve._GRID_PLANS.clear()
