@@ -678,10 +678,12 @@ KFBI_DEV double2 cis_product(double a, double b) {
 // W partial sums of a CTA are added in warp order in shared memory, the Y
 // CTA partials of a frequency block by the last CTA to finish it, in split
 // order (deterministic; the block counter resets itself).
+__host__ __device__ __forceinline__ int jn_max(int n, int Y) { return (n + Y - 1) / Y + 1; }
+
 template <typename T>
 __global__ void __launch_bounds__(512)
 spec_block_kernel(int n, int K, const T *__restrict__ jm, double2 *__restrict__ part,
-                  double2 *__restrict__ spec, unsigned int *counters) {
+                  double2 *__restrict__ spec, unsigned int *counters, int clustered) {
   constexpr int NP = std::is_same<T, double2>::value ? 2 : 1;
   constexpr int R = SPEC_COLS * NP;
   extern __shared__ double2 red_sm[];                   // [W][R][32], then the staged columns
@@ -693,6 +695,8 @@ spec_block_kernel(int n, int K, const T *__restrict__ jm, double2 *__restrict__ 
   // the CTA's control range, staged column-major [SPEC_COLS][jn] in shared memory
   const int cj0 = (int)((long)n * y / Y), cj1 = (int)((long)n * (y + 1) / Y), jn = cj1 - cj0;
   T *fs = reinterpret_cast<T *>(red_sm + (size_t)nw * R * 32);
+  double2 *fs_end = reinterpret_cast<double2 *>(
+      reinterpret_cast<unsigned char *>(fs) + (((size_t)SPEC_COLS * (jn_max(n, Y)) * sizeof(T) + 15) & ~(size_t)15));
   stage_batched<8>(SPEC_COLS * jn, [&](int i) {
     const int c = i / jn, j = i - c * jn;
     return jm[(size_t)spec_jm_col(c) * n + cj0 + j];
@@ -735,6 +739,27 @@ spec_block_kernel(int n, int K, const T *__restrict__ jm, double2 *__restrict__ 
 #pragma unroll
   for (int r = 0; r < R; ++r) red(w, r) = acc[r];
   __syncthreads();
+  if (clustered) {
+    // the Y splits of a frequency block form one thread-block cluster: the
+    // CTA column sums meet in the rank-0 CTA's view of distributed shared
+    // memory, added in split order (the order of the global-partials path)
+    double2 *csum = fs_end;                          // [R][32] after the staged columns
+    for (int r = w; r < R; r += nw) {
+      double2 sum = red(0, r);
+      for (int x = 1; x < nw; ++x) sum = cadd(sum, red(x, r));
+      csum[r * 32 + lane] = sum;
+    }
+    auto cl = cooperative_groups::this_cluster();
+    cl.sync();
+    if (cl.block_rank() == 0 && k < K)
+      for (int r = w; r < R; r += nw) {
+        double2 sum = csum[r * 32 + lane];
+        for (int x = 1; x < Y; ++x) sum = cadd(sum, cl.map_shared_rank(csum, x)[r * 32 + lane]);
+        spec[(size_t)r * K + k] = sum;
+      }
+    cl.sync();                                       // peers' shared memory read
+    return;
+  }
   // column r's warp partials summed by warp r (warp order: deterministic)
   if (k < K)
     for (int r = w; r < R; r += nw) {

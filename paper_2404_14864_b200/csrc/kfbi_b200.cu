@@ -544,9 +544,19 @@ kfbi_status edges_spectral(kfbi_plan *p, const void *jm, void *jv, const int *do
   if (y_env > 0) Y = y_env;
   // the staged control range of a CTA must fit next to the reduction buffer
   const size_t red_bytes = (size_t)16 * R * 32 * sizeof(double2);
-  while ((size_t)SPEC_COLS * ((n + Y - 1) / Y + 1) * sizeof(T) + red_bytes > (size_t)(optin - 1024) && Y < 64)
+  while (((size_t)SPEC_COLS * jn_max(n, Y) * sizeof(T) + 15) + red_bytes + (size_t)R * 32 * sizeof(double2) >
+             (size_t)(optin - 1024) && Y < 64)
     ++Y;
-  const size_t spec_smem = red_bytes + (size_t)SPEC_COLS * ((n + Y - 1) / Y + 1) * sizeof(T);
+  // Y <= 8 splits run as one thread-block cluster per frequency block (the
+  // partial sums meet in distributed shared memory; KFBI_SPEC_CLUSTER=0: the
+  // global partials + last-CTA path)
+  static const bool cl_env = [] {
+    const char *v = std::getenv("KFBI_SPEC_CLUSTER");
+    return !(v && v[0] == '0');
+  }();
+  const bool clustered = cl_env && Y > 1 && Y <= 8;
+  const size_t spec_smem = red_bytes + (((size_t)SPEC_COLS * jn_max(n, Y) * sizeof(T) + 15) & ~(size_t)15) +
+                           (clustered ? (size_t)R * 32 * sizeof(double2) : 0);
   cudaError_t e = p->spec.ensure((size_t)2 * SPEC_COLS * K);
   if (e == cudaSuccess) e = p->spec_part.ensure((size_t)Y * 2 * SPEC_COLS * K);
   if (e == cudaSuccess && p->spec_ctr.n < (size_t)kb) {
@@ -556,8 +566,25 @@ kfbi_status edges_spectral(kfbi_plan *p, const void *jm, void *jv, const int *do
   if (e != cudaSuccess) return fail(KFBI_E_CUDA, std::string("spectral edges: ") + cudaGetErrorString(e));
   if (p->n_edges == 0) return KFBI_OK;
   KFBI_TRY(launch(p, KFBI_K_JUMPS, s, [&] {
-    spec_block_kernel<T><<<dim3(kb, Y), 512, spec_smem, s>>>(
-        n, K, static_cast<const T *>(jm), p->spec_part.p, p->spec.p, p->spec_ctr.p);
+    if (!clustered) {
+      spec_block_kernel<T><<<dim3(kb, Y), 512, spec_smem, s>>>(
+          n, K, static_cast<const T *>(jm), p->spec_part.p, p->spec.p, p->spec_ctr.p, 0);
+      return cudaGetLastError();
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(kb, Y);
+    cfg.blockDim = dim3(512);
+    cfg.dynamicSmemBytes = spec_smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 1;
+    attr[0].val.clusterDim.y = Y;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, spec_block_kernel<T>, n, K, static_cast<const T *>(jm), p->spec_part.p,
+                              p->spec.p, p->spec_ctr.p, 1);
   }));
   const int ngroups = p->n_perm / EB;
   const size_t res_bytes = (size_t)R * K * sizeof(double2);
