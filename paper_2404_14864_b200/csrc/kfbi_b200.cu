@@ -554,9 +554,11 @@ kfbi_status edges_spectral(kfbi_plan *p, const void *jm, void *jv, const int *do
     const char *v = std::getenv("KFBI_SPEC_CLUSTER");
     return !(v && v[0] == '0');
   }();
-  const bool clustered = cl_env && Y > 1 && Y <= 8;
-  const size_t spec_smem = red_bytes + (((size_t)SPEC_COLS * jn_max(n, Y) * sizeof(T) + 15) & ~(size_t)15) +
-                           (clustered ? (size_t)R * 32 * sizeof(double2) : 0);
+  // (only where several CTAs fit per SM: with one CTA of ~200 KB per SM, C5's
+  // 8192 controls, the full bench measured 109 -> 155 ms per solve)
+  const size_t spec_base = red_bytes + (((size_t)SPEC_COLS * jn_max(n, Y) * sizeof(T) + 15) & ~(size_t)15);
+  const bool clustered = cl_env && Y > 1 && Y <= 8 && spec_base <= ((size_t)96 << 10);
+  const size_t spec_smem = spec_base + (clustered ? (size_t)R * 32 * sizeof(double2) : 0);
   cudaError_t e = p->spec.ensure((size_t)2 * SPEC_COLS * K);
   if (e == cudaSuccess) e = p->spec_part.ensure((size_t)Y * 2 * SPEC_COLS * K);
   if (e == cudaSuccess && p->spec_ctr.n < (size_t)kb) {
